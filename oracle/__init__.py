@@ -1,0 +1,244 @@
+"""ORACLE / TEST INFRASTRUCTURE ONLY — CPU checkers for the B200 path.
+
+Loads, via ctypes, the two CPU implementations that share the C ABI in
+``oracle/ksvm_oracle.h``:
+
+* ``Lib("oracle")`` - ``oracle/liboracle.so``, the Eigen-free restatement of
+  the reference hot path (P:src/fastsum.cpp:103-371).
+* ``Lib("ref")``    - ``oracle/_ref/libref.so``, the reference's own
+  ``fastsum.cpp``/``kernel.cpp``/``windowing.cpp`` compiled unmodified by
+  path (present when it was built in a container that has /root/reference;
+  the built file travels to the GPU box).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline
+leg may import this package. The product package never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_PATHS = {"oracle": os.path.join(HERE, "liboracle.so"),
+          "ref": os.path.join(HERE, "_ref", "libref.so")}
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+
+
+def build(quiet: bool = True) -> None:
+    """Compile liboracle.so (and oracle/_ref/libref.so when /root/reference exists)."""
+    out = subprocess.run(["make", "-C", HERE], capture_output=True, text=True)
+    if out.returncode != 0:
+        raise RuntimeError("oracle build failed:\n" + out.stdout + out.stderr)
+    if not quiet:
+        print(out.stdout)
+
+
+def available(kind: str) -> bool:
+    return os.path.exists(_PATHS[kind])
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(_dp)
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+class Lib:
+    """One of the two CPU libraries, with numpy-facing wrappers."""
+
+    _cache: dict = {}
+
+    def __init__(self, kind: str = "oracle"):
+        if kind not in _PATHS:
+            raise ValueError(kind)
+        if not os.path.exists(_PATHS[kind]):
+            raise FileNotFoundError(_PATHS[kind] + " (run oracle.build())")
+        if kind not in Lib._cache:
+            Lib._cache[kind] = self._bind(C.CDLL(_PATHS[kind]), kind)
+        self.L = Lib._cache[kind]
+        self.kind = kind
+        self.p = kind + "_"
+
+    @staticmethod
+    def _bind(L, kind):
+        p = kind + "_"
+        vp = C.c_void_p
+        sig = {
+            "last_error": (C.c_char_p, []),
+            "plan_create": (C.c_int, [_dp, C.c_int64, C.c_int, C.c_double, C.c_int, C.c_int,
+                                      C.c_int, C.c_double, C.c_double, C.POINTER(vp)]),
+            "plan_apply": (C.c_int, [vp, _dp, _dp]),
+            "plan_apply_cross": (C.c_int, [vp, _dp, C.c_int64, _dp, _dp]),
+            "plan_scaled_length": (C.c_double, [vp]),
+            "plan_coefficient_sum": (C.c_double, [vp]),
+            "plan_scale_points": (C.c_int, [vp, _dp, C.c_int64, _dp]),
+            "plan_free": (None, [vp]),
+            "anova_create": (C.c_int, [_dp, C.c_int64, C.c_int, _ip, _ip, C.c_int, _dp, _dp,
+                                       C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                       C.POINTER(vp)]),
+            "anova_apply": (C.c_int, [vp, _dp, _dp]),
+            "anova_entry": (C.c_double, [vp, C.c_int64, C.c_int64]),
+            "anova_free": (None, [vp]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, p + name)
+            f.restype = res
+            f.argtypes = args
+        if kind == "oracle":
+            for name, args in {"random_points": [C.c_int64, C.c_int64, C.c_uint64, C.c_double, _dp],
+                               "random_vector": [C.c_int64, C.c_uint64, _dp],
+                               "uniform": [C.c_int64, C.c_uint64, C.c_double, C.c_double, _dp],
+                               "bernoulli": [C.c_int64, C.c_uint64, C.c_double, _dp]}.items():
+                f = getattr(L, "oracle_" + name)
+                f.restype = None
+                f.argtypes = args
+        return L
+
+    def _fn(self, name):
+        return getattr(self.L, self.p + name)
+
+    def _check(self, code):
+        if code != 0:
+            raise OracleError(code, self._fn("last_error")().decode())
+
+    # --- per-window plan (P:include/ksvm/fastsum.hpp:25-72) -------------
+    def plan(self, pts, ell=1.0, N=32, m=4, sigma=2, torus_radius=0.25, fit=1.0):
+        return Plan(self, pts, ell, N, m, sigma, torus_radius, fit)
+
+    # --- ANOVA operator (P:src/fastsum.cpp:326-371) -----------------------
+    def anova(self, pts, windows, weights=None, ells=None, N=32, m=4, sigma=2,
+              torus_radius=0.25, fit=1.0):
+        return Anova(self, pts, windows, weights, ells, N, m, sigma, torus_radius, fit)
+
+
+class Plan:
+    def __init__(self, lib, pts, ell, N, m, sigma, rT, fit):
+        pts = np.asarray(pts, dtype=np.float64)
+        if pts.ndim == 1:
+            pts = pts[:, None]
+        self.lib, self.n, self.d = lib, pts.shape[0], pts.shape[1]
+        cm = _f64(pts.T)  # column-major n x d
+        h = C.c_void_p()
+        lib._check(lib._fn("plan_create")(_ptr(cm), self.n, self.d, ell, N, m, sigma, rT, fit,
+                                          C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib._fn("plan_free")(self.h)
+            self.h = None
+
+    def apply(self, v):
+        v = _f64(v)
+        out = np.empty(self.n)
+        self.lib._check(self.lib._fn("plan_apply")(self.h, _ptr(v), _ptr(out)))
+        return out
+
+    def apply_cross(self, targets, v):
+        t = np.asarray(targets, dtype=np.float64)
+        if t.ndim == 1:
+            t = t[:, None]
+        cm = _f64(t.T)
+        v = _f64(v)
+        out = np.empty(t.shape[0])
+        self.lib._check(self.lib._fn("plan_apply_cross")(self.h, _ptr(cm), t.shape[0], _ptr(v),
+                                                         _ptr(out)))
+        return out
+
+    def scaled_length(self):
+        return self.lib._fn("plan_scaled_length")(self.h)
+
+    def coefficient_sum(self):
+        return self.lib._fn("plan_coefficient_sum")(self.h)
+
+    def scale_points(self, pts):
+        t = np.asarray(pts, dtype=np.float64)
+        if t.ndim == 1:
+            t = t[:, None]
+        cm = _f64(t.T)
+        out = np.empty_like(cm)
+        self.lib._check(self.lib._fn("plan_scale_points")(self.h, _ptr(cm), t.shape[0], _ptr(out)))
+        return out.T.copy()
+
+
+class Anova:
+    def __init__(self, lib, pts, windows, weights, ells, N, m, sigma, rT, fit):
+        pts = _f64(pts)
+        self.lib, self.n = lib, pts.shape[0]
+        P = len(windows)
+        feats = np.ascontiguousarray([f for w in windows for f in w], dtype=np.int32)
+        sizes = np.ascontiguousarray([len(w) for w in windows], dtype=np.int32)
+        weights = _f64(weights if weights is not None else [1.0 / P] * P)
+        ells = _f64(ells if ells is not None else [1.0] * P)
+        h = C.c_void_p()
+        lib._check(lib._fn("anova_create")(_ptr(pts), self.n, pts.shape[1],
+                                           feats.ctypes.data_as(_ip), sizes.ctypes.data_as(_ip),
+                                           P, _ptr(weights), _ptr(ells), N, m, sigma, rT, fit,
+                                           C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib._fn("anova_free")(self.h)
+            self.h = None
+
+    def apply(self, v):
+        v = _f64(v)
+        out = np.empty(self.n)
+        self.lib._check(self.lib._fn("anova_apply")(self.h, _ptr(v), _ptr(out)))
+        return out
+
+    def entry(self, i, j):
+        return self.lib._fn("anova_entry")(self.h, i, j)
+
+
+# --- input generators (P:tests/helpers.hpp:15-31) --------------------------
+def random_points(n, d, seed, scale=1.0) -> np.ndarray:
+    """n x d (row-major numpy) drawn exactly like helpers::random_points."""
+    L = Lib("oracle").L
+    out = np.empty(n * d)
+    L.oracle_random_points(n, d, seed, scale, _ptr(out))
+    return out.reshape(d, n).T.copy()
+
+
+def random_vector(n, seed) -> np.ndarray:
+    L = Lib("oracle").L
+    out = np.empty(n)
+    L.oracle_random_vector(n, seed, _ptr(out))
+    return out
+
+
+def uniform(n, seed, lo, hi) -> np.ndarray:
+    L = Lib("oracle").L
+    out = np.empty(n)
+    L.oracle_uniform(n, seed, lo, hi, _ptr(out))
+    return out
+
+
+def bernoulli(n, seed, p) -> np.ndarray:
+    L = Lib("oracle").L
+    out = np.empty(n)
+    L.oracle_bernoulli(n, seed, p, _ptr(out))
+    return out
+
+
+def dense_gaussian(pts, ell=1.0) -> np.ndarray:
+    """helpers::dense_gaussian (P:tests/helpers.hpp:78-89)."""
+    pts = np.asarray(pts, dtype=np.float64)
+    if pts.ndim == 1:
+        pts = pts[:, None]
+    d2 = ((pts[:, None, :] - pts[None, :, :]) ** 2).sum(-1)
+    return np.exp(-d2 / (ell * ell))

@@ -1,0 +1,66 @@
+/* ORACLE / TEST INFRASTRUCTURE ONLY.
+ *
+ * C ABI of the CPU checkers. Two libraries export it with different
+ * prefixes and identical argument meaning:
+ *   oracle/liboracle.so   prefix "oracle_"  - the Eigen-free restatement of
+ *                                             the reference hot path
+ *                                             (oracle/fastsum_oracle.cpp)
+ *   oracle/_ref/libref.so prefix "ref_"     - the reference's OWN fastsum.cpp /
+ *                                             kernel.cpp / windowing.cpp,
+ *                                             compiled unmodified by path
+ *                                             against oracle/shim
+ *                                             (oracle/ref_capi.cpp)
+ * Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline leg may
+ * load these; the product path never does.
+ *
+ * Point matrices: `pts` is n x d COLUMN-major (Eigen's default storage, as
+ * plan_fastsum receives it, P:include/ksvm/fastsum.hpp:60-62) unless a
+ * function says row-major. Status: 0 ok, 2 DomainError/DataError,
+ * 4 invalid_argument, 5 other (P:capi/ksvm_capi.cpp:31-48).
+ */
+#ifndef KSVM_ORACLE_H
+#define KSVM_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KSVM_ORACLE_DECLARE(P)                                                           \
+    typedef struct P##plan P##plan;                                                      \
+    typedef struct P##anova P##anova;                                                    \
+    const char* P##last_error(void);                                                     \
+    int P##plan_create(const double* pts, int64_t n, int d, double ell, int N, int m,    \
+                       int sigma, double torus_radius, double fit, P##plan** out);       \
+    int P##plan_apply(const P##plan* p, const double* v, double* out);                   \
+    int P##plan_apply_cross(const P##plan* p, const double* targets, int64_t t,          \
+                            const double* v, double* out);                               \
+    double P##plan_scaled_length(const P##plan* p);                                      \
+    double P##plan_coefficient_sum(const P##plan* p);                                    \
+    int P##plan_scale_points(const P##plan* p, const double* pts, int64_t t, double* out); \
+    void P##plan_free(P##plan* p);                                                       \
+    int P##anova_create(const double* pts_rowmajor, int64_t n, int d,                   \
+                        const int* win_features, const int* win_sizes, int P_,           \
+                        const double* weights, const double* ells, int N, int m,         \
+                        int sigma, double torus_radius, double fit, P##anova** out);     \
+    int P##anova_apply(const P##anova* op, const double* v, double* out);               \
+    double P##anova_entry(const P##anova* op, int64_t i, int64_t j);                     \
+    void P##anova_free(P##anova* op);
+
+KSVM_ORACLE_DECLARE(oracle_)
+KSVM_ORACLE_DECLARE(ref_)
+
+/* Input generators matching P:tests/helpers.hpp:15-31 (libstdc++
+ * std::mt19937_64 + std::normal_distribution, row-by-row fill). Output of
+ * random_points is n x d COLUMN-major like the Eigen matrix it mirrors. */
+void oracle_random_points(int64_t n, int64_t d, uint64_t seed, double scale, double* out);
+void oracle_random_vector(int64_t n, uint64_t seed, double* out);
+void oracle_uniform(int64_t n, uint64_t seed, double lo, double hi, double* out);
+void oracle_bernoulli(int64_t n, uint64_t seed, double p, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif
