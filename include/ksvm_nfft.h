@@ -1,0 +1,147 @@
+/* ksvm_nfft.h — C ABI of the B200 ANOVA-NFFT fast-summation path.
+ *
+ * Drop-in for the reference's hot path, P:src/fastsum.cpp (P: =
+ * /root/reference/proj). It sits beside the reference C API
+ * (P:capi/ksvm.h) and uses the same conventions: integer status codes with
+ * the same numeric values, and a thread-local message for the last failure.
+ *
+ * Exported entry point             replaces (reference interface, file:line)
+ * -------------------------------  ---------------------------------------------------------
+ * ksvm_nfft_config_default         FastsumConfig defaults   P:include/ksvm/fastsum.hpp:13-17
+ * ksvm_nfft_config_validate        FastsumConfig::validate  P:src/fastsum.cpp:38-47
+ * ksvm_nfft_plan_create            plan_fastsum             P:include/ksvm/fastsum.hpp:60-62, P:src/fastsum.cpp:103-209
+ * ksvm_nfft_plan_apply             apply_fastsum            P:include/ksvm/fastsum.hpp:65, P:src/fastsum.cpp:300-305
+ * ksvm_nfft_plan_apply_cross       apply_fastsum_cross      P:include/ksvm/fastsum.hpp:70-72, P:src/fastsum.cpp:307-322
+ * ksvm_nfft_plan_num_sources/dim/  FastsumPlan accessors    P:include/ksvm/fastsum.hpp:31-40, P:src/fastsum.cpp:94-101
+ *   scaled_length/coefficient_sum/
+ *   scale_points
+ * ksvm_nfft_plan_free              ~FastsumPlan             P:src/fastsum.cpp:80-90
+ * ksvm_nfft_op_create              anova_fast_operator      P:include/ksvm/fastsum.hpp:81-84, P:src/fastsum.cpp:326-341,366-371
+ * ksvm_nfft_op_size                KernelOperator::size     P:include/ksvm/kernel.hpp:35
+ * ksvm_nfft_op_apply               KernelOperator::apply    P:include/ksvm/kernel.hpp:36, P:src/fastsum.cpp:345-352
+ * ksvm_nfft_op_apply_batch         k applies (Nystrom sketch Y = K G, P:src/low_rank.cpp:139-150)
+ * ksvm_nfft_op_entry               KernelOperator::entry    P:include/ksvm/kernel.hpp:37, P:src/fastsum.cpp:354-356
+ * ksvm_nfft_kernel_rows            WindowOperator::entry rows / anova rows for pivoted Cholesky
+ *                                                           P:src/pipeline.cpp:103-105, P:src/low_rank.cpp:49-51
+ * ksvm_nfft_kernel_diag            diagonal loop            P:src/low_rank.cpp:33-35
+ * ksvm_nfft_op_free                ~AnovaFastOperator
+ *
+ * Status values equal ksvm_status (P:capi/ksvm.h:17-23): 0 ok, 2 data/domain
+ * error (DomainError, P:src/fastsum.cpp:316-320), 4 invalid argument
+ * (std::invalid_argument), 5 internal (CUDA failure, out of memory).
+ *
+ * Point matrices are n x d doubles addressed as
+ *   layout == KSVM_NFFT_ROW_MAJOR: x(i, j) = points[i * ld + j]  (ld >= d)
+ *   layout == KSVM_NFFT_COL_MAJOR: x(i, j) = points[j * ld + i]  (ld >= n)
+ * Eigen's MatrixXd (what plan_fastsum receives) is COL_MAJOR with ld = n;
+ * ksvm_dataset_from_arrays' input (P:capi/ksvm.h:46-47) is ROW_MAJOR, ld = d.
+ *
+ * Vectors v / y are length-n doubles. ptr_kind says where they live:
+ * KSVM_NFFT_HOST (the call copies, runs and synchronises) or
+ * KSVM_NFFT_DEVICE (pointers are on the plan's device; work is ordered after
+ * `stream` (a cudaStream_t, NULL = legacy default) and the call returns once
+ * it is enqueued). Plans and operators are immutable after creation; applies
+ * from several threads are safe (they serialise on the object's internal
+ * stream) and bit-reproducible run to run (no atomics anywhere on the path).
+ */
+#ifndef KSVM_NFFT_H
+#define KSVM_NFFT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    KSVM_NFFT_OK = 0,
+    KSVM_NFFT_ERR_DATA = 2,
+    KSVM_NFFT_ERR_CONFIG = 4,
+    KSVM_NFFT_ERR_INTERNAL = 5
+};
+
+enum { KSVM_NFFT_ROW_MAJOR = 0, KSVM_NFFT_COL_MAJOR = 1 };
+enum { KSVM_NFFT_HOST = 0, KSVM_NFFT_DEVICE = 1 };
+enum { KSVM_NFFT_FP64 = 0 };
+
+/* FastsumConfig (P:include/ksvm/fastsum.hpp:13-20). */
+typedef struct {
+    int bandwidth;       /* N, even, >= 2           (default 32)   */
+    int window_cutoff;   /* m, in [2, 8]            (default 4)    */
+    int oversampling;    /* sigma, grid edge M = sigma * N (default 2) */
+    double torus_radius; /* r_T in (0, 1/4]         (default 0.25) */
+} ksvm_nfft_config;
+
+typedef struct ksvm_nfft_plan ksvm_nfft_plan;
+typedef struct ksvm_nfft_op ksvm_nfft_op;
+
+const char* ksvm_nfft_last_error(void);
+/* Library build string and the number of CUDA kernel launches this process
+ * has issued through the library (instrumentation for the benchmark). */
+const char* ksvm_nfft_version(void);
+int64_t ksvm_nfft_launch_count(void);
+
+void ksvm_nfft_config_default(ksvm_nfft_config* cfg);
+int ksvm_nfft_config_validate(const ksvm_nfft_config* cfg);
+
+/* ---- single-window plan (FastsumPlan) -------------------------------- */
+int ksvm_nfft_plan_create(const double* points, int64_t n, int d, int64_t ld, int layout,
+                          double length_scale, const ksvm_nfft_config* cfg,
+                          double fit_fraction, int device, ksvm_nfft_plan** out);
+int ksvm_nfft_plan_apply(const ksvm_nfft_plan* plan, const double* v, double* out,
+                         int ptr_kind, void* stream);
+/* targets: t x d raw window coordinates (host), mapped with the plan's
+ * affine map; DomainError (status 2) if any lands outside r_T (1 + 1e-12). */
+int ksvm_nfft_plan_apply_cross(const ksvm_nfft_plan* plan, const double* targets, int64_t t,
+                               int64_t ld, int layout, const double* v, double* out,
+                               int ptr_kind, void* stream);
+int64_t ksvm_nfft_plan_num_sources(const ksvm_nfft_plan* plan);
+int ksvm_nfft_plan_dim(const ksvm_nfft_plan* plan);
+double ksvm_nfft_plan_scaled_length(const ksvm_nfft_plan* plan);
+double ksvm_nfft_plan_coefficient_sum(const ksvm_nfft_plan* plan);
+/* out: t x d, same layout/ld convention as the input. */
+int ksvm_nfft_plan_scale_points(const ksvm_nfft_plan* plan, const double* pts, int64_t t,
+                                int64_t ld, int layout, double* out);
+void ksvm_nfft_plan_free(ksvm_nfft_plan* plan);
+
+/* ---- ANOVA operator (anova_fast_operator) ------------------------------
+ * window_features: concatenation of the P windows' 0-based feature indices;
+ * window_sizes[l] in 1..3; weights = eta_l > 0; length_scales = ell_l > 0.
+ * window_mask (NULL = all windows) selects the windows this process owns
+ * when windows are sharded over GPUs: apply then returns the partial sum
+ * over the owned windows, and the caller sums partials across ranks
+ * (SURVEY.md 8(e)). Entries (op_entry / kernel_rows / kernel_diag) always use
+ * every window. */
+int ksvm_nfft_op_create(const double* points, int64_t n, int64_t d, int64_t ld, int layout,
+                        const int* window_features, const int* window_sizes,
+                        int num_windows, const double* weights,
+                        const double* length_scales, const ksvm_nfft_config* cfg,
+                        double fit_fraction, const int* window_mask, int device,
+                        int precision, ksvm_nfft_op** out);
+int64_t ksvm_nfft_op_size(const ksvm_nfft_op* op);
+int ksvm_nfft_op_num_windows(const ksvm_nfft_op* op);
+int ksvm_nfft_op_apply(const ksvm_nfft_op* op, const double* v, double* y, int ptr_kind,
+                       void* stream);
+/* k right-hand sides; column c of V / Y starts at V + c * ld (ld >= n). */
+int ksvm_nfft_op_apply_batch(const ksvm_nfft_op* op, const double* V, double* Y, int k,
+                             int64_t ld, int ptr_kind, void* stream);
+double ksvm_nfft_op_entry(const ksvm_nfft_op* op, int64_t i, int64_t j);
+/* Exact kernel rows: out[r * n + j] = K(rows[r], j) with
+ *   window >= 0 : exp(-||x_i^W - x_j^W||^2 / ell_W^2) on the op's raw window
+ *                 coordinates (P:src/pipeline.cpp:103-105)
+ *   window == -1: the ANOVA entry sum_l eta_l exp(...) (P:src/kernel.cpp:15-29)
+ * rows is a host array; out follows ptr_kind. */
+int ksvm_nfft_kernel_rows(const ksvm_nfft_op* op, int window, const int64_t* rows, int r,
+                          double* out, int ptr_kind, void* stream);
+int ksvm_nfft_kernel_diag(const ksvm_nfft_op* op, int window, double* out, int ptr_kind,
+                          void* stream);
+/* Per-apply stage timing of the last apply (device ms from CUDA events):
+ * [spread, reduce, grid, gather, combine]. Returns the number filled. */
+int ksvm_nfft_op_last_stage_ms(const ksvm_nfft_op* op, float* ms, int cap);
+void ksvm_nfft_op_free(ksvm_nfft_op* op);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,16 @@
+"""B200-native NFFT-accelerated ANOVA Gaussian-kernel matvec.
+
+The hot path of arXiv 2312.00538's kernel-SVM interior point method
+(reference: /root/reference/proj/src/fastsum.cpp), rebuilt as hand-written
+sm_100a CUDA behind a C ABI (include/ksvm_nfft.h, libksvm_nfft.so) with this
+package as the Python mirror of the reference's operator seam.
+"""
+from .fastsum import (AnovaFastOperator, AnovaKernelSpec, Dataset, DomainError, FastsumConfig,
+                      FastsumPlan, FeatureWindowing, GaussianKernelSpec, KernelOperator,
+                      anova_fast_operator, apply_fastsum, apply_fastsum_cross, plan_fastsum)
+
+__all__ = [
+    "AnovaFastOperator", "AnovaKernelSpec", "Dataset", "DomainError", "FastsumConfig",
+    "FastsumPlan", "FeatureWindowing", "GaussianKernelSpec", "KernelOperator",
+    "anova_fast_operator", "apply_fastsum", "apply_fastsum_cross", "plan_fastsum",
+]

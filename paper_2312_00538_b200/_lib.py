@@ -1,0 +1,88 @@
+"""ctypes binding of the C ABI in include/ksvm_nfft.h (libksvm_nfft.so).
+
+The library is built in-tree (``python -c "import __graft_entry__ as g; g.build()"``
+or ``make -C paper_2312_00538_b200/csrc``). There is no fallback: if the
+shared library is missing, importing the product API raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libksvm_nfft.so")
+
+OK, ERR_DATA, ERR_CONFIG, ERR_INTERNAL = 0, 2, 4, 5
+ROW_MAJOR, COL_MAJOR = 0, 1
+HOST, DEVICE = 0, 1
+FP64 = 0
+
+
+class Config(C.Structure):
+    _fields_ = [("bandwidth", C.c_int), ("window_cutoff", C.c_int),
+                ("oversampling", C.c_int), ("torus_radius", C.c_double)]
+
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+_lp = C.POINTER(C.c_int64)
+_vp = C.c_void_p
+
+_SIGS = {
+    "ksvm_nfft_last_error": (C.c_char_p, []),
+    "ksvm_nfft_version": (C.c_char_p, []),
+    "ksvm_nfft_launch_count": (C.c_int64, []),
+    "ksvm_nfft_config_default": (None, [C.POINTER(Config)]),
+    "ksvm_nfft_config_validate": (C.c_int, [C.POINTER(Config)]),
+    "ksvm_nfft_plan_create": (C.c_int, [_vp, C.c_int64, C.c_int, C.c_int64, C.c_int, C.c_double,
+                                        C.POINTER(Config), C.c_double, C.c_int, C.POINTER(_vp)]),
+    "ksvm_nfft_plan_apply": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp]),
+    "ksvm_nfft_plan_apply_cross": (C.c_int, [_vp, _vp, C.c_int64, C.c_int64, C.c_int, _vp, _vp,
+                                             C.c_int, _vp]),
+    "ksvm_nfft_plan_num_sources": (C.c_int64, [_vp]),
+    "ksvm_nfft_plan_dim": (C.c_int, [_vp]),
+    "ksvm_nfft_plan_scaled_length": (C.c_double, [_vp]),
+    "ksvm_nfft_plan_coefficient_sum": (C.c_double, [_vp]),
+    "ksvm_nfft_plan_scale_points": (C.c_int, [_vp, _vp, C.c_int64, C.c_int64, C.c_int, _vp]),
+    "ksvm_nfft_plan_free": (None, [_vp]),
+    "ksvm_nfft_op_create": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, C.c_int, _ip, _ip,
+                                      C.c_int, _dp, _dp, C.POINTER(Config), C.c_double, _ip,
+                                      C.c_int, C.c_int, C.POINTER(_vp)]),
+    "ksvm_nfft_op_size": (C.c_int64, [_vp]),
+    "ksvm_nfft_op_num_windows": (C.c_int, [_vp]),
+    "ksvm_nfft_op_apply": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp]),
+    "ksvm_nfft_op_apply_batch": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int64, C.c_int, _vp]),
+    "ksvm_nfft_op_entry": (C.c_double, [_vp, C.c_int64, C.c_int64]),
+    "ksvm_nfft_kernel_rows": (C.c_int, [_vp, C.c_int, _lp, C.c_int, _vp, C.c_int, _vp]),
+    "ksvm_nfft_kernel_diag": (C.c_int, [_vp, C.c_int, _vp, C.c_int, _vp]),
+    "ksvm_nfft_op_last_stage_ms": (C.c_int, [_vp, C.POINTER(C.c_float), C.c_int]),
+    "ksvm_nfft_op_free": (None, [_vp]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+def load():
+    """Load libksvm_nfft.so (raises if it was not built — no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+                              "(the B200 path has no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    return load().ksvm_nfft_last_error().decode()
+
+
+def launch_count() -> int:
+    return int(load().ksvm_nfft_launch_count())

@@ -1,0 +1,1007 @@
+// Host side of the B200 ANOVA-NFFT path and its C ABI (include/ksvm_nfft.h).
+//
+// Plan construction mirrors P:src/fastsum.cpp:103-209 exactly where it
+// defines results (affine map, ell_scaled, the kept Fourier multipliers) and
+// departs from it where only the execution strategy changes (points sorted
+// into cell tiles on the device; the grid FFT pair replaced by the
+// equivalent separable real convolution).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <cub/device/device_radix_sort.cuh>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ksvm_nfft.h"
+#include "nfft_engine.cuh"
+
+namespace ksvm_nfft {
+
+// launchers (nfft_kernels.cu)
+cudaError_t init_kernel_attributes();
+void launch_spread(int D, int S, int PE, const Item* items, int nitems, const DPSet* ps,
+                   const DWin* wins, const double* v, double* patches, cudaStream_t st);
+void launch_gather(int D, int S, int PE, const Item* items, int nitems, const DPSet* ps,
+                   const DWin* wins, cudaStream_t st);
+void launch_reduce(const DWin* wins, const int* slots, int nslots, long long max_nodes,
+                   const double* patches, cudaStream_t st);
+void launch_conv(const DWin* wins, const int* slots, int nslots, long long max_nodes, int stage,
+                 cudaStream_t st);
+void launch_combine(double* y, const double* parts, const double* eta, int P, long long n,
+                    cudaStream_t st);
+void launch_kernel_rows(double* out, const long long* rows, int r, const double* const* cols,
+                        const int* wdim, const double* wgt, const double* ell2, int nw,
+                        long long n, cudaStream_t st);
+void launch_fill(double* out, double val, long long n, cudaStream_t st);
+void launch_cell_keys(const double* x0, const double* x1, const double* x2, int d, long long n,
+                      double Mf, int cmin, int ncell, int TC, int ntile, unsigned* keys, int* idx,
+                      int* bad, cudaStream_t st);
+void launch_permute(double* dst, const double* src, const int* perm, long long n, cudaStream_t st);
+
+namespace {
+
+thread_local std::string t_err = "ok";
+std::atomic<int64_t> g_launches{0};
+
+struct DomainErr : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+#define CK(x) ck((x), #x)
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return KSVM_NFFT_OK;
+    } catch (const DomainErr& e) {
+        t_err = e.what();
+        return KSVM_NFFT_ERR_DATA;
+    } catch (const std::invalid_argument& e) {
+        t_err = e.what();
+        return KSVM_NFFT_ERR_CONFIG;
+    } catch (const std::bad_alloc&) {
+        t_err = "out of memory";
+        return KSVM_NFFT_ERR_INTERNAL;
+    } catch (const std::exception& e) {
+        t_err = e.what();
+        return KSVM_NFFT_ERR_INTERNAL;
+    }
+}
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
+        o.p = nullptr;
+        o.n = 0;
+    }
+    ~DevBuf() { reset(); }
+    void reset() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void alloc(size_t count) {
+        reset();
+        if (count == 0) count = 1;
+        CK(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void upload(const T* h, size_t count, cudaStream_t st) {
+        alloc(count);
+        CK(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, st));
+    }
+};
+
+struct DeviceGuard {
+    int prev = 0;
+    explicit DeviceGuard(int dev) {
+        CK(cudaGetDevice(&prev));
+        if (prev != dev) CK(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+void ensure_attributes(int dev) {
+    static std::mutex mu;
+    static std::vector<bool> done(256, false);
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev >= 0 && dev < 256 && !done[static_cast<size_t>(dev)]) {
+        CK(init_kernel_attributes());
+        done[static_cast<size_t>(dev)] = true;
+    }
+}
+
+// P:src/fastsum.cpp:38-47
+void validate_cfg(const ksvm_nfft_config& c) {
+    if (c.bandwidth < 2 || c.bandwidth % 2 != 0)
+        throw std::invalid_argument("bandwidth must be a positive even integer");
+    if (c.window_cutoff < 2 || c.window_cutoff > 8)
+        throw std::invalid_argument("window_cutoff must lie in [2, 8]");
+    if (c.oversampling < 1) throw std::invalid_argument("oversampling must be >= 1");
+    if (!(c.torus_radius > 0.0 && c.torus_radius <= 0.25))
+        throw std::invalid_argument("torus_radius must lie in (0, 1/4]");
+}
+
+inline double at(const double* p, int64_t i, int64_t j, int64_t ld, int layout) {
+    return layout == KSVM_NFFT_COL_MAJOR ? p[j * ld + i] : p[i * ld + j];
+}
+
+void check_layout(int64_t n, int64_t d, int64_t ld, int layout) {
+    if (layout != KSVM_NFFT_ROW_MAJOR && layout != KSVM_NFFT_COL_MAJOR)
+        throw std::invalid_argument("layout must be KSVM_NFFT_ROW_MAJOR or KSVM_NFFT_COL_MAJOR");
+    if (layout == KSVM_NFFT_ROW_MAJOR ? ld < d : ld < n)
+        throw std::invalid_argument("leading dimension too small");
+}
+
+const long double kPi = 3.141592653589793238462643383279502884L;
+
+// Per-dimension Fourier data of the rescaled Gaussian (P:src/fastsum.cpp:142-199).
+// The reference's d-dim coefficients are products of these 1-D factors:
+// b_J = prod_t b1[J_t] (the N^d samples are a tensor product), and so is the
+// multiplier mult[J] = b_J * prod_t exp(2 b (pi J_t / M)^2) = prod_t m1[J_t].
+struct Spectral1D {
+    std::vector<long double> b1, m1;  // index J + N/2, J in I_N = [-N/2, N/2)
+};
+
+Spectral1D spectral_1d(int N, int M, double bwin, double ell_s) {
+    Spectral1D s;
+    s.b1.assign(static_cast<size_t>(N), 0.0L);
+    s.m1.assign(static_cast<size_t>(N), 0.0L);
+    const long double inv_l2 = 1.0L / (static_cast<long double>(ell_s) * ell_s);
+    std::vector<long double> f(static_cast<size_t>(N));
+    for (int k = 0; k < N; ++k) {
+        const long double c = static_cast<long double>(k < N / 2 ? k : k - N) / N;
+        f[static_cast<size_t>(k)] = std::exp(-c * c * inv_l2);
+    }
+    for (int J = -N / 2; J < N / 2; ++J) {
+        long double acc = 0.0L;
+        for (int k = 0; k < N; ++k) {
+            const long long ph = ((static_cast<long long>(k) * J) % N + N) % N;  // exact reduction
+            acc += f[static_cast<size_t>(k)] * std::cos(2.0L * kPi * ph / N);
+        }
+        const long double bJ = acc / N;
+        const long double arg = kPi * J / M;
+        s.b1[static_cast<size_t>(J + N / 2)] = bJ;
+        s.m1[static_cast<size_t>(J + N / 2)] = bJ * std::exp(2.0L * bwin * arg * arg);
+    }
+    return s;
+}
+
+struct PointSet {
+    int64_t n = 0;
+    int d = 0;
+    DevBuf<double> x[3];
+    DevBuf<int> perm;
+    std::vector<Item> items;      // host copy (global numbering assigned later)
+    std::vector<int> tile_first;  // local item index of each tile's first item
+};
+
+struct Window {
+    int d = 0;
+    int feat[3] = {0, 0, 0};
+    double ell = 1.0, eta = 1.0;
+    bool owned = true;
+    // affine map (P:src/fastsum.cpp:126-140)
+    double center[3] = {0, 0, 0};
+    double scale = 1.0, ell_s = 0.0, coef_sum = 0.0;
+    DWin dw{};
+    DevBuf<double> G, H, T[4], tabA, tabS;
+    DevBuf<int> tile_first;
+    PointSet src;
+};
+
+struct Geometry {
+    int M, S, m, cmin, ncell, TC, ntile, PE, Lext, Lg, lo, wrap;
+};
+
+Geometry geometry(const ksvm_nfft_config& c, int d) {
+    Geometry g{};
+    g.M = c.oversampling * c.bandwidth;
+    g.m = c.window_cutoff;
+    g.S = 2 * g.m;
+    // Every admissible point (sources: |x| <= fit r_T; cross targets:
+    // ||x|| <= r_T (1 + 1e-12), P:src/fastsum.cpp:316) has floor(x M) in
+    // [cmin, cmax]; one cell of guard on each side.
+    const double rx = c.torus_radius * (1.0 + 1e-12) * g.M;
+    g.cmin = static_cast<int>(std::floor(-rx)) - 1;
+    const int cmax = static_cast<int>(std::floor(rx)) + 1;
+    g.ncell = cmax - g.cmin + 1;
+    g.TC = d == 3 ? 4 : (d == 2 ? 8 : 32);
+    g.ntile = (g.ncell + g.TC - 1) / g.TC;
+    g.PE = g.TC + g.S - 1;
+    g.Lext = g.ncell + g.S - 1;
+    g.lo = g.cmin - g.m + 1;
+    g.wrap = g.Lext > g.M ? 1 : 0;
+    g.Lg = g.wrap ? g.M : g.Lext;
+    return g;
+}
+
+// Sort a point set by (tile, cell) on the device and split tiles into items.
+void build_pointset(PointSet& ps, const std::vector<double>& scaled_cm, int64_t n, int d,
+                    const Geometry& g, cudaStream_t st) {
+    ps.n = n;
+    ps.d = d;
+    DevBuf<double> raw[3];
+    for (int t = 0; t < d; ++t) raw[t].upload(scaled_cm.data() + static_cast<size_t>(t) * n, n, st);
+    DevBuf<unsigned> keys_in, keys_out;
+    DevBuf<int> idx_in, bad;
+    keys_in.alloc(n);
+    keys_out.alloc(n);
+    idx_in.alloc(n);
+    ps.perm.alloc(n);
+    bad.alloc(1);
+    CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+    launch_cell_keys(raw[0].p, d > 1 ? raw[1].p : nullptr, d > 2 ? raw[2].p : nullptr, d, n,
+                     static_cast<double>(g.M), g.cmin, g.ncell, g.TC, g.ntile, keys_in.p,
+                     idx_in.p, bad.p, st);
+    CK(cudaGetLastError());
+    unsigned maxkey = 1;
+    for (int t = 0; t < d; ++t) maxkey *= static_cast<unsigned>(g.ntile * g.TC);
+    int bits = 1;
+    while ((1u << bits) < maxkey && bits < 32) ++bits;
+    size_t tmp_bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys_in.p, keys_out.p, idx_in.p,
+                                       ps.perm.p, static_cast<int>(n), 0, bits, st));
+    DevBuf<unsigned char> tmp;
+    tmp.alloc(tmp_bytes);
+    CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, keys_in.p, keys_out.p, idx_in.p,
+                                       ps.perm.p, static_cast<int>(n), 0, bits, st));
+    for (int t = 0; t < d; ++t) {
+        ps.x[t].alloc(n);
+        launch_permute(ps.x[t].p, raw[t].p, ps.perm.p, n, st);
+    }
+    std::vector<unsigned> hk(static_cast<size_t>(n));
+    int hbad = 0;
+    CK(cudaMemcpyAsync(hk.data(), keys_out.p, sizeof(unsigned) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (hbad) throw std::runtime_error("internal: point outside the planned cell range");
+
+    unsigned tcd = 1;
+    int ntiles = 1;
+    for (int t = 0; t < d; ++t) {
+        tcd *= static_cast<unsigned>(g.TC);
+        ntiles *= g.ntile;
+    }
+    // Items: tiles split into chunks of <= chunk points (fixed at plan time,
+    // so the summation order -- and hence every bit of the result -- is a
+    // function of the plan alone).
+    const int64_t chunk = std::max<int64_t>(256, (n + 8 * 148 - 1) / (8 * 148));
+    ps.items.clear();
+    ps.tile_first.assign(static_cast<size_t>(ntiles) + 1, 0);
+    int64_t i = 0;
+    for (int T = 0; T < ntiles; ++T) {
+        ps.tile_first[static_cast<size_t>(T)] = static_cast<int>(ps.items.size());
+        int64_t j = i;
+        while (j < n && hk[static_cast<size_t>(j)] / tcd == static_cast<unsigned>(T)) ++j;
+        const int64_t cnt = j - i;
+        if (cnt > 0) {
+            const int64_t pieces = (cnt + chunk - 1) / chunk;
+            for (int64_t q = 0; q < pieces; ++q) {
+                Item it{};
+                it.tile = T;
+                it.begin = static_cast<int>(i + cnt * q / pieces);
+                it.end = static_cast<int>(i + cnt * (q + 1) / pieces);
+                ps.items.push_back(it);
+            }
+        }
+        i = j;
+    }
+    ps.tile_first[static_cast<size_t>(ntiles)] = static_cast<int>(ps.items.size());
+}
+
+// Affine map of P:src/fastsum.cpp:126-140 on a column-major n x d block.
+void affine_map(Window& w, const std::vector<double>& cm, int64_t n, double fit, double rT) {
+    const int d = w.d;
+    for (int t = 0; t < d; ++t) {
+        double hi = cm[static_cast<size_t>(t) * n], lo = hi;
+        for (int64_t i = 1; i < n; ++i) {
+            const double x = cm[static_cast<size_t>(t * n + i)];
+            hi = std::max(hi, x);
+            lo = std::min(lo, x);
+        }
+        w.center[t] = 0.5 * (hi + lo);
+    }
+    double radius = 0.0;
+    for (int64_t i = 0; i < n; ++i) {
+        double s = 0.0;
+        for (int t = 0; t < d; ++t) {
+            const double diff = cm[static_cast<size_t>(t * n + i)] - w.center[t];
+            s += diff * diff;
+        }
+        radius = std::max(radius, std::sqrt(s));
+    }
+    w.scale = radius > 0.0 ? fit * rT / radius : 1.0;
+    w.ell_s = w.scale * w.ell;
+    if (w.ell_s > rT && std::getenv("KSVM_NFFT_QUIET") == nullptr)
+        std::fprintf(stderr,
+                     "ksvm: warning: scaled length scale %g exceeds torus radius %g; "
+                     "periodization error may be large\n",
+                     w.ell_s, rT);
+}
+
+std::vector<double> scale_cm(const Window& w, const double* pts, int64_t t, int64_t ld, int layout,
+                             const int* cols) {
+    std::vector<double> out(static_cast<size_t>(t) * w.d);
+    for (int c = 0; c < w.d; ++c)
+        for (int64_t i = 0; i < t; ++i)
+            out[static_cast<size_t>(c * t + i)] =
+                (at(pts, i, cols[c], ld, layout) - w.center[c]) * w.scale;
+    return out;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// The engine: every owned window's plan plus the per-apply scratch.
+// ---------------------------------------------------------------------------
+struct Engine {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    cudaEvent_t ev_stage[6] = {};
+    bool stage_timing = false;
+    ksvm_nfft_config cfg{};
+    double fit = 1.0;
+    int64_t n = 0;
+    int64_t dfull = 0;
+    std::vector<std::unique_ptr<Window>> wins;  // all windows, window order
+    std::vector<int> owned;                     // window indices owned here, ascending
+    std::vector<double> raw_rm;                 // row-major window features (entries)
+    std::vector<int> raw_cols;                  // feature index of each raw_rm column
+    // device state
+    DevBuf<DWin> d_wins;    // owned windows (slot = position in `owned`)
+    DevBuf<DPSet> d_ps;     // sources of owned windows
+    DevBuf<Item> d_items;   // source items of owned windows, grouped by d
+    DevBuf<int> d_slots;    // 0..P_owned-1
+    DevBuf<double> d_eta;
+    DevBuf<double> patches, parts, vbuf, ybuf;
+    DevBuf<double> d_raw;   // SoA raw window features (entries), original order
+    DevBuf<const double*> d_rawcols;
+    DevBuf<int> d_wdim;
+    int class_begin[4] = {0, 0, 0, 0}, class_end[4] = {0, 0, 0, 0};
+    int class_PE[4] = {0, 0, 0, 0};
+    long long max_nodes = 0;
+    std::mutex mu;
+    float last_ms[5] = {0, 0, 0, 0, 0};
+
+    ~Engine() {
+        if (stream) {
+            cudaSetDevice(device);
+            cudaStreamSynchronize(stream);
+            cudaStreamDestroy(stream);
+            cudaEventDestroy(ev_in);
+            cudaEventDestroy(ev_out);
+            for (auto& e : ev_stage)
+                if (e) cudaEventDestroy(e);
+        }
+    }
+
+    int P_owned() const { return static_cast<int>(owned.size()); }
+
+    void init(int dev) {
+        device = dev;
+        CK(cudaSetDevice(dev));
+        ensure_attributes(dev);
+        CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
+        stage_timing = std::getenv("KSVM_NFFT_STAGE_TIMING") != nullptr;
+        if (stage_timing)
+            for (auto& e : ev_stage) CK(cudaEventCreate(&e));
+    }
+
+    // plan_fastsum for one window (P:src/fastsum.cpp:103-209) on the device.
+    void plan_window(Window& w, const std::vector<double>& cm) {
+        const int d = w.d;
+        affine_map(w, cm, n, fit, cfg.torus_radius);
+        std::vector<double> sc(static_cast<size_t>(n) * d);
+        for (int t = 0; t < d; ++t)
+            for (int64_t i = 0; i < n; ++i)
+                sc[static_cast<size_t>(t * n + i)] = (cm[static_cast<size_t>(t * n + i)] - w.center[t]) * w.scale;
+        const Geometry g = geometry(cfg, d);
+        const double sg = static_cast<double>(cfg.oversampling);
+        const double bwin = (2.0 * sg * g.m) / ((2.0 * sg - 1.0) * 3.14159265358979323846);
+        // spectral data and the separable convolution tables
+        const Spectral1D sp = spectral_1d(cfg.bandwidth, g.M, bwin, w.ell_s);
+        long double csum1 = 0.0L;
+        for (long double b : sp.b1) csum1 += b;
+        long double cs = 1.0L;
+        for (int t = 0; t < d; ++t) cs *= csum1;
+        w.coef_sum = static_cast<double>(cs);
+        const int Lg = g.Lg, N = cfg.bandwidth;
+        std::vector<double> ta(static_cast<size_t>(2 * Lg - 1)), ts(static_cast<size_t>(2 * Lg - 1));
+        for (int r = -(Lg - 1); r <= Lg - 1; ++r) {
+            long double ca = 0.0L, cs2 = 0.0L;
+            for (int J = -N / 2; J < N / 2; ++J) {
+                const long long ph = ((static_cast<long long>(J) * r) % g.M + g.M) % g.M;
+                const long double ang = 2.0L * kPi * ph / g.M;
+                ca += sp.m1[static_cast<size_t>(J + N / 2)] * std::cos(ang);
+                cs2 += sp.m1[static_cast<size_t>(J + N / 2)] * std::sin(ang);
+            }
+            ta[static_cast<size_t>(r + Lg - 1)] = static_cast<double>(ca);
+            ts[static_cast<size_t>(r + Lg - 1)] = static_cast<double>(cs2);
+        }
+        w.tabA.upload(ta.data(), ta.size(), stream);
+        w.tabS.upload(ts.data(), ts.size(), stream);
+        long long nodes = 1;
+        for (int t = 0; t < d; ++t) nodes *= Lg;
+        max_nodes = std::max(max_nodes, nodes);
+        w.G.alloc(nodes);
+        w.H.alloc(nodes);
+        for (int k = 0; k < (d == 1 ? 0 : (d == 2 ? 2 : 4)); ++k) w.T[k].alloc(nodes);
+        build_pointset(w.src, sc, n, d, g, stream);
+
+        DWin& dw = w.dw;
+        dw.d = d;
+        dw.S = g.S;
+        dw.m = g.m;
+        dw.M = g.M;
+        dw.Lg = Lg;
+        dw.lo = g.lo;
+        dw.wrap = g.wrap;
+        dw.cmin = g.cmin;
+        dw.ncell = g.ncell;
+        dw.TC = g.TC;
+        dw.ntile = g.ntile;
+        dw.PE = g.PE;
+        dw.Lext = g.Lext;
+        dw.Mf = static_cast<double>(g.M);
+        dw.bwin = bwin;
+        dw.Cw = 1.0 / std::sqrt(3.14159265358979323846 * bwin);
+        for (int o = 0; o < kMaxSpan; ++o) dw.R[o] = o < g.S ? std::exp(-static_cast<double>(o) * o / bwin) : 0.0;
+        dw.G = w.G.p;
+        dw.H = w.H.p;
+        for (int k = 0; k < 4; ++k) dw.T[k] = w.T[k].p;
+        dw.tabA = w.tabA.p;
+        dw.tabS = w.tabS.p;
+    }
+
+    // Assign global item numbers / patch offsets and upload device tables.
+    void finalize() {
+        const int P = P_owned();
+        std::vector<Item> all;
+        std::vector<DPSet> ps(static_cast<size_t>(P));
+        long long patch_total = 0;
+        for (int D = 1; D <= 3; ++D) {
+            class_begin[D] = static_cast<int>(all.size());
+            for (int s = 0; s < P; ++s) {
+                Window& w = *wins[static_cast<size_t>(owned[static_cast<size_t>(s)])];
+                if (w.d != D) continue;
+                int PV = 1;
+                for (int t = 0; t < D; ++t) PV *= w.dw.PE;
+                class_PE[D] = w.dw.PE;
+                w.dw.item_base = static_cast<int>(all.size());
+                w.dw.patch_base = patch_total;
+                std::vector<int> tf = w.src.tile_first;
+                for (auto& v : tf) v += w.dw.item_base;
+                w.tile_first.upload(tf.data(), tf.size(), stream);
+                w.dw.tile_first = w.tile_first.p;
+                for (const Item& it0 : w.src.items) {
+                    Item it = it0;
+                    it.ps = s;
+                    it.patch = patch_total;
+                    patch_total += PV;
+                    all.push_back(it);
+                }
+            }
+            class_end[D] = static_cast<int>(all.size());
+        }
+        std::vector<DWin> dws(static_cast<size_t>(P));
+        std::vector<double> eta(static_cast<size_t>(P));
+        std::vector<int> slots(static_cast<size_t>(P));
+        parts.alloc(static_cast<size_t>(std::max(P, 1)) * n);
+        for (int s = 0; s < P; ++s) {
+            Window& w = *wins[static_cast<size_t>(owned[static_cast<size_t>(s)])];
+            dws[static_cast<size_t>(s)] = w.dw;
+            eta[static_cast<size_t>(s)] = w.eta;
+            slots[static_cast<size_t>(s)] = s;
+            DPSet& p = ps[static_cast<size_t>(s)];
+            for (int t = 0; t < 3; ++t) p.x[t] = t < w.d ? w.src.x[t].p : nullptr;
+            p.perm = w.src.perm.p;
+            p.n = n;
+            p.win = s;
+            p.out = parts.p + static_cast<size_t>(s) * n;
+        }
+        d_wins.upload(dws.data(), dws.size(), stream);
+        d_ps.upload(ps.data(), ps.size(), stream);
+        d_items.upload(all.data(), all.size(), stream);
+        d_slots.upload(slots.data(), slots.size(), stream);
+        d_eta.upload(eta.data(), eta.size(), stream);
+        patches.alloc(static_cast<size_t>(std::max<long long>(patch_total, 1)));
+        vbuf.alloc(n);
+        ybuf.alloc(n);
+        CK(cudaStreamSynchronize(stream));
+    }
+
+    void mark(int k) {
+        if (stage_timing) CK(cudaEventRecord(ev_stage[k], stream));
+    }
+
+    // spread -> reduce -> conv -> (gather over `targets` or sources)
+    void run_grid(const double* v) {
+        const int P = P_owned();
+        mark(0);
+        for (int D = 1; D <= 3; ++D) {
+            const int cnt = class_end[D] - class_begin[D];
+            if (cnt == 0) continue;
+            launch_spread(D, 2 * cfg.window_cutoff, class_PE[D], d_items.p + class_begin[D], cnt,
+                          d_ps.p, d_wins.p, v, patches.p, stream);
+            ++g_launches;
+        }
+        CK(cudaGetLastError());
+        mark(1);
+        launch_reduce(d_wins.p, d_slots.p, P, max_nodes, patches.p, stream);
+        ++g_launches;
+        mark(2);
+        int maxd = 0;
+        for (int s = 0; s < P; ++s) maxd = std::max(maxd, wins[static_cast<size_t>(owned[static_cast<size_t>(s)])]->d);
+        for (int stg = 0; stg < maxd; ++stg) {
+            launch_conv(d_wins.p, d_slots.p, P, max_nodes, stg, stream);
+            ++g_launches;
+        }
+        CK(cudaGetLastError());
+        mark(3);
+    }
+
+    void run_apply(const double* v, double* y) {
+        const int P = P_owned();
+        if (P == 0) {
+            launch_fill(y, 0.0, n, stream);
+            ++g_launches;
+            return;
+        }
+        run_grid(v);
+        for (int D = 1; D <= 3; ++D) {
+            const int cnt = class_end[D] - class_begin[D];
+            if (cnt == 0) continue;
+            launch_gather(D, 2 * cfg.window_cutoff, class_PE[D], d_items.p + class_begin[D], cnt,
+                          d_ps.p, d_wins.p, stream);
+            ++g_launches;
+        }
+        mark(4);
+        launch_combine(y, parts.p, d_eta.p, P, n, stream);
+        ++g_launches;
+        CK(cudaGetLastError());
+        mark(5);
+    }
+
+    void collect_stage_times() {
+        if (!stage_timing) return;
+        CK(cudaEventSynchronize(ev_stage[5]));
+        for (int k = 0; k < 5; ++k) CK(cudaEventElapsedTime(&last_ms[k], ev_stage[k], ev_stage[k + 1]));
+    }
+
+    // Host/device dispatch shared by every apply-like entry point.
+    template <typename F>
+    void with_io(const double* v, double* y, int ptr_kind, void* ext_stream, int64_t vin,
+                 int64_t yout, F&& body) {
+        DeviceGuard dg(device);
+        std::lock_guard<std::mutex> lk(mu);
+        if (ptr_kind == KSVM_NFFT_HOST) {
+            if (vin > 0) CK(cudaMemcpyAsync(vbuf.p, v, sizeof(double) * vin, cudaMemcpyHostToDevice, stream));
+            body(vbuf.p, ybuf.p);
+            if (yout > 0) CK(cudaMemcpyAsync(y, ybuf.p, sizeof(double) * yout, cudaMemcpyDeviceToHost, stream));
+            CK(cudaStreamSynchronize(stream));
+            collect_stage_times();
+        } else if (ptr_kind == KSVM_NFFT_DEVICE) {
+            cudaStream_t es = static_cast<cudaStream_t>(ext_stream);
+            CK(cudaEventRecord(ev_in, es));
+            CK(cudaStreamWaitEvent(stream, ev_in, 0));
+            body(v, y);
+            CK(cudaEventRecord(ev_out, stream));
+            CK(cudaStreamWaitEvent(es, ev_out, 0));
+        } else {
+            throw std::invalid_argument("ptr_kind must be KSVM_NFFT_HOST or KSVM_NFFT_DEVICE");
+        }
+    }
+};
+
+}  // namespace ksvm_nfft
+
+using namespace ksvm_nfft;
+
+struct ksvm_nfft_op {
+    Engine e;
+};
+
+struct ksvm_nfft_plan {
+    Engine e;  // one window, eta = 1
+};
+
+namespace {
+
+void build_engine(Engine& E, const double* points, int64_t n, int64_t d, int64_t ld, int layout,
+                  const int* feats, const int* sizes, int P, const double* weights,
+                  const double* ells, const ksvm_nfft_config* cfg, double fit, const int* mask,
+                  int device, int precision) {
+    if (!points || !feats || !sizes || !weights || !ells || !cfg)
+        throw std::invalid_argument("null argument");
+    validate_cfg(*cfg);
+    if (precision != KSVM_NFFT_FP64) throw std::invalid_argument("only KSVM_NFFT_FP64 is supported");
+    if (n < 1) throw std::invalid_argument("empty node set");
+    if (n > 2147483647LL) throw std::invalid_argument("n must be < 2^31");
+    if (!(fit > 0.0 && fit <= 1.0)) throw std::invalid_argument("fit_fraction must lie in (0, 1]");
+    check_layout(n, d, ld, layout);
+    // P:src/windowing.cpp:79-103 (check_windowing)
+    if (P < 1) throw std::invalid_argument("windowing has no windows");
+    std::vector<bool> seen(static_cast<size_t>(d), false);
+    int off = 0;
+    for (int l = 0; l < P; ++l) {
+        if (sizes[l] < 1 || sizes[l] > 3) throw std::invalid_argument("window size must be 1..3");
+        for (int t = 0; t < sizes[l]; ++t) {
+            const int f = feats[off + t];
+            if (f < 0 || f >= d) throw std::invalid_argument("window feature index out of range");
+            if (seen[static_cast<size_t>(f)]) throw std::invalid_argument("feature appears in two windows");
+            seen[static_cast<size_t>(f)] = true;
+        }
+        off += sizes[l];
+    }
+    for (int l = 0; l < P; ++l) {
+        if (!(weights[l] > 0.0)) throw std::invalid_argument("window weights must be positive");
+        if (!(ells[l] > 0.0)) throw std::invalid_argument("length scales must be positive");
+    }
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw std::invalid_argument("no such CUDA device");
+    DeviceGuard dg(device);
+    E.init(device);
+    E.cfg = *cfg;
+    E.fit = fit;
+    E.n = n;
+    E.dfull = d;
+    off = 0;
+    for (int l = 0; l < P; ++l) {
+        auto w = std::make_unique<Window>();
+        w->d = sizes[l];
+        for (int t = 0; t < w->d; ++t) w->feat[t] = feats[off + t];
+        off += sizes[l];
+        w->eta = weights[l];
+        w->ell = ells[l];
+        w->owned = mask ? mask[l] != 0 : true;
+        E.wins.push_back(std::move(w));
+    }
+    // raw window features for entries (row-major host copy + device SoA)
+    for (auto& w : E.wins)
+        for (int t = 0; t < w->d; ++t) E.raw_cols.push_back(w->feat[t]);
+    const int nc = static_cast<int>(E.raw_cols.size());
+    E.raw_rm.resize(static_cast<size_t>(n) * nc);
+    std::vector<double> soa(static_cast<size_t>(n) * nc);
+    for (int64_t i = 0; i < n; ++i)
+        for (int c = 0; c < nc; ++c) {
+            const double x = at(points, i, E.raw_cols[static_cast<size_t>(c)], ld, layout);
+            E.raw_rm[static_cast<size_t>(i * nc + c)] = x;
+            soa[static_cast<size_t>(c) * n + i] = x;
+        }
+    E.d_raw.upload(soa.data(), soa.size(), E.stream);
+    std::vector<const double*> cols(static_cast<size_t>(nc));
+    for (int c = 0; c < nc; ++c) cols[static_cast<size_t>(c)] = E.d_raw.p + static_cast<size_t>(c) * n;
+    E.d_rawcols.upload(cols.data(), cols.size(), E.stream);
+    std::vector<int> wdim;
+    for (auto& w : E.wins) wdim.push_back(w->d);
+    E.d_wdim.upload(wdim.data(), wdim.size(), E.stream);
+    // one plan per owned window (P:src/fastsum.cpp:333-340)
+    int col0 = 0;
+    for (int l = 0; l < P; ++l) {
+        Window& w = *E.wins[static_cast<size_t>(l)];
+        if (w.owned) {
+            std::vector<double> cm(static_cast<size_t>(n) * w.d);
+            for (int t = 0; t < w.d; ++t)
+                std::memcpy(cm.data() + static_cast<size_t>(t) * n, soa.data() + static_cast<size_t>(col0 + t) * n,
+                            sizeof(double) * n);
+            E.plan_window(w, cm);
+            E.owned.push_back(l);
+        }
+        col0 += w.d;
+    }
+    E.finalize();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ksvm_nfft_last_error(void) { return t_err.c_str(); }
+const char* ksvm_nfft_version(void) { return "ksvm_nfft 0.1 sm_100a fp64"; }
+int64_t ksvm_nfft_launch_count(void) { return g_launches.load(); }
+
+void ksvm_nfft_config_default(ksvm_nfft_config* cfg) {
+    if (!cfg) return;
+    cfg->bandwidth = 32;
+    cfg->window_cutoff = 4;
+    cfg->oversampling = 2;
+    cfg->torus_radius = 0.25;
+}
+
+int ksvm_nfft_config_validate(const ksvm_nfft_config* cfg) {
+    return guarded([&] {
+        if (!cfg) throw std::invalid_argument("null config");
+        validate_cfg(*cfg);
+    });
+}
+
+int ksvm_nfft_op_create(const double* points, int64_t n, int64_t d, int64_t ld, int layout,
+                        const int* window_features, const int* window_sizes, int num_windows,
+                        const double* weights, const double* length_scales,
+                        const ksvm_nfft_config* cfg, double fit_fraction, const int* window_mask,
+                        int device, int precision, ksvm_nfft_op** out) {
+    return guarded([&] {
+        if (!out) throw std::invalid_argument("null out");
+        auto op = std::make_unique<ksvm_nfft_op>();
+        build_engine(op->e, points, n, d, ld, layout, window_features, window_sizes, num_windows,
+                     weights, length_scales, cfg, fit_fraction, window_mask, device, precision);
+        *out = op.release();
+    });
+}
+
+int64_t ksvm_nfft_op_size(const ksvm_nfft_op* op) { return op ? op->e.n : 0; }
+int ksvm_nfft_op_num_windows(const ksvm_nfft_op* op) {
+    return op ? static_cast<int>(op->e.wins.size()) : 0;
+}
+
+int ksvm_nfft_op_apply(const ksvm_nfft_op* op, const double* v, double* y, int ptr_kind,
+                       void* stream) {
+    return guarded([&] {
+        if (!op || !v || !y) throw std::invalid_argument("null argument");
+        Engine& E = const_cast<Engine&>(op->e);
+        E.with_io(v, y, ptr_kind, stream, E.n, E.n, [&](const double* dv, double* dy) { E.run_apply(dv, dy); });
+    });
+}
+
+int ksvm_nfft_op_apply_batch(const ksvm_nfft_op* op, const double* V, double* Y, int k, int64_t ld,
+                             int ptr_kind, void* stream) {
+    return guarded([&] {
+        if (!op || !V || !Y) throw std::invalid_argument("null argument");
+        Engine& E = const_cast<Engine&>(op->e);
+        if (ld < E.n) throw std::invalid_argument("ld must be >= n");
+        for (int c = 0; c < k; ++c)
+            E.with_io(V + c * ld, Y + c * ld, ptr_kind, stream, E.n, E.n,
+                      [&](const double* dv, double* dy) { E.run_apply(dv, dy); });
+    });
+}
+
+double ksvm_nfft_op_entry(const ksvm_nfft_op* op, int64_t i, int64_t j) {
+    // P:src/kernel.cpp:15-29 on the raw coordinates, every window
+    const Engine& E = op->e;
+    const size_t nc = E.raw_cols.size();
+    double sum = 0.0;
+    size_t c = 0;
+    for (const auto& w : E.wins) {
+        double d2 = 0.0;
+        for (int t = 0; t < w->d; ++t, ++c) {
+            const double diff = E.raw_rm[static_cast<size_t>(i) * nc + c] - E.raw_rm[static_cast<size_t>(j) * nc + c];
+            d2 += diff * diff;
+        }
+        sum += w->eta * std::exp(-d2 / (w->ell * w->ell));
+    }
+    return sum;
+}
+
+int ksvm_nfft_kernel_rows(const ksvm_nfft_op* op, int window, const int64_t* rows, int r,
+                          double* out, int ptr_kind, void* stream) {
+    return guarded([&] {
+        if (!op || !rows || !out) throw std::invalid_argument("null argument");
+        Engine& E = const_cast<Engine&>(op->e);
+        const int P = static_cast<int>(E.wins.size());
+        if (window < -1 || window >= P) throw std::invalid_argument("window out of range");
+        if (r < 0) throw std::invalid_argument("r must be >= 0");
+        for (int q = 0; q < r; ++q)
+            if (rows[q] < 0 || rows[q] >= E.n) throw std::invalid_argument("row index out of range");
+        if (r == 0) return;
+        int c0 = 0;
+        for (int l = 0; l < (window < 0 ? 0 : window); ++l) c0 += E.wins[static_cast<size_t>(l)]->d;
+        const int nw = window < 0 ? P : 1;
+        std::vector<double> wgt, ell2;
+        for (int l = 0; l < P; ++l) {
+            if (window >= 0 && l != window) continue;
+            const Window& w = *E.wins[static_cast<size_t>(l)];
+            wgt.push_back(window < 0 ? w.eta : -1.0);  // -1: plain exp (WindowOperator)
+            ell2.push_back(w.ell * w.ell);
+        }
+        DeviceGuard dg(E.device);
+        std::lock_guard<std::mutex> lk(E.mu);
+        DevBuf<long long> drows;
+        DevBuf<double> dw, de, dout;
+        static_assert(sizeof(long long) == sizeof(int64_t), "int64");
+        drows.upload(reinterpret_cast<const long long*>(rows), static_cast<size_t>(r), E.stream);
+        dw.upload(wgt.data(), wgt.size(), E.stream);
+        de.upload(ell2.data(), ell2.size(), E.stream);
+        const size_t total = static_cast<size_t>(r) * E.n;
+        cudaStream_t es = static_cast<cudaStream_t>(stream);
+        double* dst = out;
+        if (ptr_kind == KSVM_NFFT_HOST) {
+            dout.alloc(total);
+            dst = dout.p;
+        } else if (ptr_kind == KSVM_NFFT_DEVICE) {
+            CK(cudaEventRecord(E.ev_in, es));
+            CK(cudaStreamWaitEvent(E.stream, E.ev_in, 0));
+        } else {
+            throw std::invalid_argument("bad ptr_kind");
+        }
+        launch_kernel_rows(dst, drows.p, r, E.d_rawcols.p + c0, E.d_wdim.p + (window < 0 ? 0 : window), dw.p, de.p,
+                           nw, E.n, E.stream);
+        ++g_launches;
+        CK(cudaGetLastError());
+        if (ptr_kind == KSVM_NFFT_HOST) {
+            CK(cudaMemcpyAsync(out, dst, sizeof(double) * total, cudaMemcpyDeviceToHost, E.stream));
+        } else {
+            CK(cudaEventRecord(E.ev_out, E.stream));
+            CK(cudaStreamWaitEvent(es, E.ev_out, 0));
+        }
+        CK(cudaStreamSynchronize(E.stream));  // scratch buffers are freed on return
+    });
+}
+
+int ksvm_nfft_kernel_diag(const ksvm_nfft_op* op, int window, double* out, int ptr_kind,
+                          void* stream) {
+    return guarded([&] {
+        if (!op || !out) throw std::invalid_argument("null argument");
+        Engine& E = const_cast<Engine&>(op->e);
+        const int P = static_cast<int>(E.wins.size());
+        if (window < -1 || window >= P) throw std::invalid_argument("window out of range");
+        // exp(-0) = 1 per window: diag = 1 (window) or sum_l eta_l (ANOVA),
+        // accumulated in window order like anova_eval.
+        double val = 1.0;
+        if (window < 0) {
+            val = 0.0;
+            for (const auto& w : E.wins) val += w->eta * 1.0;
+        }
+        if (ptr_kind == KSVM_NFFT_HOST) {
+            for (int64_t i = 0; i < E.n; ++i) out[i] = val;
+            return;
+        }
+        if (ptr_kind != KSVM_NFFT_DEVICE) throw std::invalid_argument("bad ptr_kind");
+        DeviceGuard dg(E.device);
+        launch_fill(out, val, E.n, static_cast<cudaStream_t>(stream));
+        ++g_launches;
+        CK(cudaGetLastError());
+    });
+}
+
+int ksvm_nfft_op_last_stage_ms(const ksvm_nfft_op* op, float* ms, int cap) {
+    if (!op || !ms || !op->e.stage_timing) return 0;
+    const int k = std::min(cap, 5);
+    for (int i = 0; i < k; ++i) ms[i] = op->e.last_ms[i];
+    return k;
+}
+
+void ksvm_nfft_op_free(ksvm_nfft_op* op) { delete op; }
+
+// ---- single-window plan --------------------------------------------------
+
+int ksvm_nfft_plan_create(const double* points, int64_t n, int d, int64_t ld, int layout,
+                          double length_scale, const ksvm_nfft_config* cfg, double fit_fraction,
+                          int device, ksvm_nfft_plan** out) {
+    return guarded([&] {
+        if (!out || !cfg) throw std::invalid_argument("null argument");
+        validate_cfg(*cfg);  // P:src/fastsum.cpp:106 validates before the shape checks
+        if (d < 1 || d > 3) throw std::invalid_argument("fast summation window dimension must be 1..3");
+        if (n < 1) throw std::invalid_argument("empty node set");
+        if (!(fit_fraction > 0.0 && fit_fraction <= 1.0))
+            throw std::invalid_argument("fit_fraction must lie in (0, 1]");
+        if (!(length_scale > 0.0)) throw std::invalid_argument("length scale must be positive");
+        auto p = std::make_unique<ksvm_nfft_plan>();
+        const int feats[3] = {0, 1, 2};
+        const int sizes[1] = {d};
+        const double one = 1.0;
+        build_engine(p->e, points, n, d, ld, layout, feats, sizes, 1, &one, &length_scale, cfg,
+                     fit_fraction, nullptr, device, KSVM_NFFT_FP64);
+        *out = p.release();
+    });
+}
+
+int ksvm_nfft_plan_apply(const ksvm_nfft_plan* plan, const double* v, double* out, int ptr_kind,
+                         void* stream) {
+    return guarded([&] {
+        if (!plan || !v || !out) throw std::invalid_argument("null argument");
+        Engine& E = const_cast<Engine&>(plan->e);
+        E.with_io(v, out, ptr_kind, stream, E.n, E.n, [&](const double* dv, double* dy) { E.run_apply(dv, dy); });
+    });
+}
+
+int ksvm_nfft_plan_apply_cross(const ksvm_nfft_plan* plan, const double* targets, int64_t t,
+                               int64_t ld, int layout, const double* v, double* out, int ptr_kind,
+                               void* stream) {
+    return guarded([&] {
+        if (!plan || !targets || !v || !out) throw std::invalid_argument("null argument");
+        Engine& E = const_cast<Engine&>(plan->e);
+        Window& w = *E.wins[0];
+        if (t < 0) throw std::invalid_argument("t must be >= 0");
+        if (t > 2147483647LL) throw std::invalid_argument("t must be < 2^31");
+        check_layout(t, w.d, ld, layout);
+        const int cols[3] = {0, 1, 2};
+        std::vector<double> sc = scale_cm(w, targets, t, ld, layout, cols);
+        // P:src/fastsum.cpp:316-320
+        for (int64_t j = 0; j < t; ++j) {
+            double s = 0.0;
+            for (int c = 0; c < w.d; ++c) s += sc[static_cast<size_t>(c * t + j)] * sc[static_cast<size_t>(c * t + j)];
+            if (std::sqrt(s) > E.cfg.torus_radius * (1.0 + 1e-12))
+                throw DomainErr("target " + std::to_string(j) + " falls outside the scaled torus ball");
+        }
+        if (t == 0) return;
+        DeviceGuard dg(E.device);
+        std::lock_guard<std::mutex> lk(E.mu);
+        const Geometry g = geometry(E.cfg, w.d);
+        PointSet tp;
+        build_pointset(tp, sc, t, w.d, g, E.stream);
+        DevBuf<double> tout;
+        tout.alloc(t);
+        DPSet dp{};
+        for (int c = 0; c < 3; ++c) dp.x[c] = c < w.d ? tp.x[c].p : nullptr;
+        dp.perm = tp.perm.p;
+        dp.n = t;
+        dp.win = 0;
+        dp.out = ptr_kind == KSVM_NFFT_DEVICE ? out : tout.p;
+        DevBuf<DPSet> dps;
+        dps.upload(&dp, 1, E.stream);
+        std::vector<Item> its = tp.items;
+        for (auto& it : its) it.ps = 0;
+        DevBuf<Item> ditems;
+        ditems.upload(its.data(), its.size(), E.stream);
+        const double* dv = v;
+        cudaStream_t es = static_cast<cudaStream_t>(stream);
+        if (ptr_kind == KSVM_NFFT_HOST) {
+            CK(cudaMemcpyAsync(E.vbuf.p, v, sizeof(double) * E.n, cudaMemcpyHostToDevice, E.stream));
+            dv = E.vbuf.p;
+        } else if (ptr_kind == KSVM_NFFT_DEVICE) {
+            CK(cudaEventRecord(E.ev_in, es));
+            CK(cudaStreamWaitEvent(E.stream, E.ev_in, 0));
+        } else {
+            throw std::invalid_argument("bad ptr_kind");
+        }
+        E.run_grid(dv);
+        launch_gather(w.d, 2 * E.cfg.window_cutoff, w.dw.PE, ditems.p, static_cast<int>(its.size()), dps.p,
+                      E.d_wins.p, E.stream);
+        ++g_launches;
+        CK(cudaGetLastError());
+        if (ptr_kind == KSVM_NFFT_HOST) {
+            CK(cudaMemcpyAsync(out, tout.p, sizeof(double) * t, cudaMemcpyDeviceToHost, E.stream));
+        } else {
+            CK(cudaEventRecord(E.ev_out, E.stream));
+            CK(cudaStreamWaitEvent(es, E.ev_out, 0));
+        }
+        CK(cudaStreamSynchronize(E.stream));  // target scratch is freed on return
+    });
+}
+
+int64_t ksvm_nfft_plan_num_sources(const ksvm_nfft_plan* plan) { return plan ? plan->e.n : 0; }
+int ksvm_nfft_plan_dim(const ksvm_nfft_plan* plan) { return plan ? plan->e.wins[0]->d : 0; }
+double ksvm_nfft_plan_scaled_length(const ksvm_nfft_plan* plan) { return plan->e.wins[0]->ell_s; }
+double ksvm_nfft_plan_coefficient_sum(const ksvm_nfft_plan* plan) { return plan->e.wins[0]->coef_sum; }
+
+int ksvm_nfft_plan_scale_points(const ksvm_nfft_plan* plan, const double* pts, int64_t t, int64_t ld,
+                                int layout, double* out) {
+    return guarded([&] {
+        if (!plan || !pts || !out) throw std::invalid_argument("null argument");
+        const Window& w = *plan->e.wins[0];
+        check_layout(t, w.d, ld, layout);
+        for (int64_t i = 0; i < t; ++i)
+            for (int c = 0; c < w.d; ++c) {
+                const double x = (at(pts, i, c, ld, layout) - w.center[c]) * w.scale;
+                if (layout == KSVM_NFFT_COL_MAJOR) out[c * ld + i] = x;
+                else out[i * ld + c] = x;
+            }
+    });
+}
+
+void ksvm_nfft_plan_free(ksvm_nfft_plan* plan) { delete plan; }
+
+}  // extern "C"

@@ -1,0 +1,66 @@
+// Shared host/device structures of the B200 ANOVA-NFFT engine.
+//
+// Vocabulary: a *window* is one ANOVA feature group (d_l
+// <= 3 features) with its own NFFT plan; its *sources* are the n scaled
+// nodes; the *grid* is the sigma-oversampled M^d torus grid restricted to
+// the nodes any in-ball point can touch; a *cell* is the unit grid cube a
+// point falls in (floor(x M)); a *tile* is TC^d cells whose points one CTA
+// processes; an *item* is a tile's point range (heavy tiles are split into
+// several items); a *patch* is the (TC+2m-1)^d grid block an item spreads
+// into.
+#pragma once
+
+#include <cstdint>
+
+namespace ksvm_nfft {
+
+constexpr int kMaxSpan = 16;  // 2m, m <= 8 (P:src/fastsum.cpp:41-42, w[3][16] at :225)
+
+// One tile's (or part of a tile's) sorted point range.
+struct Item {
+    int ps;         // point-set slot
+    int tile;       // linear tile index within the window's tile grid
+    int begin;      // sorted point range [begin, end)
+    int end;
+    long long patch;  // offset of this item's patch in the patch buffer (spread only)
+};
+
+// Per-window grid description and device buffers.
+struct DWin {
+    int d;       // window dimension 1..3
+    int S;       // taps per dimension, 2m
+    int m;
+    int M;       // grid edge sigma*N
+    int Lg;      // local grid edge (<= M)
+    int lo;      // global index of local node 0 (non-wrapping layout)
+    int wrap;    // 1: local index = global index mod M (Lg == M)
+    int cmin;    // smallest cell index floor(xM) any in-ball point can have
+    int ncell;   // number of cell indices per dimension
+    int TC;      // cells per tile edge
+    int ntile;   // tiles per dimension
+    int PE;      // patch edge TC + S - 1
+    int Lext;    // extended node count ncell + S - 1
+    double Mf;   // M as double
+    double bwin; // Gaussian window shape b (P:src/fastsum.cpp:124)
+    double Cw;   // 1/sqrt(pi b)        (P:src/fastsum.cpp:77)
+    double R[kMaxSpan];  // exp(-o^2/b), o = 0..S-1 (window factorisation)
+    double* G;   // spread grid, Lg^d
+    double* H;   // filtered grid, Lg^d
+    double* T[4];  // separable-convolution temporaries, Lg^d each
+    const double* tabA;  // a(r), r = -(Lg-1)..(Lg-1), index r + Lg - 1
+    const double* tabS;  // s(r)
+    const int* tile_first;  // sources: first item of each tile (ntile^d + 1 entries)
+    int item_base;          // global index of the window's first source item
+    long long patch_base;   // patch-buffer offset of that item
+};
+
+// A sorted point set (a window's sources, or cross-apply targets).
+struct DPSet {
+    const double* x[3];  // scaled coordinates, sorted by (tile, cell)
+    const int* perm;     // sorted position -> original index
+    long long n;
+    int win;             // owning window slot
+    double* out;         // gather output, original order (length n)
+};
+
+}  // namespace ksvm_nfft

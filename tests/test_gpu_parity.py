@@ -1,0 +1,117 @@
+"""GPU parity: the B200 path vs the CPU oracle on identical seeded inputs.
+
+Bar (north_star): relative l2 <= 1e-10 in fp64 against the reference's own
+NFFT matvec (the oracle restatement, pinned bit-for-bit to the reference
+compiled by path in tests/test_oracle.py). Inputs follow the reference's
+tests (P:tests/test_fastsum.cpp, P:tests/helpers.hpp) and the BASELINE
+configs (paper_2312_00538_b200/workloads.py).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2312_00538_b200 import (AnovaKernelSpec, Dataset, DomainError, FastsumConfig,
+                                   FeatureWindowing, GaussianKernelSpec, anova_fast_operator,
+                                   apply_fastsum, apply_fastsum_cross, plan_fastsum)
+from paper_2312_00538_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-10  # relative l2, fp64 (BASELINE.json north_star)
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def spec_of(windows, weights=None, ells=None):
+    P = len(windows)
+    return AnovaKernelSpec(FeatureWindowing([list(w) for w in windows],
+                                            list(weights) if weights is not None else [1.0 / P] * P,
+                                            list(ells) if ells is not None else [1.0] * P))
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_plan_apply_matches_oracle(oracle_lib, d):
+    pts = oracle.random_points(500, d, 31)
+    v = oracle.random_vector(500, 32)
+    gp = plan_fastsum(pts, GaussianKernelSpec(1.0))
+    op = oracle_lib.plan(pts)
+    assert rel(apply_fastsum(gp, v), op.apply(v)) <= TOL
+    assert gp.scaled_length() == pytest.approx(op.scaled_length(), rel=1e-15)
+    assert gp.coefficient_sum() == pytest.approx(op.coefficient_sum(), rel=1e-12)
+
+
+def test_anova_operator_matches_oracle(oracle_lib):
+    # P:tests/test_fastsum.cpp:147-161 inputs
+    pts = oracle.random_points(1000, 6, 61)
+    v = oracle.random_vector(1000, 62)
+    wins, eta, ell = [[0, 1, 2], [3, 4, 5]], [0.5, 0.5], [1.0, 1.3]
+    g = anova_fast_operator(Dataset(pts), spec_of(wins, eta, ell))
+    o = oracle_lib.anova(pts, wins, eta, ell)
+    assert rel(g.apply(v), o.apply(v)) <= TOL
+    assert g.entry(3, 8) == pytest.approx(o.entry(3, 8), rel=1e-14)
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_baseline_config_matches_oracle(oracle_lib, cfg):
+    w = workloads.make(cfg)
+    g = anova_fast_operator(Dataset(w.points), spec_of(w.windows), fit_fraction=w.fit_fraction)
+    o = oracle_lib.anova(w.points, w.windows, fit=w.fit_fraction)
+    assert rel(g.apply(w.v), o.apply(w.v)) <= TOL
+
+
+def test_bit_identical_reuse():
+    # P:tests/test_fastsum.cpp:208-215
+    pts = oracle.random_points(200, 2, 81)
+    v = oracle.random_vector(200, 82)
+    p = plan_fastsum(pts, GaussianKernelSpec(1.0))
+    a, b = apply_fastsum(p, v), apply_fastsum(p, v)
+    assert np.array_equal(a, b)
+    w = workloads.config2(n=20000)
+    op = anova_fast_operator(Dataset(w.points), spec_of(w.windows))
+    assert np.array_equal(op.apply(w.v), op.apply(w.v))
+
+
+def test_cross_apply_matches_oracle(oracle_lib):
+    # P:tests/test_fastsum.cpp:108-145
+    pts = oracle.random_points(300, 2, 51)
+    v = oracle.random_vector(300, 52)
+    gp, op = plan_fastsum(pts, 1.0), oracle_lib.plan(pts)
+    tg = oracle.random_points(100, 2, 53, 0.5)
+    assert rel(apply_fastsum_cross(gp, tg, v), op.apply_cross(tg, v)) <= TOL
+    self_ = apply_fastsum(gp, v)
+    cross = apply_fastsum_cross(gp, pts, v)
+    assert np.abs(self_ - cross).max() <= 1e-12
+    with pytest.raises(DomainError):
+        apply_fastsum_cross(gp, np.array([[1e3, 1e3]]), v)
+
+
+@pytest.mark.parametrize("N,m,sigma", [(8, 4, 2), (16, 4, 2), (32, 2, 2), (32, 3, 2), (32, 6, 2),
+                                       (16, 8, 2), (32, 4, 1), (24, 4, 3)])
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_other_parameters_match_oracle(oracle_lib, N, m, sigma, d):
+    pts = oracle.random_points(400, d, 71)
+    v = oracle.random_vector(400, 72)
+    cfg = FastsumConfig(N, m, sigma, 0.25)
+    gp = plan_fastsum(pts, 1.0, cfg)
+    op = oracle_lib.plan(pts, 1.0, N, m, sigma, 0.25)
+    assert rel(apply_fastsum(gp, v), op.apply(v)) <= TOL
+
+
+def test_kernel_rows_and_diag():
+    w = workloads.config1()
+    op = anova_fast_operator(Dataset(w.points), spec_of(w.windows))
+    rows = [0, 5, 1999]
+    R = op.kernel_rows(rows, window=-1)
+    x = w.points
+    ref = np.zeros((3, w.n))
+    for l, win in enumerate(w.windows):
+        d2 = ((x[rows][:, None, win] - x[None, :, win]) ** 2).sum(-1)
+        ref += 0.5 * np.exp(-d2)
+    assert np.abs(R - ref).max() <= 1e-14
+    R1 = op.kernel_rows(rows, window=1)
+    d2 = ((x[rows][:, None, [3, 4, 5]] - x[None, :, [3, 4, 5]]) ** 2).sum(-1)
+    assert np.abs(R1 - np.exp(-d2)).max() <= 1e-14
+    assert np.all(op.kernel_diag(0) == 1.0)
