@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 ANOVA-NFFT matvec (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+One step = one ANOVA matvec y = sum_l eta_l K~_l v over the whole workload
+(plan construction excluded, as P:tests/acceptance.cpp:232-244 does). The
+default workload is BASELINE.json configs[1] (config 2: n=60000, d=8,
+windows {0,1,2},{3,4,5},{6,7}); --config selects another (1..5).
+
+N > 1 (torchrun, one process per GPU): windows are sharded over ranks (LPT)
+and one NCCL all-reduce per step sums the length-n partial outputs, so each
+step is still ONE matvec of the fixed workload ("scaling": "strong").
+
+Timing: W untimed warm-up steps; K timed steps, each bracketed by CUDA events
+on the launching stream, with a 256 MiB L2 flush (untimed) before every step
+because config 2's inputs fit in the 126 MB L2; barrier + synchronize on both
+sides; max over ranks. nvidia-smi samples clocks during the timed region.
+
+--impl reference times the reference's own CPU fastsum (oracle/_ref, the
+reference's fastsum.cpp compiled unmodified by path; the oracle restatement
+if that library is absent) with every host thread on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--n", type=int, default=None, help="override n (debug only)")
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    return ap.parse_args()
+
+
+METRIC = "ANOVA-NFFT kernel matvecs/sec (fp64)"
+UNIT = "matvecs/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------- clocks ---
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.sw_power_cap",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown"]
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------ CPU legs -----
+def cpu_lib():
+    import oracle
+    if oracle.available("ref"):
+        return oracle.Lib("ref"), "reference"
+    if not oracle.available("oracle"):
+        oracle.build()
+    return oracle.Lib("oracle"), "port"
+
+
+def cpu_baseline(w, budget_s: float):
+    """Single-thread reference fastsum on this host (the reference hot path is
+    single-threaded): repeat full matvecs until budget_s elapses."""
+    lib, kind = cpu_lib()
+    op = lib.anova(w.points, w.windows, fit=w.fit_fraction)
+    times = []
+    t0 = time.perf_counter()
+    while True:
+        s = time.perf_counter()
+        op.apply(w.v)
+        times.append(time.perf_counter() - s)
+        if time.perf_counter() - t0 > budget_s or len(times) >= 50:
+            break
+    best = min(times)
+    return {"value": 1.0 / best, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"{len(times)} full matvecs of {w.name} (best of {len(times)}, 1 thread)",
+            "s_per_matvec_best": best}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_2312_00538_b200 import workloads
+    w = workloads.make(args.config, args.n)
+    lib, kind = cpu_lib()
+    op = lib.anova(w.points, w.windows, fit=w.fit_fraction)
+    T = max(1, os.cpu_count() or 1)
+
+    def step():
+        th = [threading.Thread(target=op.apply, args=(w.v,)) for _ in range(T)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    value = T * args.steps / el
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": w.name, "n": w.n, "d": w.d, "windows": w.windows,
+                       "fit_fraction": w.fit_fraction, "N": 32, "m": 4, "sigma": 2},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": T, "kind": kind,
+                             "sample": f"each step = {T} concurrent full matvecs (one per host thread)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------ GPU arm ------
+def kernel_bytes(w, name):
+    """Algorithmic HBM bytes of one launch (SURVEY.md 8(d) split per kernel):
+    spread_dK reads the coordinates of its windows + v once; gather_dK reads
+    the coordinates + writes y once."""
+    if not (name.startswith("spread_d") or name.startswith("gather_d")):
+        return 0
+    k = int(name[-1])
+    coords = sum(len(x) for x in w.windows if len(x) == k)
+    return 8 * w.n * (coords + 1)
+
+
+def kernel_fmas(w, name, m=4):
+    if not (name.startswith("spread_d") or name.startswith("gather_d")):
+        return 0
+    k = int(name[-1])
+    return w.n * sum((2 * m) ** len(x) for x in w.windows if len(x) == k)
+
+
+def fp64_peak_tflops(dev):
+    import torch
+    a = torch.randn(8192, 8192, dtype=torch.float64, device=dev)
+    b = torch.randn(8192, 8192, dtype=torch.float64, device=dev)
+    for _ in range(2):
+        torch.matmul(a, b)
+    torch.cuda.synchronize(dev)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = 1e30
+    for _ in range(3):
+        s.record()
+        torch.matmul(a, b)
+        e.record()
+        e.synchronize()
+        best = min(best, s.elapsed_time(e))
+    del a, b
+    return 2 * 8192 ** 3 / (best * 1e-3) / 1e12
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2312_00538_b200 import AnovaKernelSpec, Dataset, FeatureWindowing, _lib, anova_fast_operator
+    from paper_2312_00538_b200 import sharding, workloads
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    w = workloads.make(args.config, args.n)
+    spec = AnovaKernelSpec(FeatureWindowing.explicit(w.windows))
+    owner = sharding.lpt_assign(sharding.window_costs(w.windows), world)
+    mask = sharding.window_mask(owner, rank) if world > 1 else None
+    os.environ.setdefault("KSVM_NFFT_QUIET", "1")
+    op = anova_fast_operator(Dataset(w.points), spec, fit_fraction=w.fit_fraction, device=local,
+                             window_mask=mask)
+    v = torch.from_numpy(w.v).to(dev)
+    y = torch.empty_like(v)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        op.apply_into(v, y)
+        if world > 1:
+            dist.all_reduce(y)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize(dev)
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    launches0 = _lib.launch_count()
+    with ClockSampler(local) as clk:
+        for k in range(K):
+            flush.zero_()
+            ev[k][0].record()
+            step()
+            ev[k][1].record()
+        torch.cuda.synchronize(dev)
+    launches = _lib.launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    value = K / (total_ms * 1e-3)
+
+    # --- per-launch timing pass (same flush discipline) for the roofline ----
+    op.set_stage_timing(True)
+    acc = {}
+    for k in range(K):
+        flush.zero_()
+        step()
+        for name, ms in op.last_stage_ms().items():
+            acc[name] = acc.get(name, 0.0) + ms
+    op.set_stage_timing(False)
+    per_launch = {k2: v2 / K for k2, v2 in acc.items()}
+
+    # --- end-to-end through the public API with host buffers ---------------
+    vh = torch.from_numpy(w.v).pin_memory()
+    yh = torch.empty(w.n, dtype=torch.float64).pin_memory()
+    vhn = vh.numpy()
+    for _ in range(3):
+        if world > 1:
+            v.copy_(vh, non_blocking=True)
+            step()
+            yh.copy_(y, non_blocking=True)
+            torch.cuda.synchronize(dev)
+        else:
+            op.apply(vhn, out=yh)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(K):
+        if world > 1:
+            v.copy_(vh, non_blocking=True)
+            step()
+            yh.copy_(y, non_blocking=True)
+            torch.cuda.synchronize(dev)
+        else:
+            op.apply(vhn, out=yh)  # C-ABI host path: H2D v, apply, D2H y, sync
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = K / float(te.item())
+
+    if rank == 0:
+        hbm_peak, peak_kind = peaks()
+        dom = max((k2 for k2 in per_launch if kernel_bytes(w, k2) > 0), key=lambda k2: per_launch[k2],
+                  default=None)
+        roof = None
+        if dom is not None:
+            ms = per_launch[dom]
+            ach = kernel_bytes(w, dom) / (ms * 1e-3) / 1e9
+            traffic = None
+            try:
+                with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+                    traffic = json.load(f).get(f"cfg{args.config}", {}).get(dom)
+            except Exception:
+                pass
+            fpk = fp64_peak_tflops(dev)
+            fma_rate = kernel_fmas(w, dom) / (ms * 1e-3)
+            roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": ach / hbm_peak, "peak_source": peak_kind, "traffic": traffic,
+                    "kernel_ms": ms,
+                    "fp64": {"achieved_tflops": 2 * fma_rate / 1e12, "peak_tflops": fpk,
+                             "peak_source": "measured cuBLAS DGEMM 8192^3 (torch.matmul f64)",
+                             "frac": 2 * fma_rate / 1e12 / fpk}}
+        step_ms = total_ms / K
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+                "warmup": max(3, args.warmup), "ms_per_step": step_ms, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": w.name, "n": w.n, "d": w.d, "windows": w.windows,
+                           "fit_fraction": w.fit_fraction, "N": 32, "m": 4, "sigma": 2,
+                           "l2": "256 MiB flush before every timed step",
+                           "parallelism": f"window-sharded x{world} + NCCL allreduce" if world > 1 else "1 GPU",
+                           "seed": 1000 + args.config},
+                "hbm_fraction_matvec": (w.hbm_bytes() / (step_ms * 1e-3) / 1e9) / peaks()[0],
+                "per_launch_ms": per_launch,
+                "roofline": roof,
+                "clocks": clk.summary(),
+                "gpu_launches": launches,
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * w.n,
+                        "d2h_bytes_per_step": 8 * w.n}}
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(w, args.cpu_budget_s)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

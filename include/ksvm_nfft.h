@@ -135,9 +135,14 @@ int ksvm_nfft_kernel_rows(const ksvm_nfft_op* op, int window, const int64_t* row
                           double* out, int ptr_kind, void* stream);
 int ksvm_nfft_kernel_diag(const ksvm_nfft_op* op, int window, double* out, int ptr_kind,
                           void* stream);
-/* Per-apply stage timing of the last apply (device ms from CUDA events):
- * [spread, reduce, grid, gather, combine]. Returns the number filled. */
+/* Per-launch device timing (CUDA events on the op's stream, off by default;
+ * env KSVM_NFFT_STAGE_TIMING=1 also enables it). last_stage_ms fills the
+ * device ms of each kernel launch of the last apply (synchronising on it)
+ * and returns how many; stage_name(i) names launch i ("spread_d3",
+ * "reduce", "conv_0", "gather_d3", "combine", ...). */
+int ksvm_nfft_op_set_stage_timing(ksvm_nfft_op* op, int on);
 int ksvm_nfft_op_last_stage_ms(const ksvm_nfft_op* op, float* ms, int cap);
+const char* ksvm_nfft_op_stage_name(const ksvm_nfft_op* op, int i);
 void ksvm_nfft_op_free(ksvm_nfft_op* op);
 
 #ifdef __cplusplus

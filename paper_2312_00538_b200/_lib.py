@@ -55,7 +55,9 @@ _SIGS = {
     "ksvm_nfft_op_entry": (C.c_double, [_vp, C.c_int64, C.c_int64]),
     "ksvm_nfft_kernel_rows": (C.c_int, [_vp, C.c_int, _lp, C.c_int, _vp, C.c_int, _vp]),
     "ksvm_nfft_kernel_diag": (C.c_int, [_vp, C.c_int, _vp, C.c_int, _vp]),
+    "ksvm_nfft_op_set_stage_timing": (C.c_int, [_vp, C.c_int]),
     "ksvm_nfft_op_last_stage_ms": (C.c_int, [_vp, C.POINTER(C.c_float), C.c_int]),
+    "ksvm_nfft_op_stage_name": (C.c_char_p, [_vp, C.c_int]),
     "ksvm_nfft_op_free": (None, [_vp]),
 }
 

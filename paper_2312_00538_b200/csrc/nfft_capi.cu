@@ -357,7 +357,10 @@ struct Engine {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
-    cudaEvent_t ev_stage[6] = {};
+    static constexpr int kMaxTicks = 24;
+    cudaEvent_t ev_stage[kMaxTicks] = {};
+    const char* tick_name[kMaxTicks] = {};
+    int nticks = 0, last_nticks = 0;
     bool stage_timing = false;
     ksvm_nfft_config cfg{};
     double fit = 1.0;
@@ -381,7 +384,8 @@ struct Engine {
     int class_PE[4] = {0, 0, 0, 0};
     long long max_nodes = 0;
     std::mutex mu;
-    float last_ms[5] = {0, 0, 0, 0, 0};
+    float last_ms[kMaxTicks] = {};
+    const char* last_name[kMaxTicks] = {};
 
     ~Engine() {
         if (stream) {
@@ -390,8 +394,8 @@ struct Engine {
             cudaStreamDestroy(stream);
             cudaEventDestroy(ev_in);
             cudaEventDestroy(ev_out);
-            for (auto& e : ev_stage)
-                if (e) cudaEventDestroy(e);
+            for (auto& ev : ev_stage)
+                if (ev) cudaEventDestroy(ev);
         }
     }
 
@@ -405,8 +409,7 @@ struct Engine {
         CK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
         stage_timing = std::getenv("KSVM_NFFT_STAGE_TIMING") != nullptr;
-        if (stage_timing)
-            for (auto& e : ev_stage) CK(cudaEventCreate(&e));
+        for (auto& e : ev_stage) CK(cudaEventCreate(&e));
     }
 
     // plan_fastsum for one window (P:src/fastsum.cpp:103-209) on the device.
@@ -532,34 +535,39 @@ struct Engine {
         CK(cudaStreamSynchronize(stream));
     }
 
-    void mark(int k) {
-        if (stage_timing) CK(cudaEventRecord(ev_stage[k], stream));
+    // Per-launch device timing: an event before each launch and one at the end.
+    void tick(const char* name) {
+        if (!stage_timing || nticks >= kMaxTicks) return;
+        tick_name[nticks] = name;
+        CK(cudaEventRecord(ev_stage[nticks], stream));
+        ++nticks;
     }
 
     // spread -> reduce -> conv -> (gather over `targets` or sources)
     void run_grid(const double* v) {
         const int P = P_owned();
-        mark(0);
+        static const char* kSpread[4] = {"", "spread_d1", "spread_d2", "spread_d3"};
         for (int D = 1; D <= 3; ++D) {
             const int cnt = class_end[D] - class_begin[D];
             if (cnt == 0) continue;
+            tick(kSpread[D]);
             launch_spread(D, 2 * cfg.window_cutoff, class_PE[D], d_items.p + class_begin[D], cnt,
                           d_ps.p, d_wins.p, v, patches.p, stream);
             ++g_launches;
         }
         CK(cudaGetLastError());
-        mark(1);
+        tick("reduce");
         launch_reduce(d_wins.p, d_slots.p, P, max_nodes, patches.p, stream);
         ++g_launches;
-        mark(2);
         int maxd = 0;
         for (int s = 0; s < P; ++s) maxd = std::max(maxd, wins[static_cast<size_t>(owned[static_cast<size_t>(s)])]->d);
+        static const char* kConv[3] = {"conv_0", "conv_1", "conv_2"};
         for (int stg = 0; stg < maxd; ++stg) {
+            tick(kConv[stg]);
             launch_conv(d_wins.p, d_slots.p, P, max_nodes, stg, stream);
             ++g_launches;
         }
         CK(cudaGetLastError());
-        mark(3);
     }
 
     void run_apply(const double* v, double* y) {
@@ -569,25 +577,33 @@ struct Engine {
             ++g_launches;
             return;
         }
+        nticks = 0;
         run_grid(v);
+        static const char* kGather[4] = {"", "gather_d1", "gather_d2", "gather_d3"};
         for (int D = 1; D <= 3; ++D) {
             const int cnt = class_end[D] - class_begin[D];
             if (cnt == 0) continue;
+            tick(kGather[D]);
             launch_gather(D, 2 * cfg.window_cutoff, class_PE[D], d_items.p + class_begin[D], cnt,
                           d_ps.p, d_wins.p, stream);
             ++g_launches;
         }
-        mark(4);
+        tick("combine");
         launch_combine(y, parts.p, d_eta.p, P, n, stream);
         ++g_launches;
         CK(cudaGetLastError());
-        mark(5);
+        tick("end");
+        last_nticks = nticks;
     }
 
-    void collect_stage_times() {
-        if (!stage_timing) return;
-        CK(cudaEventSynchronize(ev_stage[5]));
-        for (int k = 0; k < 5; ++k) CK(cudaEventElapsedTime(&last_ms[k], ev_stage[k], ev_stage[k + 1]));
+    int collect_stage_times() {
+        if (!stage_timing || last_nticks < 2) return 0;
+        CK(cudaEventSynchronize(ev_stage[last_nticks - 1]));
+        for (int k = 0; k + 1 < last_nticks; ++k) {
+            CK(cudaEventElapsedTime(&last_ms[k], ev_stage[k], ev_stage[k + 1]));
+            last_name[k] = tick_name[k];
+        }
+        return last_nticks - 1;
     }
 
     // Host/device dispatch shared by every apply-like entry point.
@@ -601,7 +617,6 @@ struct Engine {
             body(vbuf.p, ybuf.p);
             if (yout > 0) CK(cudaMemcpyAsync(y, ybuf.p, sizeof(double) * yout, cudaMemcpyDeviceToHost, stream));
             CK(cudaStreamSynchronize(stream));
-            collect_stage_times();
         } else if (ptr_kind == KSVM_NFFT_DEVICE) {
             cudaStream_t es = static_cast<cudaStream_t>(ext_stream);
             CK(cudaEventRecord(ev_in, es));
@@ -876,11 +891,33 @@ int ksvm_nfft_kernel_diag(const ksvm_nfft_op* op, int window, double* out, int p
     });
 }
 
+int ksvm_nfft_op_set_stage_timing(ksvm_nfft_op* op, int on) {
+    if (!op) return KSVM_NFFT_ERR_CONFIG;
+    std::lock_guard<std::mutex> lk(op->e.mu);
+    op->e.stage_timing = on != 0;
+    return KSVM_NFFT_OK;
+}
+
 int ksvm_nfft_op_last_stage_ms(const ksvm_nfft_op* op, float* ms, int cap) {
     if (!op || !ms || !op->e.stage_timing) return 0;
-    const int k = std::min(cap, 5);
-    for (int i = 0; i < k; ++i) ms[i] = op->e.last_ms[i];
+    Engine& E = const_cast<Engine&>(op->e);
+    int k = 0;
+    try {
+        DeviceGuard dg(E.device);
+        std::lock_guard<std::mutex> lk(E.mu);
+        k = E.collect_stage_times();
+    } catch (const std::exception& e) {
+        t_err = e.what();
+        return 0;
+    }
+    k = std::min(cap, k);
+    for (int i = 0; i < k; ++i) ms[i] = E.last_ms[i];
     return k;
+}
+
+const char* ksvm_nfft_op_stage_name(const ksvm_nfft_op* op, int i) {
+    if (!op || i < 0 || i >= Engine::kMaxTicks || !op->e.last_name[i]) return "";
+    return op->e.last_name[i];
 }
 
 void ksvm_nfft_op_free(ksvm_nfft_op* op) { delete op; }

@@ -308,9 +308,13 @@ class AnovaFastOperator(KernelOperator):
     def size(self) -> int:
         return self._n
 
-    def apply(self, v):
+    def apply(self, v, out=None):
         a = _Vec(v, self._n, self.device)
-        out, optr = a.out(self._n)
+        if out is None:
+            out, optr = a.out(self._n)
+        else:
+            optr = C.c_void_p(out.data_ptr() if (torch is not None and isinstance(out, torch.Tensor))
+                             else out.ctypes.data)
         _raise(_lib.load().ksvm_nfft_op_apply(self._h, a.ptr, optr, a.kind, a.stream))
         return out
 
@@ -361,10 +365,20 @@ class AnovaFastOperator(KernelOperator):
                                                  C.c_void_p(0)))
         return out
 
-    def last_stage_ms(self):
-        buf = (C.c_float * 5)()
-        k = _lib.load().ksvm_nfft_op_last_stage_ms(self._h, buf, 5)
-        return list(buf)[:k]
+    def set_stage_timing(self, on: bool = True) -> None:
+        """Record CUDA events between the five stages of every apply."""
+        _raise(_lib.load().ksvm_nfft_op_set_stage_timing(self._h, 1 if on else 0))
+
+    def last_stage_ms(self) -> dict:
+        """{launch name: device ms} for each kernel launch of the last apply."""
+        buf = (C.c_float * 24)()
+        L = _lib.load()
+        k = L.ksvm_nfft_op_last_stage_ms(self._h, buf, 24)
+        out = {}
+        for i in range(k):
+            name = L.ksvm_nfft_op_stage_name(self._h, i).decode()
+            out[name] = out.get(name, 0.0) + float(buf[i])
+        return out
 
 
 def anova_fast_operator(data, spec: AnovaKernelSpec, cfg: Optional[FastsumConfig] = None,
