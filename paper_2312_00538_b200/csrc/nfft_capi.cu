@@ -219,10 +219,10 @@ Geometry geometry(const ksvm_nfft_config& c, int d) {
     g.S = 2 * g.m;
     // Every admissible point (sources: |x| <= fit r_T; cross targets:
     // ||x|| <= r_T (1 + 1e-12), P:src/fastsum.cpp:316) has floor(x M) in
-    // [cmin, cmax]; one cell of guard on each side.
+    // [cmin, cmax] (the plan-time cell-key kernel verifies it).
     const double rx = c.torus_radius * (1.0 + 1e-12) * g.M;
-    g.cmin = static_cast<int>(std::floor(-rx)) - 1;
-    const int cmax = static_cast<int>(std::floor(rx)) + 1;
+    g.cmin = static_cast<int>(std::floor(-rx));
+    const int cmax = static_cast<int>(std::floor(rx));
     g.ncell = cmax - g.cmin + 1;
     g.TC = d == 3 ? 4 : (d == 2 ? 8 : 32);
     g.ntile = (g.ncell + g.TC - 1) / g.TC;
@@ -469,6 +469,7 @@ struct Engine {
         dw.Lext = g.Lext;
         dw.Mf = static_cast<double>(g.M);
         dw.bwin = bwin;
+        dw.invb = 1.0 / bwin;
         dw.Cw = 1.0 / std::sqrt(3.14159265358979323846 * bwin);
         for (int o = 0; o < kMaxSpan; ++o) dw.R[o] = o < g.S ? std::exp(-static_cast<double>(o) * o / bwin) : 0.0;
         dw.G = w.G.p;

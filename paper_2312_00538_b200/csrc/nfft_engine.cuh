@@ -42,6 +42,7 @@ struct DWin {
     int Lext;    // extended node count ncell + S - 1
     double Mf;   // M as double
     double bwin; // Gaussian window shape b (P:src/fastsum.cpp:124)
+    double invb; // 1 / b
     double Cw;   // 1/sqrt(pi b)        (P:src/fastsum.cpp:77)
     double R[kMaxSpan];  // exp(-o^2/b), o = 0..S-1 (window factorisation)
     double* G;   // spread grid, Lg^d

@@ -40,8 +40,8 @@ __device__ __forceinline__ int window_weights(double x, const DWin& w, double* o
     const double xm = x * w.Mf;
     const double fl = floor(xm);
     const double u = (xm - fl) + static_cast<double>(w.m - 1);
-    double q = w.Cw * exp(-u * u / w.bwin);
-    const double Q = exp(2.0 * u / w.bwin);
+    double q = w.Cw * exp(-(u * u) * w.invb);
+    const double Q = exp((2.0 * u) * w.invb);
 #pragma unroll
     for (int o = 0; o < S; ++o) {
         out[o] = q * w.R[o];
@@ -54,8 +54,8 @@ __device__ __forceinline__ int window_weights_rt(double x, const DWin& w, double
     const double xm = x * w.Mf;
     const double fl = floor(xm);
     const double u = (xm - fl) + static_cast<double>(w.m - 1);
-    double q = w.Cw * exp(-u * u / w.bwin);
-    const double Q = exp(2.0 * u / w.bwin);
+    double q = w.Cw * exp(-(u * u) * w.invb);
+    const double Q = exp((2.0 * u) * w.invb);
     for (int o = 0; o < w.S; ++o) {
         out[o] = q * w.R[o];
         q *= Q;
@@ -79,7 +79,17 @@ __device__ __forceinline__ void warp_range(const Item& it, int warp, int W, int*
     *e = min(*b + per, it.end);
 }
 
-constexpr int kStage3 = 25;  // per-point staging: w0[8], w1[8], w2[8], cell
+// Per-point staging row (doubles): w0[8] w1[8] w2[8] | cell code (int) | pad.
+// 26 doubles = 208 B keeps every double2 slot 16-byte aligned.
+constexpr int kSt = 26;
+
+__device__ __forceinline__ int cell_of(const double* st) {
+    return *reinterpret_cast<const int*>(st + 24);
+}
+
+__device__ __forceinline__ double2 ld2(const double* p) {
+    return *reinterpret_cast<const double2*>(p);
+}
 
 }  // namespace
 
@@ -88,8 +98,10 @@ constexpr int kStage3 = 25;  // per-point staging: w0[8], w1[8], w2[8], cell
 // Lane L owns the 16 taps (a, b0..b0+1, 0..7) of the cell's 8^3 block with
 // a = L/4, b0 = 2 (L%4); consecutive points of one cell accumulate in
 // registers and are flushed into the warp's private SMEM patch when the
-// cell changes. The W private patches are summed in warp order and written
-// to the item's global patch.
+// cell changes. Points are sorted by cell, so a run of 4 with equal first
+// and last cell is one cell: that fast path has no branches and 16
+// independent FMA chains. The W private patches are summed in warp order
+// and written to the item's global patch.
 // ---------------------------------------------------------------------------
 template <int W>
 __global__ void __launch_bounds__(W * 32)
@@ -97,10 +109,10 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
                   const DWin* __restrict__ wins, const double* __restrict__ v,
                   double* __restrict__ patches) {
     constexpr int S = 8, TC = 4, PE = TC + S - 1, PV = PE * PE * PE;
-    extern __shared__ double smem[];
+    extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double* wp = smem + warp * PV;
-    double* stage = smem + W * PV + warp * 32 * kStage3;
+    double* stage = smem + W * PV + warp * 32 * kSt;
 
     const Item it = items[blockIdx.x];
     const DPSet& ps = psets[it.ps];
@@ -130,13 +142,26 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
             acc1[c] = 0.0;
         }
     };
+    auto accumulate = [&](const double* st) {
+        const double w0a = st[a];
+        const double2 w1 = ld2(st + 8 + b0);
+        const double u0 = w0a * w1.x, u1 = w0a * w1.y;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const double2 w2 = ld2(st + 16 + 2 * k);
+            acc0[2 * k] = fma(u0, w2.x, acc0[2 * k]);
+            acc0[2 * k + 1] = fma(u0, w2.y, acc0[2 * k + 1]);
+            acc1[2 * k] = fma(u1, w2.x, acc1[2 * k]);
+            acc1[2 * k + 1] = fma(u1, w2.y, acc1[2 * k + 1]);
+        }
+    };
 
     for (int base = wb; base < we; base += 32) {
         const int cnt = min(32, we - base);
         if (lane < cnt) {
             const int i = base + lane;
             double w[S];
-            double* st = stage + lane * kStage3;
+            double* st = stage + lane * kSt;
             const double vi = v[ps.perm[i]];
             const int c0 = window_weights<S>(ps.x[0][i], wn, w) - off0;
 #pragma unroll
@@ -147,23 +172,26 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
             const int c2 = window_weights<S>(ps.x[2][i], wn, w) - off2;
 #pragma unroll
             for (int o = 0; o < S; ++o) st[16 + o] = w[o];
-            st[24] = static_cast<double>((c0 * TC + c1) * TC + c2);
+            *reinterpret_cast<int*>(st + 24) = (c0 * TC + c1) * TC + c2;
         }
         __syncwarp();
-        for (int p = 0; p < cnt; ++p) {
-            const double* st = stage + p * kStage3;
-            const int cell = static_cast<int>(st[24]);
-            if (cell != cur) {
+        int p = 0;
+        while (p < cnt) {
+            const double* st = stage + p * kSt;
+            const int cp = cell_of(st);
+            if (cp != cur) {
                 if (cur >= 0) flush(cur);
-                cur = cell;
+                cur = cp;
             }
-            const double w0a = st[a];
-            const double u0 = w0a * st[8 + b0], u1 = w0a * st[9 + b0];
-#pragma unroll
-            for (int c = 0; c < S; ++c) {
-                const double w2 = st[16 + c];
-                acc0[c] = fma(u0, w2, acc0[c]);
-                acc1[c] = fma(u1, w2, acc1[c]);
+            if (p + 3 < cnt && cell_of(st + 3 * kSt) == cp) {
+                accumulate(st);
+                accumulate(st + kSt);
+                accumulate(st + 2 * kSt);
+                accumulate(st + 3 * kSt);
+                p += 4;
+            } else {
+                accumulate(st);
+                p += 1;
             }
         }
         __syncwarp();
@@ -182,18 +210,20 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
 // ---------------------------------------------------------------------------
 // Gather, d = 3, m = 4: the tile's 11^3 grid halo sits in SMEM; lane L holds
 // the 16 grid values of its taps for the current cell in registers and
-// computes a partial for each of 32 consecutive points; a transposed
-// butterfly (reduce-scatter) leaves point p's sum in lane p.
+// computes a partial for each of 32 consecutive points (4-point same-cell
+// fast path, 4 independent chains per point); a transposed butterfly
+// (reduce-scatter) leaves point p's sum in lane p.
 // ---------------------------------------------------------------------------
 template <int W>
 __global__ void __launch_bounds__(W * 32)
 gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
                   const DWin* __restrict__ wins) {
     constexpr int S = 8, TC = 4, PE = TC + S - 1, PV = PE * PE * PE;
-    extern __shared__ double smem[];
+    extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double* halo = smem;
-    double* stage = smem + PV + warp * 32 * kStage3;
+    // PV = 1331 doubles is not a multiple of 2: start the staging area at 1332
+    double* stage = smem + (PV + 1) + warp * 32 * kSt;
 
     const Item it = items[blockIdx.x];
     const DPSet& ps = psets[it.ps];
@@ -219,14 +249,39 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     warp_range(it, warp, W, &wb, &we);
     const int a = lane >> 2, b0 = (lane & 3) << 1;
     double h0[S], h1[S];
+#pragma unroll
+    for (int c = 0; c < S; ++c) h0[c] = h1[c] = 0.0;
     int cur = -1;
+
+    auto reload = [&](int cell) {
+        const int l0 = cell / (TC * TC), l1 = (cell / TC) % TC, l2 = cell % TC;
+        const double* src = halo + ((l0 + a) * PE + l1 + b0) * PE + l2;
+#pragma unroll
+        for (int c = 0; c < S; ++c) {
+            h0[c] = src[c];
+            h1[c] = src[PE + c];
+        }
+    };
+    auto partial = [&](const double* st) {
+        double e0 = 0.0, o0 = 0.0, e1 = 0.0, o1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const double2 w2 = ld2(st + 16 + 2 * k);
+            e0 = fma(h0[2 * k], w2.x, e0);
+            o0 = fma(h0[2 * k + 1], w2.y, o0);
+            e1 = fma(h1[2 * k], w2.x, e1);
+            o1 = fma(h1[2 * k + 1], w2.y, o1);
+        }
+        const double2 w1 = ld2(st + 8 + b0);
+        return st[a] * fma(w1.x, e0 + o0, w1.y * (e1 + o1));
+    };
 
     for (int base = wb; base < we; base += 32) {
         const int cnt = min(32, we - base);
         if (lane < cnt) {
             const int i = base + lane;
             double w[S];
-            double* st = stage + lane * kStage3;
+            double* st = stage + lane * kSt;
             const int c0 = window_weights<S>(ps.x[0][i], wn, w) - off0;
 #pragma unroll
             for (int o = 0; o < S; ++o) st[o] = w[o];
@@ -236,35 +291,37 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
             const int c2 = window_weights<S>(ps.x[2][i], wn, w) - off2;
 #pragma unroll
             for (int o = 0; o < S; ++o) st[16 + o] = w[o];
-            st[24] = static_cast<double>((c0 * TC + c1) * TC + c2);
+            *reinterpret_cast<int*>(st + 24) = (c0 * TC + c1) * TC + c2;
         }
         __syncwarp();
         double pp[32];
 #pragma unroll
-        for (int p = 0; p < 32; ++p) {
-            if (p < cnt) {
-                const double* st = stage + p * kStage3;
-                const int cell = static_cast<int>(st[24]);
-                if (cell != cur) {
-                    cur = cell;
-                    const int l0 = cell / (TC * TC), l1 = (cell / TC) % TC, l2 = cell % TC;
-                    const double* src = halo + ((l0 + a) * PE + l1 + b0) * PE + l2;
+        for (int g = 0; g < 8; ++g) {
+            const int p0 = 4 * g;
+            const double* st = stage + p0 * kSt;
+            if (p0 + 3 < cnt && cell_of(st) == cell_of(st + 3 * kSt)) {
+                const int cp = cell_of(st);
+                if (cp != cur) {
+                    cur = cp;
+                    reload(cp);
+                }
+                pp[p0] = partial(st);
+                pp[p0 + 1] = partial(st + kSt);
+                pp[p0 + 2] = partial(st + 2 * kSt);
+                pp[p0 + 3] = partial(st + 3 * kSt);
+            } else {
 #pragma unroll
-                    for (int c = 0; c < S; ++c) {
-                        h0[c] = src[c];
-                        h1[c] = src[PE + c];
+                for (int q = 0; q < 4; ++q) {
+                    pp[p0 + q] = 0.0;
+                    if (p0 + q < cnt) {
+                        const int cp = cell_of(st + q * kSt);
+                        if (cp != cur) {
+                            cur = cp;
+                            reload(cp);
+                        }
+                        pp[p0 + q] = partial(st + q * kSt);
                     }
                 }
-                double t0 = 0.0, t1 = 0.0;
-#pragma unroll
-                for (int c = 0; c < S; ++c) {
-                    const double w2 = st[16 + c];
-                    t0 = fma(h0[c], w2, t0);
-                    t1 = fma(h1[c], w2, t1);
-                }
-                pp[p] = st[a] * fma(st[8 + b0], t0, st[9 + b0] * t1);
-            } else {
-                pp[p] = 0.0;
             }
         }
         // transposed butterfly: after the 5 stages lane p holds point p's sum
@@ -660,8 +717,8 @@ __global__ void permute_kernel(double* __restrict__ dst, const double* __restric
 
 constexpr int kW3 = 4;  // warps per CTA of the d=3, m=4 kernels
 
-size_t spread3_smem() { return sizeof(double) * (kW3 * 1331 + kW3 * 32 * kStage3); }
-size_t gather3_smem() { return sizeof(double) * (1331 + kW3 * 32 * kStage3); }
+size_t spread3_smem() { return sizeof(double) * (kW3 * 1331 + kW3 * 32 * kSt); }
+size_t gather3_smem() { return sizeof(double) * (1332 + kW3 * 32 * kSt); }
 
 int generic_warps(int D, int PE, bool spread) {
     int PV = 1;
