@@ -31,10 +31,11 @@ void launch_spread(int D, int S, int PE, const Item* items, int nitems, const DP
                    const DWin* wins, const double* v, double* patches, cudaStream_t st);
 void launch_gather(int D, int S, int PE, const Item* items, int nitems, const DPSet* ps,
                    const DWin* wins, cudaStream_t st);
-void launch_reduce(const DWin* wins, const int* slots, int nslots, long long max_nodes,
+void launch_reduce(const DWin* wins, const int* slots, int nslots, long long max_nodes, int D,
                    const double* patches, cudaStream_t st);
-void launch_conv(const DWin* wins, const int* slots, int nslots, long long max_nodes, int stage,
-                 cudaStream_t st);
+void launch_conv(const DWin* wins, const int* slots, int nslots, int Lg_max, long long max_fibres,
+                 int stage, cudaStream_t st);
+int conv_max_lg();
 void launch_combine(double* y, const double* parts, const double* eta, int P, long long n,
                     cudaStream_t st);
 void launch_kernel_rows(double* out, const long long* rows, int r, const double* const* cols,
@@ -44,7 +45,9 @@ void launch_fill(double* out, double val, long long n, cudaStream_t st);
 void launch_cell_keys(const double* x0, const double* x1, const double* x2, int d, long long n,
                       double Mf, int cmin, int ncell, int TC, int ntile, unsigned* keys, int* idx,
                       int* bad, cudaStream_t st);
-void launch_permute(double* dst, const double* src, const int* perm, long long n, cudaStream_t st);
+void launch_factors(const double* x0, const double* x1, const double* x2, const int* perm, int d,
+                    long long n, double Mf, int m, double invb, double Cw, int cmin, int TC,
+                    double* P, double* Q0, double* Q1, double* Q2, int* code, cudaStream_t st);
 
 namespace {
 
@@ -188,7 +191,8 @@ Spectral1D spectral_1d(int N, int M, double bwin, double ell_s) {
 struct PointSet {
     int64_t n = 0;
     int d = 0;
-    DevBuf<double> x[3];
+    DevBuf<double> P, Q[3];  // window factors, sorted order (nfft_engine.cuh)
+    DevBuf<int> code;        // tile-local cell code
     DevBuf<int> perm;
     std::vector<Item> items;      // host copy (global numbering assigned later)
     std::vector<int> tile_first;  // local item index of each tile's first item
@@ -210,6 +214,7 @@ struct Window {
 
 struct Geometry {
     int M, S, m, cmin, ncell, TC, ntile, PE, Lext, Lg, lo, wrap;
+    double bwin, invb, Cw;
 };
 
 Geometry geometry(const ksvm_nfft_config& c, int d) {
@@ -231,6 +236,13 @@ Geometry geometry(const ksvm_nfft_config& c, int d) {
     g.lo = g.cmin - g.m + 1;
     g.wrap = g.Lext > g.M ? 1 : 0;
     g.Lg = g.wrap ? g.M : g.Lext;
+    if (g.Lg > conv_max_lg())
+        throw std::invalid_argument("oversampled grid edge too large for this build (local grid edge > " +
+                                    std::to_string(conv_max_lg()) + ")");
+    const double sg = static_cast<double>(c.oversampling);
+    g.bwin = (2.0 * sg * g.m) / ((2.0 * sg - 1.0) * 3.14159265358979323846);  // P:src/fastsum.cpp:123-124
+    g.invb = 1.0 / g.bwin;
+    g.Cw = 1.0 / std::sqrt(3.14159265358979323846 * g.bwin);
     return g;
 }
 
@@ -264,10 +276,13 @@ void build_pointset(PointSet& ps, const std::vector<double>& scaled_cm, int64_t 
     tmp.alloc(tmp_bytes);
     CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, keys_in.p, keys_out.p, idx_in.p,
                                        ps.perm.p, static_cast<int>(n), 0, bits, st));
-    for (int t = 0; t < d; ++t) {
-        ps.x[t].alloc(n);
-        launch_permute(ps.x[t].p, raw[t].p, ps.perm.p, n, st);
-    }
+    ps.P.alloc(n);
+    for (int t = 0; t < d; ++t) ps.Q[t].alloc(n);
+    ps.code.alloc(n);
+    launch_factors(raw[0].p, d > 1 ? raw[1].p : nullptr, d > 2 ? raw[2].p : nullptr, ps.perm.p, d, n,
+                   static_cast<double>(g.M), g.m, g.invb, g.Cw, g.cmin, g.TC, ps.P.p, ps.Q[0].p,
+                   d > 1 ? ps.Q[1].p : nullptr, d > 2 ? ps.Q[2].p : nullptr, ps.code.p, st);
+    CK(cudaGetLastError());
     std::vector<unsigned> hk(static_cast<size_t>(n));
     int hbad = 0;
     CK(cudaMemcpyAsync(hk.data(), keys_out.p, sizeof(unsigned) * n, cudaMemcpyDeviceToHost, st));
@@ -382,7 +397,9 @@ struct Engine {
     DevBuf<int> d_wdim;
     int class_begin[4] = {0, 0, 0, 0}, class_end[4] = {0, 0, 0, 0};
     int class_PE[4] = {0, 0, 0, 0};
-    long long max_nodes = 0;
+    long long max_nodes = 0, max_fibres = 0;
+    int max_lg = 0;
+    bool has_dim[4] = {false, false, false, false};
     std::mutex mu;
     float last_ms[kMaxTicks] = {};
     const char* last_name[kMaxTicks] = {};
@@ -421,8 +438,7 @@ struct Engine {
             for (int64_t i = 0; i < n; ++i)
                 sc[static_cast<size_t>(t * n + i)] = (cm[static_cast<size_t>(t * n + i)] - w.center[t]) * w.scale;
         const Geometry g = geometry(cfg, d);
-        const double sg = static_cast<double>(cfg.oversampling);
-        const double bwin = (2.0 * sg * g.m) / ((2.0 * sg - 1.0) * 3.14159265358979323846);
+        const double bwin = g.bwin;
         // spectral data and the separable convolution tables
         const Spectral1D sp = spectral_1d(cfg.bandwidth, g.M, bwin, w.ell_s);
         long double csum1 = 0.0L;
@@ -448,6 +464,9 @@ struct Engine {
         long long nodes = 1;
         for (int t = 0; t < d; ++t) nodes *= Lg;
         max_nodes = std::max(max_nodes, nodes);
+        max_fibres = std::max(max_fibres, nodes / Lg);
+        max_lg = std::max(max_lg, Lg);
+        has_dim[d] = true;
         w.G.alloc(nodes);
         w.H.alloc(nodes);
         for (int k = 0; k < (d == 1 ? 0 : (d == 2 ? 2 : 4)); ++k) w.T[k].alloc(nodes);
@@ -469,8 +488,8 @@ struct Engine {
         dw.Lext = g.Lext;
         dw.Mf = static_cast<double>(g.M);
         dw.bwin = bwin;
-        dw.invb = 1.0 / bwin;
-        dw.Cw = 1.0 / std::sqrt(3.14159265358979323846 * bwin);
+        dw.invb = g.invb;
+        dw.Cw = g.Cw;
         for (int o = 0; o < kMaxSpan; ++o) dw.R[o] = o < g.S ? std::exp(-static_cast<double>(o) * o / bwin) : 0.0;
         dw.G = w.G.p;
         dw.H = w.H.p;
@@ -519,7 +538,9 @@ struct Engine {
             eta[static_cast<size_t>(s)] = w.eta;
             slots[static_cast<size_t>(s)] = s;
             DPSet& p = ps[static_cast<size_t>(s)];
-            for (int t = 0; t < 3; ++t) p.x[t] = t < w.d ? w.src.x[t].p : nullptr;
+            p.P = w.src.P.p;
+            for (int t = 0; t < 3; ++t) p.Q[t] = t < w.d ? w.src.Q[t].p : nullptr;
+            p.code = w.src.code.p;
             p.perm = w.src.perm.p;
             p.n = n;
             p.win = s;
@@ -558,14 +579,17 @@ struct Engine {
         }
         CK(cudaGetLastError());
         tick("reduce");
-        launch_reduce(d_wins.p, d_slots.p, P, max_nodes, patches.p, stream);
-        ++g_launches;
+        for (int D = 1; D <= 3; ++D) {
+            if (!has_dim[D]) continue;
+            launch_reduce(d_wins.p, d_slots.p, P, max_nodes, D, patches.p, stream);
+            ++g_launches;
+        }
         int maxd = 0;
         for (int s = 0; s < P; ++s) maxd = std::max(maxd, wins[static_cast<size_t>(owned[static_cast<size_t>(s)])]->d);
         static const char* kConv[3] = {"conv_0", "conv_1", "conv_2"};
         for (int stg = 0; stg < maxd; ++stg) {
             tick(kConv[stg]);
-            launch_conv(d_wins.p, d_slots.p, P, max_nodes, stg, stream);
+            launch_conv(d_wins.p, d_slots.p, P, max_lg, max_fibres, stg, stream);
             ++g_launches;
         }
         CK(cudaGetLastError());
@@ -983,7 +1007,9 @@ int ksvm_nfft_plan_apply_cross(const ksvm_nfft_plan* plan, const double* targets
         DevBuf<double> tout;
         tout.alloc(t);
         DPSet dp{};
-        for (int c = 0; c < 3; ++c) dp.x[c] = c < w.d ? tp.x[c].p : nullptr;
+        dp.P = tp.P.p;
+        for (int c = 0; c < 3; ++c) dp.Q[c] = c < w.d ? tp.Q[c].p : nullptr;
+        dp.code = tp.code.p;
         dp.perm = tp.perm.p;
         dp.n = t;
         dp.win = 0;

@@ -8,6 +8,14 @@
 // processes; an *item* is a tile's point range (heavy tiles are split into
 // several items); a *patch* is the (TC+2m-1)^d grid block an item spreads
 // into.
+//
+// Window factors. The reference weight of tap o (0..2m-1) in dimension t is
+//   phi = exp(-(u_t - o)^2 / b) / sqrt(pi b),  u_t = x_t M - floor(x_t M) + m - 1
+// (P:src/fastsum.cpp:75-78, 222-228). Expanding the square,
+//   prod_t phi_t(o_t) = P * prod_t Q_t^{o_t} R[o_t],
+//   P = (pi b)^{-d/2} exp(-sum_t u_t^2 / b),  Q_t = exp(2 u_t / b),  R[o] = exp(-o^2 / b),
+// so a plan stores (P, Q_0..Q_{d-1}, tile-local cell code) per sorted point
+// and the apply evaluates no exp() at all.
 #pragma once
 
 #include <cstdint>
@@ -18,9 +26,9 @@ constexpr int kMaxSpan = 16;  // 2m, m <= 8 (P:src/fastsum.cpp:41-42, w[3][16] a
 
 // One tile's (or part of a tile's) sorted point range.
 struct Item {
-    int ps;         // point-set slot
-    int tile;       // linear tile index within the window's tile grid
-    int begin;      // sorted point range [begin, end)
+    int ps;           // point-set slot
+    int tile;         // linear tile index within the window's tile grid
+    int begin;        // sorted point range [begin, end)
     int end;
     long long patch;  // offset of this item's patch in the patch buffer (spread only)
 };
@@ -32,8 +40,8 @@ struct DWin {
     int m;
     int M;       // grid edge sigma*N
     int Lg;      // local grid edge (<= M)
-    int lo;      // global index of local node 0 (non-wrapping layout)
-    int wrap;    // 1: local index = global index mod M (Lg == M)
+    int lo;      // global index of extended node 0
+    int wrap;    // 1: local index = (lo + e) mod M (Lg == M); 0: local index = e
     int cmin;    // smallest cell index floor(xM) any in-ball point can have
     int ncell;   // number of cell indices per dimension
     int TC;      // cells per tile edge
@@ -44,7 +52,7 @@ struct DWin {
     double bwin; // Gaussian window shape b (P:src/fastsum.cpp:124)
     double invb; // 1 / b
     double Cw;   // 1/sqrt(pi b)        (P:src/fastsum.cpp:77)
-    double R[kMaxSpan];  // exp(-o^2/b), o = 0..S-1 (window factorisation)
+    double R[kMaxSpan];  // exp(-o^2/b), o = 0..S-1
     double* G;   // spread grid, Lg^d
     double* H;   // filtered grid, Lg^d
     double* T[4];  // separable-convolution temporaries, Lg^d each
@@ -57,7 +65,9 @@ struct DWin {
 
 // A sorted point set (a window's sources, or cross-apply targets).
 struct DPSet {
-    const double* x[3];  // scaled coordinates, sorted by (tile, cell)
+    const double* P;     // prefactor (pi b)^{-d/2} exp(-sum u^2/b), sorted order
+    const double* Q[3];  // exp(2 u_t / b)
+    const int* code;     // tile-local cell code, sum_t (c_t mod TC) TC^{d-1-t}
     const int* perm;     // sorted position -> original index
     long long n;
     int win;             // owning window slot

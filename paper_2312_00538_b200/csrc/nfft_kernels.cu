@@ -1,7 +1,7 @@
 // sm_100a kernels of the ANOVA-NFFT matvec y = sum_l eta_l K~_l v
 // (reference: P:src/fastsum.cpp:257-296 run_transform, :345-352 window sum).
 //
-// Per apply, for every window (batched over windows in each launch):
+// Per apply, for every window (each launch covers all windows of a class):
 //   spread   adjoint NFFT, sources -> per-item grid patches   (:264-272)
 //   reduce   patches -> grid G, fixed order (deterministic, no atomics)
 //   conv     G -> H: FFT, spectral multiply, inverse FFT, real part
@@ -12,7 +12,8 @@
 //
 // No global atomics anywhere: every reduction has a fixed order, so two
 // applies with the same plan and v are bit-identical
-// (P:tests/test_fastsum.cpp:208-215).
+// (P:tests/test_fastsum.cpp:208-215). Window weights come from per-point
+// factors precomputed at plan time (nfft_engine.cuh), so no exp() runs here.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -29,40 +30,6 @@ __device__ __forceinline__ int pmod(int a, int M) {
     return r < 0 ? r + M : r;
 }
 
-// Truncated-Gaussian window weights of one coordinate
-// (P:src/fastsum.cpp:75-78, 222-228): taps o = 0..S-1 sit at grid index
-// floor(xM) - m + 1 + o and weigh
-//   phi = exp(-(xM - floor(xM) + m - 1 - o)^2 / b) / sqrt(pi b)
-//       = [Cw exp(-u^2/b)] * exp(2u/b)^o * exp(-o^2/b),   u = xM - floor(xM) + m - 1,
-// i.e. two exp() per coordinate instead of 2m. Returns floor(xM).
-template <int S>
-__device__ __forceinline__ int window_weights(double x, const DWin& w, double* out) {
-    const double xm = x * w.Mf;
-    const double fl = floor(xm);
-    const double u = (xm - fl) + static_cast<double>(w.m - 1);
-    double q = w.Cw * exp(-(u * u) * w.invb);
-    const double Q = exp((2.0 * u) * w.invb);
-#pragma unroll
-    for (int o = 0; o < S; ++o) {
-        out[o] = q * w.R[o];
-        q *= Q;
-    }
-    return static_cast<int>(fl);
-}
-
-__device__ __forceinline__ int window_weights_rt(double x, const DWin& w, double* out) {
-    const double xm = x * w.Mf;
-    const double fl = floor(xm);
-    const double u = (xm - fl) + static_cast<double>(w.m - 1);
-    double q = w.Cw * exp(-(u * u) * w.invb);
-    const double Q = exp((2.0 * u) * w.invb);
-    for (int o = 0; o < w.S; ++o) {
-        out[o] = q * w.R[o];
-        q *= Q;
-    }
-    return static_cast<int>(fl);
-}
-
 __device__ __forceinline__ void tile_coords(int tile, int d, int nt, int* t) {
     for (int k = d - 1; k >= 0; --k) {
         t[k] = tile % nt;
@@ -74,53 +41,80 @@ __device__ __forceinline__ void tile_coords(int tile, int d, int nt, int* t) {
 __device__ __forceinline__ void warp_range(const Item& it, int warp, int W, int* b, int* e) {
     const int len = it.end - it.begin;
     const int per = (len + W - 1) / W;
-    *b = it.begin + warp * per;
-    if (*b > it.end) *b = it.end;
+    *b = min(it.begin + warp * per, it.end);
     *e = min(*b + per, it.end);
-}
-
-// Per-point staging row (doubles): w0[8] w1[8] w2[8] | cell code (int) | pad.
-// 26 doubles = 208 B keeps every double2 slot 16-byte aligned.
-constexpr int kSt = 26;
-
-__device__ __forceinline__ int cell_of(const double* st) {
-    return *reinterpret_cast<const int*>(st + 24);
 }
 
 __device__ __forceinline__ double2 ld2(const double* p) {
     return *reinterpret_cast<const double2*>(p);
 }
 
+// Staged per-point row: w_0[S] (times P, and v for spread) | w_1[S] | w_2[S] | code.
+template <int D, int S>
+struct Row {
+    static constexpr int kLen = ((D * S + 1) + 1) & ~1;  // even: keeps double2 slots aligned
+};
+
+__device__ __forceinline__ int row_code(const double* st, int D, int S) {
+    return *reinterpret_cast<const int*>(st + D * S);
+}
+
+// Write the tensor-factor weights of one point into its staging row.
+template <int D, int S>
+__device__ __forceinline__ void stage_row(double* st, const double* R, double P, const double* Q,
+                                          int code) {
+#pragma unroll
+    for (int t = 0; t < D; ++t) {
+        double q = t == 0 ? P : 1.0;
+#pragma unroll
+        for (int o = 0; o < S; ++o) {
+            st[t * S + o] = q * R[o];
+            q *= Q[t];
+        }
+    }
+    *reinterpret_cast<int*>(st + D * S) = code;
+}
+
+// Registers of one prefetched point (software pipeline over 32-point batches).
+template <int D>
+struct Pref {
+    double P = 0.0, Q[3] = {0.0, 0.0, 0.0};
+    int code = 0;
+    __device__ __forceinline__ void load(const DPSet& ps, int i) {
+        P = ps.P[i];
+#pragma unroll
+        for (int t = 0; t < D; ++t) Q[t] = ps.Q[t][i];
+        code = ps.code[i];
+    }
+};
+
 }  // namespace
 
-// ---------------------------------------------------------------------------
-// Spread, d = 3, m = 4 (S = 8): register-blocked per cell.
+// ===========================================================================
+// d = 3, m = 4 (S = 8): register-blocked per cell.
 // Lane L owns the 16 taps (a, b0..b0+1, 0..7) of the cell's 8^3 block with
-// a = L/4, b0 = 2 (L%4); consecutive points of one cell accumulate in
-// registers and are flushed into the warp's private SMEM patch when the
-// cell changes. Points are sorted by cell, so a run of 4 with equal first
-// and last cell is one cell: that fast path has no branches and 16
-// independent FMA chains. The W private patches are summed in warp order
-// and written to the item's global patch.
-// ---------------------------------------------------------------------------
+// a = L/4, b0 = 2 (L%4). Points are sorted by cell, so a run of 4 whose first
+// and last share a cell is one cell: that fast path has no branches and 16
+// independent FMA chains.
+// ===========================================================================
 template <int W>
 __global__ void __launch_bounds__(W * 32)
 spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
                   const DWin* __restrict__ wins, const double* __restrict__ v,
                   double* __restrict__ patches) {
-    constexpr int S = 8, TC = 4, PE = TC + S - 1, PV = PE * PE * PE;
+    constexpr int D = 3, S = 8, TC = 4, PE = TC + S - 1, PV = PE * PE * PE, RL = Row<D, S>::kLen;
     extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double* wp = smem + warp * PV;
-    double* stage = smem + W * PV + warp * 32 * kSt;
+    double* stage = smem + ((W * PV + 1) & ~1) + warp * 32 * RL;
 
     const Item it = items[blockIdx.x];
     const DPSet& ps = psets[it.ps];
     const DWin& wn = wins[ps.win];
+    double R[S];
+#pragma unroll
+    for (int o = 0; o < S; ++o) R[o] = wn.R[o];
     for (int k = lane; k < PV; k += 32) wp[k] = 0.0;
-    int tc[3];
-    tile_coords(it.tile, 3, wn.ntile, tc);
-    const int off0 = wn.cmin + tc[0] * TC, off1 = wn.cmin + tc[1] * TC, off2 = wn.cmin + tc[2] * TC;
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
     const int a = lane >> 2, b0 = (lane & 3) << 1;
@@ -129,10 +123,9 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
 #pragma unroll
     for (int c = 0; c < S; ++c) acc0[c] = acc1[c] = 0.0;
     int cur = -1;
-    __syncwarp();
 
     auto flush = [&](int cell) {
-        const int l0 = cell / (TC * TC), l1 = (cell / TC) % TC, l2 = cell % TC;
+        const int l0 = cell >> 4, l1 = (cell >> 2) & 3, l2 = cell & 3;
         double* dst = wp + ((l0 + a) * PE + l1 + b0) * PE + l2;
 #pragma unroll
         for (int c = 0; c < S; ++c) {
@@ -144,11 +137,11 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     };
     auto accumulate = [&](const double* st) {
         const double w0a = st[a];
-        const double2 w1 = ld2(st + 8 + b0);
+        const double2 w1 = ld2(st + S + b0);
         const double u0 = w0a * w1.x, u1 = w0a * w1.y;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const double2 w2 = ld2(st + 16 + 2 * k);
+            const double2 w2 = ld2(st + 2 * S + 2 * k);
             acc0[2 * k] = fma(u0, w2.x, acc0[2 * k]);
             acc0[2 * k + 1] = fma(u0, w2.y, acc0[2 * k + 1]);
             acc1[2 * k] = fma(u1, w2.x, acc1[2 * k]);
@@ -156,38 +149,45 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
         }
     };
 
+    // two-deep software pipeline: perm two batches ahead, factors and v one ahead
+    Pref<D> pf;
+    int perm1 = 0, perm2 = 0;
+    double vnext = 0.0;
+    {
+        const int i0 = wb + lane, i1 = wb + 32 + lane;
+        if (i0 < we) {
+            pf.load(ps, i0);
+            vnext = v[ps.perm[i0]];
+        }
+        if (i1 < we) perm1 = ps.perm[i1];
+    }
+    __syncwarp();
     for (int base = wb; base < we; base += 32) {
         const int cnt = min(32, we - base);
-        if (lane < cnt) {
-            const int i = base + lane;
-            double w[S];
-            double* st = stage + lane * kSt;
-            const double vi = v[ps.perm[i]];
-            const int c0 = window_weights<S>(ps.x[0][i], wn, w) - off0;
-#pragma unroll
-            for (int o = 0; o < S; ++o) st[o] = w[o] * vi;
-            const int c1 = window_weights<S>(ps.x[1][i], wn, w) - off1;
-#pragma unroll
-            for (int o = 0; o < S; ++o) st[8 + o] = w[o];
-            const int c2 = window_weights<S>(ps.x[2][i], wn, w) - off2;
-#pragma unroll
-            for (int o = 0; o < S; ++o) st[16 + o] = w[o];
-            *reinterpret_cast<int*>(st + 24) = (c0 * TC + c1) * TC + c2;
+        if (lane < cnt) stage_row<D, S>(stage + lane * RL, R, pf.P * vnext, pf.Q, pf.code);
+        {
+            const int i1 = base + 32 + lane, i2 = base + 64 + lane;
+            if (i2 < we) perm2 = ps.perm[i2];
+            if (i1 < we) {
+                pf.load(ps, i1);
+                vnext = v[perm1];
+            }
+            perm1 = perm2;
         }
         __syncwarp();
         int p = 0;
         while (p < cnt) {
-            const double* st = stage + p * kSt;
-            const int cp = cell_of(st);
+            const double* st = stage + p * RL;
+            const int cp = row_code(st, D, S);
             if (cp != cur) {
                 if (cur >= 0) flush(cur);
                 cur = cp;
             }
-            if (p + 3 < cnt && cell_of(st + 3 * kSt) == cp) {
+            if (p + 3 < cnt && row_code(st + 3 * RL, D, S) == cp) {
                 accumulate(st);
-                accumulate(st + kSt);
-                accumulate(st + 2 * kSt);
-                accumulate(st + 3 * kSt);
+                accumulate(st + RL);
+                accumulate(st + 2 * RL);
+                accumulate(st + 3 * RL);
                 p += 4;
             } else {
                 accumulate(st);
@@ -207,46 +207,76 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     }
 }
 
-// ---------------------------------------------------------------------------
-// Gather, d = 3, m = 4: the tile's 11^3 grid halo sits in SMEM; lane L holds
-// the 16 grid values of its taps for the current cell in registers and
-// computes a partial for each of 32 consecutive points (4-point same-cell
-// fast path, 4 independent chains per point); a transposed butterfly
-// (reduce-scatter) leaves point p's sum in lane p.
-// ---------------------------------------------------------------------------
+// Load the (TC+S-1)^d grid halo of a tile into SMEM (wrap / bounds aware).
+template <int D>
+__device__ __forceinline__ void load_halo(double* halo, const DWin& wn, const int* tc, int TC, int PE,
+                                          int PV) {
+    const int Lg = wn.Lg;
+    for (int k = threadIdx.x; k < PV; k += blockDim.x) {
+        int r = k, n[3] = {0, 0, 0};
+#pragma unroll
+        for (int t = D - 1; t >= 0; --t) {
+            n[t] = r % PE;
+            r /= PE;
+        }
+        long long gi = 0;
+        bool ok = true;
+#pragma unroll
+        for (int t = 0; t < D; ++t) {
+            int g = tc[t] * TC + n[t];
+            if (wn.wrap) g = pmod(wn.lo + g, wn.M);
+            else ok = ok && g < Lg;
+            gi = gi * Lg + g;
+        }
+        halo[k] = ok ? wn.H[gi] : 0.0;
+    }
+}
+
+// Transposed butterfly over 32 point partials: afterwards lane p holds the
+// full sum of point p (each sum in a fixed order).
+__device__ __forceinline__ double butterfly32(double (&pp)[32], int lane) {
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+        const bool upper = (lane & s) != 0;
+#pragma unroll
+        for (int k = 0; k < s; ++k) {
+            const double send = upper ? pp[k] : pp[k + s];
+            const double keep = upper ? pp[k + s] : pp[k];
+            pp[k] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+        }
+    }
+    return pp[0];
+}
+
 template <int W>
 __global__ void __launch_bounds__(W * 32)
 gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
                   const DWin* __restrict__ wins) {
-    constexpr int S = 8, TC = 4, PE = TC + S - 1, PV = PE * PE * PE;
+    constexpr int D = 3, S = 8, TC = 4, PE = TC + S - 1, PV = PE * PE * PE, RL = Row<D, S>::kLen;
     extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double* halo = smem;
-    // PV = 1331 doubles is not a multiple of 2: start the staging area at 1332
-    double* stage = smem + (PV + 1) + warp * 32 * kSt;
+    double* stage = smem + ((PV + 1) & ~1) + warp * 32 * RL;
 
     const Item it = items[blockIdx.x];
     const DPSet& ps = psets[it.ps];
     const DWin& wn = wins[ps.win];
-    int tc[3];
-    tile_coords(it.tile, 3, wn.ntile, tc);
-    const int Lg = wn.Lg;
-    for (int k = threadIdx.x; k < PV; k += W * 32) {
-        const int n0 = k / (PE * PE), n1 = (k / PE) % PE, n2 = k % PE;
-        int g[3] = {tc[0] * TC + n0, tc[1] * TC + n1, tc[2] * TC + n2};
-        bool ok = true;
+    double R[S];
 #pragma unroll
-        for (int t = 0; t < 3; ++t) {
-            if (wn.wrap) g[t] = pmod(wn.lo + g[t], wn.M);
-            else ok = ok && g[t] < Lg;
-        }
-        halo[k] = ok ? wn.H[(static_cast<long long>(g[0]) * Lg + g[1]) * Lg + g[2]] : 0.0;
+    for (int o = 0; o < S; ++o) R[o] = wn.R[o];
+    int tc[3];
+    tile_coords(it.tile, D, wn.ntile, tc);
+    load_halo<D>(halo, wn, tc, TC, PE, PV);
+    int wb, we;
+    warp_range(it, warp, W, &wb, &we);
+    Pref<D> pf;
+    int permc = 0, permn = 0;
+    if (wb + lane < we) {
+        pf.load(ps, wb + lane);
+        permn = ps.perm[wb + lane];
     }
     __syncthreads();
 
-    const int off0 = wn.cmin + tc[0] * TC, off1 = wn.cmin + tc[1] * TC, off2 = wn.cmin + tc[2] * TC;
-    int wb, we;
-    warp_range(it, warp, W, &wb, &we);
     const int a = lane >> 2, b0 = (lane & 3) << 1;
     double h0[S], h1[S];
 #pragma unroll
@@ -254,7 +284,7 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     int cur = -1;
 
     auto reload = [&](int cell) {
-        const int l0 = cell / (TC * TC), l1 = (cell / TC) % TC, l2 = cell % TC;
+        const int l0 = cell >> 4, l1 = (cell >> 2) & 3, l2 = cell & 3;
         const double* src = halo + ((l0 + a) * PE + l1 + b0) * PE + l2;
 #pragma unroll
         for (int c = 0; c < S; ++c) {
@@ -266,86 +296,292 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
         double e0 = 0.0, o0 = 0.0, e1 = 0.0, o1 = 0.0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const double2 w2 = ld2(st + 16 + 2 * k);
+            const double2 w2 = ld2(st + 2 * S + 2 * k);
             e0 = fma(h0[2 * k], w2.x, e0);
             o0 = fma(h0[2 * k + 1], w2.y, o0);
             e1 = fma(h1[2 * k], w2.x, e1);
             o1 = fma(h1[2 * k + 1], w2.y, o1);
         }
-        const double2 w1 = ld2(st + 8 + b0);
+        const double2 w1 = ld2(st + S + b0);
         return st[a] * fma(w1.x, e0 + o0, w1.y * (e1 + o1));
     };
 
     for (int base = wb; base < we; base += 32) {
         const int cnt = min(32, we - base);
-        if (lane < cnt) {
-            const int i = base + lane;
-            double w[S];
-            double* st = stage + lane * kSt;
-            const int c0 = window_weights<S>(ps.x[0][i], wn, w) - off0;
-#pragma unroll
-            for (int o = 0; o < S; ++o) st[o] = w[o];
-            const int c1 = window_weights<S>(ps.x[1][i], wn, w) - off1;
-#pragma unroll
-            for (int o = 0; o < S; ++o) st[8 + o] = w[o];
-            const int c2 = window_weights<S>(ps.x[2][i], wn, w) - off2;
-#pragma unroll
-            for (int o = 0; o < S; ++o) st[16 + o] = w[o];
-            *reinterpret_cast<int*>(st + 24) = (c0 * TC + c1) * TC + c2;
+        if (lane < cnt) stage_row<D, S>(stage + lane * RL, R, pf.P, pf.Q, pf.code);
+        permc = permn;
+        {
+            const int i1 = base + 32 + lane;
+            if (i1 < we) {
+                pf.load(ps, i1);
+                permn = ps.perm[i1];
+            }
         }
         __syncwarp();
         double pp[32];
 #pragma unroll
         for (int g = 0; g < 8; ++g) {
             const int p0 = 4 * g;
-            const double* st = stage + p0 * kSt;
-            if (p0 + 3 < cnt && cell_of(st) == cell_of(st + 3 * kSt)) {
-                const int cp = cell_of(st);
+            const double* st = stage + p0 * RL;
+            if (p0 + 3 < cnt && row_code(st, D, S) == row_code(st + 3 * RL, D, S)) {
+                const int cp = row_code(st, D, S);
                 if (cp != cur) {
                     cur = cp;
                     reload(cp);
                 }
                 pp[p0] = partial(st);
-                pp[p0 + 1] = partial(st + kSt);
-                pp[p0 + 2] = partial(st + 2 * kSt);
-                pp[p0 + 3] = partial(st + 3 * kSt);
+                pp[p0 + 1] = partial(st + RL);
+                pp[p0 + 2] = partial(st + 2 * RL);
+                pp[p0 + 3] = partial(st + 3 * RL);
             } else {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     pp[p0 + q] = 0.0;
                     if (p0 + q < cnt) {
-                        const int cp = cell_of(st + q * kSt);
+                        const int cp = row_code(st + q * RL, D, S);
                         if (cp != cur) {
                             cur = cp;
                             reload(cp);
                         }
-                        pp[p0 + q] = partial(st + q * kSt);
+                        pp[p0 + q] = partial(st + q * RL);
                     }
                 }
             }
         }
-        // transposed butterfly: after the 5 stages lane p holds point p's sum
-#pragma unroll
-        for (int s = 16; s >= 1; s >>= 1) {
-            const bool upper = (lane & s) != 0;
-#pragma unroll
-            for (int k = 0; k < s; ++k) {
-                const double send = upper ? pp[k] : pp[k + s];
-                const double keep = upper ? pp[k + s] : pp[k];
-                pp[k] = keep + __shfl_xor_sync(0xffffffffu, send, s);
-            }
-        }
-        if (lane < cnt) ps.out[ps.perm[base + lane]] = pp[0];
+        const double val = butterfly32(pp, lane);
+        if (lane < cnt) ps.out[permc] = val;
         __syncwarp();
     }
 }
 
-// ---------------------------------------------------------------------------
+// ===========================================================================
+// d = 2, m = 4: lane L owns taps (a, b0), (a, b0+1), a = L/4, b0 = 2 (L%4).
+// ===========================================================================
+template <int W>
+__global__ void __launch_bounds__(W * 32)
+spread2_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
+                  const DWin* __restrict__ wins, const double* __restrict__ v,
+                  double* __restrict__ patches) {
+    constexpr int D = 2, S = 8, TC = 8, PE = TC + S - 1, PV = PE * PE, RL = Row<D, S>::kLen;
+    extern __shared__ __align__(16) double smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* wp = smem + warp * PV;
+    double* stage = smem + ((W * PV + 1) & ~1) + warp * 32 * RL;
+    const Item it = items[blockIdx.x];
+    const DPSet& ps = psets[it.ps];
+    const DWin& wn = wins[ps.win];
+    double R[S];
+#pragma unroll
+    for (int o = 0; o < S; ++o) R[o] = wn.R[o];
+    for (int k = lane; k < PV; k += 32) wp[k] = 0.0;
+    int wb, we;
+    warp_range(it, warp, W, &wb, &we);
+    const int a = lane >> 2, b0 = (lane & 3) << 1;
+    double acc0 = 0.0, acc1 = 0.0;
+    int cur = -1;
+    auto flush = [&](int cell) {
+        double* dst = wp + ((cell >> 3) + a) * PE + (cell & 7) + b0;
+        dst[0] += acc0;
+        dst[1] += acc1;
+        acc0 = acc1 = 0.0;
+    };
+    Pref<D> pf;
+    int perm1 = 0, perm2 = 0;
+    double vnext = 0.0;
+    {
+        const int i0 = wb + lane, i1 = wb + 32 + lane;
+        if (i0 < we) {
+            pf.load(ps, i0);
+            vnext = v[ps.perm[i0]];
+        }
+        if (i1 < we) perm1 = ps.perm[i1];
+    }
+    __syncwarp();
+    for (int base = wb; base < we; base += 32) {
+        const int cnt = min(32, we - base);
+        if (lane < cnt) stage_row<D, S>(stage + lane * RL, R, pf.P * vnext, pf.Q, pf.code);
+        {
+            const int i1 = base + 32 + lane, i2 = base + 64 + lane;
+            if (i2 < we) perm2 = ps.perm[i2];
+            if (i1 < we) {
+                pf.load(ps, i1);
+                vnext = v[perm1];
+            }
+            perm1 = perm2;
+        }
+        __syncwarp();
+        for (int p = 0; p < cnt; ++p) {
+            const double* st = stage + p * RL;
+            const int cp = row_code(st, D, S);
+            if (cp != cur) {
+                if (cur >= 0) flush(cur);
+                cur = cp;
+            }
+            const double u = st[a];
+            const double2 w1 = ld2(st + S + b0);
+            acc0 = fma(u, w1.x, acc0);
+            acc1 = fma(u, w1.y, acc1);
+        }
+        __syncwarp();
+    }
+    if (cur >= 0) flush(cur);
+    __syncthreads();
+    double* out = patches + it.patch;
+    for (int k = threadIdx.x; k < PV; k += W * 32) {
+        double s = smem[k];
+#pragma unroll
+        for (int q = 1; q < W; ++q) s += smem[q * PV + k];
+        out[k] = s;
+    }
+}
+
+template <int W>
+__global__ void __launch_bounds__(W * 32)
+gather2_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
+                  const DWin* __restrict__ wins) {
+    constexpr int D = 2, S = 8, TC = 8, PE = TC + S - 1, PV = PE * PE, RL = Row<D, S>::kLen;
+    extern __shared__ __align__(16) double smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* halo = smem;
+    double* stage = smem + ((PV + 1) & ~1) + warp * 32 * RL;
+    const Item it = items[blockIdx.x];
+    const DPSet& ps = psets[it.ps];
+    const DWin& wn = wins[ps.win];
+    double R[S];
+#pragma unroll
+    for (int o = 0; o < S; ++o) R[o] = wn.R[o];
+    int tc[3];
+    tile_coords(it.tile, D, wn.ntile, tc);
+    load_halo<D>(halo, wn, tc, TC, PE, PV);
+    int wb, we;
+    warp_range(it, warp, W, &wb, &we);
+    Pref<D> pf;
+    int permc = 0, permn = 0;
+    if (wb + lane < we) {
+        pf.load(ps, wb + lane);
+        permn = ps.perm[wb + lane];
+    }
+    __syncthreads();
+    const int a = lane >> 2, b0 = (lane & 3) << 1;
+    double h0 = 0.0, h1 = 0.0;
+    int cur = -1;
+    for (int base = wb; base < we; base += 32) {
+        const int cnt = min(32, we - base);
+        if (lane < cnt) stage_row<D, S>(stage + lane * RL, R, pf.P, pf.Q, pf.code);
+        permc = permn;
+        {
+            const int i1 = base + 32 + lane;
+            if (i1 < we) {
+                pf.load(ps, i1);
+                permn = ps.perm[i1];
+            }
+        }
+        __syncwarp();
+        double pp[32];
+#pragma unroll
+        for (int p = 0; p < 32; ++p) {
+            pp[p] = 0.0;
+            if (p < cnt) {
+                const double* st = stage + p * RL;
+                const int cp = row_code(st, D, S);
+                if (cp != cur) {
+                    cur = cp;
+                    const double* src = halo + ((cp >> 3) + a) * PE + (cp & 7) + b0;
+                    h0 = src[0];
+                    h1 = src[1];
+                }
+                const double2 w1 = ld2(st + S + b0);
+                pp[p] = st[a] * fma(w1.x, h0, w1.y * h1);
+            }
+        }
+        const double val = butterfly32(pp, lane);
+        if (lane < cnt) ps.out[permc] = val;
+        __syncwarp();
+    }
+}
+
+// ===========================================================================
+// d = 1, m = 4: one lane per point. Spread accumulates into a lane-private
+// column of the warp's SMEM patch (node-major, lane-minor), reduced in fixed
+// (warp, lane) order at the end.
+// ===========================================================================
+template <int W>
+__global__ void __launch_bounds__(W * 32)
+spread1_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
+                  const DWin* __restrict__ wins, const double* __restrict__ v,
+                  double* __restrict__ patches) {
+    constexpr int S = 8, TC = 32, PE = TC + S - 1;
+    extern __shared__ __align__(16) double smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* lp = smem + warp * PE * 32;
+    const Item it = items[blockIdx.x];
+    const DPSet& ps = psets[it.ps];
+    const DWin& wn = wins[ps.win];
+    double R[S];
+#pragma unroll
+    for (int o = 0; o < S; ++o) R[o] = wn.R[o];
+    for (int k = lane; k < PE * 32; k += 32) lp[k] = 0.0;
+    __syncwarp();
+    int wb, we;
+    warp_range(it, warp, W, &wb, &we);
+    for (int i = wb + lane; i < we; i += 32) {
+        double q = ps.P[i] * v[ps.perm[i]];
+        const double Q = ps.Q[0][i];
+        double* col = lp + ps.code[i] * 32 + lane;
+#pragma unroll
+        for (int o = 0; o < S; ++o) {
+            col[o * 32] = fma(q, R[o], col[o * 32]);
+            q *= Q;
+        }
+    }
+    __syncthreads();
+    double* out = patches + it.patch;
+    for (int k = threadIdx.x; k < PE; k += W * 32) {
+        double s = 0.0;
+        for (int q = 0; q < W; ++q)
+            for (int l = 0; l < 32; ++l) s += smem[q * PE * 32 + k * 32 + l];
+        out[k] = s;
+    }
+}
+
+template <int W>
+__global__ void __launch_bounds__(W * 32)
+gather1_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
+                  const DWin* __restrict__ wins) {
+    constexpr int D = 1, S = 8, TC = 32, PE = TC + S - 1;
+    extern __shared__ __align__(16) double smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const Item it = items[blockIdx.x];
+    const DPSet& ps = psets[it.ps];
+    const DWin& wn = wins[ps.win];
+    double R[S];
+#pragma unroll
+    for (int o = 0; o < S; ++o) R[o] = wn.R[o];
+    int tc[3];
+    tile_coords(it.tile, D, wn.ntile, tc);
+    load_halo<D>(smem, wn, tc, TC, PE, PE);
+    __syncthreads();
+    int wb, we;
+    warp_range(it, warp, W, &wb, &we);
+    for (int i = wb + lane; i < we; i += 32) {
+        double q = ps.P[i];
+        const double Q = ps.Q[0][i];
+        const double* h = smem + ps.code[i];
+        double y = 0.0;
+#pragma unroll
+        for (int o = 0; o < S; ++o) {
+            y = fma(h[o], q * R[o], y);
+            q *= Q;
+        }
+        ps.out[ps.perm[i]] = y;
+    }
+}
+
+// ===========================================================================
 // Generic spread / gather for any d in 1..3 and any m (runtime S <= 16):
-// lanes stride over the S^d taps of one point at a time; spread accumulates
-// straight into the warp's private SMEM patch.
-// ---------------------------------------------------------------------------
-constexpr int kStageG = 3 * kMaxSpan + 1;
+// lanes stride over the S^d taps of one point at a time.
+// ===========================================================================
+constexpr int kRowG = 3 * kMaxSpan + 2;
 
 template <int D>
 __global__ void spread_generic_kernel(const Item* __restrict__ items,
@@ -353,7 +589,7 @@ __global__ void spread_generic_kernel(const Item* __restrict__ items,
                                       const DWin* __restrict__ wins,
                                       const double* __restrict__ v,
                                       double* __restrict__ patches, int W) {
-    extern __shared__ double smem[];
+    extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const Item it = items[blockIdx.x];
     const DPSet& ps = psets[it.ps];
@@ -365,10 +601,8 @@ __global__ void spread_generic_kernel(const Item* __restrict__ items,
         taps *= S;
     }
     double* wp = smem + warp * PV;
-    double* stage = smem + W * PV + warp * 32 * kStageG;
+    double* stage = smem + ((W * PV + 1) & ~1) + warp * 32 * kRowG;
     for (int k = lane; k < PV; k += 32) wp[k] = 0.0;
-    int tc[3] = {0, 0, 0};
-    tile_coords(it.tile, D, wn.ntile, tc);
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
     __syncwarp();
@@ -376,21 +610,21 @@ __global__ void spread_generic_kernel(const Item* __restrict__ items,
         const int cnt = min(32, we - base);
         if (lane < cnt) {
             const int i = base + lane;
-            double* st = stage + lane * kStageG;
-            const double vi = v[ps.perm[i]];
-            int code = 0;
+            double* st = stage + lane * kRowG;
             for (int t = 0; t < D; ++t) {
-                double w[kMaxSpan];
-                const int c = window_weights_rt(ps.x[t][i], wn, w) - wn.cmin - tc[t] * TC;
-                for (int o = 0; o < S; ++o) st[t * kMaxSpan + o] = t == 0 ? w[o] * vi : w[o];
-                code = code * TC + c;
+                double q = t == 0 ? ps.P[i] * v[ps.perm[i]] : 1.0;
+                const double Q = ps.Q[t][i];
+                for (int o = 0; o < S; ++o) {
+                    st[t * kMaxSpan + o] = q * wn.R[o];
+                    q *= Q;
+                }
             }
-            st[3 * kMaxSpan] = static_cast<double>(code);
+            *reinterpret_cast<int*>(st + 3 * kMaxSpan) = ps.code[i];
         }
         __syncwarp();
         for (int p = 0; p < cnt; ++p) {
-            const double* st = stage + p * kStageG;
-            int code = static_cast<int>(st[3 * kMaxSpan]);
+            const double* st = stage + p * kRowG;
+            int code = *reinterpret_cast<const int*>(st + 3 * kMaxSpan);
             int cl[3] = {0, 0, 0};
             for (int t = D - 1; t >= 0; --t) {
                 cl[t] = code % TC;
@@ -426,38 +660,22 @@ template <int D>
 __global__ void gather_generic_kernel(const Item* __restrict__ items,
                                       const DPSet* __restrict__ psets,
                                       const DWin* __restrict__ wins, int W) {
-    extern __shared__ double smem[];
+    extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const Item it = items[blockIdx.x];
     const DPSet& ps = psets[it.ps];
     const DWin& wn = wins[ps.win];
-    const int S = wn.S, TC = wn.TC, PE = wn.PE, Lg = wn.Lg;
+    const int S = wn.S, TC = wn.TC, PE = wn.PE;
     int PV = 1, taps = 1;
     for (int t = 0; t < D; ++t) {
         PV *= PE;
         taps *= S;
     }
     double* halo = smem;
-    double* stage = smem + PV + warp * 32 * kStageG;
+    double* stage = smem + ((PV + 1) & ~1) + warp * 32 * kRowG;
     int tc[3] = {0, 0, 0};
     tile_coords(it.tile, D, wn.ntile, tc);
-    for (int k = threadIdx.x; k < PV; k += W * 32) {
-        int r = k;
-        long long gi = 0;
-        bool ok = true;
-        int n[3];
-        for (int t = D - 1; t >= 0; --t) {
-            n[t] = r % PE;
-            r /= PE;
-        }
-        for (int t = 0; t < D; ++t) {
-            int g = tc[t] * TC + n[t];
-            if (wn.wrap) g = pmod(wn.lo + g, wn.M);
-            else ok = ok && g < Lg;
-            gi = gi * Lg + g;
-        }
-        halo[k] = ok ? wn.H[gi] : 0.0;
-    }
+    load_halo<D>(halo, wn, tc, TC, PE, PV);
     __syncthreads();
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
@@ -465,20 +683,21 @@ __global__ void gather_generic_kernel(const Item* __restrict__ items,
         const int cnt = min(32, we - base);
         if (lane < cnt) {
             const int i = base + lane;
-            double* st = stage + lane * kStageG;
-            int code = 0;
+            double* st = stage + lane * kRowG;
             for (int t = 0; t < D; ++t) {
-                double w[kMaxSpan];
-                const int c = window_weights_rt(ps.x[t][i], wn, w) - wn.cmin - tc[t] * TC;
-                for (int o = 0; o < S; ++o) st[t * kMaxSpan + o] = w[o];
-                code = code * TC + c;
+                double q = t == 0 ? ps.P[i] : 1.0;
+                const double Q = ps.Q[t][i];
+                for (int o = 0; o < S; ++o) {
+                    st[t * kMaxSpan + o] = q * wn.R[o];
+                    q *= Q;
+                }
             }
-            st[3 * kMaxSpan] = static_cast<double>(code);
+            *reinterpret_cast<int*>(st + 3 * kMaxSpan) = ps.code[i];
         }
         __syncwarp();
         for (int p = 0; p < cnt; ++p) {
-            const double* st = stage + p * kStageG;
-            int code = static_cast<int>(st[3 * kMaxSpan]);
+            const double* st = stage + p * kRowG;
+            int code = *reinterpret_cast<const int*>(st + 3 * kMaxSpan);
             int cl[3] = {0, 0, 0};
             for (int t = D - 1; t >= 0; --t) {
                 cl[t] = code % TC;
@@ -507,131 +726,190 @@ __global__ void gather_generic_kernel(const Item* __restrict__ items,
     }
 }
 
-// ---------------------------------------------------------------------------
+// ===========================================================================
 // Patch reduction: grid node <- sum of every covering item's patch value, in
 // (e0, T0, e1, T1, e2, T2, item) order. blockIdx.y = window slot.
-// ---------------------------------------------------------------------------
+// ===========================================================================
+template <int D>
 __global__ void reduce_patches_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots,
                                       const double* __restrict__ patches) {
     const DWin& wn = wins[slots[blockIdx.y]];
-    const int D = wn.d, Lg = wn.Lg, TC = wn.TC, PE = wn.PE, nt = wn.ntile;
-    long long nodes = 1;
-    int PV = 1;
+    if (wn.d != D) return;
+    const int Lg = wn.Lg, TC = wn.TC, PE = wn.PE, nt = wn.ntile;
+    int nodes = 1, PV = 1;
+#pragma unroll
     for (int t = 0; t < D; ++t) {
         nodes *= Lg;
         PV *= PE;
     }
-    const long long node = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int node = blockIdx.x * blockDim.x + threadIdx.x;
     if (node >= nodes) return;
     int lg[3] = {0, 0, 0};
-    long long r = node;
-    for (int t = D - 1; t >= 0; --t) {
-        lg[t] = static_cast<int>(r % Lg);
-        r /= Lg;
+    {
+        int r = node;
+#pragma unroll
+        for (int t = D - 1; t >= 0; --t) {
+            lg[t] = r % Lg;
+            r /= Lg;
+        }
     }
-    // candidate (extended index, tile) pairs per dimension
     const int Eext = nt * TC + wn.S - 1;
-    int ce[3][16], ct[3][16], nc[3] = {0, 0, 0};
-    for (int t = 0; t < D; ++t) {
-        int e0 = wn.wrap ? pmod(lg[t] - wn.lo, wn.M) : lg[t];
-        for (int e = e0; e < Eext; e += (wn.wrap ? wn.M : Eext)) {
-            int tlo = (e - PE + 1 + TC - 1) / TC;  // ceil((e - PE + 1) / TC) for e - PE + 1 >= 0
-            if (e - PE + 1 < 0) tlo = 0;
-            const int thi = min(e / TC, nt - 1);
-            for (int T = tlo; T <= thi && nc[t] < 16; ++T) {
-                ce[t][nc[t]] = e;
-                ct[t][nc[t]] = T;
-                ++nc[t];
-            }
-        }
-    }
+    const int step = wn.wrap ? wn.M : Eext;
+    int e0s[3] = {0, 0, 0};
+#pragma unroll
+    for (int t = 0; t < D; ++t) e0s[t] = wn.wrap ? pmod(lg[t] - wn.lo, wn.M) : lg[t];
+    const double* pb = patches + wn.patch_base;
     double sum = 0.0;
-    if (D == 1) {
-        for (int i0 = 0; i0 < nc[0]; ++i0) {
-            const int T = ct[0][i0];
-            const int off = ce[0][i0] - T * TC;
-            for (int k = wn.tile_first[T]; k < wn.tile_first[T + 1]; ++k)
-                sum += patches[wn.patch_base + static_cast<long long>(k - wn.item_base) * PV + off];
-        }
-    } else if (D == 2) {
-        for (int i0 = 0; i0 < nc[0]; ++i0)
-            for (int i1 = 0; i1 < nc[1]; ++i1) {
-                const int T = ct[0][i0] * nt + ct[1][i1];
-                const int off = (ce[0][i0] - ct[0][i0] * TC) * PE + ce[1][i1] - ct[1][i1] * TC;
-                for (int k = wn.tile_first[T]; k < wn.tile_first[T + 1]; ++k)
-                    sum += patches[wn.patch_base + static_cast<long long>(k - wn.item_base) * PV + off];
+    // tiles covering extended index e: T in [max(0, ceil((e-PE+1)/TC)), min(e/TC, nt-1)]
+#define KSVM_TLO(e) ((e) - PE + 1 <= 0 ? 0 : ((e) - PE + TC) / TC)
+#define KSVM_THI(e) min((e) / TC, nt - 1)
+    for (int e0 = e0s[0]; e0 < Eext; e0 += step)
+        for (int T0 = KSVM_TLO(e0); T0 <= KSVM_THI(e0); ++T0) {
+            const int o0 = e0 - T0 * TC;
+            if constexpr (D == 1) {
+                for (int k = wn.tile_first[T0]; k < wn.tile_first[T0 + 1]; ++k)
+                    sum += pb[static_cast<long long>(k - wn.item_base) * PV + o0];
+            } else {
+                for (int e1 = e0s[1]; e1 < Eext; e1 += step)
+                    for (int T1 = KSVM_TLO(e1); T1 <= KSVM_THI(e1); ++T1) {
+                        const int o1 = o0 * PE + e1 - T1 * TC;
+                        if constexpr (D == 2) {
+                            const int T = T0 * nt + T1;
+                            for (int k = wn.tile_first[T]; k < wn.tile_first[T + 1]; ++k)
+                                sum += pb[static_cast<long long>(k - wn.item_base) * PV + o1];
+                        } else {
+                            for (int e2 = e0s[2]; e2 < Eext; e2 += step)
+                                for (int T2 = KSVM_TLO(e2); T2 <= KSVM_THI(e2); ++T2) {
+                                    const int T = (T0 * nt + T1) * nt + T2;
+                                    const int o2 = o1 * PE + e2 - T2 * TC;
+                                    for (int k = wn.tile_first[T]; k < wn.tile_first[T + 1]; ++k)
+                                        sum += pb[static_cast<long long>(k - wn.item_base) * PV + o2];
+                                }
+                        }
+                    }
             }
-    } else {
-        for (int i0 = 0; i0 < nc[0]; ++i0)
-            for (int i1 = 0; i1 < nc[1]; ++i1)
-                for (int i2 = 0; i2 < nc[2]; ++i2) {
-                    const int T = (ct[0][i0] * nt + ct[1][i1]) * nt + ct[2][i2];
-                    const int off = ((ce[0][i0] - ct[0][i0] * TC) * PE + ce[1][i1] - ct[1][i1] * TC) * PE +
-                                    ce[2][i2] - ct[2][i2] * TC;
-                    for (int k = wn.tile_first[T]; k < wn.tile_first[T + 1]; ++k)
-                        sum += patches[wn.patch_base + static_cast<long long>(k - wn.item_base) * PV + off];
-                }
-    }
+        }
+#undef KSVM_TLO
+#undef KSVM_THI
     wn.G[node] = sum;
 }
 
-// ---------------------------------------------------------------------------
+// ===========================================================================
 // Grid stage as a real separable convolution. With
 // z(r) = sum_{J in I_N} m1[J] e^{2 pi i J r / M} = a(r) + i s(r) the
-// reference's  Re( IFFT( mult . FFT(g) ) )  equals  sum_k' g(k') Re(prod_t z(k_t - k'_t)),
+// reference's  Re( IFFT( mult . FFT(g) ) )  equals  sum_k' g(k') Re(prod_t z(k_t - k'_t)):
 //   d=1: H = A g
 //   d=2: H = A0 (A1 g) - S0 (S1 g)
 //   d=3: H = A0 [A1 A2 g - S1 S2 g] - S0 [A1 S2 g + S1 A2 g]
-// stage s works along dimension d-1-s. blockIdx.y = window slot.
-// ---------------------------------------------------------------------------
-__global__ void conv_stage_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots,
-                                  int stage) {
+// Stage s works along dimension d-1-s as a small GEMM: a CTA owns 32
+// fibres (all Lg rows), stages them in SMEM, and each thread produces two
+// rows of one fibre. blockIdx.y = window slot.
+// ===========================================================================
+constexpr int kConvFB = 32;     // fibres per CTA
+constexpr int kConvRows = 8;    // row groups (warps) per CTA
+constexpr int kConvMaxL = 130;  // Lg bound for the SMEM tile
+
+__global__ void __launch_bounds__(kConvFB * kConvRows)
+conv_stage_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots, int stage) {
+    extern __shared__ __align__(16) double smem[];
     const DWin& wn = wins[slots[blockIdx.y]];
     const int D = wn.d, Lg = wn.Lg;
     if (stage >= D) return;
-    long long nodes = 1;
-    for (int t = 0; t < D; ++t) nodes *= Lg;
-    const long long node = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (node >= nodes) return;
     const int dim = D - 1 - stage;
-    long long stride = 1;
-    for (int t = dim + 1; t < D; ++t) stride *= Lg;
-    const int i = static_cast<int>((node / stride) % Lg);
-    const long long fb = node - static_cast<long long>(i) * stride;
-    const double* A = wn.tabA + (Lg - 1 + i);  // A[i][j] = A[-j]
-    const double* Sg = wn.tabS + (Lg - 1 + i);
-    if (stage == 0) {
-        const double* g = wn.G;
-        double ya = 0.0, ys = 0.0;
-        for (int j = 0; j < Lg; ++j) {
-            const double x = g[fb + j * stride];
-            ya = fma(A[-j], x, ya);
-            ys = fma(Sg[-j], x, ys);
-        }
-        if (D == 1) {
-            wn.H[node] = ya;
+    int nfib = 1;
+    for (int t = 0; t < D - 1; ++t) nfib *= Lg;
+    const int f0 = blockIdx.x * kConvFB;
+    if (f0 >= nfib) return;
+    int inner = 1;
+    for (int t = dim + 1; t < D; ++t) inner *= Lg;
+    const int nin = stage == 0 ? 1 : 2;
+    const double* in0 = stage == 0 ? wn.G : (stage == 1 ? wn.T[0] : (D == 3 ? wn.T[2] : wn.T[0]));
+    const double* in1 = stage == 0 ? nullptr : (stage == 1 ? wn.T[1] : (D == 3 ? wn.T[3] : wn.T[1]));
+    // SMEM: X[nin][Lg][kConvFB + 1], tabA[2Lg-1], tabS[2Lg-1]
+    const int ldx = kConvFB + 1;
+    double* X = smem;
+    double* tA = smem + 2 * Lg * ldx;
+    double* tS = tA + 2 * Lg - 1;
+    const int tid = threadIdx.y * kConvFB + threadIdx.x, nth = kConvFB * kConvRows;
+    for (int k = tid; k < 2 * Lg - 1; k += nth) {
+        tA[k] = wn.tabA[k];
+        tS[k] = wn.tabS[k];
+    }
+    // element (j, f) of the fibre set lives at addr(j, f)
+    auto addr = [&](int j, int f) -> long long {
+        if (dim == D - 1) return static_cast<long long>(f) * Lg + j;
+        const int outer = f / inner, in = f - outer * inner;
+        return (static_cast<long long>(outer) * Lg + j) * inner + in;
+    };
+    for (int q = 0; q < nin; ++q) {
+        const double* src = q == 0 ? in0 : in1;
+        if (dim == D - 1) {
+            for (int k = tid; k < kConvFB * Lg; k += nth) {
+                const int fl = k / Lg, j = k - fl * Lg;
+                X[(q * Lg + j) * ldx + fl] = f0 + fl < nfib ? src[addr(j, f0 + fl)] : 0.0;
+            }
         } else {
-            wn.T[0][node] = ya;
-            wn.T[1][node] = ys;
+            for (int k = tid; k < kConvFB * Lg; k += nth) {
+                const int j = k / kConvFB, fl = k - j * kConvFB;
+                X[(q * Lg + j) * ldx + fl] = f0 + fl < nfib ? src[addr(j, f0 + fl)] : 0.0;
+            }
         }
-    } else if (stage == 1 && D == 3) {
-        const double* ta = wn.T[0];
-        const double* ts = wn.T[1];
-        double p = 0.0, q = 0.0;
-        for (int j = 0; j < Lg; ++j) {
-            const double xa = ta[fb + j * stride], xs = ts[fb + j * stride];
-            const double aj = A[-j], sj = Sg[-j];
-            p = fma(aj, xa, fma(-sj, xs, p));
-            q = fma(aj, xs, fma(sj, xa, q));
+    }
+    __syncthreads();
+    const int fl = threadIdx.x, f = f0 + fl;
+    if (f >= nfib) return;
+    for (int i0 = threadIdx.y; i0 < Lg; i0 += 2 * kConvRows) {
+        const int i1 = i0 + kConvRows;
+        const bool two = i1 < Lg;
+        const double* A0 = tA + (Lg - 1 + i0);  // A[i][j] = tab[i - j]
+        const double* S0 = tS + (Lg - 1 + i0);
+        const double* A1 = tA + (Lg - 1 + (two ? i1 : i0));
+        const double* S1 = tS + (Lg - 1 + (two ? i1 : i0));
+        double p0 = 0.0, q0 = 0.0, p1 = 0.0, q1 = 0.0;
+        if (stage == 0) {
+            for (int j = 0; j < Lg; ++j) {
+                const double x = X[j * ldx + fl];
+                p0 = fma(A0[-j], x, p0);
+                q0 = fma(S0[-j], x, q0);
+                p1 = fma(A1[-j], x, p1);
+                q1 = fma(S1[-j], x, q1);
+            }
+        } else if (stage == 1 && D == 3) {
+            for (int j = 0; j < Lg; ++j) {
+                const double xa = X[j * ldx + fl], xs = X[(Lg + j) * ldx + fl];
+                p0 = fma(A0[-j], xa, fma(-S0[-j], xs, p0));
+                q0 = fma(A0[-j], xs, fma(S0[-j], xa, q0));
+                p1 = fma(A1[-j], xa, fma(-S1[-j], xs, p1));
+                q1 = fma(A1[-j], xs, fma(S1[-j], xa, q1));
+            }
+        } else {
+            for (int j = 0; j < Lg; ++j) {
+                const double xa = X[j * ldx + fl], xs = X[(Lg + j) * ldx + fl];
+                p0 = fma(A0[-j], xa, fma(-S0[-j], xs, p0));
+                p1 = fma(A1[-j], xa, fma(-S1[-j], xs, p1));
+            }
         }
-        wn.T[2][node] = p;
-        wn.T[3][node] = q;
-    } else {
-        const double* xa = D == 3 ? wn.T[2] : wn.T[0];
-        const double* xs = D == 3 ? wn.T[3] : wn.T[1];
-        double h = 0.0;
-        for (int j = 0; j < Lg; ++j) h = fma(A[-j], xa[fb + j * stride], fma(-Sg[-j], xs[fb + j * stride], h));
-        wn.H[node] = h;
+        double* o0;
+        double* o1;
+        if (stage == 0 && D == 1) {
+            o0 = wn.H;
+            o1 = nullptr;
+        } else if (stage == 0) {
+            o0 = wn.T[0];
+            o1 = wn.T[1];
+        } else if (stage == 1 && D == 3) {
+            o0 = wn.T[2];
+            o1 = wn.T[3];
+        } else {
+            o0 = wn.H;
+            o1 = nullptr;
+        }
+        o0[addr(i0, f)] = p0;
+        if (o1) o1[addr(i0, f)] = q0;
+        if (two) {
+            o0[addr(i1, f)] = p1;
+            if (o1) o1[addr(i1, f)] = q1;
+        }
     }
 }
 
@@ -649,7 +927,8 @@ __global__ void combine_kernel(double* __restrict__ y, const double* __restrict_
 
 // Exact kernel rows for the preconditioners (P:src/pipeline.cpp:103-105,
 // P:src/kernel.cpp:15-29): out[r, j] = sum_l w_l exp(-||x_p^l - x_j^l||^2 / ell_l^2)
-// over the listed windows (raw coordinates, SoA per feature).
+// over the listed windows (raw coordinates, SoA per feature); w_l < 0 marks
+// the single-window WindowOperator entry (plain exp, no weight).
 __global__ void kernel_rows_kernel(double* __restrict__ out, const long long* __restrict__ rows,
                                    const double* const* __restrict__ cols,
                                    const int* __restrict__ wdim, const double* __restrict__ wgt,
@@ -678,7 +957,7 @@ __global__ void fill_kernel(double* __restrict__ out, double val, long long n) {
         out[j] = val;
 }
 
-// ---- plan-time helpers ---------------------------------------------------
+// ---- plan-time kernels ----------------------------------------------------
 
 // Sort key of each point: tile-major, cell-within-tile minor.
 __global__ void cell_keys_kernel(const double* __restrict__ x0, const double* __restrict__ x1,
@@ -706,26 +985,53 @@ __global__ void cell_keys_kernel(const double* __restrict__ x0, const double* __
     }
 }
 
-__global__ void permute_kernel(double* __restrict__ dst, const double* __restrict__ src,
-                               const int* __restrict__ perm, long long n) {
+// Window factors of each sorted point (nfft_engine.cuh): P, Q_t, cell code.
+__global__ void factors_kernel(const double* __restrict__ x0, const double* __restrict__ x1,
+                               const double* __restrict__ x2, const int* __restrict__ perm, int d,
+                               long long n, double Mf, int m, double invb, double Cw, int cmin,
+                               int TC, double* __restrict__ P, double* __restrict__ Q0,
+                               double* __restrict__ Q1, double* __restrict__ Q2,
+                               int* __restrict__ code) {
     for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += static_cast<long long>(gridDim.x) * blockDim.x)
-        dst[i] = src[perm[i]];
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int src = perm[i];
+        const double* xs[3] = {x0, x1, x2};
+        double* Qs[3] = {Q0, Q1, Q2};
+        double su2 = 0.0, pre = 1.0;
+        int cd = 0;
+        for (int t = 0; t < d; ++t) {
+            const double xm = xs[t][src] * Mf;
+            const double fl = floor(xm);
+            const double u = (xm - fl) + static_cast<double>(m - 1);
+            su2 += u * u;
+            pre *= Cw;
+            Qs[t][i] = exp((2.0 * u) * invb);
+            cd = cd * TC + (static_cast<int>(fl) - cmin) % TC;
+        }
+        P[i] = pre * exp(-su2 * invb);
+        code[i] = cd;
+    }
 }
 
-// ---- launchers -----------------------------------------------------------
+// ---- launchers ------------------------------------------------------------
 
 constexpr int kW3 = 4;  // warps per CTA of the d=3, m=4 kernels
+constexpr int kW2 = 4;
+constexpr int kW1 = 8;
 
-size_t spread3_smem() { return sizeof(double) * (kW3 * 1331 + kW3 * 32 * kSt); }
-size_t gather3_smem() { return sizeof(double) * (1332 + kW3 * 32 * kSt); }
+size_t spread3_smem() { return sizeof(double) * (((kW3 * 1331 + 1) & ~1) + kW3 * 32 * Row<3, 8>::kLen); }
+size_t gather3_smem() { return sizeof(double) * (1332 + kW3 * 32 * Row<3, 8>::kLen); }
+size_t spread2_smem() { return sizeof(double) * (((kW2 * 225 + 1) & ~1) + kW2 * 32 * Row<2, 8>::kLen); }
+size_t gather2_smem() { return sizeof(double) * (226 + kW2 * 32 * Row<2, 8>::kLen); }
+size_t spread1_smem() { return sizeof(double) * (kW1 * 39 * 32); }
+size_t gather1_smem() { return sizeof(double) * 40; }
 
 int generic_warps(int D, int PE, bool spread) {
     int PV = 1;
     for (int t = 0; t < D; ++t) PV *= PE;
     const size_t budget = 200 * 1024;
-    const size_t stage = sizeof(double) * 32 * kStageG;
-    const size_t patch = sizeof(double) * PV;
+    const size_t stage = sizeof(double) * 32 * kRowG;
+    const size_t patch = sizeof(double) * (PV + 2);
     int W = 8;
     while (W > 1 && (spread ? W * (patch + stage) : patch + W * stage) > budget) --W;
     return W;
@@ -734,34 +1040,45 @@ int generic_warps(int D, int PE, bool spread) {
 size_t generic_smem(int D, int PE, int W, bool spread) {
     int PV = 1;
     for (int t = 0; t < D; ++t) PV *= PE;
-    return sizeof(double) * ((spread ? W : 1) * PV + W * 32 * kStageG);
+    return sizeof(double) * ((((spread ? W : 1) * PV + 1) & ~1) + W * 32 * kRowG);
 }
 
+size_t conv_smem(int Lg) { return sizeof(double) * (2 * Lg * (kConvFB + 1) + 2 * (2 * Lg - 1)); }
+
 cudaError_t init_kernel_attributes() {
-    cudaError_t e = cudaFuncSetAttribute(spread3_s8_kernel<kW3>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(spread3_smem()));
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(gather3_s8_kernel<kW3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(gather3_smem()));
-    if (e != cudaSuccess) return e;
-    const int big = 227 * 1024;
-    cudaFuncSetAttribute(spread_generic_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(spread_generic_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(spread_generic_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(gather_generic_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(gather_generic_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    return cudaFuncSetAttribute(gather_generic_kernel<3>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaError_t e = cudaSuccess;
+    auto set = [&](const void* f, size_t bytes) {
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+    };
+    set(reinterpret_cast<const void*>(spread3_s8_kernel<kW3>), spread3_smem());
+    set(reinterpret_cast<const void*>(gather3_s8_kernel<kW3>), gather3_smem());
+    set(reinterpret_cast<const void*>(spread2_s8_kernel<kW2>), spread2_smem());
+    set(reinterpret_cast<const void*>(gather2_s8_kernel<kW2>), gather2_smem());
+    set(reinterpret_cast<const void*>(spread1_s8_kernel<kW1>), spread1_smem());
+    const size_t big = 227 * 1024;
+    set(reinterpret_cast<const void*>(spread_generic_kernel<1>), big);
+    set(reinterpret_cast<const void*>(spread_generic_kernel<2>), big);
+    set(reinterpret_cast<const void*>(spread_generic_kernel<3>), big);
+    set(reinterpret_cast<const void*>(gather_generic_kernel<1>), big);
+    set(reinterpret_cast<const void*>(gather_generic_kernel<2>), big);
+    set(reinterpret_cast<const void*>(gather_generic_kernel<3>), big);
+    set(reinterpret_cast<const void*>(conv_stage_kernel), conv_smem(kConvMaxL));
+    return e;
 }
 
 // Launch spread over `nitems` items whose windows all have dimension D and
-// span S (fast path for D = 3, S = 8).
+// span S (specialised kernels for S = 8, i.e. m = 4).
 void launch_spread(int D, int S, int PE, const Item* items, int nitems, const DPSet* ps,
                    const DWin* wins, const double* v, double* patches, cudaStream_t st) {
     if (nitems == 0) return;
-    if (D == 3 && S == 8) {
-        spread3_s8_kernel<kW3><<<nitems, kW3 * 32, spread3_smem(), st>>>(items, ps, wins, v, patches);
+    if (S == 8) {
+        if (D == 3)
+            spread3_s8_kernel<kW3><<<nitems, kW3 * 32, spread3_smem(), st>>>(items, ps, wins, v, patches);
+        else if (D == 2)
+            spread2_s8_kernel<kW2><<<nitems, kW2 * 32, spread2_smem(), st>>>(items, ps, wins, v, patches);
+        else
+            spread1_s8_kernel<kW1><<<nitems, kW1 * 32, spread1_smem(), st>>>(items, ps, wins, v, patches);
         return;
     }
     const int W = generic_warps(D, PE, true);
@@ -774,8 +1091,10 @@ void launch_spread(int D, int S, int PE, const Item* items, int nitems, const DP
 void launch_gather(int D, int S, int PE, const Item* items, int nitems, const DPSet* ps,
                    const DWin* wins, cudaStream_t st) {
     if (nitems == 0) return;
-    if (D == 3 && S == 8) {
-        gather3_s8_kernel<kW3><<<nitems, kW3 * 32, gather3_smem(), st>>>(items, ps, wins);
+    if (S == 8) {
+        if (D == 3) gather3_s8_kernel<kW3><<<nitems, kW3 * 32, gather3_smem(), st>>>(items, ps, wins);
+        else if (D == 2) gather2_s8_kernel<kW2><<<nitems, kW2 * 32, gather2_smem(), st>>>(items, ps, wins);
+        else gather1_s8_kernel<kW1><<<nitems, kW1 * 32, gather1_smem(), st>>>(items, ps, wins);
         return;
     }
     const int W = generic_warps(D, PE, false);
@@ -785,19 +1104,23 @@ void launch_gather(int D, int S, int PE, const Item* items, int nitems, const DP
     else gather_generic_kernel<3><<<nitems, W * 32, sm, st>>>(items, ps, wins, W);
 }
 
-void launch_reduce(const DWin* wins, const int* slots, int nslots, long long max_nodes,
+void launch_reduce(const DWin* wins, const int* slots, int nslots, long long max_nodes, int D,
                    const double* patches, cudaStream_t st) {
     if (nslots == 0) return;
     dim3 grid(static_cast<unsigned>((max_nodes + 255) / 256), nslots);
-    reduce_patches_kernel<<<grid, 256, 0, st>>>(wins, slots, patches);
+    if (D == 1) reduce_patches_kernel<1><<<grid, 256, 0, st>>>(wins, slots, patches);
+    else if (D == 2) reduce_patches_kernel<2><<<grid, 256, 0, st>>>(wins, slots, patches);
+    else reduce_patches_kernel<3><<<grid, 256, 0, st>>>(wins, slots, patches);
 }
 
-void launch_conv(const DWin* wins, const int* slots, int nslots, long long max_nodes, int stage,
-                 cudaStream_t st) {
+void launch_conv(const DWin* wins, const int* slots, int nslots, int Lg_max, long long max_fibres,
+                 int stage, cudaStream_t st) {
     if (nslots == 0) return;
-    dim3 grid(static_cast<unsigned>((max_nodes + 255) / 256), nslots);
-    conv_stage_kernel<<<grid, 256, 0, st>>>(wins, slots, stage);
+    dim3 grid(static_cast<unsigned>((max_fibres + kConvFB - 1) / kConvFB), nslots);
+    conv_stage_kernel<<<grid, dim3(kConvFB, kConvRows), conv_smem(Lg_max), st>>>(wins, slots, stage);
 }
+
+int conv_max_lg() { return kConvMaxL; }
 
 void launch_combine(double* y, const double* parts, const double* eta, int P, long long n,
                     cudaStream_t st) {
@@ -825,9 +1148,12 @@ void launch_cell_keys(const double* x0, const double* x1, const double* x2, int 
                                                                TC, ntile, keys, idx, bad);
 }
 
-void launch_permute(double* dst, const double* src, const int* perm, long long n, cudaStream_t st) {
+void launch_factors(const double* x0, const double* x1, const double* x2, const int* perm, int d,
+                    long long n, double Mf, int m, double invb, double Cw, int cmin, int TC,
+                    double* P, double* Q0, double* Q1, double* Q2, int* code, cudaStream_t st) {
     const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 16));
-    permute_kernel<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(dst, src, perm, n);
+    factors_kernel<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(x0, x1, x2, perm, d, n, Mf, m, invb, Cw,
+                                                             cmin, TC, P, Q0, Q1, Q2, code);
 }
 
 }  // namespace ksvm_nfft
