@@ -90,123 +90,6 @@ struct Pref {
 
 }  // namespace
 
-// ===========================================================================
-// d = 3, m = 4 (S = 8): register-blocked per cell.
-// Lane L owns the 16 taps (a, b0..b0+1, 0..7) of the cell's 8^3 block with
-// a = L/4, b0 = 2 (L%4). Points are sorted by cell, so a run of 4 whose first
-// and last share a cell is one cell: that fast path has no branches and 16
-// independent FMA chains.
-// ===========================================================================
-template <int W>
-__global__ void __launch_bounds__(W * 32)
-spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
-                  const DWin* __restrict__ wins, const double* __restrict__ v,
-                  double* __restrict__ patches) {
-    constexpr int D = 3, S = 8, TC = 4, PE = TC + S - 1, PV = PE * PE * PE, RL = Row<D, S>::kLen;
-    extern __shared__ __align__(16) double smem[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double* wp = smem + warp * PV;
-    double* stage = smem + ((W * PV + 1) & ~1) + warp * 32 * RL;
-
-    const Item it = items[blockIdx.x];
-    const DPSet& ps = psets[it.ps];
-    const DWin& wn = wins[ps.win];
-    double R[S];
-#pragma unroll
-    for (int o = 0; o < S; ++o) R[o] = wn.R[o];
-    for (int k = lane; k < PV; k += 32) wp[k] = 0.0;
-    int wb, we;
-    warp_range(it, warp, W, &wb, &we);
-    const int a = lane >> 2, b0 = (lane & 3) << 1;
-
-    double acc0[S], acc1[S];
-#pragma unroll
-    for (int c = 0; c < S; ++c) acc0[c] = acc1[c] = 0.0;
-    int cur = -1;
-
-    auto flush = [&](int cell) {
-        const int l0 = cell >> 4, l1 = (cell >> 2) & 3, l2 = cell & 3;
-        double* dst = wp + ((l0 + a) * PE + l1 + b0) * PE + l2;
-#pragma unroll
-        for (int c = 0; c < S; ++c) {
-            dst[c] += acc0[c];
-            dst[PE + c] += acc1[c];
-            acc0[c] = 0.0;
-            acc1[c] = 0.0;
-        }
-    };
-    auto accumulate = [&](const double* st) {
-        const double w0a = st[a];
-        const double2 w1 = ld2(st + S + b0);
-        const double u0 = w0a * w1.x, u1 = w0a * w1.y;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const double2 w2 = ld2(st + 2 * S + 2 * k);
-            acc0[2 * k] = fma(u0, w2.x, acc0[2 * k]);
-            acc0[2 * k + 1] = fma(u0, w2.y, acc0[2 * k + 1]);
-            acc1[2 * k] = fma(u1, w2.x, acc1[2 * k]);
-            acc1[2 * k + 1] = fma(u1, w2.y, acc1[2 * k + 1]);
-        }
-    };
-
-    // two-deep software pipeline: perm two batches ahead, factors and v one ahead
-    Pref<D> pf;
-    int perm1 = 0, perm2 = 0;
-    double vnext = 0.0;
-    {
-        const int i0 = wb + lane, i1 = wb + 32 + lane;
-        if (i0 < we) {
-            pf.load(ps, i0);
-            vnext = v[ps.perm[i0]];
-        }
-        if (i1 < we) perm1 = ps.perm[i1];
-    }
-    __syncwarp();
-    for (int base = wb; base < we; base += 32) {
-        const int cnt = min(32, we - base);
-        if (lane < cnt) stage_row<D, S>(stage + lane * RL, R, pf.P * vnext, pf.Q, pf.code);
-        {
-            const int i1 = base + 32 + lane, i2 = base + 64 + lane;
-            if (i2 < we) perm2 = ps.perm[i2];
-            if (i1 < we) {
-                pf.load(ps, i1);
-                vnext = v[perm1];
-            }
-            perm1 = perm2;
-        }
-        __syncwarp();
-        int p = 0;
-        while (p < cnt) {
-            const double* st = stage + p * RL;
-            const int cp = row_code(st, D, S);
-            if (cp != cur) {
-                if (cur >= 0) flush(cur);
-                cur = cp;
-            }
-            if (p + 3 < cnt && row_code(st + 3 * RL, D, S) == cp) {
-                accumulate(st);
-                accumulate(st + RL);
-                accumulate(st + 2 * RL);
-                accumulate(st + 3 * RL);
-                p += 4;
-            } else {
-                accumulate(st);
-                p += 1;
-            }
-        }
-        __syncwarp();
-    }
-    if (cur >= 0) flush(cur);
-    __syncthreads();
-    double* out = patches + it.patch;
-    for (int k = threadIdx.x; k < PV; k += W * 32) {
-        double s = smem[k];
-#pragma unroll
-        for (int q = 1; q < W; ++q) s += smem[q * PV + k];
-        out[k] = s;
-    }
-}
-
 // Load the (TC+S-1)^d grid halo of a tile into SMEM (wrap / bounds aware).
 template <int D>
 __device__ __forceinline__ void load_halo(double* halo, const DWin& wn, const int* tc, int TC, int PE,
@@ -248,6 +131,131 @@ __device__ __forceinline__ double butterfly32(double (&pp)[32], int lane) {
     return pp[0];
 }
 
+// One FP64 tensor-core MMA, D(8x8) += A(8x4) B(4x8) (SASS DMMA.8x8x4). Lane
+// l = 4g + t holds A[g][t], B[t][g] and D[g][2t], D[g][2t+1].
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+        : "+d"(d0), "+d"(d1)
+        : "d"(a), "d"(b));
+}
+
+// ===========================================================================
+// d = 3, m = 4 (S = 8) on the FP64 tensor cores.
+// The 8^3 block of one cell is G[(a,b), c] with a, b, c in 0..7. Spread adds
+// sum_p U[(a,b), p] W2[p, c] with U = (v P w0[a]) w1[b]: eight 8x8 tiles
+// (one per a), K = 4 points of the cell per DMMA. Points are sorted by cell;
+// a group is the run of <= 4 consecutive points in the current cell (the
+// rest of the group is masked to zero and handled next round).
+// Lane l = 4g + t: A[g][t] = U[(r, g), point t], B[t][g] = W2[point t][g],
+// accumulator tile r holds G[(r, g), 2t..2t+1].
+// ===========================================================================
+template <int W>
+__global__ void __launch_bounds__(W * 32)
+spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
+                  const DWin* __restrict__ wins, const double* __restrict__ v,
+                  double* __restrict__ patches) {
+    constexpr int D = 3, S = 8, PE = 11, PV = PE * PE * PE, RL = Row<D, S>::kLen;
+    extern __shared__ __align__(16) double smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    double* wp = smem + warp * PV;
+    double* stage = smem + ((W * PV + 1) & ~1) + warp * 32 * RL;
+
+    const Item it = items[blockIdx.x];
+    const DPSet& ps = psets[it.ps];
+    const DWin& wn = wins[ps.win];
+    double R[S];
+#pragma unroll
+    for (int o = 0; o < S; ++o) R[o] = wn.R[o];
+    for (int k = lane; k < PV; k += 32) wp[k] = 0.0;
+    int wb, we;
+    warp_range(it, warp, W, &wb, &we);
+
+    double acc[8][2];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) acc[r][0] = acc[r][1] = 0.0;
+    int cur = -1;
+    auto flush = [&](int cell) {
+        const int l0 = cell >> 4, l1 = (cell >> 2) & 3, l2 = cell & 3;
+        double* dst = wp + (l0 * PE + l1 + g) * PE + l2 + 2 * t;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            dst[r * PE * PE] += acc[r][0];
+            dst[r * PE * PE + 1] += acc[r][1];
+            acc[r][0] = acc[r][1] = 0.0;
+        }
+    };
+
+    Pref<D> pf;
+    int perm1 = 0, perm2 = 0;
+    double vnext = 0.0;
+    {
+        const int i0 = wb + lane, i1 = wb + 32 + lane;
+        if (i0 < we) {
+            pf.load(ps, i0);
+            vnext = v[ps.perm[i0]];
+        }
+        if (i1 < we) perm1 = ps.perm[i1];
+    }
+    __syncwarp();
+    for (int base = wb; base < we; base += 32) {
+        const int cnt = min(32, we - base);
+        if (lane < cnt) stage_row<D, S>(stage + lane * RL, R, pf.P * vnext, pf.Q, pf.code);
+        {
+            const int i1 = base + 32 + lane, i2 = base + 64 + lane;
+            if (i2 < we) perm2 = ps.perm[i2];
+            if (i1 < we) {
+                pf.load(ps, i1);
+                vnext = v[perm1];
+            }
+            perm1 = perm2;
+        }
+        __syncwarp();
+        int p = 0;
+        while (p < cnt) {
+            const int cp = row_code(stage + p * RL, D, S);
+            if (cp != cur) {
+                if (cur >= 0) flush(cur);
+                cur = cp;
+            }
+            const int q = p + t;
+            const bool valid = q < cnt && row_code(stage + q * RL, D, S) == cur;
+            const int nvalid = __popc(__ballot_sync(0xffffffffu, valid) & 0xFu);
+            const double* st = stage + (valid ? q : p) * RL;
+            const double w1g = valid ? st[S + g] : 0.0;
+            const double b = valid ? st[2 * S + g] : 0.0;
+            const double2 w01 = ld2(st), w23 = ld2(st + 2), w45 = ld2(st + 4), w67 = ld2(st + 6);
+            dmma(acc[0][0], acc[0][1], w01.x * w1g, b);
+            dmma(acc[1][0], acc[1][1], w01.y * w1g, b);
+            dmma(acc[2][0], acc[2][1], w23.x * w1g, b);
+            dmma(acc[3][0], acc[3][1], w23.y * w1g, b);
+            dmma(acc[4][0], acc[4][1], w45.x * w1g, b);
+            dmma(acc[5][0], acc[5][1], w45.y * w1g, b);
+            dmma(acc[6][0], acc[6][1], w67.x * w1g, b);
+            dmma(acc[7][0], acc[7][1], w67.y * w1g, b);
+            p += nvalid;
+        }
+        __syncwarp();
+    }
+    if (cur >= 0) flush(cur);
+    __syncthreads();
+    double* out = patches + it.patch;
+    for (int k = threadIdx.x; k < PV; k += W * 32) {
+        double s = smem[k];
+#pragma unroll
+        for (int q = 1; q < W; ++q) s += smem[q * PV + k];
+        out[k] = s;
+    }
+}
+
+// ===========================================================================
+// Gather, d = 3, m = 4, on the FP64 tensor cores:
+//   T[(a,b), p] = sum_c H[(a,b), c] W2[p, c]      (8 tiles x 2 k-steps, N = 8 points)
+//   y_p = sum_a w0_p[a] P sum_b w1_p[b] T[(a,b), p]   (per-point epilogue)
+// Lane l = 4g + t holds A[g][t] = H[(r, g), t + 4k] (reloaded per cell),
+// B[t][g] = W2[point g][t + 4k], and T[(r, g), points 2t, 2t+1]; the b-sum
+// is an xor-butterfly over g (fixed order).
+// ===========================================================================
 template <int W>
 __global__ void __launch_bounds__(W * 32)
 gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
@@ -255,6 +263,7 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     constexpr int D = 3, S = 8, TC = 4, PE = TC + S - 1, PV = PE * PE * PE, RL = Row<D, S>::kLen;
     extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
     double* halo = smem;
     double* stage = smem + ((PV + 1) & ~1) + warp * 32 * RL;
 
@@ -270,46 +279,34 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
     Pref<D> pf;
-    int permc = 0, permn = 0;
+    int permn = 0;
     if (wb + lane < we) {
         pf.load(ps, wb + lane);
         permn = ps.perm[wb + lane];
     }
     __syncthreads();
 
-    const int a = lane >> 2, b0 = (lane & 3) << 1;
-    double h0[S], h1[S];
+    double h[8][2];
 #pragma unroll
-    for (int c = 0; c < S; ++c) h0[c] = h1[c] = 0.0;
+    for (int r = 0; r < 8; ++r) h[r][0] = h[r][1] = 0.0;
     int cur = -1;
-
     auto reload = [&](int cell) {
         const int l0 = cell >> 4, l1 = (cell >> 2) & 3, l2 = cell & 3;
-        const double* src = halo + ((l0 + a) * PE + l1 + b0) * PE + l2;
+        const double* src = halo + (l0 * PE + l1 + g) * PE + l2 + t;
 #pragma unroll
-        for (int c = 0; c < S; ++c) {
-            h0[c] = src[c];
-            h1[c] = src[PE + c];
+        for (int r = 0; r < 8; ++r) {
+            h[r][0] = src[r * PE * PE];
+            h[r][1] = src[r * PE * PE + 4];
         }
-    };
-    auto partial = [&](const double* st) {
-        double e0 = 0.0, o0 = 0.0, e1 = 0.0, o1 = 0.0;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const double2 w2 = ld2(st + 2 * S + 2 * k);
-            e0 = fma(h0[2 * k], w2.x, e0);
-            o0 = fma(h0[2 * k + 1], w2.y, o0);
-            e1 = fma(h1[2 * k], w2.x, e1);
-            o1 = fma(h1[2 * k + 1], w2.y, o1);
-        }
-        const double2 w1 = ld2(st + S + b0);
-        return st[a] * fma(w1.x, e0 + o0, w1.y * (e1 + o1));
     };
 
     for (int base = wb; base < we; base += 32) {
         const int cnt = min(32, we - base);
-        if (lane < cnt) stage_row<D, S>(stage + lane * RL, R, pf.P, pf.Q, pf.code);
-        permc = permn;
+        if (lane < cnt) {
+            double* st = stage + lane * RL;
+            stage_row<D, S>(st, R, pf.P, pf.Q, pf.code);
+            reinterpret_cast<int*>(st + D * S)[1] = permn;
+        }
         {
             const int i1 = base + 32 + lane;
             if (i1 < we) {
@@ -318,38 +315,55 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
             }
         }
         __syncwarp();
-        double pp[32];
+        int p = 0;
+        while (p < cnt) {
+            const int cp = row_code(stage + p * RL, D, S);
+            if (cp != cur) {
+                cur = cp;
+                reload(cp);
+            }
+            const int qg = p + g;
+            const bool vg = qg < cnt && row_code(stage + qg * RL, D, S) == cur;
+            const int nvalid = __popc(__ballot_sync(0xffffffffu, vg) & 0x11111111u);
+            const double* sg = stage + (vg ? qg : p) * RL + 2 * S;
+            const double b0 = vg ? sg[t] : 0.0, b1 = vg ? sg[t + 4] : 0.0;
+            double T[8][2];
 #pragma unroll
-        for (int g = 0; g < 8; ++g) {
-            const int p0 = 4 * g;
-            const double* st = stage + p0 * RL;
-            if (p0 + 3 < cnt && row_code(st, D, S) == row_code(st + 3 * RL, D, S)) {
-                const int cp = row_code(st, D, S);
-                if (cp != cur) {
-                    cur = cp;
-                    reload(cp);
-                }
-                pp[p0] = partial(st);
-                pp[p0 + 1] = partial(st + RL);
-                pp[p0 + 2] = partial(st + 2 * RL);
-                pp[p0 + 3] = partial(st + 3 * RL);
-            } else {
+            for (int r = 0; r < 8; ++r) {
+                T[r][0] = T[r][1] = 0.0;
+                dmma(T[r][0], T[r][1], h[r][0], b0);
+                dmma(T[r][0], T[r][1], h[r][1], b1);
+            }
+            double part[2];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    pp[p0 + q] = 0.0;
-                    if (p0 + q < cnt) {
-                        const int cp = row_code(st + q * RL, D, S);
-                        if (cp != cur) {
-                            cur = cp;
-                            reload(cp);
-                        }
-                        pp[p0 + q] = partial(st + q * RL);
-                    }
+            for (int e = 0; e < 2; ++e) {
+                const int j = 2 * t + e;
+                const bool ok = j < nvalid;
+                const double* st = stage + (ok ? p + j : p) * RL;
+                const double2 w01 = ld2(st), w23 = ld2(st + 2), w45 = ld2(st + 4), w67 = ld2(st + 6);
+                double s0 = w01.x * T[0][e], s1 = w01.y * T[1][e];
+                s0 = fma(w23.x, T[2][e], s0);
+                s1 = fma(w23.y, T[3][e], s1);
+                s0 = fma(w45.x, T[4][e], s0);
+                s1 = fma(w45.y, T[5][e], s1);
+                s0 = fma(w67.x, T[6][e], s0);
+                s1 = fma(w67.y, T[7][e], s1);
+                part[e] = ok ? st[S + g] * (s0 + s1) : 0.0;
+            }
+#pragma unroll
+            for (int m = 4; m <= 16; m <<= 1) {
+                part[0] += __shfl_xor_sync(0xffffffffu, part[0], m);
+                part[1] += __shfl_xor_sync(0xffffffffu, part[1], m);
+            }
+            if (g == 0) {
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int j = 2 * t + e;
+                    if (j < nvalid) ps.out[reinterpret_cast<const int*>(stage + (p + j) * RL + D * S)[1]] = part[e];
                 }
             }
+            p += nvalid;
         }
-        const double val = butterfly32(pp, lane);
-        if (lane < cnt) ps.out[permc] = val;
         __syncwarp();
     }
 }
