@@ -81,10 +81,10 @@ struct Pref {
     double P = 0.0, Q[3] = {0.0, 0.0, 0.0};
     int code = 0;
     __device__ __forceinline__ void load(const DPSet& ps, int i) {
-        P = ps.P[i];
+        P = __ldg(ps.P + i);
 #pragma unroll
-        for (int t = 0; t < D; ++t) Q[t] = ps.Q[t][i];
-        code = ps.code[i];
+        for (int t = 0; t < D; ++t) Q[t] = __ldg(ps.Q[t] + i);
+        code = __ldg(ps.code + i);
     }
 };
 
@@ -162,7 +162,7 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     double* stage = smem + ((W * PV + 1) & ~1) + warp * 32 * RL;
 
     const Item it = items[blockIdx.x];
-    const DPSet& ps = psets[it.ps];
+    const DPSet ps = psets[it.ps];
     const DWin& wn = wins[ps.win];
     double R[S];
 #pragma unroll
@@ -193,9 +193,9 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
         const int i0 = wb + lane, i1 = wb + 32 + lane;
         if (i0 < we) {
             pf.load(ps, i0);
-            vnext = v[ps.perm[i0]];
+            vnext = __ldg(v + __ldg(ps.perm + i0));
         }
-        if (i1 < we) perm1 = ps.perm[i1];
+        if (i1 < we) perm1 = __ldg(ps.perm + i1);
     }
     __syncwarp();
     for (int base = wb; base < we; base += 32) {
@@ -203,10 +203,10 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
         if (lane < cnt) stage_row<D, S>(stage + lane * RL, R, pf.P * vnext, pf.Q, pf.code);
         {
             const int i1 = base + 32 + lane, i2 = base + 64 + lane;
-            if (i2 < we) perm2 = ps.perm[i2];
+            if (i2 < we) perm2 = __ldg(ps.perm + i2);
             if (i1 < we) {
                 pf.load(ps, i1);
-                vnext = v[perm1];
+                vnext = __ldg(v + perm1);
             }
             perm1 = perm2;
         }
@@ -268,7 +268,7 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     double* stage = smem + ((PV + 1) & ~1) + warp * 32 * RL;
 
     const Item it = items[blockIdx.x];
-    const DPSet& ps = psets[it.ps];
+    const DPSet ps = psets[it.ps];
     const DWin& wn = wins[ps.win];
     double R[S];
 #pragma unroll
@@ -282,7 +282,7 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     int permn = 0;
     if (wb + lane < we) {
         pf.load(ps, wb + lane);
-        permn = ps.perm[wb + lane];
+        permn = __ldg(ps.perm + wb + lane);
     }
     __syncthreads();
 
@@ -311,7 +311,7 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
             const int i1 = base + 32 + lane;
             if (i1 < we) {
                 pf.load(ps, i1);
-                permn = ps.perm[i1];
+                permn = __ldg(ps.perm + i1);
             }
         }
         __syncwarp();
@@ -382,7 +382,7 @@ spread2_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     double* wp = smem + warp * PV;
     double* stage = smem + ((W * PV + 1) & ~1) + warp * 32 * RL;
     const Item it = items[blockIdx.x];
-    const DPSet& ps = psets[it.ps];
+    const DPSet ps = psets[it.ps];
     const DWin& wn = wins[ps.win];
     double R[S];
 #pragma unroll
@@ -406,9 +406,9 @@ spread2_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
         const int i0 = wb + lane, i1 = wb + 32 + lane;
         if (i0 < we) {
             pf.load(ps, i0);
-            vnext = v[ps.perm[i0]];
+            vnext = __ldg(v + __ldg(ps.perm + i0));
         }
-        if (i1 < we) perm1 = ps.perm[i1];
+        if (i1 < we) perm1 = __ldg(ps.perm + i1);
     }
     __syncwarp();
     for (int base = wb; base < we; base += 32) {
@@ -416,10 +416,10 @@ spread2_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
         if (lane < cnt) stage_row<D, S>(stage + lane * RL, R, pf.P * vnext, pf.Q, pf.code);
         {
             const int i1 = base + 32 + lane, i2 = base + 64 + lane;
-            if (i2 < we) perm2 = ps.perm[i2];
+            if (i2 < we) perm2 = __ldg(ps.perm + i2);
             if (i1 < we) {
                 pf.load(ps, i1);
-                vnext = v[perm1];
+                vnext = __ldg(v + perm1);
             }
             perm1 = perm2;
         }
@@ -459,7 +459,7 @@ gather2_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     double* halo = smem;
     double* stage = smem + ((PV + 1) & ~1) + warp * 32 * RL;
     const Item it = items[blockIdx.x];
-    const DPSet& ps = psets[it.ps];
+    const DPSet ps = psets[it.ps];
     const DWin& wn = wins[ps.win];
     double R[S];
 #pragma unroll
@@ -473,7 +473,7 @@ gather2_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     int permc = 0, permn = 0;
     if (wb + lane < we) {
         pf.load(ps, wb + lane);
-        permn = ps.perm[wb + lane];
+        permn = __ldg(ps.perm + wb + lane);
     }
     __syncthreads();
     const int a = lane >> 2, b0 = (lane & 3) << 1;
@@ -487,7 +487,7 @@ gather2_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
             const int i1 = base + 32 + lane;
             if (i1 < we) {
                 pf.load(ps, i1);
-                permn = ps.perm[i1];
+                permn = __ldg(ps.perm + i1);
             }
         }
         __syncwarp();
@@ -529,7 +529,7 @@ spread1_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double* lp = smem + warp * PE * 32;
     const Item it = items[blockIdx.x];
-    const DPSet& ps = psets[it.ps];
+    const DPSet ps = psets[it.ps];
     const DWin& wn = wins[ps.win];
     double R[S];
 #pragma unroll
@@ -566,7 +566,7 @@ gather1_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const Item it = items[blockIdx.x];
-    const DPSet& ps = psets[it.ps];
+    const DPSet ps = psets[it.ps];
     const DWin& wn = wins[ps.win];
     double R[S];
 #pragma unroll
@@ -606,7 +606,7 @@ __global__ void spread_generic_kernel(const Item* __restrict__ items,
     extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const Item it = items[blockIdx.x];
-    const DPSet& ps = psets[it.ps];
+    const DPSet ps = psets[it.ps];
     const DWin& wn = wins[ps.win];
     const int S = wn.S, TC = wn.TC, PE = wn.PE;
     int PV = 1, taps = 1;
@@ -677,7 +677,7 @@ __global__ void gather_generic_kernel(const Item* __restrict__ items,
     extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const Item it = items[blockIdx.x];
-    const DPSet& ps = psets[it.ps];
+    const DPSet ps = psets[it.ps];
     const DWin& wn = wins[ps.win];
     const int S = wn.S, TC = wn.TC, PE = wn.PE;
     int PV = 1, taps = 1;
