@@ -47,7 +47,7 @@ void launch_cell_keys(const double* x0, const double* x1, const double* x2, int 
                       int* bad, cudaStream_t st);
 void launch_factors(const double* x0, const double* x1, const double* x2, const int* perm, int d,
                     long long n, double Mf, int m, double invb, double Cw, int cmin, int TC,
-                    double* P, double* Q0, double* Q1, double* Q2, int* code, cudaStream_t st);
+                    double4* F, int2* CP, cudaStream_t st);
 
 namespace {
 
@@ -191,8 +191,8 @@ Spectral1D spectral_1d(int N, int M, double bwin, double ell_s) {
 struct PointSet {
     int64_t n = 0;
     int d = 0;
-    DevBuf<double> P, Q[3];  // window factors, sorted order (nfft_engine.cuh)
-    DevBuf<int> code;        // tile-local cell code
+    DevBuf<double4> F;  // window factors {P, Q0, Q1, Q2}, sorted order (nfft_engine.cuh)
+    DevBuf<int2> CP;    // {tile-local cell code, original index}
     DevBuf<int> perm;
     std::vector<Item> items;      // host copy (global numbering assigned later)
     std::vector<int> tile_first;  // local item index of each tile's first item
@@ -276,12 +276,10 @@ void build_pointset(PointSet& ps, const std::vector<double>& scaled_cm, int64_t 
     tmp.alloc(tmp_bytes);
     CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, keys_in.p, keys_out.p, idx_in.p,
                                        ps.perm.p, static_cast<int>(n), 0, bits, st));
-    ps.P.alloc(n);
-    for (int t = 0; t < d; ++t) ps.Q[t].alloc(n);
-    ps.code.alloc(n);
+    ps.F.alloc(n);
+    ps.CP.alloc(n);
     launch_factors(raw[0].p, d > 1 ? raw[1].p : nullptr, d > 2 ? raw[2].p : nullptr, ps.perm.p, d, n,
-                   static_cast<double>(g.M), g.m, g.invb, g.Cw, g.cmin, g.TC, ps.P.p, ps.Q[0].p,
-                   d > 1 ? ps.Q[1].p : nullptr, d > 2 ? ps.Q[2].p : nullptr, ps.code.p, st);
+                   static_cast<double>(g.M), g.m, g.invb, g.Cw, g.cmin, g.TC, ps.F.p, ps.CP.p, st);
     CK(cudaGetLastError());
     std::vector<unsigned> hk(static_cast<size_t>(n));
     int hbad = 0;
@@ -538,10 +536,8 @@ struct Engine {
             eta[static_cast<size_t>(s)] = w.eta;
             slots[static_cast<size_t>(s)] = s;
             DPSet& p = ps[static_cast<size_t>(s)];
-            p.P = w.src.P.p;
-            for (int t = 0; t < 3; ++t) p.Q[t] = t < w.d ? w.src.Q[t].p : nullptr;
-            p.code = w.src.code.p;
-            p.perm = w.src.perm.p;
+            p.F = w.src.F.p;
+            p.CP = w.src.CP.p;
             p.n = n;
             p.win = s;
             p.out = parts.p + static_cast<size_t>(s) * n;
@@ -1007,10 +1003,8 @@ int ksvm_nfft_plan_apply_cross(const ksvm_nfft_plan* plan, const double* targets
         DevBuf<double> tout;
         tout.alloc(t);
         DPSet dp{};
-        dp.P = tp.P.p;
-        for (int c = 0; c < 3; ++c) dp.Q[c] = c < w.d ? tp.Q[c].p : nullptr;
-        dp.code = tp.code.p;
-        dp.perm = tp.perm.p;
+        dp.F = tp.F.p;
+        dp.CP = tp.CP.p;
         dp.n = t;
         dp.win = 0;
         dp.out = ptr_kind == KSVM_NFFT_DEVICE ? out : tout.p;

@@ -15,7 +15,8 @@
 //   prod_t phi_t(o_t) = P * prod_t Q_t^{o_t} R[o_t],
 //   P = (pi b)^{-d/2} exp(-sum_t u_t^2 / b),  Q_t = exp(2 u_t / b),  R[o] = exp(-o^2 / b),
 // so a plan stores (P, Q_0..Q_{d-1}, tile-local cell code) per sorted point
-// and the apply evaluates no exp() at all.
+// and the apply evaluates no exp() at all. Layout is AoS so a point costs
+// three vector loads: F[i] = {P, Q0, Q1, Q2} (32 B), CP[i] = {code, perm}.
 #pragma once
 
 #include <cstdint>
@@ -65,10 +66,8 @@ struct DWin {
 
 // A sorted point set (a window's sources, or cross-apply targets).
 struct DPSet {
-    const double* P;     // prefactor (pi b)^{-d/2} exp(-sum u^2/b), sorted order
-    const double* Q[3];  // exp(2 u_t / b)
-    const int* code;     // tile-local cell code, sum_t (c_t mod TC) TC^{d-1-t}
-    const int* perm;     // sorted position -> original index
+    const double4* F;    // {P, Q0, Q1, Q2}: P = (pi b)^{-d/2} exp(-sum u^2/b), Q_t = exp(2 u_t/b)
+    const int2* CP;      // {tile-local cell code sum_t (c_t mod TC) TC^{d-1-t}, original index}
     long long n;
     int win;             // owning window slot
     double* out;         // gather output, original order (length n)

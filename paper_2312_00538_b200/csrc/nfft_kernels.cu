@@ -79,12 +79,20 @@ __device__ __forceinline__ void stage_row(double* st, const double* R, double P,
 template <int D>
 struct Pref {
     double P = 0.0, Q[3] = {0.0, 0.0, 0.0};
-    int code = 0;
+    int code = 0, perm = 0;
     __device__ __forceinline__ void load(const DPSet& ps, int i) {
-        P = __ldg(ps.P + i);
-#pragma unroll
-        for (int t = 0; t < D; ++t) Q[t] = __ldg(ps.Q[t] + i);
-        code = __ldg(ps.code + i);
+        const double2* f = reinterpret_cast<const double2*>(ps.F + i);
+        const double2 a = __ldg(f);
+        P = a.x;
+        Q[0] = a.y;
+        if (D > 1) {
+            const double2 b = __ldg(f + 1);
+            Q[1] = b.x;
+            Q[2] = b.y;
+        }
+        const int2 c = __ldg(ps.CP + i);
+        code = c.x;
+        perm = c.y;
     }
 };
 
@@ -186,30 +194,24 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
         }
     };
 
-    Pref<D> pf;
-    int perm1 = 0, perm2 = 0;
-    double vnext = 0.0;
+    // software pipeline: per-point factors two batches ahead, v one batch ahead
+    Pref<D> pa, pb;
+    double va = 0.0;
     {
         const int i0 = wb + lane, i1 = wb + 32 + lane;
         if (i0 < we) {
-            pf.load(ps, i0);
-            vnext = __ldg(v + __ldg(ps.perm + i0));
+            pa.load(ps, i0);
+            va = __ldg(v + pa.perm);
         }
-        if (i1 < we) perm1 = __ldg(ps.perm + i1);
+        if (i1 < we) pb.load(ps, i1);
     }
     __syncwarp();
     for (int base = wb; base < we; base += 32) {
         const int cnt = min(32, we - base);
-        if (lane < cnt) stage_row<D, S>(stage + lane * RL, R, pf.P * vnext, pf.Q, pf.code);
-        {
-            const int i1 = base + 32 + lane, i2 = base + 64 + lane;
-            if (i2 < we) perm2 = __ldg(ps.perm + i2);
-            if (i1 < we) {
-                pf.load(ps, i1);
-                vnext = __ldg(v + perm1);
-            }
-            perm1 = perm2;
-        }
+        if (lane < cnt) stage_row<D, S>(stage + lane * RL, R, pa.P * va, pa.Q, pa.code);
+        pa = pb;
+        if (base + 32 + lane < we) va = __ldg(v + pa.perm);
+        if (base + 64 + lane < we) pb.load(ps, base + 64 + lane);
         __syncwarp();
         int p = 0;
         while (p < cnt) {
@@ -278,12 +280,9 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     load_halo<D>(halo, wn, tc, TC, PE, PV);
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
-    Pref<D> pf;
-    int permn = 0;
-    if (wb + lane < we) {
-        pf.load(ps, wb + lane);
-        permn = __ldg(ps.perm + wb + lane);
-    }
+    Pref<D> pa, pb;  // factors of the current and the next batch
+    if (wb + lane < we) pa.load(ps, wb + lane);
+    if (wb + 32 + lane < we) pb.load(ps, wb + 32 + lane);
     __syncthreads();
 
     double h[8][2];
@@ -304,16 +303,11 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
         const int cnt = min(32, we - base);
         if (lane < cnt) {
             double* st = stage + lane * RL;
-            stage_row<D, S>(st, R, pf.P, pf.Q, pf.code);
-            reinterpret_cast<int*>(st + D * S)[1] = permn;
+            stage_row<D, S>(st, R, pa.P, pa.Q, pa.code);
+            reinterpret_cast<int*>(st + D * S)[1] = pa.perm;
         }
-        {
-            const int i1 = base + 32 + lane;
-            if (i1 < we) {
-                pf.load(ps, i1);
-                permn = __ldg(ps.perm + i1);
-            }
-        }
+        pa = pb;
+        if (base + 64 + lane < we) pb.load(ps, base + 64 + lane);
         __syncwarp();
         int p = 0;
         while (p < cnt) {
@@ -399,30 +393,24 @@ spread2_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
         dst[1] += acc1;
         acc0 = acc1 = 0.0;
     };
-    Pref<D> pf;
-    int perm1 = 0, perm2 = 0;
-    double vnext = 0.0;
+    // software pipeline: per-point factors two batches ahead, v one batch ahead
+    Pref<D> pa, pb;
+    double va = 0.0;
     {
         const int i0 = wb + lane, i1 = wb + 32 + lane;
         if (i0 < we) {
-            pf.load(ps, i0);
-            vnext = __ldg(v + __ldg(ps.perm + i0));
+            pa.load(ps, i0);
+            va = __ldg(v + pa.perm);
         }
-        if (i1 < we) perm1 = __ldg(ps.perm + i1);
+        if (i1 < we) pb.load(ps, i1);
     }
     __syncwarp();
     for (int base = wb; base < we; base += 32) {
         const int cnt = min(32, we - base);
-        if (lane < cnt) stage_row<D, S>(stage + lane * RL, R, pf.P * vnext, pf.Q, pf.code);
-        {
-            const int i1 = base + 32 + lane, i2 = base + 64 + lane;
-            if (i2 < we) perm2 = __ldg(ps.perm + i2);
-            if (i1 < we) {
-                pf.load(ps, i1);
-                vnext = __ldg(v + perm1);
-            }
-            perm1 = perm2;
-        }
+        if (lane < cnt) stage_row<D, S>(stage + lane * RL, R, pa.P * va, pa.Q, pa.code);
+        pa = pb;
+        if (base + 32 + lane < we) va = __ldg(v + pa.perm);
+        if (base + 64 + lane < we) pb.load(ps, base + 64 + lane);
         __syncwarp();
         for (int p = 0; p < cnt; ++p) {
             const double* st = stage + p * RL;
@@ -469,27 +457,20 @@ gather2_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     load_halo<D>(halo, wn, tc, TC, PE, PV);
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
-    Pref<D> pf;
-    int permc = 0, permn = 0;
-    if (wb + lane < we) {
-        pf.load(ps, wb + lane);
-        permn = __ldg(ps.perm + wb + lane);
-    }
+    Pref<D> pa, pb;
+    if (wb + lane < we) pa.load(ps, wb + lane);
+    if (wb + 32 + lane < we) pb.load(ps, wb + 32 + lane);
+    int permc = 0;
     __syncthreads();
     const int a = lane >> 2, b0 = (lane & 3) << 1;
     double h0 = 0.0, h1 = 0.0;
     int cur = -1;
     for (int base = wb; base < we; base += 32) {
         const int cnt = min(32, we - base);
-        if (lane < cnt) stage_row<D, S>(stage + lane * RL, R, pf.P, pf.Q, pf.code);
-        permc = permn;
-        {
-            const int i1 = base + 32 + lane;
-            if (i1 < we) {
-                pf.load(ps, i1);
-                permn = __ldg(ps.perm + i1);
-            }
-        }
+        if (lane < cnt) stage_row<D, S>(stage + lane * RL, R, pa.P, pa.Q, pa.code);
+        permc = pa.perm;
+        pa = pb;
+        if (base + 64 + lane < we) pb.load(ps, base + 64 + lane);
         __syncwarp();
         double pp[32];
 #pragma unroll
@@ -539,9 +520,11 @@ spread1_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
     for (int i = wb + lane; i < we; i += 32) {
-        double q = ps.P[i] * v[ps.perm[i]];
-        const double Q = ps.Q[0][i];
-        double* col = lp + ps.code[i] * 32 + lane;
+        const double2 f = __ldg(reinterpret_cast<const double2*>(ps.F + i));
+        const int2 cp = __ldg(ps.CP + i);
+        double q = f.x * __ldg(v + cp.y);
+        const double Q = f.y;
+        double* col = lp + cp.x * 32 + lane;
 #pragma unroll
         for (int o = 0; o < S; ++o) {
             col[o * 32] = fma(q, R[o], col[o * 32]);
@@ -578,16 +561,18 @@ gather1_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
     for (int i = wb + lane; i < we; i += 32) {
-        double q = ps.P[i];
-        const double Q = ps.Q[0][i];
-        const double* h = smem + ps.code[i];
+        const double2 f = __ldg(reinterpret_cast<const double2*>(ps.F + i));
+        const int2 cp = __ldg(ps.CP + i);
+        double q = f.x;
+        const double Q = f.y;
+        const double* h = smem + cp.x;
         double y = 0.0;
 #pragma unroll
         for (int o = 0; o < S; ++o) {
             y = fma(h[o], q * R[o], y);
             q *= Q;
         }
-        ps.out[ps.perm[i]] = y;
+        ps.out[cp.y] = y;
     }
 }
 
@@ -625,15 +610,17 @@ __global__ void spread_generic_kernel(const Item* __restrict__ items,
         if (lane < cnt) {
             const int i = base + lane;
             double* st = stage + lane * kRowG;
+            const double4 f = ps.F[i];
+            const double Qs[3] = {f.y, f.z, f.w};
             for (int t = 0; t < D; ++t) {
-                double q = t == 0 ? ps.P[i] * v[ps.perm[i]] : 1.0;
-                const double Q = ps.Q[t][i];
+                double q = t == 0 ? f.x * v[ps.CP[i].y] : 1.0;
+                const double Q = Qs[t];
                 for (int o = 0; o < S; ++o) {
                     st[t * kMaxSpan + o] = q * wn.R[o];
                     q *= Q;
                 }
             }
-            *reinterpret_cast<int*>(st + 3 * kMaxSpan) = ps.code[i];
+            *reinterpret_cast<int*>(st + 3 * kMaxSpan) = ps.CP[i].x;
         }
         __syncwarp();
         for (int p = 0; p < cnt; ++p) {
@@ -698,15 +685,17 @@ __global__ void gather_generic_kernel(const Item* __restrict__ items,
         if (lane < cnt) {
             const int i = base + lane;
             double* st = stage + lane * kRowG;
+            const double4 f = ps.F[i];
+            const double Qs[3] = {f.y, f.z, f.w};
             for (int t = 0; t < D; ++t) {
-                double q = t == 0 ? ps.P[i] : 1.0;
-                const double Q = ps.Q[t][i];
+                double q = t == 0 ? f.x : 1.0;
+                const double Q = Qs[t];
                 for (int o = 0; o < S; ++o) {
                     st[t * kMaxSpan + o] = q * wn.R[o];
                     q *= Q;
                 }
             }
-            *reinterpret_cast<int*>(st + 3 * kMaxSpan) = ps.code[i];
+            *reinterpret_cast<int*>(st + 3 * kMaxSpan) = ps.CP[i].x;
         }
         __syncwarp();
         for (int p = 0; p < cnt; ++p) {
@@ -734,7 +723,7 @@ __global__ void gather_generic_kernel(const Item* __restrict__ items,
             }
 #pragma unroll
             for (int s = 16; s >= 1; s >>= 1) part += __shfl_xor_sync(0xffffffffu, part, s);
-            if (lane == 0) ps.out[ps.perm[base + p]] = part;
+            if (lane == 0) ps.out[ps.CP[base + p].y] = part;
         }
         __syncwarp();
     }
@@ -999,18 +988,16 @@ __global__ void cell_keys_kernel(const double* __restrict__ x0, const double* __
     }
 }
 
-// Window factors of each sorted point (nfft_engine.cuh): P, Q_t, cell code.
+// Window factors of each sorted point (nfft_engine.cuh): {P, Q_t}, {code, perm}.
 __global__ void factors_kernel(const double* __restrict__ x0, const double* __restrict__ x1,
                                const double* __restrict__ x2, const int* __restrict__ perm, int d,
                                long long n, double Mf, int m, double invb, double Cw, int cmin,
-                               int TC, double* __restrict__ P, double* __restrict__ Q0,
-                               double* __restrict__ Q1, double* __restrict__ Q2,
-                               int* __restrict__ code) {
+                               int TC, double4* __restrict__ F, int2* __restrict__ CP) {
     for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         const int src = perm[i];
         const double* xs[3] = {x0, x1, x2};
-        double* Qs[3] = {Q0, Q1, Q2};
+        double Q[3] = {0.0, 0.0, 0.0};
         double su2 = 0.0, pre = 1.0;
         int cd = 0;
         for (int t = 0; t < d; ++t) {
@@ -1019,11 +1006,11 @@ __global__ void factors_kernel(const double* __restrict__ x0, const double* __re
             const double u = (xm - fl) + static_cast<double>(m - 1);
             su2 += u * u;
             pre *= Cw;
-            Qs[t][i] = exp((2.0 * u) * invb);
+            Q[t] = exp((2.0 * u) * invb);
             cd = cd * TC + (static_cast<int>(fl) - cmin) % TC;
         }
-        P[i] = pre * exp(-su2 * invb);
-        code[i] = cd;
+        F[i] = make_double4(pre * exp(-su2 * invb), Q[0], Q[1], Q[2]);
+        CP[i] = make_int2(cd, src);
     }
 }
 
@@ -1164,10 +1151,10 @@ void launch_cell_keys(const double* x0, const double* x1, const double* x2, int 
 
 void launch_factors(const double* x0, const double* x1, const double* x2, const int* perm, int d,
                     long long n, double Mf, int m, double invb, double Cw, int cmin, int TC,
-                    double* P, double* Q0, double* Q1, double* Q2, int* code, cudaStream_t st) {
+                    double4* F, int2* CP, cudaStream_t st) {
     const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 16));
     factors_kernel<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(x0, x1, x2, perm, d, n, Mf, m, invb, Cw,
-                                                             cmin, TC, P, Q0, Q1, Q2, code);
+                                                             cmin, TC, F, CP);
 }
 
 }  // namespace ksvm_nfft
