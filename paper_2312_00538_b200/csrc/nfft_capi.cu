@@ -33,6 +33,8 @@ void launch_gather(int D, int S, int PE, const Item* items, int nitems, const DP
                    const DWin* wins, cudaStream_t st);
 void launch_reduce(const DWin* wins, const int* slots, int nslots, long long max_nodes, int D,
                    const double* patches, cudaStream_t st);
+void launch_tile_reduce(const DWin* wins, const int2* multi, int nmulti, int max_pv, double* patches,
+                        cudaStream_t st);
 void launch_conv(const DWin* wins, const int* slots, int nslots, int Lg_max, long long max_fibres,
                  int stage, cudaStream_t st);
 int conv_max_lg();
@@ -388,6 +390,8 @@ struct Engine {
     DevBuf<DPSet> d_ps;     // sources of owned windows
     DevBuf<Item> d_items;   // source items of owned windows, grouped by d
     DevBuf<int> d_slots;    // 0..P_owned-1
+    DevBuf<int2> d_multi;   // (slot, tile) of tiles split into several items
+    int n_multi = 0, max_pv = 0;
     DevBuf<double> d_eta;
     DevBuf<double> patches, parts, vbuf, ybuf;
     DevBuf<double> d_raw;   // SoA raw window features (entries), original order
@@ -500,6 +504,7 @@ struct Engine {
     void finalize() {
         const int P = P_owned();
         std::vector<Item> all;
+        std::vector<int2> multi;
         std::vector<DPSet> ps(static_cast<size_t>(P));
         long long patch_total = 0;
         for (int D = 1; D <= 3; ++D) {
@@ -513,6 +518,9 @@ struct Engine {
                 w.dw.item_base = static_cast<int>(all.size());
                 w.dw.patch_base = patch_total;
                 std::vector<int> tf = w.src.tile_first;
+                for (size_t T = 0; T + 1 < tf.size(); ++T)
+                    if (tf[T + 1] - tf[T] > 1) multi.push_back(make_int2(s, static_cast<int>(T)));
+                max_pv = std::max(max_pv, PV);
                 for (auto& v : tf) v += w.dw.item_base;
                 w.tile_first.upload(tf.data(), tf.size(), stream);
                 w.dw.tile_first = w.tile_first.p;
@@ -546,6 +554,8 @@ struct Engine {
         d_ps.upload(ps.data(), ps.size(), stream);
         d_items.upload(all.data(), all.size(), stream);
         d_slots.upload(slots.data(), slots.size(), stream);
+        n_multi = static_cast<int>(multi.size());
+        if (n_multi) d_multi.upload(multi.data(), multi.size(), stream);
         d_eta.upload(eta.data(), eta.size(), stream);
         patches.alloc(static_cast<size_t>(std::max<long long>(patch_total, 1)));
         vbuf.alloc(n);
@@ -574,6 +584,11 @@ struct Engine {
             ++g_launches;
         }
         CK(cudaGetLastError());
+        tick("tile_reduce");
+        if (n_multi) {
+            launch_tile_reduce(d_wins.p, d_multi.p, n_multi, max_pv, patches.p, stream);
+            ++g_launches;
+        }
         tick("reduce");
         for (int D = 1; D <= 3; ++D) {
             if (!has_dim[D]) continue;

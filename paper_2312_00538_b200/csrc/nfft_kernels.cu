@@ -259,7 +259,7 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
 // is an xor-butterfly over g (fixed order).
 // ===========================================================================
 template <int W>
-__global__ void __launch_bounds__(W * 32)
+__global__ void __launch_bounds__(W * 32, 4)
 gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
                   const DWin* __restrict__ wins) {
     constexpr int D = 3, S = 8, TC = 4, PE = TC + S - 1, PV = PE * PE * PE, RL = Row<D, S>::kLen;
@@ -730,8 +730,29 @@ __global__ void gather_generic_kernel(const Item* __restrict__ items,
 }
 
 // ===========================================================================
-// Patch reduction: grid node <- sum of every covering item's patch value, in
-// (e0, T0, e1, T1, e2, T2, item) order. blockIdx.y = window slot.
+// Tile pre-reduction: for every tile split into several items, sum the
+// items' patches (ascending item order) into the tile's first patch, so the
+// node reduction below reads one patch per covering tile. Work list:
+// (window slot, tile) pairs of multi-item tiles; blockIdx.y = pair.
+// ===========================================================================
+__global__ void tile_reduce_kernel(const DWin* __restrict__ wins, const int2* __restrict__ multi,
+                                   double* __restrict__ patches) {
+    const int2 wt = multi[blockIdx.y];
+    const DWin& wn = wins[wt.x];
+    int PV = 1;
+    for (int t = 0; t < wn.d; ++t) PV *= wn.PE;
+    const int k0 = wn.tile_first[wt.y], k1 = wn.tile_first[wt.y + 1];
+    double* base = patches + wn.patch_base + static_cast<long long>(k0 - wn.item_base) * PV;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < PV; e += gridDim.x * blockDim.x) {
+        double s = base[e];
+        for (int k = 1; k < k1 - k0; ++k) s += base[static_cast<long long>(k) * PV + e];
+        base[e] = s;
+    }
+}
+
+// ===========================================================================
+// Patch reduction: grid node <- sum over every covering tile's (pre-reduced)
+// patch value, in (e0, T0, e1, T1, e2, T2) order. blockIdx.y = window slot.
 // ===========================================================================
 template <int D>
 __global__ void reduce_patches_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots,
@@ -770,22 +791,23 @@ __global__ void reduce_patches_kernel(const DWin* __restrict__ wins, const int* 
         for (int T0 = KSVM_TLO(e0); T0 <= KSVM_THI(e0); ++T0) {
             const int o0 = e0 - T0 * TC;
             if constexpr (D == 1) {
-                for (int k = wn.tile_first[T0]; k < wn.tile_first[T0 + 1]; ++k)
-                    sum += pb[static_cast<long long>(k - wn.item_base) * PV + o0];
+                const int k = wn.tile_first[T0];
+                if (k < wn.tile_first[T0 + 1]) sum += pb[static_cast<long long>(k - wn.item_base) * PV + o0];
             } else {
                 for (int e1 = e0s[1]; e1 < Eext; e1 += step)
                     for (int T1 = KSVM_TLO(e1); T1 <= KSVM_THI(e1); ++T1) {
                         const int o1 = o0 * PE + e1 - T1 * TC;
                         if constexpr (D == 2) {
                             const int T = T0 * nt + T1;
-                            for (int k = wn.tile_first[T]; k < wn.tile_first[T + 1]; ++k)
-                                sum += pb[static_cast<long long>(k - wn.item_base) * PV + o1];
+                            const int k = wn.tile_first[T];
+                            if (k < wn.tile_first[T + 1]) sum += pb[static_cast<long long>(k - wn.item_base) * PV + o1];
                         } else {
                             for (int e2 = e0s[2]; e2 < Eext; e2 += step)
                                 for (int T2 = KSVM_TLO(e2); T2 <= KSVM_THI(e2); ++T2) {
                                     const int T = (T0 * nt + T1) * nt + T2;
                                     const int o2 = o1 * PE + e2 - T2 * TC;
-                                    for (int k = wn.tile_first[T]; k < wn.tile_first[T + 1]; ++k)
+                                    const int k = wn.tile_first[T];
+                                    if (k < wn.tile_first[T + 1])
                                         sum += pb[static_cast<long long>(k - wn.item_base) * PV + o2];
                                 }
                         }
@@ -1103,6 +1125,13 @@ void launch_gather(int D, int S, int PE, const Item* items, int nitems, const DP
     if (D == 1) gather_generic_kernel<1><<<nitems, W * 32, sm, st>>>(items, ps, wins, W);
     else if (D == 2) gather_generic_kernel<2><<<nitems, W * 32, sm, st>>>(items, ps, wins, W);
     else gather_generic_kernel<3><<<nitems, W * 32, sm, st>>>(items, ps, wins, W);
+}
+
+void launch_tile_reduce(const DWin* wins, const int2* multi, int nmulti, int max_pv, double* patches,
+                        cudaStream_t st) {
+    if (nmulti == 0) return;
+    dim3 grid(static_cast<unsigned>((max_pv + 255) / 256), static_cast<unsigned>(nmulti));
+    tile_reduce_kernel<<<grid, 256, 0, st>>>(wins, multi, patches);
 }
 
 void launch_reduce(const DWin* wins, const int* slots, int nslots, long long max_nodes, int D,
