@@ -743,10 +743,17 @@ __global__ void tile_reduce_kernel(const DWin* __restrict__ wins, const int2* __
     for (int t = 0; t < wn.d; ++t) PV *= wn.PE;
     const int k0 = wn.tile_first[wt.y], k1 = wn.tile_first[wt.y + 1];
     double* base = patches + wn.patch_base + static_cast<long long>(k0 - wn.item_base) * PV;
+    const int nk = k1 - k0;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < PV; e += gridDim.x * blockDim.x) {
-        double s = base[e];
-        for (int k = 1; k < k1 - k0; ++k) s += base[static_cast<long long>(k) * PV + e];
-        base[e] = s;
+        // eight interleaved partial sums (8 loads in flight), combined in a fixed order
+        double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        int k = 0;
+        for (; k + 8 <= nk; k += 8) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) s[j] += base[static_cast<long long>(k + j) * PV + e];
+        }
+        for (int j = 0; k + j < nk; ++j) s[j] += base[static_cast<long long>(k + j) * PV + e];
+        base[e] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
     }
 }
 
