@@ -250,7 +250,7 @@ Geometry geometry(const ksvm_nfft_config& c, int d) {
 
 // Sort a point set by (tile, cell) on the device and split tiles into items.
 void build_pointset(PointSet& ps, const std::vector<double>& scaled_cm, int64_t n, int d,
-                    const Geometry& g, cudaStream_t st) {
+                    const Geometry& g, int64_t chunk_points, cudaStream_t st) {
     ps.n = n;
     ps.d = d;
     DevBuf<double> raw[3];
@@ -296,10 +296,10 @@ void build_pointset(PointSet& ps, const std::vector<double>& scaled_cm, int64_t 
         tcd *= static_cast<unsigned>(g.TC);
         ntiles *= g.ntile;
     }
-    // Items: tiles split into chunks of <= chunk points (fixed at plan time,
-    // so the summation order -- and hence every bit of the result -- is a
-    // function of the plan alone).
-    const int64_t chunk = std::max<int64_t>(256, (n + 8 * 148 - 1) / (8 * 148));
+    // Items: tiles split into chunks of <= chunk_points points (fixed at plan
+    // time, so the summation order -- and hence every bit of the result -- is
+    // a function of the plan alone).
+    const int64_t chunk = chunk_points;
     ps.items.clear();
     ps.tile_first.assign(static_cast<size_t>(ntiles) + 1, 0);
     int64_t i = 0;
@@ -321,6 +321,13 @@ void build_pointset(PointSet& ps, const std::vector<double>& scaled_cm, int64_t 
         i = j;
     }
     ps.tile_first[static_cast<size_t>(ntiles)] = static_cast<int>(ps.items.size());
+}
+
+// Points per item: about 12 items per SM over all windows of the operator
+// (load balance), but at least 1024 so heavy tiles are not cut into hundreds
+// of patches (each item writes one (TC+2m-1)^d patch that must be reduced).
+int64_t item_chunk(int64_t total_points) {
+    return std::max<int64_t>(1024, (total_points + 148 * 12 - 1) / (148 * 12));
 }
 
 // Affine map of P:src/fastsum.cpp:126-140 on a column-major n x d block.
@@ -419,6 +426,7 @@ struct Engine {
     }
 
     int P_owned() const { return static_cast<int>(owned.size()); }
+    int64_t n_owned_windows = 1;  // set before planning (item sizing)
 
     void init(int dev) {
         device = dev;
@@ -472,7 +480,7 @@ struct Engine {
         w.G.alloc(nodes);
         w.H.alloc(nodes);
         for (int k = 0; k < (d == 1 ? 0 : (d == 2 ? 2 : 4)); ++k) w.T[k].alloc(nodes);
-        build_pointset(w.src, sc, n, d, g, stream);
+        build_pointset(w.src, sc, n, d, g, item_chunk(n * n_owned_windows), stream);
 
         DWin& dw = w.dw;
         dw.d = d;
@@ -750,6 +758,9 @@ void build_engine(Engine& E, const double* points, int64_t n, int64_t d, int64_t
     for (auto& w : E.wins) wdim.push_back(w->d);
     E.d_wdim.upload(wdim.data(), wdim.size(), E.stream);
     // one plan per owned window (P:src/fastsum.cpp:333-340)
+    E.n_owned_windows = 0;
+    for (auto& w : E.wins) E.n_owned_windows += w->owned ? 1 : 0;
+    E.n_owned_windows = std::max<int64_t>(1, E.n_owned_windows);
     int col0 = 0;
     for (int l = 0; l < P; ++l) {
         Window& w = *E.wins[static_cast<size_t>(l)];
@@ -1014,7 +1025,7 @@ int ksvm_nfft_plan_apply_cross(const ksvm_nfft_plan* plan, const double* targets
         std::lock_guard<std::mutex> lk(E.mu);
         const Geometry g = geometry(E.cfg, w.d);
         PointSet tp;
-        build_pointset(tp, sc, t, w.d, g, E.stream);
+        build_pointset(tp, sc, t, w.d, g, item_chunk(t), E.stream);
         DevBuf<double> tout;
         tout.alloc(t);
         DPSet dp{};

@@ -216,51 +216,29 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
         if (base + 32 + lane < we) va = __ldg(v + pa.perm);
         if (base + 64 + lane < we) pb.load(ps, base + 64 + lane);
         __syncwarp();
-        // static groups of 4 points (K of one DMMA); lane t carries point 4 gq + t
-#pragma unroll
-        for (int gq = 0; gq < 8; ++gq) {
-            if (4 * gq >= cnt) break;
-            const int q = 4 * gq + t;
-            const bool inb = q < cnt;
-            const double* st = stage + (inb ? q : 4 * gq) * RL;
-            const int cq = inb ? row_code(st, D, S) : -1;
-            const int c0 = __shfl_sync(0xffffffffu, cq, 0);
-            const int c3 = __shfl_sync(0xffffffffu, cq, 3);
-            const double2 w01 = ld2(st), w23 = ld2(st + 2), w45 = ld2(st + 4), w67 = ld2(st + 6);
-            const double w1g = st[S + g], bq = st[2 * S + g];
-            if (c0 == cur && c3 == cur) {
-                dmma(acc[0][0], acc[0][1], w01.x * w1g, bq);
-                dmma(acc[1][0], acc[1][1], w01.y * w1g, bq);
-                dmma(acc[2][0], acc[2][1], w23.x * w1g, bq);
-                dmma(acc[3][0], acc[3][1], w23.y * w1g, bq);
-                dmma(acc[4][0], acc[4][1], w45.x * w1g, bq);
-                dmma(acc[5][0], acc[5][1], w45.y * w1g, bq);
-                dmma(acc[6][0], acc[6][1], w67.x * w1g, bq);
-                dmma(acc[7][0], acc[7][1], w67.y * w1g, bq);
-            } else {
-                // the group straddles cells: one masked pass per cell, in point order
-                bool done = !inb;
-                for (;;) {
-                    const unsigned pend = __ballot_sync(0xffffffffu, !done) & 0xFu;
-                    if (pend == 0u) break;
-                    const int cn = __shfl_sync(0xffffffffu, cq, __ffs(pend) - 1);
-                    if (cn != cur) {
-                        if (cur >= 0) flush(cur);
-                        cur = cn;
-                    }
-                    const bool sel = !done && cq == cur;
-                    const double u = sel ? w1g : 0.0, b = sel ? bq : 0.0;
-                    dmma(acc[0][0], acc[0][1], w01.x * u, b);
-                    dmma(acc[1][0], acc[1][1], w01.y * u, b);
-                    dmma(acc[2][0], acc[2][1], w23.x * u, b);
-                    dmma(acc[3][0], acc[3][1], w23.y * u, b);
-                    dmma(acc[4][0], acc[4][1], w45.x * u, b);
-                    dmma(acc[5][0], acc[5][1], w45.y * u, b);
-                    dmma(acc[6][0], acc[6][1], w67.x * u, b);
-                    dmma(acc[7][0], acc[7][1], w67.y * u, b);
-                    done = done || sel;
-                }
+        int p = 0;
+        while (p < cnt) {
+            const int cp = row_code(stage + p * RL, D, S);
+            if (cp != cur) {
+                if (cur >= 0) flush(cur);
+                cur = cp;
             }
+            const int q = p + t;
+            const bool valid = q < cnt && row_code(stage + q * RL, D, S) == cur;
+            const int nvalid = __popc(__ballot_sync(0xffffffffu, valid) & 0xFu);
+            const double* st = stage + (valid ? q : p) * RL;
+            const double w1g = valid ? st[S + g] : 0.0;
+            const double b = valid ? st[2 * S + g] : 0.0;
+            const double2 w01 = ld2(st), w23 = ld2(st + 2), w45 = ld2(st + 4), w67 = ld2(st + 6);
+            dmma(acc[0][0], acc[0][1], w01.x * w1g, b);
+            dmma(acc[1][0], acc[1][1], w01.y * w1g, b);
+            dmma(acc[2][0], acc[2][1], w23.x * w1g, b);
+            dmma(acc[3][0], acc[3][1], w23.y * w1g, b);
+            dmma(acc[4][0], acc[4][1], w45.x * w1g, b);
+            dmma(acc[5][0], acc[5][1], w45.y * w1g, b);
+            dmma(acc[6][0], acc[6][1], w67.x * w1g, b);
+            dmma(acc[7][0], acc[7][1], w67.y * w1g, b);
+            p += nvalid;
         }
         __syncwarp();
     }
@@ -334,85 +312,54 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
         pa = pb;
         if (base + 64 + lane < we) pb.load(ps, base + 64 + lane);
         __syncwarp();
-        // static groups of 8 points (N of the DMMAs): B column g = point 8 gq + g
+        int p = 0;
+        while (p < cnt) {
+            const int cp = row_code(stage + p * RL, D, S);
+            if (cp != cur) {
+                cur = cp;
+                reload(cp);
+            }
+            const int qg = p + g;
+            const bool vg = qg < cnt && row_code(stage + qg * RL, D, S) == cur;
+            const int nvalid = __popc(__ballot_sync(0xffffffffu, vg) & 0x11111111u);
+            const double* sg = stage + (vg ? qg : p) * RL + 2 * S;
+            const double b0 = vg ? sg[t] : 0.0, b1 = vg ? sg[t + 4] : 0.0;
+            double T[8][2];
 #pragma unroll
-        for (int gq = 0; gq < 4; ++gq) {
-            if (8 * gq >= cnt) break;
-            const int qg = 8 * gq + g;
-            const bool ing = qg < cnt;
-            const double* sgp = stage + (ing ? qg : 8 * gq) * RL;
-            const int cg = ing ? row_code(sgp, D, S) : -1;
-            const int c0 = __shfl_sync(0xffffffffu, cg, 0);
-            const int c7 = __shfl_sync(0xffffffffu, cg, 28);
-            const double bq0 = sgp[2 * S + t], bq1 = sgp[2 * S + 4 + t];
-            // epilogue operands of points j = 2t, 2t+1 of the group
-            double w0v[2][8], w1v[2];
-            int cj[2];
-            bool inj[2];
+            for (int r = 0; r < 8; ++r) {
+                T[r][0] = T[r][1] = 0.0;
+                dmma(T[r][0], T[r][1], h[r][0], b0);
+                dmma(T[r][0], T[r][1], h[r][1], b1);
+            }
+            double part[2];
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const int j = 8 * gq + 2 * t + e;
-                inj[e] = j < cnt;
-                const double* sj = stage + (inj[e] ? j : 8 * gq) * RL;
-                const double2 a01 = ld2(sj), a23 = ld2(sj + 2), a45 = ld2(sj + 4), a67 = ld2(sj + 6);
-                w0v[e][0] = a01.x; w0v[e][1] = a01.y; w0v[e][2] = a23.x; w0v[e][3] = a23.y;
-                w0v[e][4] = a45.x; w0v[e][5] = a45.y; w0v[e][6] = a67.x; w0v[e][7] = a67.y;
-                w1v[e] = sj[S + g];
-                cj[e] = inj[e] ? row_code(sj, D, S) : -1;
+                const int j = 2 * t + e;
+                const bool ok = j < nvalid;
+                const double* st = stage + (ok ? p + j : p) * RL;
+                const double2 w01 = ld2(st), w23 = ld2(st + 2), w45 = ld2(st + 4), w67 = ld2(st + 6);
+                double s0 = w01.x * T[0][e], s1 = w01.y * T[1][e];
+                s0 = fma(w23.x, T[2][e], s0);
+                s1 = fma(w23.y, T[3][e], s1);
+                s0 = fma(w45.x, T[4][e], s0);
+                s1 = fma(w45.y, T[5][e], s1);
+                s0 = fma(w67.x, T[6][e], s0);
+                s1 = fma(w67.y, T[7][e], s1);
+                part[e] = ok ? st[S + g] * (s0 + s1) : 0.0;
             }
-            bool done = !ing;
-            bool first = true;
-            for (;;) {
-                int cn;
-                if (first && c0 == c7 && c0 >= 0) {
-                    cn = c0;  // whole group in one cell (common case)
-                } else {
-                    const unsigned pend = __ballot_sync(0xffffffffu, !done) & 0x11111111u;
-                    if (pend == 0u) break;
-                    cn = __shfl_sync(0xffffffffu, cg, __ffs(pend) - 1);
-                }
-                if (cn != cur) {
-                    cur = cn;
-                    reload(cn);
-                }
-                const bool sel = !done && cg == cur;
-                const double b0 = sel ? bq0 : 0.0, b1 = sel ? bq1 : 0.0;
-                double T[8][2];
 #pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    T[r][0] = T[r][1] = 0.0;
-                    dmma(T[r][0], T[r][1], h[r][0], b0);
-                    dmma(T[r][0], T[r][1], h[r][1], b1);
-                }
-                double part[2];
+            for (int m = 4; m <= 16; m <<= 1) {
+                part[0] += __shfl_xor_sync(0xffffffffu, part[0], m);
+                part[1] += __shfl_xor_sync(0xffffffffu, part[1], m);
+            }
+            if (g == 0) {
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
-                    double s0 = w0v[e][0] * T[0][e], s1 = w0v[e][1] * T[1][e];
-                    s0 = fma(w0v[e][2], T[2][e], s0);
-                    s1 = fma(w0v[e][3], T[3][e], s1);
-                    s0 = fma(w0v[e][4], T[4][e], s0);
-                    s1 = fma(w0v[e][5], T[5][e], s1);
-                    s0 = fma(w0v[e][6], T[6][e], s0);
-                    s1 = fma(w0v[e][7], T[7][e], s1);
-                    part[e] = w1v[e] * (s0 + s1);
+                    const int j = 2 * t + e;
+                    if (j < nvalid) ps.out[reinterpret_cast<const int*>(stage + (p + j) * RL + D * S)[1]] = part[e];
                 }
-#pragma unroll
-                for (int m = 4; m <= 16; m <<= 1) {
-                    part[0] += __shfl_xor_sync(0xffffffffu, part[0], m);
-                    part[1] += __shfl_xor_sync(0xffffffffu, part[1], m);
-                }
-                if (g == 0) {
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int j = 8 * gq + 2 * t + e;
-                        if (inj[e] && cj[e] == cur)
-                            ps.out[reinterpret_cast<const int*>(stage + j * RL + D * S)[1]] = part[e];
-                    }
-                }
-                done = done || sel;
-                if (first && c0 == c7 && c0 >= 0) break;
-                first = false;
             }
+            p += nvalid;
         }
         __syncwarp();
     }
