@@ -196,8 +196,9 @@ struct PointSet {
     DevBuf<double4> F;  // window factors {P, Q0, Q1, Q2}, sorted order (nfft_engine.cuh)
     DevBuf<int2> CP;    // {tile-local cell code, original index}
     DevBuf<int> perm;
-    std::vector<Item> items;      // host copy (global numbering assigned later)
-    std::vector<int> tile_first;  // local item index of each tile's first item
+    std::vector<Item> items;      // spread items (one patch each; global numbering later)
+    std::vector<int> tile_first;  // local item index of each tile's first spread item
+    std::vector<Item> gitems;     // gather items (finer: no patch cost, better balance)
 };
 
 struct Window {
@@ -250,7 +251,7 @@ Geometry geometry(const ksvm_nfft_config& c, int d) {
 
 // Sort a point set by (tile, cell) on the device and split tiles into items.
 void build_pointset(PointSet& ps, const std::vector<double>& scaled_cm, int64_t n, int d,
-                    const Geometry& g, int64_t chunk_points, cudaStream_t st) {
+                    const Geometry& g, int64_t chunk_points, int64_t gather_chunk, cudaStream_t st) {
     ps.n = n;
     ps.d = d;
     DevBuf<double> raw[3];
@@ -299,9 +300,19 @@ void build_pointset(PointSet& ps, const std::vector<double>& scaled_cm, int64_t 
     // Items: tiles split into chunks of <= chunk_points points (fixed at plan
     // time, so the summation order -- and hence every bit of the result -- is
     // a function of the plan alone).
-    const int64_t chunk = chunk_points;
     ps.items.clear();
+    ps.gitems.clear();
     ps.tile_first.assign(static_cast<size_t>(ntiles) + 1, 0);
+    auto split = [](std::vector<Item>& out, int T, int64_t i, int64_t cnt, int64_t chunk) {
+        const int64_t pieces = (cnt + chunk - 1) / chunk;
+        for (int64_t q = 0; q < pieces; ++q) {
+            Item it{};
+            it.tile = T;
+            it.begin = static_cast<int>(i + cnt * q / pieces);
+            it.end = static_cast<int>(i + cnt * (q + 1) / pieces);
+            out.push_back(it);
+        }
+    };
     int64_t i = 0;
     for (int T = 0; T < ntiles; ++T) {
         ps.tile_first[static_cast<size_t>(T)] = static_cast<int>(ps.items.size());
@@ -309,25 +320,22 @@ void build_pointset(PointSet& ps, const std::vector<double>& scaled_cm, int64_t 
         while (j < n && hk[static_cast<size_t>(j)] / tcd == static_cast<unsigned>(T)) ++j;
         const int64_t cnt = j - i;
         if (cnt > 0) {
-            const int64_t pieces = (cnt + chunk - 1) / chunk;
-            for (int64_t q = 0; q < pieces; ++q) {
-                Item it{};
-                it.tile = T;
-                it.begin = static_cast<int>(i + cnt * q / pieces);
-                it.end = static_cast<int>(i + cnt * (q + 1) / pieces);
-                ps.items.push_back(it);
-            }
+            split(ps.items, T, i, cnt, chunk_points);
+            split(ps.gitems, T, i, cnt, gather_chunk);
         }
         i = j;
     }
     ps.tile_first[static_cast<size_t>(ntiles)] = static_cast<int>(ps.items.size());
 }
 
-// Points per item: about 12 items per SM over all windows of the operator
-// (load balance), but at least 1024 so heavy tiles are not cut into hundreds
-// of patches (each item writes one (TC+2m-1)^d patch that must be reduced).
+// Points per spread item: ~24 items per SM over all windows of the operator
+// (load balance) but no more, since each item writes one (TC+2m-1)^d patch
+// that must be reduced. Gather items carry no patch, so they are finer.
 int64_t item_chunk(int64_t total_points) {
-    return std::max<int64_t>(1024, (total_points + 148 * 12 - 1) / (148 * 12));
+    return std::max<int64_t>(256, (total_points + 148 * 24 - 1) / (148 * 24));
+}
+int64_t gather_chunk(int64_t total_points) {
+    return std::max<int64_t>(128, (total_points + 148 * 48 - 1) / (148 * 48));
 }
 
 // Affine map of P:src/fastsum.cpp:126-140 on a column-major n x d block.
@@ -395,7 +403,9 @@ struct Engine {
     // device state
     DevBuf<DWin> d_wins;    // owned windows (slot = position in `owned`)
     DevBuf<DPSet> d_ps;     // sources of owned windows
-    DevBuf<Item> d_items;   // source items of owned windows, grouped by d
+    DevBuf<Item> d_items;   // spread items of owned windows, grouped by d
+    DevBuf<Item> d_gitems;  // gather items of owned windows, grouped by d
+    int gclass_begin[4] = {0, 0, 0, 0}, gclass_end[4] = {0, 0, 0, 0};
     DevBuf<int> d_slots;    // 0..P_owned-1
     DevBuf<int2> d_multi;   // (slot, tile) of tiles split into several items
     int n_multi = 0, max_pv = 0;
@@ -480,7 +490,8 @@ struct Engine {
         w.G.alloc(nodes);
         w.H.alloc(nodes);
         for (int k = 0; k < (d == 1 ? 0 : (d == 2 ? 2 : 4)); ++k) w.T[k].alloc(nodes);
-        build_pointset(w.src, sc, n, d, g, item_chunk(n * n_owned_windows), stream);
+        build_pointset(w.src, sc, n, d, g, item_chunk(n * n_owned_windows),
+                       gather_chunk(n * n_owned_windows), stream);
 
         DWin& dw = w.dw;
         dw.d = d;
@@ -511,7 +522,7 @@ struct Engine {
     // Assign global item numbers / patch offsets and upload device tables.
     void finalize() {
         const int P = P_owned();
-        std::vector<Item> all;
+        std::vector<Item> all, gall;
         std::vector<int2> multi;
         std::vector<DPSet> ps(static_cast<size_t>(P));
         long long patch_total = 0;
@@ -541,6 +552,17 @@ struct Engine {
                 }
             }
             class_end[D] = static_cast<int>(all.size());
+            gclass_begin[D] = static_cast<int>(gall.size());
+            for (int s = 0; s < P; ++s) {
+                Window& w = *wins[static_cast<size_t>(owned[static_cast<size_t>(s)])];
+                if (w.d != D) continue;
+                for (const Item& it0 : w.src.gitems) {
+                    Item it = it0;
+                    it.ps = s;
+                    gall.push_back(it);
+                }
+            }
+            gclass_end[D] = static_cast<int>(gall.size());
         }
         std::vector<DWin> dws(static_cast<size_t>(P));
         std::vector<double> eta(static_cast<size_t>(P));
@@ -561,6 +583,7 @@ struct Engine {
         d_wins.upload(dws.data(), dws.size(), stream);
         d_ps.upload(ps.data(), ps.size(), stream);
         d_items.upload(all.data(), all.size(), stream);
+        d_gitems.upload(gall.data(), gall.size(), stream);
         d_slots.upload(slots.data(), slots.size(), stream);
         n_multi = static_cast<int>(multi.size());
         if (n_multi) d_multi.upload(multi.data(), multi.size(), stream);
@@ -625,10 +648,10 @@ struct Engine {
         run_grid(v);
         static const char* kGather[4] = {"", "gather_d1", "gather_d2", "gather_d3"};
         for (int D = 1; D <= 3; ++D) {
-            const int cnt = class_end[D] - class_begin[D];
+            const int cnt = gclass_end[D] - gclass_begin[D];
             if (cnt == 0) continue;
             tick(kGather[D]);
-            launch_gather(D, 2 * cfg.window_cutoff, class_PE[D], d_items.p + class_begin[D], cnt,
+            launch_gather(D, 2 * cfg.window_cutoff, class_PE[D], d_gitems.p + gclass_begin[D], cnt,
                           d_ps.p, d_wins.p, stream);
             ++g_launches;
         }
@@ -1025,7 +1048,7 @@ int ksvm_nfft_plan_apply_cross(const ksvm_nfft_plan* plan, const double* targets
         std::lock_guard<std::mutex> lk(E.mu);
         const Geometry g = geometry(E.cfg, w.d);
         PointSet tp;
-        build_pointset(tp, sc, t, w.d, g, item_chunk(t), E.stream);
+        build_pointset(tp, sc, t, w.d, g, item_chunk(t), gather_chunk(t), E.stream);
         DevBuf<double> tout;
         tout.alloc(t);
         DPSet dp{};
@@ -1036,7 +1059,7 @@ int ksvm_nfft_plan_apply_cross(const ksvm_nfft_plan* plan, const double* targets
         dp.out = ptr_kind == KSVM_NFFT_DEVICE ? out : tout.p;
         DevBuf<DPSet> dps;
         dps.upload(&dp, 1, E.stream);
-        std::vector<Item> its = tp.items;
+        std::vector<Item> its = tp.gitems;
         for (auto& it : its) it.ps = 0;
         DevBuf<Item> ditems;
         ditems.upload(its.data(), its.size(), E.stream);

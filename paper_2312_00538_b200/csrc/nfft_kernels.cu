@@ -254,12 +254,14 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
 }
 
 // ===========================================================================
-// Gather, d = 3, m = 4, on the FP64 tensor cores:
-//   T[(a,b), p] = sum_c H[(a,b), c] W2[p, c]      (8 tiles x 2 k-steps, N = 8 points)
-//   y_p = sum_a w0_p[a] P sum_b w1_p[b] T[(a,b), p]   (per-point epilogue)
-// Lane l = 4g + t holds A[g][t] = H[(r, g), t + 4k] (reloaded per cell),
-// B[t][g] = W2[point g][t + 4k], and T[(r, g), points 2t, 2t+1]; the b-sum
-// is an xor-butterfly over g (fixed order).
+// Gather, d = 3, m = 4, on the FP64 tensor cores, 8 same-cell points per round:
+//   Z[p, c] = sum_{(a,b)} U[p, (a,b)] H[(a,b), c],  U[p, (a,b)] = P_p w0_p[a] w1_p[b]
+//   y_p     = sum_c Z[p, c] w2_p[c]
+// M = 8 points, N = c, K = 64 (a,b) pairs in 16 k-steps of 4, split over four
+// accumulators (fixed combine order). Lane l = 4g + t: A[g][t] = U[point g,
+// (k/2, 4(k%2)+t)] (one DMUL each), B[t][g] = H[(k/2, 4(k%2)+t), c=g] (16
+// values, reloaded per cell), D holds Z[point g][2t..2t+1]; the c-sum is a
+// 2-step xor over t.
 // ===========================================================================
 template <int W>
 __global__ void __launch_bounds__(W * 32, 4)
@@ -288,18 +290,16 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     if (wb + 32 + lane < we) pb.load(ps, wb + 32 + lane);
     __syncthreads();
 
-    double h[8][2];
+    // B fragments: hb[k] = H[(k/2, 4(k%2)+t), c = g] of the current cell
+    double hb[16];
 #pragma unroll
-    for (int r = 0; r < 8; ++r) h[r][0] = h[r][1] = 0.0;
+    for (int k = 0; k < 16; ++k) hb[k] = 0.0;
     int cur = -1;
     auto reload = [&](int cell) {
         const int l0 = cell >> 4, l1 = (cell >> 2) & 3, l2 = cell & 3;
-        const double* src = halo + (l0 * PE + l1 + g) * PE + l2 + t;
+        const double* src = halo + (l0 * PE + l1 + t) * PE + l2 + g;
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            h[r][0] = src[r * PE * PE];
-            h[r][1] = src[r * PE * PE + 4];
-        }
+        for (int k = 0; k < 16; ++k) hb[k] = src[(k >> 1) * PE * PE + 4 * (k & 1) * PE];
     };
 
     for (int base = wb; base < we; base += 32) {
@@ -322,43 +322,20 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
             const int qg = p + g;
             const bool vg = qg < cnt && row_code(stage + qg * RL, D, S) == cur;
             const int nvalid = __popc(__ballot_sync(0xffffffffu, vg) & 0x11111111u);
-            const double* sg = stage + (vg ? qg : p) * RL + 2 * S;
-            const double b0 = vg ? sg[t] : 0.0, b1 = vg ? sg[t + 4] : 0.0;
-            double T[8][2];
+            const double* sg = stage + (vg ? qg : p) * RL;
+            const double2 w01 = ld2(sg), w23 = ld2(sg + 2), w45 = ld2(sg + 4), w67 = ld2(sg + 6);
+            const double w0[8] = {w01.x, w01.y, w23.x, w23.y, w45.x, w45.y, w67.x, w67.y};
+            const double u0 = vg ? sg[S + t] : 0.0, u1 = vg ? sg[S + 4 + t] : 0.0;
+            const double2 w2 = ld2(sg + 2 * S + 2 * t);
+            double z[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
 #pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                T[r][0] = T[r][1] = 0.0;
-                dmma(T[r][0], T[r][1], h[r][0], b0);
-                dmma(T[r][0], T[r][1], h[r][1], b1);
-            }
-            double part[2];
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int j = 2 * t + e;
-                const bool ok = j < nvalid;
-                const double* st = stage + (ok ? p + j : p) * RL;
-                const double2 w01 = ld2(st), w23 = ld2(st + 2), w45 = ld2(st + 4), w67 = ld2(st + 6);
-                double s0 = w01.x * T[0][e], s1 = w01.y * T[1][e];
-                s0 = fma(w23.x, T[2][e], s0);
-                s1 = fma(w23.y, T[3][e], s1);
-                s0 = fma(w45.x, T[4][e], s0);
-                s1 = fma(w45.y, T[5][e], s1);
-                s0 = fma(w67.x, T[6][e], s0);
-                s1 = fma(w67.y, T[7][e], s1);
-                part[e] = ok ? st[S + g] * (s0 + s1) : 0.0;
-            }
-#pragma unroll
-            for (int m = 4; m <= 16; m <<= 1) {
-                part[0] += __shfl_xor_sync(0xffffffffu, part[0], m);
-                part[1] += __shfl_xor_sync(0xffffffffu, part[1], m);
-            }
-            if (g == 0) {
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int j = 2 * t + e;
-                    if (j < nvalid) ps.out[reinterpret_cast<const int*>(stage + (p + j) * RL + D * S)[1]] = part[e];
-                }
-            }
+            for (int k = 0; k < 16; ++k) dmma(z[k & 3][0], z[k & 3][1], w0[k >> 1] * ((k & 1) ? u1 : u0), hb[k]);
+            const double z0 = (z[0][0] + z[1][0]) + (z[2][0] + z[3][0]);
+            const double z1 = (z[0][1] + z[1][1]) + (z[2][1] + z[3][1]);
+            double part = fma(z0, w2.x, z1 * w2.y);
+            part += __shfl_xor_sync(0xffffffffu, part, 1);
+            part += __shfl_xor_sync(0xffffffffu, part, 2);
+            if (t == 0 && vg) ps.out[reinterpret_cast<const int*>(sg + D * S)[1]] = part;
             p += nvalid;
         }
         __syncwarp();
