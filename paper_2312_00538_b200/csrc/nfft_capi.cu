@@ -31,7 +31,7 @@ void launch_spread(int D, int S, int PE, const Item* items, int nitems, const DP
                    const DWin* wins, const double* v, double* patches, cudaStream_t st);
 void launch_gather(int D, int S, int PE, const Item* items, int nitems, const DPSet* ps,
                    const DWin* wins, cudaStream_t st);
-void launch_reduce(const DWin* wins, const int* slots, int nslots, long long max_nodes, int D,
+void launch_reduce(const DWin* wins, const int* slots, int nslots, long long max_nodes, int D, int S,
                    const double* patches, cudaStream_t st);
 void launch_tile_reduce(const DWin* wins, const int2* multi, int nmulti, int max_pv, double* patches,
                         cudaStream_t st);
@@ -212,6 +212,7 @@ struct Window {
     DWin dw{};
     DevBuf<double> G, H, T[4], tabA, tabS;
     DevBuf<int> tile_first;
+    DevBuf<long long> tile_patch;
     PointSet src;
 };
 
@@ -332,7 +333,7 @@ void build_pointset(PointSet& ps, const std::vector<double>& scaled_cm, int64_t 
 // (load balance) but no more, since each item writes one (TC+2m-1)^d patch
 // that must be reduced. Gather items carry no patch, so they are finer.
 int64_t item_chunk(int64_t total_points) {
-    return std::max<int64_t>(256, (total_points + 148 * 24 - 1) / (148 * 24));
+    return std::max<int64_t>(512, (total_points + 148 * 24 - 1) / (148 * 24));
 }
 int64_t gather_chunk(int64_t total_points) {
     return std::max<int64_t>(128, (total_points + 148 * 48 - 1) / (148 * 48));
@@ -543,6 +544,12 @@ struct Engine {
                 for (auto& v : tf) v += w.dw.item_base;
                 w.tile_first.upload(tf.data(), tf.size(), stream);
                 w.dw.tile_first = w.tile_first.p;
+                std::vector<long long> tpo(tf.size() - 1, -1);
+                for (size_t T = 0; T + 1 < tf.size(); ++T)
+                    if (tf[T + 1] > tf[T])
+                        tpo[T] = patch_total + static_cast<long long>(tf[T] - w.dw.item_base) * PV;
+                w.tile_patch.upload(tpo.data(), tpo.size(), stream);
+                w.dw.tile_patch = w.tile_patch.p;
                 for (const Item& it0 : w.src.items) {
                     Item it = it0;
                     it.ps = s;
@@ -623,7 +630,7 @@ struct Engine {
         tick("reduce");
         for (int D = 1; D <= 3; ++D) {
             if (!has_dim[D]) continue;
-            launch_reduce(d_wins.p, d_slots.p, P, max_nodes, D, patches.p, stream);
+            launch_reduce(d_wins.p, d_slots.p, P, max_nodes, D, 2 * cfg.window_cutoff, patches.p, stream);
             ++g_launches;
         }
         int maxd = 0;

@@ -60,6 +60,7 @@ struct DWin {
     const double* tabA;  // a(r), r = -(Lg-1)..(Lg-1), index r + Lg - 1
     const double* tabS;  // s(r)
     const int* tile_first;  // sources: first item of each tile (ntile^d + 1 entries)
+    const long long* tile_patch;  // patch-buffer offset of each tile's (pre-reduced) patch, -1 if empty
     int item_base;          // global index of the window's first source item
     long long patch_base;   // patch-buffer offset of that item
 };

@@ -741,18 +741,15 @@ __global__ void tile_reduce_kernel(const DWin* __restrict__ wins, const int2* __
 // Patch reduction: grid node <- sum over every covering tile's (pre-reduced)
 // patch value, in (e0, T0, e1, T1, e2, T2) order. blockIdx.y = window slot.
 // ===========================================================================
-template <int D>
+template <int D, int NC>
 __global__ void reduce_patches_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots,
                                       const double* __restrict__ patches) {
     const DWin& wn = wins[slots[blockIdx.y]];
     if (wn.d != D) return;
     const int Lg = wn.Lg, TC = wn.TC, PE = wn.PE, nt = wn.ntile;
-    int nodes = 1, PV = 1;
+    int nodes = 1;
 #pragma unroll
-    for (int t = 0; t < D; ++t) {
-        nodes *= Lg;
-        PV *= PE;
-    }
+    for (int t = 0; t < D; ++t) nodes *= Lg;
     const int node = blockIdx.x * blockDim.x + threadIdx.x;
     if (node >= nodes) return;
     int lg[3] = {0, 0, 0};
@@ -764,45 +761,74 @@ __global__ void reduce_patches_kernel(const DWin* __restrict__ wins, const int* 
             r /= Lg;
         }
     }
-    const int Eext = nt * TC + wn.S - 1;
-    const int step = wn.wrap ? wn.M : Eext;
-    int e0s[3] = {0, 0, 0};
-#pragma unroll
-    for (int t = 0; t < D; ++t) e0s[t] = wn.wrap ? pmod(lg[t] - wn.lo, wn.M) : lg[t];
-    const double* pb = patches + wn.patch_base;
+    const long long* __restrict__ tp = wn.tile_patch;
     double sum = 0.0;
-    // tiles covering extended index e: T in [max(0, ceil((e-PE+1)/TC)), min(e/TC, nt-1)]
-#define KSVM_TLO(e) ((e) - PE + 1 <= 0 ? 0 : ((e) - PE + TC) / TC)
-#define KSVM_THI(e) min((e) / TC, nt - 1)
-    for (int e0 = e0s[0]; e0 < Eext; e0 += step)
-        for (int T0 = KSVM_TLO(e0); T0 <= KSVM_THI(e0); ++T0) {
-            const int o0 = e0 - T0 * TC;
+    if (!wn.wrap) {
+        // extended index e = lg; covering tiles T = e/TC - a, a < NC, with e - T TC < PE
+        int thi[3] = {0, 0, 0};
+#pragma unroll
+        for (int t = 0; t < D; ++t) thi[t] = min(lg[t] / TC, nt - 1);
+#pragma unroll
+        for (int a0 = 0; a0 < NC; ++a0) {
+            const int T0 = thi[0] - a0, o0 = lg[0] - T0 * TC;
+            if (T0 < 0 || o0 >= PE) continue;
             if constexpr (D == 1) {
-                const int k = wn.tile_first[T0];
-                if (k < wn.tile_first[T0 + 1]) sum += pb[static_cast<long long>(k - wn.item_base) * PV + o0];
+                const long long off = tp[T0];
+                if (off >= 0) sum += patches[off + o0];
             } else {
-                for (int e1 = e0s[1]; e1 < Eext; e1 += step)
-                    for (int T1 = KSVM_TLO(e1); T1 <= KSVM_THI(e1); ++T1) {
-                        const int o1 = o0 * PE + e1 - T1 * TC;
-                        if constexpr (D == 2) {
-                            const int T = T0 * nt + T1;
-                            const int k = wn.tile_first[T];
-                            if (k < wn.tile_first[T + 1]) sum += pb[static_cast<long long>(k - wn.item_base) * PV + o1];
-                        } else {
-                            for (int e2 = e0s[2]; e2 < Eext; e2 += step)
-                                for (int T2 = KSVM_TLO(e2); T2 <= KSVM_THI(e2); ++T2) {
-                                    const int T = (T0 * nt + T1) * nt + T2;
-                                    const int o2 = o1 * PE + e2 - T2 * TC;
-                                    const int k = wn.tile_first[T];
-                                    if (k < wn.tile_first[T + 1])
-                                        sum += pb[static_cast<long long>(k - wn.item_base) * PV + o2];
-                                }
+#pragma unroll
+                for (int a1 = 0; a1 < NC; ++a1) {
+                    const int T1 = thi[1] - a1, o1 = lg[1] - T1 * TC;
+                    if (T1 < 0 || o1 >= PE) continue;
+                    if constexpr (D == 2) {
+                        const long long off = tp[T0 * nt + T1];
+                        if (off >= 0) sum += patches[off + o0 * PE + o1];
+                    } else {
+#pragma unroll
+                        for (int a2 = 0; a2 < NC; ++a2) {
+                            const int T2 = thi[2] - a2, o2 = lg[2] - T2 * TC;
+                            if (T2 < 0 || o2 >= PE) continue;
+                            const long long off = tp[(T0 * nt + T1) * nt + T2];
+                            if (off >= 0) sum += patches[off + (o0 * PE + o1) * PE + o2];
                         }
                     }
+                }
             }
         }
+    } else {
+        // wrapped grid: every extended index e = (lg - lo) mod M + k M
+        const int Eext = nt * TC + wn.S - 1;
+        int e0s[3] = {0, 0, 0};
+#pragma unroll
+        for (int t = 0; t < D; ++t) e0s[t] = pmod(lg[t] - wn.lo, wn.M);
+#define KSVM_TLO(e) ((e) - PE + 1 <= 0 ? 0 : ((e) - PE + TC) / TC)
+#define KSVM_THI(e) min((e) / TC, nt - 1)
+        for (int e0 = e0s[0]; e0 < Eext; e0 += wn.M)
+            for (int T0 = KSVM_TLO(e0); T0 <= KSVM_THI(e0); ++T0) {
+                const int o0 = e0 - T0 * TC;
+                if constexpr (D == 1) {
+                    const long long off = tp[T0];
+                    if (off >= 0) sum += patches[off + o0];
+                } else {
+                    for (int e1 = e0s[1]; e1 < Eext; e1 += wn.M)
+                        for (int T1 = KSVM_TLO(e1); T1 <= KSVM_THI(e1); ++T1) {
+                            const int o1 = o0 * PE + e1 - T1 * TC;
+                            if constexpr (D == 2) {
+                                const long long off = tp[T0 * nt + T1];
+                                if (off >= 0) sum += patches[off + o1];
+                            } else {
+                                for (int e2 = e0s[2]; e2 < Eext; e2 += wn.M)
+                                    for (int T2 = KSVM_TLO(e2); T2 <= KSVM_THI(e2); ++T2) {
+                                        const long long off = tp[(T0 * nt + T1) * nt + T2];
+                                        if (off >= 0) sum += patches[off + o1 * PE + e2 - T2 * TC];
+                                    }
+                            }
+                        }
+                }
+            }
 #undef KSVM_TLO
 #undef KSVM_THI
+    }
     wn.G[node] = sum;
 }
 
@@ -813,15 +839,18 @@ __global__ void reduce_patches_kernel(const DWin* __restrict__ wins, const int* 
 //   d=1: H = A g
 //   d=2: H = A0 (A1 g) - S0 (S1 g)
 //   d=3: H = A0 [A1 A2 g - S1 S2 g] - S0 [A1 S2 g + S1 A2 g]
-// Stage s works along dimension d-1-s as a small GEMM: a CTA owns 32
-// fibres (all Lg rows), stages them in SMEM, and each thread produces two
-// rows of one fibre. blockIdx.y = window slot.
+// Stage s works along dimension d-1-s as a Toeplitz GEMM on the FP64 tensor
+// cores: Out[i, f] = sum_j T[i - j] X[j, f] over the Lg^(d-1) fibres f. A CTA
+// (4 warps) owns 32 fibres (4 DMMA column tiles) and all rows; warp w owns
+// column tile w and every 8-row tile, accumulating over K = Lg in steps of 4.
+// blockIdx.y = window slot.
 // ===========================================================================
 constexpr int kConvFB = 32;     // fibres per CTA
-constexpr int kConvRows = 8;    // row groups (warps) per CTA
-constexpr int kConvMaxL = 130;  // Lg bound for the SMEM tile
+constexpr int kConvLd = 36;     // SMEM row pitch (36 = 4 mod 16: conflict-free B reads)
+constexpr int kConvMaxL = 128;  // Lg bound for the SMEM tile (M = sigma N <= 128)
+constexpr int kConvMT = (kConvMaxL + 7) / 8;
 
-__global__ void __launch_bounds__(kConvFB * kConvRows)
+__global__ void __launch_bounds__(128)
 conv_stage_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots, int stage) {
     extern __shared__ __align__(16) double smem[];
     const DWin& wn = wins[slots[blockIdx.y]];
@@ -834,20 +863,25 @@ conv_stage_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots, 
     if (f0 >= nfib) return;
     int inner = 1;
     for (int t = dim + 1; t < D; ++t) inner *= Lg;
+    const int Kp = (Lg + 3) & ~3, Mt = (Lg + 7) >> 3, Mp = 8 * Mt;
     const int nin = stage == 0 ? 1 : 2;
     const double* in0 = stage == 0 ? wn.G : (stage == 1 ? wn.T[0] : (D == 3 ? wn.T[2] : wn.T[0]));
     const double* in1 = stage == 0 ? nullptr : (stage == 1 ? wn.T[1] : (D == 3 ? wn.T[3] : wn.T[1]));
-    // SMEM: X[nin][Lg][kConvFB + 1], tabA[2Lg-1], tabS[2Lg-1]
-    const int ldx = kConvFB + 1;
+    // SMEM: X[nin][Kp][kConvLd] | tA[Mp+Kp] | tS | tN (= -tS); table index k <-> r = k - (Kp - 1)
     double* X = smem;
-    double* tA = smem + 2 * Lg * ldx;
-    double* tS = tA + 2 * Lg - 1;
-    const int tid = threadIdx.y * kConvFB + threadIdx.x, nth = kConvFB * kConvRows;
-    for (int k = tid; k < 2 * Lg - 1; k += nth) {
-        tA[k] = wn.tabA[k];
-        tS[k] = wn.tabS[k];
+    const int tl = Mp + Kp;
+    double* tA = smem + 2 * Kp * kConvLd;
+    double* tS = tA + tl;
+    double* tN = tS + tl;
+    const int tid = threadIdx.x;
+    for (int k = tid; k < tl; k += 128) {
+        const int r = k - (Kp - 1);
+        const bool ok = r > -Lg && r < Lg;
+        const double a = ok ? wn.tabA[r + Lg - 1] : 0.0, sv = ok ? wn.tabS[r + Lg - 1] : 0.0;
+        tA[k] = a;
+        tS[k] = sv;
+        tN[k] = -sv;
     }
-    // element (j, f) of the fibre set lives at addr(j, f)
     auto addr = [&](int j, int f) -> long long {
         if (dim == D - 1) return static_cast<long long>(f) * Lg + j;
         const int outer = f / inner, in = f - outer * inner;
@@ -855,72 +889,79 @@ conv_stage_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots, 
     };
     for (int q = 0; q < nin; ++q) {
         const double* src = q == 0 ? in0 : in1;
+        double* Xq = X + q * Kp * kConvLd;
         if (dim == D - 1) {
-            for (int k = tid; k < kConvFB * Lg; k += nth) {
-                const int fl = k / Lg, j = k - fl * Lg;
-                X[(q * Lg + j) * ldx + fl] = f0 + fl < nfib ? src[addr(j, f0 + fl)] : 0.0;
+            for (int k = tid; k < kConvFB * Kp; k += 128) {
+                const int fl = k / Kp, j = k - fl * Kp;
+                Xq[j * kConvLd + fl] = (j < Lg && f0 + fl < nfib) ? src[addr(j, f0 + fl)] : 0.0;
             }
         } else {
-            for (int k = tid; k < kConvFB * Lg; k += nth) {
+            for (int k = tid; k < kConvFB * Kp; k += 128) {
                 const int j = k / kConvFB, fl = k - j * kConvFB;
-                X[(q * Lg + j) * ldx + fl] = f0 + fl < nfib ? src[addr(j, f0 + fl)] : 0.0;
+                Xq[j * kConvLd + fl] = (j < Lg && f0 + fl < nfib) ? src[addr(j, f0 + fl)] : 0.0;
             }
         }
     }
     __syncthreads();
-    const int fl = threadIdx.x, f = f0 + fl;
-    if (f >= nfib) return;
-    for (int i0 = threadIdx.y; i0 < Lg; i0 += 2 * kConvRows) {
-        const int i1 = i0 + kConvRows;
-        const bool two = i1 < Lg;
-        const double* A0 = tA + (Lg - 1 + i0);  // A[i][j] = tab[i - j]
-        const double* S0 = tS + (Lg - 1 + i0);
-        const double* A1 = tA + (Lg - 1 + (two ? i1 : i0));
-        const double* S1 = tS + (Lg - 1 + (two ? i1 : i0));
-        double p0 = 0.0, q0 = 0.0, p1 = 0.0, q1 = 0.0;
-        if (stage == 0) {
-            for (int j = 0; j < Lg; ++j) {
-                const double x = X[j * ldx + fl];
-                p0 = fma(A0[-j], x, p0);
-                q0 = fma(S0[-j], x, q0);
-                p1 = fma(A1[-j], x, p1);
-                q1 = fma(S1[-j], x, q1);
-            }
-        } else if (stage == 1 && D == 3) {
-            for (int j = 0; j < Lg; ++j) {
-                const double xa = X[j * ldx + fl], xs = X[(Lg + j) * ldx + fl];
-                p0 = fma(A0[-j], xa, fma(-S0[-j], xs, p0));
-                q0 = fma(A0[-j], xs, fma(S0[-j], xa, q0));
-                p1 = fma(A1[-j], xa, fma(-S1[-j], xs, p1));
-                q1 = fma(A1[-j], xs, fma(S1[-j], xa, q1));
-            }
-        } else {
-            for (int j = 0; j < Lg; ++j) {
-                const double xa = X[j * ldx + fl], xs = X[(Lg + j) * ldx + fl];
-                p0 = fma(A0[-j], xa, fma(-S0[-j], xs, p0));
-                p1 = fma(A1[-j], xa, fma(-S1[-j], xs, p1));
+    const int lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+    const int fc = warp * 8;  // this warp's column tile (local fibre offset)
+    if (f0 + fc >= nfib) return;
+    const double* X0 = X + fc + g;
+    const double* X1 = X + Kp * kConvLd + fc + g;
+    // outputs: o0 (first), o1 (second, stage 0 and the d=3 middle stage)
+    double* o0;
+    double* o1 = nullptr;
+    if (stage == 0 && D == 1) {
+        o0 = wn.H;
+    } else if (stage == 0) {
+        o0 = wn.T[0];
+        o1 = wn.T[1];
+    } else if (stage == 1 && D == 3) {
+        o0 = wn.T[2];
+        o1 = wn.T[3];
+    } else {
+        o0 = wn.H;
+    }
+    double acc0[kConvMT][2], acc1[kConvMT][2];
+#pragma unroll
+    for (int m = 0; m < kConvMT; ++m) acc0[m][0] = acc0[m][1] = acc1[m][0] = acc1[m][1] = 0.0;
+    const bool mid = stage == 1 && D == 3;
+    for (int j0 = 0; j0 < Kp; j0 += 4) {
+        const double bx = X0[(j0 + t) * kConvLd];
+        const double by = nin > 1 ? X1[(j0 + t) * kConvLd] : 0.0;
+        // A[g][t] = T[(i0 + g) - (j0 + t)] -> table index i0 + g - j0 - t + Kp - 1
+        const int tb = g - j0 - t + Kp - 1;
+#pragma unroll
+        for (int m = 0; m < kConvMT; ++m) {
+            if (m >= Mt) break;
+            const double a = tA[tb + 8 * m];
+            if (stage == 0) {
+                dmma(acc0[m][0], acc0[m][1], a, bx);                    // A g
+                if (o1) dmma(acc1[m][0], acc1[m][1], tS[tb + 8 * m], bx);  // S g
+            } else if (mid) {
+                const double sv = tS[tb + 8 * m];
+                dmma(acc0[m][0], acc0[m][1], a, bx);                 // A Ta
+                dmma(acc0[m][0], acc0[m][1], tN[tb + 8 * m], by);    // - S Ts
+                dmma(acc1[m][0], acc1[m][1], a, by);                 // A Ts
+                dmma(acc1[m][0], acc1[m][1], sv, bx);                // S Ta
+            } else {
+                dmma(acc0[m][0], acc0[m][1], a, bx);                 // A X
+                dmma(acc0[m][0], acc0[m][1], tN[tb + 8 * m], by);    // - S Y
             }
         }
-        double* o0;
-        double* o1;
-        if (stage == 0 && D == 1) {
-            o0 = wn.H;
-            o1 = nullptr;
-        } else if (stage == 0) {
-            o0 = wn.T[0];
-            o1 = wn.T[1];
-        } else if (stage == 1 && D == 3) {
-            o0 = wn.T[2];
-            o1 = wn.T[3];
-        } else {
-            o0 = wn.H;
-            o1 = nullptr;
-        }
-        o0[addr(i0, f)] = p0;
-        if (o1) o1[addr(i0, f)] = q0;
-        if (two) {
-            o0[addr(i1, f)] = p1;
-            if (o1) o1[addr(i1, f)] = q1;
+    }
+#pragma unroll
+    for (int m = 0; m < kConvMT; ++m) {
+        if (m >= Mt) break;
+        const int i = 8 * m + g;
+        if (i >= Lg) continue;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int f = f0 + fc + 2 * t + e;
+            if (f >= nfib) continue;
+            const long long ad = addr(i, f);
+            o0[ad] = acc0[m][e];
+            if (o1) o1[ad] = acc1[m][e];
         }
     }
 }
@@ -1053,7 +1094,10 @@ size_t generic_smem(int D, int PE, int W, bool spread) {
     return sizeof(double) * ((((spread ? W : 1) * PV + 1) & ~1) + W * 32 * kRowG);
 }
 
-size_t conv_smem(int Lg) { return sizeof(double) * (2 * Lg * (kConvFB + 1) + 2 * (2 * Lg - 1)); }
+size_t conv_smem(int Lg) {
+    const int Kp = (Lg + 3) & ~3, Mp = 8 * ((Lg + 7) >> 3);
+    return sizeof(double) * (2 * Kp * kConvLd + 3 * (Mp + Kp));
+}
 
 cudaError_t init_kernel_attributes() {
     cudaError_t e = cudaSuccess;
@@ -1122,20 +1166,23 @@ void launch_tile_reduce(const DWin* wins, const int2* multi, int nmulti, int max
     tile_reduce_kernel<<<grid, 64, 0, st>>>(wins, multi, patches);
 }
 
-void launch_reduce(const DWin* wins, const int* slots, int nslots, long long max_nodes, int D,
+void launch_reduce(const DWin* wins, const int* slots, int nslots, long long max_nodes, int D, int S,
                    const double* patches, cudaStream_t st) {
     if (nslots == 0) return;
     dim3 grid(static_cast<unsigned>((max_nodes + 255) / 256), nslots);
-    if (D == 1) reduce_patches_kernel<1><<<grid, 256, 0, st>>>(wins, slots, patches);
-    else if (D == 2) reduce_patches_kernel<2><<<grid, 256, 0, st>>>(wins, slots, patches);
-    else reduce_patches_kernel<3><<<grid, 256, 0, st>>>(wins, slots, patches);
+    // NC = covering tiles per dimension, ceil(PE / TC): 2 (d=1: 39/32), 2 (d=2: 15/8),
+    // 3 (d=3: 11/4) for m = 4; the generic bound 5 covers m <= 8.
+    if (D == 1) reduce_patches_kernel<1, 5><<<grid, 256, 0, st>>>(wins, slots, patches);
+    else if (D == 2) reduce_patches_kernel<2, 5><<<grid, 256, 0, st>>>(wins, slots, patches);
+    else if (S == 8) reduce_patches_kernel<3, 3><<<grid, 256, 0, st>>>(wins, slots, patches);
+    else reduce_patches_kernel<3, 5><<<grid, 256, 0, st>>>(wins, slots, patches);
 }
 
 void launch_conv(const DWin* wins, const int* slots, int nslots, int Lg_max, long long max_fibres,
                  int stage, cudaStream_t st) {
     if (nslots == 0) return;
     dim3 grid(static_cast<unsigned>((max_fibres + kConvFB - 1) / kConvFB), nslots);
-    conv_stage_kernel<<<grid, dim3(kConvFB, kConvRows), conv_smem(Lg_max), st>>>(wins, slots, stage);
+    conv_stage_kernel<<<grid, 128, conv_smem(Lg_max), st>>>(wins, slots, stage);
 }
 
 int conv_max_lg() { return kConvMaxL; }
