@@ -428,6 +428,7 @@ struct Engine {
         if (stream) {
             cudaSetDevice(device);
             cudaStreamSynchronize(stream);
+            drop_graphs();
             cudaStreamDestroy(stream);
             cudaEventDestroy(ev_in);
             cudaEventDestroy(ev_out);
@@ -680,6 +681,73 @@ struct Engine {
         return last_nticks - 1;
     }
 
+    // ---- CUDA graph of the whole apply, cached per (v, y, timing) ----------
+    struct GraphEntry {
+        const double* v;
+        double* y;
+        bool timed;
+        cudaGraphExec_t exec;
+        int nticks;
+        int64_t launches;
+        const char* names[kMaxTicks];
+    };
+    std::vector<GraphEntry> graphs;  // most recent last; at most kMaxGraphs
+    static constexpr size_t kMaxGraphs = 8;
+    bool use_graphs = std::getenv("KSVM_NFFT_NO_GRAPH") == nullptr;
+
+    void drop_graphs() {
+        for (auto& gph : graphs) cudaGraphExecDestroy(gph.exec);
+        graphs.clear();
+    }
+
+    // One apply: replays a captured graph (one launch) or captures it first.
+    void apply(const double* v, double* y) {
+        if (!use_graphs || P_owned() == 0) {
+            run_apply(v, y);
+            return;
+        }
+        for (size_t k = 0; k < graphs.size(); ++k) {
+            GraphEntry& gph = graphs[k];
+            if (gph.v == v && gph.y == y && gph.timed == stage_timing) {
+                CK(cudaGraphLaunch(gph.exec, stream));
+                g_launches += gph.launches;
+                last_nticks = gph.nticks;
+                for (int i = 0; i < gph.nticks; ++i) tick_name[i] = gph.names[i];
+                if (k + 1 != graphs.size()) std::rotate(graphs.begin() + k, graphs.begin() + k + 1, graphs.end());
+                return;
+            }
+        }
+        cudaGraph_t graph = nullptr;
+        const int64_t before = g_launches.load();
+        CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            run_apply(v, y);
+        } catch (...) {
+            cudaStreamEndCapture(stream, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            throw;
+        }
+        CK(cudaStreamEndCapture(stream, &graph));
+        GraphEntry gph{};
+        gph.v = v;
+        gph.y = y;
+        gph.timed = stage_timing;
+        gph.launches = g_launches.load() - before;
+        g_launches -= gph.launches;  // counted when launched
+        gph.nticks = last_nticks;
+        for (int i = 0; i < last_nticks; ++i) gph.names[i] = tick_name[i];
+        const cudaError_t e = cudaGraphInstantiate(&gph.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        CK(e);
+        if (graphs.size() >= kMaxGraphs) {
+            cudaGraphExecDestroy(graphs.front().exec);
+            graphs.erase(graphs.begin());
+        }
+        graphs.push_back(gph);
+        CK(cudaGraphLaunch(gph.exec, stream));
+        g_launches += gph.launches;
+    }
+
     // Host/device dispatch shared by every apply-like entry point.
     template <typename F>
     void with_io(const double* v, double* y, int ptr_kind, void* ext_stream, int64_t vin,
@@ -854,7 +922,7 @@ int ksvm_nfft_op_apply(const ksvm_nfft_op* op, const double* v, double* y, int p
     return guarded([&] {
         if (!op || !v || !y) throw std::invalid_argument("null argument");
         Engine& E = const_cast<Engine&>(op->e);
-        E.with_io(v, y, ptr_kind, stream, E.n, E.n, [&](const double* dv, double* dy) { E.run_apply(dv, dy); });
+        E.with_io(v, y, ptr_kind, stream, E.n, E.n, [&](const double* dv, double* dy) { E.apply(dv, dy); });
     });
 }
 
@@ -866,7 +934,7 @@ int ksvm_nfft_op_apply_batch(const ksvm_nfft_op* op, const double* V, double* Y,
         if (ld < E.n) throw std::invalid_argument("ld must be >= n");
         for (int c = 0; c < k; ++c)
             E.with_io(V + c * ld, Y + c * ld, ptr_kind, stream, E.n, E.n,
-                      [&](const double* dv, double* dy) { E.run_apply(dv, dy); });
+                      [&](const double* dv, double* dy) { E.run_apply(dv, dy); });  // pointers vary: eager
     });
 }
 
@@ -1027,7 +1095,7 @@ int ksvm_nfft_plan_apply(const ksvm_nfft_plan* plan, const double* v, double* ou
     return guarded([&] {
         if (!plan || !v || !out) throw std::invalid_argument("null argument");
         Engine& E = const_cast<Engine&>(plan->e);
-        E.with_io(v, out, ptr_kind, stream, E.n, E.n, [&](const double* dv, double* dy) { E.run_apply(dv, dy); });
+        E.with_io(v, out, ptr_kind, stream, E.n, E.n, [&](const double* dv, double* dy) { E.apply(dv, dy); });
     });
 }
 
