@@ -606,7 +606,8 @@ struct Engine {
     void tick(const char* name) {
         if (!stage_timing || nticks >= kMaxTicks) return;
         tick_name[nticks] = name;
-        CK(cudaEventRecord(ev_stage[nticks], stream));
+        // external event node when captured into a graph, so the event stays timeable
+        CK(cudaEventRecordWithFlags(ev_stage[nticks], stream, capturing ? cudaEventRecordExternal : 0));
         ++nticks;
     }
 
@@ -694,6 +695,7 @@ struct Engine {
     std::vector<GraphEntry> graphs;  // most recent last; at most kMaxGraphs
     static constexpr size_t kMaxGraphs = 8;
     bool use_graphs = std::getenv("KSVM_NFFT_NO_GRAPH") == nullptr;
+    bool capturing = false;
 
     void drop_graphs() {
         for (auto& gph : graphs) cudaGraphExecDestroy(gph.exec);
@@ -702,6 +704,7 @@ struct Engine {
 
     // One apply: replays a captured graph (one launch) or captures it first.
     void apply(const double* v, double* y) {
+        (void)cudaGetLastError();  // a stale error must not be blamed on this apply
         if (!use_graphs || P_owned() == 0) {
             run_apply(v, y);
             return;
@@ -720,9 +723,12 @@ struct Engine {
         cudaGraph_t graph = nullptr;
         const int64_t before = g_launches.load();
         CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+        capturing = true;
         try {
             run_apply(v, y);
+            capturing = false;
         } catch (...) {
+            capturing = false;
             cudaStreamEndCapture(stream, &graph);
             if (graph) cudaGraphDestroy(graph);
             throw;
