@@ -101,7 +101,8 @@ class Lib:
             for name, args in {"random_points": [C.c_int64, C.c_int64, C.c_uint64, C.c_double, _dp],
                                "random_vector": [C.c_int64, C.c_uint64, _dp],
                                "uniform": [C.c_int64, C.c_uint64, C.c_double, C.c_double, _dp],
-                               "bernoulli": [C.c_int64, C.c_uint64, C.c_double, _dp]}.items():
+                               "bernoulli": [C.c_int64, C.c_uint64, C.c_double, _dp],
+                               "fft": [_dp, _dp, C.c_int, _ip, C.c_int]}.items():
                 f = getattr(L, "oracle_" + name)
                 f.restype = None
                 f.argtypes = args
@@ -232,6 +233,16 @@ def bernoulli(n, seed, p) -> np.ndarray:
     L = Lib("oracle").L
     out = np.empty(n)
     L.oracle_bernoulli(n, seed, p, _ptr(out))
+    return out
+
+
+def fft(x: np.ndarray, sign: int = -1) -> np.ndarray:
+    """Unnormalised multi-dimensional DFT of the oracle (FFTW sign convention)."""
+    L = Lib("oracle").L
+    a = np.ascontiguousarray(x, dtype=np.complex128)
+    out = np.empty_like(a)
+    dims = np.ascontiguousarray(a.shape, dtype=np.int32)
+    L.oracle_fft(a.ctypes.data_as(_dp), out.ctypes.data_as(_dp), a.ndim, dims.ctypes.data_as(_ip), sign)
     return out
 
 

@@ -368,6 +368,13 @@ double oracle_anova_entry(const oracle_anova* op, int64_t i, int64_t j) {
 
 void oracle_anova_free(oracle_anova* op) { delete op; }
 
+// The exact DFT behind both the restatement and the FFTW shim (offt.hpp),
+// exposed so tests can pin it against numpy.fft. in/out: interleaved complex.
+void oracle_fft(const double* in, double* out, int rank, const int* dims, int sign) {
+    offt::PlanND(std::vector<int>(dims, dims + rank), sign)
+        .execute(reinterpret_cast<const offt::cd*>(in), reinterpret_cast<offt::cd*>(out));
+}
+
 // P:tests/helpers.hpp:15-31
 void oracle_random_points(int64_t n, int64_t d, uint64_t seed, double scale, double* out) {
     std::mt19937_64 rng(seed);

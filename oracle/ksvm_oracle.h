@@ -58,6 +58,7 @@ void oracle_random_points(int64_t n, int64_t d, uint64_t seed, double scale, dou
 void oracle_random_vector(int64_t n, uint64_t seed, double* out);
 void oracle_uniform(int64_t n, uint64_t seed, double lo, double hi, double* out);
 void oracle_bernoulli(int64_t n, uint64_t seed, double p, double* out);
+void oracle_fft(const double* in, double* out, int rank, const int* dims, int sign);
 
 #ifdef __cplusplus
 }

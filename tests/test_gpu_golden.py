@@ -1,0 +1,106 @@
+"""GPU: the B200 path against the committed golden fixtures (outputs of the
+reference's own fastsum.cpp, tests/golden/make_golden.py), plus edge cases.
+
+Tolerance: relative l2 <= 1e-10 (fp64, BASELINE.json north_star).
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from paper_2312_00538_b200 import (AnovaKernelSpec, Dataset, DomainError, FastsumConfig,
+                                   FeatureWindowing, _lib, anova_fast_operator, apply_fastsum,
+                                   apply_fastsum_cross, plan_fastsum)
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def windows_of(g):
+    wins, off = [], 0
+    for s in g["win_sizes"]:
+        wins.append([int(x) for x in g["win_features"][off:off + s]])
+        off += s
+    return wins
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p) for p in GOLDEN])
+def test_golden(path):
+    g = np.load(path)
+    cfg = FastsumConfig(int(g["N"]), int(g["m"]), int(g["sigma"]), float(g["rT"]))
+    if str(g["kind"]) == "plan":
+        p = plan_fastsum(g["points"], float(g["ell"]), cfg, float(g["fit"]))
+        assert rel(apply_fastsum(p, g["v"]), g["y"]) <= TOL
+        assert p.scaled_length() == float(g["scaled_length"])
+        assert p.coefficient_sum() == pytest.approx(float(g["coefficient_sum"]), rel=1e-12)
+        if "targets" in g:
+            assert rel(apply_fastsum_cross(p, g["targets"], g["v"]), g["y_cross"]) <= TOL
+    else:
+        spec = AnovaKernelSpec(FeatureWindowing(windows_of(g), list(g["weights"]), list(g["ells"])))
+        op = anova_fast_operator(Dataset(g["points"]), spec, cfg, float(g["fit"]))
+        assert rel(op.apply(g["v"]), g["y"]) <= TOL
+        assert op.entry(3, 8) == pytest.approx(float(g["entry_3_8"]), rel=1e-14)
+
+
+def test_device_pointer_path_matches_host_path():
+    import torch
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "ref_cfg2_n3000.npz"))
+    spec = AnovaKernelSpec(FeatureWindowing(windows_of(g), list(g["weights"]), list(g["ells"])))
+    op = anova_fast_operator(Dataset(g["points"]), spec, fit_fraction=float(g["fit"]))
+    host = op.apply(g["v"])
+    vd = torch.from_numpy(g["v"]).cuda()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        yd = op.apply(vd)
+        y2 = torch.empty_like(vd)
+        op.apply_into(vd, y2)
+    torch.cuda.synchronize()
+    assert np.array_equal(yd.cpu().numpy(), host)
+    assert np.array_equal(y2.cpu().numpy(), host)
+    assert rel(host, g["y"]) <= TOL
+
+
+def test_apply_batch_equals_single_applies():
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "ref_cfg1.npz"))
+    spec = AnovaKernelSpec(FeatureWindowing(windows_of(g), list(g["weights"]), list(g["ells"])))
+    op = anova_fast_operator(Dataset(g["points"]), spec, fit_fraction=float(g["fit"]))
+    rng = np.random.default_rng(5)
+    V = rng.standard_normal((g["points"].shape[0], 5))
+    Y = op.apply_batch(V)
+    for c in range(5):
+        assert np.array_equal(Y[:, c], op.apply(V[:, c]))
+
+
+def test_edge_cases():
+    # one point; identical points (radius 0 -> scale 1, P:src/fastsum.cpp:134); zero vector
+    p = plan_fastsum(np.array([[0.1, -0.2]]), 1.0)
+    assert apply_fastsum(p, np.array([2.0]))[0] == pytest.approx(2.0 * p.coefficient_sum(), rel=1e-3)
+    import oracle
+    z = np.zeros((5, 2))
+    assert rel(apply_fastsum(plan_fastsum(z, 1.0), np.arange(5.0)),
+               oracle.Lib("oracle").plan(z).apply(np.arange(5.0))) <= TOL
+    pts = oracle.random_points(50, 3, 1)
+    assert np.linalg.norm(apply_fastsum(plan_fastsum(pts, 1.0), np.zeros(50))) == 0.0
+    # empty cross-target set; a target on the ball boundary is admissible
+    p = plan_fastsum(pts, 1.0)
+    assert apply_fastsum_cross(p, np.zeros((0, 3)), np.ones(50)).shape == (0,)
+    s = p.scale_points(pts)
+    with pytest.raises(DomainError):
+        apply_fastsum_cross(p, pts * 10, np.ones(50))
+    with pytest.raises(ValueError):
+        apply_fastsum(p, np.ones(49))
+
+
+def test_launch_counter_and_kernels_run():
+    before = _lib.launch_count()
+    import oracle
+    pts = oracle.random_points(300, 3, 3)
+    apply_fastsum(plan_fastsum(pts, 1.0), np.ones(300))
+    assert _lib.launch_count() > before

@@ -1,0 +1,143 @@
+"""CPU: host logic of the B200 path that runs without a GPU.
+
+* libksvm_nfft.so loads and exports every entry point include/ksvm_nfft.h
+  declares; config validation mirrors P:src/fastsum.cpp:38-47; creating a
+  plan without a CUDA device fails loudly (no CPU fallback).
+* The Python mirror validates arguments like the reference API.
+* Workload generators produce the BASELINE shapes.
+* Window sharding: LPT assignment, and a world_size-2 gloo
+  run whose all-reduced partial sums equal the full ANOVA matvec (oracle
+  operators stand in for the per-rank GPU operators on this CPU box).
+"""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2312_00538_b200 import (AnovaKernelSpec, Dataset, FastsumConfig, FeatureWindowing, _lib,
+                                   anova_fast_operator, plan_fastsum, sharding, workloads)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    text = open(os.path.join(ROOT, "include", "ksvm_nfft.h")).read()
+    return sorted(set(re.findall(r"\b(ksvm_nfft_\w+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = ctypes.CDLL(_lib.LIB_PATH)
+    names = declared_symbols()
+    assert len(names) >= 20
+    for name in names:
+        assert hasattr(L, name), name
+    assert set(names) <= set(_lib.EXPORTED) | {"ksvm_nfft_version", "ksvm_nfft_launch_count"}
+
+
+def test_config_validation_mirrors_reference():
+    FastsumConfig().validate()
+    for kw in (dict(bandwidth=15), dict(bandwidth=0), dict(torus_radius=0.3), dict(torus_radius=0.0),
+               dict(window_cutoff=1), dict(window_cutoff=9), dict(oversampling=0)):
+        with pytest.raises(ValueError):
+            FastsumConfig(**kw).validate()
+
+
+def _has_gpu():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+@pytest.mark.skipif(_has_gpu(), reason="checks the no-device error path")
+def test_no_silent_cpu_fallback():
+    with pytest.raises(RuntimeError):
+        plan_fastsum(np.zeros((4, 2)), 1.0)
+    with pytest.raises(RuntimeError):
+        anova_fast_operator(Dataset(np.zeros((4, 3))), AnovaKernelSpec(FeatureWindowing.explicit([[0, 1, 2]])))
+
+
+def test_argument_errors_before_device():
+    # shape/window errors are reported as invalid_argument (ValueError) like the reference
+    with pytest.raises(ValueError):
+        plan_fastsum(np.zeros((4, 4)), 1.0)  # d > 3
+    with pytest.raises(ValueError):
+        plan_fastsum(np.zeros((0, 2)), 1.0)  # empty
+    with pytest.raises(ValueError):
+        plan_fastsum(np.zeros((4, 2)), 1.0, fit_fraction=1.5)
+    bad = AnovaKernelSpec(FeatureWindowing([[0, 1], [1, 2]], [0.5, 0.5], [1.0, 1.0]))
+    with pytest.raises(ValueError):
+        anova_fast_operator(Dataset(np.zeros((4, 3))), bad)  # feature in two windows
+    bad = AnovaKernelSpec(FeatureWindowing([[0, 1, 2, 3]], [1.0], [1.0]))
+    with pytest.raises(ValueError):
+        anova_fast_operator(Dataset(np.zeros((4, 4))), bad)  # window of 4
+
+
+@pytest.mark.parametrize("cfg,n", [(1, None), (2, 5000), (3, 4000), (4, 4000), (5, 4000)])
+def test_workloads(cfg, n):
+    w = workloads.make(cfg, n)
+    expect = {1: (6, 2), 2: (8, 3), 3: (22, 8), 4: (54, 18), 5: (28, 10)}[cfg]
+    assert (w.d, len(w.windows)) == expect
+    assert w.points.min() >= -0.25 - 1e-15 and w.points.max() <= 0.25 + 1e-15
+    flat = [f for win in w.windows for f in win]
+    assert sorted(flat) == list(range(w.d))
+    assert w.v.shape == (w.n,)
+    assert w.hbm_bytes() == 8 * w.n * (2 * w.D + 2)
+
+
+def test_lpt_assignment():
+    costs = sharding.window_costs([[0, 1, 2]] * 9 + [[27]])
+    for world in (1, 2, 4, 8):
+        owner = sharding.lpt_assign(costs, world)
+        assert sorted(set(owner)) == list(range(min(world, len(costs))))
+        loads = [sum(c for c, o in zip(costs, owner) if o == r) for r in range(world)]
+        assert max(loads) - min(loads) <= max(costs)
+    assert sharding.lpt_assign(costs, 3) == sharding.lpt_assign(costs, 3)  # deterministic
+
+
+def _sharded_worker(rank, world, port, result_path):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    w = workloads.config2(n=1500)
+    lib = oracle.Lib("oracle")
+
+    class Local:
+        """Oracle stand-in for the rank's GPU operator over its owned windows."""
+
+        def __init__(self, mask):
+            self.ops = [(lib.anova(w.points, [win], [1.0 / len(w.windows)], [1.0]), m)
+                        for win, m in zip(w.windows, mask)]
+
+        def apply(self, v):
+            y = np.zeros_like(v)
+            for op, m in self.ops:
+                if m:
+                    y += op.apply(v)
+            return y
+
+    op = sharding.ShardedAnovaOperator(w.windows, rank, world, Local, sharding.numpy_allreduce_via_torch)
+    y = op.apply(w.v)
+    if rank == 0:
+        np.save(result_path, y)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_window_sharding_gloo_world2(tmp_path):
+    import socket
+
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = str(tmp_path / "y.npy")
+    mp.spawn(_sharded_worker, args=(2, port, out), nprocs=2, join=True)
+    w = workloads.config2(n=1500)
+    full = oracle.Lib("oracle").anova(w.points, w.windows).apply(w.v)
+    y = np.load(out)
+    assert np.linalg.norm(y - full) <= 1e-13 * np.linalg.norm(full)
