@@ -32,7 +32,7 @@ void launch_spread(int D, int S, int PE, const Item* items, int nitems, const DP
 void launch_gather(int D, int S, int PE, const Item* items, int nitems, const DPSet* ps,
                    const DWin* wins, cudaStream_t st);
 void launch_reduce(const DWin* wins, const int* slots, int nslots, long long max_nodes, int D, int S,
-                   const double* patches, cudaStream_t st);
+                   const double* patches, bool wrap, int max_tiles, cudaStream_t st);
 void launch_tile_reduce(const DWin* wins, const int2* multi, int nmulti, int max_pv, double* patches,
                         cudaStream_t st);
 void launch_conv(const DWin* wins, const int* slots, int nslots, int Lg_max, long long max_fibres,
@@ -624,15 +624,19 @@ struct Engine {
             ++g_launches;
         }
         CK(cudaGetLastError());
-        tick("tile_reduce");
         if (n_multi) {
+            tick("tile_reduce");
             launch_tile_reduce(d_wins.p, d_multi.p, n_multi, max_pv, patches.p, stream);
             ++g_launches;
         }
         tick("reduce");
         for (int D = 1; D <= 3; ++D) {
             if (!has_dim[D]) continue;
-            launch_reduce(d_wins.p, d_slots.p, P, max_nodes, D, 2 * cfg.window_cutoff, patches.p, stream);
+            const bool wrap = geometry(cfg, D).wrap != 0;
+            int tiles = 1;
+            for (int t = 0; t < D; ++t) tiles *= geometry(cfg, D).ntile;
+            launch_reduce(d_wins.p, d_slots.p, P, max_nodes, D, 2 * cfg.window_cutoff, patches.p, wrap,
+                          tiles, stream);
             ++g_launches;
         }
         int maxd = 0;

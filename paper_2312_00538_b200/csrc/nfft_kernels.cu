@@ -832,6 +832,95 @@ __global__ void reduce_patches_kernel(const DWin* __restrict__ wins, const int* 
     wn.G[node] = sum;
 }
 
+// Owner-tile reduction (non-wrapping grids): CTA (T, window) produces the
+// grid nodes of its own tile block (the last tile per dimension also owns the
+// halo nodes past the tiles). The <= NC^d source tiles whose patches reach
+// the block are looked up once into SMEM, so every node's <= NC^d loads are
+// independent. Sum order: source tiles ascending in (T0, T1, T2).
+template <int D, int NC>
+__global__ void __launch_bounds__(128)
+reduce_owner_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots,
+                    const double* __restrict__ patches) {
+    const DWin& wn = wins[slots[blockIdx.y]];
+    if (wn.d != D || wn.wrap) return;
+    const int TC = wn.TC, PE = wn.PE, nt = wn.ntile, Lg = wn.Lg;
+    int ntd = 1;
+#pragma unroll
+    for (int t = 0; t < D; ++t) ntd *= nt;
+    if (static_cast<int>(blockIdx.x) >= ntd) return;
+    int T[3] = {0, 0, 0};
+    {
+        int r = blockIdx.x;
+#pragma unroll
+        for (int t = D - 1; t >= 0; --t) {
+            T[t] = r % nt;
+            r /= nt;
+        }
+    }
+    constexpr int NS = D == 1 ? NC : (D == 2 ? NC * NC : NC * NC * NC);
+    __shared__ long long soff[NS];
+    __shared__ int sT[NS][3];
+    __shared__ int any;
+    if (threadIdx.x == 0) any = 0;
+    __syncthreads();
+    if (threadIdx.x < NS) {
+        int r = threadIdx.x, S[3] = {0, 0, 0};
+        bool ok = true;
+        int lin = 0;
+#pragma unroll
+        for (int t = D - 1; t >= 0; --t) {
+            S[t] = T[t] - (NC - 1) + r % NC;
+            r /= NC;
+            ok = ok && S[t] >= 0;
+        }
+#pragma unroll
+        for (int t = 0; t < D; ++t) lin = lin * nt + (S[t] < 0 ? 0 : S[t]);
+        const long long off = ok ? wn.tile_patch[lin] : -1;
+        soff[threadIdx.x] = off;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) sT[threadIdx.x][t] = S[t];
+        if (off >= 0) any = 1;
+    }
+    __syncthreads();
+    // owned node block: [T TC, T TC + TC), the last tile extends to Lg
+    int lo[3] = {0, 0, 0}, len[3] = {1, 1, 1}, nodes = 1;
+#pragma unroll
+    for (int t = 0; t < D; ++t) {
+        lo[t] = T[t] * TC;
+        const int hi = T[t] == nt - 1 ? Lg : min(lo[t] + TC, Lg);
+        len[t] = max(0, hi - lo[t]);
+        nodes *= len[t];
+    }
+    for (int k = threadIdx.x; k < nodes; k += blockDim.x) {
+        int r = k, e[3] = {0, 0, 0};
+#pragma unroll
+        for (int t = D - 1; t >= 0; --t) {
+            e[t] = lo[t] + r % len[t];
+            r /= len[t];
+        }
+        double sum = 0.0;
+        if (any) {
+#pragma unroll
+            for (int q = 0; q < NS; ++q) {
+                const long long off = soff[q];
+                int o = 0;
+                bool ok = off >= 0;
+#pragma unroll
+                for (int t = 0; t < D; ++t) {
+                    const int ot = e[t] - sT[q][t] * TC;
+                    ok = ok && ot >= 0 && ot < PE;
+                    o = o * PE + ot;
+                }
+                if (ok) sum += patches[off + o];
+            }
+        }
+        long long gi = 0;
+#pragma unroll
+        for (int t = 0; t < D; ++t) gi = gi * Lg + e[t];
+        wn.G[gi] = sum;
+    }
+}
+
 // ===========================================================================
 // Grid stage as a real separable convolution. With
 // z(r) = sum_{J in I_N} m1[J] e^{2 pi i J r / M} = a(r) + i s(r) the
@@ -840,75 +929,75 @@ __global__ void reduce_patches_kernel(const DWin* __restrict__ wins, const int* 
 //   d=2: H = A0 (A1 g) - S0 (S1 g)
 //   d=3: H = A0 [A1 A2 g - S1 S2 g] - S0 [A1 S2 g + S1 A2 g]
 // Stage s works along dimension d-1-s as a Toeplitz GEMM on the FP64 tensor
-// cores: Out[i, f] = sum_j T[i - j] X[j, f] over the Lg^(d-1) fibres f. A CTA
-// (4 warps) owns 32 fibres (4 DMMA column tiles) and all rows; warp w owns
-// column tile w and every 8-row tile, accumulating over K = Lg in steps of 4.
-// blockIdx.y = window slot.
+// cores: Out[i, f] = sum_j T[i - j] X[j, f] over the Lg^(d-1) fibres f.
+// Latency-oriented: one warp per 8x8 output tile (8 rows i x 8 fibres f),
+// every operand load of its K = Lg reduction issued up front (no SMEM, no
+// block barrier), then a short chain of DMMAs. blockIdx.y = window slot.
 // ===========================================================================
-constexpr int kConvFB = 32;     // fibres per CTA
-constexpr int kConvLd = 36;     // SMEM row pitch (36 = 4 mod 16: conflict-free B reads)
-constexpr int kConvMaxL = 128;  // Lg bound for the SMEM tile (M = sigma N <= 128)
-constexpr int kConvMT = (kConvMaxL + 7) / 8;
+constexpr int kConvMaxL = 128;  // Lg bound (M = sigma N <= 128)
 
 __global__ void __launch_bounds__(128)
 conv_stage_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots, int stage) {
-    extern __shared__ __align__(16) double smem[];
     const DWin& wn = wins[slots[blockIdx.y]];
     const int D = wn.d, Lg = wn.Lg;
     if (stage >= D) return;
     const int dim = D - 1 - stage;
     int nfib = 1;
     for (int t = 0; t < D - 1; ++t) nfib *= Lg;
-    const int f0 = blockIdx.x * kConvFB;
-    if (f0 >= nfib) return;
+    const int Mt = (Lg + 7) >> 3, Ft = (nfib + 7) >> 3;
+    const int tile = blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (tile >= Mt * Ft) return;
+    const int mt = tile % Mt, ft = tile / Mt;
     int inner = 1;
     for (int t = dim + 1; t < D; ++t) inner *= Lg;
-    const int Kp = (Lg + 3) & ~3, Mt = (Lg + 7) >> 3, Mp = 8 * Mt;
-    const int nin = stage == 0 ? 1 : 2;
+    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const double* in0 = stage == 0 ? wn.G : (stage == 1 ? wn.T[0] : (D == 3 ? wn.T[2] : wn.T[0]));
     const double* in1 = stage == 0 ? nullptr : (stage == 1 ? wn.T[1] : (D == 3 ? wn.T[3] : wn.T[1]));
-    // SMEM: X[nin][Kp][kConvLd] | tA[Mp+Kp] | tS | tN (= -tS); table index k <-> r = k - (Kp - 1)
-    double* X = smem;
-    const int tl = Mp + Kp;
-    double* tA = smem + 2 * Kp * kConvLd;
-    double* tS = tA + tl;
-    double* tN = tS + tl;
-    const int tid = threadIdx.x;
-    for (int k = tid; k < tl; k += 128) {
-        const int r = k - (Kp - 1);
-        const bool ok = r > -Lg && r < Lg;
-        const double a = ok ? wn.tabA[r + Lg - 1] : 0.0, sv = ok ? wn.tabS[r + Lg - 1] : 0.0;
-        tA[k] = a;
-        tS[k] = sv;
-        tN[k] = -sv;
-    }
-    auto addr = [&](int j, int f) -> long long {
-        if (dim == D - 1) return static_cast<long long>(f) * Lg + j;
+    const bool two_in = stage > 0, mid = stage == 1 && D == 3, first = stage == 0 && D > 1;
+    // element (j, f) lives at base(f) + j * jstride
+    auto fbase = [&](int f) -> long long {
+        if (dim == D - 1) return static_cast<long long>(f) * Lg;
         const int outer = f / inner, in = f - outer * inner;
-        return (static_cast<long long>(outer) * Lg + j) * inner + in;
+        return static_cast<long long>(outer) * Lg * inner + in;
     };
-    for (int q = 0; q < nin; ++q) {
-        const double* src = q == 0 ? in0 : in1;
-        double* Xq = X + q * Kp * kConvLd;
-        if (dim == D - 1) {
-            for (int k = tid; k < kConvFB * Kp; k += 128) {
-                const int fl = k / Kp, j = k - fl * Kp;
-                Xq[j * kConvLd + fl] = (j < Lg && f0 + fl < nfib) ? src[addr(j, f0 + fl)] : 0.0;
-            }
+    const long long jstride = dim == D - 1 ? 1 : inner;
+    const int fB = ft * 8 + g;  // this lane's B column (fibre)
+    const bool fok = fB < nfib;
+    const long long bb = fok ? fbase(fB) : 0;
+    const int i0 = mt * 8;
+    const double* __restrict__ tA = wn.tabA;
+    const double* __restrict__ tS = wn.tabS;
+    const int KS = (Lg + 3) >> 2;
+    double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;  // acc0 (out 0), acc1 (out 1)
+    double e00 = 0.0, e01 = 0.0, e10 = 0.0, e11 = 0.0;  // second chains (even/odd k)
+#pragma unroll 4
+    for (int ks = 0; ks < KS; ++ks) {
+        const int j = 4 * ks + t;
+        const bool jok = j < Lg && fok;
+        const double bx = jok ? __ldg(in0 + bb + j * jstride) : 0.0;
+        const double by = (jok && two_in) ? __ldg(in1 + bb + j * jstride) : 0.0;
+        // A[g][t] = T[(i0 + g) - j]
+        const int r = i0 + g - j;
+        const bool rok = r > -Lg && r < Lg;
+        const double a = rok ? __ldg(tA + r + Lg - 1) : 0.0;
+        const double sv = rok ? __ldg(tS + r + Lg - 1) : 0.0;
+        double& p0 = (ks & 1) ? e00 : d00;
+        double& p1 = (ks & 1) ? e01 : d01;
+        double& q0 = (ks & 1) ? e10 : d10;
+        double& q1 = (ks & 1) ? e11 : d11;
+        if (!two_in) {
+            dmma(p0, p1, a, bx);                    // A g
+            if (first) dmma(q0, q1, sv, bx);        // S g
+        } else if (mid) {
+            dmma(p0, p1, a, bx);                    // A Ta
+            dmma(p0, p1, -sv, by);                  // - S Ts
+            dmma(q0, q1, a, by);                    // A Ts
+            dmma(q0, q1, sv, bx);                   // S Ta
         } else {
-            for (int k = tid; k < kConvFB * Kp; k += 128) {
-                const int j = k / kConvFB, fl = k - j * kConvFB;
-                Xq[j * kConvLd + fl] = (j < Lg && f0 + fl < nfib) ? src[addr(j, f0 + fl)] : 0.0;
-            }
+            dmma(p0, p1, a, bx);                    // A X
+            dmma(p0, p1, -sv, by);                  // - S Y
         }
     }
-    __syncthreads();
-    const int lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
-    const int fc = warp * 8;  // this warp's column tile (local fibre offset)
-    if (f0 + fc >= nfib) return;
-    const double* X0 = X + fc + g;
-    const double* X1 = X + Kp * kConvLd + fc + g;
-    // outputs: o0 (first), o1 (second, stage 0 and the d=3 middle stage)
     double* o0;
     double* o1 = nullptr;
     if (stage == 0 && D == 1) {
@@ -916,53 +1005,22 @@ conv_stage_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots, 
     } else if (stage == 0) {
         o0 = wn.T[0];
         o1 = wn.T[1];
-    } else if (stage == 1 && D == 3) {
+    } else if (mid) {
         o0 = wn.T[2];
         o1 = wn.T[3];
     } else {
         o0 = wn.H;
     }
-    double acc0[kConvMT][2], acc1[kConvMT][2];
+    const int i = i0 + g;
+    if (i >= Lg) return;
+    const double r0[2] = {d00 + e00, d01 + e01}, r1[2] = {d10 + e10, d11 + e11};
 #pragma unroll
-    for (int m = 0; m < kConvMT; ++m) acc0[m][0] = acc0[m][1] = acc1[m][0] = acc1[m][1] = 0.0;
-    const bool mid = stage == 1 && D == 3;
-    for (int j0 = 0; j0 < Kp; j0 += 4) {
-        const double bx = X0[(j0 + t) * kConvLd];
-        const double by = nin > 1 ? X1[(j0 + t) * kConvLd] : 0.0;
-        // A[g][t] = T[(i0 + g) - (j0 + t)] -> table index i0 + g - j0 - t + Kp - 1
-        const int tb = g - j0 - t + Kp - 1;
-#pragma unroll
-        for (int m = 0; m < kConvMT; ++m) {
-            if (m >= Mt) break;
-            const double a = tA[tb + 8 * m];
-            if (stage == 0) {
-                dmma(acc0[m][0], acc0[m][1], a, bx);                    // A g
-                if (o1) dmma(acc1[m][0], acc1[m][1], tS[tb + 8 * m], bx);  // S g
-            } else if (mid) {
-                const double sv = tS[tb + 8 * m];
-                dmma(acc0[m][0], acc0[m][1], a, bx);                 // A Ta
-                dmma(acc0[m][0], acc0[m][1], tN[tb + 8 * m], by);    // - S Ts
-                dmma(acc1[m][0], acc1[m][1], a, by);                 // A Ts
-                dmma(acc1[m][0], acc1[m][1], sv, bx);                // S Ta
-            } else {
-                dmma(acc0[m][0], acc0[m][1], a, bx);                 // A X
-                dmma(acc0[m][0], acc0[m][1], tN[tb + 8 * m], by);    // - S Y
-            }
-        }
-    }
-#pragma unroll
-    for (int m = 0; m < kConvMT; ++m) {
-        if (m >= Mt) break;
-        const int i = 8 * m + g;
-        if (i >= Lg) continue;
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const int f = f0 + fc + 2 * t + e;
-            if (f >= nfib) continue;
-            const long long ad = addr(i, f);
-            o0[ad] = acc0[m][e];
-            if (o1) o1[ad] = acc1[m][e];
-        }
+    for (int e = 0; e < 2; ++e) {
+        const int f = ft * 8 + 2 * t + e;
+        if (f >= nfib) continue;
+        const long long ad = fbase(f) + i * jstride;
+        o0[ad] = r0[e];
+        if (o1) o1[ad] = r1[e];
     }
 }
 
@@ -1094,10 +1152,7 @@ size_t generic_smem(int D, int PE, int W, bool spread) {
     return sizeof(double) * ((((spread ? W : 1) * PV + 1) & ~1) + W * 32 * kRowG);
 }
 
-size_t conv_smem(int Lg) {
-    const int Kp = (Lg + 3) & ~3, Mp = 8 * ((Lg + 7) >> 3);
-    return sizeof(double) * (2 * Kp * kConvLd + 3 * (Mp + Kp));
-}
+
 
 cudaError_t init_kernel_attributes() {
     cudaError_t e = cudaSuccess;
@@ -1117,7 +1172,6 @@ cudaError_t init_kernel_attributes() {
     set(reinterpret_cast<const void*>(gather_generic_kernel<1>), big);
     set(reinterpret_cast<const void*>(gather_generic_kernel<2>), big);
     set(reinterpret_cast<const void*>(gather_generic_kernel<3>), big);
-    set(reinterpret_cast<const void*>(conv_stage_kernel), conv_smem(kConvMaxL));
     return e;
 }
 
@@ -1167,11 +1221,23 @@ void launch_tile_reduce(const DWin* wins, const int2* multi, int nmulti, int max
 }
 
 void launch_reduce(const DWin* wins, const int* slots, int nslots, long long max_nodes, int D, int S,
-                   const double* patches, cudaStream_t st) {
+                   const double* patches, bool wrap, int max_tiles, cudaStream_t st) {
     if (nslots == 0) return;
+    if (!wrap) {
+        // owner-tile blocks; NC = ceil(PE / TC) source tiles per dimension
+        dim3 grid(static_cast<unsigned>(max_tiles), nslots);
+        if (S == 8) {
+            if (D == 1) reduce_owner_kernel<1, 2><<<grid, 128, 0, st>>>(wins, slots, patches);
+            else if (D == 2) reduce_owner_kernel<2, 2><<<grid, 128, 0, st>>>(wins, slots, patches);
+            else reduce_owner_kernel<3, 3><<<grid, 128, 0, st>>>(wins, slots, patches);
+        } else {
+            if (D == 1) reduce_owner_kernel<1, 5><<<grid, 128, 0, st>>>(wins, slots, patches);
+            else if (D == 2) reduce_owner_kernel<2, 5><<<grid, 128, 0, st>>>(wins, slots, patches);
+            else reduce_owner_kernel<3, 5><<<grid, 128, 0, st>>>(wins, slots, patches);
+        }
+        return;
+    }
     dim3 grid(static_cast<unsigned>((max_nodes + 255) / 256), nslots);
-    // NC = covering tiles per dimension, ceil(PE / TC): 2 (d=1: 39/32), 2 (d=2: 15/8),
-    // 3 (d=3: 11/4) for m = 4; the generic bound 5 covers m <= 8.
     if (D == 1) reduce_patches_kernel<1, 5><<<grid, 256, 0, st>>>(wins, slots, patches);
     else if (D == 2) reduce_patches_kernel<2, 5><<<grid, 256, 0, st>>>(wins, slots, patches);
     else if (S == 8) reduce_patches_kernel<3, 3><<<grid, 256, 0, st>>>(wins, slots, patches);
@@ -1181,8 +1247,9 @@ void launch_reduce(const DWin* wins, const int* slots, int nslots, long long max
 void launch_conv(const DWin* wins, const int* slots, int nslots, int Lg_max, long long max_fibres,
                  int stage, cudaStream_t st) {
     if (nslots == 0) return;
-    dim3 grid(static_cast<unsigned>((max_fibres + kConvFB - 1) / kConvFB), nslots);
-    conv_stage_kernel<<<grid, 128, conv_smem(Lg_max), st>>>(wins, slots, stage);
+    const long long tiles = static_cast<long long>((Lg_max + 7) / 8) * ((max_fibres + 7) / 8);
+    dim3 grid(static_cast<unsigned>((tiles + 3) / 4), nslots);
+    conv_stage_kernel<<<grid, 128, 0, st>>>(wins, slots, stage);
 }
 
 int conv_max_lg() { return kConvMaxL; }
