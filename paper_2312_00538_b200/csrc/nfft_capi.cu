@@ -38,8 +38,7 @@ void launch_tile_reduce(const DWin* wins, const int2* multi, int nmulti, int max
 void launch_conv(const DWin* wins, const int* slots, int nslots, int Lg_max, long long max_fibres,
                  int stage, cudaStream_t st);
 int conv_max_lg();
-cudaError_t launch_grid_phase(const DWin* wins, int P, const int2* multi, int n_multi, int max_pv, int S,
-                              double* patches, int max_units, cudaStream_t st);
+
 void launch_combine(double* y, const double* parts, const double* eta, int P, long long n,
                     cudaStream_t st);
 void launch_kernel_rows(double* out, const long long* rows, int r, const double* const* cols,
@@ -596,22 +595,7 @@ struct Engine {
         d_gitems.upload(gall.data(), gall.size(), stream);
         d_slots.upload(slots.data(), slots.size(), stream);
         n_multi = static_cast<int>(multi.size());
-        {
-            long long red = 0, conv = 0;
-            for (int s = 0; s < P; ++s) {
-                const DWin& dw = wins[static_cast<size_t>(owned[static_cast<size_t>(s)])]->dw;
-                long long u = 1, nodes = 1, nfib = 1;
-                for (int t = 0; t < dw.d; ++t) {
-                    u *= dw.ntile;
-                    nodes *= dw.Lg;
-                }
-                for (int t = 0; t + 1 < dw.d; ++t) nfib *= dw.Lg;
-                red += dw.wrap ? (nodes + 127) / 128 : u;
-                conv += ((dw.Lg + 7) / 8) * ((nfib + 7) / 8);
-            }
-            const long long mb = (max_pv + 127) / 128;
-            max_grid_units = static_cast<int>(std::max({red, (conv + 3) / 4, mb * n_multi, 1LL}));
-        }
+
         if (n_multi) d_multi.upload(multi.data(), multi.size(), stream);
         d_eta.upload(eta.data(), eta.size(), stream);
         patches.alloc(static_cast<size_t>(std::max<long long>(patch_total, 1)));
@@ -642,36 +626,29 @@ struct Engine {
             ++g_launches;
         }
         CK(cudaGetLastError());
-        if (fused_grid) {
-            tick("grid_phase");
-            CK(launch_grid_phase(d_wins.p, P, d_multi.p, n_multi, max_pv, 2 * cfg.window_cutoff, patches.p,
-                                 max_grid_units, stream));
+        if (n_multi) {
+            tick("tile_reduce");
+            launch_tile_reduce(d_wins.p, d_multi.p, n_multi, max_pv, patches.p, stream);
             ++g_launches;
-        } else {
-            if (n_multi) {
-                tick("tile_reduce");
-                launch_tile_reduce(d_wins.p, d_multi.p, n_multi, max_pv, patches.p, stream);
-                ++g_launches;
-            }
-            tick("reduce");
-            for (int D = 1; D <= 3; ++D) {
-                if (!has_dim[D]) continue;
-                const bool wrap = geometry(cfg, D).wrap != 0;
-                int tiles = 1;
-                for (int t = 0; t < D; ++t) tiles *= geometry(cfg, D).ntile;
-                launch_reduce(d_wins.p, d_slots.p, P, max_nodes, D, 2 * cfg.window_cutoff, patches.p, wrap,
-                              tiles, stream);
-                ++g_launches;
-            }
-            int maxd = 0;
-            for (int s = 0; s < P; ++s)
-                maxd = std::max(maxd, wins[static_cast<size_t>(owned[static_cast<size_t>(s)])]->d);
-            static const char* kConv[3] = {"conv_0", "conv_1", "conv_2"};
-            for (int stg = 0; stg < maxd; ++stg) {
-                tick(kConv[stg]);
-                launch_conv(d_wins.p, d_slots.p, P, max_lg, max_fibres, stg, stream);
-                ++g_launches;
-            }
+        }
+        tick("reduce");
+        for (int D = 1; D <= 3; ++D) {
+            if (!has_dim[D]) continue;
+            const bool wrap = geometry(cfg, D).wrap != 0;
+            int tiles = 1;
+            for (int t = 0; t < D; ++t) tiles *= geometry(cfg, D).ntile;
+            launch_reduce(d_wins.p, d_slots.p, P, max_nodes, D, 2 * cfg.window_cutoff, patches.p, wrap,
+                          tiles, stream);
+            ++g_launches;
+        }
+        int maxd = 0;
+        for (int s = 0; s < P; ++s)
+            maxd = std::max(maxd, wins[static_cast<size_t>(owned[static_cast<size_t>(s)])]->d);
+        static const char* kConv[3] = {"conv_0", "conv_1", "conv_2"};
+        for (int stg = 0; stg < maxd; ++stg) {
+            tick(kConv[stg]);
+            launch_conv(d_wins.p, d_slots.p, P, max_lg, max_fibres, stg, stream);
+            ++g_launches;
         }
         CK(cudaGetLastError());
     }
@@ -725,8 +702,7 @@ struct Engine {
     std::vector<GraphEntry> graphs;  // most recent last; at most kMaxGraphs
     static constexpr size_t kMaxGraphs = 8;
     bool use_graphs = std::getenv("KSVM_NFFT_NO_GRAPH") == nullptr;
-    bool fused_grid = std::getenv("KSVM_NFFT_NO_FUSED_GRID") == nullptr;
-    int max_grid_units = 1;  // most work units of any grid phase (sizes the cooperative grid)
+
     bool capturing = false;
 
     void drop_graphs() {

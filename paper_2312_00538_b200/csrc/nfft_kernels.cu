@@ -14,7 +14,6 @@
 // applies with the same plan and v are bit-identical
 // (P:tests/test_fastsum.cpp:208-215). Window weights come from per-point
 // factors precomputed at plan time (nfft_engine.cuh), so no exp() runs here.
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -833,95 +832,6 @@ __global__ void reduce_patches_kernel(const DWin* __restrict__ wins, const int* 
     wn.G[node] = sum;
 }
 
-// Owner-tile reduction (non-wrapping grids): CTA (T, window) produces the
-// grid nodes of its own tile block (the last tile per dimension also owns the
-// halo nodes past the tiles). The <= NC^d source tiles whose patches reach
-// the block are looked up once into SMEM, so every node's <= NC^d loads are
-// independent. Sum order: source tiles ascending in (T0, T1, T2).
-template <int D, int NC>
-__global__ void __launch_bounds__(128)
-reduce_owner_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots,
-                    const double* __restrict__ patches) {
-    const DWin& wn = wins[slots[blockIdx.y]];
-    if (wn.d != D || wn.wrap) return;
-    const int TC = wn.TC, PE = wn.PE, nt = wn.ntile, Lg = wn.Lg;
-    int ntd = 1;
-#pragma unroll
-    for (int t = 0; t < D; ++t) ntd *= nt;
-    if (static_cast<int>(blockIdx.x) >= ntd) return;
-    int T[3] = {0, 0, 0};
-    {
-        int r = blockIdx.x;
-#pragma unroll
-        for (int t = D - 1; t >= 0; --t) {
-            T[t] = r % nt;
-            r /= nt;
-        }
-    }
-    constexpr int NS = D == 1 ? NC : (D == 2 ? NC * NC : NC * NC * NC);
-    __shared__ long long soff[NS];
-    __shared__ int sT[NS][3];
-    __shared__ int any;
-    if (threadIdx.x == 0) any = 0;
-    __syncthreads();
-    if (threadIdx.x < NS) {
-        int r = threadIdx.x, S[3] = {0, 0, 0};
-        bool ok = true;
-        int lin = 0;
-#pragma unroll
-        for (int t = D - 1; t >= 0; --t) {
-            S[t] = T[t] - (NC - 1) + r % NC;
-            r /= NC;
-            ok = ok && S[t] >= 0;
-        }
-#pragma unroll
-        for (int t = 0; t < D; ++t) lin = lin * nt + (S[t] < 0 ? 0 : S[t]);
-        const long long off = ok ? wn.tile_patch[lin] : -1;
-        soff[threadIdx.x] = off;
-#pragma unroll
-        for (int t = 0; t < 3; ++t) sT[threadIdx.x][t] = S[t];
-        if (off >= 0) any = 1;
-    }
-    __syncthreads();
-    // owned node block: [T TC, T TC + TC), the last tile extends to Lg
-    int lo[3] = {0, 0, 0}, len[3] = {1, 1, 1}, nodes = 1;
-#pragma unroll
-    for (int t = 0; t < D; ++t) {
-        lo[t] = T[t] * TC;
-        const int hi = T[t] == nt - 1 ? Lg : min(lo[t] + TC, Lg);
-        len[t] = max(0, hi - lo[t]);
-        nodes *= len[t];
-    }
-    for (int k = threadIdx.x; k < nodes; k += blockDim.x) {
-        int r = k, e[3] = {0, 0, 0};
-#pragma unroll
-        for (int t = D - 1; t >= 0; --t) {
-            e[t] = lo[t] + r % len[t];
-            r /= len[t];
-        }
-        double sum = 0.0;
-        if (any) {
-#pragma unroll
-            for (int q = 0; q < NS; ++q) {
-                const long long off = soff[q];
-                int o = 0;
-                bool ok = off >= 0;
-#pragma unroll
-                for (int t = 0; t < D; ++t) {
-                    const int ot = e[t] - sT[q][t] * TC;
-                    ok = ok && ot >= 0 && ot < PE;
-                    o = o * PE + ot;
-                }
-                if (ok) sum += patches[off + o];
-            }
-        }
-        long long gi = 0;
-#pragma unroll
-        for (int t = 0; t < D; ++t) gi = gi * Lg + e[t];
-        wn.G[gi] = sum;
-    }
-}
-
 // ===========================================================================
 // Grid stage as a real separable convolution. With
 // z(r) = sum_{J in I_N} m1[J] e^{2 pi i J r / M} = a(r) + i s(r) the
@@ -933,104 +843,14 @@ reduce_owner_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots
 // cores: Out[i, f] = sum_j T[i - j] X[j, f] over the Lg^(d-1) fibres f.
 // Latency-oriented: one warp per 8x8 output tile (8 rows i x 8 fibres f),
 // every operand load of its K = Lg reduction issued up front (no SMEM, no
-// block barrier), then a short chain of DMMAs. blockIdx.y = window slot.
+// block barrier), then a short chain of DMMAs (conv_tile_unit below).
 // ===========================================================================
 constexpr int kConvMaxL = 128;  // Lg bound (M = sigma N <= 128)
 
-__global__ void __launch_bounds__(128)
-conv_stage_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots, int stage) {
-    const DWin& wn = wins[slots[blockIdx.y]];
-    const int D = wn.d, Lg = wn.Lg;
-    if (stage >= D) return;
-    const int dim = D - 1 - stage;
-    int nfib = 1;
-    for (int t = 0; t < D - 1; ++t) nfib *= Lg;
-    const int Mt = (Lg + 7) >> 3, Ft = (nfib + 7) >> 3;
-    const int tile = blockIdx.x * 4 + (threadIdx.x >> 5);
-    if (tile >= Mt * Ft) return;
-    const int mt = tile % Mt, ft = tile / Mt;
-    int inner = 1;
-    for (int t = dim + 1; t < D; ++t) inner *= Lg;
-    const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-    const double* in0 = stage == 0 ? wn.G : (stage == 1 ? wn.T[0] : (D == 3 ? wn.T[2] : wn.T[0]));
-    const double* in1 = stage == 0 ? nullptr : (stage == 1 ? wn.T[1] : (D == 3 ? wn.T[3] : wn.T[1]));
-    const bool two_in = stage > 0, mid = stage == 1 && D == 3, first = stage == 0 && D > 1;
-    // element (j, f) lives at base(f) + j * jstride
-    auto fbase = [&](int f) -> long long {
-        if (dim == D - 1) return static_cast<long long>(f) * Lg;
-        const int outer = f / inner, in = f - outer * inner;
-        return static_cast<long long>(outer) * Lg * inner + in;
-    };
-    const long long jstride = dim == D - 1 ? 1 : inner;
-    const int fB = ft * 8 + g;  // this lane's B column (fibre)
-    const bool fok = fB < nfib;
-    const long long bb = fok ? fbase(fB) : 0;
-    const int i0 = mt * 8;
-    const double* __restrict__ tA = wn.tabA;
-    const double* __restrict__ tS = wn.tabS;
-    const int KS = (Lg + 3) >> 2;
-    double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;  // acc0 (out 0), acc1 (out 1)
-    double e00 = 0.0, e01 = 0.0, e10 = 0.0, e11 = 0.0;  // second chains (even/odd k)
-#pragma unroll 4
-    for (int ks = 0; ks < KS; ++ks) {
-        const int j = 4 * ks + t;
-        const bool jok = j < Lg && fok;
-        const double bx = jok ? __ldg(in0 + bb + j * jstride) : 0.0;
-        const double by = (jok && two_in) ? __ldg(in1 + bb + j * jstride) : 0.0;
-        // A[g][t] = T[(i0 + g) - j]
-        const int r = i0 + g - j;
-        const bool rok = r > -Lg && r < Lg;
-        const double a = rok ? __ldg(tA + r + Lg - 1) : 0.0;
-        const double sv = rok ? __ldg(tS + r + Lg - 1) : 0.0;
-        double& p0 = (ks & 1) ? e00 : d00;
-        double& p1 = (ks & 1) ? e01 : d01;
-        double& q0 = (ks & 1) ? e10 : d10;
-        double& q1 = (ks & 1) ? e11 : d11;
-        if (!two_in) {
-            dmma(p0, p1, a, bx);                    // A g
-            if (first) dmma(q0, q1, sv, bx);        // S g
-        } else if (mid) {
-            dmma(p0, p1, a, bx);                    // A Ta
-            dmma(p0, p1, -sv, by);                  // - S Ts
-            dmma(q0, q1, a, by);                    // A Ts
-            dmma(q0, q1, sv, bx);                   // S Ta
-        } else {
-            dmma(p0, p1, a, bx);                    // A X
-            dmma(p0, p1, -sv, by);                  // - S Y
-        }
-    }
-    double* o0;
-    double* o1 = nullptr;
-    if (stage == 0 && D == 1) {
-        o0 = wn.H;
-    } else if (stage == 0) {
-        o0 = wn.T[0];
-        o1 = wn.T[1];
-    } else if (mid) {
-        o0 = wn.T[2];
-        o1 = wn.T[3];
-    } else {
-        o0 = wn.H;
-    }
-    const int i = i0 + g;
-    if (i >= Lg) return;
-    const double r0[2] = {d00 + e00, d01 + e01}, r1[2] = {d10 + e10, d11 + e11};
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-        const int f = ft * 8 + 2 * t + e;
-        if (f >= nfib) continue;
-        const long long ad = fbase(f) + i * jstride;
-        o0[ad] = r0[e];
-        if (o1) o1[ad] = r1[e];
-    }
-}
-
 // ===========================================================================
-// Fused grid phase: tile pre-reduce -> node reduce -> conv stages 0..d-1 of
-// every window in ONE persistent cooperative kernel (grid-wide barriers
-// between phases). All five phases are small and latency-bound; as separate
-// launches each paid its own ramp and drain. The grid is sized from the
-// occupancy API so every CTA is resident (required by grid.sync()).
+// Grid-side work units (reduce and convolution), shared by the kernels below.
+// (A single persistent cooperative kernel running all of them with grid-wide
+// barriers was measured slower than separate launches: profiles/README.md.)
 // ===========================================================================
 namespace {
 
@@ -1126,55 +946,6 @@ __device__ void reduce_owner_unit(const DWin& wn, int tileT, const double* __res
     __syncthreads();  // scratch reuse by the next unit
 }
 
-// Wrapped grids: node-per-thread reduction (same order as reduce_patches_kernel).
-template <int D>
-__device__ void reduce_wrap_node(const DWin& wn, int node, const double* __restrict__ patches) {
-    const int Lg = wn.Lg, TC = wn.TC, PE = wn.PE, nt = wn.ntile;
-    int lg[3] = {0, 0, 0};
-    {
-        int r = node;
-#pragma unroll
-        for (int t = D - 1; t >= 0; --t) {
-            lg[t] = r % Lg;
-            r /= Lg;
-        }
-    }
-    const long long* __restrict__ tp = wn.tile_patch;
-    const int Eext = nt * TC + wn.S - 1;
-    int e0s[3] = {0, 0, 0};
-#pragma unroll
-    for (int t = 0; t < D; ++t) e0s[t] = pmod(lg[t] - wn.lo, wn.M);
-    double sum = 0.0;
-#define KSVM_TLO(e) ((e) - PE + 1 <= 0 ? 0 : ((e) - PE + TC) / TC)
-#define KSVM_THI(e) min((e) / TC, nt - 1)
-    for (int e0 = e0s[0]; e0 < Eext; e0 += wn.M)
-        for (int T0 = KSVM_TLO(e0); T0 <= KSVM_THI(e0); ++T0) {
-            const int o0 = e0 - T0 * TC;
-            if constexpr (D == 1) {
-                const long long off = tp[T0];
-                if (off >= 0) sum += patches[off + o0];
-            } else {
-                for (int e1 = e0s[1]; e1 < Eext; e1 += wn.M)
-                    for (int T1 = KSVM_TLO(e1); T1 <= KSVM_THI(e1); ++T1) {
-                        const int o1 = o0 * PE + e1 - T1 * TC;
-                        if constexpr (D == 2) {
-                            const long long off = tp[T0 * nt + T1];
-                            if (off >= 0) sum += patches[off + o1];
-                        } else {
-                            for (int e2 = e0s[2]; e2 < Eext; e2 += wn.M)
-                                for (int T2 = KSVM_TLO(e2); T2 <= KSVM_THI(e2); ++T2) {
-                                    const long long off = tp[(T0 * nt + T1) * nt + T2];
-                                    if (off >= 0) sum += patches[off + o1 * PE + e2 - T2 * TC];
-                                }
-                        }
-                    }
-            }
-        }
-#undef KSVM_TLO
-#undef KSVM_THI
-    wn.G[node] = sum;
-}
-
 // One 8x8 output tile of a separable-convolution stage (one warp).
 __device__ void conv_tile_unit(const DWin& wn, int stage, int tile) {
     const int D = wn.d, Lg = wn.Lg;
@@ -1263,93 +1034,34 @@ __device__ __forceinline__ int conv_tiles(const DWin& wn) {
     return ((wn.Lg + 7) >> 3) * ((nfib + 7) >> 3);
 }
 
-__device__ __forceinline__ int reduce_units(const DWin& wn) {
-    int u = 1;
-    if (!wn.wrap) {
-        for (int t = 0; t < wn.d; ++t) u *= wn.ntile;
-        return u;
-    }
-    for (int t = 0; t < wn.d; ++t) u *= wn.Lg;
-    return (u + 127) / 128;
-}
-
 }  // namespace
 
-__global__ void __launch_bounds__(128, 4)
-grid_phase_kernel(const DWin* __restrict__ wins, int P, const int2* __restrict__ multi, int n_multi,
-                  int multi_blocks, int S, double* __restrict__ patches) {
-    namespace cg = cooperative_groups;
-    cg::grid_group grid = cg::this_grid();
-    __shared__ long long soff[125];
-    __shared__ int sT[125][3];
+// Owner-tile reduction (non-wrapping grids): CTA (T, window) produces the
+// grid nodes of its own tile block; the <= NC^d source tiles whose patches
+// reach it are looked up once into SMEM (reduce_owner_unit).
+template <int D, int NC>
+__global__ void __launch_bounds__(128)
+reduce_owner_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots,
+                    const double* __restrict__ patches) {
+    const DWin& wn = wins[slots[blockIdx.y]];
+    if (wn.d != D || wn.wrap) return;
+    int ntd = 1;
+    for (int t = 0; t < D; ++t) ntd *= wn.ntile;
+    if (static_cast<int>(blockIdx.x) >= ntd) return;
+    constexpr int NS = D == 1 ? NC : (D == 2 ? NC * NC : NC * NC * NC);
+    __shared__ long long soff[NS];
+    __shared__ int sT[NS][3];
     __shared__ int any;
-    // phase A: pre-reduce tiles split over several items (fixed item order)
-    for (int u = blockIdx.x; u < n_multi * multi_blocks; u += gridDim.x) {
-        const int2 wt = multi[u / multi_blocks];
-        const DWin& wn = wins[wt.x];
-        int PV = 1;
-        for (int t = 0; t < wn.d; ++t) PV *= wn.PE;
-        const int e = (u % multi_blocks) * 128 + threadIdx.x;
-        if (e >= PV) continue;
-        const int k0 = wn.tile_first[wt.y], nk = wn.tile_first[wt.y + 1] - k0;
-        double* base = patches + wn.patch_base + static_cast<long long>(k0 - wn.item_base) * PV;
-        double sacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        int k = 0;
-        for (; k + 8 <= nk; k += 8) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) sacc[j] += base[static_cast<long long>(k + j) * PV + e];
-        }
-        for (int j = 0; k + j < nk; ++j) sacc[j] += base[static_cast<long long>(k + j) * PV + e];
-        base[e] = ((sacc[0] + sacc[1]) + (sacc[2] + sacc[3])) + ((sacc[4] + sacc[5]) + (sacc[6] + sacc[7]));
-    }
-    grid.sync();
-    // phase B: grid nodes <- patches (owner tiles; node blocks when wrapped)
-    int total = 0;
-    for (int w = 0; w < P; ++w) total += reduce_units(wins[w]);
-    for (int u = blockIdx.x; u < total; u += gridDim.x) {
-        int w = 0, base = 0;
-        while (base + reduce_units(wins[w]) <= u) base += reduce_units(wins[w++]);
-        const DWin& wn = wins[w];
-        const int lu = u - base;
-        if (!wn.wrap) {
-            if (S == 8) {
-                if (wn.d == 1) reduce_owner_unit<1, 2>(wn, lu, patches, soff, sT, &any);
-                else if (wn.d == 2) reduce_owner_unit<2, 2>(wn, lu, patches, soff, sT, &any);
-                else reduce_owner_unit<3, 3>(wn, lu, patches, soff, sT, &any);
-            } else {
-                if (wn.d == 1) reduce_owner_unit<1, 5>(wn, lu, patches, soff, sT, &any);
-                else if (wn.d == 2) reduce_owner_unit<2, 5>(wn, lu, patches, soff, sT, &any);
-                else reduce_owner_unit<3, 5>(wn, lu, patches, soff, sT, &any);
-            }
-        } else {
-            int nodes = 1;
-            for (int t = 0; t < wn.d; ++t) nodes *= wn.Lg;
-            const int node = lu * 128 + threadIdx.x;
-            if (node < nodes) {
-                if (wn.d == 1) reduce_wrap_node<1>(wn, node, patches);
-                else if (wn.d == 2) reduce_wrap_node<2>(wn, node, patches);
-                else reduce_wrap_node<3>(wn, node, patches);
-            }
-        }
-    }
-    // phases C..: the separable convolution, one stage per dimension
-    int maxd = 0;
-    for (int w = 0; w < P; ++w) maxd = max(maxd, wins[w].d);
-    const int gw = blockIdx.x * 4 + (threadIdx.x >> 5), nwarps = gridDim.x * 4;
-    for (int stage = 0; stage < maxd; ++stage) {
-        grid.sync();
-        int tot = 0;
-        for (int w = 0; w < P; ++w) tot += wins[w].d > stage ? conv_tiles(wins[w]) : 0;
-        for (int u = gw; u < tot; u += nwarps) {
-            int w = 0, base = 0;
-            for (;; ++w) {
-                const int c = wins[w].d > stage ? conv_tiles(wins[w]) : 0;
-                if (u < base + c) break;
-                base += c;
-            }
-            conv_tile_unit(wins[w], stage, u - base);
-        }
-    }
+    reduce_owner_unit<D, NC>(wn, blockIdx.x, patches, soff, sT, &any);
+}
+
+__global__ void __launch_bounds__(128)
+conv_stage_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots, int stage) {
+    const DWin& wn = wins[slots[blockIdx.y]];
+    if (stage >= wn.d) return;
+    const int tile = blockIdx.x * 4 + (threadIdx.x >> 5);
+    if (tile >= conv_tiles(wn)) return;
+    conv_tile_unit(wn, stage, tile);
 }
 
 // y[j] = sum over owned windows (ascending) of eta_l * out_l[j]
@@ -1581,34 +1293,6 @@ void launch_conv(const DWin* wins, const int* slots, int nslots, int Lg_max, lon
 }
 
 int conv_max_lg() { return kConvMaxL; }
-
-// Cooperative launch of the fused grid phase (captured into the apply graph).
-cudaError_t launch_grid_phase(const DWin* wins, int P, const int2* multi, int n_multi, int max_pv, int S,
-                              double* patches, int max_units, cudaStream_t st) {
-    static int per_sm = -1;
-    static int sms = 0;
-    if (per_sm < 0) {
-        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, grid_phase_kernel, 128, 0);
-        if (e != cudaSuccess) return e;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    const int multi_blocks = (max_pv + 127) / 128;
-    int blocks = per_sm * sms;
-    blocks = std::max(1, std::min(blocks, std::max(max_units, 1)));
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(static_cast<unsigned>(blocks));
-    cfg.blockDim = dim3(128);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, grid_phase_kernel, wins, P, multi, n_multi, multi_blocks, S, patches);
-}
 
 void launch_combine(double* y, const double* parts, const double* eta, int P, long long n,
                     cudaStream_t st) {
