@@ -191,6 +191,11 @@ Spectral1D spectral_1d(int N, int M, double bwin, double ell_s) {
     return s;
 }
 
+struct Geometry {
+    int M, S, m, cmin, ncell, TC, ntile, PE, Lext, Lg, lo, wrap;
+    double bwin, invb, Cw;
+};
+
 struct PointSet {
     int64_t n = 0;
     int d = 0;
@@ -211,29 +216,32 @@ struct Window {
     double center[3] = {0, 0, 0};
     double scale = 1.0, ell_s = 0.0, coef_sum = 0.0;
     DWin dw{};
+    Geometry geom{};
     DevBuf<double> G, H, T[4], tabA, tabS;
     DevBuf<int> tile_first;
     DevBuf<long long> tile_patch;
     PointSet src;
 };
 
-struct Geometry {
-    int M, S, m, cmin, ncell, TC, ntile, PE, Lext, Lg, lo, wrap;
-    double bwin, invb, Cw;
-};
-
-Geometry geometry(const ksvm_nfft_config& c, int d) {
+// Grid geometry of one window. Without `range` it covers every admissible
+// point (sources: |x| <= fit r_T; cross targets: ||x|| <= r_T (1 + 1e-12),
+// P:src/fastsum.cpp:316). With range = {min, max} of the scaled source
+// coordinates over all dimensions (ANOVA operators, which only self-apply)
+// it covers just the cells the data occupy. The plan-time cell-key kernel
+// verifies every point lands in [cmin, cmax].
+Geometry geometry(const ksvm_nfft_config& c, int d, const double* range = nullptr) {
     Geometry g{};
     g.M = c.oversampling * c.bandwidth;
     g.m = c.window_cutoff;
     g.S = 2 * g.m;
-    // Every admissible point (sources: |x| <= fit r_T; cross targets:
-    // ||x|| <= r_T (1 + 1e-12), P:src/fastsum.cpp:316) has floor(x M) in
-    // [cmin, cmax] (the plan-time cell-key kernel verifies it).
     const double rx = c.torus_radius * (1.0 + 1e-12) * g.M;
     g.cmin = static_cast<int>(std::floor(-rx));
-    const int cmax = static_cast<int>(std::floor(rx));
-    g.ncell = cmax - g.cmin + 1;
+    int cmax = static_cast<int>(std::floor(rx));
+    if (range) {
+        g.cmin = std::max(g.cmin, static_cast<int>(std::floor(range[0] * g.M)));
+        cmax = std::min(cmax, static_cast<int>(std::floor(range[1] * g.M)));
+    }
+    g.ncell = std::max(1, cmax - g.cmin + 1);
     g.TC = d == 3 ? 4 : (d == 2 ? 8 : 32);
     g.ntile = (g.ncell + g.TC - 1) / g.TC;
     g.PE = g.TC + g.S - 1;
@@ -440,6 +448,9 @@ struct Engine {
 
     int P_owned() const { return static_cast<int>(owned.size()); }
     int64_t n_owned_windows = 1;  // set before planning (item sizing)
+    bool data_range = false;      // grid range from the data (self-apply only operators)
+    bool has_wrap[4] = {false, false, false, false}, has_nowrap[4] = {false, false, false, false};
+    int max_tiles[4] = {0, 0, 0, 0};
 
     void init(int dev) {
         device = dev;
@@ -460,7 +471,16 @@ struct Engine {
         for (int t = 0; t < d; ++t)
             for (int64_t i = 0; i < n; ++i)
                 sc[static_cast<size_t>(t * n + i)] = (cm[static_cast<size_t>(t * n + i)] - w.center[t]) * w.scale;
-        const Geometry g = geometry(cfg, d);
+        double range[2] = {0.0, 0.0};
+        if (data_range) {
+            range[0] = range[1] = sc[0];
+            for (double x : sc) {
+                range[0] = std::min(range[0], x);
+                range[1] = std::max(range[1], x);
+            }
+        }
+        const Geometry g = geometry(cfg, d, data_range ? range : nullptr);
+        w.geom = g;
         const double bwin = g.bwin;
         // spectral data and the separable convolution tables
         const Spectral1D sp = spectral_1d(cfg.bandwidth, g.M, bwin, w.ell_s);
@@ -490,6 +510,10 @@ struct Engine {
         max_fibres = std::max(max_fibres, nodes / Lg);
         max_lg = std::max(max_lg, Lg);
         has_dim[d] = true;
+        (g.wrap ? has_wrap : has_nowrap)[d] = true;
+        int tiles = 1;
+        for (int t = 0; t < d; ++t) tiles *= g.ntile;
+        max_tiles[d] = std::max(max_tiles[d], tiles);
         w.G.alloc(nodes);
         w.H.alloc(nodes);
         for (int k = 0; k < (d == 1 ? 0 : (d == 2 ? 2 : 4)); ++k) w.T[k].alloc(nodes);
@@ -633,13 +657,12 @@ struct Engine {
         }
         tick("reduce");
         for (int D = 1; D <= 3; ++D) {
-            if (!has_dim[D]) continue;
-            const bool wrap = geometry(cfg, D).wrap != 0;
-            int tiles = 1;
-            for (int t = 0; t < D; ++t) tiles *= geometry(cfg, D).ntile;
-            launch_reduce(d_wins.p, d_slots.p, P, max_nodes, D, 2 * cfg.window_cutoff, patches.p, wrap,
-                          tiles, stream);
-            ++g_launches;
+            for (int wrap = 0; wrap < 2; ++wrap) {
+                if (!(wrap ? has_wrap : has_nowrap)[D]) continue;
+                launch_reduce(d_wins.p, d_slots.p, P, max_nodes, D, 2 * cfg.window_cutoff, patches.p,
+                              wrap != 0, max_tiles[D], stream);
+                ++g_launches;
+            }
         }
         int maxd = 0;
         for (int s = 0; s < P; ++s)
@@ -803,7 +826,7 @@ namespace {
 void build_engine(Engine& E, const double* points, int64_t n, int64_t d, int64_t ld, int layout,
                   const int* feats, const int* sizes, int P, const double* weights,
                   const double* ells, const ksvm_nfft_config* cfg, double fit, const int* mask,
-                  int device, int precision) {
+                  int device, int precision, bool data_range) {
     if (!points || !feats || !sizes || !weights || !ells || !cfg)
         throw std::invalid_argument("null argument");
     validate_cfg(*cfg);
@@ -837,6 +860,7 @@ void build_engine(Engine& E, const double* points, int64_t n, int64_t d, int64_t
     E.init(device);
     E.cfg = *cfg;
     E.fit = fit;
+    E.data_range = data_range;
     E.n = n;
     E.dfull = d;
     off = 0;
@@ -921,7 +945,8 @@ int ksvm_nfft_op_create(const double* points, int64_t n, int64_t d, int64_t ld, 
         if (!out) throw std::invalid_argument("null out");
         auto op = std::make_unique<ksvm_nfft_op>();
         build_engine(op->e, points, n, d, ld, layout, window_features, window_sizes, num_windows,
-                     weights, length_scales, cfg, fit_fraction, window_mask, device, precision);
+                     weights, length_scales, cfg, fit_fraction, window_mask, device, precision,
+                     /*data_range=*/true);
         *out = op.release();
     });
 }
@@ -1099,7 +1124,7 @@ int ksvm_nfft_plan_create(const double* points, int64_t n, int d, int64_t ld, in
         const int sizes[1] = {d};
         const double one = 1.0;
         build_engine(p->e, points, n, d, ld, layout, feats, sizes, 1, &one, &length_scale, cfg,
-                     fit_fraction, nullptr, device, KSVM_NFFT_FP64);
+                     fit_fraction, nullptr, device, KSVM_NFFT_FP64, /*data_range=*/false);
         *out = p.release();
     });
 }
@@ -1135,7 +1160,7 @@ int ksvm_nfft_plan_apply_cross(const ksvm_nfft_plan* plan, const double* targets
         if (t == 0) return;
         DeviceGuard dg(E.device);
         std::lock_guard<std::mutex> lk(E.mu);
-        const Geometry g = geometry(E.cfg, w.d);
+        const Geometry g = w.geom;
         PointSet tp;
         build_pointset(tp, sc, t, w.d, g, item_chunk(t), gather_chunk(t), E.stream);
         DevBuf<double> tout;

@@ -745,7 +745,7 @@ template <int D, int NC>
 __global__ void reduce_patches_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots,
                                       const double* __restrict__ patches) {
     const DWin& wn = wins[slots[blockIdx.y]];
-    if (wn.d != D) return;
+    if (wn.d != D || !wn.wrap) return;  // non-wrapping grids use reduce_owner_kernel
     const int Lg = wn.Lg, TC = wn.TC, PE = wn.PE, nt = wn.ntile;
     int nodes = 1;
 #pragma unroll
