@@ -511,8 +511,8 @@ struct Engine {
         max_lg = std::max(max_lg, Lg);
         has_dim[d] = true;
         (g.wrap ? has_wrap : has_nowrap)[d] = true;
-        int tiles = 1;
-        for (int t = 0; t < d; ++t) tiles *= g.ntile;
+        int tiles = 1;  // owner blocks of the node reduction: ceil(Lg / TC)^d
+        for (int t = 0; t < d; ++t) tiles *= (Lg + g.TC - 1) / g.TC;
         max_tiles[d] = std::max(max_tiles[d], tiles);
         w.G.alloc(nodes);
         w.H.alloc(nodes);

@@ -859,14 +859,15 @@ template <int D, int NC>
 __device__ void reduce_owner_unit(const DWin& wn, int tileT, const double* __restrict__ patches,
                                   long long* soff, int (*sT)[3], int* any) {
     const int TC = wn.TC, PE = wn.PE, nt = wn.ntile, Lg = wn.Lg;
+    const int nown = (Lg + TC - 1) / TC;  // owner blocks per dimension (tiles + halo blocks)
     constexpr int NS = D == 1 ? NC : (D == 2 ? NC * NC : NC * NC * NC);
     int T[3] = {0, 0, 0};
     {
         int r = tileT;
 #pragma unroll
         for (int t = D - 1; t >= 0; --t) {
-            T[t] = r % nt;
-            r /= nt;
+            T[t] = r % nown;
+            r /= nown;
         }
     }
     if (threadIdx.x == 0) *any = 0;
@@ -879,10 +880,10 @@ __device__ void reduce_owner_unit(const DWin& wn, int tileT, const double* __res
         for (int t = D - 1; t >= 0; --t) {
             Sx[t] = T[t] - (NC - 1) + r % NC;
             r /= NC;
-            ok = ok && Sx[t] >= 0;
+            ok = ok && Sx[t] >= 0 && Sx[t] < nt;
         }
 #pragma unroll
-        for (int t = 0; t < D; ++t) lin = lin * nt + (Sx[t] < 0 ? 0 : Sx[t]);
+        for (int t = 0; t < D; ++t) lin = lin * nt + min(max(Sx[t], 0), nt - 1);
         const long long off = ok ? wn.tile_patch[lin] : -1;
         soff[threadIdx.x] = off;
 #pragma unroll
@@ -894,8 +895,7 @@ __device__ void reduce_owner_unit(const DWin& wn, int tileT, const double* __res
 #pragma unroll
     for (int t = 0; t < D; ++t) {
         lo[t] = T[t] * TC;
-        const int hi = T[t] == nt - 1 ? Lg : min(lo[t] + TC, Lg);
-        len[t] = max(0, hi - lo[t]);
+        len[t] = max(0, min(lo[t] + TC, Lg) - lo[t]);
         nodes *= len[t];
     }
     const bool have = *any != 0;
@@ -1037,7 +1037,8 @@ __device__ __forceinline__ int conv_tiles(const DWin& wn) {
 }  // namespace
 
 // Owner-tile reduction (non-wrapping grids): CTA (T, window) produces the
-// grid nodes of its own tile block; the <= NC^d source tiles whose patches
+// grid nodes of its own TC^d block (blocks past the last tile own the halo);
+// the <= NC^d source tiles whose patches
 // reach it are looked up once into SMEM (reduce_owner_unit).
 template <int D, int NC>
 __global__ void __launch_bounds__(128)
@@ -1045,8 +1046,9 @@ reduce_owner_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots
                     const double* __restrict__ patches) {
     const DWin& wn = wins[slots[blockIdx.y]];
     if (wn.d != D || wn.wrap) return;
+    const int nown = (wn.Lg + wn.TC - 1) / wn.TC;
     int ntd = 1;
-    for (int t = 0; t < D; ++t) ntd *= wn.ntile;
+    for (int t = 0; t < D; ++t) ntd *= nown;
     if (static_cast<int>(blockIdx.x) >= ntd) return;
     constexpr int NS = D == 1 ? NC : (D == 2 ? NC * NC : NC * NC * NC);
     __shared__ long long soff[NS];
