@@ -345,7 +345,7 @@ int64_t item_chunk(int64_t total_points) {
     return std::max<int64_t>(512, (total_points + 148 * 24 - 1) / (148 * 24));
 }
 int64_t gather_chunk(int64_t total_points) {
-    return std::max<int64_t>(512, (total_points + 148 * 48 - 1) / (148 * 48));
+    return std::max<int64_t>(128, (total_points + 148 * 48 - 1) / (148 * 48));
 }
 
 // Affine map of P:src/fastsum.cpp:126-140 on a column-major n x d block.
@@ -565,7 +565,7 @@ struct Engine {
                 w.dw.patch_base = patch_total;
                 std::vector<int> tf = w.src.tile_first;
                 for (size_t T = 0; T + 1 < tf.size(); ++T)
-                    if (tf[T + 1] - tf[T] > kHeavyItems) multi.push_back(make_int2(s, static_cast<int>(T)));
+                    if (tf[T + 1] - tf[T] > 1) multi.push_back(make_int2(s, static_cast<int>(T)));
                 max_pv = std::max(max_pv, PV);
                 for (auto& v : tf) v += w.dw.item_base;
                 w.tile_first.upload(tf.data(), tf.size(), stream);

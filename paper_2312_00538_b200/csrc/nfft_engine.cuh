@@ -23,10 +23,7 @@
 
 namespace ksvm_nfft {
 
-constexpr int kMaxSpan = 16;
-// Tiles split into more items than this are pre-reduced (tile_reduce); the
-// node reduction sums the patches of lighter tiles directly.
-constexpr int kHeavyItems = 4;  // 2m, m <= 8 (P:src/fastsum.cpp:41-42, w[3][16] at :225)
+constexpr int kMaxSpan = 16;  // 2m, m <= 8 (P:src/fastsum.cpp:41-42, w[3][16] at :225)
 
 // One tile's (or part of a tile's) sorted point range.
 struct Item {

@@ -774,18 +774,6 @@ __global__ void reduce_patches_kernel(const DWin* __restrict__ wins, const int* 
         }
     }
     const long long* __restrict__ tp = wn.tile_patch;
-    int PV = 1;
-    for (int t = 0; t < D; ++t) PV *= PE;
-    // all patches of tile T at element o (heavy tiles: pre-reduced into the first)
-    auto tile_sum = [&](int T, int o) {
-        const long long off = tp[T];
-        if (off < 0) return 0.0;
-        const int ni = wn.tile_first[T + 1] - wn.tile_first[T];
-        const int cnt = ni > kHeavyItems ? 1 : ni;
-        double s = 0.0;
-        for (int k = 0; k < cnt; ++k) s += patches[off + static_cast<long long>(k) * PV + o];
-        return s;
-    };
     double sum = 0.0;
     if (!wn.wrap) {
         // extended index e = lg; covering tiles T = e/TC - a, a < NC, with e - T TC < PE
@@ -797,20 +785,23 @@ __global__ void reduce_patches_kernel(const DWin* __restrict__ wins, const int* 
             const int T0 = thi[0] - a0, o0 = lg[0] - T0 * TC;
             if (T0 < 0 || o0 >= PE) continue;
             if constexpr (D == 1) {
-                sum += tile_sum(T0, o0);
+                const long long off = tp[T0];
+                if (off >= 0) sum += patches[off + o0];
             } else {
 #pragma unroll
                 for (int a1 = 0; a1 < NC; ++a1) {
                     const int T1 = thi[1] - a1, o1 = lg[1] - T1 * TC;
                     if (T1 < 0 || o1 >= PE) continue;
                     if constexpr (D == 2) {
-                        sum += tile_sum(T0 * nt + T1, o0 * PE + o1);
+                        const long long off = tp[T0 * nt + T1];
+                        if (off >= 0) sum += patches[off + o0 * PE + o1];
                     } else {
 #pragma unroll
                         for (int a2 = 0; a2 < NC; ++a2) {
                             const int T2 = thi[2] - a2, o2 = lg[2] - T2 * TC;
                             if (T2 < 0 || o2 >= PE) continue;
-                            sum += tile_sum((T0 * nt + T1) * nt + T2, (o0 * PE + o1) * PE + o2);
+                            const long long off = tp[(T0 * nt + T1) * nt + T2];
+                            if (off >= 0) sum += patches[off + (o0 * PE + o1) * PE + o2];
                         }
                     }
                 }
@@ -828,17 +819,20 @@ __global__ void reduce_patches_kernel(const DWin* __restrict__ wins, const int* 
             for (int T0 = KSVM_TLO(e0); T0 <= KSVM_THI(e0); ++T0) {
                 const int o0 = e0 - T0 * TC;
                 if constexpr (D == 1) {
-                    sum += tile_sum(T0, o0);
+                    const long long off = tp[T0];
+                    if (off >= 0) sum += patches[off + o0];
                 } else {
                     for (int e1 = e0s[1]; e1 < Eext; e1 += wn.M)
                         for (int T1 = KSVM_TLO(e1); T1 <= KSVM_THI(e1); ++T1) {
                             const int o1 = o0 * PE + e1 - T1 * TC;
                             if constexpr (D == 2) {
-                                sum += tile_sum(T0 * nt + T1, o1);
+                                const long long off = tp[T0 * nt + T1];
+                                if (off >= 0) sum += patches[off + o1];
                             } else {
                                 for (int e2 = e0s[2]; e2 < Eext; e2 += wn.M)
                                     for (int T2 = KSVM_TLO(e2); T2 <= KSVM_THI(e2); ++T2) {
-                                        sum += tile_sum((T0 * nt + T1) * nt + T2, o1 * PE + e2 - T2 * TC);
+                                        const long long off = tp[(T0 * nt + T1) * nt + T2];
+                                        if (off >= 0) sum += patches[off + o1 * PE + e2 - T2 * TC];
                                     }
                             }
                         }
@@ -875,10 +869,8 @@ namespace {
 // Owner-tile block reduction of one tile (whole CTA). soff/sT: SMEM scratch.
 template <int D, int NC>
 __device__ void reduce_owner_unit(const DWin& wn, int tileT, const double* __restrict__ patches,
-                                  long long* soff, int* scnt, int (*sT)[3], int* any) {
+                                  long long* soff, int (*sT)[3], int* any) {
     const int TC = wn.TC, PE = wn.PE, nt = wn.ntile, Lg = wn.Lg;
-    int PVw = 1;
-    for (int t = 0; t < D; ++t) PVw *= PE;
     const int nown = (Lg + TC - 1) / TC;  // owner blocks per dimension (tiles + halo blocks)
     constexpr int NS = D == 1 ? NC : (D == 2 ? NC * NC : NC * NC * NC);
     int T[3] = {0, 0, 0};
@@ -906,9 +898,6 @@ __device__ void reduce_owner_unit(const DWin& wn, int tileT, const double* __res
         for (int t = 0; t < D; ++t) lin = lin * nt + min(max(Sx[t], 0), nt - 1);
         const long long off = ok ? wn.tile_patch[lin] : -1;
         soff[threadIdx.x] = off;
-        // items whose patches to sum: heavy tiles were pre-reduced into their first patch
-        const int ni = ok ? wn.tile_first[lin + 1] - wn.tile_first[lin] : 0;
-        scnt[threadIdx.x] = ni > kHeavyItems ? 1 : ni;
 #pragma unroll
         for (int t = 0; t < 3; ++t) sT[threadIdx.x][t] = Sx[t];
         if (off >= 0) *any = 1;
@@ -958,10 +947,7 @@ __device__ void reduce_owner_unit(const DWin& wn, int tileT, const double* __res
                     o = o * PE + od[t][a[t]];
                 }
                 const long long off = soff[q];
-                if (ok && off >= 0) {
-                    const int cnt = scnt[q];
-                    for (int k = 0; k < cnt; ++k) sum += patches[off + static_cast<long long>(k) * PVw + o];
-                }
+                if (ok && off >= 0) sum += patches[off + o];
             }
         }
         long long gi = 0;
@@ -1078,10 +1064,9 @@ reduce_owner_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots
     if (static_cast<int>(blockIdx.x) >= ntd) return;
     constexpr int NS = D == 1 ? NC : (D == 2 ? NC * NC : NC * NC * NC);
     __shared__ long long soff[NS];
-    __shared__ int scnt[NS];
     __shared__ int sT[NS][3];
     __shared__ int any;
-    reduce_owner_unit<D, NC>(wn, blockIdx.x, patches, soff, scnt, sT, &any);
+    reduce_owner_unit<D, NC>(wn, blockIdx.x, patches, soff, sT, &any);
 }
 
 __global__ void __launch_bounds__(128)
