@@ -78,6 +78,24 @@ __device__ __forceinline__ void stage_row(double* st, const double* R, double P,
     *reinterpret_cast<int*>(st + D * S) = code;
 }
 
+// Power-only staging row: w_t[o] = (P for t = 0) * Q_t^o. The constant factor
+// R[o] = exp(-o^2/b) of each tap is applied per cell block instead (spread:
+// at flush; it is a fixed product R[a] R[b] R[c] per block node), which
+// saves 24 FP64 multiplies per point on the datapath DMMA shares.
+template <int D, int S>
+__device__ __forceinline__ void stage_pow(double* st, double P, const double* Q, int code) {
+#pragma unroll
+    for (int t = 0; t < D; ++t) {
+        double q = t == 0 ? P : 1.0;
+#pragma unroll
+        for (int o = 0; o < S; ++o) {
+            st[t * S + o] = q;
+            q *= Q[t];
+        }
+    }
+    *reinterpret_cast<int*>(st + D * S) = code;
+}
+
 // Registers of one prefetched point (software pipeline over 32-point batches).
 template <int D>
 struct Pref {
@@ -190,6 +208,8 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     double R[S];
 #pragma unroll
     for (int o = 0; o < S; ++o) R[o] = wn.R[o];
+    // this lane's block nodes are (a = r, b = g, c = 2t + e): window factor R[r] R[g] R[2t+e]
+    const double rg0 = wn.R[g] * wn.R[2 * t], rg1 = wn.R[g] * wn.R[2 * t + 1];
     for (int k = lane; k < PV; k += 32) wp[k] = 0.0;
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
@@ -203,10 +223,24 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
         double* dst = wp + (l0 * PE + l1 + g) * PE + l2 + 2 * t;
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-            dst[r * PE * PE] += acc[r][0];
-            dst[r * PE * PE + 1] += acc[r][1];
+            dst[r * PE * PE] = fma(acc[r][0], R[r] * rg0, dst[r * PE * PE]);
+            dst[r * PE * PE + 1] = fma(acc[r][1], R[r] * rg1, dst[r * PE * PE + 1]);
             acc[r][0] = acc[r][1] = 0.0;
         }
+    };
+    // 4 points of the current cell (lane t carries point p0 + t), no masking
+    auto group4 = [&](int p0) {
+        const double* st = stage + (p0 + t) * RL;
+        const double2 w01 = ld2(st), w23 = ld2(st + 2), w45 = ld2(st + 4), w67 = ld2(st + 6);
+        const double w1g = st[S + g], bq = st[2 * S + g];
+        dmma(acc[0][0], acc[0][1], w01.x * w1g, bq);
+        dmma(acc[1][0], acc[1][1], w01.y * w1g, bq);
+        dmma(acc[2][0], acc[2][1], w23.x * w1g, bq);
+        dmma(acc[3][0], acc[3][1], w23.y * w1g, bq);
+        dmma(acc[4][0], acc[4][1], w45.x * w1g, bq);
+        dmma(acc[5][0], acc[5][1], w45.y * w1g, bq);
+        dmma(acc[6][0], acc[6][1], w67.x * w1g, bq);
+        dmma(acc[7][0], acc[7][1], w67.y * w1g, bq);
     };
 
     // software pipeline: per-point factors two batches ahead, v one batch ahead
@@ -223,7 +257,7 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     __syncwarp();
     for (int base = wb; base < we; base += 32) {
         const int cnt = min(32, we - base);
-        if (lane < cnt) stage_row<D, S>(stage + lane * RL, R, pa.P * va, pa.Q, pa.code);
+        if (lane < cnt) stage_pow<D, S>(stage + lane * RL, pa.P * va, pa.Q, pa.code);
         pa = pb;
         if (base + 32 + lane < we) va = __ldg(v + pa.perm);
         if (base + 64 + lane < we) pb.load(ps, base + 64 + lane);
@@ -234,6 +268,12 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
             if (cp != cur) {
                 if (cur >= 0) flush(cur);
                 cur = cp;
+            }
+            if (p + 7 < cnt && row_code(stage + (p + 7) * RL, D, S) == cur) {
+                group4(p);  // 8 points of one cell (sorted): two unmasked rounds
+                group4(p + 4);
+                p += 8;
+                continue;
             }
             const int q = p + t;
             const bool valid = q < cnt && row_code(stage + q * RL, D, S) == cur;
