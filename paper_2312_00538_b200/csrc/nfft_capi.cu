@@ -50,7 +50,7 @@ void launch_cell_keys(const double* x0, const double* x1, const double* x2, int 
                       int* bad, cudaStream_t st);
 void launch_factors(const double* x0, const double* x1, const double* x2, const int* perm, int d,
                     long long n, double Mf, int m, double invb, double Cw, int cmin, int TC,
-                    double4* F, int2* CP, cudaStream_t st);
+                    int tile_rel, double4* F, int2* CP, cudaStream_t st);
 
 namespace {
 
@@ -292,7 +292,8 @@ void build_pointset(PointSet& ps, const std::vector<double>& scaled_cm, int64_t 
     ps.F.alloc(n);
     ps.CP.alloc(n);
     launch_factors(raw[0].p, d > 1 ? raw[1].p : nullptr, d > 2 ? raw[2].p : nullptr, ps.perm.p, d, n,
-                   static_cast<double>(g.M), g.m, g.invb, g.Cw, g.cmin, g.TC, ps.F.p, ps.CP.p, st);
+                   static_cast<double>(g.M), g.m, g.invb, g.Cw, g.cmin, g.TC,
+                   /*tile_rel=*/(d == 3 && g.S == 8) ? 1 : 0, ps.F.p, ps.CP.p, st);
     CK(cudaGetLastError());
     std::vector<unsigned> hk(static_cast<size_t>(n));
     int hbad = 0;
@@ -538,7 +539,7 @@ struct Engine {
         dw.bwin = bwin;
         dw.invb = g.invb;
         dw.Cw = g.Cw;
-        for (int o = 0; o < kMaxSpan; ++o) dw.R[o] = o < g.S ? std::exp(-static_cast<double>(o) * o / bwin) : 0.0;
+        for (int o = 0; o < kMaxSpan; ++o) dw.R[o] = std::exp(-static_cast<double>(o) * o / bwin);
         dw.G = w.G.p;
         dw.H = w.H.p;
         for (int k = 0; k < 4; ++k) dw.T[k] = w.T[k].p;

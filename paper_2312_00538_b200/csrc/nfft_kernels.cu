@@ -122,7 +122,7 @@ struct Pref {
 // Load the (TC+S-1)^d grid halo of a tile into SMEM (wrap / bounds aware).
 // PEc/TCc > 0: compile-time patch/tile edge (the m = 4 kernels), so the
 // per-element index arithmetic has no runtime divisions.
-template <int D, int PEc = 0, int TCc = 0>
+template <int D, int PEc = 0, int TCc = 0, bool kFoldR = false>
 __device__ __forceinline__ void load_halo(double* halo, const DWin& wn, const int* tc, int TCr, int PEr,
                                           int PV) {
     const int PE = PEc > 0 ? PEc : PEr, TC = TCc > 0 ? TCc : TCr;
@@ -146,12 +146,22 @@ __device__ __forceinline__ void load_halo(double* halo, const DWin& wn, const in
                 ok = ok && tc[t] * TC + n[t] < Lg;
                 off = off * Lg + n[t];
             }
-            halo[k] = ok ? __ldg(wn.H + base + off) : 0.0;
+            double h = ok ? __ldg(wn.H + base + off) : 0.0;
+            if (kFoldR) {  // tile-relative window factor R[j0] R[j1] R[j2] (factors_kernel)
+#pragma unroll
+                for (int t = 0; t < D; ++t) h *= wn.R[n[t]];
+            }
+            halo[k] = h;
         } else {
             long long gi = 0;
 #pragma unroll
             for (int t = 0; t < D; ++t) gi = gi * Lg + pmod(wn.lo + tc[t] * TC + n[t], wn.M);
-            halo[k] = __ldg(wn.H + gi);
+            double h = __ldg(wn.H + gi);
+            if (kFoldR) {
+#pragma unroll
+                for (int t = 0; t < D; ++t) h *= wn.R[n[t]];
+            }
+            halo[k] = h;
         }
     }
 }
@@ -205,11 +215,6 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     const Item it = items[blockIdx.x];
     const DPSet ps = psets[it.ps];
     const DWin& wn = wins[ps.win];
-    double R[S];
-#pragma unroll
-    for (int o = 0; o < S; ++o) R[o] = wn.R[o];
-    // this lane's block nodes are (a = r, b = g, c = 2t + e): window factor R[r] R[g] R[2t+e]
-    const double rg0 = wn.R[g] * wn.R[2 * t], rg1 = wn.R[g] * wn.R[2 * t + 1];
     for (int k = lane; k < PV; k += 32) wp[k] = 0.0;
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
@@ -223,8 +228,8 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
         double* dst = wp + (l0 * PE + l1 + g) * PE + l2 + 2 * t;
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-            dst[r * PE * PE] = fma(acc[r][0], R[r] * rg0, dst[r * PE * PE]);
-            dst[r * PE * PE + 1] = fma(acc[r][1], R[r] * rg1, dst[r * PE * PE + 1]);
+            dst[r * PE * PE] += acc[r][0];
+            dst[r * PE * PE + 1] += acc[r][1];
             acc[r][0] = acc[r][1] = 0.0;
         }
     };
@@ -296,12 +301,14 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     }
     if (cur >= 0) flush(cur);
     __syncthreads();
+    // tile-relative factors (factors_kernel): node (j0, j1, j2) of the patch
+    // carries R[j0] R[j1] R[j2]
     double* out = patches + it.patch;
     for (int k = threadIdx.x; k < PV; k += W * 32) {
         double s = smem[k];
 #pragma unroll
         for (int q = 1; q < W; ++q) s += smem[q * PV + k];
-        out[k] = s;
+        out[k] = s * (wn.R[k / (PE * PE)] * wn.R[(k / PE) % PE] * wn.R[k % PE]);
     }
 }
 
@@ -329,12 +336,9 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     const Item it = items[blockIdx.x];
     const DPSet ps = psets[it.ps];
     const DWin& wn = wins[ps.win];
-    double R[S];
-#pragma unroll
-    for (int o = 0; o < S; ++o) R[o] = wn.R[o];
     int tc[3];
     tile_coords(it.tile, D, wn.ntile, tc);
-    load_halo<D, PE, TC>(halo, wn, tc, TC, PE, PV);
+    load_halo<D, PE, TC, true>(halo, wn, tc, TC, PE, PV);
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
     Pref<D> pa, pb;  // factors of the current and the next batch
@@ -358,7 +362,7 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
         const int cnt = min(32, we - base);
         if (lane < cnt) {
             double* st = stage + lane * RL;
-            stage_row<D, S>(st, R, pa.P, pa.Q, pa.code);
+            stage_pow<D, S>(st, pa.P, pa.Q, pa.code);
             reinterpret_cast<int*>(st + D * S)[1] = pa.perm;
         }
         pa = pb;
@@ -1191,27 +1195,35 @@ __global__ void cell_keys_kernel(const double* __restrict__ x0, const double* __
 }
 
 // Window factors of each sorted point (nfft_engine.cuh): {P, Q_t}, {code, perm}.
+// tile_rel (d = 3, m = 4 kernels): factors relative to the tile origin node
+// instead of the cell's first tap: delta_t = u_t + l_t (l_t = cell offset in
+// its tile), P = C^d exp(-sum_t (delta_t^2 - 2 l_t delta_t) / b) (this folds
+// Q_t^{l_t}), Q_t = exp(2 delta_t / b). Tap o of the point then weighs
+// P prod Q_t^{o_t} R[l_t + o_t], and R[j] = exp(-j^2/b) depends only on the
+// tile-relative node j, so the kernels apply it per patch / halo node.
 __global__ void factors_kernel(const double* __restrict__ x0, const double* __restrict__ x1,
                                const double* __restrict__ x2, const int* __restrict__ perm, int d,
                                long long n, double Mf, int m, double invb, double Cw, int cmin,
-                               int TC, double4* __restrict__ F, int2* __restrict__ CP) {
+                               int TC, int tile_rel, double4* __restrict__ F, int2* __restrict__ CP) {
     for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x) {
         const int src = perm[i];
         const double* xs[3] = {x0, x1, x2};
         double Q[3] = {0.0, 0.0, 0.0};
-        double su2 = 0.0, pre = 1.0;
+        double ex = 0.0, pre = 1.0;
         int cd = 0;
         for (int t = 0; t < d; ++t) {
             const double xm = xs[t][src] * Mf;
             const double fl = floor(xm);
             const double u = (xm - fl) + static_cast<double>(m - 1);
-            su2 += u * u;
+            const int l = (static_cast<int>(fl) - cmin) % TC;
+            const double dl = tile_rel ? u + l : u;
+            ex += tile_rel ? dl * dl - 2.0 * l * dl : dl * dl;
             pre *= Cw;
-            Q[t] = exp((2.0 * u) * invb);
-            cd = cd * TC + (static_cast<int>(fl) - cmin) % TC;
+            Q[t] = exp((2.0 * dl) * invb);
+            cd = cd * TC + l;
         }
-        F[i] = make_double4(pre * exp(-su2 * invb), Q[0], Q[1], Q[2]);
+        F[i] = make_double4(pre * exp(-ex * invb), Q[0], Q[1], Q[2]);
         CP[i] = make_int2(cd, src);
     }
 }
@@ -1376,10 +1388,10 @@ void launch_cell_keys(const double* x0, const double* x1, const double* x2, int 
 
 void launch_factors(const double* x0, const double* x1, const double* x2, const int* perm, int d,
                     long long n, double Mf, int m, double invb, double Cw, int cmin, int TC,
-                    double4* F, int2* CP, cudaStream_t st) {
+                    int tile_rel, double4* F, int2* CP, cudaStream_t st) {
     const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 16));
     factors_kernel<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(x0, x1, x2, perm, d, n, Mf, m, invb, Cw,
-                                                             cmin, TC, F, CP);
+                                                             cmin, TC, tile_rel, F, CP);
 }
 
 }  // namespace ksvm_nfft
