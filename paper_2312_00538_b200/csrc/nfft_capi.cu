@@ -397,6 +397,8 @@ std::vector<double> scale_cm(const Window& w, const double* pts, int64_t t, int6
 struct Engine {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t side[4] = {nullptr, nullptr, nullptr, nullptr};  // class branches (d = 1, 2)
+    cudaEvent_t ev_fork = nullptr, ev_join[4] = {nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     static constexpr int kMaxTicks = 24;
     cudaEvent_t ev_stage[kMaxTicks] = {};
@@ -418,8 +420,10 @@ struct Engine {
     DevBuf<Item> d_gitems;  // gather items of owned windows, grouped by d
     int gclass_begin[4] = {0, 0, 0, 0}, gclass_end[4] = {0, 0, 0, 0};
     DevBuf<int> d_slots;    // 0..P_owned-1
-    DevBuf<int2> d_multi;   // (slot, tile) of tiles split into several items
+    DevBuf<int2> d_multi;   // (slot, tile) of tiles split into several items, grouped by d
     int n_multi = 0, max_pv = 0;
+    int multi_begin[4] = {0, 0, 0, 0}, n_multi_cls[4] = {0, 0, 0, 0};
+    int slot_begin[4] = {0, 0, 0, 0}, nslots_cls[4] = {0, 0, 0, 0};  // d_slots grouped by d
     DevBuf<double> d_eta;
     DevBuf<double> patches, parts, vbuf, ybuf;
     DevBuf<double> d_raw;   // SoA raw window features (entries), original order
@@ -439,6 +443,14 @@ struct Engine {
             cudaSetDevice(device);
             cudaStreamSynchronize(stream);
             drop_graphs();
+            for (int D = 1; D <= 2; ++D) {
+                if (side[D]) {
+                    cudaStreamSynchronize(side[D]);
+                    cudaStreamDestroy(side[D]);
+                }
+                if (ev_join[D]) cudaEventDestroy(ev_join[D]);
+            }
+            if (ev_fork) cudaEventDestroy(ev_fork);
             cudaStreamDestroy(stream);
             cudaEventDestroy(ev_in);
             cudaEventDestroy(ev_out);
@@ -458,6 +470,11 @@ struct Engine {
         CK(cudaSetDevice(dev));
         ensure_attributes(dev);
         CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        for (int D = 1; D <= 2; ++D) {
+            CK(cudaStreamCreateWithFlags(&side[D], cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&ev_join[D], cudaEventDisableTiming));
+        }
+        CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
         stage_timing = std::getenv("KSVM_NFFT_STAGE_TIMING") != nullptr;
@@ -556,6 +573,7 @@ struct Engine {
         long long patch_total = 0;
         for (int D = 1; D <= 3; ++D) {
             class_begin[D] = static_cast<int>(all.size());
+            multi_begin[D] = static_cast<int>(multi.size());
             for (int s = 0; s < P; ++s) {
                 Window& w = *wins[static_cast<size_t>(owned[static_cast<size_t>(s)])];
                 if (w.d != D) continue;
@@ -597,16 +615,22 @@ struct Engine {
                 }
             }
             gclass_end[D] = static_cast<int>(gall.size());
+            n_multi_cls[D] = static_cast<int>(multi.size()) - multi_begin[D];
         }
         std::vector<DWin> dws(static_cast<size_t>(P));
         std::vector<double> eta(static_cast<size_t>(P));
-        std::vector<int> slots(static_cast<size_t>(P));
+        std::vector<int> slots;  // window slots grouped by d (per-class launches)
+        for (int D = 1; D <= 3; ++D) {
+            slot_begin[D] = static_cast<int>(slots.size());
+            for (int s = 0; s < P; ++s)
+                if (wins[static_cast<size_t>(owned[static_cast<size_t>(s)])]->d == D) slots.push_back(s);
+            nslots_cls[D] = static_cast<int>(slots.size()) - slot_begin[D];
+        }
         parts.alloc(static_cast<size_t>(std::max(P, 1)) * n);
         for (int s = 0; s < P; ++s) {
             Window& w = *wins[static_cast<size_t>(owned[static_cast<size_t>(s)])];
             dws[static_cast<size_t>(s)] = w.dw;
             eta[static_cast<size_t>(s)] = w.eta;
-            slots[static_cast<size_t>(s)] = s;
             DPSet& p = ps[static_cast<size_t>(s)];
             p.F = w.src.F.p;
             p.CP = w.src.CP.p;
@@ -618,7 +642,7 @@ struct Engine {
         d_ps.upload(ps.data(), ps.size(), stream);
         d_items.upload(all.data(), all.size(), stream);
         d_gitems.upload(gall.data(), gall.size(), stream);
-        d_slots.upload(slots.data(), slots.size(), stream);
+        if (!slots.empty()) d_slots.upload(slots.data(), slots.size(), stream);
         n_multi = static_cast<int>(multi.size());
 
         if (n_multi) d_multi.upload(multi.data(), multi.size(), stream);
@@ -638,44 +662,74 @@ struct Engine {
         ++nticks;
     }
 
-    // spread -> reduce -> conv -> (gather over `targets` or sources)
-    void run_grid(const double* v) {
-        const int P = P_owned();
+    // One dimension class (all owned windows with d_l = D): spread -> patch
+    // reduce -> separable convolution -> (gather). Classes are independent
+    // until `combine`, so they run on separate streams (graph branches).
+    void run_class(int D, const double* v, cudaStream_t st, bool gather) {
         static const char* kSpread[4] = {"", "spread_d1", "spread_d2", "spread_d3"};
-        for (int D = 1; D <= 3; ++D) {
-            const int cnt = class_end[D] - class_begin[D];
-            if (cnt == 0) continue;
-            tick(kSpread[D]);
-            launch_spread(D, 2 * cfg.window_cutoff, class_PE[D], d_items.p + class_begin[D], cnt,
-                          d_ps.p, d_wins.p, v, patches.p, stream);
-            ++g_launches;
-        }
-        CK(cudaGetLastError());
-        if (n_multi) {
+        static const char* kGather[4] = {"", "gather_d1", "gather_d2", "gather_d3"};
+        static const char* kConv[3] = {"conv_0", "conv_1", "conv_2"};
+        const int cnt = class_end[D] - class_begin[D];
+        if (cnt == 0) return;
+        tick(kSpread[D]);
+        launch_spread(D, 2 * cfg.window_cutoff, class_PE[D], d_items.p + class_begin[D], cnt, d_ps.p,
+                      d_wins.p, v, patches.p, st);
+        ++g_launches;
+        if (n_multi_cls[D]) {
             tick("tile_reduce");
-            launch_tile_reduce(d_wins.p, d_multi.p, n_multi, max_pv, patches.p, stream);
+            launch_tile_reduce(d_wins.p, d_multi.p + multi_begin[D], n_multi_cls[D], max_pv, patches.p, st);
             ++g_launches;
         }
         tick("reduce");
-        for (int D = 1; D <= 3; ++D) {
-            for (int wrap = 0; wrap < 2; ++wrap) {
-                if (!(wrap ? has_wrap : has_nowrap)[D]) continue;
-                launch_reduce(d_wins.p, d_slots.p, P, max_nodes, D, 2 * cfg.window_cutoff, patches.p,
-                              wrap != 0, max_tiles[D], stream);
-                ++g_launches;
-            }
+        for (int wrap = 0; wrap < 2; ++wrap) {
+            if (!(wrap ? has_wrap : has_nowrap)[D]) continue;
+            launch_reduce(d_wins.p, d_slots.p + slot_begin[D], nslots_cls[D], max_nodes, D,
+                          2 * cfg.window_cutoff, patches.p, wrap != 0, max_tiles[D], st);
+            ++g_launches;
         }
-        int maxd = 0;
-        for (int s = 0; s < P; ++s)
-            maxd = std::max(maxd, wins[static_cast<size_t>(owned[static_cast<size_t>(s)])]->d);
-        static const char* kConv[3] = {"conv_0", "conv_1", "conv_2"};
-        for (int stg = 0; stg < maxd; ++stg) {
+        for (int stg = 0; stg < D; ++stg) {
             tick(kConv[stg]);
-            launch_conv(d_wins.p, d_slots.p, P, max_lg, max_fibres, stg, stream);
+            launch_conv(d_wins.p, d_slots.p + slot_begin[D], nslots_cls[D], max_lg, max_fibres, stg, st);
+            ++g_launches;
+        }
+        if (gather) {
+            const int gcnt = gclass_end[D] - gclass_begin[D];
+            tick(kGather[D]);
+            launch_gather(D, 2 * cfg.window_cutoff, class_PE[D], d_gitems.p + gclass_begin[D], gcnt, d_ps.p,
+                          d_wins.p, st);
             ++g_launches;
         }
         CK(cudaGetLastError());
     }
+
+    // All classes; concurrent branches unless per-launch timing is on.
+    void run_classes(const double* v, bool gather) {
+        int ncls = 0;
+        for (int D = 1; D <= 3; ++D) ncls += class_end[D] > class_begin[D] ? 1 : 0;
+        if (stage_timing || ncls < 2) {
+            for (int D = 3; D >= 1; --D) run_class(D, v, stream, gather);
+            return;
+        }
+        CK(cudaEventRecord(ev_fork, stream));
+        bool first = true;
+        for (int D = 3; D >= 1; --D) {
+            if (class_end[D] == class_begin[D]) continue;
+            cudaStream_t st = stream;
+            if (!first) {
+                st = side[D];
+                CK(cudaStreamWaitEvent(st, ev_fork, 0));
+            }
+            run_class(D, v, st, gather);
+            if (!first) {
+                CK(cudaEventRecord(ev_join[D], st));
+                CK(cudaStreamWaitEvent(stream, ev_join[D], 0));
+            }
+            first = false;
+        }
+    }
+
+    // grid stage only (cross applies gather over their own targets afterwards)
+    void run_grid(const double* v) { run_classes(v, false); }
 
     void run_apply(const double* v, double* y) {
         const int P = P_owned();
@@ -685,16 +739,7 @@ struct Engine {
             return;
         }
         nticks = 0;
-        run_grid(v);
-        static const char* kGather[4] = {"", "gather_d1", "gather_d2", "gather_d3"};
-        for (int D = 1; D <= 3; ++D) {
-            const int cnt = gclass_end[D] - gclass_begin[D];
-            if (cnt == 0) continue;
-            tick(kGather[D]);
-            launch_gather(D, 2 * cfg.window_cutoff, class_PE[D], d_gitems.p + gclass_begin[D], cnt,
-                          d_ps.p, d_wins.p, stream);
-            ++g_launches;
-        }
+        run_classes(v, true);
         tick("combine");
         launch_combine(y, parts.p, d_eta.p, P, n, stream);
         ++g_launches;
