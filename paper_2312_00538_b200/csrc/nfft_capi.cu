@@ -38,8 +38,6 @@ void launch_tile_reduce(const DWin* wins, const int2* multi, int nmulti, int max
 void launch_conv(const DWin* wins, const int* slots, int nslots, int Lg_max, long long max_fibres,
                  int stage, cudaStream_t st);
 int conv_max_lg();
-int conv_plane_max_lg();
-void launch_conv_plane(const DWin* wins, const int* slots, int nslots, int Lg_max, cudaStream_t st);
 
 void launch_combine(double* y, const double* parts, const double* eta, int P, long long n,
                     cudaStream_t st);
@@ -689,18 +687,9 @@ struct Engine {
                           2 * cfg.window_cutoff, patches.p, wrap != 0, max_tiles[D], st);
             ++g_launches;
         }
-        // separable convolution: per-stage Toeplitz GEMMs; the last two stages
-        // (d >= 2) fused per plane when a plane fits in SMEM
-        const bool plane = D >= 2 && max_lg <= conv_plane_max_lg();
-        const int nstage = plane ? D - 2 : D;  // d = 3: stage 0 only; d = 2: none
-        for (int stg = 0; stg < nstage; ++stg) {
+        for (int stg = 0; stg < D; ++stg) {
             tick(kConv[stg]);
             launch_conv(d_wins.p, d_slots.p + slot_begin[D], nslots_cls[D], max_lg, max_fibres, stg, st);
-            ++g_launches;
-        }
-        if (plane) {
-            tick("conv_plane");
-            launch_conv_plane(d_wins.p, d_slots.p + slot_begin[D], nslots_cls[D], max_lg, st);
             ++g_launches;
         }
         if (gather) {

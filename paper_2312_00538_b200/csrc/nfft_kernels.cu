@@ -1122,73 +1122,6 @@ conv_stage_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots, 
     conv_tile_unit(wn, stage, tile);
 }
 
-// The last two separable-convolution stages fused per plane: for d = 3,
-// stage 1 (along dim 1) and stage 2 (along dim 0) both stay inside the plane
-// of fixed i2, so one CTA keeps the plane in SMEM (Ta, Ts -> P, Q -> H); for
-// d = 2 the whole grid is that plane (stages 0 and 1 from G). blockIdx.x =
-// plane (i2), blockIdx.y = window slot. Used when 4 Lg^2 doubles fit in SMEM.
-constexpr int kPlaneMaxL = 72;
-
-__global__ void __launch_bounds__(256)
-conv_plane_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots) {
-    extern __shared__ __align__(16) double smem[];
-    const DWin& wn = wins[slots[blockIdx.y]];
-    const int D = wn.d, Lg = wn.Lg, L2 = Lg * Lg;
-    const int plane = blockIdx.x;
-    if (D < 2 || (D == 2 && plane > 0) || plane >= Lg) return;
-    double* X0 = smem;
-    double* X1 = X0 + L2;
-    double* Y0 = X1 + L2;
-    double* Y1 = Y0 + L2;
-    double* tA = Y1 + L2;
-    double* tS = tA + 2 * Lg - 1;
-    for (int k = threadIdx.x; k < 2 * Lg - 1; k += blockDim.x) {
-        tA[k] = wn.tabA[k];
-        tS[k] = wn.tabS[k];
-    }
-    // element (i0, i1) of the plane lives at (i0 Lg + i1) * pstride + plane
-    const int pstride = D == 3 ? Lg : 1;
-    const double* in0 = D == 3 ? wn.T[0] : wn.G;
-    for (int e = threadIdx.x; e < L2; e += blockDim.x) {
-        const long long ad = static_cast<long long>(e) * pstride + plane;
-        X0[e] = in0[ad];
-        if (D == 3) X1[e] = wn.T[1][ad];
-    }
-    __syncthreads();
-    // along i1: D = 3: P = A Ta - S Ts, Q = A Ts + S Ta;  D = 2: Ta = A G, Ts = S G
-    for (int e = threadIdx.x; e < L2; e += blockDim.x) {
-        const int i0 = e / Lg, i1 = e - i0 * Lg;
-        const double* x0 = X0 + i0 * Lg;
-        const double* x1 = X1 + i0 * Lg;
-        const double* a = tA + (Lg - 1 + i1);  // A[i1][j] = a(i1 - j)
-        const double* sv = tS + (Lg - 1 + i1);
-        double p = 0.0, q = 0.0;
-        if (D == 3) {
-            for (int j = 0; j < Lg; ++j) {
-                p = fma(a[-j], x0[j], fma(-sv[-j], x1[j], p));
-                q = fma(a[-j], x1[j], fma(sv[-j], x0[j], q));
-            }
-        } else {
-            for (int j = 0; j < Lg; ++j) {
-                p = fma(a[-j], x0[j], p);
-                q = fma(sv[-j], x0[j], q);
-            }
-        }
-        Y0[e] = p;
-        Y1[e] = q;
-    }
-    __syncthreads();
-    // along i0: H = A Y0 - S Y1
-    for (int e = threadIdx.x; e < L2; e += blockDim.x) {
-        const int i0 = e / Lg, i1 = e - i0 * Lg;
-        const double* a = tA + (Lg - 1 + i0);
-        const double* sv = tS + (Lg - 1 + i0);
-        double h = 0.0;
-        for (int j = 0; j < Lg; ++j) h = fma(a[-j], Y0[j * Lg + i1], fma(-sv[-j], Y1[j * Lg + i1], h));
-        wn.H[static_cast<long long>(e) * pstride + plane] = h;
-    }
-}
-
 // y[j] = sum over owned windows (ascending) of eta_l * out_l[j]
 // (P:src/fastsum.cpp:346-351: out = 0; out += eta_l * apply_l).
 __global__ void combine_kernel(double* __restrict__ y, const double* __restrict__ parts,
@@ -1338,7 +1271,6 @@ cudaError_t init_kernel_attributes() {
     set(reinterpret_cast<const void*>(spread2_s8_kernel<kW2>), spread2_smem());
     set(reinterpret_cast<const void*>(gather2_s8_kernel<kW2>), gather2_smem());
     set(reinterpret_cast<const void*>(spread1_s8_kernel<kW1>), spread1_smem());
-    set(reinterpret_cast<const void*>(conv_plane_kernel), sizeof(double) * (4 * kPlaneMaxL * kPlaneMaxL + 4 * kPlaneMaxL));
     const size_t big = 227 * 1024;
     set(reinterpret_cast<const void*>(spread_generic_kernel<1>), big);
     set(reinterpret_cast<const void*>(spread_generic_kernel<2>), big);
@@ -1427,14 +1359,6 @@ void launch_conv(const DWin* wins, const int* slots, int nslots, int Lg_max, lon
 }
 
 int conv_max_lg() { return kConvMaxL; }
-
-size_t conv_plane_smem(int Lg) { return sizeof(double) * (4 * Lg * Lg + 2 * (2 * Lg - 1)); }
-int conv_plane_max_lg() { return kPlaneMaxL; }
-
-void launch_conv_plane(const DWin* wins, const int* slots, int nslots, int Lg_max, cudaStream_t st) {
-    if (nslots == 0) return;
-    conv_plane_kernel<<<dim3(static_cast<unsigned>(Lg_max), nslots), 256, conv_plane_smem(Lg_max), st>>>(wins, slots);
-}
 
 void launch_combine(double* y, const double* parts, const double* eta, int P, long long n,
                     cudaStream_t st) {
