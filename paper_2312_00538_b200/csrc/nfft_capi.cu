@@ -343,7 +343,7 @@ void build_pointset(PointSet& ps, const std::vector<double>& scaled_cm, int64_t 
 // (load balance) but no more, since each item writes one (TC+2m-1)^d patch
 // that must be reduced. Gather items carry no patch, so they are finer.
 int64_t item_chunk(int64_t total_points) {
-    return std::max<int64_t>(1024, (total_points + 148 * 24 - 1) / (148 * 24));
+    return std::max<int64_t>(2048, (total_points + 148 * 24 - 1) / (148 * 24));
 }
 int64_t gather_chunk(int64_t total_points) {
     return std::max<int64_t>(128, (total_points + 148 * 48 - 1) / (148 * 48));

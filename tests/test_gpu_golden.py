@@ -104,3 +104,21 @@ def test_launch_counter_and_kernels_run():
     pts = oracle.random_points(300, 3, 3)
     apply_fastsum(plan_fastsum(pts, 1.0), np.ones(300))
     assert _lib.launch_count() > before
+
+
+def test_window_mask_partial_sums_add_up():
+    # rank-local operators of the window-sharded path:
+    # the partial sums over complementary window sets add up to the full apply
+    from paper_2312_00538_b200 import sharding, workloads
+    w = workloads.config3(n=6000)
+    spec = AnovaKernelSpec(FeatureWindowing.explicit(w.windows))
+    full = anova_fast_operator(Dataset(w.points), spec, fit_fraction=w.fit_fraction).apply(w.v)
+    owner = sharding.lpt_assign(sharding.window_costs(w.windows), 3)
+    total = np.zeros_like(full)
+    for r in range(3):
+        op = anova_fast_operator(Dataset(w.points), spec, fit_fraction=w.fit_fraction,
+                                 window_mask=sharding.window_mask(owner, r))
+        total += op.apply(w.v)
+    assert rel(total, full) <= 1e-14
+    none = anova_fast_operator(Dataset(w.points), spec, window_mask=[False] * len(w.windows))
+    assert np.all(none.apply(w.v) == 0.0)
