@@ -342,8 +342,10 @@ void build_pointset(PointSet& ps, const std::vector<double>& scaled_cm, int64_t 
 // Points per spread item: ~24 items per SM over all windows of the operator
 // (load balance) but no more, since each item writes one (TC+2m-1)^d patch
 // that must be reduced. Gather items carry no patch, so they are finer.
-int64_t item_chunk(int64_t total_points) {
-    return std::max<int64_t>(2048, (total_points + 148 * 24 - 1) / (148 * 24));
+int64_t item_chunk(int64_t total_points, int d) {
+    // d = 3: large items (a 4^3-cell tile is rarely split, so no pre-reduce);
+    // d <= 2 have few, large tiles and need splitting for parallelism
+    return std::max<int64_t>(d == 3 ? 2048 : 512, (total_points + 148 * 24 - 1) / (148 * 24));
 }
 int64_t gather_chunk(int64_t total_points) {
     return std::max<int64_t>(128, (total_points + 148 * 48 - 1) / (148 * 48));
@@ -535,7 +537,7 @@ struct Engine {
         w.G.alloc(nodes);
         w.H.alloc(nodes);
         for (int k = 0; k < (d == 1 ? 0 : (d == 2 ? 2 : 4)); ++k) w.T[k].alloc(nodes);
-        build_pointset(w.src, sc, n, d, g, item_chunk(n * n_owned_windows),
+        build_pointset(w.src, sc, n, d, g, item_chunk(n * n_owned_windows, d),
                        gather_chunk(n * n_owned_windows), stream);
 
         DWin& dw = w.dw;
@@ -1208,7 +1210,7 @@ int ksvm_nfft_plan_apply_cross(const ksvm_nfft_plan* plan, const double* targets
         std::lock_guard<std::mutex> lk(E.mu);
         const Geometry g = w.geom;
         PointSet tp;
-        build_pointset(tp, sc, t, w.d, g, item_chunk(t), gather_chunk(t), E.stream);
+        build_pointset(tp, sc, t, w.d, g, item_chunk(t, w.d), gather_chunk(t), E.stream);
         DevBuf<double> tout;
         tout.alloc(t);
         DPSet dp{};
