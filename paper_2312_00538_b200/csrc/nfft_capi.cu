@@ -28,7 +28,7 @@ namespace ksvm_nfft {
 // launchers (nfft_kernels.cu)
 cudaError_t init_kernel_attributes();
 void launch_spread(int D, int S, int PE, const Item* items, int nitems, const DPSet* ps,
-                   const DWin* wins, const double* v, double* patches, cudaStream_t st);
+                   const DWin* wins, const double* v, double* patches, bool columns, cudaStream_t st);
 void launch_gather(int D, int S, int PE, const Item* items, int nitems, const DPSet* ps,
                    const DWin* wins, cudaStream_t st);
 void launch_reduce(const DWin* wins, const int* slots, int nslots, long long max_nodes, int D, int S,
@@ -396,6 +396,8 @@ std::vector<double> scale_cm(const Window& w, const double* pts, int64_t t, int6
 // ---------------------------------------------------------------------------
 // The engine: every owned window's plan plus the per-apply scratch.
 // ---------------------------------------------------------------------------
+constexpr long long kColumnSpreadDensity = 10;  // points per cell below which spread3c runs
+
 struct Engine {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -433,6 +435,7 @@ struct Engine {
     DevBuf<int> d_wdim;
     int class_begin[4] = {0, 0, 0, 0}, class_end[4] = {0, 0, 0, 0};
     int class_PE[4] = {0, 0, 0, 0};
+    bool spread_columns[4] = {false, false, false, false};  // d = 3: column-accumulating spread
     long long max_nodes = 0, max_fibres = 0;
     int max_lg = 0;
     bool has_dim[4] = {false, false, false, false};
@@ -566,6 +569,24 @@ struct Engine {
         dw.tabS = w.tabS.p;
     }
 
+    // Sparse cells favour the column-accumulating d = 3 spread (fewer SMEM
+    // flushes); dense cells the per-cell one (fewer FP64 operations per
+    // point). Threshold: mean points per cell of the occupied tiles.
+    bool use_column_spread(int D) const {
+        if (const char* e = std::getenv("KSVM_NFFT_SPREAD3")) return std::strcmp(e, "column") == 0;
+        long long pts = 0, cells = 0;
+        for (size_t s = 0; s < owned.size(); ++s) {
+            const Window& w = *wins[static_cast<size_t>(owned[s])];
+            if (w.d != D || w.dw.S != 8) continue;
+            const std::vector<int>& tf = w.src.tile_first;
+            long long occ = 0;
+            for (size_t T = 0; T + 1 < tf.size(); ++T) occ += tf[T + 1] > tf[T] ? 1 : 0;
+            pts += n;
+            cells += occ * w.dw.TC * w.dw.TC * w.dw.TC;
+        }
+        return cells > 0 && pts < kColumnSpreadDensity * cells;
+    }
+
     // Assign global item numbers / patch offsets and upload device tables.
     void finalize() {
         const int P = P_owned();
@@ -606,6 +627,7 @@ struct Engine {
                 }
             }
             class_end[D] = static_cast<int>(all.size());
+            spread_columns[D] = D == 3 && use_column_spread(D);
             gclass_begin[D] = static_cast<int>(gall.size());
             for (int s = 0; s < P; ++s) {
                 Window& w = *wins[static_cast<size_t>(owned[static_cast<size_t>(s)])];
@@ -675,7 +697,7 @@ struct Engine {
         if (cnt == 0) return;
         tick(kSpread[D]);
         launch_spread(D, 2 * cfg.window_cutoff, class_PE[D], d_items.p + class_begin[D], cnt, d_ps.p,
-                      d_wins.p, v, patches.p, st);
+                      d_wins.p, v, patches.p, spread_columns[D], st);
         ++g_launches;
         if (n_multi_cls[D]) {
             tick("tile_reduce");

@@ -124,7 +124,7 @@ struct Pref {
 // per-element index arithmetic has no runtime divisions.
 template <int D, int PEc = 0, int TCc = 0, bool kFoldR = false>
 __device__ __forceinline__ void load_halo(double* halo, const DWin& wn, const int* tc, int TCr, int PEr,
-                                          int PV) {
+                                          int PV, const double* sR = nullptr) {
     const int PE = PEc > 0 ? PEc : PEr, TC = TCc > 0 ? TCc : TCr;
     const int Lg = wn.Lg;
     const bool wrap = wn.wrap != 0;
@@ -149,7 +149,7 @@ __device__ __forceinline__ void load_halo(double* halo, const DWin& wn, const in
             double h = ok ? __ldg(wn.H + base + off) : 0.0;
             if (kFoldR) {  // tile-relative window factor R[j0] R[j1] R[j2] (factors_kernel)
 #pragma unroll
-                for (int t = 0; t < D; ++t) h *= wn.R[n[t]];
+                for (int t = 0; t < D; ++t) h *= sR[n[t]];
             }
             halo[k] = h;
         } else {
@@ -159,9 +159,41 @@ __device__ __forceinline__ void load_halo(double* halo, const DWin& wn, const in
             double h = __ldg(wn.H + gi);
             if (kFoldR) {
 #pragma unroll
-                for (int t = 0; t < D; ++t) h *= wn.R[n[t]];
+                for (int t = 0; t < D; ++t) h *= sR[n[t]];
             }
             halo[k] = h;
+        }
+    }
+}
+
+// d = 3, m = 4 halo with the tile-relative factor R[n0] R[n1] R[n2]
+// (factors_kernel) folded in. Thread k < PE^2 owns the column (n1, n2) and
+// walks n0, so the index arithmetic is per column, not per element.
+template <int PE, int TC>
+__device__ __forceinline__ void load_halo3_r(double* halo, const DWin& wn, const int* tc, const double* sR) {
+    const int k = threadIdx.x;
+    if (k >= PE * PE) return;
+    const int n1 = k / PE, n2 = k - n1 * PE;
+    const int Lg = wn.Lg;
+    const long long plane = static_cast<long long>(Lg) * Lg;
+    const double r12 = sR[n1] * sR[n2];
+    if (!wn.wrap) {
+        const int i0 = tc[0] * TC, i1 = tc[1] * TC + n1, i2 = tc[2] * TC + n2;
+        const bool ok12 = i1 < Lg && i2 < Lg;
+        const double* src = wn.H + (static_cast<long long>(i0) * Lg + i1) * Lg + i2;
+#pragma unroll
+        for (int n0 = 0; n0 < PE; ++n0) {
+            const bool ok = ok12 && i0 + n0 < Lg;
+            halo[n0 * PE * PE + k] = ok ? __ldg(src + n0 * plane) * (r12 * sR[n0]) : 0.0;
+        }
+    } else {
+        const long long o12 = static_cast<long long>(pmod(wn.lo + tc[1] * TC + n1, wn.M)) * Lg +
+                              pmod(wn.lo + tc[2] * TC + n2, wn.M);
+        int i0 = pmod(wn.lo + tc[0] * TC, wn.M);
+#pragma unroll
+        for (int n0 = 0; n0 < PE; ++n0) {
+            halo[n0 * PE * PE + k] = __ldg(wn.H + i0 * plane + o12) * (r12 * sR[n0]);
+            i0 = i0 + 1 == wn.M ? 0 : i0 + 1;
         }
     }
 }
@@ -189,6 +221,27 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
         : "+d"(d0), "+d"(d1)
         : "d"(a), "d"(b));
 }
+
+// Sum the per-warp patches (fixed warp order) and apply the tile-relative
+// factor R[j0] R[j1] R[j2] of node (j0, j1, j2) (factors_kernel). Thread
+// k < PE^2 owns the column (j1, j2) and walks j0.
+template <int W, int PE>
+__device__ __forceinline__ void spread3_epilogue(const double* smem, const DWin& wn, double* out) {
+    constexpr int PV = PE * PE * PE;
+    if (threadIdx.x >= PE * PE) return;
+    const int k = threadIdx.x, n1 = k / PE, n2 = k - n1 * PE;
+    const double r12 = wn.R[n1] * wn.R[n2];
+#pragma unroll
+    for (int n0 = 0; n0 < PE; ++n0) {
+        const int e = n0 * PE * PE + k;
+        double s = smem[e];
+#pragma unroll
+        for (int q = 1; q < W; ++q) s += smem[q * PV + e];
+        out[e] = s * (r12 * wn.R[n0]);
+    }
+}
+
+constexpr int kCol3Row = 28;  // staging row of spread3c: w0[8] w1[8] w2p[11] code
 
 // ===========================================================================
 // d = 3, m = 4 (S = 8) on the FP64 tensor cores.
@@ -301,15 +354,133 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     }
     if (cur >= 0) flush(cur);
     __syncthreads();
-    // tile-relative factors (factors_kernel): node (j0, j1, j2) of the patch
-    // carries R[j0] R[j1] R[j2]
-    double* out = patches + it.patch;
-    for (int k = threadIdx.x; k < PV; k += W * 32) {
-        double s = smem[k];
+    spread3_epilogue<W, PE>(smem, wn, patches + it.patch);
+}
+
+// ===========================================================================
+// d = 3, m = 4 spread for sparse cells (few points per cell): one accumulator
+// block per cell COLUMN (l0, l1 fixed, l2 = 0..3; consecutive in the sorted
+// order), so the SMEM flush happens once per column instead of once per cell
+// and 4-point groups rarely need masking. Eleven 8x8 tiles r = c = 0..10;
+// tile rows are b = l1 + g, tile columns a = l0 + n:
+//   A[g][t] = w1_t[g] w2_t[r - l2_t]   (zero outside the point's 8 taps)
+//   B[t][g] = (P v w0)_t[g]
+// The staging row holds w2 pre-shifted into 11 slots (w2p).
+// ===========================================================================
+template <int W>
+__global__ void __launch_bounds__(W * 32)
+spread3c_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
+                   const DWin* __restrict__ wins, const double* __restrict__ v,
+                   double* __restrict__ patches) {
+    constexpr int S = 8, PE = 11, PV = PE * PE * PE, RL = kCol3Row;
+    constexpr int kW2p = 2 * S, kCode = kW2p + PE;  // row: w0[8] w1[8] w2p[11] code
+    extern __shared__ __align__(16) double smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    double* wp = smem + warp * PV;
+    double* stage = smem + ((W * PV + 1) & ~1) + warp * 32 * RL;
+
+    const Item it = items[blockIdx.x];
+    const DPSet ps = psets[it.ps];
+    const DWin& wn = wins[ps.win];
+    for (int k = lane; k < PV; k += 32) wp[k] = 0.0;
+    int wb, we;
+    warp_range(it, warp, W, &wb, &we);
+
+    double acc[PE][2];
 #pragma unroll
-        for (int q = 1; q < W; ++q) s += smem[q * PV + k];
-        out[k] = s * (wn.R[k / (PE * PE)] * wn.R[(k / PE) % PE] * wn.R[k % PE]);
+    for (int r = 0; r < PE; ++r) acc[r][0] = acc[r][1] = 0.0;
+    int cur = -1;
+    auto col_of = [&](int p) { return *reinterpret_cast<const int*>(stage + p * RL + kCode) >> 2; };
+    auto flush = [&](int col) {  // col = l0 * 4 + l1
+        double* dst = wp + ((col >> 2) + 2 * t) * PE * PE + ((col & 3) + g) * PE;
+#pragma unroll
+        for (int r = 0; r < PE; ++r) {
+            dst[r] += acc[r][0];
+            dst[PE * PE + r] += acc[r][1];
+            acc[r][0] = acc[r][1] = 0.0;
+        }
+    };
+    auto group = [&](const double* st, bool valid) {
+        const double bq = valid ? st[g] : 0.0;
+        const double w1g = st[S + g];
+        const double2 c01 = ld2(st + kW2p), c23 = ld2(st + kW2p + 2), c45 = ld2(st + kW2p + 4),
+                      c67 = ld2(st + kW2p + 6), c89 = ld2(st + kW2p + 8);
+        const double c10 = st[kW2p + 10];
+        dmma(acc[0][0], acc[0][1], c01.x * w1g, bq);
+        dmma(acc[1][0], acc[1][1], c01.y * w1g, bq);
+        dmma(acc[2][0], acc[2][1], c23.x * w1g, bq);
+        dmma(acc[3][0], acc[3][1], c23.y * w1g, bq);
+        dmma(acc[4][0], acc[4][1], c45.x * w1g, bq);
+        dmma(acc[5][0], acc[5][1], c45.y * w1g, bq);
+        dmma(acc[6][0], acc[6][1], c67.x * w1g, bq);
+        dmma(acc[7][0], acc[7][1], c67.y * w1g, bq);
+        dmma(acc[8][0], acc[8][1], c89.x * w1g, bq);
+        dmma(acc[9][0], acc[9][1], c89.y * w1g, bq);
+        dmma(acc[10][0], acc[10][1], c10 * w1g, bq);
+    };
+
+    Pref<3> pa, pb;
+    double va = 0.0;
+    {
+        const int i0 = wb + lane, i1 = wb + 32 + lane;
+        if (i0 < we) {
+            pa.load(ps, i0);
+            va = __ldg(v + pa.perm);
+        }
+        if (i1 < we) pb.load(ps, i1);
     }
+    __syncwarp();
+    for (int base = wb; base < we; base += 32) {
+        const int cnt = min(32, we - base);
+        if (lane < cnt) {
+            double* st = stage + lane * RL;
+            double q0 = pa.P * va, q1 = 1.0;
+#pragma unroll
+            for (int o = 0; o < S; ++o) {
+                st[o] = q0;
+                st[S + o] = q1;
+                q0 *= pa.Q[0];
+                q1 *= pa.Q[1];
+            }
+            const int l2 = pa.code & 3;
+            double q2 = 1.0;
+#pragma unroll
+            for (int r = 0; r < PE; ++r) {
+                const bool in = r >= l2 && r < l2 + S;
+                st[kW2p + r] = in ? q2 : 0.0;
+                if (in) q2 *= pa.Q[2];
+            }
+            *reinterpret_cast<int*>(st + kCode) = pa.code;
+        }
+        pa = pb;
+        if (base + 32 + lane < we) va = __ldg(v + pa.perm);
+        if (base + 64 + lane < we) pb.load(ps, base + 64 + lane);
+        __syncwarp();
+        int p = 0;
+        while (p < cnt) {
+            const int cp = col_of(p);
+            if (cp != cur) {
+                if (cur >= 0) flush(cur);
+                cur = cp;
+            }
+            if (p + 7 < cnt && col_of(p + 7) == cur) {
+                group(stage + (p + t) * RL, true);  // 8 points of one column: two unmasked rounds
+                group(stage + (p + 4 + t) * RL, true);
+                p += 8;
+                continue;
+            }
+            const int q = p + t;
+            const bool valid = q < cnt && col_of(q) == cur;
+            const int nvalid = __popc(__ballot_sync(0xffffffffu, valid) & 0xFu);
+            group(stage + (valid ? q : p) * RL, valid);
+            p += nvalid;
+        }
+        __syncwarp();
+    }
+    if (cur >= 0) flush(cur);
+    __syncthreads();
+    spread3_epilogue<W, PE>(smem, wn, patches + it.patch);
 }
 
 // ===========================================================================
@@ -338,7 +509,10 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     const DWin& wn = wins[ps.win];
     int tc[3];
     tile_coords(it.tile, D, wn.ntile, tc);
-    load_halo<D, PE, TC, true>(halo, wn, tc, TC, PE, PV);
+    __shared__ double sR[PE];
+    if (threadIdx.x < PE) sR[threadIdx.x] = wn.R[threadIdx.x];
+    __syncthreads();
+    load_halo3_r<PE, TC>(halo, wn, tc, sR);
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
     Pref<D> pa, pb;  // factors of the current and the next batch
@@ -1231,9 +1405,11 @@ __global__ void factors_kernel(const double* __restrict__ x0, const double* __re
 // ---- launchers ------------------------------------------------------------
 
 constexpr int kW3 = 4;  // warps per CTA of the d=3, m=4 kernels
+static_assert(kW3 * 32 >= 11 * 11, "load_halo3_r / spread3 epilogue: one thread per (n1, n2) column");
 constexpr int kW2 = 4;
 constexpr int kW1 = 8;
 
+static_assert(kCol3Row == Row<3, 8>::kLen, "spread3c shares spread3's SMEM layout");
 size_t spread3_smem() { return sizeof(double) * (((kW3 * 1331 + 1) & ~1) + kW3 * 32 * Row<3, 8>::kLen); }
 size_t gather3_smem() { return sizeof(double) * (1332 + kW3 * 32 * Row<3, 8>::kLen); }
 size_t spread2_smem() { return sizeof(double) * (((kW2 * 225 + 1) & ~1) + kW2 * 32 * Row<2, 8>::kLen); }
@@ -1267,6 +1443,7 @@ cudaError_t init_kernel_attributes() {
             e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
     };
     set(reinterpret_cast<const void*>(spread3_s8_kernel<kW3>), spread3_smem());
+    set(reinterpret_cast<const void*>(spread3c_s8_kernel<kW3>), spread3_smem());
     set(reinterpret_cast<const void*>(gather3_s8_kernel<kW3>), gather3_smem());
     set(reinterpret_cast<const void*>(spread2_s8_kernel<kW2>), spread2_smem());
     set(reinterpret_cast<const void*>(gather2_s8_kernel<kW2>), gather2_smem());
@@ -1284,10 +1461,12 @@ cudaError_t init_kernel_attributes() {
 // Launch spread over `nitems` items whose windows all have dimension D and
 // span S (specialised kernels for S = 8, i.e. m = 4).
 void launch_spread(int D, int S, int PE, const Item* items, int nitems, const DPSet* ps,
-                   const DWin* wins, const double* v, double* patches, cudaStream_t st) {
+                   const DWin* wins, const double* v, double* patches, bool columns, cudaStream_t st) {
     if (nitems == 0) return;
     if (S == 8) {
-        if (D == 3)
+        if (D == 3 && columns)
+            spread3c_s8_kernel<kW3><<<nitems, kW3 * 32, spread3_smem(), st>>>(items, ps, wins, v, patches);
+        else if (D == 3)
             spread3_s8_kernel<kW3><<<nitems, kW3 * 32, spread3_smem(), st>>>(items, ps, wins, v, patches);
         else if (D == 2)
             spread2_s8_kernel<kW2><<<nitems, kW2 * 32, spread2_smem(), st>>>(items, ps, wins, v, patches);

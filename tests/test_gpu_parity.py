@@ -115,3 +115,16 @@ def test_kernel_rows_and_diag():
     d2 = ((x[rows][:, None, [3, 4, 5]] - x[None, :, [3, 4, 5]]) ** 2).sum(-1)
     assert np.abs(R1 - np.exp(-d2)).max() <= 1e-14
     assert np.all(op.kernel_diag(0) == 1.0)
+
+
+@pytest.mark.parametrize("variant", ["cell", "column"])
+@pytest.mark.parametrize("n,seed", [(3000, 91), (60000, 92)])
+def test_spread3_variants_match_oracle(oracle_lib, monkeypatch, variant, n, seed):
+    # both d = 3 spread kernels (per-cell and column-accumulating; the engine
+    # picks one by the mean points per cell) at sparse and dense cell counts
+    monkeypatch.setenv("KSVM_NFFT_SPREAD3", variant)
+    pts = oracle.random_points(n, 3, seed)
+    v = oracle.random_vector(n, seed + 1)
+    g = anova_fast_operator(Dataset(pts), spec_of([[0, 1, 2]]))
+    o = oracle_lib.anova(pts, [[0, 1, 2]])
+    assert rel(g.apply(v), o.apply(v)) <= TOL
