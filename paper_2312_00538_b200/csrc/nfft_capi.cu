@@ -396,7 +396,7 @@ std::vector<double> scale_cm(const Window& w, const double* pts, int64_t t, int6
 // ---------------------------------------------------------------------------
 // The engine: every owned window's plan plus the per-apply scratch.
 // ---------------------------------------------------------------------------
-constexpr long long kColumnSpreadDensity = 10;  // points per cell below which spread3c runs
+constexpr long long kColumnDensity = 10;  // points per cell below which spread3c runs
 
 struct Engine {
     int device = 0;
@@ -569,11 +569,13 @@ struct Engine {
         dw.tabS = w.tabS.p;
     }
 
-    // Sparse cells favour the column-accumulating d = 3 spread (fewer SMEM
-    // flushes); dense cells the per-cell one (fewer FP64 operations per
-    // point). Threshold: mean points per cell of the occupied tiles.
-    bool use_column_spread(int D) const {
-        if (const char* e = std::getenv("KSVM_NFFT_SPREAD3")) return std::strcmp(e, "column") == 0;
+    // Sparse cells favour the column-accumulating d = 3 spread (one SMEM
+    // flush per cell column, fuller point groups); dense cells the per-cell
+    // kernel (fewer FP64 operations per point). A column-blocked gather was
+    // measured slower (gather items are ~128 points, ~1 column per warp).
+    // Threshold: mean points per cell of the occupied tiles.
+    bool use_columns(int D, const char* env) const {
+        if (const char* e = std::getenv(env)) return std::strcmp(e, "column") == 0;
         long long pts = 0, cells = 0;
         for (size_t s = 0; s < owned.size(); ++s) {
             const Window& w = *wins[static_cast<size_t>(owned[s])];
@@ -584,7 +586,7 @@ struct Engine {
             pts += n;
             cells += occ * w.dw.TC * w.dw.TC * w.dw.TC;
         }
-        return cells > 0 && pts < kColumnSpreadDensity * cells;
+        return cells > 0 && pts < kColumnDensity * cells;
     }
 
     // Assign global item numbers / patch offsets and upload device tables.
@@ -627,7 +629,7 @@ struct Engine {
                 }
             }
             class_end[D] = static_cast<int>(all.size());
-            spread_columns[D] = D == 3 && use_column_spread(D);
+            spread_columns[D] = D == 3 && use_columns(D, "KSVM_NFFT_SPREAD3");
             gclass_begin[D] = static_cast<int>(gall.size());
             for (int s = 0; s < P; ++s) {
                 Window& w = *wins[static_cast<size_t>(owned[static_cast<size_t>(s)])];

@@ -117,14 +117,18 @@ def test_kernel_rows_and_diag():
     assert np.all(op.kernel_diag(0) == 1.0)
 
 
-@pytest.mark.parametrize("variant", ["cell", "column"])
+@pytest.mark.parametrize("spread", ["cell", "column"])
 @pytest.mark.parametrize("n,seed", [(3000, 91), (60000, 92)])
-def test_spread3_variants_match_oracle(oracle_lib, monkeypatch, variant, n, seed):
+def test_d3_spread_variants_match_oracle(oracle_lib, monkeypatch, spread, n, seed):
     # both d = 3 spread kernels (per-cell and column-accumulating; the engine
-    # picks one by the mean points per cell) at sparse and dense cell counts
-    monkeypatch.setenv("KSVM_NFFT_SPREAD3", variant)
+    # picks by the mean points per cell) at sparse and dense cells, for the
+    # operator and for a cross apply
+    monkeypatch.setenv("KSVM_NFFT_SPREAD3", spread)
     pts = oracle.random_points(n, 3, seed)
     v = oracle.random_vector(n, seed + 1)
     g = anova_fast_operator(Dataset(pts), spec_of([[0, 1, 2]]))
     o = oracle_lib.anova(pts, [[0, 1, 2]])
     assert rel(g.apply(v), o.apply(v)) <= TOL
+    p, q = plan_fastsum(pts, GaussianKernelSpec(1.0)), oracle_lib.plan(pts)
+    tg = pts[: n // 3] * 0.9
+    assert rel(apply_fastsum_cross(p, tg, v), q.apply_cross(tg, v)) <= TOL
