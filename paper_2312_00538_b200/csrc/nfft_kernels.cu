@@ -18,12 +18,22 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "nfft_engine.cuh"
 
 namespace ksvm_nfft {
 
 namespace {
+
+// Programmatic dependent launch (apply-path kernels, launch_k): every kernel
+// lets its stream successor start at once (pdl_trigger), does its plan-only
+// prologue (items, DWin, tile tables: immutable during an apply), and waits
+// for its predecessor's results (pdl_wait) before touching any buffer an
+// earlier kernel writes or reads. Every CTA waits before it exits, so grid
+// completion stays transitive along the stream.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ int pmod(int a, int M) {
     int r = a % M;
@@ -265,12 +275,14 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     double* wp = smem + warp * PV;
     double* stage = smem + ((W * PV + 1) & ~1) + warp * 32 * RL;
 
+    pdl_trigger();
     const Item it = items[blockIdx.x];
     const DPSet ps = psets[it.ps];
     const DWin& wn = wins[ps.win];
     for (int k = lane; k < PV; k += 32) wp[k] = 0.0;
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
+    pdl_wait();
 
     double acc[8][2];
 #pragma unroll
@@ -380,12 +392,14 @@ spread3c_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pse
     double* wp = smem + warp * PV;
     double* stage = smem + ((W * PV + 1) & ~1) + warp * 32 * RL;
 
+    pdl_trigger();
     const Item it = items[blockIdx.x];
     const DPSet ps = psets[it.ps];
     const DWin& wn = wins[ps.win];
     for (int k = lane; k < PV; k += 32) wp[k] = 0.0;
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
+    pdl_wait();
 
     double acc[PE][2];
 #pragma unroll
@@ -504,6 +518,7 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     double* halo = smem;
     double* stage = smem + ((PV + 1) & ~1) + warp * 32 * RL;
 
+    pdl_trigger();
     const Item it = items[blockIdx.x];
     const DPSet ps = psets[it.ps];
     const DWin& wn = wins[ps.win];
@@ -512,6 +527,7 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     __shared__ double sR[PE];
     if (threadIdx.x < PE) sR[threadIdx.x] = wn.R[threadIdx.x];
     __syncthreads();
+    pdl_wait();
     load_halo3_r<PE, TC>(halo, wn, tc, sR);
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
@@ -585,6 +601,7 @@ spread2_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double* wp = smem + warp * PV;
     double* stage = smem + ((W * PV + 1) & ~1) + warp * 32 * RL;
+    pdl_trigger();
     const Item it = items[blockIdx.x];
     const DPSet ps = psets[it.ps];
     const DWin& wn = wins[ps.win];
@@ -594,6 +611,7 @@ spread2_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     for (int k = lane; k < PV; k += 32) wp[k] = 0.0;
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
+    pdl_wait();
     const int a = lane >> 2, b0 = (lane & 3) << 1;
     double acc0 = 0.0, acc1 = 0.0;
     int cur = -1;
@@ -656,6 +674,7 @@ gather2_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double* halo = smem;
     double* stage = smem + ((PV + 1) & ~1) + warp * 32 * RL;
+    pdl_trigger();
     const Item it = items[blockIdx.x];
     const DPSet ps = psets[it.ps];
     const DWin& wn = wins[ps.win];
@@ -664,6 +683,7 @@ gather2_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     for (int o = 0; o < S; ++o) R[o] = wn.R[o];
     int tc[3];
     tile_coords(it.tile, D, wn.ntile, tc);
+    pdl_wait();
     load_halo<D, PE, TC>(halo, wn, tc, TC, PE, PV);
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
@@ -719,6 +739,7 @@ spread1_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double* lp = smem + warp * PE * 32;
+    pdl_trigger();
     const Item it = items[blockIdx.x];
     const DPSet ps = psets[it.ps];
     const DWin& wn = wins[ps.win];
@@ -729,6 +750,7 @@ spread1_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     __syncwarp();
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
+    pdl_wait();
     for (int i = wb + lane; i < we; i += 32) {
         const double2 f = __ldg(reinterpret_cast<const double2*>(ps.F + i));
         const int2 cp = __ldg(ps.CP + i);
@@ -758,6 +780,7 @@ gather1_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     constexpr int D = 1, S = 8, TC = 32, PE = TC + S - 1;
     extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    pdl_trigger();
     const Item it = items[blockIdx.x];
     const DPSet ps = psets[it.ps];
     const DWin& wn = wins[ps.win];
@@ -766,6 +789,7 @@ gather1_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     for (int o = 0; o < S; ++o) R[o] = wn.R[o];
     int tc[3];
     tile_coords(it.tile, D, wn.ntile, tc);
+    pdl_wait();
     load_halo<D, PE, TC>(smem, wn, tc, TC, PE, PE);
     __syncthreads();
     int wb, we;
@@ -800,6 +824,7 @@ __global__ void spread_generic_kernel(const Item* __restrict__ items,
                                       double* __restrict__ patches, int W) {
     extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    pdl_trigger();
     const Item it = items[blockIdx.x];
     const DPSet ps = psets[it.ps];
     const DWin& wn = wins[ps.win];
@@ -814,6 +839,7 @@ __global__ void spread_generic_kernel(const Item* __restrict__ items,
     for (int k = lane; k < PV; k += 32) wp[k] = 0.0;
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
+    pdl_wait();
     __syncwarp();
     for (int base = wb; base < we; base += 32) {
         const int cnt = min(32, we - base);
@@ -873,6 +899,7 @@ __global__ void gather_generic_kernel(const Item* __restrict__ items,
                                       const DWin* __restrict__ wins, int W) {
     extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    pdl_trigger();
     const Item it = items[blockIdx.x];
     const DPSet ps = psets[it.ps];
     const DWin& wn = wins[ps.win];
@@ -886,6 +913,7 @@ __global__ void gather_generic_kernel(const Item* __restrict__ items,
     double* stage = smem + ((PV + 1) & ~1) + warp * 32 * kRowG;
     int tc[3] = {0, 0, 0};
     tile_coords(it.tile, D, wn.ntile, tc);
+    pdl_wait();
     load_halo<D>(halo, wn, tc, TC, PE, PV);
     __syncthreads();
     int wb, we;
@@ -947,6 +975,7 @@ __global__ void gather_generic_kernel(const Item* __restrict__ items,
 // ===========================================================================
 __global__ void tile_reduce_kernel(const DWin* __restrict__ wins, const int2* __restrict__ multi,
                                    double* __restrict__ patches) {
+    pdl_trigger();
     const int2 wt = multi[blockIdx.y];
     const DWin& wn = wins[wt.x];
     int PV = 1;
@@ -954,6 +983,7 @@ __global__ void tile_reduce_kernel(const DWin* __restrict__ wins, const int2* __
     const int k0 = wn.tile_first[wt.y], k1 = wn.tile_first[wt.y + 1];
     double* base = patches + wn.patch_base + static_cast<long long>(k0 - wn.item_base) * PV;
     const int nk = k1 - k0;
+    pdl_wait();
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < PV; e += gridDim.x * blockDim.x) {
         // eight interleaved partial sums (8 loads in flight), combined in a fixed order
         double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -974,7 +1004,9 @@ __global__ void tile_reduce_kernel(const DWin* __restrict__ wins, const int2* __
 template <int D, int NC>
 __global__ void reduce_patches_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots,
                                       const double* __restrict__ patches) {
+    pdl_trigger();
     const DWin& wn = wins[slots[blockIdx.y]];
+    pdl_wait();
     if (wn.d != D || !wn.wrap) return;  // non-wrapping grids use reduce_owner_kernel
     const int Lg = wn.Lg, TC = wn.TC, PE = wn.PE, nt = wn.ntile;
     int nodes = 1;
@@ -1084,7 +1116,8 @@ constexpr int kConvMaxL = 128;  // Lg bound (M = sigma N <= 128)
 // ===========================================================================
 namespace {
 
-// Owner-tile block reduction of one tile (whole CTA). soff/sT: SMEM scratch.
+// Owner-tile block reduction of one tile (whole CTA; one unit per CTA).
+// soff/sT: SMEM scratch.
 template <int D, int NC>
 __device__ void reduce_owner_unit(const DWin& wn, int tileT, const double* __restrict__ patches,
                                   long long* soff, int (*sT)[3], int* any) {
@@ -1129,6 +1162,7 @@ __device__ void reduce_owner_unit(const DWin& wn, int tileT, const double* __res
         nodes *= len[t];
     }
     const bool have = *any != 0;
+    pdl_wait();  // patches come from the spread / tile_reduce kernels
     for (int k = threadIdx.x; k < nodes; k += blockDim.x) {
         int r = k, e[3] = {0, 0, 0};
 #pragma unroll
@@ -1173,7 +1207,6 @@ __device__ void reduce_owner_unit(const DWin& wn, int tileT, const double* __res
         for (int t = 0; t < D; ++t) gi = gi * Lg + e[t];
         wn.G[gi] = sum;
     }
-    __syncthreads();  // scratch reuse by the next unit
 }
 
 // One 8x8 output tile of a separable-convolution stage (one warp).
@@ -1203,6 +1236,7 @@ __device__ void conv_tile_unit(const DWin& wn, int stage, int tile) {
     const double* __restrict__ tA = wn.tabA;
     const double* __restrict__ tS = wn.tabS;
     const int KS = (Lg + 3) >> 2;
+    pdl_wait();  // G / T come from the reduce / previous stage
     double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
     double e00 = 0.0, e01 = 0.0, e10 = 0.0, e11 = 0.0;
 #pragma unroll 4
@@ -1274,12 +1308,15 @@ template <int D, int NC>
 __global__ void __launch_bounds__(128)
 reduce_owner_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots,
                     const double* __restrict__ patches) {
+    pdl_trigger();
     const DWin& wn = wins[slots[blockIdx.y]];
-    if (wn.d != D || wn.wrap) return;
     const int nown = (wn.Lg + wn.TC - 1) / wn.TC;
     int ntd = 1;
     for (int t = 0; t < D; ++t) ntd *= nown;
-    if (static_cast<int>(blockIdx.x) >= ntd) return;
+    if (wn.d != D || wn.wrap || static_cast<int>(blockIdx.x) >= ntd) {
+        pdl_wait();
+        return;
+    }
     constexpr int NS = D == 1 ? NC : (D == 2 ? NC * NC : NC * NC * NC);
     __shared__ long long soff[NS];
     __shared__ int sT[NS][3];
@@ -1289,10 +1326,13 @@ reduce_owner_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots
 
 __global__ void __launch_bounds__(128)
 conv_stage_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots, int stage) {
+    pdl_trigger();
     const DWin& wn = wins[slots[blockIdx.y]];
-    if (stage >= wn.d) return;
     const int tile = blockIdx.x * 4 + (threadIdx.x >> 5);
-    if (tile >= conv_tiles(wn)) return;
+    if (stage >= wn.d || tile >= conv_tiles(wn)) {
+        pdl_wait();
+        return;
+    }
     conv_tile_unit(wn, stage, tile);
 }
 
@@ -1300,6 +1340,8 @@ conv_stage_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots, 
 // (P:src/fastsum.cpp:346-351: out = 0; out += eta_l * apply_l).
 __global__ void combine_kernel(double* __restrict__ y, const double* __restrict__ parts,
                                const double* __restrict__ eta, int P, long long n) {
+    pdl_trigger();
+    pdl_wait();
     for (long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
          j += static_cast<long long>(gridDim.x) * blockDim.x) {
         double acc = 0.0;
@@ -1335,6 +1377,8 @@ __global__ void kernel_rows_kernel(double* __restrict__ out, const long long* __
 }
 
 __global__ void fill_kernel(double* __restrict__ out, double val, long long n) {
+    pdl_trigger();
+    pdl_wait();
     for (long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
          j += static_cast<long long>(gridDim.x) * blockDim.x)
         out[j] = val;
@@ -1404,6 +1448,31 @@ __global__ void factors_kernel(const double* __restrict__ x0, const double* __re
 
 // ---- launchers ------------------------------------------------------------
 
+// Apply-path launches carry the programmatic-stream-serialization attribute
+// (PDL, see pdl_trigger/pdl_wait); KSVM_NFFT_PDL=0 turns it off.
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("KSVM_NFFT_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    (void)cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);  // errors: cudaGetLastError
+}
+
 constexpr int kW3 = 4;  // warps per CTA of the d=3, m=4 kernels
 static_assert(kW3 * 32 >= 11 * 11, "load_halo3_r / spread3 epilogue: one thread per (n1, n2) column");
 constexpr int kW2 = 4;
@@ -1465,36 +1534,36 @@ void launch_spread(int D, int S, int PE, const Item* items, int nitems, const DP
     if (nitems == 0) return;
     if (S == 8) {
         if (D == 3 && columns)
-            spread3c_s8_kernel<kW3><<<nitems, kW3 * 32, spread3_smem(), st>>>(items, ps, wins, v, patches);
+            launch_k(spread3c_s8_kernel<kW3>, dim3(nitems), dim3(kW3 * 32), spread3_smem(), st, items, ps, wins, v, patches);
         else if (D == 3)
-            spread3_s8_kernel<kW3><<<nitems, kW3 * 32, spread3_smem(), st>>>(items, ps, wins, v, patches);
+            launch_k(spread3_s8_kernel<kW3>, dim3(nitems), dim3(kW3 * 32), spread3_smem(), st, items, ps, wins, v, patches);
         else if (D == 2)
-            spread2_s8_kernel<kW2><<<nitems, kW2 * 32, spread2_smem(), st>>>(items, ps, wins, v, patches);
+            launch_k(spread2_s8_kernel<kW2>, dim3(nitems), dim3(kW2 * 32), spread2_smem(), st, items, ps, wins, v, patches);
         else
-            spread1_s8_kernel<kW1><<<nitems, kW1 * 32, spread1_smem(), st>>>(items, ps, wins, v, patches);
+            launch_k(spread1_s8_kernel<kW1>, dim3(nitems), dim3(kW1 * 32), spread1_smem(), st, items, ps, wins, v, patches);
         return;
     }
     const int W = generic_warps(D, PE, true);
     const size_t sm = generic_smem(D, PE, W, true);
-    if (D == 1) spread_generic_kernel<1><<<nitems, W * 32, sm, st>>>(items, ps, wins, v, patches, W);
-    else if (D == 2) spread_generic_kernel<2><<<nitems, W * 32, sm, st>>>(items, ps, wins, v, patches, W);
-    else spread_generic_kernel<3><<<nitems, W * 32, sm, st>>>(items, ps, wins, v, patches, W);
+    if (D == 1) launch_k(spread_generic_kernel<1>, dim3(nitems), dim3(W * 32), sm, st, items, ps, wins, v, patches, W);
+    else if (D == 2) launch_k(spread_generic_kernel<2>, dim3(nitems), dim3(W * 32), sm, st, items, ps, wins, v, patches, W);
+    else launch_k(spread_generic_kernel<3>, dim3(nitems), dim3(W * 32), sm, st, items, ps, wins, v, patches, W);
 }
 
 void launch_gather(int D, int S, int PE, const Item* items, int nitems, const DPSet* ps,
                    const DWin* wins, cudaStream_t st) {
     if (nitems == 0) return;
     if (S == 8) {
-        if (D == 3) gather3_s8_kernel<kW3><<<nitems, kW3 * 32, gather3_smem(), st>>>(items, ps, wins);
-        else if (D == 2) gather2_s8_kernel<kW2><<<nitems, kW2 * 32, gather2_smem(), st>>>(items, ps, wins);
-        else gather1_s8_kernel<kW1><<<nitems, kW1 * 32, gather1_smem(), st>>>(items, ps, wins);
+        if (D == 3) launch_k(gather3_s8_kernel<kW3>, dim3(nitems), dim3(kW3 * 32), gather3_smem(), st, items, ps, wins);
+        else if (D == 2) launch_k(gather2_s8_kernel<kW2>, dim3(nitems), dim3(kW2 * 32), gather2_smem(), st, items, ps, wins);
+        else launch_k(gather1_s8_kernel<kW1>, dim3(nitems), dim3(kW1 * 32), gather1_smem(), st, items, ps, wins);
         return;
     }
     const int W = generic_warps(D, PE, false);
     const size_t sm = generic_smem(D, PE, W, false);
-    if (D == 1) gather_generic_kernel<1><<<nitems, W * 32, sm, st>>>(items, ps, wins, W);
-    else if (D == 2) gather_generic_kernel<2><<<nitems, W * 32, sm, st>>>(items, ps, wins, W);
-    else gather_generic_kernel<3><<<nitems, W * 32, sm, st>>>(items, ps, wins, W);
+    if (D == 1) launch_k(gather_generic_kernel<1>, dim3(nitems), dim3(W * 32), sm, st, items, ps, wins, W);
+    else if (D == 2) launch_k(gather_generic_kernel<2>, dim3(nitems), dim3(W * 32), sm, st, items, ps, wins, W);
+    else launch_k(gather_generic_kernel<3>, dim3(nitems), dim3(W * 32), sm, st, items, ps, wins, W);
 }
 
 void launch_tile_reduce(const DWin* wins, const int2* multi, int nmulti, int max_pv, double* patches,
@@ -1502,7 +1571,7 @@ void launch_tile_reduce(const DWin* wins, const int2* multi, int nmulti, int max
     if (nmulti == 0) return;
     // narrow blocks: one heavy tile's patches are read by ~max_pv/64 SMs
     dim3 grid(static_cast<unsigned>((max_pv + 63) / 64), static_cast<unsigned>(nmulti));
-    tile_reduce_kernel<<<grid, 64, 0, st>>>(wins, multi, patches);
+    launch_k(tile_reduce_kernel, dim3(grid), dim3(64), 0, st, wins, multi, patches);
 }
 
 void launch_reduce(const DWin* wins, const int* slots, int nslots, long long max_nodes, int D, int S,
@@ -1512,21 +1581,21 @@ void launch_reduce(const DWin* wins, const int* slots, int nslots, long long max
         // owner-tile blocks; NC = ceil(PE / TC) source tiles per dimension
         dim3 grid(static_cast<unsigned>(max_tiles), nslots);
         if (S == 8) {
-            if (D == 1) reduce_owner_kernel<1, 2><<<grid, 128, 0, st>>>(wins, slots, patches);
-            else if (D == 2) reduce_owner_kernel<2, 2><<<grid, 128, 0, st>>>(wins, slots, patches);
-            else reduce_owner_kernel<3, 3><<<grid, 128, 0, st>>>(wins, slots, patches);
+            if (D == 1) launch_k(reduce_owner_kernel<1, 2>, dim3(grid), dim3(64), 0, st, wins, slots, patches);
+            else if (D == 2) launch_k(reduce_owner_kernel<2, 2>, dim3(grid), dim3(64), 0, st, wins, slots, patches);
+            else launch_k(reduce_owner_kernel<3, 3>, dim3(grid), dim3(64), 0, st, wins, slots, patches);
         } else {
-            if (D == 1) reduce_owner_kernel<1, 5><<<grid, 128, 0, st>>>(wins, slots, patches);
-            else if (D == 2) reduce_owner_kernel<2, 5><<<grid, 128, 0, st>>>(wins, slots, patches);
-            else reduce_owner_kernel<3, 5><<<grid, 128, 0, st>>>(wins, slots, patches);
+            if (D == 1) launch_k(reduce_owner_kernel<1, 5>, dim3(grid), dim3(64), 0, st, wins, slots, patches);
+            else if (D == 2) launch_k(reduce_owner_kernel<2, 5>, dim3(grid), dim3(64), 0, st, wins, slots, patches);
+            else launch_k(reduce_owner_kernel<3, 5>, dim3(grid), dim3(128), 0, st, wins, slots, patches);
         }
         return;
     }
     dim3 grid(static_cast<unsigned>((max_nodes + 255) / 256), nslots);
-    if (D == 1) reduce_patches_kernel<1, 5><<<grid, 256, 0, st>>>(wins, slots, patches);
-    else if (D == 2) reduce_patches_kernel<2, 5><<<grid, 256, 0, st>>>(wins, slots, patches);
-    else if (S == 8) reduce_patches_kernel<3, 3><<<grid, 256, 0, st>>>(wins, slots, patches);
-    else reduce_patches_kernel<3, 5><<<grid, 256, 0, st>>>(wins, slots, patches);
+    if (D == 1) launch_k(reduce_patches_kernel<1, 5>, dim3(grid), dim3(256), 0, st, wins, slots, patches);
+    else if (D == 2) launch_k(reduce_patches_kernel<2, 5>, dim3(grid), dim3(256), 0, st, wins, slots, patches);
+    else if (S == 8) launch_k(reduce_patches_kernel<3, 3>, dim3(grid), dim3(256), 0, st, wins, slots, patches);
+    else launch_k(reduce_patches_kernel<3, 5>, dim3(grid), dim3(256), 0, st, wins, slots, patches);
 }
 
 void launch_conv(const DWin* wins, const int* slots, int nslots, int Lg_max, long long max_fibres,
@@ -1534,7 +1603,7 @@ void launch_conv(const DWin* wins, const int* slots, int nslots, int Lg_max, lon
     if (nslots == 0) return;
     const long long tiles = static_cast<long long>((Lg_max + 7) / 8) * ((max_fibres + 7) / 8);
     dim3 grid(static_cast<unsigned>((tiles + 3) / 4), nslots);
-    conv_stage_kernel<<<grid, 128, 0, st>>>(wins, slots, stage);
+    launch_k(conv_stage_kernel, dim3(grid), dim3(128), 0, st, wins, slots, stage);
 }
 
 int conv_max_lg() { return kConvMaxL; }
@@ -1542,7 +1611,7 @@ int conv_max_lg() { return kConvMaxL; }
 void launch_combine(double* y, const double* parts, const double* eta, int P, long long n,
                     cudaStream_t st) {
     const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 16));
-    combine_kernel<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(y, parts, eta, P, n);
+    launch_k(combine_kernel, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, st, y, parts, eta, P, n);
 }
 
 void launch_kernel_rows(double* out, const long long* rows, int r, const double* const* cols,
@@ -1554,7 +1623,7 @@ void launch_kernel_rows(double* out, const long long* rows, int r, const double*
 
 void launch_fill(double* out, double val, long long n, cudaStream_t st) {
     const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 16));
-    fill_kernel<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(out, val, n);
+    launch_k(fill_kernel, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, st, out, val, n);
 }
 
 void launch_cell_keys(const double* x0, const double* x1, const double* x2, int d, long long n,
