@@ -28,9 +28,11 @@ namespace ksvm_nfft {
 // launchers (nfft_kernels.cu)
 cudaError_t init_kernel_attributes();
 void launch_spread(int D, int S, int PE, const Item* items, int nitems, const DPSet* ps,
-                   const DWin* wins, const double* v, double* patches, bool columns, cudaStream_t st);
+                   const DWin* wins, const double* v, double* patches, const int* colb, cudaStream_t st);
 void launch_gather(int D, int S, int PE, const Item* items, int nitems, const DPSet* ps,
                    const DWin* wins, cudaStream_t st);
+void launch_gather3c(const Item* items, int nitems, const DPSet* ps, const DWin* wins, const int* colb,
+                     cudaStream_t st);
 void launch_reduce(const DWin* wins, const int* slots, int nslots, long long max_nodes, int D, int S,
                    const double* patches, bool wrap, int max_tiles, cudaStream_t st);
 void launch_tile_reduce(const DWin* wins, const int2* multi, int nmulti, int max_pv, double* patches,
@@ -205,6 +207,10 @@ struct PointSet {
     std::vector<Item> items;      // spread items (one patch each; global numbering later)
     std::vector<int> tile_first;  // local item index of each tile's first spread item
     std::vector<Item> gitems;     // gather items (finer: no patch cost, better balance)
+    // d = 3, TC = 4: per spread item, the first point of cell columns
+    // 0..16 (column = l0 * 4 + l1; kColBounds entries per item), the warp
+    // ranges of spread3c / gather3c
+    std::vector<int> colb;
 };
 
 struct Window {
@@ -313,6 +319,7 @@ void build_pointset(PointSet& ps, const std::vector<double>& scaled_cm, int64_t 
     // a function of the plan alone).
     ps.items.clear();
     ps.gitems.clear();
+    ps.colb.clear();
     ps.tile_first.assign(static_cast<size_t>(ntiles) + 1, 0);
     auto split = [](std::vector<Item>& out, int T, int64_t i, int64_t cnt, int64_t chunk) {
         const int64_t pieces = (cnt + chunk - 1) / chunk;
@@ -331,8 +338,19 @@ void build_pointset(PointSet& ps, const std::vector<double>& scaled_cm, int64_t 
         while (j < n && hk[static_cast<size_t>(j)] / tcd == static_cast<unsigned>(T)) ++j;
         const int64_t cnt = j - i;
         if (cnt > 0) {
+            const size_t first = ps.items.size();
             split(ps.items, T, i, cnt, chunk_points);
             split(ps.gitems, T, i, cnt, gather_chunk);
+            if (d == 3 && g.TC == 4) {
+                for (size_t q = first; q < ps.items.size(); ++q) {
+                    const Item& it = ps.items[q];
+                    int p = it.begin;
+                    for (int b = 0; b < kColBounds; ++b) {  // first point of column b
+                        while (p < it.end && static_cast<int>((hk[static_cast<size_t>(p)] % tcd) >> 2) < b) ++p;
+                        ps.colb.push_back(p);
+                    }
+                }
+            }
         }
         i = j;
     }
@@ -421,6 +439,7 @@ struct Engine {
     DevBuf<DWin> d_wins;    // owned windows (slot = position in `owned`)
     DevBuf<DPSet> d_ps;     // sources of owned windows
     DevBuf<Item> d_items;   // spread items of owned windows, grouped by d
+    DevBuf<int> d_colb;     // column bounds of the d = 3 spread items (PointSet::colb)
     DevBuf<Item> d_gitems;  // gather items of owned windows, grouped by d
     int gclass_begin[4] = {0, 0, 0, 0}, gclass_end[4] = {0, 0, 0, 0};
     DevBuf<int> d_slots;    // 0..P_owned-1
@@ -436,6 +455,7 @@ struct Engine {
     int class_begin[4] = {0, 0, 0, 0}, class_end[4] = {0, 0, 0, 0};
     int class_PE[4] = {0, 0, 0, 0};
     bool spread_columns[4] = {false, false, false, false};  // d = 3: column-accumulating spread
+    bool gather_columns[4] = {false, false, false, false};  // d = 3: column-slab gather
     long long max_nodes = 0, max_fibres = 0;
     int max_lg = 0;
     bool has_dim[4] = {false, false, false, false};
@@ -569,10 +589,10 @@ struct Engine {
         dw.tabS = w.tabS.p;
     }
 
-    // Sparse cells favour the column-accumulating d = 3 spread (one SMEM
-    // flush per cell column, fuller point groups); dense cells the per-cell
-    // kernel (fewer FP64 operations per point). A column-blocked gather was
-    // measured slower (gather items are ~128 points, ~1 column per warp).
+    // Sparse cells favour the column kernels for d = 3 (spread: one SMEM
+    // flush per cell column; gather: one fragment load per column; both:
+    // full point groups); dense cells the per-cell kernels (fewer FP64
+    // operations per point).
     // Threshold: mean points per cell of the occupied tiles.
     bool use_columns(int D, const char* env) const {
         if (const char* e = std::getenv(env)) return std::strcmp(e, "column") == 0;
@@ -593,6 +613,7 @@ struct Engine {
     void finalize() {
         const int P = P_owned();
         std::vector<Item> all, gall;
+        std::vector<int> colb;  // kColBounds per item of `all` (zeros unless d = 3, TC = 4)
         std::vector<int2> multi;
         std::vector<DPSet> ps(static_cast<size_t>(P));
         long long patch_total = 0;
@@ -620,16 +641,20 @@ struct Engine {
                         tpo[T] = patch_total + static_cast<long long>(tf[T] - w.dw.item_base) * PV;
                 w.tile_patch.upload(tpo.data(), tpo.size(), stream);
                 w.dw.tile_patch = w.tile_patch.p;
-                for (const Item& it0 : w.src.items) {
-                    Item it = it0;
+                const bool has_colb = w.src.colb.size() == w.src.items.size() * kColBounds;
+                for (size_t q = 0; q < w.src.items.size(); ++q) {
+                    Item it = w.src.items[q];
                     it.ps = s;
                     it.patch = patch_total;
                     patch_total += PV;
                     all.push_back(it);
+                    for (int b = 0; b < kColBounds; ++b)
+                        colb.push_back(has_colb ? w.src.colb[q * kColBounds + b] : 0);
                 }
             }
             class_end[D] = static_cast<int>(all.size());
             spread_columns[D] = D == 3 && use_columns(D, "KSVM_NFFT_SPREAD3");
+            gather_columns[D] = D == 3 && use_columns(D, "KSVM_NFFT_GATHER3");
             gclass_begin[D] = static_cast<int>(gall.size());
             for (int s = 0; s < P; ++s) {
                 Window& w = *wins[static_cast<size_t>(owned[static_cast<size_t>(s)])];
@@ -667,6 +692,7 @@ struct Engine {
         d_wins.upload(dws.data(), dws.size(), stream);
         d_ps.upload(ps.data(), ps.size(), stream);
         d_items.upload(all.data(), all.size(), stream);
+        d_colb.upload(colb.data(), colb.size(), stream);
         d_gitems.upload(gall.data(), gall.size(), stream);
         if (!slots.empty()) d_slots.upload(slots.data(), slots.size(), stream);
         n_multi = static_cast<int>(multi.size());
@@ -699,7 +725,9 @@ struct Engine {
         if (cnt == 0) return;
         tick(kSpread[D]);
         launch_spread(D, 2 * cfg.window_cutoff, class_PE[D], d_items.p + class_begin[D], cnt, d_ps.p,
-                      d_wins.p, v, patches.p, spread_columns[D], st);
+                      d_wins.p, v, patches.p,
+                      spread_columns[D] ? d_colb.p + static_cast<size_t>(class_begin[D]) * kColBounds : nullptr,
+                      st);
         ++g_launches;
         if (n_multi_cls[D]) {
             tick("tile_reduce");
@@ -721,8 +749,13 @@ struct Engine {
         if (gather) {
             const int gcnt = gclass_end[D] - gclass_begin[D];
             tick(kGather[D]);
-            launch_gather(D, 2 * cfg.window_cutoff, class_PE[D], d_gitems.p + gclass_begin[D], gcnt, d_ps.p,
-                          d_wins.p, st);
+            if (gather_columns[D]) {
+                launch_gather3c(d_items.p + class_begin[D], cnt, d_ps.p, d_wins.p,
+                                d_colb.p + static_cast<size_t>(class_begin[D]) * kColBounds, st);
+            } else {
+                launch_gather(D, 2 * cfg.window_cutoff, class_PE[D], d_gitems.p + gclass_begin[D], gcnt, d_ps.p,
+                              d_wins.p, st);
+            }
             ++g_launches;
         }
         CK(cudaGetLastError());

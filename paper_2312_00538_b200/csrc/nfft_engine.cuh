@@ -24,6 +24,12 @@
 namespace ksvm_nfft {
 
 constexpr int kMaxSpan = 16;  // 2m, m <= 8 (P:src/fastsum.cpp:41-42, w[3][16] at :225)
+// d = 3 column kernels (sparse cells): the 16 cell columns (l0, l1) of a
+// 4^3-cell tile; per spread item the first sorted point of columns 0..16.
+// spread3c: 8 warps, two columns each; gather3c: one CTA per l0 slab, one
+// warp per column.
+constexpr int kColWarps = 8;
+constexpr int kColBounds = 17;
 
 // One tile's (or part of a tile's) sorted point range.
 struct Item {

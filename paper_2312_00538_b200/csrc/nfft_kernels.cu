@@ -251,8 +251,6 @@ __device__ __forceinline__ void spread3_epilogue(const double* smem, const DWin&
     }
 }
 
-constexpr int kCol3Row = 28;  // staging row of spread3c: w0[8] w1[8] w2p[11] code
-
 // ===========================================================================
 // d = 3, m = 4 (S = 8) on the FP64 tensor cores.
 // The 8^3 block of one cell is G[(a,b), c] with a, b, c in 0..7. Spread adds
@@ -378,27 +376,34 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
 //   A[g][t] = w1_t[g] w2_t[r - l2_t]   (zero outside the point's 8 taps)
 //   B[t][g] = (P v w0)_t[g]
 // The staging row holds w2 pre-shifted into 11 slots (w2p).
+// Warp w owns the columns 2w, 2w+1 (l0 = w/2, l1 = 2(w%2) + {0,1}; point
+// ranges from the plan's colb table), so its private SMEM sub-patch is only
+// the 8 x 9 x 11 footprint of those columns, and 8 warps per CTA fit twice
+// per SM. The epilogue adds the sub-patches in warp order.
 // ===========================================================================
-template <int W>
-__global__ void __launch_bounds__(W * 32)
+constexpr int kCol3Row = 28;                 // staging row: w0[8] w1[8] w2p[11] code
+constexpr int kCol3Sub = 8 * 9 * 11;         // a x b x c footprint of a warp's two columns
+
+__global__ void __launch_bounds__(kColWarps * 32, 2)
 spread3c_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
                    const DWin* __restrict__ wins, const double* __restrict__ v,
-                   double* __restrict__ patches) {
-    constexpr int S = 8, PE = 11, PV = PE * PE * PE, RL = kCol3Row;
-    constexpr int kW2p = 2 * S, kCode = kW2p + PE;  // row: w0[8] w1[8] w2p[11] code
+                   double* __restrict__ patches, const int* __restrict__ colb) {
+    constexpr int W = kColWarps, S = 8, PE = 11, RL = kCol3Row, SUB = kCol3Sub;
+    constexpr int kW2p = 2 * S, kCode = kW2p + PE;
     extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
-    double* wp = smem + warp * PV;
-    double* stage = smem + ((W * PV + 1) & ~1) + warp * 32 * RL;
+    double* wp = smem + warp * SUB;
+    double* stage = smem + W * SUB + warp * 32 * RL;
+    const int l1w = 2 * (warp & 1);  // b offset of this warp's footprint
 
     pdl_trigger();
     const Item it = items[blockIdx.x];
     const DPSet ps = psets[it.ps];
     const DWin& wn = wins[ps.win];
-    for (int k = lane; k < PV; k += 32) wp[k] = 0.0;
-    int wb, we;
-    warp_range(it, warp, W, &wb, &we);
+    for (int k = lane; k < SUB; k += 32) wp[k] = 0.0;
+    const int wb = __ldg(colb + blockIdx.x * kColBounds + 2 * warp);
+    const int we = __ldg(colb + blockIdx.x * kColBounds + 2 * warp + 2);
     pdl_wait();
 
     double acc[PE][2];
@@ -406,12 +411,12 @@ spread3c_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pse
     for (int r = 0; r < PE; ++r) acc[r][0] = acc[r][1] = 0.0;
     int cur = -1;
     auto col_of = [&](int p) { return *reinterpret_cast<const int*>(stage + p * RL + kCode) >> 2; };
-    auto flush = [&](int col) {  // col = l0 * 4 + l1
-        double* dst = wp + ((col >> 2) + 2 * t) * PE * PE + ((col & 3) + g) * PE;
+    auto flush = [&](int col) {  // col = l0 * 4 + l1, l0 = warp / 2
+        double* dst = wp + (2 * t * 9 + (col & 3) - l1w + g) * PE;
 #pragma unroll
         for (int r = 0; r < PE; ++r) {
             dst[r] += acc[r][0];
-            dst[PE * PE + r] += acc[r][1];
+            dst[9 * PE + r] += acc[r][1];
             acc[r][0] = acc[r][1] = 0.0;
         }
     };
@@ -494,7 +499,24 @@ spread3c_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pse
     }
     if (cur >= 0) flush(cur);
     __syncthreads();
-    spread3_epilogue<W, PE>(smem, wn, patches + it.patch);
+    // node (n0, n1, n2) = sum over warps w (ascending) whose footprint
+    // [w/2, w/2 + 8) x [2(w%2), 2(w%2) + 9) x [0, 11) holds it, times the
+    // tile-relative factor R[n0] R[n1] R[n2]
+    double* out = patches + it.patch;
+    if (threadIdx.x < PE * PE) {
+        const int k = threadIdx.x, n1 = k / PE, n2 = k - n1 * PE;
+        const double r12 = wn.R[n1] * wn.R[n2];
+#pragma unroll
+        for (int n0 = 0; n0 < PE; ++n0) {
+            double s = 0.0;
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                const int a = n0 - (w >> 1), b = n1 - 2 * (w & 1);
+                if (a >= 0 && a < 8 && b >= 0 && b < 9) s += smem[w * SUB + (a * 9 + b) * PE + n2];
+            }
+            out[(n0 * PE + n1) * PE + n2] = s * (r12 * wn.R[n0]);
+        }
+    }
 }
 
 // ===========================================================================
@@ -583,6 +605,128 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
             part += __shfl_xor_sync(0xffffffffu, part, 2);
             if (t == 0 && vg) ps.out[reinterpret_cast<const int*>(sg + D * S)[1]] = part;
             p += nvalid;
+        }
+        __syncwarp();
+    }
+}
+
+// ===========================================================================
+// Gather, d = 3, m = 4, sparse cells: CTA (item, l0) handles the cell slab l0
+// of a tile, warp w the cell column (l0, l1 = w), whose points are
+// consecutive (plan colb table), so every 8-point group is full but the last.
+// N = a (8 taps), K = (b, c) over the column's 8 x 11 (b, c) block in 22
+// k-steps (k-step j: c = j/2, b = 4(j%2) + t):
+//   A[g][t] = P w1_g[b] w2_g[c - l2_g]  (w2 pre-shifted into 11 slots, w2p)
+//   B[t][g] = H[l0 + g, l1 + b, c]     (22 values per lane, loaded once)
+//   y_p     = sum_a Z[p, a] w0_p[a]
+// The slab halo (8 x 11 x 11 nodes, tile-relative R folded in) is loaded once
+// per CTA.
+// ===========================================================================
+__global__ void __launch_bounds__(128, 4)
+gather3c_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
+                   const DWin* __restrict__ wins, const int* __restrict__ colb) {
+    constexpr int S = 8, TC = 4, PE = TC + S - 1, SL = S * PE * PE, RL = kCol3Row;
+    constexpr int kW2p = 2 * S, kCode = kW2p + PE;  // row: P w0[8] w1[8] w2p[11] code perm
+    extern __shared__ __align__(16) double smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int l0 = blockIdx.y;
+    double* halo = smem;
+    double* stage = smem + SL + warp * 32 * RL;
+
+    pdl_trigger();
+    const Item it = items[blockIdx.x];
+    const DPSet ps = psets[it.ps];
+    const DWin& wn = wins[ps.win];
+    int tc[3];
+    tile_coords(it.tile, 3, wn.ntile, tc);
+    __shared__ double sR[PE];
+    if (threadIdx.x < PE) sR[threadIdx.x] = wn.R[threadIdx.x];
+    const int col = 4 * l0 + warp;
+    const int wb = __ldg(colb + blockIdx.x * kColBounds + col);
+    const int we = __ldg(colb + blockIdx.x * kColBounds + col + 1);
+    __syncthreads();
+    pdl_wait();
+    if (threadIdx.x < PE * PE) {  // column (n1, n2) of the slab, walking n0 = l0 .. l0 + 7
+        const int k = threadIdx.x, n1 = k / PE, n2 = k - n1 * PE;
+        const int Lg = wn.Lg;
+        const long long plane = static_cast<long long>(Lg) * Lg;
+        const double r12 = sR[n1] * sR[n2];
+        if (!wn.wrap) {
+            const int i0 = tc[0] * TC + l0, i1 = tc[1] * TC + n1, i2 = tc[2] * TC + n2;
+            const bool ok12 = i1 < Lg && i2 < Lg;
+            const double* src = wn.H + (static_cast<long long>(i0) * Lg + i1) * Lg + i2;
+#pragma unroll
+            for (int a = 0; a < S; ++a) {
+                const bool ok = ok12 && i0 + a < Lg;
+                halo[a * PE * PE + k] = ok ? __ldg(src + a * plane) * (r12 * sR[l0 + a]) : 0.0;
+            }
+        } else {
+            const long long o12 = static_cast<long long>(pmod(wn.lo + tc[1] * TC + n1, wn.M)) * Lg +
+                                  pmod(wn.lo + tc[2] * TC + n2, wn.M);
+            int i0 = pmod(wn.lo + tc[0] * TC + l0, wn.M);
+#pragma unroll
+            for (int a = 0; a < S; ++a) {
+                halo[a * PE * PE + k] = __ldg(wn.H + i0 * plane + o12) * (r12 * sR[l0 + a]);
+                i0 = i0 + 1 == wn.M ? 0 : i0 + 1;
+            }
+        }
+    }
+    Pref<3> pa, pb;
+    if (wb + lane < we) pa.load(ps, wb + lane);
+    if (wb + 32 + lane < we) pb.load(ps, wb + 32 + lane);
+    __syncthreads();
+    if (wb >= we) return;
+
+    double hb[2 * PE];
+    {
+        const double* src = halo + g * PE * PE + (warp + t) * PE;
+#pragma unroll
+        for (int j = 0; j < 2 * PE; ++j) hb[j] = src[(j & 1) * 4 * PE + (j >> 1)];
+    }
+    for (int base = wb; base < we; base += 32) {
+        const int cnt = min(32, we - base);
+        if (lane < cnt) {
+            double* st = stage + lane * RL;
+            double q0 = pa.P, q1 = 1.0;
+#pragma unroll
+            for (int o = 0; o < S; ++o) {
+                st[o] = q0;
+                st[S + o] = q1;
+                q0 *= pa.Q[0];
+                q1 *= pa.Q[1];
+            }
+            const int l2 = pa.code & 3;
+            double q2 = 1.0;
+#pragma unroll
+            for (int r = 0; r < PE; ++r) {
+                const bool in = r >= l2 && r < l2 + S;
+                st[kW2p + r] = in ? q2 : 0.0;
+                if (in) q2 *= pa.Q[2];
+            }
+            reinterpret_cast<int*>(st + kCode)[1] = pa.perm;
+        }
+        pa = pb;
+        if (base + 64 + lane < we) pb.load(ps, base + 64 + lane);
+        __syncwarp();
+        for (int p = 0; p < cnt; p += 8) {
+            const bool vg = p + g < cnt;
+            const double* sg = stage + (vg ? p + g : p) * RL;
+            const double u0 = vg ? sg[S + t] : 0.0, u1 = vg ? sg[S + 4 + t] : 0.0;
+            const double2 c01 = ld2(sg + kW2p), c23 = ld2(sg + kW2p + 2), c45 = ld2(sg + kW2p + 4),
+                          c67 = ld2(sg + kW2p + 6), c89 = ld2(sg + kW2p + 8);
+            const double c[PE] = {c01.x, c01.y, c23.x, c23.y, c45.x, c45.y, c67.x, c67.y, c89.x, c89.y,
+                                  sg[kW2p + 10]};
+            const double2 w0 = ld2(sg + 2 * t);
+            double z[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+#pragma unroll
+            for (int j = 0; j < 2 * PE; ++j) dmma(z[j & 3][0], z[j & 3][1], c[j >> 1] * ((j & 1) ? u1 : u0), hb[j]);
+            const double z0 = (z[0][0] + z[1][0]) + (z[2][0] + z[3][0]);
+            const double z1 = (z[0][1] + z[1][1]) + (z[2][1] + z[3][1]);
+            double part = fma(z0, w0.x, z1 * w0.y);
+            part += __shfl_xor_sync(0xffffffffu, part, 1);
+            part += __shfl_xor_sync(0xffffffffu, part, 2);
+            if (t == 0 && vg) ps.out[reinterpret_cast<const int*>(sg + kCode)[1]] = part;
         }
         __syncwarp();
     }
@@ -1478,7 +1622,8 @@ static_assert(kW3 * 32 >= 11 * 11, "load_halo3_r / spread3 epilogue: one thread 
 constexpr int kW2 = 4;
 constexpr int kW1 = 8;
 
-static_assert(kCol3Row == Row<3, 8>::kLen, "spread3c shares spread3's SMEM layout");
+size_t gather3c_smem() { return sizeof(double) * (8 * 121 + 4 * 32 * kCol3Row); }
+size_t spread3c_smem() { return sizeof(double) * (kColWarps * (kCol3Sub + 32 * kCol3Row)); }
 size_t spread3_smem() { return sizeof(double) * (((kW3 * 1331 + 1) & ~1) + kW3 * 32 * Row<3, 8>::kLen); }
 size_t gather3_smem() { return sizeof(double) * (1332 + kW3 * 32 * Row<3, 8>::kLen); }
 size_t spread2_smem() { return sizeof(double) * (((kW2 * 225 + 1) & ~1) + kW2 * 32 * Row<2, 8>::kLen); }
@@ -1512,7 +1657,8 @@ cudaError_t init_kernel_attributes() {
             e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
     };
     set(reinterpret_cast<const void*>(spread3_s8_kernel<kW3>), spread3_smem());
-    set(reinterpret_cast<const void*>(spread3c_s8_kernel<kW3>), spread3_smem());
+    set(reinterpret_cast<const void*>(spread3c_s8_kernel), spread3c_smem());
+    set(reinterpret_cast<const void*>(gather3c_s8_kernel), gather3c_smem());
     set(reinterpret_cast<const void*>(gather3_s8_kernel<kW3>), gather3_smem());
     set(reinterpret_cast<const void*>(spread2_s8_kernel<kW2>), spread2_smem());
     set(reinterpret_cast<const void*>(gather2_s8_kernel<kW2>), gather2_smem());
@@ -1530,11 +1676,12 @@ cudaError_t init_kernel_attributes() {
 // Launch spread over `nitems` items whose windows all have dimension D and
 // span S (specialised kernels for S = 8, i.e. m = 4).
 void launch_spread(int D, int S, int PE, const Item* items, int nitems, const DPSet* ps,
-                   const DWin* wins, const double* v, double* patches, bool columns, cudaStream_t st) {
+                   const DWin* wins, const double* v, double* patches, const int* colb, cudaStream_t st) {
     if (nitems == 0) return;
     if (S == 8) {
-        if (D == 3 && columns)
-            launch_k(spread3c_s8_kernel<kW3>, dim3(nitems), dim3(kW3 * 32), spread3_smem(), st, items, ps, wins, v, patches);
+        if (D == 3 && colb)
+            launch_k(spread3c_s8_kernel, dim3(nitems), dim3(kColWarps * 32), spread3c_smem(), st, items, ps, wins, v,
+                     patches, colb);
         else if (D == 3)
             launch_k(spread3_s8_kernel<kW3>, dim3(nitems), dim3(kW3 * 32), spread3_smem(), st, items, ps, wins, v, patches);
         else if (D == 2)
@@ -1548,6 +1695,14 @@ void launch_spread(int D, int S, int PE, const Item* items, int nitems, const DP
     if (D == 1) launch_k(spread_generic_kernel<1>, dim3(nitems), dim3(W * 32), sm, st, items, ps, wins, v, patches, W);
     else if (D == 2) launch_k(spread_generic_kernel<2>, dim3(nitems), dim3(W * 32), sm, st, items, ps, wins, v, patches, W);
     else launch_k(spread_generic_kernel<3>, dim3(nitems), dim3(W * 32), sm, st, items, ps, wins, v, patches, W);
+}
+
+// Sparse d = 3 gather over the spread items (whole tiles) and their column
+// bounds: CTA (item, l0 slab).
+void launch_gather3c(const Item* items, int nitems, const DPSet* ps, const DWin* wins, const int* colb,
+                     cudaStream_t st) {
+    if (nitems == 0) return;
+    launch_k(gather3c_s8_kernel, dim3(nitems, 4), dim3(128), gather3c_smem(), st, items, ps, wins, colb);
 }
 
 void launch_gather(int D, int S, int PE, const Item* items, int nitems, const DPSet* ps,

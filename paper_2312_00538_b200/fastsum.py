@@ -185,12 +185,13 @@ class FastsumPlan:
 
     def __init__(self, handle, n: int, d: int, device: int):
         self._h = handle
+        self._free = _lib.load().ksvm_nfft_plan_free  # kept: module globals may be gone in __del__
         self._n, self._d, self.device = n, d, device
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h:
-            _lib.load().ksvm_nfft_plan_free(h)
+        h, free = getattr(self, "_h", None), getattr(self, "_free", None)
+        if h and free is not None:
+            free(h)
             self._h = None
 
     def num_sources(self) -> int:
@@ -294,15 +295,16 @@ class AnovaFastOperator(KernelOperator):
                                                sizes, P, eta, ell, C.byref(c), float(fit_fraction), mask,
                                                int(device), _lib.FP64, C.byref(h)))
         self._h = h
+        self._free = _lib.load().ksvm_nfft_op_free  # kept: module globals may be gone in __del__
         self._n = n
         self.device = int(device)
         self.num_windows = P
         self.window_mask = list(window_mask) if window_mask is not None else [True] * P
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h:
-            _lib.load().ksvm_nfft_op_free(h)
+        h, free = getattr(self, "_h", None), getattr(self, "_free", None)
+        if h and free is not None:
+            free(h)
             self._h = None
 
     def size(self) -> int:

@@ -117,13 +117,14 @@ def test_kernel_rows_and_diag():
     assert np.all(op.kernel_diag(0) == 1.0)
 
 
-@pytest.mark.parametrize("spread", ["cell", "column"])
+@pytest.mark.parametrize("spread,gather", [("cell", "column"), ("column", "cell")])
 @pytest.mark.parametrize("n,seed", [(3000, 91), (60000, 92)])
-def test_d3_spread_variants_match_oracle(oracle_lib, monkeypatch, spread, n, seed):
-    # both d = 3 spread kernels (per-cell and column-accumulating; the engine
-    # picks by the mean points per cell) at sparse and dense cells, for the
-    # operator and for a cross apply
+def test_d3_kernel_variants_match_oracle(oracle_lib, monkeypatch, spread, gather, n, seed):
+    # both d = 3 spread and gather kernels (per-cell and column-blocked; the
+    # engine picks by the mean points per cell) at sparse and dense cells,
+    # for the operator and for a cross apply
     monkeypatch.setenv("KSVM_NFFT_SPREAD3", spread)
+    monkeypatch.setenv("KSVM_NFFT_GATHER3", gather)
     pts = oracle.random_points(n, 3, seed)
     v = oracle.random_vector(n, seed + 1)
     g = anova_fast_operator(Dataset(pts), spec_of([[0, 1, 2]]))
