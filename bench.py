@@ -222,22 +222,24 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------ GPU arm ------
-def kernel_bytes(w, name):
+def kernel_bytes(w, name, pts):
     """Algorithmic HBM bytes of one launch (SURVEY.md 8(d) split per kernel):
     spread_dK reads the coordinates of its windows + v once; gather_dK reads
-    the coordinates + writes y once."""
+    the coordinates + writes y once. pts[l] = points window l is evaluated
+    on (n, or its distinct points after the exact duplicate merge)."""
     if not (name.startswith("spread_d") or name.startswith("gather_d")):
         return 0
     k = int(name[-1])
-    coords = sum(len(x) for x in w.windows if len(x) == k)
-    return 8 * w.n * (coords + 1)
+    sel = [(len(x), p) for x, p in zip(w.windows, pts) if len(x) == k and p > 0]
+    return 8 * (sum(d * p for d, p in sel) + max((p for _, p in sel), default=0))
 
 
-def kernel_fmas(w, name, m=4):
+def kernel_fmas(w, name, pts, m=4):
+    """FP64 FMAs one launch executes: (2m)^d per evaluated point and window."""
     if not (name.startswith("spread_d") or name.startswith("gather_d")):
         return 0
     k = int(name[-1])
-    return w.n * sum((2 * m) ** len(x) for x in w.windows if len(x) == k)
+    return sum(p * (2 * m) ** len(x) for x, p in zip(w.windows, pts) if len(x) == k)
 
 
 def fp64_peak_tflops(dev):
@@ -359,12 +361,13 @@ def run_ours(args):
 
     if rank == 0:
         hbm_peak, peak_kind = peaks()
-        dom = max((k2 for k2 in per_launch if kernel_bytes(w, k2) > 0), key=lambda k2: per_launch[k2],
+        pts = [op.window_points(l) for l in range(len(w.windows))]
+        dom = max((k2 for k2 in per_launch if kernel_bytes(w, k2, pts) > 0), key=lambda k2: per_launch[k2],
                   default=None)
         roof = None
         if dom is not None:
             ms = per_launch[dom]
-            ach = kernel_bytes(w, dom) / (ms * 1e-3) / 1e9
+            ach = kernel_bytes(w, dom, pts) / (ms * 1e-3) / 1e9
             traffic = None
             try:
                 with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
@@ -372,7 +375,7 @@ def run_ours(args):
             except Exception:
                 pass
             fpk = fp64_peak_tflops(dev)
-            fma_rate = kernel_fmas(w, dom) / (ms * 1e-3)
+            fma_rate = kernel_fmas(w, dom, pts) / (ms * 1e-3)
             roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
                     "frac": ach / hbm_peak, "peak_source": peak_kind, "traffic": traffic,
                     "kernel_ms": ms,
@@ -387,7 +390,8 @@ def run_ours(args):
                            "fit_fraction": w.fit_fraction, "N": 32, "m": 4, "sigma": 2,
                            "l2": "256 MiB flush before every timed step",
                            "parallelism": f"window-sharded x{world} + NCCL allreduce" if world > 1 else "1 GPU",
-                           "seed": 1000 + args.config},
+                           "seed": 1000 + args.config,
+                           "dedup": {str(l): p for l, p in enumerate(pts) if 0 < p < w.n}},
                 "hbm_fraction_matvec": (w.hbm_bytes() / (step_ms * 1e-3) / 1e9) / peaks()[0],
                 "per_launch_ms": per_launch,
                 "roofline": roof,

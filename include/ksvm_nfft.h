@@ -18,6 +18,7 @@
  * ksvm_nfft_plan_free              ~FastsumPlan             P:src/fastsum.cpp:80-90
  * ksvm_nfft_op_create              anova_fast_operator      P:include/ksvm/fastsum.hpp:81-84, P:src/fastsum.cpp:326-341,366-371
  * ksvm_nfft_op_size                KernelOperator::size     P:include/ksvm/kernel.hpp:35
+ * ksvm_nfft_op_window_points       (diagnostic: work actually executed per window)
  * ksvm_nfft_op_apply               KernelOperator::apply    P:include/ksvm/kernel.hpp:36, P:src/fastsum.cpp:345-352
  * ksvm_nfft_op_apply_batch         k applies (Nystrom sketch Y = K G, P:src/low_rank.cpp:139-150)
  * ksvm_nfft_op_entry               KernelOperator::entry    P:include/ksvm/kernel.hpp:37, P:src/fastsum.cpp:354-356
@@ -120,6 +121,11 @@ int ksvm_nfft_op_create(const double* points, int64_t n, int64_t d, int64_t ld, 
                         int precision, ksvm_nfft_op** out);
 int64_t ksvm_nfft_op_size(const ksvm_nfft_op* op);
 int ksvm_nfft_op_num_windows(const ksvm_nfft_op* op);
+/* Points window `window` is evaluated on: n, or the number of distinct scaled
+ * points when exact duplicates were merged (binary / low-cardinality
+ * features; the merge is exact); 0 for windows outside
+ * window_mask or an invalid index. */
+int64_t ksvm_nfft_op_window_points(const ksvm_nfft_op* op, int window);
 int ksvm_nfft_op_apply(const ksvm_nfft_op* op, const double* v, double* y, int ptr_kind,
                        void* stream);
 /* k right-hand sides; column c of V / Y starts at V + c * ld (ld >= n). */

@@ -50,6 +50,7 @@ _SIGS = {
                                       C.c_int, C.c_int, C.POINTER(_vp)]),
     "ksvm_nfft_op_size": (C.c_int64, [_vp]),
     "ksvm_nfft_op_num_windows": (C.c_int, [_vp]),
+    "ksvm_nfft_op_window_points": (C.c_int64, [_vp, C.c_int]),
     "ksvm_nfft_op_apply": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp]),
     "ksvm_nfft_op_apply_batch": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int64, C.c_int, _vp]),
     "ksvm_nfft_op_entry": (C.c_double, [_vp, C.c_int64, C.c_int64]),

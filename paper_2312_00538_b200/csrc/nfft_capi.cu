@@ -18,6 +18,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/ksvm_nfft.h"
@@ -41,8 +42,12 @@ void launch_conv(const DWin* wins, const int* slots, int nslots, int Lg_max, lon
                  int stage, cudaStream_t st);
 int conv_max_lg();
 
-void launch_combine(double* y, const double* parts, const double* eta, int P, long long n,
-                    cudaStream_t st);
+void launch_combine(double* y, const double* const* src, const int* const* inv, const uint8_t* const* inv8,
+                    const double* eta, int P, long long n, cudaStream_t st);
+void launch_bin_sums(const double* v, const uint8_t* const* codes, int nwl, long long n, double* partial,
+                     int nblk, const long long* vs_off, const int* nu, double* vs, cudaStream_t st);
+void launch_seg_sums(const double* v, const int* members, const int2* chunks, double* partial, int C,
+                     const int* seg_cb, double* vs, int U, cudaStream_t st);
 void launch_kernel_rows(double* out, const long long* rows, int r, const double* const* cols,
                         const int* wdim, const double* wgt, const double* ell2, int nw,
                         long long n, cudaStream_t st);
@@ -227,7 +232,65 @@ struct Window {
     DevBuf<int> tile_first;
     DevBuf<long long> tile_patch;
     PointSet src;
+    // Exact duplicates (operators only): the window runs on its nu distinct
+    // scaled points; members (CSR by distinct point, ascending original
+    // index) feed the segmented sum of v, inv maps each point to its
+    // distinct point for the output broadcast.
+    int64_t nu = 0;  // 0: no dedup
+    std::vector<int> offs, members;  // nu > kSmallBins only
+    DevBuf<int> inv;                 // nu > kSmallBins
+    DevBuf<uint8_t> inv8;            // nu <= kSmallBins (register-bin sums)
 };
+
+// Distinct points of a window's scaled coordinates (column-major n x d),
+// compared bit for bit: identical coordinates give identical kernel rows and
+// columns, so K~ v = K~_u (sum of v over each duplicate group) exactly up to
+// summation order. Used only when it shrinks the point count at least
+// kDedupRatio-fold; a leading sample rejects continuous data cheaply.
+constexpr int64_t kDedupRatio = 8;
+
+bool dedup_enabled() {  // KSVM_NFFT_DEDUP=0 turns the duplicate merge off
+    const char* e = std::getenv("KSVM_NFFT_DEDUP");
+    return !(e && e[0] == '0');
+}
+
+struct DedupKey {
+    uint64_t x[3];
+    bool operator==(const DedupKey& o) const { return x[0] == o.x[0] && x[1] == o.x[1] && x[2] == o.x[2]; }
+};
+struct DedupHash {
+    size_t operator()(const DedupKey& k) const {
+        uint64_t h = 1469598103934665603ull;
+        for (uint64_t v : k.x) h = (h ^ v) * 1099511628211ull ^ (v >> 29);
+        return static_cast<size_t>(h);
+    }
+};
+
+bool find_duplicates(const std::vector<double>& sc, int64_t n, int d, std::vector<int>& inv, int64_t& nu) {
+    auto key = [&](int64_t i) {
+        DedupKey k{{0, 0, 0}};
+        for (int t = 0; t < d; ++t) std::memcpy(&k.x[t], &sc[static_cast<size_t>(t * n + i)], sizeof(double));
+        return k;
+    };
+    const int64_t sample = std::min<int64_t>(n, 4096);
+    {
+        std::unordered_map<DedupKey, int, DedupHash> ids;
+        for (int64_t i = 0; i < sample; ++i) {
+            ids.emplace(key(i), 0);
+            if (static_cast<int64_t>(ids.size()) * kDedupRatio > sample) return false;
+        }
+    }
+    std::unordered_map<DedupKey, int, DedupHash> ids;
+    ids.reserve(static_cast<size_t>(n / kDedupRatio + 1));
+    inv.assign(static_cast<size_t>(n), 0);
+    for (int64_t i = 0; i < n; ++i) {
+        auto r = ids.emplace(key(i), static_cast<int>(ids.size()));
+        inv[static_cast<size_t>(i)] = r.first->second;
+        if (static_cast<int64_t>(ids.size()) * kDedupRatio > n) return false;
+    }
+    nu = static_cast<int64_t>(ids.size());
+    return n >= 2 * kDedupRatio;
+}
 
 // Grid geometry of one window. Without `range` it covers every admissible
 // point (sources: |x| <= fit r_T; cross targets: ||x|| <= r_T (1 + 1e-12),
@@ -449,6 +512,19 @@ struct Engine {
     int slot_begin[4] = {0, 0, 0, 0}, nslots_cls[4] = {0, 0, 0, 0};  // d_slots grouped by d
     DevBuf<double> d_eta;
     DevBuf<double> patches, parts, vbuf, ybuf;
+    // exact-duplicate windows (Window::nu): segmented sums of v and output maps
+    DevBuf<int> seg_members, seg_cb;
+    DevBuf<int2> seg_chunks;
+    DevBuf<double> seg_partial, vs_all, uout_all;
+    int n_seg_chunks = 0, n_segs = 0;
+    DevBuf<const double*> d_src;
+    DevBuf<const int*> d_inv;
+    DevBuf<const uint8_t*> d_inv8, d_codes;  // combine maps; codes of the register-bin windows
+    DevBuf<long long> d_small_off;
+    DevBuf<int> d_small_nu;
+    DevBuf<double> bin_partial;
+    int n_small = 0;
+    static constexpr int kBinBlocks = 148 * 2;
     DevBuf<double> d_raw;   // SoA raw window features (entries), original order
     DevBuf<const double*> d_rawcols;
     DevBuf<int> d_wdim;
@@ -560,8 +636,44 @@ struct Engine {
         w.G.alloc(nodes);
         w.H.alloc(nodes);
         for (int k = 0; k < (d == 1 ? 0 : (d == 2 ? 2 : 4)); ++k) w.T[k].alloc(nodes);
-        build_pointset(w.src, sc, n, d, g, item_chunk(n * n_owned_windows, d),
-                       gather_chunk(n * n_owned_windows), stream);
+        std::vector<int> inv;
+        int64_t nu = 0;
+        if (data_range && dedup_enabled() && find_duplicates(sc, n, d, inv, nu)) {
+            // distinct points (first occurrence order) and the CSR member lists
+            std::vector<double> su(static_cast<size_t>(nu) * d);
+            std::vector<int> first(static_cast<size_t>(nu), -1);
+            w.offs.assign(static_cast<size_t>(nu) + 1, 0);
+            for (int64_t i = 0; i < n; ++i) {
+                const int u = inv[static_cast<size_t>(i)];
+                if (first[static_cast<size_t>(u)] < 0) first[static_cast<size_t>(u)] = static_cast<int>(i);
+                ++w.offs[static_cast<size_t>(u) + 1];
+            }
+            for (int64_t u = 0; u < nu; ++u) {
+                w.offs[static_cast<size_t>(u) + 1] += w.offs[static_cast<size_t>(u)];
+                for (int t = 0; t < d; ++t)
+                    su[static_cast<size_t>(t * nu + u)] =
+                        sc[static_cast<size_t>(t * n + first[static_cast<size_t>(u)])];
+            }
+            w.nu = nu;
+            if (nu <= kSmallBins) {
+                std::vector<uint8_t> i8(inv.begin(), inv.end());
+                w.inv8.upload(i8.data(), i8.size(), stream);
+                w.offs.clear();
+            } else {
+                w.members.assign(static_cast<size_t>(n), 0);
+                std::vector<int> fill(w.offs.begin(), w.offs.end() - 1);
+                for (int64_t i = 0; i < n; ++i)
+                    w.members[static_cast<size_t>(fill[static_cast<size_t>(inv[static_cast<size_t>(i)])]++)] =
+                        static_cast<int>(i);
+                w.inv.upload(inv.data(), inv.size(), stream);
+            }
+            build_pointset(w.src, su, nu, d, g, item_chunk(n * n_owned_windows, d),
+                           gather_chunk(n * n_owned_windows), stream);
+        } else {
+            w.nu = 0;
+            build_pointset(w.src, sc, n, d, g, item_chunk(n * n_owned_windows, d),
+                           gather_chunk(n * n_owned_windows), stream);
+        }
 
         DWin& dw = w.dw;
         dw.d = d;
@@ -603,7 +715,7 @@ struct Engine {
             const std::vector<int>& tf = w.src.tile_first;
             long long occ = 0;
             for (size_t T = 0; T + 1 < tf.size(); ++T) occ += tf[T + 1] > tf[T] ? 1 : 0;
-            pts += n;
+            pts += w.src.n;
             cells += occ * w.dw.TC * w.dw.TC * w.dw.TC;
         }
         return cells > 0 && pts < kColumnDensity * cells;
@@ -678,6 +790,22 @@ struct Engine {
             nslots_cls[D] = static_cast<int>(slots.size()) - slot_begin[D];
         }
         parts.alloc(static_cast<size_t>(std::max(P, 1)) * n);
+        // exact-duplicate windows: member chunks of <= kSegChunk within one
+        // distinct point, global distinct-point numbering in slot order
+        std::vector<int> segm, segcb(1, 0);
+        std::vector<int2> chunks;
+        long long utotal = 0;
+        for (int s = 0; s < P; ++s) utotal += wins[static_cast<size_t>(owned[static_cast<size_t>(s)])]->nu;
+        if (utotal > 0) {
+            vs_all.alloc(static_cast<size_t>(utotal));
+            uout_all.alloc(static_cast<size_t>(utotal));
+        }
+        std::vector<const double*> srcs(static_cast<size_t>(P));
+        std::vector<const int*> invs(static_cast<size_t>(P), nullptr);
+        std::vector<const uint8_t*> inv8s(static_cast<size_t>(P), nullptr), codes;
+        std::vector<long long> small_off;
+        std::vector<int> small_nu;
+        long long uoff = 0;
         for (int s = 0; s < P; ++s) {
             Window& w = *wins[static_cast<size_t>(owned[static_cast<size_t>(s)])];
             dws[static_cast<size_t>(s)] = w.dw;
@@ -685,9 +813,58 @@ struct Engine {
             DPSet& p = ps[static_cast<size_t>(s)];
             p.F = w.src.F.p;
             p.CP = w.src.CP.p;
-            p.n = n;
             p.win = s;
-            p.out = parts.p + static_cast<size_t>(s) * n;
+            if (w.nu > 0 && w.nu <= kSmallBins) {
+                codes.push_back(w.inv8.p);
+                small_off.push_back(uoff);
+                small_nu.push_back(static_cast<int>(w.nu));
+                p.n = w.nu;
+                p.vsrc = vs_all.p + uoff;
+                p.out = uout_all.p + uoff;
+                srcs[static_cast<size_t>(s)] = p.out;
+                inv8s[static_cast<size_t>(s)] = w.inv8.p;
+                uoff += w.nu;
+            } else if (w.nu > 0) {
+                // the CSR segments are numbered in vs_all order: pad the
+                // register-bin windows' entries with empty segments
+                while (static_cast<long long>(segcb.size()) - 1 < uoff) segcb.push_back(static_cast<int>(chunks.size()));
+                const int base = static_cast<int>(segm.size());
+                segm.insert(segm.end(), w.members.begin(), w.members.end());
+                for (int64_t u = 0; u < w.nu; ++u) {
+                    for (int b = w.offs[static_cast<size_t>(u)]; b < w.offs[static_cast<size_t>(u) + 1]; b += kSegChunk)
+                        chunks.push_back(make_int2(base + b, base + std::min(b + kSegChunk, w.offs[static_cast<size_t>(u) + 1])));
+                    segcb.push_back(static_cast<int>(chunks.size()));
+                }
+                p.n = w.nu;
+                p.vsrc = vs_all.p + uoff;
+                p.out = uout_all.p + uoff;
+                srcs[static_cast<size_t>(s)] = p.out;
+                invs[static_cast<size_t>(s)] = w.inv.p;
+                uoff += w.nu;
+            } else {
+                p.n = n;
+                p.vsrc = nullptr;
+                p.out = parts.p + static_cast<size_t>(s) * n;
+                srcs[static_cast<size_t>(s)] = p.out;
+            }
+        }
+        n_seg_chunks = static_cast<int>(chunks.size());
+        n_segs = static_cast<int>(segcb.size()) - 1;
+        if (n_seg_chunks > 0) {
+            seg_members.upload(segm.data(), segm.size(), stream);
+            seg_chunks.upload(chunks.data(), chunks.size(), stream);
+            seg_cb.upload(segcb.data(), segcb.size(), stream);
+            seg_partial.alloc(static_cast<size_t>(n_seg_chunks));
+        }
+        d_src.upload(srcs.data(), srcs.size(), stream);
+        d_inv.upload(invs.data(), invs.size(), stream);
+        d_inv8.upload(inv8s.data(), inv8s.size(), stream);
+        n_small = static_cast<int>(codes.size());
+        if (n_small > 0) {
+            d_codes.upload(codes.data(), codes.size(), stream);
+            d_small_off.upload(small_off.data(), small_off.size(), stream);
+            d_small_nu.upload(small_nu.data(), small_nu.size(), stream);
+            bin_partial.alloc(static_cast<size_t>(kBinBlocks) * n_small * kSmallBins);
         }
         d_wins.upload(dws.data(), dws.size(), stream);
         d_ps.upload(ps.data(), ps.size(), stream);
@@ -763,6 +940,17 @@ struct Engine {
 
     // All classes; concurrent branches unless per-launch timing is on.
     void run_classes(const double* v, bool gather) {
+        if (n_small > 0 || n_seg_chunks > 0) tick("dedup_sums");  // per-distinct-point sums of v
+        if (n_small > 0) {
+            launch_bin_sums(v, d_codes.p, n_small, n, bin_partial.p, kBinBlocks, d_small_off.p, d_small_nu.p,
+                            vs_all.p, stream);
+            g_launches += 2;
+        }
+        if (n_seg_chunks > 0) {
+            launch_seg_sums(v, seg_members.p, seg_chunks.p, seg_partial.p, n_seg_chunks, seg_cb.p, vs_all.p,
+                            n_segs, stream);
+            g_launches += 2;
+        }
         int ncls = 0;
         for (int D = 1; D <= 3; ++D) ncls += class_end[D] > class_begin[D] ? 1 : 0;
         if (stage_timing || ncls < 2) {
@@ -800,7 +988,7 @@ struct Engine {
         nticks = 0;
         run_classes(v, true);
         tick("combine");
-        launch_combine(y, parts.p, d_eta.p, P, n, stream);
+        launch_combine(y, d_src.p, d_inv.p, d_inv8.p, d_eta.p, P, n, stream);
         ++g_launches;
         CK(cudaGetLastError());
         tick("end");
@@ -1059,6 +1247,13 @@ int ksvm_nfft_op_create(const double* points, int64_t n, int64_t d, int64_t ld, 
 int64_t ksvm_nfft_op_size(const ksvm_nfft_op* op) { return op ? op->e.n : 0; }
 int ksvm_nfft_op_num_windows(const ksvm_nfft_op* op) {
     return op ? static_cast<int>(op->e.wins.size()) : 0;
+}
+
+int64_t ksvm_nfft_op_window_points(const ksvm_nfft_op* op, int window) {
+    if (!op || window < 0 || window >= static_cast<int>(op->e.wins.size())) return 0;
+    const Window& w = *op->e.wins[static_cast<size_t>(window)];
+    if (!w.owned) return 0;
+    return w.nu > 0 ? w.nu : op->e.n;
 }
 
 int ksvm_nfft_op_apply(const ksvm_nfft_op* op, const double* v, double* y, int ptr_kind,

@@ -78,6 +78,11 @@ struct DPSet {
     long long n;
     int win;             // owning window slot
     double* out;         // gather output, original order (length n)
+    const double* vsrc;  // spread input (length n) if not the apply's v: the per-distinct-point
+                         // sums of an exact-duplicate window; nullptr otherwise
 };
+
+constexpr int kSegChunk = 256;  // members per warp in the duplicate-group sums of v
+constexpr int kSmallBins = 16;  // windows with <= this many distinct points use register bins
 
 }  // namespace ksvm_nfft

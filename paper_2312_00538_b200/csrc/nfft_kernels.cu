@@ -276,6 +276,7 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     pdl_trigger();
     const Item it = items[blockIdx.x];
     const DPSet ps = psets[it.ps];
+    if (ps.vsrc) v = ps.vsrc;  // exact-duplicate window: per-distinct-point sums of v
     const DWin& wn = wins[ps.win];
     for (int k = lane; k < PV; k += 32) wp[k] = 0.0;
     int wb, we;
@@ -400,6 +401,7 @@ spread3c_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pse
     pdl_trigger();
     const Item it = items[blockIdx.x];
     const DPSet ps = psets[it.ps];
+    if (ps.vsrc) v = ps.vsrc;  // exact-duplicate window: per-distinct-point sums of v
     const DWin& wn = wins[ps.win];
     for (int k = lane; k < SUB; k += 32) wp[k] = 0.0;
     const int wb = __ldg(colb + blockIdx.x * kColBounds + 2 * warp);
@@ -748,6 +750,7 @@ spread2_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     pdl_trigger();
     const Item it = items[blockIdx.x];
     const DPSet ps = psets[it.ps];
+    if (ps.vsrc) v = ps.vsrc;  // exact-duplicate window: per-distinct-point sums of v
     const DWin& wn = wins[ps.win];
     double R[S];
 #pragma unroll
@@ -886,6 +889,7 @@ spread1_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     pdl_trigger();
     const Item it = items[blockIdx.x];
     const DPSet ps = psets[it.ps];
+    if (ps.vsrc) v = ps.vsrc;  // exact-duplicate window: per-distinct-point sums of v
     const DWin& wn = wins[ps.win];
     double R[S];
 #pragma unroll
@@ -971,6 +975,7 @@ __global__ void spread_generic_kernel(const Item* __restrict__ items,
     pdl_trigger();
     const Item it = items[blockIdx.x];
     const DPSet ps = psets[it.ps];
+    if (ps.vsrc) v = ps.vsrc;  // exact-duplicate window: per-distinct-point sums of v
     const DWin& wn = wins[ps.win];
     const int S = wn.S, TC = wn.TC, PE = wn.PE;
     int PV = 1, taps = 1;
@@ -1482,16 +1487,134 @@ conv_stage_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots, 
 
 // y[j] = sum over owned windows (ascending) of eta_l * out_l[j]
 // (P:src/fastsum.cpp:346-351: out = 0; out += eta_l * apply_l).
-__global__ void combine_kernel(double* __restrict__ y, const double* __restrict__ parts,
+__global__ void combine_kernel(double* __restrict__ y, const double* const* __restrict__ src,
+                               const int* const* __restrict__ inv, const uint8_t* const* __restrict__ inv8,
                                const double* __restrict__ eta, int P, long long n) {
+    constexpr int kMaxP = 64;  // window table staged in SMEM (plan data, before the wait)
+    __shared__ const double* s_src[kMaxP];
+    __shared__ const int* s_inv[kMaxP];
+    __shared__ const uint8_t* s_inv8[kMaxP];
+    __shared__ double s_eta[kMaxP];
+    __shared__ int s_any;
     pdl_trigger();
+    if (threadIdx.x == 0) s_any = 0;
+    __syncthreads();
+    for (int l = threadIdx.x; l < min(P, kMaxP); l += blockDim.x) {
+        s_src[l] = src[l];
+        s_inv[l] = inv[l];
+        s_inv8[l] = inv8[l];
+        s_eta[l] = eta[l];
+        if (inv[l] || inv8[l]) s_any = 1;
+    }
+    __syncthreads();
+    const bool any_map = s_any != 0 || P > kMaxP;
     pdl_wait();
     for (long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
          j += static_cast<long long>(gridDim.x) * blockDim.x) {
         double acc = 0.0;
-        for (int l = 0; l < P; ++l) acc += eta[l] * parts[static_cast<long long>(l) * n + j];
+        if (!any_map) {
+            for (int l = 0; l < P; ++l) acc += s_eta[l] * __ldg(s_src[l] + j);
+        } else {
+            for (int l = 0; l < P; ++l) {
+                // exact-duplicate window: the value of the point's distinct point
+                const bool sm = l < kMaxP;
+                const int* iv = sm ? s_inv[l] : inv[l];
+                const uint8_t* i8 = sm ? s_inv8[l] : inv8[l];
+                const long long k =
+                    i8 ? static_cast<long long>(__ldg(i8 + j)) : (iv ? static_cast<long long>(__ldg(iv + j)) : j);
+                acc += (sm ? s_eta[l] : eta[l]) * (sm ? s_src[l] : src[l])[k];
+            }
+        }
         y[j] = acc;
     }
+}
+
+// Exact-duplicate windows, pass 1: one warp per chunk of <= kSegChunk members
+// of one distinct point; fixed lane assignment and butterfly, so the sum is
+// bit-reproducible.
+__global__ void seg_partial_kernel(const double* __restrict__ v, const int* __restrict__ members,
+                                   const int2* __restrict__ chunks, double* __restrict__ partial, int C) {
+    pdl_trigger();
+    pdl_wait();
+    const int lane = threadIdx.x & 31;
+    const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (c >= C) return;
+    const int2 ch = chunks[c];
+    double s = 0.0;
+    for (int i = ch.x + lane; i < ch.y; i += 32) s += __ldg(v + __ldg(members + i));
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) partial[c] = s;
+}
+
+// Exact-duplicate windows with <= NB distinct points: CTA (b, q) sums v over
+// the fixed point range b into lane-private SMEM bins of window q (one per
+// distinct point; no two lanes share a cell, so no atomics), then adds each
+// bin over the lanes and the warps in a fixed order. v is streamed once per
+// range and the codes are one byte, instead of chasing member lists.
+template <int NB>
+__global__ void __launch_bounds__(256)
+bins_partial_kernel(const double* __restrict__ v, const uint8_t* const* __restrict__ codes, int nwl, long long n,
+                    double* __restrict__ partial) {
+    constexpr int kW = 8;
+    __shared__ double bins[kW][NB][33];
+    __shared__ double red[NB][kW];
+    pdl_trigger();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long per = (n + gridDim.x - 1) / gridDim.x;
+    const long long b0 = static_cast<long long>(blockIdx.x) * per, b1 = min(n, b0 + per);
+    const int q = blockIdx.y;
+    const uint8_t* __restrict__ cq = codes[q];
+#pragma unroll
+    for (int u = 0; u < NB; ++u) bins[warp][u][lane] = 0.0;
+    pdl_wait();
+    for (long long i = b0 + threadIdx.x; i < b1; i += blockDim.x) bins[warp][__ldg(cq + i)][lane] += __ldg(v + i);
+    __syncwarp();
+    if (lane < NB) {
+        double s = 0.0;
+        for (int l = 0; l < 32; ++l) s += bins[warp][lane][l];
+        red[lane][warp] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < NB) {
+        double sum = 0.0;
+        for (int w = 0; w < kW; ++w) sum += red[threadIdx.x][w];
+        partial[(static_cast<long long>(blockIdx.x) * nwl + q) * NB + threadIdx.x] = sum;
+    }
+}
+
+// Pass 2 of the register-bin sums: vs[q][u] = sum of the block partials,
+// one warp per (window q, distinct point u): fixed lane stride + butterfly.
+__global__ void bins_sum_kernel(const double* __restrict__ partial, int nblk, int nwl, int NB,
+                                const long long* __restrict__ vs_off, const int* __restrict__ nu,
+                                double* __restrict__ vs) {
+    pdl_trigger();
+    pdl_wait();
+    const int q = blockIdx.x, u = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (q >= nwl || u >= nu[q]) return;
+    double acc = 0.0;
+    for (int b = lane; b < nblk; b += 32) acc += partial[(static_cast<long long>(b) * nwl + q) * NB + u];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) vs[vs_off[q] + u] = acc;
+}
+
+// Pass 2: per distinct point (one warp each), its chunk partials with a
+// fixed lane stride + butterfly.
+__global__ void seg_sum_kernel(const double* __restrict__ partial, const int* __restrict__ seg_cb,
+                               double* __restrict__ vs, int U) {
+    pdl_trigger();
+    pdl_wait();
+    const int lane = threadIdx.x & 31;
+    const int u = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (u >= U) return;
+    const int c0 = seg_cb[u], c1 = seg_cb[u + 1];
+    if (c0 == c1) return;  // entry of a register-bin window (bins_sum_kernel)
+    double acc = 0.0;
+    for (int c = c0 + lane; c < c1; c += 32) acc += partial[c];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) vs[u] = acc;
 }
 
 // Exact kernel rows for the preconditioners (P:src/pipeline.cpp:103-105,
@@ -1763,10 +1886,25 @@ void launch_conv(const DWin* wins, const int* slots, int nslots, int Lg_max, lon
 
 int conv_max_lg() { return kConvMaxL; }
 
-void launch_combine(double* y, const double* parts, const double* eta, int P, long long n,
-                    cudaStream_t st) {
+void launch_combine(double* y, const double* const* src, const int* const* inv, const uint8_t* const* inv8,
+                    const double* eta, int P, long long n, cudaStream_t st) {
     const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 16));
-    launch_k(combine_kernel, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, st, y, parts, eta, P, n);
+    launch_k(combine_kernel, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, st, y, src, inv, inv8, eta, P, n);
+}
+
+void launch_bin_sums(const double* v, const uint8_t* const* codes, int nwl, long long n, double* partial,
+                     int nblk, const long long* vs_off, const int* nu, double* vs, cudaStream_t st) {
+    if (nwl == 0) return;
+    launch_k(bins_partial_kernel<kSmallBins>, dim3(nblk, nwl), dim3(256), 0, st, v, codes, nwl, n, partial);
+    launch_k(bins_sum_kernel, dim3(nwl), dim3(32 * kSmallBins), 0, st, static_cast<const double*>(partial), nblk,
+             nwl, kSmallBins, vs_off, nu, vs);
+}
+
+void launch_seg_sums(const double* v, const int* members, const int2* chunks, double* partial, int C,
+                     const int* seg_cb, double* vs, int U, cudaStream_t st) {
+    if (C == 0) return;
+    launch_k(seg_partial_kernel, dim3((C + 7) / 8), dim3(256), 0, st, v, members, chunks, partial, C);
+    launch_k(seg_sum_kernel, dim3((U + 7) / 8), dim3(256), 0, st, static_cast<const double*>(partial), seg_cb, vs, U);
 }
 
 void launch_kernel_rows(double* out, const long long* rows, int r, const double* const* cols,

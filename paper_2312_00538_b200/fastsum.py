@@ -367,6 +367,11 @@ class AnovaFastOperator(KernelOperator):
                                                  C.c_void_p(0)))
         return out
 
+    def window_points(self, window: int) -> int:
+        """Points the window is evaluated on (distinct points after the exact
+        duplicate merge; 0 outside window_mask)."""
+        return int(_lib.load().ksvm_nfft_op_window_points(self._h, int(window)))
+
     def set_stage_timing(self, on: bool = True) -> None:
         """Record CUDA events between the five stages of every apply."""
         _raise(_lib.load().ksvm_nfft_op_set_stage_timing(self._h, 1 if on else 0))

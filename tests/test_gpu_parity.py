@@ -133,3 +133,47 @@ def test_d3_kernel_variants_match_oracle(oracle_lib, monkeypatch, spread, gather
     p, q = plan_fastsum(pts, GaussianKernelSpec(1.0)), oracle_lib.plan(pts)
     tg = pts[: n // 3] * 0.9
     assert rel(apply_fastsum_cross(p, tg, v), q.apply_cross(tg, v)) <= TOL
+
+
+@pytest.mark.parametrize("dedup", ["1", "0"])
+def test_duplicate_points_match_oracle(oracle_lib, monkeypatch, dedup):
+    # config-4-like windows: all-binary features (8 distinct points: the
+    # exact-duplicate path), one mixed window and one continuous window
+    monkeypatch.setenv("KSVM_NFFT_DEDUP", dedup)
+    rng = np.random.default_rng(41)
+    n = 20000
+    X = np.empty((n, 9))
+    X[:, 0:3] = rng.standard_normal((n, 3))
+    X[:, 3] = rng.standard_normal(n)
+    X[:, 4:9] = (rng.random((n, 5)) < 0.1).astype(float)
+    X = (X - X.min(0)) / (X.max(0) - X.min(0)) * 0.5 - 0.25
+    v = rng.standard_normal(n)
+    wins = [[0, 1, 2], [3, 4, 5], [6, 7, 8]]
+    g = anova_fast_operator(Dataset(X), spec_of(wins))
+    o = oracle_lib.anova(X, wins)
+    y = g.apply(v)
+    assert rel(y, o.apply(v)) <= TOL
+    assert np.array_equal(y, g.apply(v))
+    # a 2-d and a 1-d binary window
+    wins = [[4, 5], [6], [0, 1, 2]]
+    g = anova_fast_operator(Dataset(X), spec_of(wins))
+    assert rel(g.apply(v), oracle_lib.anova(X, wins).apply(v)) <= TOL
+    # 4-level features: 64 distinct points per window (member-list sums),
+    # next to register-bin and plain windows
+    L = np.floor(rng.random((n, 3)) * 4) / 3 * 0.5 - 0.25
+    X2 = np.hstack([X, L])
+    wins = [[4, 5, 6], [9, 10, 11], [0, 1, 2], [7, 8]]
+    g = anova_fast_operator(Dataset(X2), spec_of(wins))
+    o = oracle_lib.anova(X2, wins)
+    assert rel(g.apply(v), o.apply(v)) <= TOL
+    V = rng.standard_normal((n, 3))
+    Y = g.apply_batch(V)
+    for c in range(3):
+        assert rel(Y[:, c], o.apply(V[:, c])) <= TOL
+
+
+def test_duplicate_config4_shape_matches_oracle(oracle_lib):
+    w = workloads.make(4, 8000)
+    g = anova_fast_operator(Dataset(w.points), spec_of(w.windows), fit_fraction=w.fit_fraction)
+    o = oracle_lib.anova(w.points, w.windows, fit=w.fit_fraction)
+    assert rel(g.apply(w.v), o.apply(w.v)) <= TOL
