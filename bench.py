@@ -278,7 +278,7 @@ def run_ours(args):
 
     w = workloads.make(args.config, args.n)
     spec = AnovaKernelSpec(FeatureWindowing.explicit(w.windows))
-    owner = sharding.lpt_assign(sharding.window_costs(w.windows), world)
+    owner = sharding.lpt_assign(sharding.window_costs(w.windows, points=w.points), world)
     mask = sharding.window_mask(owner, rank) if world > 1 else None
     os.environ.setdefault("KSVM_NFFT_QUIET", "1")
     op = anova_fast_operator(Dataset(w.points), spec, fit_fraction=w.fit_fraction, device=local,

@@ -12,9 +12,28 @@ from typing import Callable, List, Sequence
 import numpy as np
 
 
-def window_costs(windows: Sequence[Sequence[int]], m: int = 4) -> List[int]:
-    """Per-point spread+gather cost of each window, 2 (2m)^{d_l} FMA."""
-    return [2 * (2 * m) ** len(w) for w in windows]
+DEDUP_RATIO = 8  # = kDedupRatio in nfft_capi.cu
+
+
+def evaluated_points(points: np.ndarray, window: Sequence[int]) -> int:
+    """Points a window is evaluated on: n, or its distinct tuples when the
+    library's exact duplicate merge applies (>= DEDUP_RATIO-fold shrink;
+    same 4096-point sample test as find_duplicates in nfft_capi.cu)."""
+    x = np.ascontiguousarray(points[:, list(window)])
+    n = x.shape[0]
+    s = x[:4096]
+    if len(np.unique(s, axis=0)) * DEDUP_RATIO > len(s) or n < 2 * DEDUP_RATIO:
+        return n
+    u = len(np.unique(x, axis=0))
+    return u if u * DEDUP_RATIO <= n else n
+
+
+def window_costs(windows: Sequence[Sequence[int]], m: int = 4, points: np.ndarray = None) -> List[int]:
+    """Spread+gather cost of each window, 2 (2m)^{d_l} FMA per evaluated
+    point (per point of the dataset when `points` is not given)."""
+    if points is None:
+        return [2 * (2 * m) ** len(w) for w in windows]
+    return [2 * (2 * m) ** len(w) * evaluated_points(points, w) for w in windows]
 
 
 def lpt_assign(costs: Sequence[float], world: int) -> List[int]:

@@ -13,8 +13,12 @@ ARGS="--steps 5 --warmup 3 --no-cpu-baseline"
 python bench.py $ARGS > gpurun_out/plain_cfg2.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none --csv --log-file gpurun_out/launches_cfg2.csv python bench.py $ARGS > gpurun_out/ncu_launch.log 2>&1
 python bench.py $ARGS > gpurun_out/plain_cfg2b.log 2>&1 && \
-ncu --set full --clock-control none --cache-control none --import-source on -k regex:"spread3|gather3" -s 4 -c 2 -o gpurun_out/prof_cfg2 python bench.py $ARGS > gpurun_out/ncu_full2.log 2>&1
+ncu --set full --clock-control none --cache-control all --import-source on -k regex:"spread3|gather3" -s 4 -c 2 -o gpurun_out/prof_cfg2 python bench.py $ARGS > gpurun_out/ncu_full2.log 2>&1
 ARGS4="--config 4 --steps 3 --warmup 3 --no-cpu-baseline"
 python bench.py $ARGS4 > gpurun_out/plain_cfg4.log 2>&1 && \
-ncu --set full --clock-control none --cache-control none --import-source on -k regex:"spread3|gather3" -s 4 -c 2 -o gpurun_out/prof_cfg4 python bench.py $ARGS4 > gpurun_out/ncu_full4.log 2>&1
+ncu --set full --clock-control none --cache-control all --import-source on -k regex:"spread3|gather3" -s 4 -c 2 -o gpurun_out/prof_cfg4 python bench.py $ARGS4 > gpurun_out/ncu_full4.log 2>&1
+python scripts/traffic.py cfg2=gpurun_out/prof_cfg2.ncu-rep cfg4=gpurun_out/prof_cfg4.ncu-rep > gpurun_out/traffic.json
+python scripts/ncu_summary.py gpurun_out/prof_cfg2.ncu-rep > gpurun_out/ncu_cfg2_full.txt
+python scripts/ncu_summary.py gpurun_out/prof_cfg4.ncu-rep > gpurun_out/ncu_cfg4_full.txt
+python scripts/launch_table.py gpurun_out/launches_cfg2.csv > gpurun_out/launches_cfg2.txt
 tail -1 gpurun_out/ncu_full2.log gpurun_out/ncu_full4.log

@@ -151,3 +151,15 @@ def test_c_example_compiles_and_links(tmp_path):
                         os.path.dirname(_lib.LIB_PATH), "-lksvm_nfft", "-lm", "-o", str(exe)],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_window_costs_count_distinct_points():
+    # binary windows are evaluated on their distinct points (exact duplicate
+    # merge), so LPT spreads the heavy continuous windows first
+    w = workloads.make(4, 4000)
+    pts = [sharding.evaluated_points(w.points, win) for win in w.windows]
+    assert all(p == w.n for p in pts[:4]) and all(p <= 8 for p in pts[4:])
+    costs = sharding.window_costs(w.windows, points=w.points)
+    owner = sharding.lpt_assign(costs, 4)
+    assert sorted(owner[:4]) == [0, 1, 2, 3]  # one heavy window per rank
+    assert sharding.window_costs(w.windows) == [1024] * 18
