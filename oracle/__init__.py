@@ -253,3 +253,78 @@ def dense_gaussian(pts, ell=1.0) -> np.ndarray:
         pts = pts[:, None]
     d2 = ((pts[:, None, :] - pts[None, :, :]) ** 2).sum(-1)
     return np.exp(-d2 / (ell * ell))
+
+
+# --- Newton saddle system (oracle/saddle_oracle.cpp, P:src/saddle.cpp) ------
+def _saddle_lib():
+    L = Lib("oracle").L
+    if not getattr(L, "_saddle_bound", False):
+        vp = C.c_void_p
+        L.oracle_saddle_last_error.restype = C.c_char_p
+        L.oracle_saddle_apply.restype = C.c_int
+        L.oracle_saddle_apply.argtypes = [vp, vp, C.c_int64, _dp, _dp, _dp, _dp]
+        L.oracle_precond_apply.restype = C.c_int
+        L.oracle_precond_apply.argtypes = [vp, C.c_int, C.c_int64, _dp, _dp, _dp, _dp, _ip]
+        L.oracle_gmres_solve.restype = C.c_int
+        L.oracle_gmres_solve.argtypes = [vp, vp, C.c_int64, _dp, _dp, vp, C.c_int, _dp, C.c_double, C.c_int,
+                                         _dp, _dp, _dp]
+        L._saddle_bound = True
+    return L
+
+
+def _saddle_check(L, code):
+    if code != 0:
+        raise OracleError(code, L.oracle_saddle_last_error().decode())
+
+
+def _kop(K):
+    """K: an oracle Anova (the NFFT operator) or a dense n x n matrix."""
+    if isinstance(K, Anova):
+        return K.h, None, K.n, None
+    D = np.ascontiguousarray(K, dtype=np.float64)
+    return None, C.c_void_p(D.ctypes.data), D.shape[0], D
+
+
+def saddle_apply(K, y, theta, vw) -> np.ndarray:
+    """SaddleOperator::apply (P:src/saddle.cpp:22-33)."""
+    L = _saddle_lib()
+    h, dense, n, keep = _kop(K)
+    y, theta, vw = _f64(y), _f64(theta), _f64(vw)
+    out = np.empty(n + 1)
+    _saddle_check(L, L.oracle_saddle_apply(h, dense, n, _ptr(y), _ptr(theta), _ptr(vw), _ptr(out)))
+    return out
+
+
+def precond_apply(Z, y, theta, g):
+    """SaddlePreconditioner(refresh(theta)).apply(g) (P:src/saddle.cpp:41-90);
+    Z None -> identity. Returns (out, diagonal_fallback)."""
+    L = _saddle_lib()
+    y, theta, g = _f64(y), _f64(theta), _f64(g)
+    n = y.shape[0]
+    Zc = None if Z is None else np.ascontiguousarray(Z, dtype=np.float64)
+    out = np.empty(n + 1)
+    fb = C.c_int(0)
+    _saddle_check(L, L.oracle_precond_apply(None if Zc is None else C.c_void_p(Zc.ctypes.data),
+                                            0 if Zc is None else Zc.shape[0], n, _ptr(y), _ptr(theta), _ptr(g),
+                                            _ptr(out), C.byref(fb)))
+    return out, bool(fb.value)
+
+
+def gmres_solve(K, y, theta, Z, rhs, tol, max_iter):
+    """gmres_solve with SaddleOperator(K, y, theta) and
+    SaddlePreconditioner(Z, y) refreshed at theta (P:src/saddle.cpp:92-178).
+    Returns (x, stats dict with residual_history)."""
+    L = _saddle_lib()
+    h, dense, n, keep = _kop(K)
+    y, theta, rhs = _f64(y), _f64(theta), _f64(rhs)
+    Zc = None if Z is None else np.ascontiguousarray(Z, dtype=np.float64)
+    x = np.empty(n + 1)
+    st = np.zeros(4)
+    hist = np.zeros(max(max_iter, 1))
+    _saddle_check(L, L.oracle_gmres_solve(h, dense, n, _ptr(y), _ptr(theta),
+                                          None if Zc is None else C.c_void_p(Zc.ctypes.data),
+                                          0 if Zc is None else Zc.shape[0], _ptr(rhs), float(tol), int(max_iter),
+                                          _ptr(x), _ptr(st), _ptr(hist)))
+    it = int(st[0])
+    return x, {"iterations": it, "relative_residual": float(st[1]), "converged": bool(st[2]),
+               "breakdown": bool(st[3]), "residual_history": hist[:it].copy()}

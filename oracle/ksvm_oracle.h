@@ -58,6 +58,20 @@ void oracle_random_points(int64_t n, int64_t d, uint64_t seed, double scale, dou
 void oracle_random_vector(int64_t n, uint64_t seed, double* out);
 void oracle_uniform(int64_t n, uint64_t seed, double lo, double hi, double* out);
 void oracle_bernoulli(int64_t n, uint64_t seed, double p, double* out);
+
+/* Saddle system (oracle/saddle_oracle.cpp, restating P:src/saddle.cpp). K is
+ * the ANOVA operator `op`, or, when `dense` is not NULL, the row-major n x n
+ * matrix (P:tests/helpers.hpp DenseOperator). Z: k x n row-major factor
+ * (StackedFactor::Z) or NULL for the identity preconditioner. gmres stats:
+ * {iterations, relative_residual, converged, breakdown}. */
+const char* oracle_saddle_last_error(void);
+int oracle_saddle_apply(const oracle_anova* op, const double* dense, int64_t n, const double* y,
+                        const double* theta, const double* vw, double* out);
+int oracle_precond_apply(const double* Z, int k, int64_t n, const double* y, const double* theta,
+                         const double* g, double* out, int* fallback);
+int oracle_gmres_solve(const oracle_anova* op, const double* dense, int64_t n, const double* y,
+                       const double* theta, const double* Z, int k, const double* rhs, double tol,
+                       int max_iter, double* x_out, double* stats, double* history);
 void oracle_fft(const double* in, double* out, int rank, const int* dims, int sign);
 
 #ifdef __cplusplus
