@@ -26,6 +26,12 @@
  *                                                           P:src/pipeline.cpp:103-105, P:src/low_rank.cpp:49-51
  * ksvm_nfft_kernel_diag            diagonal loop            P:src/low_rank.cpp:33-35
  * ksvm_nfft_op_free                ~AnovaFastOperator
+ * ksvm_nfft_saddle_create/         SaddleOperator           P:include/ksvm/saddle.hpp:14-31, P:src/saddle.cpp:7-33
+ *   set_theta/apply/free
+ * ksvm_nfft_precond_create/        SaddlePreconditioner     P:include/ksvm/saddle.hpp:33-58, P:src/saddle.cpp:35-90
+ *   refresh/apply/identity/
+ *   diagonal_fallback/free
+ * ksvm_nfft_gmres_solve            gmres_solve              P:include/ksvm/saddle.hpp:60-77, P:src/saddle.cpp:92-178
  *
  * Status values equal ksvm_status (P:capi/ksvm.h:17-23): 0 ok, 2 data/domain
  * error (DomainError, P:src/fastsum.cpp:316-320), 4 invalid argument
@@ -149,6 +155,48 @@ int ksvm_nfft_kernel_diag(const ksvm_nfft_op* op, int window, double* out, int p
 int ksvm_nfft_op_set_stage_timing(ksvm_nfft_op* op, int on);
 int ksvm_nfft_op_last_stage_ms(const ksvm_nfft_op* op, float* ms, int cap);
 const char* ksvm_nfft_op_stage_name(const ksvm_nfft_op* op, int i);
+int ksvm_nfft_op_device(const ksvm_nfft_op* op);
+
+/* ---- Newton saddle system, GPU resident ----------------
+ * The IPM's inner solve, A [v; w] = [Y K Y v + Theta v - w y; -y^T v] with K
+ * the ANOVA operator, right-preconditioned by the block-triangular SMW
+ * preconditioner of A-hat = Theta + Y Z^T Z Y (Z: k x n row-major, the
+ * stacked low-rank factor; NULL or k == 0 gives the identity, like a null
+ * StackedFactor). Every vector stays on the operator's GPU; GMRES keeps its
+ * Krylov basis in HBM and only the (k+2)-entry Hessenberg column crosses to
+ * the host per iteration. Vectors of the saddle system have n + 1 entries.
+ * y, theta, Z are host arrays copied at create/refresh time. Theta must be
+ * positive (std::invalid_argument, status 4); precond_apply before refresh
+ * is std::logic_error (status 5). The rank is limited to k <= 1024. */
+typedef struct ksvm_nfft_saddle ksvm_nfft_saddle;
+typedef struct ksvm_nfft_precond ksvm_nfft_precond;
+typedef struct ksvm_nfft_gmres_stats {
+    int iterations;            /* GmresStats::iterations */
+    double relative_residual;  /* true relative residual of the returned x */
+    int converged;
+    int breakdown;
+} ksvm_nfft_gmres_stats;
+
+int ksvm_nfft_saddle_create(const ksvm_nfft_op* op, const double* y, const double* theta,
+                            ksvm_nfft_saddle** out);
+int ksvm_nfft_saddle_set_theta(ksvm_nfft_saddle* s, const double* theta);
+int ksvm_nfft_saddle_apply(const ksvm_nfft_saddle* s, const double* vw, double* out, int ptr_kind,
+                           void* stream);
+void ksvm_nfft_saddle_free(ksvm_nfft_saddle* s);
+
+int ksvm_nfft_precond_create(const double* Z, int k, int64_t n, const double* y, int device,
+                             ksvm_nfft_precond** out);
+int ksvm_nfft_precond_refresh(ksvm_nfft_precond* p, const double* theta);
+int ksvm_nfft_precond_apply(const ksvm_nfft_precond* p, const double* g, double* out, int ptr_kind,
+                            void* stream);
+int ksvm_nfft_precond_identity(const ksvm_nfft_precond* p);
+int ksvm_nfft_precond_diagonal_fallback(const ksvm_nfft_precond* p);
+void ksvm_nfft_precond_free(ksvm_nfft_precond* p);
+
+/* residual_history: NULL or room for max_iter estimates (host). */
+int ksvm_nfft_gmres_solve(const ksvm_nfft_saddle* s, const ksvm_nfft_precond* p, const double* rhs,
+                          double tol, int max_iter, double* x, ksvm_nfft_gmres_stats* stats,
+                          double* residual_history, int ptr_kind, void* stream);
 void ksvm_nfft_op_free(ksvm_nfft_op* op);
 
 #ifdef __cplusplus

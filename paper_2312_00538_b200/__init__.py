@@ -8,9 +8,11 @@ package as the Python mirror of the reference's operator seam.
 from .fastsum import (AnovaFastOperator, AnovaKernelSpec, Dataset, DomainError, FastsumConfig,
                       FastsumPlan, FeatureWindowing, GaussianKernelSpec, KernelOperator,
                       anova_fast_operator, apply_fastsum, apply_fastsum_cross, plan_fastsum)
+from .saddle import GmresStats, SaddleOperator, SaddlePreconditioner, gmres_solve
 
 __all__ = [
     "AnovaFastOperator", "AnovaKernelSpec", "Dataset", "DomainError", "FastsumConfig",
     "FastsumPlan", "FeatureWindowing", "GaussianKernelSpec", "KernelOperator",
     "anova_fast_operator", "apply_fastsum", "apply_fastsum_cross", "plan_fastsum",
+    "GmresStats", "SaddleOperator", "SaddlePreconditioner", "gmres_solve",
 ]

@@ -18,6 +18,11 @@ HOST, DEVICE = 0, 1
 FP64 = 0
 
 
+class GmresStats(C.Structure):
+    _fields_ = [("iterations", C.c_int), ("relative_residual", C.c_double),
+                ("converged", C.c_int), ("breakdown", C.c_int)]
+
+
 class Config(C.Structure):
     _fields_ = [("bandwidth", C.c_int), ("window_cutoff", C.c_int),
                 ("oversampling", C.c_int), ("torus_radius", C.c_double)]
@@ -60,6 +65,19 @@ _SIGS = {
     "ksvm_nfft_op_last_stage_ms": (C.c_int, [_vp, C.POINTER(C.c_float), C.c_int]),
     "ksvm_nfft_op_stage_name": (C.c_char_p, [_vp, C.c_int]),
     "ksvm_nfft_op_free": (None, [_vp]),
+    "ksvm_nfft_op_device": (C.c_int, [_vp]),
+    # Newton saddle system
+    "ksvm_nfft_saddle_create": (C.c_int, [_vp, _vp, _vp, C.POINTER(_vp)]),
+    "ksvm_nfft_saddle_set_theta": (C.c_int, [_vp, _vp]),
+    "ksvm_nfft_saddle_apply": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp]),
+    "ksvm_nfft_saddle_free": (None, [_vp]),
+    "ksvm_nfft_precond_create": (C.c_int, [_vp, C.c_int, C.c_int64, _vp, C.c_int, C.POINTER(_vp)]),
+    "ksvm_nfft_precond_refresh": (C.c_int, [_vp, _vp]),
+    "ksvm_nfft_precond_apply": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp]),
+    "ksvm_nfft_precond_identity": (C.c_int, [_vp]),
+    "ksvm_nfft_precond_diagonal_fallback": (C.c_int, [_vp]),
+    "ksvm_nfft_precond_free": (None, [_vp]),
+    "ksvm_nfft_gmres_solve": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_int, _vp, _vp, _vp, C.c_int, _vp]),
 }
 
 EXPORTED = tuple(_SIGS)

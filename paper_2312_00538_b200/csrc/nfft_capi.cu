@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "../../include/ksvm_nfft.h"
+#include "capi_common.cuh"
 #include "nfft_engine.cuh"
 
 namespace ksvm_nfft {
@@ -60,77 +61,6 @@ void launch_factors(const double* x0, const double* x1, const double* x2, const 
                     int tile_rel, double4* F, int2* CP, cudaStream_t st);
 
 namespace {
-
-thread_local std::string t_err = "ok";
-std::atomic<int64_t> g_launches{0};
-
-struct DomainErr : std::runtime_error {
-    using std::runtime_error::runtime_error;
-};
-
-void ck(cudaError_t e, const char* what) {
-    if (e != cudaSuccess)
-        throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
-}
-#define CK(x) ck((x), #x)
-
-template <typename F>
-int guarded(F&& f) {
-    try {
-        f();
-        return KSVM_NFFT_OK;
-    } catch (const DomainErr& e) {
-        t_err = e.what();
-        return KSVM_NFFT_ERR_DATA;
-    } catch (const std::invalid_argument& e) {
-        t_err = e.what();
-        return KSVM_NFFT_ERR_CONFIG;
-    } catch (const std::bad_alloc&) {
-        t_err = "out of memory";
-        return KSVM_NFFT_ERR_INTERNAL;
-    } catch (const std::exception& e) {
-        t_err = e.what();
-        return KSVM_NFFT_ERR_INTERNAL;
-    }
-}
-
-template <typename T>
-struct DevBuf {
-    T* p = nullptr;
-    size_t n = 0;
-    DevBuf() = default;
-    DevBuf(const DevBuf&) = delete;
-    DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
-        o.p = nullptr;
-        o.n = 0;
-    }
-    ~DevBuf() { reset(); }
-    void reset() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        n = 0;
-    }
-    void alloc(size_t count) {
-        reset();
-        if (count == 0) count = 1;
-        CK(cudaMalloc(&p, count * sizeof(T)));
-        n = count;
-    }
-    void upload(const T* h, size_t count, cudaStream_t st) {
-        alloc(count);
-        CK(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, st));
-    }
-};
-
-struct DeviceGuard {
-    int prev = 0;
-    explicit DeviceGuard(int dev) {
-        CK(cudaGetDevice(&prev));
-        if (prev != dev) CK(cudaSetDevice(dev));
-    }
-    ~DeviceGuard() { cudaSetDevice(prev); }
-};
 
 void ensure_attributes(int dev) {
     static std::mutex mu;
@@ -905,23 +835,23 @@ struct Engine {
                       d_wins.p, v, patches.p,
                       spread_columns[D] ? d_colb.p + static_cast<size_t>(class_begin[D]) * kColBounds : nullptr,
                       st);
-        ++g_launches;
+        ++launch_counter();
         if (n_multi_cls[D]) {
             tick("tile_reduce");
             launch_tile_reduce(d_wins.p, d_multi.p + multi_begin[D], n_multi_cls[D], max_pv, patches.p, st);
-            ++g_launches;
+            ++launch_counter();
         }
         tick("reduce");
         for (int wrap = 0; wrap < 2; ++wrap) {
             if (!(wrap ? has_wrap : has_nowrap)[D]) continue;
             launch_reduce(d_wins.p, d_slots.p + slot_begin[D], nslots_cls[D], max_nodes, D,
                           2 * cfg.window_cutoff, patches.p, wrap != 0, max_tiles[D], st);
-            ++g_launches;
+            ++launch_counter();
         }
         for (int stg = 0; stg < D; ++stg) {
             tick(kConv[stg]);
             launch_conv(d_wins.p, d_slots.p + slot_begin[D], nslots_cls[D], max_lg, max_fibres, stg, st);
-            ++g_launches;
+            ++launch_counter();
         }
         if (gather) {
             const int gcnt = gclass_end[D] - gclass_begin[D];
@@ -933,7 +863,7 @@ struct Engine {
                 launch_gather(D, 2 * cfg.window_cutoff, class_PE[D], d_gitems.p + gclass_begin[D], gcnt, d_ps.p,
                               d_wins.p, st);
             }
-            ++g_launches;
+            ++launch_counter();
         }
         CK(cudaGetLastError());
     }
@@ -944,12 +874,12 @@ struct Engine {
         if (n_small > 0) {
             launch_bin_sums(v, d_codes.p, n_small, n, bin_partial.p, kBinBlocks, d_small_off.p, d_small_nu.p,
                             vs_all.p, stream);
-            g_launches += 2;
+            launch_counter() += 2;
         }
         if (n_seg_chunks > 0) {
             launch_seg_sums(v, seg_members.p, seg_chunks.p, seg_partial.p, n_seg_chunks, seg_cb.p, vs_all.p,
                             n_segs, stream);
-            g_launches += 2;
+            launch_counter() += 2;
         }
         int ncls = 0;
         for (int D = 1; D <= 3; ++D) ncls += class_end[D] > class_begin[D] ? 1 : 0;
@@ -982,14 +912,14 @@ struct Engine {
         const int P = P_owned();
         if (P == 0) {
             launch_fill(y, 0.0, n, stream);
-            ++g_launches;
+            ++launch_counter();
             return;
         }
         nticks = 0;
         run_classes(v, true);
         tick("combine");
         launch_combine(y, d_src.p, d_inv.p, d_inv8.p, d_eta.p, P, n, stream);
-        ++g_launches;
+        ++launch_counter();
         CK(cudaGetLastError());
         tick("end");
         last_nticks = nticks;
@@ -1037,7 +967,7 @@ struct Engine {
             GraphEntry& gph = graphs[k];
             if (gph.v == v && gph.y == y && gph.timed == stage_timing) {
                 CK(cudaGraphLaunch(gph.exec, stream));
-                g_launches += gph.launches;
+                launch_counter() += gph.launches;
                 last_nticks = gph.nticks;
                 for (int i = 0; i < gph.nticks; ++i) tick_name[i] = gph.names[i];
                 if (k + 1 != graphs.size()) std::rotate(graphs.begin() + k, graphs.begin() + k + 1, graphs.end());
@@ -1045,7 +975,7 @@ struct Engine {
             }
         }
         cudaGraph_t graph = nullptr;
-        const int64_t before = g_launches.load();
+        const int64_t before = launch_counter().load();
         CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
         capturing = true;
         try {
@@ -1062,8 +992,8 @@ struct Engine {
         gph.v = v;
         gph.y = y;
         gph.timed = stage_timing;
-        gph.launches = g_launches.load() - before;
-        g_launches -= gph.launches;  // counted when launched
+        gph.launches = launch_counter().load() - before;
+        launch_counter() -= gph.launches;  // counted when launched
         gph.nticks = last_nticks;
         for (int i = 0; i < last_nticks; ++i) gph.names[i] = tick_name[i];
         const cudaError_t e = cudaGraphInstantiate(&gph.exec, graph, 0);
@@ -1075,7 +1005,7 @@ struct Engine {
         }
         graphs.push_back(gph);
         CK(cudaGraphLaunch(gph.exec, stream));
-        g_launches += gph.launches;
+        launch_counter() += gph.launches;
     }
 
     // Host/device dispatch shared by every apply-like entry point.
@@ -1210,9 +1140,9 @@ void build_engine(Engine& E, const double* points, int64_t n, int64_t d, int64_t
 
 extern "C" {
 
-const char* ksvm_nfft_last_error(void) { return t_err.c_str(); }
+const char* ksvm_nfft_last_error(void) { return last_error_ref().c_str(); }
 const char* ksvm_nfft_version(void) { return "ksvm_nfft 0.1 sm_100a fp64"; }
-int64_t ksvm_nfft_launch_count(void) { return g_launches.load(); }
+int64_t ksvm_nfft_launch_count(void) { return launch_counter().load(); }
 
 void ksvm_nfft_config_default(ksvm_nfft_config* cfg) {
     if (!cfg) return;
@@ -1337,7 +1267,7 @@ int ksvm_nfft_kernel_rows(const ksvm_nfft_op* op, int window, const int64_t* row
         }
         launch_kernel_rows(dst, drows.p, r, E.d_rawcols.p + c0, E.d_wdim.p + (window < 0 ? 0 : window), dw.p, de.p,
                            nw, E.n, E.stream);
-        ++g_launches;
+        ++launch_counter();
         CK(cudaGetLastError());
         if (ptr_kind == KSVM_NFFT_HOST) {
             CK(cudaMemcpyAsync(out, dst, sizeof(double) * total, cudaMemcpyDeviceToHost, E.stream));
@@ -1370,10 +1300,12 @@ int ksvm_nfft_kernel_diag(const ksvm_nfft_op* op, int window, double* out, int p
         if (ptr_kind != KSVM_NFFT_DEVICE) throw std::invalid_argument("bad ptr_kind");
         DeviceGuard dg(E.device);
         launch_fill(out, val, E.n, static_cast<cudaStream_t>(stream));
-        ++g_launches;
+        ++launch_counter();
         CK(cudaGetLastError());
     });
 }
+
+int ksvm_nfft_op_device(const ksvm_nfft_op* op) { return op ? op->e.device : -1; }
 
 int ksvm_nfft_op_set_stage_timing(ksvm_nfft_op* op, int on) {
     if (!op) return KSVM_NFFT_ERR_CONFIG;
@@ -1391,7 +1323,7 @@ int ksvm_nfft_op_last_stage_ms(const ksvm_nfft_op* op, float* ms, int cap) {
         std::lock_guard<std::mutex> lk(E.mu);
         k = E.collect_stage_times();
     } catch (const std::exception& e) {
-        t_err = e.what();
+        last_error_ref() = e.what();
         return 0;
     }
     k = std::min(cap, k);
@@ -1491,7 +1423,7 @@ int ksvm_nfft_plan_apply_cross(const ksvm_nfft_plan* plan, const double* targets
         E.run_grid(dv);
         launch_gather(w.d, 2 * E.cfg.window_cutoff, w.dw.PE, ditems.p, static_cast<int>(its.size()), dps.p,
                       E.d_wins.p, E.stream);
-        ++g_launches;
+        ++launch_counter();
         CK(cudaGetLastError());
         if (ptr_kind == KSVM_NFFT_HOST) {
             CK(cudaMemcpyAsync(out, tout.p, sizeof(double) * t, cudaMemcpyDeviceToHost, E.stream));
