@@ -20,20 +20,13 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include "launch.cuh"
 #include "nfft_engine.cuh"
 
 namespace ksvm_nfft {
 
 namespace {
 
-// Programmatic dependent launch (apply-path kernels, launch_k): every kernel
-// lets its stream successor start at once (pdl_trigger), does its plan-only
-// prologue (items, DWin, tile tables: immutable during an apply), and waits
-// for its predecessor's results (pdl_wait) before touching any buffer an
-// earlier kernel writes or reads. Every CTA waits before it exits, so grid
-// completion stays transitive along the stream.
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ int pmod(int a, int M) {
     int r = a % M;
@@ -1714,31 +1707,6 @@ __global__ void factors_kernel(const double* __restrict__ x0, const double* __re
 }
 
 // ---- launchers ------------------------------------------------------------
-
-// Apply-path launches carry the programmatic-stream-serialization attribute
-// (PDL, see pdl_trigger/pdl_wait); KSVM_NFFT_PDL=0 turns it off.
-bool pdl_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("KSVM_NFFT_PDL");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
-
-template <typename... KArgs, typename... Args>
-void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
-    (void)cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);  // errors: cudaGetLastError
-}
 
 constexpr int kW3 = 4;  // warps per CTA of the d=3, m=4 kernels
 static_assert(kW3 * 32 >= 11 * 11, "load_halo3_r / spread3 epilogue: one thread per (n1, n2) column");

@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "capi_common.cuh"
+#include "launch.cuh"
 
 namespace ksvm_nfft {
 namespace {
@@ -60,6 +61,8 @@ __device__ __forceinline__ void block_partial(double v, double* partial) {
 
 __global__ void __launch_bounds__(kRT) k_mul(double* __restrict__ out, const double* __restrict__ a,
                                              const double* __restrict__ b, long long n) {
+    pdl_trigger();
+    pdl_wait();
     KSVM_FOR_BLOCK_INDEX(j, n) out[j] = a[j] * b[j];
 }
 
@@ -68,6 +71,8 @@ __global__ void __launch_bounds__(kRT) k_saddle_post(double* __restrict__ out, c
                                                      const double* __restrict__ kv, const double* __restrict__ theta,
                                                      const double* __restrict__ vw, long long n,
                                                      double* __restrict__ partial) {
+    pdl_trigger();
+    pdl_wait();
     const double w = vw[n];
     double acc = 0.0;
     KSVM_FOR_BLOCK_INDEX(j, n) {
@@ -81,6 +86,8 @@ __global__ void __launch_bounds__(kRT) k_saddle_post(double* __restrict__ out, c
 // *dst = coef * sum(partial) - (sub ? *sub : 0), or sqrt(sum) when root.
 __global__ void k_finish_scalar(const double* __restrict__ partial, int nb, double* __restrict__ dst, double coef,
                                 const double* __restrict__ sub, int root) {
+    pdl_trigger();
+    pdl_wait();
     double s = 0.0;
     for (int b = threadIdx.x; b < nb; b += 32) s += partial[b];
     s = warp_sum(s);
@@ -92,6 +99,8 @@ __global__ void k_finish_scalar(const double* __restrict__ partial, int nb, doub
 __global__ void __launch_bounds__(kRT) k_mdot(const double* __restrict__ M, long long ld, int rows, long long L,
                                               int mode, const double* __restrict__ w, const double* __restrict__ y,
                                               const double* __restrict__ theta, double* __restrict__ partial) {
+    pdl_trigger();
+    pdl_wait();
     __shared__ double sh[kRT / 32][kRows];
     for (int a0 = 0; a0 < rows; a0 += kRows) {
         double acc[kRows];
@@ -121,6 +130,8 @@ __global__ void __launch_bounds__(kRT) k_mdot(const double* __restrict__ M, long
 
 // out[a] = sum_b partial[b * rows + a] (one warp per row).
 __global__ void k_rows_finish(const double* __restrict__ partial, int nb, int rows, double* __restrict__ out) {
+    pdl_trigger();
+    pdl_wait();
     const int a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (a >= rows) return;
     double s = 0.0;
@@ -132,6 +143,8 @@ __global__ void k_rows_finish(const double* __restrict__ partial, int nb, int ro
 // inner = Cinv s (k x k, k <= kMaxRank)
 __global__ void k_gemv_small(const double* __restrict__ Cinv, int k, const double* __restrict__ s,
                              double* __restrict__ inner) {
+    pdl_trigger();
+    pdl_wait();
     const int a = blockIdx.x * blockDim.x + threadIdx.x;
     if (a >= k) return;
     double acc = 0.0;
@@ -144,6 +157,8 @@ __global__ void __launch_bounds__(kRT) k_smw_out(double* __restrict__ out, const
                                                  const double* __restrict__ y, const double* __restrict__ theta,
                                                  const double* __restrict__ Z, int k, const double* __restrict__ inner,
                                                  long long n, double* __restrict__ partial) {
+    pdl_trigger();
+    pdl_wait();
     extern __shared__ double s_inner[];
     for (int a = threadIdx.x; a < k; a += blockDim.x) s_inner[a] = inner[a];
     __syncthreads();
@@ -162,6 +177,8 @@ __global__ void __launch_bounds__(kRT) k_smw_out(double* __restrict__ out, const
 __global__ void __launch_bounds__(kRT) k_diag_out(double* __restrict__ out, const double* __restrict__ g,
                                                   const double* __restrict__ y, const double* __restrict__ theta,
                                                   long long n, double* __restrict__ partial) {
+    pdl_trigger();
+    pdl_wait();
     double acc = 0.0;
     KSVM_FOR_BLOCK_INDEX(j, n) {
         const double x1 = g[j] / theta[j];
@@ -175,6 +192,8 @@ __global__ void __launch_bounds__(kRT) k_diag_out(double* __restrict__ out, cons
 __global__ void __launch_bounds__(kRT) k_combine_rows(double* __restrict__ w, const double* __restrict__ V,
                                                       long long ld, int rows, const double* __restrict__ c,
                                                       long long L, int mode) {
+    pdl_trigger();
+    pdl_wait();
     KSVM_FOR_BLOCK_INDEX(i, L) {
         double s = 0.0;
         for (int a = 0; a < rows; ++a) s += V[static_cast<long long>(a) * ld + i] * c[a];
@@ -184,12 +203,16 @@ __global__ void __launch_bounds__(kRT) k_combine_rows(double* __restrict__ w, co
 
 __global__ void __launch_bounds__(kRT) k_scale(double* __restrict__ dst, const double* __restrict__ src, long long L,
                                                const double* __restrict__ denom) {
+    pdl_trigger();
+    pdl_wait();
     const double d = *denom;
     KSVM_FOR_BLOCK_INDEX(i, L) dst[i] = src[i] / d;
 }
 
 __global__ void __launch_bounds__(kRT) k_sq_diff(const double* __restrict__ a, const double* __restrict__ b, long long L,
                                                  double* __restrict__ partial) {
+    pdl_trigger();
+    pdl_wait();
     double acc = 0.0;
     KSVM_FOR_BLOCK_INDEX(i, L) {
         const double d = a[i] - b[i];
@@ -203,6 +226,8 @@ __global__ void __launch_bounds__(kRT) k_sq_diff(const double* __restrict__ a, c
 // (P:src/saddle.cpp:52-54 computes Z * Theta^{-1} * Z^T).
 __global__ void k_cap_partial(const double* __restrict__ Z, const double* __restrict__ theta, int k, long long n,
                               long long chunk, int nt, double* __restrict__ partial) {
+    pdl_trigger();
+    pdl_wait();
     const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const int ta = blockIdx.x / nt, tb = blockIdx.x % nt;
     const long long j0 = static_cast<long long>(blockIdx.y) * chunk, j1 = min(n, j0 + chunk);
@@ -224,6 +249,8 @@ __global__ void k_cap_partial(const double* __restrict__ Z, const double* __rest
 
 // C[a][b] = (a == b) + sum over chunks (in order) of the tile partials
 __global__ void k_cap_finish(const double* __restrict__ partial, int nchunks, int nt, int k, double* __restrict__ C) {
+    pdl_trigger();
+    pdl_wait();
     const int idx = blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= k * k) return;
     const int a = idx / k, b = idx % k;
@@ -282,11 +309,11 @@ void check_theta(const double* theta, int64_t n, const char* who) {
 void saddle_apply_dev(const ksvm_nfft_saddle& S, const double* vw, double* out, cudaStream_t st) {
     const long long n = S.n;
     const int nb = blocks_for(n);
-    k_mul<<<nb, kRT, 0, st>>>(S.u.p, S.y.p, vw, n);
+    launch_k(k_mul, dim3(nb), dim3(kRT), 0, st, S.u.p, S.y.p, vw, n);
     const int rc = ksvm_nfft_op_apply(S.op, S.u.p, S.kv.p, KSVM_NFFT_DEVICE, st);
     if (rc != KSVM_NFFT_OK) throw std::runtime_error(std::string("saddle apply: ") + ksvm_nfft_last_error());
-    k_saddle_post<<<nb, kRT, 0, st>>>(out, S.y.p, S.kv.p, S.theta.p, vw, n, S.partial.p);
-    k_finish_scalar<<<1, 32, 0, st>>>(S.partial.p, nb, out + n, -1.0, nullptr, 0);
+    launch_k(k_saddle_post, dim3(nb), dim3(kRT), 0, st, out, S.y.p, S.kv.p, S.theta.p, vw, n, S.partial.p);
+    launch_k(k_finish_scalar, dim3(1), dim3(32), 0, st, S.partial.p, nb, out + n, -1.0, nullptr, 0);
     launch_counter() += 4;
     CK(cudaGetLastError());
 }
@@ -301,17 +328,16 @@ void precond_apply_dev(const ksvm_nfft_precond& P, const double* g, double* out,
     if (!P.fresh) throw std::logic_error("SaddlePreconditioner: refresh() before apply()");
     const int nb = blocks_for(n);
     if (P.fallback || P.k == 0) {
-        k_diag_out<<<nb, kRT, 0, st>>>(out, g, P.y.p, P.theta.p, n, P.partial.p);
+        launch_k(k_diag_out, dim3(nb), dim3(kRT), 0, st, out, g, P.y.p, P.theta.p, n, P.partial.p);
         launch_counter() += 1;
     } else {
-        k_mdot<<<nb, kRT, 0, st>>>(P.Z.p, n, P.k, n, 1, g, P.y.p, P.theta.p, P.partial.p);
-        k_rows_finish<<<(P.k + 7) / 8, 256, 0, st>>>(P.partial.p, nb, P.k, P.s.p);
-        k_gemv_small<<<(P.k + 127) / 128, 128, 0, st>>>(P.Cinv.p, P.k, P.s.p, P.inner.p);
-        k_smw_out<<<nb, kRT, sizeof(double) * P.k, st>>>(out, g, P.y.p, P.theta.p, P.Z.p, P.k, P.inner.p, n,
-                                                          P.partial.p);
+        launch_k(k_mdot, dim3(nb), dim3(kRT), 0, st, P.Z.p, n, P.k, n, 1, g, P.y.p, P.theta.p, P.partial.p);
+        launch_k(k_rows_finish, dim3((P.k + 7) / 8), dim3(256), 0, st, P.partial.p, nb, P.k, P.s.p);
+        launch_k(k_gemv_small, dim3((P.k + 127) / 128), dim3(128), 0, st, P.Cinv.p, P.k, P.s.p, P.inner.p);
+        launch_k(k_smw_out, dim3(nb), dim3(kRT), sizeof(double) * P.k, st, out, g, P.y.p, P.theta.p, P.Z.p, P.k, P.inner.p, n, P.partial.p);
         launch_counter() += 4;
     }
-    k_finish_scalar<<<1, 32, 0, st>>>(P.partial.p, nb, out + n, -1.0, g + n, 0);
+    launch_k(k_finish_scalar, dim3(1), dim3(32), 0, st, P.partial.p, nb, out + n, -1.0, g + n, 0);
     launch_counter() += 1;
     CK(cudaGetLastError());
 }
@@ -334,8 +360,8 @@ void precond_refresh(ksvm_nfft_precond& P, const double* theta_h) {
     DevBuf<double> part, C;
     part.alloc(static_cast<size_t>(nchunks) * nt * nt * 64);
     C.alloc(static_cast<size_t>(k) * k);
-    k_cap_partial<<<dim3(nt * nt, nchunks), 32, 0, st>>>(P.Z.p, P.theta.p, k, n, chunk, nt, part.p);
-    k_cap_finish<<<(k * k + 255) / 256, 256, 0, st>>>(part.p, nchunks, nt, k, C.p);
+    launch_k(k_cap_partial, dim3(dim3(nt * nt, nchunks)), dim3(32), 0, st, P.Z.p, P.theta.p, k, n, chunk, nt, part.p);
+    launch_k(k_cap_finish, dim3((k * k + 255) / 256), dim3(256), 0, st, part.p, nchunks, nt, k, C.p);
     launch_counter() += 2;
     CK(cudaGetLastError());
     std::vector<double> cap(static_cast<size_t>(k) * k);
@@ -563,10 +589,10 @@ int ksvm_nfft_gmres_solve(const ksvm_nfft_saddle* s, const ksvm_nfft_precond* p,
         double* hp = S.pinned;
         auto norm_into = [&](const double* a, const double* b, double* dst) {  // sqrt(sum (a-b)^2) or |a|
             if (b)
-                k_sq_diff<<<nb, kRT, 0, st>>>(a, b, n1, S.partial_rows.p);
+                launch_k(k_sq_diff, dim3(nb), dim3(kRT), 0, st, a, b, n1, S.partial_rows.p);
             else
-                k_mdot<<<nb, kRT, 0, st>>>(a, n1, 1, n1, 0, a, nullptr, nullptr, S.partial_rows.p);
-            k_finish_scalar<<<1, 32, 0, st>>>(S.partial_rows.p, nb, dst, 1.0, nullptr, 1);
+                launch_k(k_mdot, dim3(nb), dim3(kRT), 0, st, a, n1, 1, n1, 0, a, nullptr, nullptr, S.partial_rows.p);
+            launch_k(k_finish_scalar, dim3(1), dim3(32), 0, st, S.partial_rows.p, nb, dst, 1.0, nullptr, 1);
             launch_counter() += 2;
         };
         // right-hand side
@@ -591,7 +617,7 @@ int ksvm_nfft_gmres_solve(const ksvm_nfft_saddle* s, const ksvm_nfft_precond* p,
             *stats = out;
             return;
         }
-        k_scale<<<nb, kRT, 0, st>>>(S.V.p, S.r.p, n1, S.scal.p);
+        launch_k(k_scale, dim3(nb), dim3(kRT), 0, st, S.V.p, S.r.p, n1, S.scal.p);
         ++launch_counter();
         std::vector<double> H(static_cast<size_t>(MI + 1) * std::max(MI, 1), 0.0);
         auto Hk = [&](int i, int j) -> double& { return H[static_cast<size_t>(i) * std::max(MI, 1) + j]; };
@@ -605,9 +631,9 @@ int ksvm_nfft_gmres_solve(const ksvm_nfft_saddle* s, const ksvm_nfft_precond* p,
             // classical Gram-Schmidt, two passes: h = V^T w; w -= V h
             for (int pass = 0; pass < 2; ++pass) {
                 double* hd = S.h.p + pass * (k + 1);
-                k_mdot<<<nb, kRT, 0, st>>>(S.V.p, n1, k + 1, n1, 0, S.w.p, nullptr, nullptr, S.partial_rows.p);
-                k_rows_finish<<<(k + 1 + 7) / 8, 256, 0, st>>>(S.partial_rows.p, nb, k + 1, hd);
-                k_combine_rows<<<nb, kRT, 0, st>>>(S.w.p, S.V.p, n1, k + 1, hd, n1, 0);
+                launch_k(k_mdot, dim3(nb), dim3(kRT), 0, st, S.V.p, n1, k + 1, n1, 0, S.w.p, nullptr, nullptr, S.partial_rows.p);
+                launch_k(k_rows_finish, dim3((k + 1 + 7) / 8), dim3(256), 0, st, S.partial_rows.p, nb, k + 1, hd);
+                launch_k(k_combine_rows, dim3(nb), dim3(kRT), 0, st, S.w.p, S.V.p, n1, k + 1, hd, n1, 0);
                 launch_counter() += 3;
             }
             norm_into(S.w.p, nullptr, S.scal.p + 1);
@@ -648,7 +674,7 @@ int ksvm_nfft_gmres_solve(const ksvm_nfft_saddle* s, const ksvm_nfft_precond* p,
                 ++k;
                 break;
             }
-            k_scale<<<nb, kRT, 0, st>>>(S.V.p + static_cast<long long>(k + 1) * n1, S.w.p, n1, S.scal.p + 1);
+            launch_k(k_scale, dim3(nb), dim3(kRT), 0, st, S.V.p + static_cast<long long>(k + 1) * n1, S.w.p, n1, S.scal.p + 1);
             ++launch_counter();
         }
         // u = V_k y_k with the upper-triangular solve, x = P^{-1} u
@@ -661,7 +687,7 @@ int ksvm_nfft_gmres_solve(const ksvm_nfft_saddle* s, const ksvm_nfft_precond* p,
             }
             std::memcpy(hp, yk.data(), sizeof(double) * k);
             CK(cudaMemcpyAsync(S.coef.p, hp, sizeof(double) * k, cudaMemcpyHostToDevice, st));
-            k_combine_rows<<<nb, kRT, 0, st>>>(S.z.p, S.V.p, n1, k, S.coef.p, n1, 1);
+            launch_k(k_combine_rows, dim3(nb), dim3(kRT), 0, st, S.z.p, S.V.p, n1, k, S.coef.p, n1, 1);
             ++launch_counter();
         } else {
             CK(cudaMemsetAsync(S.z.p, 0, sizeof(double) * n1, st));
