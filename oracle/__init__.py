@@ -328,3 +328,59 @@ def gmres_solve(K, y, theta, Z, rhs, tol, max_iter):
     it = int(st[0])
     return x, {"iterations": it, "relative_residual": float(st[1]), "converged": bool(st[2]),
                "breakdown": bool(st[3]), "residual_history": hist[:it].copy()}
+
+
+# --- greedy pivoted Cholesky (oracle/lowrank_oracle.cpp, P:src/low_rank.cpp) --
+def _lowrank_lib():
+    L = Lib("oracle").L
+    if not getattr(L, "_lowrank_bound", False):
+        L.oracle_lowrank_last_error.restype = C.c_char_p
+        L.oracle_pivoted_cholesky.restype = C.c_int
+        L.oracle_pivoted_cholesky.argtypes = [_dp, C.c_int64, C.c_int, _ip, _ip, C.c_int, _dp, _dp, C.c_int,
+                                              C.c_int, C.c_double, _dp, _ip, _dp, C.POINTER(C.c_int64)]
+        L.oracle_pivoted_cholesky_dense.restype = C.c_int
+        L.oracle_pivoted_cholesky_dense.argtypes = [_dp, C.c_int64, C.c_int, C.c_double, _dp, _ip, _dp,
+                                                    C.POINTER(C.c_int64)]
+        L._lowrank_bound = True
+    return L
+
+
+def pivoted_cholesky_dense(M, rank, err_tol=0.0):
+    """pivoted_cholesky_greedy over a DenseOperator (P:tests/helpers.hpp).
+    Returns (Z r x n, trace_residual, pivots)."""
+    L = _lowrank_lib()
+    M = np.ascontiguousarray(M, dtype=np.float64)
+    n = M.shape[0]
+    rr = max(1, min(int(rank), n))
+    Z = np.zeros(rr * n)
+    piv = np.zeros(rr, dtype=np.int64)
+    r, tr = C.c_int(0), C.c_double(0.0)
+    code = L.oracle_pivoted_cholesky_dense(_ptr(M), n, int(rank), float(err_tol), _ptr(Z), C.byref(r), C.byref(tr),
+                                           piv.ctypes.data_as(C.POINTER(C.c_int64)))
+    if code != 0:
+        raise OracleError(code, L.oracle_lowrank_last_error().decode())
+    return Z[: r.value * n].reshape(r.value, n), tr.value, piv[: r.value]
+
+
+def pivoted_cholesky(pts, windows, window=0, rank=10, err_tol=0.0, weights=None, ells=None):
+    """pivoted_cholesky_greedy over WindowOperator(window) (window >= 0) or
+    the ANOVA entries (window = -1). Returns (Z r x n, trace_residual, pivots)."""
+    L = _lowrank_lib()
+    pts = np.ascontiguousarray(pts, dtype=np.float64)
+    n, d = pts.shape
+    P = len(windows)
+    feats = np.ascontiguousarray([f for w in windows for f in w], dtype=np.int32)
+    sizes = np.ascontiguousarray([len(w) for w in windows], dtype=np.int32)
+    weights = _f64(weights if weights is not None else [1.0 / P] * P)
+    ells = _f64(ells if ells is not None else [1.0] * P)
+    rr = max(1, min(int(rank), n))
+    Z = np.zeros(rr * n)
+    piv = np.zeros(rr, dtype=np.int64)
+    r = C.c_int(0)
+    tr = C.c_double(0.0)
+    code = L.oracle_pivoted_cholesky(_ptr(pts), n, d, feats.ctypes.data_as(_ip), sizes.ctypes.data_as(_ip), P,
+                                     _ptr(weights), _ptr(ells), int(window), int(rank), float(err_tol), _ptr(Z),
+                                     C.byref(r), C.byref(tr), piv.ctypes.data_as(C.POINTER(C.c_int64)))
+    if code != 0:
+        raise OracleError(code, L.oracle_lowrank_last_error().decode())
+    return Z[: r.value * n].reshape(r.value, n), tr.value, piv[: r.value]

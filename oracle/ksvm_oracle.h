@@ -72,6 +72,18 @@ int oracle_precond_apply(const double* Z, int k, int64_t n, const double* y, con
 int oracle_gmres_solve(const oracle_anova* op, const double* dense, int64_t n, const double* y,
                        const double* theta, const double* Z, int k, const double* rhs, double tol,
                        int max_iter, double* x_out, double* stats, double* history);
+
+/* Greedy pivoted Cholesky (oracle/lowrank_oracle.cpp, restating
+ * P:src/low_rank.cpp:25-92) on exact entries: window >= 0 the
+ * WindowOperator entry of that window, -1 the weighted ANOVA entry. Z_out
+ * holds rank x n (row-major); pivots (may be NULL) the chosen indices. */
+const char* oracle_lowrank_last_error(void);
+int oracle_pivoted_cholesky(const double* pts_rowmajor, int64_t n, int d, const int* win_features,
+                            const int* win_sizes, int P, const double* weights, const double* ells,
+                            int window, int rank, double err_tol, double* Z_out, int* achieved_rank,
+                            double* trace_residual, int64_t* pivots);
+int oracle_pivoted_cholesky_dense(const double* M, int64_t n, int rank, double err_tol, double* Z_out,
+                                  int* achieved_rank, double* trace_residual, int64_t* pivots);
 void oracle_fft(const double* in, double* out, int rank, const int* dims, int sign);
 
 #ifdef __cplusplus
