@@ -32,6 +32,7 @@
  *   refresh/apply/identity/
  *   diagonal_fallback/free
  * ksvm_nfft_gmres_solve            gmres_solve              P:include/ksvm/saddle.hpp:60-77, P:src/saddle.cpp:92-178
+ * ksvm_nfft_pivoted_cholesky       pivoted_cholesky_greedy  P:include/ksvm/low_rank.hpp, P:src/low_rank.cpp:25-92
  *
  * Status values equal ksvm_status (P:capi/ksvm.h:17-23): 0 ok, 2 data/domain
  * error (DomainError, P:src/fastsum.cpp:316-320), 4 invalid argument
@@ -192,6 +193,18 @@ int ksvm_nfft_precond_apply(const ksvm_nfft_precond* p, const double* g, double*
 int ksvm_nfft_precond_identity(const ksvm_nfft_precond* p);
 int ksvm_nfft_precond_diagonal_fallback(const ksvm_nfft_precond* p);
 void ksvm_nfft_precond_free(ksvm_nfft_precond* p);
+
+/* ---- greedy pivoted Cholesky, GPU resident -----------
+ * pivoted_cholesky_greedy(op, rank, err_tol) of the exact kernel: window
+ * >= 0 factorizes that window's WindowOperator (exp(-||dx||^2/ell^2) on its
+ * raw coordinates, P:src/pipeline.cpp:103-105); window == -1 the weighted
+ * ANOVA kernel (P:src/kernel.cpp:33-48). Z receives achieved_rank x n rows
+ * (row-major; room for min(rank, n) rows), pivots (may be NULL) the chosen
+ * indices. rank < 1: status 4; a non-PSD operator: status 5 with the
+ * reference's message. */
+int ksvm_nfft_pivoted_cholesky(const ksvm_nfft_op* op, int window, int rank, double err_tol, double* Z,
+                               int* achieved_rank, double* trace_residual, int64_t* pivots, int ptr_kind,
+                               void* stream);
 
 /* residual_history: NULL or room for max_iter estimates (host). */
 int ksvm_nfft_gmres_solve(const ksvm_nfft_saddle* s, const ksvm_nfft_precond* p, const double* rhs,

@@ -8,6 +8,7 @@ package as the Python mirror of the reference's operator seam.
 from .fastsum import (AnovaFastOperator, AnovaKernelSpec, Dataset, DomainError, FastsumConfig,
                       FastsumPlan, FeatureWindowing, GaussianKernelSpec, KernelOperator,
                       anova_fast_operator, apply_fastsum, apply_fastsum_cross, plan_fastsum)
+from .lowrank import LowRankFactor, pivoted_cholesky_greedy, stack_anova_factors
 from .saddle import GmresStats, SaddleOperator, SaddlePreconditioner, gmres_solve
 
 __all__ = [
@@ -15,4 +16,5 @@ __all__ = [
     "FastsumPlan", "FeatureWindowing", "GaussianKernelSpec", "KernelOperator",
     "anova_fast_operator", "apply_fastsum", "apply_fastsum_cross", "plan_fastsum",
     "GmresStats", "SaddleOperator", "SaddlePreconditioner", "gmres_solve",
+    "LowRankFactor", "pivoted_cholesky_greedy", "stack_anova_factors",
 ]

@@ -78,6 +78,9 @@ _SIGS = {
     "ksvm_nfft_precond_diagonal_fallback": (C.c_int, [_vp]),
     "ksvm_nfft_precond_free": (None, [_vp]),
     "ksvm_nfft_gmres_solve": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_int, _vp, _vp, _vp, C.c_int, _vp]),
+    # greedy pivoted Cholesky
+    "ksvm_nfft_pivoted_cholesky": (C.c_int, [_vp, C.c_int, C.c_int, C.c_double, _vp, _ip, _dp, _vp, C.c_int,
+                                             _vp]),
 }
 
 EXPORTED = tuple(_SIGS)

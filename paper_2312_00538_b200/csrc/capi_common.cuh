@@ -7,9 +7,11 @@
 
 #include <atomic>
 #include <cstdint>
+#include <mutex>
 #include <new>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "../../include/ksvm_nfft.h"
 
@@ -91,6 +93,22 @@ struct DeviceGuard {
         if (prev != dev) CK(cudaSetDevice(dev));
     }
     ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+// Exact kernel entries of an operator's window (or of the whole ANOVA
+// kernel), for the preconditioner factorizations (lowrank.cu): the raw
+// feature columns on the device plus the per-window weights (< 0: plain
+// WindowOperator entry) and squared length scales. Filled by op_entry_view
+// (nfft_capi.cu); `mu` / `stream` are the operator's.
+struct EntryView {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::mutex* mu = nullptr;
+    int64_t n = 0;
+    int nw = 0;
+    const double* const* cols = nullptr;  // device: the windows' feature columns, in window order
+    const int* wdim = nullptr;            // device: dimension of each of the nw windows
+    std::vector<double> wgt, ell2;        // host, nw entries
 };
 
 }  // namespace ksvm_nfft

@@ -1224,6 +1224,36 @@ double ksvm_nfft_op_entry(const ksvm_nfft_op* op, int64_t i, int64_t j) {
     return sum;
 }
 
+extern "C++" {
+namespace ksvm_nfft {
+// lowrank.cu: entries of window `window` (-1: the weighted ANOVA kernel),
+// the same arithmetic as ksvm_nfft_kernel_rows.
+void op_entry_view(const ksvm_nfft_op* op, int window, EntryView& v) {
+    if (!op) throw std::invalid_argument("null operator");
+    Engine& E = const_cast<Engine&>(op->e);
+    const int P = static_cast<int>(E.wins.size());
+    if (window < -1 || window >= P) throw std::invalid_argument("window out of range");
+    int c0 = 0;
+    for (int l = 0; l < (window < 0 ? 0 : window); ++l) c0 += E.wins[static_cast<size_t>(l)]->d;
+    v.device = E.device;
+    v.stream = E.stream;
+    v.mu = &E.mu;
+    v.n = E.n;
+    v.nw = window < 0 ? P : 1;
+    v.cols = E.d_rawcols.p + c0;
+    v.wdim = E.d_wdim.p + (window < 0 ? 0 : window);
+    v.wgt.clear();
+    v.ell2.clear();
+    for (int l = 0; l < P; ++l) {
+        if (window >= 0 && l != window) continue;
+        const Window& w = *E.wins[static_cast<size_t>(l)];
+        v.wgt.push_back(window < 0 ? w.eta : -1.0);
+        v.ell2.push_back(w.ell * w.ell);
+    }
+}
+}  // namespace ksvm_nfft
+}  // extern "C++"
+
 int ksvm_nfft_kernel_rows(const ksvm_nfft_op* op, int window, const int64_t* rows, int r,
                           double* out, int ptr_kind, void* stream) {
     return guarded([&] {

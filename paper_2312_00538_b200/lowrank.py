@@ -1,0 +1,52 @@
+"""GPU greedy pivoted Cholesky: Python mirror of the
+reference's pivoted_cholesky_greedy (P:include/ksvm/low_rank.hpp,
+P:src/low_rank.cpp:25-92) on an AnovaFastOperator's exact entries.
+
+    f = pivoted_cholesky_greedy(op, rank, err_tol, window=l)   # WindowOperator(l)
+    f = pivoted_cholesky_greedy(op, rank, err_tol)             # the ANOVA kernel
+    f.Z (achieved_rank x n), f.achieved_rank, f.trace_residual, f.pivots
+
+The factor of window l is what the IPM stacks with sqrt(eta_l)
+(stack_anova_factors, P:src/low_rank.cpp:200-222) into the Z of
+SaddlePreconditioner.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .fastsum import AnovaFastOperator, _raise
+
+
+@dataclass
+class LowRankFactor:
+    """P:include/ksvm/low_rank.hpp LowRankFactor (+ the pivot sequence)."""
+    Z: np.ndarray
+    method: str
+    achieved_rank: int
+    trace_residual: float
+    pivots: np.ndarray
+
+
+def pivoted_cholesky_greedy(op: AnovaFastOperator, rank: int, err_tol: float = 0.0, window: int = -1):
+    n = op.size()
+    rr = max(1, min(int(rank), n))
+    Z = np.empty((rr, n))
+    piv = np.zeros(rr, dtype=np.int64)
+    r = C.c_int(0)
+    tr = C.c_double(0.0)
+    _raise(_lib.load().ksvm_nfft_pivoted_cholesky(op._h, int(window), int(rank), float(err_tol),
+                                                  C.c_void_p(Z.ctypes.data), C.byref(r), C.byref(tr),
+                                                  C.c_void_p(piv.ctypes.data), _lib.HOST, C.c_void_p(0)))
+    k = r.value
+    return LowRankFactor(Z[:k].copy(), "cholesky-greedy", k, tr.value, piv[:k].copy())
+
+
+def stack_anova_factors(factors, weights) -> np.ndarray:
+    """sqrt(eta_l) Z_l stacked in window order (P:src/low_rank.cpp:200-222)."""
+    if not factors or len(factors) != len(weights):
+        raise ValueError("stack_anova_factors: size mismatch")
+    return np.vstack([np.sqrt(w) * f.Z for f, w in zip(factors, weights)])
