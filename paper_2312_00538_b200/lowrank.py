@@ -31,18 +31,27 @@ class LowRankFactor:
     pivots: np.ndarray
 
 
-def pivoted_cholesky_greedy(op: AnovaFastOperator, rank: int, err_tol: float = 0.0, window: int = -1):
+def pivoted_cholesky_greedy(op: AnovaFastOperator, rank: int, err_tol: float = 0.0, window: int = -1,
+                            on_device: bool = False):
+    """on_device=True keeps Z on the operator's GPU (a CUDA torch tensor,
+    ordered on torch's current stream), e.g. for SaddlePreconditioner."""
     n = op.size()
     rr = max(1, min(int(rank), n))
-    Z = np.empty((rr, n))
     piv = np.zeros(rr, dtype=np.int64)
     r = C.c_int(0)
     tr = C.c_double(0.0)
-    _raise(_lib.load().ksvm_nfft_pivoted_cholesky(op._h, int(window), int(rank), float(err_tol),
-                                                  C.c_void_p(Z.ctypes.data), C.byref(r), C.byref(tr),
-                                                  C.c_void_p(piv.ctypes.data), _lib.HOST, C.c_void_p(0)))
+    if on_device:
+        import torch
+        Z = torch.empty((rr, n), dtype=torch.float64, device=f"cuda:{op.device}")
+        kind, stream = _lib.DEVICE, C.c_void_p(torch.cuda.current_stream(Z.device).cuda_stream)
+        zp = C.c_void_p(Z.data_ptr())
+    else:
+        Z = np.empty((rr, n))
+        kind, stream, zp = _lib.HOST, C.c_void_p(0), C.c_void_p(Z.ctypes.data)
+    _raise(_lib.load().ksvm_nfft_pivoted_cholesky(op._h, int(window), int(rank), float(err_tol), zp, C.byref(r),
+                                                  C.byref(tr), C.c_void_p(piv.ctypes.data), kind, stream))
     k = r.value
-    return LowRankFactor(Z[:k].copy(), "cholesky-greedy", k, tr.value, piv[:k].copy())
+    return LowRankFactor(Z[:k], "cholesky-greedy", k, tr.value, piv[:k].copy())
 
 
 def stack_anova_factors(factors, weights) -> np.ndarray:
