@@ -33,6 +33,7 @@
  *   diagonal_fallback/free
  * ksvm_nfft_gmres_solve            gmres_solve              P:include/ksvm/saddle.hpp:60-77, P:src/saddle.cpp:92-178
  * ksvm_nfft_pivoted_cholesky       pivoted_cholesky_greedy  P:include/ksvm/low_rank.hpp, P:src/low_rank.cpp:25-92
+ * ksvm_nfft_decision_values        TrainedModel::decision_values  P:include/ksvm/ipm.hpp:51-69, P:src/ipm.cpp:213-288
  *
  * Status values equal ksvm_status (P:capi/ksvm.h:17-23): 0 ok, 2 data/domain
  * error (DomainError, P:src/fastsum.cpp:316-320), 4 invalid argument
@@ -205,6 +206,25 @@ void ksvm_nfft_precond_free(ksvm_nfft_precond* p);
 int ksvm_nfft_pivoted_cholesky(const ksvm_nfft_op* op, int window, int rank, double err_tol, double* Z,
                                int* achieved_rank, double* trace_residual, int64_t* pivots, int ptr_kind,
                                void* stream);
+
+/* ---- prediction, GPU -----------------------------------
+ * TrainedModel::decision_values (P:src/ipm.cpp:213-288): f_j = sum_i coeff_i
+ * K(x_i, t_j) + bias for the t test points, coeff = alpha .* y. Backend FAST
+ * builds one plan per window over the training points (fit 1/1.2, :258),
+ * evaluates the targets whose scaled norm is <= r_T by the cross transform
+ * and recomputes the others exactly (:261-284); EXACT sums every target
+ * directly (:236-239). Points are already normalized (the reference applies
+ * the model's z-score first, :216-218); layout / ld as in plan_create, the
+ * same layout for train and test. n_exact (may be NULL) returns how many
+ * targets took the exact path. Host arrays. */
+#define KSVM_NFFT_PREDICT_EXACT 0
+#define KSVM_NFFT_PREDICT_FAST 1
+int ksvm_nfft_decision_values(const double* train, int64_t n, int d, int64_t ld_train, int layout,
+                              const int* window_features, const int* window_sizes, int P,
+                              const double* weights, const double* length_scales,
+                              const ksvm_nfft_config* cfg, const double* coeff, double bias,
+                              const double* test, int64_t t, int64_t ld_test, int backend, int device,
+                              double* f_out, int64_t* n_exact);
 
 /* residual_history: NULL or room for max_iter estimates (host). */
 int ksvm_nfft_gmres_solve(const ksvm_nfft_saddle* s, const ksvm_nfft_precond* p, const double* rhs,

@@ -384,3 +384,43 @@ def pivoted_cholesky(pts, windows, window=0, rank=10, err_tol=0.0, weights=None,
     if code != 0:
         raise OracleError(code, L.oracle_lowrank_last_error().decode())
     return Z[: r.value * n].reshape(r.value, n), tr.value, piv[: r.value]
+
+
+# --- prediction (P:src/ipm.cpp:213-288, TrainedModel::decision_values) -------
+def decision_values(train, windows, weights, ells, coeff, bias, test, fast=True, N=32, m=4, sigma=2,
+                    torus_radius=0.25, kind="oracle"):
+    """Restatement of decision_values on the oracle's (or the reference
+    build's, kind="ref") plans: kFast per-window cross transforms over
+    targets with ||scaled|| <= r_T, exact sums for the rest; kExact all
+    exact (anova_eval, P:src/kernel.cpp:15-29). Returns (f + bias, #exact)."""
+    lib = Lib(kind)
+    train = np.asarray(train, dtype=np.float64)
+    test = np.asarray(test, dtype=np.float64)
+    coeff = _f64(coeff)
+    t = test.shape[0]
+    f = np.zeros(t)
+    offending = np.full(t, not fast)
+    if fast:
+        for l, win in enumerate(windows):
+            plan = lib.plan(train[:, win], ells[l], N, m, sigma, torus_radius, 1.0 / 1.2)
+            sc = plan.scale_points(test[:, win])
+            ok = np.sqrt((sc * sc).sum(axis=1)) <= torus_radius
+            offending |= ~ok
+            if ok.any():
+                part = plan.apply_cross(test[ok][:, win], coeff)
+                f[np.nonzero(ok)[0]] += weights[l] * part
+    redo = np.nonzero(offending)[0]
+    for j in redo:  # exact_rows: acc += coeff_i * anova_eval(x_i, t_j)
+        acc = 0.0
+        x = test[j]
+        for i in range(train.shape[0]):
+            s = 0.0
+            for l, win in enumerate(windows):
+                d2 = 0.0
+                for fidx in win:
+                    diff = train[i, fidx] - x[fidx]
+                    d2 += diff * diff
+                s += weights[l] * np.exp(-d2 / (ells[l] * ells[l]))
+            acc += coeff[i] * s
+        f[j] = acc
+    return f + bias, len(redo)

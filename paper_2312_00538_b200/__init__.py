@@ -7,14 +7,15 @@ package as the Python mirror of the reference's operator seam.
 """
 from .fastsum import (AnovaFastOperator, AnovaKernelSpec, Dataset, DomainError, FastsumConfig,
                       FastsumPlan, FeatureWindowing, GaussianKernelSpec, KernelOperator,
-                      anova_fast_operator, apply_fastsum, apply_fastsum_cross, plan_fastsum)
+                      anova_fast_operator, apply_fastsum, apply_fastsum_cross, decision_values,
+                      plan_fastsum)
 from .lowrank import LowRankFactor, pivoted_cholesky_greedy, stack_anova_factors
 from .saddle import GmresStats, SaddleOperator, SaddlePreconditioner, gmres_solve
 
 __all__ = [
     "AnovaFastOperator", "AnovaKernelSpec", "Dataset", "DomainError", "FastsumConfig",
     "FastsumPlan", "FeatureWindowing", "GaussianKernelSpec", "KernelOperator",
-    "anova_fast_operator", "apply_fastsum", "apply_fastsum_cross", "plan_fastsum",
+    "anova_fast_operator", "apply_fastsum", "apply_fastsum_cross", "decision_values", "plan_fastsum",
     "GmresStats", "SaddleOperator", "SaddlePreconditioner", "gmres_solve",
     "LowRankFactor", "pivoted_cholesky_greedy", "stack_anova_factors",
 ]

@@ -16,6 +16,7 @@ OK, ERR_DATA, ERR_CONFIG, ERR_INTERNAL = 0, 2, 4, 5
 ROW_MAJOR, COL_MAJOR = 0, 1
 HOST, DEVICE = 0, 1
 FP64 = 0
+PREDICT_EXACT, PREDICT_FAST = 0, 1
 
 
 class GmresStats(C.Structure):
@@ -78,6 +79,10 @@ _SIGS = {
     "ksvm_nfft_precond_diagonal_fallback": (C.c_int, [_vp]),
     "ksvm_nfft_precond_free": (None, [_vp]),
     "ksvm_nfft_gmres_solve": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_int, _vp, _vp, _vp, C.c_int, _vp]),
+    # prediction
+    "ksvm_nfft_decision_values": (C.c_int, [_vp, C.c_int64, C.c_int, C.c_int64, C.c_int, _vp, _vp, C.c_int, _vp,
+                                            _vp, C.POINTER(Config), _vp, C.c_double, _vp, C.c_int64, C.c_int64,
+                                            C.c_int, C.c_int, _vp, _vp]),
     # greedy pivoted Cholesky
     "ksvm_nfft_pivoted_cholesky": (C.c_int, [_vp, C.c_int, C.c_int, C.c_double, _vp, _ip, _dp, _vp, C.c_int,
                                              _vp]),

@@ -392,3 +392,38 @@ def anova_fast_operator(data, spec: AnovaKernelSpec, cfg: Optional[FastsumConfig
                         fit_fraction: float = 1.0, device: int = 0, window_mask=None) -> AnovaFastOperator:
     """anova_fast_operator (P:src/fastsum.cpp:366-371) on cuda:`device`."""
     return AnovaFastOperator(data, spec, cfg, fit_fraction, device, window_mask)
+
+
+# ---- prediction (SURVEY.md 8(f)4) -------------------------------------------
+
+def decision_values(train, spec: AnovaKernelSpec, coeff, bias: float, test, backend: str = "fast",
+                    cfg: FastsumConfig = None, device: int = 0):
+    """TrainedModel::decision_values (P:src/ipm.cpp:213-288) on the GPU:
+    f = K(test, train) coeff + bias with coeff = alpha .* y; backend "fast"
+    (per-window cross transforms, exact fallback outside the torus ball) or
+    "exact". Points must already be normalized like the model's training
+    data. Returns (f, number of targets evaluated exactly)."""
+    tr = _host_matrix(train)
+    te = _host_matrix(test)
+    n, d = tr.shape
+    if te.shape[1] != d:
+        raise ValueError("predict: feature dimension mismatch")  # P:src/ipm.cpp:215-216
+    w = spec.windowing
+    feats = (C.c_int * max(1, sum(len(x) for x in w.windows)))(*[f for x in w.windows for f in x])
+    sizes = (C.c_int * len(w.windows))(*[len(x) for x in w.windows])
+    eta = np.ascontiguousarray(w.weights, dtype=np.float64)
+    ell = np.ascontiguousarray(w.length_scales, dtype=np.float64)
+    co = np.ascontiguousarray(np.asarray(coeff, dtype=np.float64).reshape(-1))
+    if co.shape[0] != n:
+        raise ValueError("coeff length mismatch")
+    t = te.shape[0]
+    out = np.empty(t)
+    nex = C.c_int64(0)
+    c = (cfg or FastsumConfig())._c()
+    kind = {"fast": _lib.PREDICT_FAST, "exact": _lib.PREDICT_EXACT}[backend]
+    _raise(_lib.load().ksvm_nfft_decision_values(C.c_void_p(tr.ctypes.data), n, d, d, _lib.ROW_MAJOR, feats, sizes,
+                                                 len(w.windows), C.c_void_p(eta.ctypes.data),
+                                                 C.c_void_p(ell.ctypes.data), C.byref(c), C.c_void_p(co.ctypes.data),
+                                                 float(bias), C.c_void_p(te.ctypes.data), t, d, kind, int(device),
+                                                 C.c_void_p(out.ctypes.data), C.byref(nex)))
+    return out, int(nex.value)
