@@ -76,6 +76,11 @@ def test_apply_batch_equals_single_applies():
     Y = op.apply_batch(V)
     for c in range(5):
         assert np.array_equal(Y[:, c], op.apply(V[:, c]))
+    import torch
+    Yd = op.apply_batch(torch.from_numpy(V).cuda())
+    torch.cuda.synchronize()
+    assert np.array_equal(Yd.cpu().numpy(), Y)
+    assert op.apply_batch(np.zeros((V.shape[0], 0))).shape == (V.shape[0], 0)
 
 
 def test_edge_cases():
