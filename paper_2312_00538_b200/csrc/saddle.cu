@@ -60,9 +60,11 @@ __device__ __forceinline__ void block_partial(double v, double* partial) {
     for (long long i = static_cast<long long>(blockIdx.x) * kRT + threadIdx.x; i < (L); i += static_cast<long long>(kRB) * kRT)
 
 __global__ void __launch_bounds__(kRT) k_mul(double* __restrict__ out, const double* __restrict__ a,
-                                             const double* __restrict__ b, long long n) {
+                                             const double* __restrict__ b, long long n,
+        const int* __restrict__ stop) {
     pdl_trigger();
     pdl_wait();
+    if (stop && *stop) return;  // GMRES look-ahead past convergence
     KSVM_FOR_BLOCK_INDEX(j, n) out[j] = a[j] * b[j];
 }
 
@@ -70,9 +72,11 @@ __global__ void __launch_bounds__(kRT) k_mul(double* __restrict__ out, const dou
 __global__ void __launch_bounds__(kRT) k_saddle_post(double* __restrict__ out, const double* __restrict__ y,
                                                      const double* __restrict__ kv, const double* __restrict__ theta,
                                                      const double* __restrict__ vw, long long n,
-                                                     double* __restrict__ partial) {
+                                                     double* __restrict__ partial,
+        const int* __restrict__ stop) {
     pdl_trigger();
     pdl_wait();
+    if (stop && *stop) return;  // GMRES look-ahead past convergence
     const double w = vw[n];
     double acc = 0.0;
     KSVM_FOR_BLOCK_INDEX(j, n) {
@@ -85,9 +89,11 @@ __global__ void __launch_bounds__(kRT) k_saddle_post(double* __restrict__ out, c
 
 // *dst = coef * sum(partial) - (sub ? *sub : 0), or sqrt(sum) when root.
 __global__ void k_finish_scalar(const double* __restrict__ partial, int nb, double* __restrict__ dst, double coef,
-                                const double* __restrict__ sub, int root) {
+                                const double* __restrict__ sub, int root,
+        const int* __restrict__ stop) {
     pdl_trigger();
     pdl_wait();
+    if (stop && *stop) return;  // GMRES look-ahead past convergence
     double s = 0.0;
     for (int b = threadIdx.x; b < nb; b += 32) s += partial[b];
     s = warp_sum(s);
@@ -98,9 +104,11 @@ __global__ void k_finish_scalar(const double* __restrict__ partial, int nb, doub
 // x_i = w_i (mode 0) or y_i g_i / theta_i (mode 1, P:src/saddle.cpp:80).
 __global__ void __launch_bounds__(kRT) k_mdot(const double* __restrict__ M, long long ld, int rows, long long L,
                                               int mode, const double* __restrict__ w, const double* __restrict__ y,
-                                              const double* __restrict__ theta, double* __restrict__ partial) {
+                                              const double* __restrict__ theta, double* __restrict__ partial,
+        const int* __restrict__ stop) {
     pdl_trigger();
     pdl_wait();
+    if (stop && *stop) return;  // GMRES look-ahead past convergence
     __shared__ double sh[kRT / 32][kRows];
     for (int a0 = 0; a0 < rows; a0 += kRows) {
         double acc[kRows];
@@ -129,9 +137,11 @@ __global__ void __launch_bounds__(kRT) k_mdot(const double* __restrict__ M, long
 }
 
 // out[a] = sum_b partial[b * rows + a] (one warp per row).
-__global__ void k_rows_finish(const double* __restrict__ partial, int nb, int rows, double* __restrict__ out) {
+__global__ void k_rows_finish(const double* __restrict__ partial, int nb, int rows, double* __restrict__ out,
+        const int* __restrict__ stop) {
     pdl_trigger();
     pdl_wait();
+    if (stop && *stop) return;  // GMRES look-ahead past convergence
     const int a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (a >= rows) return;
     double s = 0.0;
@@ -142,9 +152,11 @@ __global__ void k_rows_finish(const double* __restrict__ partial, int nb, int ro
 
 // inner = Cinv s (k x k, k <= kMaxRank)
 __global__ void k_gemv_small(const double* __restrict__ Cinv, int k, const double* __restrict__ s,
-                             double* __restrict__ inner) {
+                             double* __restrict__ inner,
+        const int* __restrict__ stop) {
     pdl_trigger();
     pdl_wait();
+    if (stop && *stop) return;  // GMRES look-ahead past convergence
     const int a = blockIdx.x * blockDim.x + threadIdx.x;
     if (a >= k) return;
     double acc = 0.0;
@@ -156,9 +168,11 @@ __global__ void k_gemv_small(const double* __restrict__ Cinv, int k, const doubl
 __global__ void __launch_bounds__(kRT) k_smw_out(double* __restrict__ out, const double* __restrict__ g,
                                                  const double* __restrict__ y, const double* __restrict__ theta,
                                                  const double* __restrict__ Z, int k, const double* __restrict__ inner,
-                                                 long long n, double* __restrict__ partial) {
+                                                 long long n, double* __restrict__ partial,
+        const int* __restrict__ stop) {
     pdl_trigger();
     pdl_wait();
+    if (stop && *stop) return;  // GMRES look-ahead past convergence
     extern __shared__ double s_inner[];
     for (int a = threadIdx.x; a < k; a += blockDim.x) s_inner[a] = inner[a];
     __syncthreads();
@@ -176,9 +190,11 @@ __global__ void __launch_bounds__(kRT) k_smw_out(double* __restrict__ out, const
 // P:src/saddle.cpp:74-75 (fallback / rank 0): x1 = g / theta
 __global__ void __launch_bounds__(kRT) k_diag_out(double* __restrict__ out, const double* __restrict__ g,
                                                   const double* __restrict__ y, const double* __restrict__ theta,
-                                                  long long n, double* __restrict__ partial) {
+                                                  long long n, double* __restrict__ partial,
+        const int* __restrict__ stop) {
     pdl_trigger();
     pdl_wait();
+    if (stop && *stop) return;  // GMRES look-ahead past convergence
     double acc = 0.0;
     KSVM_FOR_BLOCK_INDEX(j, n) {
         const double x1 = g[j] / theta[j];
@@ -191,9 +207,11 @@ __global__ void __launch_bounds__(kRT) k_diag_out(double* __restrict__ out, cons
 // mode 0: w_i -= sum_a V[a][i] c[a]; mode 1: w_i = sum_a V[a][i] c[a]
 __global__ void __launch_bounds__(kRT) k_combine_rows(double* __restrict__ w, const double* __restrict__ V,
                                                       long long ld, int rows, const double* __restrict__ c,
-                                                      long long L, int mode) {
+                                                      long long L, int mode,
+        const int* __restrict__ stop) {
     pdl_trigger();
     pdl_wait();
+    if (stop && *stop) return;  // GMRES look-ahead past convergence
     KSVM_FOR_BLOCK_INDEX(i, L) {
         double s = 0.0;
         for (int a = 0; a < rows; ++a) s += V[static_cast<long long>(a) * ld + i] * c[a];
@@ -202,9 +220,11 @@ __global__ void __launch_bounds__(kRT) k_combine_rows(double* __restrict__ w, co
 }
 
 __global__ void __launch_bounds__(kRT) k_scale(double* __restrict__ dst, const double* __restrict__ src, long long L,
-                                               const double* __restrict__ denom) {
+                                               const double* __restrict__ denom,
+        const int* __restrict__ stop) {
     pdl_trigger();
     pdl_wait();
+    if (stop && *stop) return;  // GMRES look-ahead past convergence
     const double d = *denom;
     KSVM_FOR_BLOCK_INDEX(i, L) dst[i] = src[i] / d;
 }
@@ -260,6 +280,58 @@ __global__ void k_cap_finish(const double* __restrict__ partial, int nchunks, in
     C[idx] = (a == b ? 1.0 : 0.0) + s;
 }
 
+// One GMRES step's Givens update on the device (P:src/saddle.cpp:127-163),
+// so the host can enqueue iterations ahead instead of waiting for each
+// Hessenberg column: H(:,k) = h1 + h2, H(k+1,k) = hnext, stored rotations,
+// new rotation, beta, the relative residual estimate and the stop rules.
+// stat = {stop, iterations, converged, breakdown, kfinal}.
+__global__ void k_givens(int k, int MI, const double* __restrict__ h, const double* __restrict__ hnext_p,
+                         double rhs_norm, double tol, double* __restrict__ H, double* __restrict__ cs,
+                         double* __restrict__ sn, double* __restrict__ beta, double* __restrict__ hist,
+                         int* __restrict__ stat) {
+    pdl_trigger();
+    pdl_wait();
+    if (threadIdx.x != 0 || stat[0]) return;
+    auto Hk = [&](int i, int j) -> double& { return H[static_cast<long long>(i) * MI + j]; };
+    for (int i = 0; i <= k; ++i) Hk(i, k) = h[i] + h[k + 1 + i];
+    const double hnext = *hnext_p;
+    Hk(k + 1, k) = hnext;
+    for (int i = 0; i < k; ++i) {
+        const double tmp = cs[i] * Hk(i, k) + sn[i] * Hk(i + 1, k);
+        Hk(i + 1, k) = -sn[i] * Hk(i, k) + cs[i] * Hk(i + 1, k);
+        Hk(i, k) = tmp;
+    }
+    const double denom = hypot(Hk(k, k), Hk(k + 1, k));
+    if (denom == 0.0) {
+        stat[3] = 1;
+        stat[0] = 1;
+        stat[4] = k;
+        return;
+    }
+    cs[k] = Hk(k, k) / denom;
+    sn[k] = Hk(k + 1, k) / denom;
+    Hk(k, k) = denom;
+    Hk(k + 1, k) = 0.0;
+    beta[k + 1] = -sn[k] * beta[k];
+    beta[k] = cs[k] * beta[k];
+    const double rel = fabs(beta[k + 1]) / rhs_norm;
+    hist[stat[1]] = rel;
+    stat[1] += 1;
+    if (rel <= tol) {
+        stat[2] = 1;
+        stat[0] = 1;
+        stat[4] = k + 1;
+    } else if (hnext <= 1e-14 * rhs_norm) {  // happy breakdown
+        stat[3] = 1;
+        stat[2] = 1;
+        stat[0] = 1;
+        stat[4] = k + 1;
+    } else if (k + 1 == MI) {
+        stat[0] = 1;
+        stat[4] = MI;
+    }
+}
+
 int blocks_for(long long L) { return static_cast<int>(std::min<long long>(kRB, (L + kRT - 1) / kRT)); }
 
 }  // namespace
@@ -277,6 +349,8 @@ struct ksvm_nfft_saddle {
     // GMRES workspace, reused while max_iter does not grow
     int ws_iter = -1;
     DevBuf<double> V, z, w, x, r, ax, h, coef, partial_rows, scal;
+    DevBuf<double> gH, gcs, gsn, gbeta, ghist;  // device-side Givens state (k_givens)
+    DevBuf<int> gstat;                          // {stop, iterations, converged, breakdown, kfinal}
     double* pinned = nullptr;
     ~ksvm_nfft_saddle() {
         if (pinned) cudaFreeHost(pinned);
@@ -306,20 +380,22 @@ void check_theta(const double* theta, int64_t n, const char* who) {
 }
 
 // out = A vw (device vectors of length n + 1), P:src/saddle.cpp:22-33
-void saddle_apply_dev(const ksvm_nfft_saddle& S, const double* vw, double* out, cudaStream_t st) {
+void saddle_apply_dev(const ksvm_nfft_saddle& S, const double* vw, double* out, cudaStream_t st,
+                      const int* stop = nullptr) {
     const long long n = S.n;
     const int nb = blocks_for(n);
-    launch_k(k_mul, dim3(nb), dim3(kRT), 0, st, S.u.p, S.y.p, vw, n);
+    launch_k(k_mul, dim3(nb), dim3(kRT), 0, st, S.u.p, S.y.p, vw, n, stop);
     const int rc = ksvm_nfft_op_apply(S.op, S.u.p, S.kv.p, KSVM_NFFT_DEVICE, st);
     if (rc != KSVM_NFFT_OK) throw std::runtime_error(std::string("saddle apply: ") + ksvm_nfft_last_error());
-    launch_k(k_saddle_post, dim3(nb), dim3(kRT), 0, st, out, S.y.p, S.kv.p, S.theta.p, vw, n, S.partial.p);
-    launch_k(k_finish_scalar, dim3(1), dim3(32), 0, st, S.partial.p, nb, out + n, -1.0, nullptr, 0);
+    launch_k(k_saddle_post, dim3(nb), dim3(kRT), 0, st, out, S.y.p, S.kv.p, S.theta.p, vw, n, S.partial.p, stop);
+    launch_k(k_finish_scalar, dim3(1), dim3(32), 0, st, S.partial.p, nb, out + n, -1.0, nullptr, 0, stop);
     launch_counter() += 4;
     CK(cudaGetLastError());
 }
 
 // out = P^{-1} g (device vectors of length n + 1), P:src/saddle.cpp:65-90
-void precond_apply_dev(const ksvm_nfft_precond& P, const double* g, double* out, cudaStream_t st) {
+void precond_apply_dev(const ksvm_nfft_precond& P, const double* g, double* out, cudaStream_t st,
+                       const int* stop = nullptr) {
     const long long n = P.n;
     if (P.identity) {
         CK(cudaMemcpyAsync(out, g, sizeof(double) * (n + 1), cudaMemcpyDeviceToDevice, st));
@@ -328,16 +404,16 @@ void precond_apply_dev(const ksvm_nfft_precond& P, const double* g, double* out,
     if (!P.fresh) throw std::logic_error("SaddlePreconditioner: refresh() before apply()");
     const int nb = blocks_for(n);
     if (P.fallback || P.k == 0) {
-        launch_k(k_diag_out, dim3(nb), dim3(kRT), 0, st, out, g, P.y.p, P.theta.p, n, P.partial.p);
+        launch_k(k_diag_out, dim3(nb), dim3(kRT), 0, st, out, g, P.y.p, P.theta.p, n, P.partial.p, stop);
         launch_counter() += 1;
     } else {
-        launch_k(k_mdot, dim3(nb), dim3(kRT), 0, st, P.Z.p, n, P.k, n, 1, g, P.y.p, P.theta.p, P.partial.p);
-        launch_k(k_rows_finish, dim3((P.k + 7) / 8), dim3(256), 0, st, P.partial.p, nb, P.k, P.s.p);
-        launch_k(k_gemv_small, dim3((P.k + 127) / 128), dim3(128), 0, st, P.Cinv.p, P.k, P.s.p, P.inner.p);
-        launch_k(k_smw_out, dim3(nb), dim3(kRT), sizeof(double) * P.k, st, out, g, P.y.p, P.theta.p, P.Z.p, P.k, P.inner.p, n, P.partial.p);
+        launch_k(k_mdot, dim3(nb), dim3(kRT), 0, st, P.Z.p, n, P.k, n, 1, g, P.y.p, P.theta.p, P.partial.p, stop);
+        launch_k(k_rows_finish, dim3((P.k + 7) / 8), dim3(256), 0, st, P.partial.p, nb, P.k, P.s.p, stop);
+        launch_k(k_gemv_small, dim3((P.k + 127) / 128), dim3(128), 0, st, P.Cinv.p, P.k, P.s.p, P.inner.p, stop);
+        launch_k(k_smw_out, dim3(nb), dim3(kRT), sizeof(double) * P.k, st, out, g, P.y.p, P.theta.p, P.Z.p, P.k, P.inner.p, n, P.partial.p, stop);
         launch_counter() += 4;
     }
-    launch_k(k_finish_scalar, dim3(1), dim3(32), 0, st, P.partial.p, nb, out + n, -1.0, g + n, 0);
+    launch_k(k_finish_scalar, dim3(1), dim3(32), 0, st, P.partial.p, nb, out + n, -1.0, g + n, 0, stop);
     launch_counter() += 1;
     CK(cudaGetLastError());
 }
@@ -566,15 +642,21 @@ int ksvm_nfft_gmres_solve(const ksvm_nfft_saddle* s, const ksvm_nfft_precond* p,
         DeviceGuard dg(S.device);
         cudaStream_t st = pick_stream(ptr_kind, stream, S.stream);
         const long long n1 = S.n + 1;
-        const int MI = max_iter;
+        const int MI = max_iter, MIc = std::max(MI, 1);
         if (S.ws_iter < MI) {
             S.V.alloc(static_cast<size_t>(MI + 1) * n1);
             S.h.alloc(static_cast<size_t>(2 * (MI + 1) + 2));
             S.coef.alloc(static_cast<size_t>(MI + 1));
             S.partial_rows.alloc(static_cast<size_t>(kRB) * (MI + 1));
+            S.gH.alloc(static_cast<size_t>(MI + 1) * MIc);
+            S.gcs.alloc(static_cast<size_t>(MIc));
+            S.gsn.alloc(static_cast<size_t>(MIc));
+            S.gbeta.alloc(static_cast<size_t>(MI + 1));
+            S.ghist.alloc(static_cast<size_t>(MIc));
+            S.gstat.alloc(8);
             if (S.pinned) cudaFreeHost(S.pinned);
             S.pinned = nullptr;
-            CK(cudaMallocHost(&S.pinned, sizeof(double) * (2 * (MI + 1) + 4)));
+            CK(cudaMallocHost(&S.pinned, sizeof(double) * (static_cast<size_t>(MI + 1) * MIc + 2 * MIc + 16)));
             S.ws_iter = MI;
         }
         if (S.z.n < static_cast<size_t>(n1)) {
@@ -587,20 +669,23 @@ int ksvm_nfft_gmres_solve(const ksvm_nfft_saddle* s, const ksvm_nfft_precond* p,
         }
         const int nb = blocks_for(n1);
         double* hp = S.pinned;
-        auto norm_into = [&](const double* a, const double* b, double* dst) {  // sqrt(sum (a-b)^2) or |a|
+        const int* nostop = nullptr;
+        auto norm_into = [&](const double* a, const double* b, double* dst, const int* stop) {  // |a - b| or |a|
             if (b)
                 launch_k(k_sq_diff, dim3(nb), dim3(kRT), 0, st, a, b, n1, S.partial_rows.p);
             else
-                launch_k(k_mdot, dim3(nb), dim3(kRT), 0, st, a, n1, 1, n1, 0, a, nullptr, nullptr, S.partial_rows.p);
-            launch_k(k_finish_scalar, dim3(1), dim3(32), 0, st, S.partial_rows.p, nb, dst, 1.0, nullptr, 1);
+                launch_k(k_mdot, dim3(nb), dim3(kRT), 0, st, a, n1, 1, n1, 0, a, nullptr, nullptr, S.partial_rows.p,
+                         stop);
+            launch_k(k_finish_scalar, dim3(1), dim3(32), 0, st, static_cast<const double*>(S.partial_rows.p), nb, dst,
+                     1.0, nullptr, 1, stop);
             launch_counter() += 2;
         };
-        // right-hand side
+        // right-hand side and its norm
         if (ptr_kind == KSVM_NFFT_HOST)
             CK(cudaMemcpyAsync(S.r.p, rhs, sizeof(double) * n1, cudaMemcpyHostToDevice, st));
         else
             CK(cudaMemcpyAsync(S.r.p, rhs, sizeof(double) * n1, cudaMemcpyDeviceToDevice, st));
-        norm_into(S.r.p, nullptr, S.scal.p);
+        norm_into(S.r.p, nullptr, S.scal.p, nostop);
         CK(cudaMemcpyAsync(hp, S.scal.p, sizeof(double), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         const double rhs_norm = hp[0];
@@ -617,88 +702,91 @@ int ksvm_nfft_gmres_solve(const ksvm_nfft_saddle* s, const ksvm_nfft_precond* p,
             *stats = out;
             return;
         }
-        launch_k(k_scale, dim3(nb), dim3(kRT), 0, st, S.V.p, S.r.p, n1, S.scal.p);
+        launch_k(k_scale, dim3(nb), dim3(kRT), 0, st, S.V.p, static_cast<const double*>(S.r.p), n1,
+                 static_cast<const double*>(S.scal.p), nostop);
         ++launch_counter();
-        std::vector<double> H(static_cast<size_t>(MI + 1) * std::max(MI, 1), 0.0);
-        auto Hk = [&](int i, int j) -> double& { return H[static_cast<size_t>(i) * std::max(MI, 1) + j]; };
-        std::vector<double> cs(static_cast<size_t>(std::max(MI, 1)), 0.0), sn(cs), beta(static_cast<size_t>(MI) + 1, 0.0);
-        beta[0] = rhs_norm;
-        int k = 0;
-        for (; k < MI; ++k) {
+        // device-side Hessenberg / Givens state
+        CK(cudaMemsetAsync(S.gH.p, 0, sizeof(double) * S.gH.n, st));
+        CK(cudaMemsetAsync(S.gcs.p, 0, sizeof(double) * S.gcs.n, st));
+        CK(cudaMemsetAsync(S.gsn.p, 0, sizeof(double) * S.gsn.n, st));
+        CK(cudaMemsetAsync(S.gbeta.p, 0, sizeof(double) * S.gbeta.n, st));
+        CK(cudaMemsetAsync(S.gstat.p, 0, sizeof(int) * 8, st));
+        CK(cudaMemcpyAsync(S.gbeta.p, &rhs_norm, sizeof(double), cudaMemcpyHostToDevice, st));
+        if (MI == 0) {
+            const int st0[5] = {1, 0, 0, 0, 0};
+            CK(cudaMemcpyAsync(S.gstat.p, st0, sizeof(st0), cudaMemcpyHostToDevice, st));
+        }
+        // Iterations are enqueued ahead (kLookAhead per host check); once
+        // k_givens sets stop, every later loop kernel returns at once, so
+        // the look-ahead only costs the matvec graphs it launched.
+        constexpr int kLookAhead = 4;
+        const int* stop = S.gstat.p;
+        int* hstat = reinterpret_cast<int*>(hp + static_cast<size_t>(MI + 1) * MIc + 2 * MIc);
+        for (int k = 0; k < MI; ++k) {
             const double* vk = S.V.p + static_cast<long long>(k) * n1;
-            precond_apply_dev(P, vk, S.z.p, st);
-            saddle_apply_dev(S, S.z.p, S.w.p, st);
+            precond_apply_dev(P, vk, S.z.p, st, stop);
+            saddle_apply_dev(S, S.z.p, S.w.p, st, stop);
             // classical Gram-Schmidt, two passes: h = V^T w; w -= V h
             for (int pass = 0; pass < 2; ++pass) {
                 double* hd = S.h.p + pass * (k + 1);
-                launch_k(k_mdot, dim3(nb), dim3(kRT), 0, st, S.V.p, n1, k + 1, n1, 0, S.w.p, nullptr, nullptr, S.partial_rows.p);
-                launch_k(k_rows_finish, dim3((k + 1 + 7) / 8), dim3(256), 0, st, S.partial_rows.p, nb, k + 1, hd);
-                launch_k(k_combine_rows, dim3(nb), dim3(kRT), 0, st, S.w.p, S.V.p, n1, k + 1, hd, n1, 0);
+                launch_k(k_mdot, dim3(nb), dim3(kRT), 0, st, static_cast<const double*>(S.V.p), n1, k + 1, n1, 0,
+                         static_cast<const double*>(S.w.p), nullptr, nullptr, S.partial_rows.p, stop);
+                launch_k(k_rows_finish, dim3((k + 1 + 7) / 8), dim3(256), 0, st,
+                         static_cast<const double*>(S.partial_rows.p), nb, k + 1, hd, stop);
+                launch_k(k_combine_rows, dim3(nb), dim3(kRT), 0, st, S.w.p, static_cast<const double*>(S.V.p), n1,
+                         k + 1, static_cast<const double*>(hd), n1, 0, stop);
                 launch_counter() += 3;
             }
-            norm_into(S.w.p, nullptr, S.scal.p + 1);
-            CK(cudaMemcpyAsync(hp, S.h.p, sizeof(double) * 2 * (k + 1), cudaMemcpyDeviceToHost, st));
-            CK(cudaMemcpyAsync(hp + 2 * (k + 1), S.scal.p + 1, sizeof(double), cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            for (int i = 0; i <= k; ++i) Hk(i, k) = hp[i] + hp[k + 1 + i];
-            const double hnext = hp[2 * (k + 1)];
-            Hk(k + 1, k) = hnext;
-            for (int i = 0; i < k; ++i) {  // stored Givens rotations
-                const double tmp = cs[static_cast<size_t>(i)] * Hk(i, k) + sn[static_cast<size_t>(i)] * Hk(i + 1, k);
-                Hk(i + 1, k) = -sn[static_cast<size_t>(i)] * Hk(i, k) + cs[static_cast<size_t>(i)] * Hk(i + 1, k);
-                Hk(i, k) = tmp;
+            norm_into(S.w.p, nullptr, S.scal.p + 1, stop);
+            launch_k(k_givens, dim3(1), dim3(32), 0, st, k, MI, static_cast<const double*>(S.h.p),
+                     static_cast<const double*>(S.scal.p + 1), rhs_norm, tol, S.gH.p, S.gcs.p, S.gsn.p, S.gbeta.p,
+                     S.ghist.p, S.gstat.p);
+            launch_k(k_scale, dim3(nb), dim3(kRT), 0, st, S.V.p + static_cast<long long>(k + 1) * n1,
+                     static_cast<const double*>(S.w.p), n1, static_cast<const double*>(S.scal.p + 1), stop);
+            launch_counter() += 2;
+            if ((k + 1) % kLookAhead == 0 && k + 1 < MI) {
+                CK(cudaMemcpyAsync(hstat, S.gstat.p, sizeof(int) * 8, cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                if (hstat[0]) break;
             }
-            const double denom = std::hypot(Hk(k, k), Hk(k + 1, k));
-            if (denom == 0.0) {
-                out.breakdown = 1;
-                break;
-            }
-            const size_t K = static_cast<size_t>(k);
-            cs[K] = Hk(k, k) / denom;
-            sn[K] = Hk(k + 1, k) / denom;
-            Hk(k, k) = denom;
-            Hk(k + 1, k) = 0.0;
-            beta[K + 1] = -sn[K] * beta[K];
-            beta[K] = cs[K] * beta[K];
-            const double rel = std::fabs(beta[K + 1]) / rhs_norm;
-            if (residual_history) residual_history[out.iterations] = rel;
-            ++out.iterations;
-            if (rel <= tol) {
-                ++k;
-                out.converged = 1;
-                break;
-            }
-            if (hnext <= 1e-14 * rhs_norm) {  // happy breakdown
-                out.breakdown = 1;
-                out.converged = 1;
-                ++k;
-                break;
-            }
-            launch_k(k_scale, dim3(nb), dim3(kRT), 0, st, S.V.p + static_cast<long long>(k + 1) * n1, S.w.p, n1, S.scal.p + 1);
-            ++launch_counter();
         }
+        // final state: H, beta, history, counters
+        CK(cudaMemcpyAsync(hstat, S.gstat.p, sizeof(int) * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hp, S.gH.p, sizeof(double) * static_cast<size_t>(MI + 1) * MIc, cudaMemcpyDeviceToHost, st));
+        double* hbeta = hp + static_cast<size_t>(MI + 1) * MIc;
+        double* hhist = hbeta + MIc;
+        CK(cudaMemcpyAsync(hbeta, S.gbeta.p, sizeof(double) * std::min(MI + 1, MIc), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hhist, S.ghist.p, sizeof(double) * MIc, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const int k = hstat[4];
+        out.iterations = hstat[1];
+        out.converged = hstat[2];
+        out.breakdown = hstat[3];
+        if (residual_history)
+            for (int i = 0; i < out.iterations; ++i) residual_history[i] = hhist[i];
         // u = V_k y_k with the upper-triangular solve, x = P^{-1} u
         if (k > 0) {
             std::vector<double> yk(static_cast<size_t>(k));
             for (int i = k - 1; i >= 0; --i) {
-                double sacc = beta[static_cast<size_t>(i)];
-                for (int j = i + 1; j < k; ++j) sacc -= Hk(i, j) * yk[static_cast<size_t>(j)];
-                yk[static_cast<size_t>(i)] = sacc / Hk(i, i);
+                double sacc = hbeta[i];
+                for (int j = i + 1; j < k; ++j) sacc -= hp[static_cast<size_t>(i) * MIc + j] * yk[static_cast<size_t>(j)];
+                yk[static_cast<size_t>(i)] = sacc / hp[static_cast<size_t>(i) * MIc + i];
             }
-            std::memcpy(hp, yk.data(), sizeof(double) * k);
-            CK(cudaMemcpyAsync(S.coef.p, hp, sizeof(double) * k, cudaMemcpyHostToDevice, st));
-            launch_k(k_combine_rows, dim3(nb), dim3(kRT), 0, st, S.z.p, S.V.p, n1, k, S.coef.p, n1, 1);
+            CK(cudaMemcpyAsync(S.coef.p, yk.data(), sizeof(double) * k, cudaMemcpyHostToDevice, st));
+            launch_k(k_combine_rows, dim3(nb), dim3(kRT), 0, st, S.z.p, static_cast<const double*>(S.V.p), n1, k,
+                     static_cast<const double*>(S.coef.p), n1, 1, nostop);
             ++launch_counter();
         } else {
             CK(cudaMemsetAsync(S.z.p, 0, sizeof(double) * n1, st));
         }
         precond_apply_dev(P, S.z.p, S.x.p, st);
         saddle_apply_dev(S, S.x.p, S.ax.p, st);
-        norm_into(S.r.p, S.ax.p, S.scal.p + 2);
-        CK(cudaMemcpyAsync(hp, S.scal.p + 2, sizeof(double), cudaMemcpyDeviceToHost, st));
+        norm_into(S.r.p, S.ax.p, S.scal.p + 2, nostop);
+        double rr = 0.0;
+        CK(cudaMemcpyAsync(&rr, S.scal.p + 2, sizeof(double), cudaMemcpyDeviceToHost, st));
         put_x(S.x.p);
         CK(cudaStreamSynchronize(st));
-        out.relative_residual = hp[0] / rhs_norm;
+        out.relative_residual = rr / rhs_norm;
         if (out.relative_residual <= tol) out.converged = 1;
         *stats = out;
     });
