@@ -73,3 +73,49 @@ def test_config5_full_size_linearity():
     assert np.array_equal(y2, 2.0 * y)  # scaling by 2 is exact in binary floating point
     assert np.array_equal(y, op.apply(w.v))
     assert np.all(np.isfinite(y))
+
+
+def test_concurrent_applies_from_threads_are_safe():
+    # P:include/ksvm/kernel.hpp:28-31: concurrent apply() on one operator
+    import threading
+    import oracle
+    from paper_2312_00538_b200 import AnovaKernelSpec, Dataset, FeatureWindowing, anova_fast_operator
+    pts = oracle.random_points(5000, 6, 71)
+    op = anova_fast_operator(Dataset(pts), AnovaKernelSpec(FeatureWindowing.explicit([[0, 1, 2], [3, 4], [5]])))
+    vs = [oracle.random_vector(5000, 100 + t) for t in range(8)]
+    want = [op.apply(v) for v in vs]
+    got = [None] * 8
+    errs = []
+
+    def run(t):
+        try:
+            for _ in range(5):
+                got[t] = op.apply(vs[t])
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(t,)) for t in range(8)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errs
+    for t in range(8):
+        assert np.array_equal(got[t], want[t])
+
+
+def test_duplicate_merge_extremes():
+    import oracle
+    from paper_2312_00538_b200 import AnovaKernelSpec, Dataset, FeatureWindowing, anova_fast_operator
+    lib = oracle.Lib("oracle")
+    rng = np.random.default_rng(9)
+    # every point identical in every window (one distinct point), and a 1-d binary window
+    X = np.zeros((3000, 4))
+    X[:, 3] = (rng.random(3000) < 0.5) * 0.5 - 0.25
+    v = rng.standard_normal(3000)
+    for wins in ([[0, 1, 2]], [[0, 1, 2], [3]], [[3], [0, 1]]):
+        g = anova_fast_operator(Dataset(X), AnovaKernelSpec(FeatureWindowing.explicit(wins)))
+        o = lib.anova(X, wins)
+        y, yo = g.apply(v), o.apply(v)
+        assert np.linalg.norm(y - yo) <= 1e-10 * np.linalg.norm(yo)
+        assert all(g.window_points(l) <= 2 for l in range(len(wins)))
