@@ -296,6 +296,7 @@ class AnovaFastOperator(KernelOperator):
                                                int(device), _lib.FP64, C.byref(h)))
         self._h = h
         self._free = _lib.load().ksvm_nfft_op_free  # kept: module globals may be gone in __del__
+        self._apply_fn = _lib.load().ksvm_nfft_op_apply
         self._n = n
         self.device = int(device)
         self.num_windows = P
@@ -311,6 +312,18 @@ class AnovaFastOperator(KernelOperator):
         return self._n
 
     def apply(self, v, out=None):
+        # fast path: contiguous float64 numpy vectors (the per-iteration call
+        # of a host-driven solver) -- no wrapper objects, one ctypes call
+        if (type(v) is np.ndarray and v.dtype == np.float64 and v.ndim == 1 and v.shape[0] == self._n
+                and v.flags.c_contiguous and (out is None or (type(out) is np.ndarray and out.dtype == np.float64
+                                                              and out.shape == v.shape and out.flags.c_contiguous))):
+            if out is None:
+                out = np.empty(self._n)
+            rc = self._apply_fn(self._h, v.__array_interface__["data"][0], out.__array_interface__["data"][0],
+                                _lib.HOST, None)
+            if rc:
+                _raise(rc)
+            return out
         a = _Vec(v, self._n, self.device)
         if out is None:
             out, optr = a.out(self._n)
