@@ -407,7 +407,8 @@ std::vector<double> scale_cm(const Window& w, const double* pts, int64_t t, int6
 // ---------------------------------------------------------------------------
 // The engine: every owned window's plan plus the per-apply scratch.
 // ---------------------------------------------------------------------------
-constexpr long long kColumnDensity = 10;  // points per cell below which spread3c runs
+constexpr long long kColumnDensity = 10;
+constexpr int kBatchLanes = 4;  // concurrent applies of a multi-RHS batch  // points per cell below which spread3c runs
 
 struct Engine {
     int device = 0;
@@ -798,6 +799,9 @@ struct Engine {
         }
         d_wins.upload(dws.data(), dws.size(), stream);
         d_ps.upload(ps.data(), ps.size(), stream);
+        h_dws = dws;
+        h_ps = ps;
+        h_srcs = srcs;
         d_items.upload(all.data(), all.size(), stream);
         d_colb.upload(colb.data(), colb.size(), stream);
         d_gitems.upload(gall.data(), gall.size(), stream);
@@ -831,37 +835,37 @@ struct Engine {
         const int cnt = class_end[D] - class_begin[D];
         if (cnt == 0) return;
         tick(kSpread[D]);
-        launch_spread(D, 2 * cfg.window_cutoff, class_PE[D], d_items.p + class_begin[D], cnt, d_ps.p,
-                      d_wins.p, v, patches.p,
+        launch_spread(D, 2 * cfg.window_cutoff, class_PE[D], d_items.p + class_begin[D], cnt, PS(),
+                      WINS(), v, PATCHES(),
                       spread_columns[D] ? d_colb.p + static_cast<size_t>(class_begin[D]) * kColBounds : nullptr,
                       st);
         ++launch_counter();
         if (n_multi_cls[D]) {
             tick("tile_reduce");
-            launch_tile_reduce(d_wins.p, d_multi.p + multi_begin[D], n_multi_cls[D], max_pv, patches.p, st);
+            launch_tile_reduce(WINS(), d_multi.p + multi_begin[D], n_multi_cls[D], max_pv, PATCHES(), st);
             ++launch_counter();
         }
         tick("reduce");
         for (int wrap = 0; wrap < 2; ++wrap) {
             if (!(wrap ? has_wrap : has_nowrap)[D]) continue;
-            launch_reduce(d_wins.p, d_slots.p + slot_begin[D], nslots_cls[D], max_nodes, D,
-                          2 * cfg.window_cutoff, patches.p, wrap != 0, max_tiles[D], st);
+            launch_reduce(WINS(), d_slots.p + slot_begin[D], nslots_cls[D], max_nodes, D,
+                          2 * cfg.window_cutoff, PATCHES(), wrap != 0, max_tiles[D], st);
             ++launch_counter();
         }
         for (int stg = 0; stg < D; ++stg) {
             tick(kConv[stg]);
-            launch_conv(d_wins.p, d_slots.p + slot_begin[D], nslots_cls[D], max_lg, max_fibres, stg, st);
+            launch_conv(WINS(), d_slots.p + slot_begin[D], nslots_cls[D], max_lg, max_fibres, stg, st);
             ++launch_counter();
         }
         if (gather) {
             const int gcnt = gclass_end[D] - gclass_begin[D];
             tick(kGather[D]);
             if (gather_columns[D]) {
-                launch_gather3c(d_items.p + class_begin[D], cnt, d_ps.p, d_wins.p,
+                launch_gather3c(d_items.p + class_begin[D], cnt, PS(), WINS(),
                                 d_colb.p + static_cast<size_t>(class_begin[D]) * kColBounds, st);
             } else {
-                launch_gather(D, 2 * cfg.window_cutoff, class_PE[D], d_gitems.p + gclass_begin[D], gcnt, d_ps.p,
-                              d_wins.p, st);
+                launch_gather(D, 2 * cfg.window_cutoff, class_PE[D], d_gitems.p + gclass_begin[D], gcnt, PS(),
+                              WINS(), st);
             }
             ++launch_counter();
         }
@@ -872,34 +876,34 @@ struct Engine {
     void run_classes(const double* v, bool gather) {
         if (n_small > 0 || n_seg_chunks > 0) tick("dedup_sums");  // per-distinct-point sums of v
         if (n_small > 0) {
-            launch_bin_sums(v, d_codes.p, n_small, n, bin_partial.p, kBinBlocks, d_small_off.p, d_small_nu.p,
-                            vs_all.p, stream);
+            launch_bin_sums(v, d_codes.p, n_small, n, BINP(), kBinBlocks, d_small_off.p, d_small_nu.p,
+                            VSALL(), S());
             launch_counter() += 2;
         }
         if (n_seg_chunks > 0) {
-            launch_seg_sums(v, seg_members.p, seg_chunks.p, seg_partial.p, n_seg_chunks, seg_cb.p, vs_all.p,
-                            n_segs, stream);
+            launch_seg_sums(v, seg_members.p, seg_chunks.p, SEGP(), n_seg_chunks, seg_cb.p, VSALL(),
+                            n_segs, S());
             launch_counter() += 2;
         }
         int ncls = 0;
         for (int D = 1; D <= 3; ++D) ncls += class_end[D] > class_begin[D] ? 1 : 0;
         if (stage_timing || ncls < 2) {
-            for (int D = 3; D >= 1; --D) run_class(D, v, stream, gather);
+            for (int D = 3; D >= 1; --D) run_class(D, v, S(), gather);
             return;
         }
-        CK(cudaEventRecord(ev_fork, stream));
+        CK(cudaEventRecord(EVF(), S()));
         bool first = true;
         for (int D = 3; D >= 1; --D) {
             if (class_end[D] == class_begin[D]) continue;
-            cudaStream_t st = stream;
+            cudaStream_t st = S();
             if (!first) {
-                st = side[D];
-                CK(cudaStreamWaitEvent(st, ev_fork, 0));
+                st = SIDE(D);
+                CK(cudaStreamWaitEvent(st, EVF(), 0));
             }
             run_class(D, v, st, gather);
             if (!first) {
-                CK(cudaEventRecord(ev_join[D], st));
-                CK(cudaStreamWaitEvent(stream, ev_join[D], 0));
+                CK(cudaEventRecord(EVJ(D), st));
+                CK(cudaStreamWaitEvent(S(), EVJ(D), 0));
             }
             first = false;
         }
@@ -911,14 +915,14 @@ struct Engine {
     void run_apply(const double* v, double* y) {
         const int P = P_owned();
         if (P == 0) {
-            launch_fill(y, 0.0, n, stream);
+            launch_fill(y, 0.0, n, S());
             ++launch_counter();
             return;
         }
         nticks = 0;
         run_classes(v, true);
         tick("combine");
-        launch_combine(y, d_src.p, d_inv.p, d_inv8.p, d_eta.p, P, n, stream);
+        launch_combine(y, SRC(), d_inv.p, d_inv8.p, d_eta.p, P, n, S());
         ++launch_counter();
         CK(cudaGetLastError());
         tick("end");
@@ -951,6 +955,118 @@ struct Engine {
 
     bool capturing = false;
 
+    // ---- apply lanes: extra scratch sets so independent applies (the
+    // columns of a batch) run concurrently. A lane owns everything an
+    // in-flight apply writes -- streams, grids G/H/T, patches, per-window
+    // outputs, staging, the duplicate-merge sums and the device tables that
+    // point at them -- and shares the immutable plan. Lane 0 is the
+    // engine's own members (cur == nullptr).
+    struct Lane {
+        cudaStream_t stream = nullptr, side[4] = {nullptr, nullptr, nullptr, nullptr};
+        cudaEvent_t ev_fork = nullptr, ev_join[4] = {nullptr, nullptr, nullptr, nullptr}, ev_done = nullptr;
+        DevBuf<double> grids, patches, parts, vbuf, ybuf, seg_partial, vs_all, uout_all, bin_partial;
+        DevBuf<DWin> d_wins;
+        DevBuf<DPSet> d_ps;
+        DevBuf<const double*> d_src;
+        std::vector<GraphEntry> graphs;
+        ~Lane() {
+            for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+            if (stream) cudaStreamSynchronize(stream);
+            for (int D = 1; D <= 2; ++D) {
+                if (side[D]) cudaStreamDestroy(side[D]);
+                if (ev_join[D]) cudaEventDestroy(ev_join[D]);
+            }
+            if (ev_fork) cudaEventDestroy(ev_fork);
+            if (ev_done) cudaEventDestroy(ev_done);
+            if (stream) cudaStreamDestroy(stream);
+        }
+    };
+    std::vector<std::unique_ptr<Lane>> lanes;  // lanes 1..
+    Lane* cur = nullptr;
+    std::vector<DWin> h_dws;        // host copies of the lane-0 tables (finalize)
+    std::vector<DPSet> h_ps;
+    std::vector<const double*> h_srcs;
+
+    cudaStream_t S() const { return cur ? cur->stream : stream; }
+    cudaStream_t SIDE(int D) const { return cur ? cur->side[D] : side[D]; }
+    cudaEvent_t EVF() const { return cur ? cur->ev_fork : ev_fork; }
+    cudaEvent_t EVJ(int D) const { return cur ? cur->ev_join[D] : ev_join[D]; }
+    double* PATCHES() const { return cur ? cur->patches.p : patches.p; }
+    DWin* WINS() const { return cur ? cur->d_wins.p : d_wins.p; }
+    DPSet* PS() const { return cur ? cur->d_ps.p : d_ps.p; }
+    const double* const* SRC() const { return cur ? cur->d_src.p : d_src.p; }
+    double* BINP() const { return cur ? cur->bin_partial.p : bin_partial.p; }
+    double* SEGP() const { return cur ? cur->seg_partial.p : seg_partial.p; }
+    double* VSALL() const { return cur ? cur->vs_all.p : vs_all.p; }
+    std::vector<GraphEntry>& GR() { return cur ? cur->graphs : graphs; }
+
+    // map a lane-0 scratch pointer into the same offset of lane L's buffer
+    static double* remap(const double* p, const DevBuf<double>& from, DevBuf<double>& to) {
+        return const_cast<double*>(p) - from.p + to.p;
+    }
+    static bool inside(const double* p, const DevBuf<double>& b) { return p && b.p && p >= b.p && p < b.p + b.n; }
+
+    void add_lane() {
+        auto L = std::make_unique<Lane>();
+        CK(cudaStreamCreateWithFlags(&L->stream, cudaStreamNonBlocking));
+        for (int D = 1; D <= 2; ++D) {
+            CK(cudaStreamCreateWithFlags(&L->side[D], cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&L->ev_join[D], cudaEventDisableTiming));
+        }
+        CK(cudaEventCreateWithFlags(&L->ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&L->ev_done, cudaEventDisableTiming));
+        std::vector<DWin> dws = h_dws;
+        size_t total = 0;
+        for (const DWin& w : dws) {
+            long long nodes = 1;
+            for (int t = 0; t < w.d; ++t) nodes *= w.Lg;
+            total += static_cast<size_t>(nodes) * (2 + (w.d == 1 ? 0 : (w.d == 2 ? 2 : 4)));
+        }
+        L->grids.alloc(total);
+        size_t off = 0;
+        for (DWin& w : dws) {
+            long long nodes = 1;
+            for (int t = 0; t < w.d; ++t) nodes *= w.Lg;
+            w.G = L->grids.p + off;
+            off += static_cast<size_t>(nodes);
+            w.H = L->grids.p + off;
+            off += static_cast<size_t>(nodes);
+            for (int k = 0; k < 4; ++k) {
+                if (k < (w.d == 1 ? 0 : (w.d == 2 ? 2 : 4))) {
+                    w.T[k] = L->grids.p + off;
+                    off += static_cast<size_t>(nodes);
+                } else {
+                    w.T[k] = nullptr;
+                }
+            }
+        }
+        L->patches.alloc(patches.n);
+        L->parts.alloc(parts.n);
+        L->vbuf.alloc(vbuf.n);
+        L->ybuf.alloc(ybuf.n);
+        if (vs_all.p) L->vs_all.alloc(vs_all.n);
+        if (uout_all.p) L->uout_all.alloc(uout_all.n);
+        if (seg_partial.p) L->seg_partial.alloc(seg_partial.n);
+        if (bin_partial.p) L->bin_partial.alloc(bin_partial.n);
+        std::vector<DPSet> ps = h_ps;
+        std::vector<const double*> srcs = h_srcs;
+        auto map_out = [&](const double* q) -> double* {
+            if (inside(q, parts)) return remap(q, parts, L->parts);
+            if (inside(q, uout_all)) return remap(q, uout_all, L->uout_all);
+            throw std::logic_error("add_lane: unmapped output pointer");
+        };
+        for (size_t i = 0; i < ps.size(); ++i) {
+            ps[i].out = map_out(ps[i].out);
+            if (ps[i].vsrc) ps[i].vsrc = remap(ps[i].vsrc, vs_all, L->vs_all);
+            srcs[i] = map_out(srcs[i]);
+        }
+        L->d_wins.upload(dws.data(), dws.size(), stream);
+        L->d_ps.upload(ps.data(), ps.size(), stream);
+        L->d_src.upload(srcs.data(), srcs.size(), stream);
+        CK(cudaStreamSynchronize(stream));
+        lanes.push_back(std::move(L));
+    }
+
     void drop_graphs() {
         for (auto& gph : graphs) cudaGraphExecDestroy(gph.exec);
         graphs.clear();
@@ -963,31 +1079,31 @@ struct Engine {
             run_apply(v, y);
             return;
         }
-        for (size_t k = 0; k < graphs.size(); ++k) {
-            GraphEntry& gph = graphs[k];
+        for (size_t k = 0; k < GR().size(); ++k) {
+            GraphEntry& gph = GR()[k];
             if (gph.v == v && gph.y == y && gph.timed == stage_timing) {
-                CK(cudaGraphLaunch(gph.exec, stream));
+                CK(cudaGraphLaunch(gph.exec, S()));
                 launch_counter() += gph.launches;
                 last_nticks = gph.nticks;
                 for (int i = 0; i < gph.nticks; ++i) tick_name[i] = gph.names[i];
-                if (k + 1 != graphs.size()) std::rotate(graphs.begin() + k, graphs.begin() + k + 1, graphs.end());
+                if (k + 1 != GR().size()) std::rotate(GR().begin() + k, GR().begin() + k + 1, GR().end());
                 return;
             }
         }
         cudaGraph_t graph = nullptr;
         const int64_t before = launch_counter().load();
-        CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+        CK(cudaStreamBeginCapture(S(), cudaStreamCaptureModeThreadLocal));
         capturing = true;
         try {
             run_apply(v, y);
             capturing = false;
         } catch (...) {
             capturing = false;
-            cudaStreamEndCapture(stream, &graph);
+            cudaStreamEndCapture(S(), &graph);
             if (graph) cudaGraphDestroy(graph);
             throw;
         }
-        CK(cudaStreamEndCapture(stream, &graph));
+        CK(cudaStreamEndCapture(S(), &graph));
         GraphEntry gph{};
         gph.v = v;
         gph.y = y;
@@ -999,12 +1115,12 @@ struct Engine {
         const cudaError_t e = cudaGraphInstantiate(&gph.exec, graph, 0);
         cudaGraphDestroy(graph);
         CK(e);
-        if (graphs.size() >= kMaxGraphs) {
-            cudaGraphExecDestroy(graphs.front().exec);
-            graphs.erase(graphs.begin());
+        if (GR().size() >= kMaxGraphs) {
+            cudaGraphExecDestroy(GR().front().exec);
+            GR().erase(GR().begin());
         }
-        graphs.push_back(gph);
-        CK(cudaGraphLaunch(gph.exec, stream));
+        GR().push_back(gph);
+        CK(cudaGraphLaunch(gph.exec, S()));
         launch_counter() += gph.launches;
     }
 
@@ -1205,9 +1321,10 @@ int ksvm_nfft_op_apply_batch(const ksvm_nfft_op* op, const double* V, double* Y,
         if (ptr_kind != KSVM_NFFT_HOST && ptr_kind != KSVM_NFFT_DEVICE)
             throw std::invalid_argument("ptr_kind must be KSVM_NFFT_HOST or KSVM_NFFT_DEVICE");
         if (k == 0) return;
-        // One upload / download for all columns; every column replays the
-        // operator's cached graph through its fixed staging buffers (so the
-        // result is bit-identical to k single applies).
+        // One upload / download for all columns. Columns are spread over up
+        // to kBatchLanes apply lanes (independent scratch, shared plan) that
+        // run concurrently; each column replays its lane's cached graph, so
+        // every result is bit-identical to a single apply.
         DeviceGuard dg(E.device);
         std::lock_guard<std::mutex> lk(E.mu);
         const int64_t n = E.n;
@@ -1228,10 +1345,29 @@ int ksvm_nfft_op_apply_batch(const ksvm_nfft_op* op, const double* V, double* Y,
             CK(cudaEventRecord(E.ev_in, es));
             CK(cudaStreamWaitEvent(st, E.ev_in, 0));
         }
+        int B = (E.use_graphs && !E.stage_timing && E.P_owned() > 0) ? std::min(k, kBatchLanes) : 1;
+        if (const char* e = std::getenv("KSVM_NFFT_LANES")) B = std::max(1, std::min(B, std::atoi(e)));
+        while (static_cast<int>(E.lanes.size()) < B - 1) E.add_lane();
+        CK(cudaEventRecord(E.ev_in, st));  // inputs staged
+        for (int b = 1; b < B; ++b) CK(cudaStreamWaitEvent(E.lanes[static_cast<size_t>(b - 1)]->stream, E.ev_in, 0));
+        struct LaneReset {  // the engine is back on lane 0 whatever happens
+            Engine& e;
+            ~LaneReset() { e.cur = nullptr; }
+        } lane_reset{E};
         for (int c = 0; c < k; ++c) {
-            CK(cudaMemcpyAsync(E.vbuf.p, vsrc + c * vld, col, cudaMemcpyDeviceToDevice, st));
-            E.apply(E.vbuf.p, E.ybuf.p);
-            CK(cudaMemcpyAsync(ydst + c * yld, E.ybuf.p, col, cudaMemcpyDeviceToDevice, st));
+            const int b = c % B;
+            E.cur = b == 0 ? nullptr : E.lanes[static_cast<size_t>(b - 1)].get();
+            double* lv = b == 0 ? E.vbuf.p : E.cur->vbuf.p;
+            double* ly = b == 0 ? E.ybuf.p : E.cur->ybuf.p;
+            CK(cudaMemcpyAsync(lv, vsrc + c * vld, col, cudaMemcpyDeviceToDevice, E.S()));
+            E.apply(lv, ly);
+            CK(cudaMemcpyAsync(ydst + c * yld, ly, col, cudaMemcpyDeviceToDevice, E.S()));
+        }
+        E.cur = nullptr;
+        for (int b = 1; b < B; ++b) {
+            auto& L = *E.lanes[static_cast<size_t>(b - 1)];
+            CK(cudaEventRecord(L.ev_done, L.stream));
+            CK(cudaStreamWaitEvent(st, L.ev_done, 0));
         }
         if (ptr_kind == KSVM_NFFT_HOST) {
             CK(cudaMemcpy2DAsync(Y, sizeof(double) * ld, Yd.p, col, col, k, cudaMemcpyDeviceToHost, st));

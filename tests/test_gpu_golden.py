@@ -81,6 +81,15 @@ def test_apply_batch_equals_single_applies():
     torch.cuda.synchronize()
     assert np.array_equal(Yd.cpu().numpy(), Y)
     assert op.apply_batch(np.zeros((V.shape[0], 0))).shape == (V.shape[0], 0)
+    # more columns than lanes, and an operator with duplicate-merged windows
+    rng2 = np.random.default_rng(6)
+    X = np.hstack([rng2.standard_normal((6000, 3)), (rng2.random((6000, 3)) < 0.2).astype(float)])
+    X = (X - X.min(0)) / (X.max(0) - X.min(0)) * 0.5 - 0.25
+    op2 = anova_fast_operator(Dataset(X), AnovaKernelSpec(FeatureWindowing.explicit([[0, 1, 2], [3, 4, 5]])))
+    V2 = rng2.standard_normal((6000, 7))
+    Y2 = op2.apply_batch(V2)
+    for c in range(7):
+        assert np.array_equal(Y2[:, c], op2.apply(V2[:, c]))
 
 
 def test_edge_cases():
