@@ -42,6 +42,24 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// Warp sum of p[q * stride] for q < count <= kRB (one warp): every load is
+// issued before the adds (fixed lane assignment, fixed order), so a finisher
+// costs one L2 round trip instead of one per element.
+__device__ __forceinline__ double warp_sum_strided(const double* __restrict__ p, int count, long long stride) {
+    constexpr int kPer = (kRB + 31) / 32;
+    const int lane = threadIdx.x & 31;
+    double v[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const int q = lane + 32 * j;
+        v[j] = q < count ? p[static_cast<long long>(q) * stride] : 0.0;
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) s += v[j];
+    return warp_sum(s);
+}
+
 // Block b owns indices b*kRT + t + q*kRB*kRT; its sum is written to
 // partial[b] (lane butterfly, then warps in order).
 __device__ __forceinline__ void block_partial(double v, double* partial) {
@@ -94,9 +112,7 @@ __global__ void k_finish_scalar(const double* __restrict__ partial, int nb, doub
     pdl_trigger();
     pdl_wait();
     if (stop && *stop) return;  // GMRES look-ahead past convergence
-    double s = 0.0;
-    for (int b = threadIdx.x; b < nb; b += 32) s += partial[b];
-    s = warp_sum(s);
+    const double s = warp_sum_strided(partial, nb, 1);
     if (threadIdx.x == 0) *dst = root ? sqrt(s) : coef * s - (sub ? *sub : 0.0);
 }
 
@@ -144,9 +160,7 @@ __global__ void k_rows_finish(const double* __restrict__ partial, int nb, int ro
     if (stop && *stop) return;  // GMRES look-ahead past convergence
     const int a = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
     if (a >= rows) return;
-    double s = 0.0;
-    for (int b = lane; b < nb; b += 32) s += partial[static_cast<long long>(b) * rows + a];
-    s = warp_sum(s);
+    const double s = warp_sum_strided(partial + a, nb, rows);
     if (lane == 0) out[a] = s;
 }
 
@@ -280,38 +294,202 @@ __global__ void k_cap_finish(const double* __restrict__ partial, int nchunks, in
     C[idx] = (a == b ? 1.0 : 0.0) + s;
 }
 
+// ---- fused GMRES-iteration kernels ----------------------------------------
+// The iteration's vector work, fused where the pieces share a block's index
+// set (no grid-wide dependency between them): the preconditioner output also
+// writes the matvec input u = y .* z; the saddle post-step and the first
+// Gram-Schmidt pass finish the scalar entries (z_n, w_n) from the previous
+// kernel's block partials themselves; each Gram-Schmidt subtraction is fused
+// with the next pass's dot partials (or the norm partial).
+
+// s[a] = sum_b partial[b*k + a] (warp per row), then inner = Cinv s
+__global__ void __launch_bounds__(1024) gk_inner(const double* __restrict__ partial, int nb, int k,
+                                                 const double* __restrict__ Cinv, double* __restrict__ inner,
+                                                 const int* __restrict__ stop) {
+    extern __shared__ double s_s[];
+    pdl_trigger();
+    pdl_wait();
+    if (stop && *stop) return;
+    const int lane = threadIdx.x & 31;
+    for (int a = threadIdx.x >> 5; a < k; a += blockDim.x >> 5) {
+        const double acc = warp_sum_strided(partial + a, nb, k);
+        if (lane == 0) s_s[a] = acc;
+    }
+    __syncthreads();
+    for (int a = threadIdx.x; a < k; a += blockDim.x) {
+        double acc = 0.0;
+        for (int c = 0; c < k; ++c) acc += Cinv[static_cast<long long>(a) * k + c] * s_s[c];
+        inner[a] = acc;
+    }
+}
+
+// z = P^{-1} g on [0, n) (mode 0: SMW, 1: diagonal fallback / rank 0,
+// 2: identity), u = y .* z, partial of y . z (z_n is finished by gk_post)
+__global__ void __launch_bounds__(kRT) gk_precond_out(double* __restrict__ z, double* __restrict__ u,
+                                                      const double* __restrict__ y_op,
+                                                      const double* __restrict__ g, const double* __restrict__ y,
+                                                      const double* __restrict__ theta, const double* __restrict__ Z,
+                                                      int k, const double* __restrict__ inner, long long n, int mode,
+                                                      double* __restrict__ partial, const int* __restrict__ stop) {
+    extern __shared__ double s_inner[];
+    pdl_trigger();
+    pdl_wait();
+    if (stop && *stop) return;
+    if (mode == 0) {
+        for (int a = threadIdx.x; a < k; a += blockDim.x) s_inner[a] = inner[a];
+        __syncthreads();
+    }
+    double acc = 0.0;
+    KSVM_FOR_BLOCK_INDEX(j, n) {
+        double x1;
+        if (mode == 0) {
+            double s = 0.0;
+            for (int a = 0; a < k; ++a) s += Z[static_cast<long long>(a) * n + j] * s_inner[a];
+            x1 = g[j] / theta[j] - y[j] * s / theta[j];
+        } else if (mode == 1) {
+            x1 = g[j] / theta[j];
+        } else {
+            x1 = g[j];
+        }
+        z[j] = x1;
+        u[j] = y_op[j] * x1;  // the saddle matvec's input y .* z (P:src/saddle.cpp:29)
+        acc += y[j] * x1;
+    }
+    block_partial(acc, partial);
+}
+
+// z_n (P:src/saddle.cpp:88: -y.x1 - g_n; identity: g_n) from the
+// preconditioner's partials, then w = A z on [0, n) and partial of y . z
+__global__ void __launch_bounds__(kRT) gk_post(double* __restrict__ w, const double* __restrict__ y,
+                                               const double* __restrict__ kv, const double* __restrict__ theta,
+                                               const double* __restrict__ z, const double* __restrict__ g,
+                                               const double* __restrict__ pre_partial, int pre_nb, int identity,
+                                               long long n, double* __restrict__ partial, const int* __restrict__ stop) {
+    __shared__ double s_zn;
+    pdl_trigger();
+    pdl_wait();
+    if (stop && *stop) return;
+    if (threadIdx.x < 32) {
+        const double s = identity ? 0.0 : warp_sum_strided(pre_partial, pre_nb, 1);
+        if (threadIdx.x == 0) s_zn = identity ? g[n] : -s - g[n];
+    }
+    __syncthreads();
+    const double zn = s_zn;
+    double acc = 0.0;
+    KSVM_FOR_BLOCK_INDEX(j, n) {
+        const double v = z[j];
+        w[j] = y[j] * kv[j] + theta[j] * v - zn * y[j];
+        acc += y[j] * v;
+    }
+    block_partial(acc, partial);
+}
+
+// row-tiled partial dots of V[0..rows) with x over this block's indices
+__device__ __forceinline__ void mdot_block(const double* __restrict__ V, long long ld, int rows, long long L,
+                                           const double* __restrict__ x, double* __restrict__ partial) {
+    __shared__ double sh[kRT / 32][kRows];
+    for (int a0 = 0; a0 < rows; a0 += kRows) {
+        double acc[kRows];
+#pragma unroll
+        for (int r = 0; r < kRows; ++r) acc[r] = 0.0;
+        KSVM_FOR_BLOCK_INDEX(i, L) {
+            const double xi = x[i];
+#pragma unroll
+            for (int r = 0; r < kRows; ++r)
+                if (a0 + r < rows) acc[r] += V[static_cast<long long>(a0 + r) * ld + i] * xi;
+        }
+#pragma unroll
+        for (int r = 0; r < kRows; ++r) acc[r] = warp_sum(acc[r]);
+        if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+            for (int r = 0; r < kRows; ++r) sh[threadIdx.x >> 5][r] = acc[r];
+        }
+        __syncthreads();
+        if (threadIdx.x < kRows && a0 + static_cast<int>(threadIdx.x) < rows) {
+            double s = 0.0;
+            for (int wv = 0; wv < kRT / 32; ++wv) s += sh[wv][threadIdx.x];
+            partial[static_cast<long long>(blockIdx.x) * rows + a0 + threadIdx.x] = s;
+        }
+        __syncthreads();
+    }
+}
+
+// w_n = -y . z (P:src/saddle.cpp:32) from gk_post's partials (the block that
+// owns index n stores it first), then the first Gram-Schmidt pass's partial
+// dots h = V^T w
+__global__ void __launch_bounds__(kRT) gk_cgs_first(const double* __restrict__ V, long long ld, int rows,
+                                                    double* __restrict__ w, long long n1,
+                                                    const double* __restrict__ post_partial, int post_nb,
+                                                    double* __restrict__ partial, const int* __restrict__ stop) {
+    pdl_trigger();
+    pdl_wait();
+    if (stop && *stop) return;
+    const long long nidx = n1 - 1;
+    const bool owner = (nidx / kRT) % kRB == blockIdx.x;
+    if (owner) {
+        if (threadIdx.x < 32) {
+            const double s = warp_sum_strided(post_partial, post_nb, 1);
+            if (threadIdx.x == 0) w[nidx] = -s;
+        }
+        __syncthreads();
+    }
+    mdot_block(V, ld, rows, n1, w, partial);
+}
+
+// w -= V h (this block's indices); then either the next pass's partial dots
+// (norm == 0) or the partial of |w|^2 (norm == 1)
+__global__ void __launch_bounds__(kRT) gk_cgs_combine(const double* __restrict__ V, long long ld, int rows,
+                                                      const double* __restrict__ h, double* __restrict__ w,
+                                                      long long n1, int norm, double* __restrict__ partial,
+                                                      const int* __restrict__ stop) {
+    pdl_trigger();
+    pdl_wait();
+    if (stop && *stop) return;
+    double sq = 0.0;
+    KSVM_FOR_BLOCK_INDEX(i, n1) {
+        double s = 0.0;
+        for (int a = 0; a < rows; ++a) s += V[static_cast<long long>(a) * ld + i] * h[a];
+        const double wi = w[i] - s;
+        w[i] = wi;
+        sq += wi * wi;
+    }
+    if (norm)
+        block_partial(sq, partial);
+    else
+        mdot_block(V, ld, rows, n1, w, partial);
+}
+
+// hnext = |w| from gk_cgs_combine's partials, then the Givens step
+__global__ void gk_norm_givens(const double* __restrict__ npartial, int nb, double* __restrict__ hnext_out, int k,
+                               int MI, const double* __restrict__ h, double rhs_norm, double tol,
+                               double* __restrict__ H, double* __restrict__ cs, double* __restrict__ sn,
+                               double* __restrict__ beta, double* __restrict__ hist, int* __restrict__ stat);
+
 // One GMRES step's Givens update on the device (P:src/saddle.cpp:127-163),
 // so the host can enqueue iterations ahead instead of waiting for each
 // Hessenberg column: H(:,k) = h1 + h2, H(k+1,k) = hnext, stored rotations,
 // new rotation, beta, the relative residual estimate and the stop rules.
 // stat = {stop, iterations, converged, breakdown, kfinal}.
-__global__ void k_givens(int k, int MI, const double* __restrict__ h, const double* __restrict__ hnext_p,
-                         double rhs_norm, double tol, double* __restrict__ H, double* __restrict__ cs,
-                         double* __restrict__ sn, double* __restrict__ beta, double* __restrict__ hist,
-                         int* __restrict__ stat) {
-    pdl_trigger();
-    pdl_wait();
-    if (threadIdx.x != 0 || stat[0]) return;
-    auto Hk = [&](int i, int j) -> double& { return H[static_cast<long long>(i) * MI + j]; };
-    for (int i = 0; i <= k; ++i) Hk(i, k) = h[i] + h[k + 1 + i];
-    const double hnext = *hnext_p;
-    Hk(k + 1, k) = hnext;
-    for (int i = 0; i < k; ++i) {
-        const double tmp = cs[i] * Hk(i, k) + sn[i] * Hk(i + 1, k);
-        Hk(i + 1, k) = -sn[i] * Hk(i, k) + cs[i] * Hk(i + 1, k);
-        Hk(i, k) = tmp;
-    }
-    const double denom = hypot(Hk(k, k), Hk(k + 1, k));
+
+
+// The new rotation, beta, the residual estimate and the stop rules
+// (P:src/saddle.cpp:135-163) on the rotated column col[0..k+1] (col[k+1]
+// = hnext on entry); col[k], col[k+1] are updated in place.
+__device__ void givens_tail(int k, int MI, double* col, double hnext, double rhs_norm, double tol,
+                            double* __restrict__ cs, double* __restrict__ sn, double* __restrict__ beta,
+                            double* __restrict__ hist, int* __restrict__ stat) {
+    col[k + 1] = hnext;
+    const double denom = hypot(col[k], col[k + 1]);
     if (denom == 0.0) {
         stat[3] = 1;
         stat[0] = 1;
         stat[4] = k;
         return;
     }
-    cs[k] = Hk(k, k) / denom;
-    sn[k] = Hk(k + 1, k) / denom;
-    Hk(k, k) = denom;
-    Hk(k + 1, k) = 0.0;
+    cs[k] = col[k] / denom;
+    sn[k] = col[k + 1] / denom;
+    col[k] = denom;
+    col[k + 1] = 0.0;
     beta[k + 1] = -sn[k] * beta[k];
     beta[k] = cs[k] * beta[k];
     const double rel = fabs(beta[k + 1]) / rhs_norm;
@@ -332,6 +510,41 @@ __global__ void k_givens(int k, int MI, const double* __restrict__ h, const doub
     }
 }
 
+
+__global__ void gk_norm_givens(const double* __restrict__ npartial, int nb, double* __restrict__ hnext_out, int k,
+                               int MI, const double* __restrict__ h, double rhs_norm, double tol,
+                               double* __restrict__ H, double* __restrict__ cs, double* __restrict__ sn,
+                               double* __restrict__ beta, double* __restrict__ hist, int* __restrict__ stat) {
+    extern __shared__ double sg[];  // [0, k+1): H(:,k) = h1 + h2; [k+1, 2k+1): cs; [2k+1, 3k+1): sn
+    pdl_trigger();
+    pdl_wait();
+    if (stat[0] || threadIdx.x >= 32) return;
+    const double s = warp_sum_strided(npartial, nb, 1);
+    for (int i = threadIdx.x; i <= k; i += 32) sg[i] = h[i] + h[k + 1 + i];
+    for (int i = threadIdx.x; i < k; i += 32) {
+        sg[k + 1 + i] = cs[i];
+        sg[2 * k + 1 + i] = sn[i];
+    }
+    __syncwarp();
+    if (threadIdx.x == 0) {
+        const double hnext = sqrt(s);
+        *hnext_out = hnext;
+        // stored rotations on the new column: carried in a register chain
+        // (P:src/saddle.cpp:130-134)
+        double x = sg[0];
+        for (int i = 0; i < k; ++i) {
+            const double c = sg[k + 1 + i], sv = sg[2 * k + 1 + i], yv = sg[i + 1];
+            sg[i] = c * x + sv * yv;
+            x = -sv * x + c * yv;
+        }
+        sg[k] = x;
+        givens_tail(k, MI, sg, hnext, rhs_norm, tol, cs, sn, beta, hist, stat);
+    }
+    __syncwarp();
+    for (int i = threadIdx.x; i <= k + 1; i += 32) H[static_cast<long long>(i) * MI + k] = sg[i];
+}
+
+
 int blocks_for(long long L) { return static_cast<int>(std::min<long long>(kRB, (L + kRT - 1) / kRT)); }
 
 }  // namespace
@@ -349,7 +562,8 @@ struct ksvm_nfft_saddle {
     // GMRES workspace, reused while max_iter does not grow
     int ws_iter = -1;
     DevBuf<double> V, z, w, x, r, ax, h, coef, partial_rows, scal;
-    DevBuf<double> gH, gcs, gsn, gbeta, ghist;  // device-side Givens state (k_givens)
+    DevBuf<double> gH, gcs, gsn, gbeta, ghist;  // device-side Givens state (gk_norm_givens)
+    DevBuf<double> pre_partial, norm_partial;   // fused-iteration block partials
     DevBuf<int> gstat;                          // {stop, iterations, converged, breakdown, kfinal}
     double* pinned = nullptr;
     ~ksvm_nfft_saddle() {
@@ -666,6 +880,8 @@ int ksvm_nfft_gmres_solve(const ksvm_nfft_saddle* s, const ksvm_nfft_precond* p,
             S.r.alloc(n1);
             S.ax.alloc(n1);
             S.scal.alloc(4);
+            S.pre_partial.alloc(kRB);
+            S.norm_partial.alloc(kRB);
         }
         const int nb = blocks_for(n1);
         double* hp = S.pinned;
@@ -717,33 +933,56 @@ int ksvm_nfft_gmres_solve(const ksvm_nfft_saddle* s, const ksvm_nfft_precond* p,
             CK(cudaMemcpyAsync(S.gstat.p, st0, sizeof(st0), cudaMemcpyHostToDevice, st));
         }
         // Iterations are enqueued ahead (kLookAhead per host check); once
-        // k_givens sets stop, every later loop kernel returns at once, so
+        // gk_norm_givens sets stop, every later loop kernel returns at once, so
         // the look-ahead only costs the matvec graphs it launched.
         constexpr int kLookAhead = 4;
         const int* stop = S.gstat.p;
         int* hstat = reinterpret_cast<int*>(hp + static_cast<size_t>(MI + 1) * MIc + 2 * MIc);
+        const long long n = S.n;
+        const int nbn = blocks_for(n);
+        const int pmode = P.identity ? 2 : ((P.fallback || P.k == 0) ? 1 : 0);
         for (int k = 0; k < MI; ++k) {
             const double* vk = S.V.p + static_cast<long long>(k) * n1;
-            precond_apply_dev(P, vk, S.z.p, st, stop);
-            saddle_apply_dev(S, S.z.p, S.w.p, st, stop);
-            // classical Gram-Schmidt, two passes: h = V^T w; w -= V h
-            for (int pass = 0; pass < 2; ++pass) {
-                double* hd = S.h.p + pass * (k + 1);
-                launch_k(k_mdot, dim3(nb), dim3(kRT), 0, st, static_cast<const double*>(S.V.p), n1, k + 1, n1, 0,
-                         static_cast<const double*>(S.w.p), nullptr, nullptr, S.partial_rows.p, stop);
-                launch_k(k_rows_finish, dim3((k + 1 + 7) / 8), dim3(256), 0, st,
-                         static_cast<const double*>(S.partial_rows.p), nb, k + 1, hd, stop);
-                launch_k(k_combine_rows, dim3(nb), dim3(kRT), 0, st, S.w.p, static_cast<const double*>(S.V.p), n1,
-                         k + 1, static_cast<const double*>(hd), n1, 0, stop);
-                launch_counter() += 3;
+            // z = P^{-1} v_k (z_n deferred), u = y .* z
+            if (pmode == 0) {
+                launch_k(k_mdot, dim3(nbn), dim3(kRT), 0, st, static_cast<const double*>(P.Z.p), n, P.k, n, 1, vk,
+                         static_cast<const double*>(P.y.p), static_cast<const double*>(P.theta.p), P.partial.p, stop);
+                launch_k(gk_inner, dim3(1), dim3(1024), sizeof(double) * P.k, st,
+                         static_cast<const double*>(P.partial.p), nbn, P.k, static_cast<const double*>(P.Cinv.p),
+                         P.inner.p, stop);
+                launch_counter() += 2;
             }
-            norm_into(S.w.p, nullptr, S.scal.p + 1, stop);
-            launch_k(k_givens, dim3(1), dim3(32), 0, st, k, MI, static_cast<const double*>(S.h.p),
-                     static_cast<const double*>(S.scal.p + 1), rhs_norm, tol, S.gH.p, S.gcs.p, S.gsn.p, S.gbeta.p,
-                     S.ghist.p, S.gstat.p);
+            launch_k(gk_precond_out, dim3(nbn), dim3(kRT), pmode == 0 ? sizeof(double) * P.k : 0, st, S.z.p, S.u.p,
+                     static_cast<const double*>(S.y.p), vk, static_cast<const double*>(P.y.p),
+                     static_cast<const double*>(P.theta.p), static_cast<const double*>(P.Z.p), P.k,
+                     static_cast<const double*>(P.inner.p), n, pmode, S.pre_partial.p, stop);
+            // w = A z (matvec on u, then the saddle rows; z_n from the partials)
+            const int rc = ksvm_nfft_op_apply(S.op, S.u.p, S.kv.p, KSVM_NFFT_DEVICE, st);
+            if (rc != KSVM_NFFT_OK) throw std::runtime_error(std::string("saddle apply: ") + ksvm_nfft_last_error());
+            launch_k(gk_post, dim3(nbn), dim3(kRT), 0, st, S.w.p, static_cast<const double*>(S.y.p),
+                     static_cast<const double*>(S.kv.p), static_cast<const double*>(S.theta.p),
+                     static_cast<const double*>(S.z.p), vk, static_cast<const double*>(S.pre_partial.p), nbn,
+                     pmode == 2 ? 1 : 0, n, S.partial.p, stop);
+            // classical Gram-Schmidt, two passes (w_n finished in the first)
+            double* h1 = S.h.p;
+            double* h2 = S.h.p + (k + 1);
+            launch_k(gk_cgs_first, dim3(nb), dim3(kRT), 0, st, static_cast<const double*>(S.V.p), n1, k + 1, S.w.p,
+                     n1, static_cast<const double*>(S.partial.p), nbn, S.partial_rows.p, stop);
+            launch_k(k_rows_finish, dim3((k + 1 + 7) / 8), dim3(256), 0, st,
+                     static_cast<const double*>(S.partial_rows.p), nb, k + 1, h1, stop);
+            launch_k(gk_cgs_combine, dim3(nb), dim3(kRT), 0, st, static_cast<const double*>(S.V.p), n1, k + 1,
+                     static_cast<const double*>(h1), S.w.p, n1, 0, S.partial_rows.p, stop);
+            launch_k(k_rows_finish, dim3((k + 1 + 7) / 8), dim3(256), 0, st,
+                     static_cast<const double*>(S.partial_rows.p), nb, k + 1, h2, stop);
+            launch_k(gk_cgs_combine, dim3(nb), dim3(kRT), 0, st, static_cast<const double*>(S.V.p), n1, k + 1,
+                     static_cast<const double*>(h2), S.w.p, n1, 1, S.norm_partial.p, stop);
+            launch_k(gk_norm_givens, dim3(1), dim3(32), sizeof(double) * (3 * k + 3), st,
+                     static_cast<const double*>(S.norm_partial.p), nb,
+                     S.scal.p + 1, k, MI, static_cast<const double*>(S.h.p), rhs_norm, tol, S.gH.p, S.gcs.p, S.gsn.p,
+                     S.gbeta.p, S.ghist.p, S.gstat.p);
             launch_k(k_scale, dim3(nb), dim3(kRT), 0, st, S.V.p + static_cast<long long>(k + 1) * n1,
                      static_cast<const double*>(S.w.p), n1, static_cast<const double*>(S.scal.p + 1), stop);
-            launch_counter() += 2;
+            launch_counter() += 9;
             if ((k + 1) % kLookAhead == 0 && k + 1 < MI) {
                 CK(cudaMemcpyAsync(hstat, S.gstat.p, sizeof(int) * 8, cudaMemcpyDeviceToHost, st));
                 CK(cudaStreamSynchronize(st));
