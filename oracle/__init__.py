@@ -424,3 +424,63 @@ def decision_values(train, windows, weights, ells, coeff, bias, test, fast=True,
             acc += coeff[i] * s
         f[j] = acc
     return f + bias, len(redo)
+
+
+# --- interior point loop (P:src/ipm.cpp) --------------------------------------
+IPM_DEFAULTS = {"C": 0.5, "sigma": 0.6, "gamma0": 0.99995, "tol_ip": 1e-1, "max_ip_iters": 50,
+                "tol_gmres": 1e-3, "max_gmres_iters": 100, "mu0": 1.0}  # P:include/ksvm/ipm.hpp:15-24
+
+
+def _ipm_lib():
+    L = _saddle_lib()
+    if not getattr(L, "_ipm_bound", False):
+        vp = C.c_void_p
+        L.oracle_ipm_train.restype = C.c_int
+        L.oracle_ipm_train.argtypes = [vp, vp, C.c_int64, _dp, vp, C.c_int, _dp, _dp, _dp, vp]
+        L.oracle_compute_bias.restype = C.c_int
+        L.oracle_compute_bias.argtypes = [vp, vp, C.c_int64, _dp, _dp, C.c_double, C.c_double, _dp]
+        L.oracle_blobs.restype = None
+        L.oracle_blobs.argtypes = [C.c_int64, C.c_int64, C.c_double, C.c_uint64, C.c_double, _dp, _dp]
+        L._ipm_bound = True
+    return L
+
+
+def ipm_train(K, y, Z=None, **cfg):
+    """ipm_train (P:src/ipm.cpp:76-155). K: oracle Anova or dense matrix.
+    Returns (alpha, result dict, per-iteration log array)."""
+    L = _ipm_lib()
+    c = dict(IPM_DEFAULTS, **cfg)
+    carr = _f64([c[k] for k in ("C", "sigma", "gamma0", "tol_ip", "max_ip_iters", "tol_gmres", "max_gmres_iters",
+                                 "mu0")])
+    h, dense, n, keep = _kop(K)
+    y = _f64(y)
+    Zc = None if Z is None else np.ascontiguousarray(Z, dtype=np.float64)
+    alpha = np.empty(n)
+    res = np.zeros(7)
+    log = np.zeros((int(c["max_ip_iters"]), 6))
+    _saddle_check(L, L.oracle_ipm_train(h, dense, n, _ptr(y), None if Zc is None else C.c_void_p(Zc.ctypes.data),
+                                        0 if Zc is None else Zc.shape[0], _ptr(carr), _ptr(alpha), _ptr(res),
+                                        C.c_void_p(log.ctypes.data)))
+    it = int(res[5])
+    status = {0: "converged", 1: "max_iterations", 2: "stalled"}[int(res[4])]
+    return alpha, {"lambda": res[0], "mu_final": res[1], "xi_alpha_rel": res[2], "xi_lambda_rel": res[3],
+                   "status": status, "iterations": it, "mean_gmres_iters": res[6]}, log[:it].copy()
+
+
+def compute_bias(K, alpha, y, C, eps_sv):
+    """compute_bias (P:src/ipm.cpp:157-185)."""
+    L = _ipm_lib()
+    h, dense, n, keep = _kop(K)
+    alpha, y = _f64(alpha), _f64(y)
+    b = np.zeros(1)
+    _saddle_check(L, L.oracle_compute_bias(h, dense, n, _ptr(alpha), _ptr(y), float(C), float(eps_sv), _ptr(b)))
+    return float(b[0])
+
+
+def blobs(n, d, gap, seed, noise=0.5):
+    """helpers::blobs (P:tests/helpers.hpp:41-56): (n x d points, labels)."""
+    L = _ipm_lib()
+    pts = np.empty(n * d)
+    lab = np.empty(n)
+    L.oracle_blobs(n, d, gap, seed, noise, _ptr(pts), _ptr(lab))
+    return pts.reshape(d, n).T.copy(), lab

@@ -73,6 +73,14 @@ int oracle_gmres_solve(const oracle_anova* op, const double* dense, int64_t n, c
                        const double* theta, const double* Z, int k, const double* rhs, double tol,
                        int max_iter, double* x_out, double* stats, double* history);
 
+/* Interior point loop (P:src/ipm.cpp), compute_bias and helpers::blobs; see
+ * oracle/saddle_oracle.cpp for the array layouts. */
+int oracle_ipm_train(const oracle_anova* op, const double* dense, int64_t n, const double* y, const double* Z, int k,
+                     const double* cfg, double* alpha_out, double* res, double* log);
+int oracle_compute_bias(const oracle_anova* op, const double* dense, int64_t n, const double* alpha, const double* y,
+                        double C, double eps_sv, double* bias);
+void oracle_blobs(int64_t n, int64_t d, double gap, uint64_t seed, double noise, double* pts_cm, double* labels);
+
 /* Greedy pivoted Cholesky (oracle/lowrank_oracle.cpp, restating
  * P:src/low_rank.cpp:25-92) on exact entries: window >= 0 the
  * WindowOperator entry of that window, -1 the weighted ANOVA entry. Z_out
