@@ -230,6 +230,79 @@ int ksvm_nfft_decision_values(const double* train, int64_t n, int d, int64_t ld_
 int ksvm_nfft_gmres_solve(const ksvm_nfft_saddle* s, const ksvm_nfft_precond* p, const double* rhs,
                           double tol, int max_iter, double* x, ksvm_nfft_gmres_stats* stats,
                           double* residual_history, int ptr_kind, void* stream);
+
+/* Theta from host (ptr_kind HOST; stream ignored) or device memory (ordered
+ * on `stream`), for device-resident drivers such as ksvm_nfft_ipm_train.
+ * Replaces constructing a fresh SaddleOperator(op, y, theta)
+ * (P:src/ipm.cpp:107) / SaddlePreconditioner::refresh(theta) (P:src/saddle.cpp:41-63). */
+int ksvm_nfft_saddle_set_theta_ex(ksvm_nfft_saddle* s, const double* theta, int ptr_kind, void* stream);
+int ksvm_nfft_precond_refresh_ex(ksvm_nfft_precond* p, const double* theta, int ptr_kind, void* stream);
+
+/* ---- interior point trainer, GPU resident ---------------------------------
+ * ipm_train(op, y, factor, cfg) (P:src/ipm.cpp:76-155; IpmConfig /
+ * IpmResult / IpmIterationLog, P:include/ksvm/ipm.hpp:15-53): alpha, Theta,
+ * the Newton systems and the Krylov bases stay on op's GPU; every matvec is
+ * op's NFFT apply. y: n labels (+-1, host); Z: the stacked low-rank factor
+ * (k x n row-major, host) or NULL for the unpreconditioned run (null
+ * StackedFactor); alpha: n entries out (host); log: NULL or room for
+ * cfg->max_ip_iters entries. Invalid config / labels: status 4 with the
+ * reference's messages; degenerate initial infeasibility: status 5. */
+typedef struct ksvm_nfft_ipm_config {
+    double C;             /* 0.5 */
+    double sigma;         /* 0.6, barrier reduction */
+    double gamma0;        /* 0.99995, fraction to boundary */
+    double tol_ip;        /* 1e-1 */
+    int max_ip_iters;     /* 50 */
+    double tol_gmres;     /* 1e-3 */
+    int max_gmres_iters;  /* 100 */
+    double mu0;           /* 1.0 */
+} ksvm_nfft_ipm_config;
+
+#define KSVM_NFFT_IPM_CONVERGED 0
+#define KSVM_NFFT_IPM_MAX_ITERATIONS 1
+#define KSVM_NFFT_IPM_STALLED 2
+
+typedef struct ksvm_nfft_ipm_result {
+    double lambda;
+    double mu_final;
+    double xi_alpha_rel;
+    double xi_lambda_rel;
+    int status;            /* KSVM_NFFT_IPM_* */
+    int iterations;
+    double mean_gmres_iters;
+} ksvm_nfft_ipm_result;
+
+typedef struct ksvm_nfft_ipm_log {
+    int it;
+    double mu;
+    double xi_alpha_rel;
+    double xi_lambda_rel;
+    double step_alpha;
+    int gmres_iterations;
+    double gmres_relative_residual;
+    int gmres_converged;
+    int gmres_breakdown;
+} ksvm_nfft_ipm_log;
+
+void ksvm_nfft_ipm_config_default(ksvm_nfft_ipm_config* cfg);
+int ksvm_nfft_ipm_train(const ksvm_nfft_op* op, const double* y, const double* Z, int k,
+                        const ksvm_nfft_ipm_config* cfg, double* alpha, ksvm_nfft_ipm_result* result,
+                        ksvm_nfft_ipm_log* log);
+
+/* compute_bias (P:src/ipm.cpp:157-185): mean of y_j - (K(alpha.*y))_j over
+ * free support vectors (eps_sv < alpha_j < C - eps_sv), else the median
+ * over all support vectors, else 0. Host arrays of op_size entries;
+ * n_support (may be NULL) returns #{alpha_j > eps_sv}. */
+int ksvm_nfft_compute_bias(const ksvm_nfft_op* op, const double* alpha, const double* y, double C,
+                           double eps_sv, double* bias, int64_t* n_support);
+
+/* balance_and_split (P:src/dataset.cpp:212-262) as row indices: the
+ * reference's std::mt19937_64(seed) + std::shuffle stream, the training part
+ * balanced by down-sampling the majority class and sorted. train_idx and
+ * test_idx need room for n entries. Bad fraction / one class / too few
+ * points: status 2 (DataError) with the reference's messages. CPU only. */
+int ksvm_nfft_balance_and_split(const double* labels, int64_t n, double train_fraction, uint64_t seed,
+                                int64_t* train_idx, int64_t* n_train, int64_t* test_idx, int64_t* n_test);
 void ksvm_nfft_op_free(ksvm_nfft_op* op);
 
 #ifdef __cplusplus

@@ -484,3 +484,41 @@ def blobs(n, d, gap, seed, noise=0.5):
     lab = np.empty(n)
     L.oracle_blobs(n, d, gap, seed, noise, _ptr(pts), _ptr(lab))
     return pts.reshape(d, n).T.copy(), lab
+
+
+# --- training-data preparation (P:src/dataset.cpp:212-282) -------------------
+def balance_and_split(labels, train_fraction=0.5, seed=0, kind="oracle"):
+    """balance_and_split as (train_idx sorted, test_idx) row indices; kind
+    "ref" runs the reference's own dataset.cpp (oracle/_ref)."""
+    L = Lib(kind).L
+    f = getattr(L, kind + "_balance_and_split")
+    lp = C.POINTER(C.c_int64)
+    f.restype = C.c_int
+    f.argtypes = [_dp, C.c_int64, C.c_double, C.c_uint64, lp, lp, lp, lp]
+    lab = _f64(labels)
+    n = lab.shape[0]
+    tr = np.zeros(max(n, 1), dtype=np.int64)
+    te = np.zeros(max(n, 1), dtype=np.int64)
+    ntr, nte = C.c_int64(0), C.c_int64(0)
+    code = f(_ptr(lab), n, float(train_fraction), int(seed), tr.ctypes.data_as(lp), C.byref(ntr),
+             te.ctypes.data_as(lp), C.byref(nte))
+    if code != 0:
+        raise OracleError(code, "balance_and_split failed")
+    return tr[: ntr.value].copy(), te[: nte.value].copy()
+
+
+def zscore(train, test=None, kind="oracle"):
+    """zscore_fit_transform: returns (train_z, test_z, means, stddevs)."""
+    L = Lib(kind).L
+    f = getattr(L, kind + "_zscore")
+    f.restype = C.c_int
+    f.argtypes = [_dp, C.c_int64, _dp, C.c_int64, C.c_int, _dp, _dp]
+    tr = np.asfortranarray(np.asarray(train, dtype=np.float64))
+    n, d = tr.shape
+    te = None if test is None else np.asfortranarray(np.asarray(test, dtype=np.float64))
+    nt = 0 if te is None else te.shape[0]
+    mu, sd = np.zeros(d), np.zeros(d)
+    code = f(tr.ctypes.data_as(_dp), n, None if te is None else te.ctypes.data_as(_dp), nt, d, _ptr(mu), _ptr(sd))
+    if code != 0:
+        raise OracleError(code, "zscore failed")
+    return np.ascontiguousarray(tr), None if te is None else np.ascontiguousarray(te), mu, sd

@@ -46,10 +46,21 @@ extern "C" {
                         int sigma, double torus_radius, double fit, P##anova** out);     \
     int P##anova_apply(const P##anova* op, const double* v, double* out);               \
     double P##anova_entry(const P##anova* op, int64_t i, int64_t j);                     \
-    void P##anova_free(P##anova* op);
+    void P##anova_free(P##anova* op);                                                    \
+    int P##balance_and_split(const double* labels, int64_t n, double train_fraction,     \
+                             uint64_t seed, int64_t* train_idx, int64_t* n_train,        \
+                             int64_t* test_idx, int64_t* n_test);                        \
+    int P##zscore(double* train_cm, int64_t n_train, double* test_cm, int64_t n_test,    \
+                  int d, double* means, double* stddevs);
 
 KSVM_ORACLE_DECLARE(oracle_)
 KSVM_ORACLE_DECLARE(ref_)
+
+/* balance_and_split (P:src/dataset.cpp:212-262) as row indices (train
+ * sorted, test in shuffled order; arrays of room n) and
+ * zscore_fit_transform (:264-282) in place on column-major n x d matrices
+ * (test may be NULL when n_test == 0); means / stddevs receive the d
+ * FeatureStats. */
 
 /* Input generators matching P:tests/helpers.hpp:15-31 (libstdc++
  * std::mt19937_64 + std::normal_distribution, row-by-row fill). Output of

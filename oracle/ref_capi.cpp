@@ -12,6 +12,7 @@
 #include "ksvm/fastsum.hpp"
 #include "ksvm/kernel.hpp"
 #include "ksvm/windowing.hpp"
+#include "ksvm/dataset.hpp"
 #include "ksvm_oracle.h"
 
 namespace {
@@ -142,3 +143,40 @@ double ref_anova_entry(const ref_anova* op, int64_t i, int64_t j) { return op->o
 void ref_anova_free(ref_anova* op) { delete op; }
 
 }  // extern "C"
+
+// ---- P:src/dataset.cpp: the reference's own split / z-score ---------------
+// balance_and_split returns datasets, not indices: the wrapper feeds a 1-column
+// dataset whose entries are the row numbers and reads them back.
+extern "C" int ref_balance_and_split(const double* labels, int64_t n, double train_fraction, uint64_t seed,
+                                     int64_t* train_idx, int64_t* n_train, int64_t* test_idx, int64_t* n_test) {
+    return guard([&] {
+        ksvm::Dataset d;
+        d.points = Eigen::MatrixXd(n, 1);
+        d.labels = Eigen::VectorXd(n);
+        for (int64_t i = 0; i < n; ++i) {
+            d.points(i, 0) = static_cast<double>(i);
+            d.labels[i] = labels[i];
+        }
+        auto [tr, te] = ksvm::balance_and_split(d, train_fraction, seed);
+        *n_train = tr.n();
+        *n_test = te.n();
+        for (int64_t i = 0; i < tr.n(); ++i) train_idx[i] = static_cast<int64_t>(tr.points(i, 0));
+        for (int64_t i = 0; i < te.n(); ++i) test_idx[i] = static_cast<int64_t>(te.points(i, 0));
+    });
+}
+
+extern "C" int ref_zscore(double* train_cm, int64_t n_train, double* test_cm, int64_t n_test, int d, double* means,
+                          double* stddevs) {
+    return guard([&] {
+        ksvm::Dataset tr, te;
+        tr.points = colmajor(train_cm, n_train, d);
+        te.points = n_test > 0 ? colmajor(test_cm, n_test, d) : Eigen::MatrixXd(0, d);
+        ksvm::zscore_fit_transform(tr, te);
+        std::memcpy(train_cm, tr.points.data(), sizeof(double) * static_cast<std::size_t>(n_train * d));
+        if (n_test > 0) std::memcpy(test_cm, te.points.data(), sizeof(double) * static_cast<std::size_t>(n_test * d));
+        for (int j = 0; j < d; ++j) {
+            means[j] = (*tr.normalization)[static_cast<std::size_t>(j)].mean;
+            stddevs[j] = (*tr.normalization)[static_cast<std::size_t>(j)].stddev;
+        }
+    });
+}

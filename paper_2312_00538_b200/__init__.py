@@ -11,6 +11,10 @@ from .fastsum import (AnovaFastOperator, AnovaKernelSpec, Dataset, DomainError, 
                       plan_fastsum)
 from .lowrank import LowRankFactor, pivoted_cholesky_greedy, stack_anova_factors
 from .saddle import GmresStats, SaddleOperator, SaddlePreconditioner, gmres_solve
+from .ipm import (FeatureStats, IpmConfig, IpmResult, IpmStatus, TrainedModel, apply_normalization, compute_bias,
+                  dual_objective, ipm_train, make_model)
+from .pipeline import (PipelineConfig, TrainReport, balance_and_split, build_precond_factor, parse_window_spec,
+                       train_on_prepared, train_pipeline, zscore_fit_transform)
 
 __all__ = [
     "AnovaFastOperator", "AnovaKernelSpec", "Dataset", "DomainError", "FastsumConfig",
@@ -18,4 +22,8 @@ __all__ = [
     "anova_fast_operator", "apply_fastsum", "apply_fastsum_cross", "decision_values", "plan_fastsum",
     "GmresStats", "SaddleOperator", "SaddlePreconditioner", "gmres_solve",
     "LowRankFactor", "pivoted_cholesky_greedy", "stack_anova_factors",
+    "FeatureStats", "IpmConfig", "IpmResult", "IpmStatus", "TrainedModel", "apply_normalization", "compute_bias",
+    "dual_objective", "ipm_train", "make_model",
+    "PipelineConfig", "TrainReport", "balance_and_split", "build_precond_factor", "parse_window_spec",
+    "train_on_prepared", "train_pipeline", "zscore_fit_transform",
 ]

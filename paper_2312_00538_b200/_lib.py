@@ -24,6 +24,24 @@ class GmresStats(C.Structure):
                 ("converged", C.c_int), ("breakdown", C.c_int)]
 
 
+class IpmConfig(C.Structure):
+    _fields_ = [("C", C.c_double), ("sigma", C.c_double), ("gamma0", C.c_double), ("tol_ip", C.c_double),
+                ("max_ip_iters", C.c_int), ("tol_gmres", C.c_double), ("max_gmres_iters", C.c_int),
+                ("mu0", C.c_double)]
+
+
+class IpmResult(C.Structure):
+    _fields_ = [("lambda_", C.c_double), ("mu_final", C.c_double), ("xi_alpha_rel", C.c_double),
+                ("xi_lambda_rel", C.c_double), ("status", C.c_int), ("iterations", C.c_int),
+                ("mean_gmres_iters", C.c_double)]
+
+
+class IpmLog(C.Structure):
+    _fields_ = [("it", C.c_int), ("mu", C.c_double), ("xi_alpha_rel", C.c_double), ("xi_lambda_rel", C.c_double),
+                ("step_alpha", C.c_double), ("gmres_iterations", C.c_int), ("gmres_relative_residual", C.c_double),
+                ("gmres_converged", C.c_int), ("gmres_breakdown", C.c_int)]
+
+
 class Config(C.Structure):
     _fields_ = [("bandwidth", C.c_int), ("window_cutoff", C.c_int),
                 ("oversampling", C.c_int), ("torus_radius", C.c_double)]
@@ -79,6 +97,14 @@ _SIGS = {
     "ksvm_nfft_precond_diagonal_fallback": (C.c_int, [_vp]),
     "ksvm_nfft_precond_free": (None, [_vp]),
     "ksvm_nfft_gmres_solve": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_int, _vp, _vp, _vp, C.c_int, _vp]),
+    "ksvm_nfft_saddle_set_theta_ex": (C.c_int, [_vp, _vp, C.c_int, _vp]),
+    "ksvm_nfft_precond_refresh_ex": (C.c_int, [_vp, _vp, C.c_int, _vp]),
+    # interior point trainer
+    "ksvm_nfft_ipm_config_default": (None, [C.POINTER(IpmConfig)]),
+    "ksvm_nfft_ipm_train": (C.c_int, [_vp, _vp, _vp, C.c_int, C.POINTER(IpmConfig), _vp, C.POINTER(IpmResult),
+                                      C.POINTER(IpmLog)]),
+    "ksvm_nfft_compute_bias": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_double, _dp, _lp]),
+    "ksvm_nfft_balance_and_split": (C.c_int, [_vp, C.c_int64, C.c_double, C.c_uint64, _vp, _lp, _vp, _lp]),
     # prediction
     "ksvm_nfft_decision_values": (C.c_int, [_vp, C.c_int64, C.c_int, C.c_int64, C.c_int, _vp, _vp, C.c_int, _vp,
                                             _vp, C.POINTER(Config), _vp, C.c_double, _vp, C.c_int64, C.c_int64,

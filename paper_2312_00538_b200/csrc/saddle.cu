@@ -27,55 +27,13 @@
 
 #include "capi_common.cuh"
 #include "launch.cuh"
+#include "reduce.cuh"
 
 namespace ksvm_nfft {
 namespace {
 
-constexpr int kRB = 296;   // reduction blocks: fixed, so partial sums have a fixed order
-constexpr int kRT = 256;   // threads per reduction block
 constexpr int kRows = 8;   // basis rows per pass of the multi-dot kernel
 constexpr int kMaxRank = 1024;
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-// Warp sum of p[q * stride] for q < count <= kRB (one warp): every load is
-// issued before the adds (fixed lane assignment, fixed order), so a finisher
-// costs one L2 round trip instead of one per element.
-__device__ __forceinline__ double warp_sum_strided(const double* __restrict__ p, int count, long long stride) {
-    constexpr int kPer = (kRB + 31) / 32;
-    const int lane = threadIdx.x & 31;
-    double v[kPer];
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-        const int q = lane + 32 * j;
-        v[j] = q < count ? p[static_cast<long long>(q) * stride] : 0.0;
-    }
-    double s = 0.0;
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) s += v[j];
-    return warp_sum(s);
-}
-
-// Block b owns indices b*kRT + t + q*kRB*kRT; its sum is written to
-// partial[b] (lane butterfly, then warps in order).
-__device__ __forceinline__ void block_partial(double v, double* partial) {
-    __shared__ double sh[kRT / 32];
-    v = warp_sum(v);
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int w = 0; w < kRT / 32; ++w) s += sh[w];
-        partial[blockIdx.x] = s;
-    }
-}
-
-#define KSVM_FOR_BLOCK_INDEX(i, L) \
-    for (long long i = static_cast<long long>(blockIdx.x) * kRT + threadIdx.x; i < (L); i += static_cast<long long>(kRB) * kRT)
 
 __global__ void __launch_bounds__(kRT) k_mul(double* __restrict__ out, const double* __restrict__ a,
                                              const double* __restrict__ b, long long n,
@@ -545,7 +503,7 @@ __global__ void gk_norm_givens(const double* __restrict__ npartial, int nb, doub
 }
 
 
-int blocks_for(long long L) { return static_cast<int>(std::min<long long>(kRB, (L + kRT - 1) / kRT)); }
+int blocks_for(long long L) { return reduce_blocks(L); }
 
 }  // namespace
 }  // namespace ksvm_nfft
@@ -593,6 +551,30 @@ void check_theta(const double* theta, int64_t n, const char* who) {
         if (!(theta[j] > 0.0)) throw std::invalid_argument(std::string(who) + ": Theta must be positive");
 }
 
+// count of entries that are not > 0 (NaN included)
+__global__ void __launch_bounds__(kRT) k_count_nonpositive(const double* __restrict__ theta, long long n,
+                                                           int* __restrict__ bad) {
+    int c = 0;
+    KSVM_FOR_BLOCK_INDEX(j, n) c += !(theta[j] > 0.0);
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(bad, c);
+}
+
+// Device-side check_theta: one small kernel and a 4-byte read back (syncs st).
+void check_theta_dev(const double* theta, int64_t n, cudaStream_t st, const char* who) {
+    if (!theta) throw std::invalid_argument(std::string(who) + ": null Theta");
+    DevBuf<int> bad;
+    bad.alloc(1);
+    CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+    k_count_nonpositive<<<blocks_for(n), kRT, 0, st>>>(theta, n, bad.p);
+    ++launch_counter();
+    CK(cudaGetLastError());
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h) throw std::invalid_argument(std::string(who) + ": Theta must be positive");
+}
+
 // out = A vw (device vectors of length n + 1), P:src/saddle.cpp:22-33
 void saddle_apply_dev(const ksvm_nfft_saddle& S, const double* vw, double* out, cudaStream_t st,
                       const int* stop = nullptr) {
@@ -633,11 +615,19 @@ void precond_apply_dev(const ksvm_nfft_precond& P, const double* g, double* out,
 }
 
 // Capacitance I + Z Theta^{-1} Z^T, partial-pivot LU, rcond, inverse.
-void precond_refresh(ksvm_nfft_precond& P, const double* theta_h) {
-    check_theta(theta_h, P.n, "SaddlePreconditioner");
+// Theta on the host (device == false, P's own stream) or on the device
+// (ordered on the caller's stream st).
+void precond_refresh(ksvm_nfft_precond& P, const double* theta_in, bool device, cudaStream_t st) {
     const long long n = P.n;
-    cudaStream_t st = P.stream;
-    P.theta.upload(theta_h, static_cast<size_t>(n), st);
+    if (device) {
+        check_theta_dev(theta_in, n, st, "SaddlePreconditioner");
+        if (P.theta.n < static_cast<size_t>(n)) P.theta.alloc(static_cast<size_t>(n));
+        CK(cudaMemcpyAsync(P.theta.p, theta_in, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    } else {
+        check_theta(theta_in, P.n, "SaddlePreconditioner");
+        st = P.stream;
+        P.theta.upload(theta_in, static_cast<size_t>(n), st);
+    }
     P.fallback = false;
     P.fresh = true;
     if (P.identity || P.k == 0) {
@@ -781,6 +771,26 @@ int ksvm_nfft_saddle_apply(const ksvm_nfft_saddle* s, const double* vw, double* 
     });
 }
 
+int ksvm_nfft_saddle_set_theta_ex(ksvm_nfft_saddle* s, const double* theta, int ptr_kind, void* stream) {
+    return guarded([&] {
+        if (!s) throw std::invalid_argument("null saddle operator");
+        if (ptr_kind == KSVM_NFFT_HOST) {
+            check_theta(theta, s->n, "SaddleOperator");
+            std::lock_guard<std::mutex> lk(s->mu);
+            DeviceGuard dg(s->device);
+            CK(cudaMemcpyAsync(s->theta.p, theta, sizeof(double) * s->n, cudaMemcpyHostToDevice, s->stream));
+            CK(cudaStreamSynchronize(s->stream));
+            return;
+        }
+        if (ptr_kind != KSVM_NFFT_DEVICE) throw std::invalid_argument("bad ptr_kind");
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard dg(s->device);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        check_theta_dev(theta, s->n, st, "SaddleOperator");
+        CK(cudaMemcpyAsync(s->theta.p, theta, sizeof(double) * s->n, cudaMemcpyDeviceToDevice, st));
+    });
+}
+
 void ksvm_nfft_saddle_free(ksvm_nfft_saddle* s) { delete s; }
 
 int ksvm_nfft_precond_create(const double* Z, int k, int64_t n, const double* y, int device, ksvm_nfft_precond** out) {
@@ -809,7 +819,17 @@ int ksvm_nfft_precond_refresh(ksvm_nfft_precond* p, const double* theta) {
         if (!p) throw std::invalid_argument("null preconditioner");
         std::lock_guard<std::mutex> lk(p->mu);
         DeviceGuard dg(p->device);
-        precond_refresh(*p, theta);
+        precond_refresh(*p, theta, false, nullptr);
+    });
+}
+
+int ksvm_nfft_precond_refresh_ex(ksvm_nfft_precond* p, const double* theta, int ptr_kind, void* stream) {
+    return guarded([&] {
+        if (!p) throw std::invalid_argument("null preconditioner");
+        if (ptr_kind != KSVM_NFFT_HOST && ptr_kind != KSVM_NFFT_DEVICE) throw std::invalid_argument("bad ptr_kind");
+        std::lock_guard<std::mutex> lk(p->mu);
+        DeviceGuard dg(p->device);
+        precond_refresh(*p, theta, ptr_kind == KSVM_NFFT_DEVICE, static_cast<cudaStream_t>(stream));
     });
 }
 

@@ -1,0 +1,213 @@
+"""End-to-end training on the B200 path: Python mirror of the reference's
+pipeline (P:include/ksvm/pipeline.hpp, P:src/pipeline.cpp) for the parts
+that reach the hot path:
+
+    model, test, report = train_pipeline(Dataset(X, y), PipelineConfig(
+        explicit_windows=[[0, 1, 2], [3, 4, 5]], rank=50, ipm=IpmConfig(C=1.0)))
+    acc = (model.predict(test_raw_points) == test.labels).mean()
+
+balance_and_split -> zscore_fit_transform -> explicit windows (eta = 1/P,
+ell = 1) -> GPU greedy pivoted-Cholesky factor per window, stacked with
+sqrt(eta) -> GPU interior point loop over the NFFT operator (fit 1/1.2) ->
+compute_bias -> TrainedModel (GPU prediction). Mutual-information windowing
+and the randomized factorizations are outside this path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import _lib
+from .fastsum import (AnovaKernelSpec, Dataset, FastsumConfig, FeatureWindowing, _raise, anova_fast_operator)
+from .ipm import FeatureStats, IpmConfig, IpmResult, IpmStatus, TrainedModel, ipm_train, make_model
+from .lowrank import pivoted_cholesky_greedy, stack_anova_factors
+
+PRECOND_METHODS = ("none", "cholesky-greedy")  # P:src/pipeline.cpp:8-18 (the ones on this path)
+
+
+@dataclass
+class PipelineConfig:
+    """P:include/ksvm/pipeline.hpp:32-47 (defaults kept)."""
+    train_fraction: float = 0.5
+    seed: int = 0
+    explicit_windows: list = field(default_factory=list)   # [[0, 1, 2], [3, 4]] (0-based)
+    length_scales: list = field(default_factory=list)      # empty = 1 per window; 1 entry = shared
+    precond: str = "cholesky-greedy"
+    rank: int = 200
+    per_window_ranks: list = field(default_factory=list)
+    cholesky_err_tol: float = 1e-5
+    fastsum: FastsumConfig = field(default_factory=FastsumConfig)
+    ipm: IpmConfig = field(default_factory=IpmConfig)
+    device: int = 0
+
+
+@dataclass
+class TrainReport:
+    """P:include/ksvm/pipeline.hpp:49-63."""
+    n_train: int = 0
+    n_test: int = 0
+    d: int = 0
+    P: int = 0
+    rank: int = 0
+    fit_seconds: float = 0.0
+    precond_setup_seconds: float = 0.0
+    ipm_iters: int = 0
+    mean_gmres: float = 0.0
+    xi_alpha: float = 0.0
+    xi_lambda: float = 0.0
+    mu_final: float = 0.0
+    status: IpmStatus = IpmStatus.CONVERGED
+
+
+def parse_window_spec(spec: str, d: int) -> List[List[int]]:
+    """P:src/pipeline.cpp:28-52: "0,1,2;3,4" -> [[0, 1, 2], [3, 4]]."""
+    windows = []
+    for group in spec.split(";"):
+        win = []
+        for item in group.split(","):
+            if not item:
+                continue
+            try:
+                f = int(item)
+            except ValueError:
+                raise ValueError(f"bad window spec item: '{item}'") from None
+            if f < 0 or f >= d:
+                raise ValueError(f"window feature index out of range: {item}")
+            win.append(f)
+        if win:
+            windows.append(win)
+    if not windows:
+        raise ValueError(f"window spec has no windows: '{spec}'")
+    return windows
+
+
+def balance_and_split(data: Dataset, train_fraction: float = 0.5, seed: int = 0):
+    """balance_and_split (P:src/dataset.cpp:212-262): the reference's
+    std::mt19937_64 / std::shuffle stream (libksvm_nfft.so), so the split is
+    the reference's. Returns (train, test) Datasets."""
+    lab = np.ascontiguousarray(np.asarray(data.labels, dtype=np.float64).reshape(-1))
+    n = lab.shape[0]
+    tr = np.zeros(max(n, 1), dtype=np.int64)
+    te = np.zeros(max(n, 1), dtype=np.int64)
+    ntr, nte = C.c_int64(0), C.c_int64(0)
+    _raise(_lib.load().ksvm_nfft_balance_and_split(C.c_void_p(lab.ctypes.data), n, float(train_fraction), int(seed),
+                                                   C.c_void_p(tr.ctypes.data), C.byref(ntr),
+                                                   C.c_void_p(te.ctypes.data), C.byref(nte)))
+    tr, te = tr[: ntr.value], te[: nte.value]
+    pts = np.asarray(data.points, dtype=np.float64)
+    return Dataset(pts[tr].copy(), lab[tr].copy()), Dataset(pts[te].copy(), lab[te].copy())
+
+
+def zscore_fit_transform(train: Dataset, test: Dataset):
+    """zscore_fit_transform (P:src/dataset.cpp:264-282): per-feature mean and
+    population standard deviation of the training part (sd < 1e-300 -> 1),
+    applied to both parts. Returns the FeatureStats list."""
+    if train.n() == 0:
+        raise ValueError("empty training split")
+    X = np.asarray(train.points, dtype=np.float64)
+    n = X.shape[0]
+    stats = []
+    Xo = np.empty_like(X)
+    T = np.asarray(test.points, dtype=np.float64) if test is not None and test.n() > 0 else None
+    To = None if T is None else np.empty_like(T)
+    for j in range(X.shape[1]):
+        col = X[:, j]
+        mean = float(col.sum() / n)
+        sd = float(np.sqrt(((col - mean) ** 2).sum() / n))
+        if sd < 1e-300:
+            sd = 1.0
+        stats.append(FeatureStats(mean, sd))
+        Xo[:, j] = (col - mean) / sd
+        if T is not None:
+            To[:, j] = (T[:, j] - mean) / sd
+    train.points = Xo
+    if To is not None:
+        test.points = To
+    return stats
+
+
+def window_ranks(cfg: PipelineConfig, P: int, n: int) -> List[int]:
+    """P:src/pipeline.cpp:73-86."""
+    if cfg.per_window_ranks:
+        if len(cfg.per_window_ranks) != P:
+            raise ValueError("per_window_ranks size must equal P")
+        ranks = list(cfg.per_window_ranks)
+    else:
+        ranks = [max(1, cfg.rank // P)] * P
+    return [min(int(r), n) for r in ranks]
+
+
+def build_precond_factor(op, train: Dataset, spec: AnovaKernelSpec, cfg: PipelineConfig):
+    """build_precond_factor (P:src/pipeline.cpp:137-196) for greedy pivoted
+    Cholesky: one WindowOperator factor per window on the GPU (exact entries
+    on the window's coordinates), stacked with sqrt(eta_l). Returns
+    (Z k x n, setup seconds)."""
+    if cfg.precond != "cholesky-greedy":
+        raise ValueError(f"preconditioner '{cfg.precond}' is not on the B200 path "
+                         f"(supported: {', '.join(PRECOND_METHODS)})")
+    w = spec.windowing
+    P = w.num_windows()
+    ranks = window_ranks(cfg, P, train.n())
+    t0 = time.perf_counter()
+    factors = [pivoted_cholesky_greedy(op, ranks[l], cfg.cholesky_err_tol, window=l) for l in range(P)]
+    Z = stack_anova_factors(factors, w.weights)
+    return Z, time.perf_counter() - t0
+
+
+def train_on_prepared(train: Dataset, spec: AnovaKernelSpec, cfg: PipelineConfig, report: TrainReport,
+                      normalization=None):
+    """train_on_prepared (P:src/pipeline.cpp:198-227) with the fast backend:
+    returns (TrainedModel, IpmResult)."""
+    t0 = time.perf_counter()
+    op = anova_fast_operator(train, spec, cfg.fastsum, 1.0 / 1.2, device=cfg.device)
+    Z = None
+    if cfg.precond != "none":
+        Z, report.precond_setup_seconds = build_precond_factor(op, train, spec, cfg)
+    res = ipm_train(op, train.labels, Z, cfg.ipm)
+    model = make_model(res, train, spec, cfg.fastsum, op, cfg.ipm.C, normalization)
+    report.n_train = train.n()
+    report.d = train.dim()
+    report.P = spec.windowing.num_windows()
+    report.rank = 0 if Z is None else int(Z.shape[0])
+    report.fit_seconds = time.perf_counter() - t0
+    report.ipm_iters = len(res.iterations)
+    report.mean_gmres = res.mean_gmres_iters()
+    report.xi_alpha = res.xi_alpha_rel
+    report.xi_lambda = res.xi_lambda_rel
+    report.mu_final = res.mu_final
+    report.status = res.status
+    return model, res
+
+
+def train_pipeline(raw: Dataset, cfg: PipelineConfig):
+    """train_pipeline (P:src/pipeline.cpp:229-265) with explicit windows:
+    returns (TrainedModel, normalized test Dataset, TrainReport, IpmResult)."""
+    train, test = balance_and_split(raw, cfg.train_fraction, cfg.seed)
+    stats = zscore_fit_transform(train, test)
+    if not cfg.explicit_windows:
+        raise ValueError("mutual-information windowing is outside the B200 path: pass explicit_windows")
+    windows = cfg.explicit_windows
+    if isinstance(windows, str):
+        windows = parse_window_spec(windows, train.dim())
+    for win in windows:
+        for f in win:
+            if f < 0 or f >= train.dim():
+                raise ValueError(f"window feature index out of range: {f}")
+    wnd = FeatureWindowing.explicit(windows)
+    if cfg.length_scales:
+        P = wnd.num_windows()
+        if len(cfg.length_scales) == 1:
+            wnd.length_scales = [float(cfg.length_scales[0])] * P
+        elif len(cfg.length_scales) == P:
+            wnd.length_scales = [float(x) for x in cfg.length_scales]
+        else:
+            raise ValueError("length_scales must have 1 or P entries")
+    spec = AnovaKernelSpec(wnd)
+    report = TrainReport()
+    model, res = train_on_prepared(train, spec, cfg, report, stats)
+    report.n_test = test.n()
+    return model, test, report, res

@@ -1,0 +1,145 @@
+"""GPU: the GPU-resident interior point trainer (csrc/ipm.cu) and the
+end-to-end pipeline against the oracle restatements of P:src/ipm.cpp,
+P:src/low_rank.cpp, P:src/dataset.cpp (pinned to the reference's tests in
+tests/test_oracle_ipm.py, tests/test_oracle_lowrank.py and
+tests/test_pipeline_host.py), with K the same NFFT ANOVA operator (fit
+1/1.2, P:src/pipeline.cpp:202) on both sides.
+
+What must agree: the IPM trajectory (status, iteration count, GMRES
+iterations per step), the dual objective 1'a - a'YKYa/2 (1e-9 relative),
+alpha (1e-6 relative: GMRES stops at a 1e-3 residual, so rounding-level
+differences of the two matvecs and of classical vs modified Gram-Schmidt
+are carried into each Newton step), the bias and the predicted labels.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2312_00538_b200 import (AnovaKernelSpec, Dataset, FeatureWindowing, IpmConfig, IpmStatus,
+                                   PipelineConfig, anova_fast_operator, compute_bias, dual_objective, ipm_train,
+                                   train_pipeline, workloads)
+
+pytestmark = pytest.mark.gpu
+
+FIT = 1.0 / 1.2
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def ops(pts, windows):
+    P = len(windows)
+    spec = AnovaKernelSpec(FeatureWindowing([list(w) for w in windows], [1.0 / P] * P, [1.0] * P))
+    return anova_fast_operator(Dataset(pts), spec, fit_fraction=FIT), oracle.Lib("oracle").anova(pts, windows, fit=FIT)
+
+
+def dual(alpha, y, Ko):
+    ya = y * alpha
+    return alpha.sum() - 0.5 * ya @ Ko.apply(ya)
+
+
+def check_same_run(res, alpha_o, r_o, log_o, y, Ko, alpha_tol=1e-6):
+    assert res.status.name.lower() == r_o["status"]
+    assert len(res.iterations) == r_o["iterations"]
+    assert [it.gmres.iterations for it in res.iterations] == [int(x) for x in log_o[:, 4]]
+    assert np.allclose([it.mu for it in res.iterations], log_o[:, 0], rtol=1e-14)
+    assert rel(res.alpha, alpha_o) <= alpha_tol
+    assert abs(res.lambda_ - r_o["lambda"]) <= 1e-6 * max(1.0, abs(r_o["lambda"]))
+    assert abs(res.xi_lambda_rel - r_o["xi_lambda_rel"]) <= 1e-5 * max(r_o["xi_lambda_rel"], 1e-3)
+    d_gpu, d_o = dual(res.alpha, y, Ko), dual(alpha_o, y, Ko)
+    assert abs(d_gpu - d_o) <= 1e-9 * abs(d_o)
+
+
+@pytest.mark.parametrize("n,seed", [(200, 11), (600, 23)])
+def test_ipm_unpreconditioned_matches_oracle(n, seed):
+    pts, y = oracle.blobs(n, 2, 3.0, seed)
+    K, Ko = ops(pts, [[0, 1]])
+    res = ipm_train(K, y, None, IpmConfig())
+    alpha_o, r_o, log_o = oracle.ipm_train(Ko, y)
+    check_same_run(res, alpha_o, r_o, log_o, y, Ko)
+    assert res.status == IpmStatus.CONVERGED
+    assert res.alpha.min() > 0.0 and res.alpha.max() < 0.5
+
+
+def test_ipm_preconditioned_matches_oracle():
+    pts, y = oracle.blobs(800, 3, 2.0, 31)
+    windows = [[0, 1], [2]]
+    K, Ko = ops(pts, windows)
+    Zs = [oracle.pivoted_cholesky(pts, windows, window=l, rank=20, err_tol=1e-5)[0] for l in range(2)]
+    Z = np.vstack([np.sqrt(0.5) * z for z in Zs])
+    res = ipm_train(K, y, Z, IpmConfig(C=1.0))
+    alpha_o, r_o, log_o = oracle.ipm_train(Ko, y, Z, C=1.0)
+    check_same_run(res, alpha_o, r_o, log_o, y, Ko)
+    b = compute_bias(res.alpha, y, K, 1.0, 1e-4)
+    b_o = oracle.compute_bias(Ko, alpha_o, y, 1.0, 1e-4)
+    assert abs(b - b_o) <= 1e-6
+    assert abs(dual_objective(res.alpha, y, K) - dual(res.alpha, y, Ko)) <= 1e-10 * abs(dual(res.alpha, y, Ko))
+
+
+def test_ipm_deterministic():
+    pts, y = oracle.blobs(300, 2, 3.0, 19)
+    K, _ = ops(pts, [[0, 1]])
+    a = ipm_train(K, y)
+    b = ipm_train(K, y)
+    assert np.array_equal(a.alpha, b.alpha) and a.lambda_ == b.lambda_
+    assert [i.gmres.iterations for i in a.iterations] == [i.gmres.iterations for i in b.iterations]
+
+
+def test_ipm_errors():
+    pts, y = oracle.blobs(40, 2, 3.0, 3)
+    K, _ = ops(pts, [[0, 1]])
+    for bad in (dict(C=0.0), dict(sigma=1.0), dict(gamma0=0.0), dict(tol_ip=0.0), dict(max_ip_iters=0),
+                dict(mu0=-1.0)):
+        with pytest.raises(ValueError):
+            ipm_train(K, y, None, IpmConfig(**bad))
+    yb = y.copy()
+    yb[3] = 0.5
+    with pytest.raises(ValueError):
+        ipm_train(K, yb)
+    with pytest.raises(ValueError):
+        ipm_train(K, y[:-1])
+
+
+def test_compute_bias_rules_match_oracle():
+    pts, y = oracle.blobs(120, 2, 3.0, 5)
+    K, Ko = ops(pts, [[0, 1]])
+    rng = np.random.default_rng(0)
+    for alpha in (rng.uniform(0, 1, 120), np.where(rng.random(120) < 0.5, 1.0, 0.0), np.zeros(120)):
+        assert abs(compute_bias(alpha, y, K, 1.0, 1e-4) - oracle.compute_bias(Ko, alpha, y, 1.0, 1e-4)) <= 1e-10
+
+
+def oracle_pipeline(w, windows, rank, C, seed=0):
+    """train_pipeline restated on the oracle pieces (P:src/pipeline.cpp:229-265)."""
+    tr, te = oracle.balance_and_split(w.labels, 0.5, seed)
+    Xtr, Xte, mu, sd = oracle.zscore(w.points[tr], w.points[te])
+    ytr = w.labels[tr]
+    P = len(windows)
+    Zs = [oracle.pivoted_cholesky(Xtr, windows, window=l, rank=max(1, rank // P), err_tol=1e-5)[0]
+          for l in range(P)]
+    Z = np.vstack([np.sqrt(1.0 / P) * z for z in Zs])
+    Ko = oracle.Lib("oracle").anova(Xtr, windows, fit=FIT)
+    alpha, res, log = oracle.ipm_train(Ko, ytr, Z, C=C)
+    b = oracle.compute_bias(Ko, alpha, ytr, C, 1e-4 * C)
+    f, _ = oracle.decision_values(Xtr, windows, [1.0 / P] * P, [1.0] * P, alpha * ytr, b, Xte, fast=True)
+    return dict(tr=tr, te=te, alpha=alpha, res=res, log=log, bias=b, f=f, Ko=Ko, ytr=ytr, Z=Z)
+
+
+def test_pipeline_config1_matches_oracle():
+    """BASELINE config 1 end to end: split, z-score, greedy pivoted Cholesky
+    rank 50, IPM with C = 1, bias, fast prediction on the held-out split."""
+    w = workloads.config1()
+    windows = [[0, 1, 2], [3, 4, 5]]
+    ref = oracle_pipeline(w, windows, 50, 1.0)
+    model, test, report, res = train_pipeline(Dataset(w.points, w.labels), PipelineConfig(
+        explicit_windows=windows, rank=50, ipm=IpmConfig(C=1.0)))
+    assert report.n_train == len(ref["tr"]) and report.n_test == len(ref["te"]) == 1000
+    assert report.rank == ref["Z"].shape[0]
+    check_same_run(res, ref["alpha"], ref["res"], ref["log"], ref["ytr"], ref["Ko"])
+    assert abs(model.bias - ref["bias"]) <= 1e-6
+    f = model.decision_values(w.points[ref["te"]])
+    assert rel(f, ref["f"]) <= 1e-6
+    labels, labels_o = np.where(f >= 0, 1.0, -1.0), np.where(ref["f"] >= 0, 1.0, -1.0)
+    assert (labels == labels_o).mean() >= 0.999
+    assert (labels == w.labels[ref["te"]]).mean() >= 0.55  # oracle: 0.607 (IPM stops at tol_ip = 0.1)
