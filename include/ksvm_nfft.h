@@ -34,6 +34,13 @@
  * ksvm_nfft_gmres_solve            gmres_solve              P:include/ksvm/saddle.hpp:60-77, P:src/saddle.cpp:92-178
  * ksvm_nfft_pivoted_cholesky       pivoted_cholesky_greedy  P:include/ksvm/low_rank.hpp, P:src/low_rank.cpp:25-92
  * ksvm_nfft_decision_values        TrainedModel::decision_values  P:include/ksvm/ipm.hpp:51-69, P:src/ipm.cpp:213-288
+ * ksvm_nfft_saddle_set_theta_ex/   SaddleOperator(op, y, theta) per IPM step / refresh(theta) on device Theta
+ *   precond_refresh_ex                                      P:src/ipm.cpp:105-107, P:src/saddle.cpp:41-63
+ * ksvm_nfft_ipm_config_default/    IpmConfig / ipm_train    P:include/ksvm/ipm.hpp:15-49, P:src/ipm.cpp:76-155
+ *   ipm_train
+ * ksvm_nfft_compute_bias           compute_bias             P:src/ipm.cpp:157-185
+ * ksvm_nfft_nystrom                nystrom                  P:include/ksvm/low_rank.hpp:42-47, P:src/low_rank.cpp:115-168
+ * ksvm_nfft_balance_and_split      balance_and_split        P:include/ksvm/dataset.hpp, P:src/dataset.cpp:212-262
  *
  * Status values equal ksvm_status (P:capi/ksvm.h:17-23): 0 ok, 2 data/domain
  * error (DomainError, P:src/fastsum.cpp:316-320), 4 invalid argument
@@ -206,6 +213,22 @@ void ksvm_nfft_precond_free(ksvm_nfft_precond* p);
 int ksvm_nfft_pivoted_cholesky(const ksvm_nfft_op* op, int window, int rank, double err_tol, double* Z,
                                int* achieved_rank, double* trace_residual, int64_t* pivots, int ptr_kind,
                                void* stream);
+
+/* ---- Nystrom factor, GPU (P:src/low_rank.cpp:115-168) ----------------------
+ * nystrom(op, rank, mode, seed, ldl_threshold) -> Z (rank x n row-major,
+ * host or device per ptr_kind). GAUSSIAN sketches op's own applies (window
+ * must be -1): the reference builds it on the FastWindowOperator of one
+ * window (P:src/pipeline.cpp:172-181), i.e. a one-window operator with
+ * weight 1 and fit 1.0; Y = K G and KQ = K Q run as batched applies.
+ * COLUMNS takes exact kernel columns of `window` (>= 0: WindowOperator,
+ * -1: the ANOVA entries). The draws are the reference's
+ * (std::mt19937_64(seed)); Z^T Z equals the reference's to rounding (the
+ * orthonormal basis of range(Y) may differ by signs). rank outside
+ * [1, n]: status 4. */
+#define KSVM_NFFT_NYSTROM_COLUMNS 0
+#define KSVM_NFFT_NYSTROM_GAUSSIAN 1
+int ksvm_nfft_nystrom(const ksvm_nfft_op* op, int window, int rank, int mode, uint64_t seed,
+                      double ldl_threshold, double* Z, int ptr_kind, void* stream);
 
 /* ---- prediction, GPU -----------------------------------
  * TrainedModel::decision_values (P:src/ipm.cpp:213-288): f_j = sum_i coeff_i

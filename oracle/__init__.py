@@ -522,3 +522,50 @@ def zscore(train, test=None, kind="oracle"):
     if code != 0:
         raise OracleError(code, "zscore failed")
     return np.ascontiguousarray(tr), None if te is None else np.ascontiguousarray(te), mu, sd
+
+
+# --- Nystrom factor (oracle/nystrom_oracle.cpp, P:src/low_rank.cpp:115-168) ---
+NYSTROM_COLUMNS, NYSTROM_GAUSSIAN = 0, 1
+
+
+def _nystrom_lib():
+    L = Lib("oracle").L
+    if not getattr(L, "_nystrom_bound", False):
+        L.oracle_nystrom_last_error.restype = C.c_char_p
+        L.oracle_nystrom_dense.restype = C.c_int
+        L.oracle_nystrom_dense.argtypes = [_dp, C.c_int64, C.c_int, C.c_int, C.c_uint64, C.c_double, _dp]
+        L.oracle_nystrom_window.restype = C.c_int
+        L.oracle_nystrom_window.argtypes = [_dp, C.c_int64, C.c_int, _ip, C.c_int, C.c_double, C.c_void_p, C.c_int,
+                                            C.c_int, C.c_uint64, C.c_double, _dp]
+        L._nystrom_bound = True
+    return L
+
+
+def nystrom_dense(M, rank, mode, seed, ldl_threshold=1e-8):
+    """nystrom(DenseOperator(M), rank, mode, seed): Z (rank x n)."""
+    L = _nystrom_lib()
+    M = np.ascontiguousarray(M, dtype=np.float64)
+    n = M.shape[0]
+    Z = np.zeros(max(int(rank), 1) * n)
+    code = L.oracle_nystrom_dense(_ptr(M), n, int(rank), int(mode), int(seed), float(ldl_threshold), _ptr(Z))
+    if code != 0:
+        raise OracleError(code, L.oracle_nystrom_last_error().decode())
+    return Z.reshape(-1, n)[: int(rank)]
+
+
+def nystrom_window(pts, feats, ell, rank, mode, seed, ldl_threshold=1e-8, N=32, m=4, sigma=2, torus_radius=0.25):
+    """nystrom over one window of row-major points: mode 0 on the exact
+    WindowOperator, mode 1 on the FastWindowOperator (plan fit 1.0,
+    P:src/pipeline.cpp:114-133)."""
+    L = _nystrom_lib()
+    pts = np.ascontiguousarray(pts, dtype=np.float64)
+    n, d = pts.shape
+    f = np.ascontiguousarray(feats, dtype=np.int32)
+    plan = Lib("oracle").plan(pts[:, f], ell, N, m, sigma, torus_radius, 1.0) if mode == 1 else None
+    Z = np.zeros(max(int(rank), 1) * n)
+    code = L.oracle_nystrom_window(_ptr(pts), n, d, f.ctypes.data_as(_ip), len(f), float(ell),
+                                   plan.h if plan is not None else None, int(rank), int(mode), int(seed),
+                                   float(ldl_threshold), _ptr(Z))
+    if code != 0:
+        raise OracleError(code, L.oracle_nystrom_last_error().decode())
+    return Z.reshape(-1, n)[: int(rank)]

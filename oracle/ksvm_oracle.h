@@ -62,6 +62,16 @@ KSVM_ORACLE_DECLARE(ref_)
  * (test may be NULL when n_test == 0); means / stddevs receive the d
  * FeatureStats. */
 
+/* Nystrom factor (oracle/nystrom_oracle.cpp, restating P:src/low_rank.cpp:115-168):
+ * mode 0 kColumns, 1 kGaussian; Z_out rank x n row-major. _dense: the row-major
+ * n x n DenseOperator; _window: the window `feats` (nf of them) of row-major
+ * n x d points, exact WindowOperator (mode 0) or the FastWindowOperator plan
+ * `plan` (mode 1, built with fit 1.0 over those columns). */
+const char* oracle_nystrom_last_error(void);
+int oracle_nystrom_dense(const double* M, int64_t n, int rank, int mode, uint64_t seed, double thr, double* Z_out);
+int oracle_nystrom_window(const double* pts_rm, int64_t n, int d, const int* feats, int nf, double ell,
+                          const oracle_plan* plan, int rank, int mode, uint64_t seed, double thr, double* Z_out);
+
 /* Input generators matching P:tests/helpers.hpp:15-31 (libstdc++
  * std::mt19937_64 + std::normal_distribution, row-by-row fill). Output of
  * random_points is n x d COLUMN-major like the Eigen matrix it mirrors. */

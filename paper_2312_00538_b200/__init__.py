@@ -9,7 +9,7 @@ from .fastsum import (AnovaFastOperator, AnovaKernelSpec, Dataset, DomainError, 
                       FastsumPlan, FeatureWindowing, GaussianKernelSpec, KernelOperator,
                       anova_fast_operator, apply_fastsum, apply_fastsum_cross, decision_values,
                       plan_fastsum)
-from .lowrank import LowRankFactor, pivoted_cholesky_greedy, stack_anova_factors
+from .lowrank import LowRankFactor, fast_window_operator, nystrom, pivoted_cholesky_greedy, stack_anova_factors
 from .saddle import GmresStats, SaddleOperator, SaddlePreconditioner, gmres_solve
 from .ipm import (FeatureStats, IpmConfig, IpmResult, IpmStatus, TrainedModel, apply_normalization, compute_bias,
                   dual_objective, ipm_train, make_model)
@@ -21,7 +21,7 @@ __all__ = [
     "FastsumPlan", "FeatureWindowing", "GaussianKernelSpec", "KernelOperator",
     "anova_fast_operator", "apply_fastsum", "apply_fastsum_cross", "decision_values", "plan_fastsum",
     "GmresStats", "SaddleOperator", "SaddlePreconditioner", "gmres_solve",
-    "LowRankFactor", "pivoted_cholesky_greedy", "stack_anova_factors",
+    "LowRankFactor", "fast_window_operator", "nystrom", "pivoted_cholesky_greedy", "stack_anova_factors",
     "FeatureStats", "IpmConfig", "IpmResult", "IpmStatus", "TrainedModel", "apply_normalization", "compute_bias",
     "dual_objective", "ipm_train", "make_model",
     "PipelineConfig", "TrainReport", "balance_and_split", "build_precond_factor", "parse_window_spec",

@@ -104,6 +104,7 @@ _SIGS = {
     "ksvm_nfft_ipm_train": (C.c_int, [_vp, _vp, _vp, C.c_int, C.POINTER(IpmConfig), _vp, C.POINTER(IpmResult),
                                       C.POINTER(IpmLog)]),
     "ksvm_nfft_compute_bias": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_double, _dp, _lp]),
+    "ksvm_nfft_nystrom": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_double, _vp, C.c_int, _vp]),
     "ksvm_nfft_balance_and_split": (C.c_int, [_vp, C.c_int64, C.c_double, C.c_uint64, _vp, _lp, _vp, _lp]),
     # prediction
     "ksvm_nfft_decision_values": (C.c_int, [_vp, C.c_int64, C.c_int, C.c_int64, C.c_int, _vp, _vp, C.c_int, _vp,

@@ -59,3 +59,36 @@ def stack_anova_factors(factors, weights) -> np.ndarray:
     if not factors or len(factors) != len(weights):
         raise ValueError("stack_anova_factors: size mismatch")
     return np.vstack([np.sqrt(w) * f.Z for f, w in zip(factors, weights)])
+
+
+NYSTROM_COLUMNS, NYSTROM_GAUSSIAN = 0, 1
+
+
+def nystrom(op: AnovaFastOperator, rank: int, mode: str, seed: int, ldl_threshold: float = 1e-8, window: int = -1,
+            on_device: bool = False):
+    """nystrom(op, rank, mode, seed, ldl_threshold) (P:src/low_rank.cpp:115-168).
+    mode "gaussian" sketches op's own NFFT applies (window -1; the reference
+    uses a one-window FastWindowOperator, see fast_window_operator); mode
+    "columns" samples exact kernel columns of `window` (-1: ANOVA entries).
+    Returns a LowRankFactor (Z: rank x n)."""
+    m = {"columns": NYSTROM_COLUMNS, "gaussian": NYSTROM_GAUSSIAN}[mode]
+    n = op.size()
+    k = int(rank)
+    if on_device:
+        import torch
+        Z = torch.empty((max(k, 1), n), dtype=torch.float64, device=f"cuda:{op.device}")
+        kind, stream = _lib.DEVICE, C.c_void_p(torch.cuda.current_stream(Z.device).cuda_stream)
+        zp = C.c_void_p(Z.data_ptr())
+    else:
+        Z = np.empty((max(k, 1), n))
+        kind, stream, zp = _lib.HOST, C.c_void_p(0), C.c_void_p(Z.ctypes.data)
+    _raise(_lib.load().ksvm_nfft_nystrom(op._h, int(window), k, m, int(seed), float(ldl_threshold), zp, kind, stream))
+    return LowRankFactor(Z[:k], "nystrom-" + mode, k, 0.0, np.zeros(0, dtype=np.int64))
+
+
+def fast_window_operator(points, window, length_scale: float, cfg=None, device: int = 0) -> AnovaFastOperator:
+    """FastWindowOperator (P:src/pipeline.cpp:114-133): the fast transform of
+    one window (weight 1, plan fit 1.0) as an operator."""
+    from .fastsum import AnovaKernelSpec, FeatureWindowing, anova_fast_operator
+    spec = AnovaKernelSpec(FeatureWindowing([list(window)], [1.0], [float(length_scale)], []))
+    return anova_fast_operator(points, spec, cfg, 1.0, device=device)

@@ -9,8 +9,10 @@ that reach the hot path:
 balance_and_split -> zscore_fit_transform -> explicit windows (eta = 1/P,
 ell = 1) -> GPU greedy pivoted-Cholesky factor per window, stacked with
 sqrt(eta) -> GPU interior point loop over the NFFT operator (fit 1/1.2) ->
-compute_bias -> TrainedModel (GPU prediction). Mutual-information windowing
-and the randomized factorizations are outside this path.
+compute_bias -> TrainedModel (GPU prediction). Nystrom factors (columns /
+Gaussian sketch) are built on the GPU too; mutual-information windowing,
+random-pivot Cholesky and random Fourier features are outside this path
+(DESIGN.md).
 """
 from __future__ import annotations
 
@@ -24,9 +26,9 @@ import numpy as np
 from . import _lib
 from .fastsum import (AnovaKernelSpec, Dataset, FastsumConfig, FeatureWindowing, _raise, anova_fast_operator)
 from .ipm import FeatureStats, IpmConfig, IpmResult, IpmStatus, TrainedModel, ipm_train, make_model
-from .lowrank import pivoted_cholesky_greedy, stack_anova_factors
+from .lowrank import fast_window_operator, nystrom, pivoted_cholesky_greedy, stack_anova_factors
 
-PRECOND_METHODS = ("none", "cholesky-greedy")  # P:src/pipeline.cpp:8-18 (the ones on this path)
+PRECOND_METHODS = ("none", "cholesky-greedy", "nystrom-columns", "nystrom-gaussian")  # P:src/pipeline.cpp:8-18
 
 
 @dataclass
@@ -142,18 +144,29 @@ def window_ranks(cfg: PipelineConfig, P: int, n: int) -> List[int]:
 
 
 def build_precond_factor(op, train: Dataset, spec: AnovaKernelSpec, cfg: PipelineConfig):
-    """build_precond_factor (P:src/pipeline.cpp:137-196) for greedy pivoted
-    Cholesky: one WindowOperator factor per window on the GPU (exact entries
-    on the window's coordinates), stacked with sqrt(eta_l). Returns
-    (Z k x n, setup seconds)."""
-    if cfg.precond != "cholesky-greedy":
+    """build_precond_factor (P:src/pipeline.cpp:137-196): one factor per
+    window on the GPU, stacked with sqrt(eta_l). cholesky-greedy and
+    nystrom-columns use the window's exact kernel (WindowOperator);
+    nystrom-gaussian sketches the window's FastWindowOperator (a one-window
+    NFFT operator, fit 1.0) with seed cfg.seed + l. Returns (Z k x n, setup
+    seconds)."""
+    if cfg.precond not in PRECOND_METHODS[1:]:
         raise ValueError(f"preconditioner '{cfg.precond}' is not on the B200 path "
                          f"(supported: {', '.join(PRECOND_METHODS)})")
     w = spec.windowing
     P = w.num_windows()
     ranks = window_ranks(cfg, P, train.n())
     t0 = time.perf_counter()
-    factors = [pivoted_cholesky_greedy(op, ranks[l], cfg.cholesky_err_tol, window=l) for l in range(P)]
+    factors = []
+    for l in range(P):
+        seed = int(cfg.seed) + l
+        if cfg.precond == "cholesky-greedy":
+            factors.append(pivoted_cholesky_greedy(op, ranks[l], cfg.cholesky_err_tol, window=l))
+        elif cfg.precond == "nystrom-columns":
+            factors.append(nystrom(op, ranks[l], "columns", seed, window=l))
+        else:
+            fop = fast_window_operator(train.points, w.windows[l], w.length_scales[l], cfg.fastsum, op.device)
+            factors.append(nystrom(fop, ranks[l], "gaussian", seed))
     Z = stack_anova_factors(factors, w.weights)
     return Z, time.perf_counter() - t0
 

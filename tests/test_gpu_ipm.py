@@ -110,14 +110,18 @@ def test_compute_bias_rules_match_oracle():
         assert abs(compute_bias(alpha, y, K, 1.0, 1e-4) - oracle.compute_bias(Ko, alpha, y, 1.0, 1e-4)) <= 1e-10
 
 
-def oracle_pipeline(w, windows, rank, C, seed=0):
+def oracle_pipeline(w, windows, rank, C, seed=0, precond="cholesky-greedy"):
     """train_pipeline restated on the oracle pieces (P:src/pipeline.cpp:229-265)."""
     tr, te = oracle.balance_and_split(w.labels, 0.5, seed)
     Xtr, Xte, mu, sd = oracle.zscore(w.points[tr], w.points[te])
     ytr = w.labels[tr]
     P = len(windows)
-    Zs = [oracle.pivoted_cholesky(Xtr, windows, window=l, rank=max(1, rank // P), err_tol=1e-5)[0]
-          for l in range(P)]
+    if precond == "cholesky-greedy":
+        Zs = [oracle.pivoted_cholesky(Xtr, windows, window=l, rank=max(1, rank // P), err_tol=1e-5)[0]
+              for l in range(P)]
+    else:
+        mode = oracle.NYSTROM_GAUSSIAN if precond == "nystrom-gaussian" else oracle.NYSTROM_COLUMNS
+        Zs = [oracle.nystrom_window(Xtr, windows[l], 1.0, max(1, rank // P), mode, seed + l) for l in range(P)]
     Z = np.vstack([np.sqrt(1.0 / P) * z for z in Zs])
     Ko = oracle.Lib("oracle").anova(Xtr, windows, fit=FIT)
     alpha, res, log = oracle.ipm_train(Ko, ytr, Z, C=C)
@@ -126,14 +130,16 @@ def oracle_pipeline(w, windows, rank, C, seed=0):
     return dict(tr=tr, te=te, alpha=alpha, res=res, log=log, bias=b, f=f, Ko=Ko, ytr=ytr, Z=Z)
 
 
-def test_pipeline_config1_matches_oracle():
-    """BASELINE config 1 end to end: split, z-score, greedy pivoted Cholesky
-    rank 50, IPM with C = 1, bias, fast prediction on the held-out split."""
+@pytest.mark.parametrize("precond", ["cholesky-greedy", "nystrom-gaussian", "nystrom-columns"])
+def test_pipeline_config1_matches_oracle(precond):
+    """BASELINE config 1 end to end: split, z-score, rank-50 preconditioner
+    (greedy pivoted Cholesky as in BASELINE; the Nystrom sketches config 3
+    names), IPM with C = 1, bias, fast prediction on the held-out split."""
     w = workloads.config1()
     windows = [[0, 1, 2], [3, 4, 5]]
-    ref = oracle_pipeline(w, windows, 50, 1.0)
+    ref = oracle_pipeline(w, windows, 50, 1.0, precond=precond)
     model, test, report, res = train_pipeline(Dataset(w.points, w.labels), PipelineConfig(
-        explicit_windows=windows, rank=50, ipm=IpmConfig(C=1.0)))
+        explicit_windows=windows, rank=50, precond=precond, ipm=IpmConfig(C=1.0)))
     assert report.n_train == len(ref["tr"]) and report.n_test == len(ref["te"]) == 1000
     assert report.rank == ref["Z"].shape[0]
     check_same_run(res, ref["alpha"], ref["res"], ref["log"], ref["ytr"], ref["Ko"])
