@@ -195,6 +195,9 @@ void ksvm_nfft_saddle_free(ksvm_nfft_saddle* s);
 
 int ksvm_nfft_precond_create(const double* Z, int k, int64_t n, const double* y, int device,
                              ksvm_nfft_precond** out);
+/* Same with Z on the device (z_ptr_kind DEVICE: copied after `stream`). */
+int ksvm_nfft_precond_create_ex(const double* Z, int k, int64_t n, const double* y, int device,
+                                int z_ptr_kind, void* stream, ksvm_nfft_precond** out);
 int ksvm_nfft_precond_refresh(ksvm_nfft_precond* p, const double* theta);
 int ksvm_nfft_precond_apply(const ksvm_nfft_precond* p, const double* g, double* out, int ptr_kind,
                             void* stream);
@@ -266,8 +269,8 @@ int ksvm_nfft_precond_refresh_ex(ksvm_nfft_precond* p, const double* theta, int 
  * IpmResult / IpmIterationLog, P:include/ksvm/ipm.hpp:15-53): alpha, Theta,
  * the Newton systems and the Krylov bases stay on op's GPU; every matvec is
  * op's NFFT apply. y: n labels (+-1, host); Z: the stacked low-rank factor
- * (k x n row-major, host) or NULL for the unpreconditioned run (null
- * StackedFactor); alpha: n entries out (host); log: NULL or room for
+ * (k x n row-major, host or op's GPU per z_ptr_kind) or NULL for the
+ * unpreconditioned run (null StackedFactor); alpha: n entries out (host); log: NULL or room for
  * cfg->max_ip_iters entries. Invalid config / labels: status 4 with the
  * reference's messages; degenerate initial infeasibility: status 5. */
 typedef struct ksvm_nfft_ipm_config {
@@ -308,7 +311,7 @@ typedef struct ksvm_nfft_ipm_log {
 } ksvm_nfft_ipm_log;
 
 void ksvm_nfft_ipm_config_default(ksvm_nfft_ipm_config* cfg);
-int ksvm_nfft_ipm_train(const ksvm_nfft_op* op, const double* y, const double* Z, int k,
+int ksvm_nfft_ipm_train(const ksvm_nfft_op* op, const double* y, const double* Z, int k, int z_ptr_kind,
                         const ksvm_nfft_ipm_config* cfg, double* alpha, ksvm_nfft_ipm_result* result,
                         ksvm_nfft_ipm_log* log);
 

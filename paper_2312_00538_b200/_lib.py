@@ -91,6 +91,8 @@ _SIGS = {
     "ksvm_nfft_saddle_apply": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp]),
     "ksvm_nfft_saddle_free": (None, [_vp]),
     "ksvm_nfft_precond_create": (C.c_int, [_vp, C.c_int, C.c_int64, _vp, C.c_int, C.POINTER(_vp)]),
+    "ksvm_nfft_precond_create_ex": (C.c_int, [_vp, C.c_int, C.c_int64, _vp, C.c_int, C.c_int, _vp,
+                                              C.POINTER(_vp)]),
     "ksvm_nfft_precond_refresh": (C.c_int, [_vp, _vp]),
     "ksvm_nfft_precond_apply": (C.c_int, [_vp, _vp, _vp, C.c_int, _vp]),
     "ksvm_nfft_precond_identity": (C.c_int, [_vp]),
@@ -101,7 +103,8 @@ _SIGS = {
     "ksvm_nfft_precond_refresh_ex": (C.c_int, [_vp, _vp, C.c_int, _vp]),
     # interior point trainer
     "ksvm_nfft_ipm_config_default": (None, [C.POINTER(IpmConfig)]),
-    "ksvm_nfft_ipm_train": (C.c_int, [_vp, _vp, _vp, C.c_int, C.POINTER(IpmConfig), _vp, C.POINTER(IpmResult),
+    "ksvm_nfft_ipm_train": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.POINTER(IpmConfig), _vp,
+                                      C.POINTER(IpmResult),
                                       C.POINTER(IpmLog)]),
     "ksvm_nfft_compute_bias": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_double, _dp, _lp]),
     "ksvm_nfft_nystrom": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_double, _vp, C.c_int, _vp]),

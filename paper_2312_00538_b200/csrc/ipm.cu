@@ -170,7 +170,7 @@ void ksvm_nfft_ipm_config_default(ksvm_nfft_ipm_config* c) {  // P:include/ksvm/
     c->mu0 = 1.0;
 }
 
-int ksvm_nfft_ipm_train(const ksvm_nfft_op* op, const double* y_h, const double* Z, int k,
+int ksvm_nfft_ipm_train(const ksvm_nfft_op* op, const double* y_h, const double* Z, int k, int z_ptr_kind,
                         const ksvm_nfft_ipm_config* cfg, double* alpha_out, ksvm_nfft_ipm_result* result,
                         ksvm_nfft_ipm_log* log) {
     return guarded([&] {
@@ -239,7 +239,7 @@ int ksvm_nfft_ipm_train(const ksvm_nfft_op* op, const double* y_h, const double*
         // created once and re-pointed at each iteration's Theta.
         std::vector<double> ones(N, 1.0);
         ok(ksvm_nfft_saddle_create(op, y_h, ones.data(), &H.s), "ipm_train");
-        ok(ksvm_nfft_precond_create(Z, Z ? k : 0, n, y_h, dev, &H.p), "ipm_train");
+        ok(ksvm_nfft_precond_create_ex(Z, Z ? k : 0, n, y_h, dev, z_ptr_kind, st, &H.p), "ipm_train");
 
         double xi_a = 1.0, xi_l = 1.0, gm_sum = 0.0;
         int it = 0, streak = 0, status = -1;

@@ -794,7 +794,13 @@ int ksvm_nfft_saddle_set_theta_ex(ksvm_nfft_saddle* s, const double* theta, int 
 void ksvm_nfft_saddle_free(ksvm_nfft_saddle* s) { delete s; }
 
 int ksvm_nfft_precond_create(const double* Z, int k, int64_t n, const double* y, int device, ksvm_nfft_precond** out) {
+    return ksvm_nfft_precond_create_ex(Z, k, n, y, device, KSVM_NFFT_HOST, nullptr, out);
+}
+
+int ksvm_nfft_precond_create_ex(const double* Z, int k, int64_t n, const double* y, int device, int z_ptr_kind,
+                                void* stream, ksvm_nfft_precond** out) {
     return guarded([&] {
+        if (z_ptr_kind != KSVM_NFFT_HOST && z_ptr_kind != KSVM_NFFT_DEVICE) throw std::invalid_argument("bad ptr_kind");
         if (!y || !out || n < 1) throw std::invalid_argument("SaddlePreconditioner: bad argument");
         if (Z && (k < 0 || k > kMaxRank)) throw std::invalid_argument("SaddlePreconditioner: rank must be in [0, 1024]");
         auto P = std::make_unique<ksvm_nfft_precond>();
@@ -805,7 +811,14 @@ int ksvm_nfft_precond_create(const double* Z, int k, int64_t n, const double* y,
         DeviceGuard dg(device);
         CK(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
         P->y.upload(y, static_cast<size_t>(n), P->stream);
-        if (P->k > 0) P->Z.upload(Z, static_cast<size_t>(P->k) * n, P->stream);
+        if (P->k > 0 && z_ptr_kind == KSVM_NFFT_DEVICE) {  // Z already on this GPU: ordered after `stream`
+            cudaStream_t zs = static_cast<cudaStream_t>(stream);
+            P->Z.alloc(static_cast<size_t>(P->k) * n);
+            CK(cudaMemcpyAsync(P->Z.p, Z, sizeof(double) * P->k * n, cudaMemcpyDeviceToDevice, zs));
+            CK(cudaStreamSynchronize(zs));
+        } else if (P->k > 0) {
+            P->Z.upload(Z, static_cast<size_t>(P->k) * n, P->stream);
+        }
         P->partial.alloc(static_cast<size_t>(kRB) * std::max(P->k, 1));
         P->s.alloc(static_cast<size_t>(std::max(P->k, 1)));
         P->inner.alloc(static_cast<size_t>(std::max(P->k, 1)));

@@ -21,7 +21,7 @@ from typing import List, Optional
 import numpy as np
 
 from . import _lib
-from .fastsum import AnovaFastOperator, AnovaKernelSpec, FastsumConfig, _raise, decision_values
+from .fastsum import AnovaFastOperator, AnovaKernelSpec, FastsumConfig, _is_cuda_tensor, _raise, decision_values
 
 
 @dataclass
@@ -94,23 +94,31 @@ def _labels(y, n) -> np.ndarray:
 
 def ipm_train(op: AnovaFastOperator, y, factor=None, cfg: Optional[IpmConfig] = None) -> IpmResult:
     """ipm_train (P:src/ipm.cpp:76-155) on op's GPU. factor: the stacked
-    k x n factor (numpy; stack_anova_factors) or None (unpreconditioned)."""
+    k x n factor (stack_anova_factors) as a numpy array or a CUDA tensor on
+    op's GPU (kept there), or None (unpreconditioned)."""
     cfg = cfg or IpmConfig()
     n = op.size()
     y = _labels(y, n)
-    Z = None
+    zp, k, zkind = None, 0, _lib.HOST
     if factor is not None:
-        Z = np.ascontiguousarray(factor, dtype=np.float64)
-        if Z.ndim != 2 or Z.shape[1] != n:
-            raise ValueError("factor must be k x n")
+        if _is_cuda_tensor(factor):
+            import torch
+            Zt = factor.to(torch.float64).contiguous()
+            if Zt.dim() != 2 or Zt.shape[1] != n:
+                raise ValueError("factor must be k x n")
+            torch.cuda.current_stream(Zt.device).synchronize()  # Z complete before the library's stream reads it
+            zp, k, zkind, keep = C.c_void_p(Zt.data_ptr()), int(Zt.shape[0]), _lib.DEVICE, Zt
+        else:
+            Z = np.ascontiguousarray(factor, dtype=np.float64)
+            if Z.ndim != 2 or Z.shape[1] != n:
+                raise ValueError("factor must be k x n")
+            zp, k, keep = C.c_void_p(Z.ctypes.data), int(Z.shape[0]), Z
     alpha = np.empty(n)
     res = _lib.IpmResult()
     log = (_lib.IpmLog * int(max(cfg.max_ip_iters, 1)))()
     c = cfg._c()
-    _raise(_lib.load().ksvm_nfft_ipm_train(op._h, C.c_void_p(y.ctypes.data),
-                                           None if Z is None else C.c_void_p(Z.ctypes.data),
-                                           0 if Z is None else Z.shape[0], C.byref(c), C.c_void_p(alpha.ctypes.data),
-                                           C.byref(res), log))
+    _raise(_lib.load().ksvm_nfft_ipm_train(op._h, C.c_void_p(y.ctypes.data), zp, k, zkind, C.byref(c),
+                                           C.c_void_p(alpha.ctypes.data), C.byref(res), log))
     its = [IpmIterationLog(L.it, L.mu, L.xi_alpha_rel, L.xi_lambda_rel, L.step_alpha,
                            GmresLog(L.gmres_iterations, L.gmres_relative_residual, bool(L.gmres_converged),
                                     bool(L.gmres_breakdown)))

@@ -63,6 +63,7 @@ class TrainReport:
     xi_lambda: float = 0.0
     mu_final: float = 0.0
     status: IpmStatus = IpmStatus.CONVERGED
+    phase_seconds: dict = field(default_factory=dict)  # (addition) operator / factor / ipm / model wall times
 
 
 def parse_window_spec(spec: str, d: int) -> List[List[int]]:
@@ -143,13 +144,15 @@ def window_ranks(cfg: PipelineConfig, P: int, n: int) -> List[int]:
     return [min(int(r), n) for r in ranks]
 
 
-def build_precond_factor(op, train: Dataset, spec: AnovaKernelSpec, cfg: PipelineConfig):
+def build_precond_factor(op, train: Dataset, spec: AnovaKernelSpec, cfg: PipelineConfig, on_device: bool = False):
     """build_precond_factor (P:src/pipeline.cpp:137-196): one factor per
-    window on the GPU, stacked with sqrt(eta_l). cholesky-greedy and
-    nystrom-columns use the window's exact kernel (WindowOperator);
-    nystrom-gaussian sketches the window's FastWindowOperator (a one-window
-    NFFT operator, fit 1.0) with seed cfg.seed + l. Returns (Z k x n, setup
-    seconds)."""
+    window on the GPU, stacked with sqrt(eta_l) (stack_anova_factors,
+    P:src/low_rank.cpp:200-222). cholesky-greedy and nystrom-columns use the
+    window's exact kernel (WindowOperator); nystrom-gaussian sketches the
+    window's FastWindowOperator (a one-window NFFT operator, fit 1.0) with
+    seed cfg.seed + l. on_device keeps every factor and the stack in HBM (a
+    CUDA tensor; the IPM's preconditioner then never crosses PCIe). Returns
+    (Z k x n, setup seconds)."""
     if cfg.precond not in PRECOND_METHODS[1:]:
         raise ValueError(f"preconditioner '{cfg.precond}' is not on the B200 path "
                          f"(supported: {', '.join(PRECOND_METHODS)})")
@@ -161,13 +164,19 @@ def build_precond_factor(op, train: Dataset, spec: AnovaKernelSpec, cfg: Pipelin
     for l in range(P):
         seed = int(cfg.seed) + l
         if cfg.precond == "cholesky-greedy":
-            factors.append(pivoted_cholesky_greedy(op, ranks[l], cfg.cholesky_err_tol, window=l))
+            f = pivoted_cholesky_greedy(op, ranks[l], cfg.cholesky_err_tol, window=l, on_device=on_device)
         elif cfg.precond == "nystrom-columns":
-            factors.append(nystrom(op, ranks[l], "columns", seed, window=l))
+            f = nystrom(op, ranks[l], "columns", seed, window=l, on_device=on_device)
         else:
             fop = fast_window_operator(train.points, w.windows[l], w.length_scales[l], cfg.fastsum, op.device)
-            factors.append(nystrom(fop, ranks[l], "gaussian", seed))
-    Z = stack_anova_factors(factors, w.weights)
+            f = nystrom(fop, ranks[l], "gaussian", seed, on_device=on_device)
+        factors.append(f)
+    if on_device:
+        import torch
+        Z = torch.cat([f.Z * float(np.sqrt(wt)) for f, wt in zip(factors, w.weights)], dim=0)
+        torch.cuda.current_stream(Z.device).synchronize()
+    else:
+        Z = stack_anova_factors(factors, w.weights)
     return Z, time.perf_counter() - t0
 
 
@@ -177,11 +186,16 @@ def train_on_prepared(train: Dataset, spec: AnovaKernelSpec, cfg: PipelineConfig
     returns (TrainedModel, IpmResult)."""
     t0 = time.perf_counter()
     op = anova_fast_operator(train, spec, cfg.fastsum, 1.0 / 1.2, device=cfg.device)
+    t1 = time.perf_counter()
     Z = None
     if cfg.precond != "none":
-        Z, report.precond_setup_seconds = build_precond_factor(op, train, spec, cfg)
+        Z, report.precond_setup_seconds = build_precond_factor(op, train, spec, cfg, on_device=True)
+    t2 = time.perf_counter()
     res = ipm_train(op, train.labels, Z, cfg.ipm)
+    t3 = time.perf_counter()
     model = make_model(res, train, spec, cfg.fastsum, op, cfg.ipm.C, normalization)
+    report.phase_seconds = {"operator": t1 - t0, "factor": t2 - t1, "ipm": t3 - t2,
+                            "model": time.perf_counter() - t3}
     report.n_train = train.n()
     report.d = train.dim()
     report.P = spec.windowing.num_windows()
@@ -199,8 +213,10 @@ def train_on_prepared(train: Dataset, spec: AnovaKernelSpec, cfg: PipelineConfig
 def train_pipeline(raw: Dataset, cfg: PipelineConfig):
     """train_pipeline (P:src/pipeline.cpp:229-265) with explicit windows:
     returns (TrainedModel, normalized test Dataset, TrainReport, IpmResult)."""
+    t0 = time.perf_counter()
     train, test = balance_and_split(raw, cfg.train_fraction, cfg.seed)
     stats = zscore_fit_transform(train, test)
+    t_prep = time.perf_counter() - t0
     if not cfg.explicit_windows:
         raise ValueError("mutual-information windowing is outside the B200 path: pass explicit_windows")
     windows = cfg.explicit_windows
@@ -222,5 +238,6 @@ def train_pipeline(raw: Dataset, cfg: PipelineConfig):
     spec = AnovaKernelSpec(wnd)
     report = TrainReport()
     model, res = train_on_prepared(train, spec, cfg, report, stats)
+    report.phase_seconds["split_zscore"] = t_prep
     report.n_test = test.n()
     return model, test, report, res
