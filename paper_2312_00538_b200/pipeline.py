@@ -113,24 +113,13 @@ def zscore_fit_transform(train: Dataset, test: Dataset):
         raise ValueError("empty training split")
     X = np.asarray(train.points, dtype=np.float64)
     n = X.shape[0]
-    stats = []
-    Xo = np.empty_like(X)
-    T = np.asarray(test.points, dtype=np.float64) if test is not None and test.n() > 0 else None
-    To = None if T is None else np.empty_like(T)
-    for j in range(X.shape[1]):
-        col = X[:, j]
-        mean = float(col.sum() / n)
-        sd = float(np.sqrt(((col - mean) ** 2).sum() / n))
-        if sd < 1e-300:
-            sd = 1.0
-        stats.append(FeatureStats(mean, sd))
-        Xo[:, j] = (col - mean) / sd
-        if T is not None:
-            To[:, j] = (T[:, j] - mean) / sd
-    train.points = Xo
-    if To is not None:
-        test.points = To
-    return stats
+    mean = X.sum(axis=0) / n
+    sd = np.sqrt(((X - mean) ** 2).sum(axis=0) / n)
+    sd[sd < 1e-300] = 1.0  # constant column maps to zeros
+    train.points = (X - mean) / sd
+    if test is not None and test.n() > 0:
+        test.points = (np.asarray(test.points, dtype=np.float64) - mean) / sd
+    return [FeatureStats(float(a), float(b)) for a, b in zip(mean, sd)]
 
 
 def window_ranks(cfg: PipelineConfig, P: int, n: int) -> List[int]:
