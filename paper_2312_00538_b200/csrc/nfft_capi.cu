@@ -42,6 +42,12 @@ void launch_tile_reduce(const DWin* wins, const int2* multi, int nmulti, int max
 void launch_conv(const DWin* wins, const int* slots, int nslots, int Lg_max, long long max_fibres,
                  int stage, cudaStream_t st);
 int conv_max_lg();
+// fused grid side (grid_fused.cu)
+cudaError_t init_fused_attributes();
+size_t fused_smem_bytes(int D, int Lg);
+bool fused3_supported(int Lg, int NC);
+void launch_grid_fused(const DWin* wins, const int* slots, int nslots, int D, int NC, int Lg_max,
+                       const double* patches, cudaStream_t st);
 
 void launch_combine(double* y, const double* const* src, const int* const* inv, const uint8_t* const* inv8,
                     const double* eta, int P, long long n, cudaStream_t st);
@@ -68,6 +74,7 @@ void ensure_attributes(int dev) {
     std::lock_guard<std::mutex> lk(mu);
     if (dev >= 0 && dev < 256 && !done[static_cast<size_t>(dev)]) {
         CK(init_kernel_attributes());
+        CK(init_fused_attributes());
         done[static_cast<size_t>(dev)] = true;
     }
 }
@@ -441,6 +448,9 @@ struct Engine {
     int n_multi = 0, max_pv = 0;
     int multi_begin[4] = {0, 0, 0, 0}, n_multi_cls[4] = {0, 0, 0, 0};
     int slot_begin[4] = {0, 0, 0, 0}, nslots_cls[4] = {0, 0, 0, 0};  // d_slots grouped by d
+    // fused grid side per class (grid_fused.cu): reduce + all conv stages in one launch
+    bool grid_fused[4] = {false, false, false, false};
+    int grid_nc[4] = {0, 0, 0, 0}, grid_lg[4] = {0, 0, 0, 0};
     DevBuf<double> d_eta;
     DevBuf<double> patches, parts, vbuf, ybuf;
     // exact-duplicate windows (Window::nu): segmented sums of v and output maps
@@ -720,6 +730,32 @@ struct Engine {
                 if (wins[static_cast<size_t>(owned[static_cast<size_t>(s)])]->d == D) slots.push_back(s);
             nslots_cls[D] = static_cast<int>(slots.size()) - slot_begin[D];
         }
+        // Fused grid side: every owned window of the class has a non-wrapping
+        // grid whose on-chip working set fits (KSVM_NFFT_GRID=staged disables).
+        {
+            const char* ge = std::getenv("KSVM_NFFT_GRID");
+            const bool allow = !(ge && std::string(ge) == "staged");
+            for (int D = 1; D <= 3; ++D) {
+                bool ok = allow && nslots_cls[D] > 0;
+                int lg = 0, nc = 0;
+                for (int s = 0; s < P && ok; ++s) {
+                    const Window& w = *wins[static_cast<size_t>(owned[static_cast<size_t>(s)])];
+                    if (w.d != D) continue;
+                    const Geometry& g = w.geom;
+                    if (g.wrap) ok = false;
+                    lg = std::max(lg, g.Lg);
+                    const int pe = g.PE;
+                    nc = std::max(nc, (pe + g.TC - 1) / g.TC);
+                }
+                const int ncT = nc <= (D == 3 ? 3 : 2) ? (D == 3 ? 3 : 2) : 5;
+                if (ok && nc > 5) ok = false;
+                if (ok && fused_smem_bytes(D, lg) > 227 * 1024) ok = false;
+                if (ok && D == 3 && !fused3_supported(lg, ncT)) ok = false;
+                grid_fused[D] = ok;
+                grid_nc[D] = ncT;
+                grid_lg[D] = lg;
+            }
+        }
         parts.alloc(static_cast<size_t>(std::max(P, 1)) * n);
         // exact-duplicate windows: member chunks of <= kSegChunk within one
         // distinct point, global distinct-point numbering in slot order
@@ -845,17 +881,25 @@ struct Engine {
             launch_tile_reduce(WINS(), d_multi.p + multi_begin[D], n_multi_cls[D], max_pv, PATCHES(), st);
             ++launch_counter();
         }
-        tick("reduce");
-        for (int wrap = 0; wrap < 2; ++wrap) {
-            if (!(wrap ? has_wrap : has_nowrap)[D]) continue;
-            launch_reduce(WINS(), d_slots.p + slot_begin[D], nslots_cls[D], max_nodes, D,
-                          2 * cfg.window_cutoff, PATCHES(), wrap != 0, max_tiles[D], st);
+        if (grid_fused[D]) {
+            static const char* kGrid[4] = {"", "grid_d1", "grid_d2", "grid_d3"};
+            tick(kGrid[D]);
+            launch_grid_fused(WINS(), d_slots.p + slot_begin[D], nslots_cls[D], D, grid_nc[D], grid_lg[D],
+                              PATCHES(), st);
             ++launch_counter();
-        }
-        for (int stg = 0; stg < D; ++stg) {
-            tick(kConv[stg]);
-            launch_conv(WINS(), d_slots.p + slot_begin[D], nslots_cls[D], max_lg, max_fibres, stg, st);
-            ++launch_counter();
+        } else {
+            tick("reduce");
+            for (int wrap = 0; wrap < 2; ++wrap) {
+                if (!(wrap ? has_wrap : has_nowrap)[D]) continue;
+                launch_reduce(WINS(), d_slots.p + slot_begin[D], nslots_cls[D], max_nodes, D,
+                              2 * cfg.window_cutoff, PATCHES(), wrap != 0, max_tiles[D], st);
+                ++launch_counter();
+            }
+            for (int stg = 0; stg < D; ++stg) {
+                tick(kConv[stg]);
+                launch_conv(WINS(), d_slots.p + slot_begin[D], nslots_cls[D], max_lg, max_fibres, stg, st);
+                ++launch_counter();
+            }
         }
         if (gather) {
             const int gcnt = gclass_end[D] - gclass_begin[D];

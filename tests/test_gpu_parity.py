@@ -177,3 +177,19 @@ def test_duplicate_config4_shape_matches_oracle(oracle_lib):
     g = anova_fast_operator(Dataset(w.points), spec_of(w.windows), fit_fraction=w.fit_fraction)
     o = oracle_lib.anova(w.points, w.windows, fit=w.fit_fraction)
     assert rel(g.apply(w.v), o.apply(w.v)) <= TOL
+
+
+@pytest.mark.parametrize("grid", ["fused", "staged"])
+@pytest.mark.parametrize("cfg,n,m", [(2, 60000, 4), (3, 8000, 4), (1, 2000, 4), (2, 5000, 3), (2, 4000, 6)])
+def test_grid_side_variants_match_oracle(oracle_lib, monkeypatch, grid, cfg, n, m):
+    # the fused grid side (reduce + separable convolution in one launch: a
+    # thread-block cluster per 3-d window, one CTA per 1-/2-d window) and the
+    # staged kernels, on operator data-range grids, m = 3 / 4 / 6
+    monkeypatch.setenv("KSVM_NFFT_GRID", grid)
+    w = workloads.make(cfg, n)
+    c = FastsumConfig(window_cutoff=m)
+    g = anova_fast_operator(Dataset(w.points), spec_of(w.windows), c, fit_fraction=w.fit_fraction)
+    o = oracle_lib.anova(w.points, w.windows, m=m, fit=w.fit_fraction)
+    y = g.apply(w.v)
+    assert rel(y, o.apply(w.v)) <= TOL
+    assert np.array_equal(y, g.apply(w.v))
