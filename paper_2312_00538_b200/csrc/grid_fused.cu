@@ -124,43 +124,57 @@ __device__ __forceinline__ Acc8 line_conv2(const double* __restrict__ sA, const 
 }
 
 // Grid node (e0, e1, e2) of a non-wrapping grid <- sum of the covering
-// tiles' (pre-reduced) patch values, in (a0, a1, a2) order.
+// tiles' (pre-reduced) patch values, in (a0, a1, a2) order. soff: the
+// tile_patch offsets of tiles T0 in [t0lo, t0lo + n0), all T1, T2, staged in
+// SMEM, so the <= NC^d patch loads of a node are independent (no dependent
+// offset load in front of each).
 template <int D, int NC>
-__device__ __forceinline__ double node_sum(const DWin& wn, const double* __restrict__ patches, const int* e) {
+__device__ __forceinline__ double node_sum(const DWin& wn, const double* __restrict__ patches,
+                                           const long long* __restrict__ soff, int t0lo, const int* e) {
     const int TC = wn.TC, PE = wn.PE, nt = wn.ntile;
-    const long long* __restrict__ tp = wn.tile_patch;
     int thi[3] = {0, 0, 0};
 #pragma unroll
     for (int t = 0; t < D; ++t) thi[t] = min(e[t] / TC, nt - 1);
-    double sum = 0.0;
+    double v[D == 1 ? NC : (D == 2 ? NC * NC : NC * NC * NC)];
 #pragma unroll
     for (int a0 = 0; a0 < NC; ++a0) {
         const int T0 = thi[0] - a0, o0 = e[0] - T0 * TC;
-        if (T0 < 0 || o0 >= PE) continue;
+        const bool ok0 = T0 >= 0 && o0 < PE;
         if constexpr (D == 1) {
-            const long long off = tp[T0];
-            if (off >= 0) sum += patches[off + o0];
+            const long long off = ok0 ? soff[T0 - t0lo] : -1;
+            v[a0] = off >= 0 ? patches[off + o0] : 0.0;
         } else {
 #pragma unroll
             for (int a1 = 0; a1 < NC; ++a1) {
                 const int T1 = thi[1] - a1, o1 = e[1] - T1 * TC;
-                if (T1 < 0 || o1 >= PE) continue;
+                const bool ok1 = ok0 && T1 >= 0 && o1 < PE;
                 if constexpr (D == 2) {
-                    const long long off = tp[T0 * nt + T1];
-                    if (off >= 0) sum += patches[off + o0 * PE + o1];
+                    const long long off = ok1 ? soff[(T0 - t0lo) * nt + T1] : -1;
+                    v[a0 * NC + a1] = off >= 0 ? patches[off + o0 * PE + o1] : 0.0;
                 } else {
 #pragma unroll
                     for (int a2 = 0; a2 < NC; ++a2) {
                         const int T2 = thi[2] - a2, o2 = e[2] - T2 * TC;
-                        if (T2 < 0 || o2 >= PE) continue;
-                        const long long off = tp[(T0 * nt + T1) * nt + T2];
-                        if (off >= 0) sum += patches[off + (o0 * PE + o1) * PE + o2];
+                        const bool ok2 = ok1 && T2 >= 0 && o2 < PE;
+                        const long long off = ok2 ? soff[((T0 - t0lo) * nt + T1) * nt + T2] : -1;
+                        v[(a0 * NC + a1) * NC + a2] = off >= 0 ? patches[off + (o0 * PE + o1) * PE + o2] : 0.0;
                     }
                 }
             }
         }
     }
+    double sum = 0.0;  // skipped terms are exact zeros: same value as the staged reduction's skip
+#pragma unroll
+    for (int q = 0; q < (D == 1 ? NC : (D == 2 ? NC * NC : NC * NC * NC)); ++q) sum += v[q];
     return sum;
+}
+
+// Stage tile_patch offsets for tiles T0 in [t0lo, t0hi] (all T1, T2) into SMEM.
+__device__ void stage_offsets(const DWin& wn, int D, int t0lo, int t0hi, long long* soff) {
+    int per = 1;
+    for (int t = 1; t < D; ++t) per *= wn.ntile;
+    const int cnt = max(0, t0hi - t0lo + 1) * per;
+    for (int k = threadIdx.x; k < cnt; k += blockDim.x) soff[k] = wn.tile_patch[static_cast<long long>(t0lo) * per + k];
 }
 
 __device__ __forceinline__ void cluster_barrier() {
@@ -196,12 +210,18 @@ __global__ void __launch_bounds__(kFusedThreads) grid3_fused_kernel(const DWin* 
     double* slab2 = slab1 + SL;  // T1, then X3
     double* slab3 = slab2 + SL;  // T3
     const int p0 = rank * np, p1 = min(Lg, p0 + np), mine = max(0, p1 - p0);
+    long long* soff = reinterpret_cast<long long*>(slab3 + SL);
+    const int t0lo = max(0, min(p0 / wn.TC, wn.ntile - 1) - (NC - 1));
+    const int t0hi = min(wn.ntile - 1, max(p1 - 1, 0) / wn.TC);
     stage_tables(wn, sA, sS);
+    stage_offsets(wn, 3, t0lo, t0hi, soff);
+    __syncthreads();
     pdl_wait();  // patches come from the spread / tile_reduce kernels
     // 1. node reduction of my planes
+#pragma unroll 2
     for (int k = threadIdx.x; k < mine * L2; k += blockDim.x) {
         const int e[3] = {p0 + k / L2, (k / Lg) % Lg, k % Lg};
-        slab0[k] = node_sum<3, NC>(wn, patches, e);
+        slab0[k] = node_sum<3, NC>(wn, patches, soff, t0lo, e);
     }
     __syncthreads();
     // 2. stage 0 along dim 2: T0 = A2 g, T1 = S2 g (lines (p, i1), 4-output blocks)
@@ -233,6 +253,7 @@ __global__ void __launch_bounds__(kFusedThreads) grid3_fused_kernel(const DWin* 
     // 4. transpose: my dim-1 rows [q0, q1) of T2 / T3 over all planes j, from
     //    the owning CTAs' shared memory: X[(j * qn + qq) * Lg + i2]
     const int q0 = rank * np, q1 = min(Lg, q0 + np), qn = max(0, q1 - q0);
+#pragma unroll 4
     for (int k = threadIdx.x; k < Lg * qn * Lg; k += blockDim.x) {
         const int i2 = k % Lg, qq = (k / Lg) % max(qn, 1), j = k / (qn * Lg);
         const int own = j / np, jj = j - own * np;
@@ -274,7 +295,10 @@ __global__ void __launch_bounds__(kFusedThreads) grid12_fused_kernel(const DWin*
     double* sG = sS + ((TL + 1) & ~1);
     double* sT0 = sG + nodes;
     double* sT1 = sT0 + nodes;
+    long long* soff = reinterpret_cast<long long*>(sT1 + nodes);
     stage_tables(wn, sA, sS);
+    stage_offsets(wn, D, 0, wn.ntile - 1, soff);
+    __syncthreads();
     pdl_wait();
     for (int k = threadIdx.x; k < nodes; k += blockDim.x) {
         int e[3] = {0, 0, 0};
@@ -284,7 +308,7 @@ __global__ void __launch_bounds__(kFusedThreads) grid12_fused_kernel(const DWin*
             e[0] = k / Lg;
             e[1] = k % Lg;
         }
-        sG[k] = node_sum<D, NC>(wn, patches, e);
+        sG[k] = node_sum<D, NC>(wn, patches, soff, 0, e);
     }
     __syncthreads();
     const int nb = (Lg + 3) >> 2;
@@ -328,13 +352,21 @@ static size_t tables_doubles(int Lg) { return static_cast<size_t>(((2 * Lg + 6) 
 // Planes per CTA for d = 3 (C = ceil(Lg / np) CTAs per cluster, C <= 16).
 int fused3_planes(int Lg) { return (Lg + kFusedMaxCluster - 1) / kFusedMaxCluster; }
 
+// Tile grid bound: ntile = ceil(ncell / TC) <= ceil(Lg / TC), TC = 4 / 8 / 32 for d = 3 / 2 / 1.
+static long long tiles_bound(int D, int Lg) {
+    const int TC = D == 3 ? 4 : (D == 2 ? 8 : 32);
+    return (Lg + TC - 1) / TC;
+}
+
 size_t fused_smem_bytes(int D, int Lg) {
+    const long long nt = tiles_bound(D, Lg);
     if (D == 3) {
         const long long np = fused3_planes(Lg);
-        return sizeof(double) * (tables_doubles(Lg) + 4 * np * Lg * Lg);
+        const long long n0 = 5 + (np + 3) / 4;  // T0 range of a slab: <= NC - 1 + ceil(np / TC) + 1
+        return sizeof(double) * (tables_doubles(Lg) + 4 * np * Lg * Lg) + sizeof(long long) * n0 * nt * nt;
     }
     const long long nodes = D == 1 ? Lg : static_cast<long long>(Lg) * Lg;
-    return sizeof(double) * (tables_doubles(Lg) + 3 * nodes);
+    return sizeof(double) * (tables_doubles(Lg) + 3 * nodes) + sizeof(long long) * (D == 1 ? nt : nt * nt);
 }
 
 static cudaError_t set_fused_attrs(const void* f, bool cluster) {
