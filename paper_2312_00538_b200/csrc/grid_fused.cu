@@ -33,7 +33,7 @@ namespace cg = cooperative_groups;
 
 namespace ksvm_nfft {
 
-constexpr int kFusedThreads = 256;
+constexpr int kFusedThreads = 512;
 constexpr int kFusedMaxCluster = 16;
 
 namespace {
@@ -70,6 +70,7 @@ __device__ __forceinline__ Acc8 line_conv1(const double* __restrict__ sA, const 
         r.a[u] = 0.0;
         r.s[u] = 0.0;
     }
+#pragma unroll 4
     for (int j = 0; j < Lg; ++j) {
         const double xv = x[j * xs];
 #pragma unroll
@@ -101,6 +102,7 @@ __device__ __forceinline__ Acc8 line_conv2(const double* __restrict__ sA, const 
         r.a[u] = 0.0;
         r.s[u] = 0.0;
     }
+#pragma unroll 4
     for (int j = 0; j < Lg; ++j) {
         const double xv = x[j * xs], yv = y[j * xs];
 #pragma unroll
@@ -135,14 +137,23 @@ __device__ __forceinline__ double node_sum(const DWin& wn, const double* __restr
     int thi[3] = {0, 0, 0};
 #pragma unroll
     for (int t = 0; t < D; ++t) thi[t] = min(e[t] / TC, nt - 1);
-    double v[D == 1 ? NC : (D == 2 ? NC * NC : NC * NC * NC)];
+    // NC^d values loaded first (independent loads), summed in index order;
+    // for large NC^d (generic m) the running sum keeps registers bounded
+    constexpr int NV = D == 1 ? NC : (D == 2 ? NC * NC : NC * NC * NC);
+    constexpr bool kArr = NV <= 27;
+    double v[kArr ? NV : 1];
+    double run = 0.0;
+    auto put = [&](int q, double x) {
+        if constexpr (kArr) v[q] = x;
+        else run += x;
+    };
 #pragma unroll
     for (int a0 = 0; a0 < NC; ++a0) {
         const int T0 = thi[0] - a0, o0 = e[0] - T0 * TC;
         const bool ok0 = T0 >= 0 && o0 < PE;
         if constexpr (D == 1) {
             const long long off = ok0 ? soff[T0 - t0lo] : -1;
-            v[a0] = off >= 0 ? patches[off + o0] : 0.0;
+            put(a0, off >= 0 ? patches[off + o0] : 0.0);
         } else {
 #pragma unroll
             for (int a1 = 0; a1 < NC; ++a1) {
@@ -150,22 +161,23 @@ __device__ __forceinline__ double node_sum(const DWin& wn, const double* __restr
                 const bool ok1 = ok0 && T1 >= 0 && o1 < PE;
                 if constexpr (D == 2) {
                     const long long off = ok1 ? soff[(T0 - t0lo) * nt + T1] : -1;
-                    v[a0 * NC + a1] = off >= 0 ? patches[off + o0 * PE + o1] : 0.0;
+                    put(a0 * NC + a1, off >= 0 ? patches[off + o0 * PE + o1] : 0.0);
                 } else {
 #pragma unroll
                     for (int a2 = 0; a2 < NC; ++a2) {
                         const int T2 = thi[2] - a2, o2 = e[2] - T2 * TC;
                         const bool ok2 = ok1 && T2 >= 0 && o2 < PE;
                         const long long off = ok2 ? soff[((T0 - t0lo) * nt + T1) * nt + T2] : -1;
-                        v[(a0 * NC + a1) * NC + a2] = off >= 0 ? patches[off + (o0 * PE + o1) * PE + o2] : 0.0;
+                        put((a0 * NC + a1) * NC + a2, off >= 0 ? patches[off + (o0 * PE + o1) * PE + o2] : 0.0);
                     }
                 }
             }
         }
     }
+    if constexpr (!kArr) return run;
     double sum = 0.0;  // skipped terms are exact zeros: same value as the staged reduction's skip
 #pragma unroll
-    for (int q = 0; q < (D == 1 ? NC : (D == 2 ? NC * NC : NC * NC * NC)); ++q) sum += v[q];
+    for (int q = 0; q < (kArr ? NV : 0); ++q) sum += v[q];
     return sum;
 }
 
@@ -218,7 +230,7 @@ __global__ void __launch_bounds__(kFusedThreads) grid3_fused_kernel(const DWin* 
     __syncthreads();
     pdl_wait();  // patches come from the spread / tile_reduce kernels
     // 1. node reduction of my planes
-#pragma unroll 2
+#pragma unroll 3
     for (int k = threadIdx.x; k < mine * L2; k += blockDim.x) {
         const int e[3] = {p0 + k / L2, (k / Lg) % Lg, k % Lg};
         slab0[k] = node_sum<3, NC>(wn, patches, soff, t0lo, e);

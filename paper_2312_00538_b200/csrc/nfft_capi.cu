@@ -731,11 +731,14 @@ struct Engine {
             nslots_cls[D] = static_cast<int>(slots.size()) - slot_begin[D];
         }
         // Fused grid side: every owned window of the class has a non-wrapping
-        // grid whose on-chip working set fits (KSVM_NFFT_GRID=staged disables).
+        // grid whose on-chip working set fits. KSVM_NFFT_GRID = fused12
+        // (default: 1-/2-d classes fused, 3-d staged), fused (all classes),
+        // staged (none).
         {
             const char* ge = std::getenv("KSVM_NFFT_GRID");
-            const bool allow = !(ge && std::string(ge) == "staged");
+            const std::string gm = ge ? ge : "fused12";
             for (int D = 1; D <= 3; ++D) {
+                const bool allow = gm == "fused" || (gm == "fused12" && D < 3);
                 bool ok = allow && nslots_cls[D] > 0;
                 int lg = 0, nc = 0;
                 for (int s = 0; s < P && ok; ++s) {
