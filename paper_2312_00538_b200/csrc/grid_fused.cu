@@ -198,7 +198,10 @@ __device__ __forceinline__ void cluster_barrier() {
 
 // d = 3: grid (C, nslots), cluster (C, 1, 1). Dynamic SMEM: two tables and
 // four slabs of np * Lg^2 doubles (G -> T2, T0 -> X2, T1 -> X3, T3).
-template <int NC>
+// kReduce = false: the grid G was produced by the staged node reduction
+// (reduce_owner_kernel on every SM) and the cluster only runs the three
+// convolution stages (its slab of G is one coalesced read from L2).
+template <int NC, bool kReduce = true>
 __global__ void __launch_bounds__(kFusedThreads) grid3_fused_kernel(const DWin* __restrict__ wins,
                                                                     const int* __restrict__ slots,
                                                                     const double* __restrict__ patches, int np) {
@@ -226,14 +229,20 @@ __global__ void __launch_bounds__(kFusedThreads) grid3_fused_kernel(const DWin* 
     const int t0lo = max(0, min(p0 / wn.TC, wn.ntile - 1) - (NC - 1));
     const int t0hi = min(wn.ntile - 1, max(p1 - 1, 0) / wn.TC);
     stage_tables(wn, sA, sS);
-    stage_offsets(wn, 3, t0lo, t0hi, soff);
+    if constexpr (kReduce) stage_offsets(wn, 3, t0lo, t0hi, soff);
     __syncthreads();
-    pdl_wait();  // patches come from the spread / tile_reduce kernels
-    // 1. node reduction of my planes
+    pdl_wait();  // patches (G) come from the spread / tile_reduce (reduce) kernels
+    // 1. node reduction of my planes (or my planes of the staged reduction's G)
+    if constexpr (kReduce) {
 #pragma unroll 3
-    for (int k = threadIdx.x; k < mine * L2; k += blockDim.x) {
-        const int e[3] = {p0 + k / L2, (k / Lg) % Lg, k % Lg};
-        slab0[k] = node_sum<3, NC>(wn, patches, soff, t0lo, e);
+        for (int k = threadIdx.x; k < mine * L2; k += blockDim.x) {
+            const int e[3] = {p0 + k / L2, (k / Lg) % Lg, k % Lg};
+            slab0[k] = node_sum<3, NC>(wn, patches, soff, t0lo, e);
+        }
+    } else {
+        const double* __restrict__ G = wn.G + static_cast<long long>(p0) * L2;
+#pragma unroll 4
+        for (int k = threadIdx.x; k < mine * L2; k += blockDim.x) slab0[k] = G[k];
     }
     __syncthreads();
     // 2. stage 0 along dim 2: T0 = A2 g, T1 = S2 g (lines (p, i1), 4-output blocks)
@@ -390,7 +399,8 @@ static cudaError_t set_fused_attrs(const void* f, bool cluster) {
 cudaError_t init_fused_attributes() {
     cudaError_t e = cudaSuccess;
     for (const void* f : {reinterpret_cast<const void*>(grid3_fused_kernel<3>),
-                          reinterpret_cast<const void*>(grid3_fused_kernel<5>)})
+                          reinterpret_cast<const void*>(grid3_fused_kernel<5>),
+                          reinterpret_cast<const void*>(grid3_fused_kernel<3, false>)})
         if (e == cudaSuccess) e = set_fused_attrs(f, true);
     for (const void* f : {reinterpret_cast<const void*>(grid12_fused_kernel<1, 2>),
                           reinterpret_cast<const void*>(grid12_fused_kernel<1, 5>),
@@ -428,7 +438,7 @@ bool fused3_supported(int Lg, int NC) {
 // One launch for the grid side of a class: D = 3 as clusters of C CTAs
 // (one cluster per window slot), D = 1, 2 as one CTA per slot.
 void launch_grid_fused(const DWin* wins, const int* slots, int nslots, int D, int NC, int Lg_max,
-                       const double* patches, cudaStream_t st) {
+                       const double* patches, cudaStream_t st, bool conv_only) {
     if (nslots == 0) return;
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(kFusedThreads, 1, 1);
@@ -450,7 +460,9 @@ void launch_grid_fused(const DWin* wins, const int* slots, int nslots, int D, in
         ++na;
         cfg.attrs = attr;
         cfg.numAttrs = na;
-        if (NC == 3)
+        if (conv_only)
+            (void)cudaLaunchKernelEx(&cfg, grid3_fused_kernel<3, false>, wins, slots, patches, np);
+        else if (NC == 3)
             (void)cudaLaunchKernelEx(&cfg, grid3_fused_kernel<3>, wins, slots, patches, np);
         else
             (void)cudaLaunchKernelEx(&cfg, grid3_fused_kernel<5>, wins, slots, patches, np);

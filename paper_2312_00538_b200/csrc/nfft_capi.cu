@@ -47,7 +47,7 @@ cudaError_t init_fused_attributes();
 size_t fused_smem_bytes(int D, int Lg);
 bool fused3_supported(int Lg, int NC);
 void launch_grid_fused(const DWin* wins, const int* slots, int nslots, int D, int NC, int Lg_max,
-                       const double* patches, cudaStream_t st);
+                       const double* patches, cudaStream_t st, bool conv_only);
 
 void launch_combine(double* y, const double* const* src, const int* const* inv, const uint8_t* const* inv8,
                     const double* eta, int P, long long n, cudaStream_t st);
@@ -450,6 +450,7 @@ struct Engine {
     int slot_begin[4] = {0, 0, 0, 0}, nslots_cls[4] = {0, 0, 0, 0};  // d_slots grouped by d
     // fused grid side per class (grid_fused.cu): reduce + all conv stages in one launch
     bool grid_fused[4] = {false, false, false, false};
+    bool grid_conv_only[4] = {false, false, false, false};  // d = 3: staged reduce + fused conv cluster
     int grid_nc[4] = {0, 0, 0, 0}, grid_lg[4] = {0, 0, 0, 0};
     DevBuf<double> d_eta;
     DevBuf<double> patches, parts, vbuf, ybuf;
@@ -731,14 +732,18 @@ struct Engine {
             nslots_cls[D] = static_cast<int>(slots.size()) - slot_begin[D];
         }
         // Fused grid side: every owned window of the class has a non-wrapping
-        // grid whose on-chip working set fits. KSVM_NFFT_GRID = fused12
-        // (default: 1-/2-d classes fused, 3-d staged), fused (all classes),
-        // staged (none).
+        // grid whose on-chip working set fits. KSVM_NFFT_GRID = conv3
+        // (default: 1-/2-d classes fused; 3-d: staged node reduction on every
+        // SM, then the three convolution stages in one cluster launch),
+        // fused12 (3-d fully staged), fused (3-d reduction inside the cluster
+        // too: measured slower, the patch reads on 14 SMs are L2-latency
+        // bound), staged (no fusion).
         {
             const char* ge = std::getenv("KSVM_NFFT_GRID");
-            const std::string gm = ge ? ge : "fused12";
+            const std::string gm = ge ? ge : "conv3";
             for (int D = 1; D <= 3; ++D) {
-                const bool allow = gm == "fused" || (gm == "fused12" && D < 3);
+                const bool conv3 = gm == "conv3" && D == 3;
+                const bool allow = gm == "fused" || ((gm == "fused12" || gm == "conv3") && D < 3) || conv3;
                 bool ok = allow && nslots_cls[D] > 0;
                 int lg = 0, nc = 0;
                 for (int s = 0; s < P && ok; ++s) {
@@ -754,7 +759,9 @@ struct Engine {
                 if (ok && nc > 5) ok = false;
                 if (ok && fused_smem_bytes(D, lg) > 227 * 1024) ok = false;
                 if (ok && D == 3 && !fused3_supported(lg, ncT)) ok = false;
+                if (ok && conv3 && ncT != 3) ok = false;
                 grid_fused[D] = ok;
+                grid_conv_only[D] = ok && conv3;
                 grid_nc[D] = ncT;
                 grid_lg[D] = lg;
             }
@@ -884,11 +891,19 @@ struct Engine {
             launch_tile_reduce(WINS(), d_multi.p + multi_begin[D], n_multi_cls[D], max_pv, PATCHES(), st);
             ++launch_counter();
         }
-        if (grid_fused[D]) {
+        if (grid_conv_only[D]) {  // staged node reduction, then one cluster launch for the conv stages
+            tick("reduce");
+            launch_reduce(WINS(), d_slots.p + slot_begin[D], nslots_cls[D], max_nodes, D, 2 * cfg.window_cutoff,
+                          PATCHES(), false, max_tiles[D], st);
+            tick("conv_d3");
+            launch_grid_fused(WINS(), d_slots.p + slot_begin[D], nslots_cls[D], D, grid_nc[D], grid_lg[D],
+                              PATCHES(), st, true);
+            launch_counter() += 2;
+        } else if (grid_fused[D]) {
             static const char* kGrid[4] = {"", "grid_d1", "grid_d2", "grid_d3"};
             tick(kGrid[D]);
             launch_grid_fused(WINS(), d_slots.p + slot_begin[D], nslots_cls[D], D, grid_nc[D], grid_lg[D],
-                              PATCHES(), st);
+                              PATCHES(), st, false);
             ++launch_counter();
         } else {
             tick("reduce");

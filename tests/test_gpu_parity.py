@@ -179,7 +179,7 @@ def test_duplicate_config4_shape_matches_oracle(oracle_lib):
     assert rel(g.apply(w.v), o.apply(w.v)) <= TOL
 
 
-@pytest.mark.parametrize("grid", ["fused", "fused12", "staged"])
+@pytest.mark.parametrize("grid", ["fused", "fused12", "conv3", "staged"])
 @pytest.mark.parametrize("cfg,n,m", [(2, 60000, 4), (3, 8000, 4), (1, 2000, 4), (2, 5000, 3), (2, 4000, 6)])
 def test_grid_side_variants_match_oracle(oracle_lib, monkeypatch, grid, cfg, n, m):
     # the fused grid side (reduce + separable convolution in one launch: a
