@@ -153,7 +153,7 @@ __device__ __forceinline__ double node_sum(const DWin& wn, const double* __restr
         const bool ok0 = T0 >= 0 && o0 < PE;
         if constexpr (D == 1) {
             const long long off = ok0 ? soff[T0 - t0lo] : -1;
-            put(a0, off >= 0 ? patches[off + o0] : 0.0);
+            put(a0, off >= 0 ? __ldcg(patches + off + o0) : 0.0);
         } else {
 #pragma unroll
             for (int a1 = 0; a1 < NC; ++a1) {
@@ -161,14 +161,14 @@ __device__ __forceinline__ double node_sum(const DWin& wn, const double* __restr
                 const bool ok1 = ok0 && T1 >= 0 && o1 < PE;
                 if constexpr (D == 2) {
                     const long long off = ok1 ? soff[(T0 - t0lo) * nt + T1] : -1;
-                    put(a0 * NC + a1, off >= 0 ? patches[off + o0 * PE + o1] : 0.0);
+                    put(a0 * NC + a1, off >= 0 ? __ldcg(patches + off + o0 * PE + o1) : 0.0);
                 } else {
 #pragma unroll
                     for (int a2 = 0; a2 < NC; ++a2) {
                         const int T2 = thi[2] - a2, o2 = e[2] - T2 * TC;
                         const bool ok2 = ok1 && T2 >= 0 && o2 < PE;
                         const long long off = ok2 ? soff[((T0 - t0lo) * nt + T1) * nt + T2] : -1;
-                        put((a0 * NC + a1) * NC + a2, off >= 0 ? patches[off + (o0 * PE + o1) * PE + o2] : 0.0);
+                        put((a0 * NC + a1) * NC + a2, off >= 0 ? __ldcg(patches + off + (o0 * PE + o1) * PE + o2) : 0.0);
                     }
                 }
             }
@@ -232,6 +232,8 @@ __global__ void __launch_bounds__(kFusedThreads) grid3_fused_kernel(const DWin* 
     if constexpr (kReduce) stage_offsets(wn, 3, t0lo, t0hi, soff);
     __syncthreads();
     pdl_wait();  // patches (G) come from the spread / tile_reduce (reduce) kernels
+    patches = launder(patches);
+    const DWin& wg = *launder(&wn);  // G: read through a pointer loaded after the wait
     // 1. node reduction of my planes (or my planes of the staged reduction's G)
     if constexpr (kReduce) {
 #pragma unroll 3
@@ -240,9 +242,9 @@ __global__ void __launch_bounds__(kFusedThreads) grid3_fused_kernel(const DWin* 
             slab0[k] = node_sum<3, NC>(wn, patches, soff, t0lo, e);
         }
     } else {
-        const double* __restrict__ G = wn.G + static_cast<long long>(p0) * L2;
+        const double* __restrict__ G = wg.G + static_cast<long long>(p0) * L2;
 #pragma unroll 4
-        for (int k = threadIdx.x; k < mine * L2; k += blockDim.x) slab0[k] = G[k];
+        for (int k = threadIdx.x; k < mine * L2; k += blockDim.x) slab0[k] = __ldcg(G + k);
     }
     __syncthreads();
     // 2. stage 0 along dim 2: T0 = A2 g, T1 = S2 g (lines (p, i1), 4-output blocks)
@@ -321,6 +323,7 @@ __global__ void __launch_bounds__(kFusedThreads) grid12_fused_kernel(const DWin*
     stage_offsets(wn, D, 0, wn.ntile - 1, soff);
     __syncthreads();
     pdl_wait();
+    patches = launder(patches);
     for (int k = threadIdx.x; k < nodes; k += blockDim.x) {
         int e[3] = {0, 0, 0};
         if (D == 1) {

@@ -17,6 +17,21 @@ namespace ksvm_nfft {
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// Data a predecessor kernel writes must be read after pdl_wait() with
+// COHERENT loads (__ldcg / ld.global), never ld.global.nc (__ldg, or a plain
+// load through a const __restrict__ pointer): ptxas treats .nc loads as
+// reading memory that is invariant for the whole kernel and may schedule
+// them above griddepcontrol.wait (observed: a v[perm] load issued before the
+// wait; scripts/sass_pdl_check.py lists the .nc loads that precede the wait
+// in every kernel, which must all be plan data). launder() additionally
+// hides a pointer's value from the compiler, so address arithmetic on it
+// cannot be hoisted either.
+template <typename T>
+__device__ __forceinline__ T* launder(T* p) {
+    asm volatile("" : "+l"(p));
+    return p;
+}
+
 inline bool pdl_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("KSVM_NFFT_PDL");

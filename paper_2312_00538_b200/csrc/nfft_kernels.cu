@@ -149,7 +149,7 @@ __device__ __forceinline__ void load_halo(double* halo, const DWin& wn, const in
                 ok = ok && tc[t] * TC + n[t] < Lg;
                 off = off * Lg + n[t];
             }
-            double h = ok ? __ldg(wn.H + base + off) : 0.0;
+            double h = ok ? __ldcg(wn.H + base + off) : 0.0;
             if (kFoldR) {  // tile-relative window factor R[j0] R[j1] R[j2] (factors_kernel)
 #pragma unroll
                 for (int t = 0; t < D; ++t) h *= sR[n[t]];
@@ -159,7 +159,7 @@ __device__ __forceinline__ void load_halo(double* halo, const DWin& wn, const in
             long long gi = 0;
 #pragma unroll
             for (int t = 0; t < D; ++t) gi = gi * Lg + pmod(wn.lo + tc[t] * TC + n[t], wn.M);
-            double h = __ldg(wn.H + gi);
+            double h = __ldcg(wn.H + gi);
             if (kFoldR) {
 #pragma unroll
                 for (int t = 0; t < D; ++t) h *= sR[n[t]];
@@ -187,7 +187,7 @@ __device__ __forceinline__ void load_halo3_r(double* halo, const DWin& wn, const
 #pragma unroll
         for (int n0 = 0; n0 < PE; ++n0) {
             const bool ok = ok12 && i0 + n0 < Lg;
-            halo[n0 * PE * PE + k] = ok ? __ldg(src + n0 * plane) * (r12 * sR[n0]) : 0.0;
+            halo[n0 * PE * PE + k] = ok ? __ldcg(src + n0 * plane) * (r12 * sR[n0]) : 0.0;
         }
     } else {
         const long long o12 = static_cast<long long>(pmod(wn.lo + tc[1] * TC + n1, wn.M)) * Lg +
@@ -195,7 +195,7 @@ __device__ __forceinline__ void load_halo3_r(double* halo, const DWin& wn, const
         int i0 = pmod(wn.lo + tc[0] * TC, wn.M);
 #pragma unroll
         for (int n0 = 0; n0 < PE; ++n0) {
-            halo[n0 * PE * PE + k] = __ldg(wn.H + i0 * plane + o12) * (r12 * sR[n0]);
+            halo[n0 * PE * PE + k] = __ldcg(wn.H + i0 * plane + o12) * (r12 * sR[n0]);
             i0 = i0 + 1 == wn.M ? 0 : i0 + 1;
         }
     }
@@ -274,7 +274,9 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     for (int k = lane; k < PV; k += 32) wp[k] = 0.0;
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
-    pdl_wait();
+    Pref<D> pa, pb;  // plan data: prefetched before the dependency wait
+    if (wb + lane < we) pa.load(ps, wb + lane);
+    if (wb + 32 + lane < we) pb.load(ps, wb + 32 + lane);
 
     double acc[8][2];
 #pragma unroll
@@ -306,22 +308,19 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     };
 
     // software pipeline: per-point factors two batches ahead, v one batch ahead
-    Pref<D> pa, pb;
     double va = 0.0;
     {
-        const int i0 = wb + lane, i1 = wb + 32 + lane;
-        if (i0 < we) {
-            pa.load(ps, i0);
-            va = __ldg(v + pa.perm);
-        }
-        if (i1 < we) pb.load(ps, i1);
+        const int i0 = wb + lane;
+        pdl_wait();  // v may come from the previous kernel (plan factors above did not)
+        v = launder(v);
+        if (i0 < we) va = __ldcg(v + pa.perm);
     }
     __syncwarp();
     for (int base = wb; base < we; base += 32) {
         const int cnt = min(32, we - base);
         if (lane < cnt) stage_pow<D, S>(stage + lane * RL, pa.P * va, pa.Q, pa.code);
         pa = pb;
-        if (base + 32 + lane < we) va = __ldg(v + pa.perm);
+        if (base + 32 + lane < we) va = __ldcg(v + pa.perm);
         if (base + 64 + lane < we) pb.load(ps, base + 64 + lane);
         __syncwarp();
         int p = 0;
@@ -399,7 +398,9 @@ spread3c_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pse
     for (int k = lane; k < SUB; k += 32) wp[k] = 0.0;
     const int wb = __ldg(colb + blockIdx.x * kColBounds + 2 * warp);
     const int we = __ldg(colb + blockIdx.x * kColBounds + 2 * warp + 2);
-    pdl_wait();
+    Pref<3> pa, pb;  // plan data: prefetched before the dependency wait
+    if (wb + lane < we) pa.load(ps, wb + lane);
+    if (wb + 32 + lane < we) pb.load(ps, wb + 32 + lane);
 
     double acc[PE][2];
 #pragma unroll
@@ -434,16 +435,10 @@ spread3c_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pse
         dmma(acc[10][0], acc[10][1], c10 * w1g, bq);
     };
 
-    Pref<3> pa, pb;
     double va = 0.0;
-    {
-        const int i0 = wb + lane, i1 = wb + 32 + lane;
-        if (i0 < we) {
-            pa.load(ps, i0);
-            va = __ldg(v + pa.perm);
-        }
-        if (i1 < we) pb.load(ps, i1);
-    }
+    pdl_wait();  // v may come from the previous kernel (plan factors above did not)
+    v = launder(v);
+    if (wb + lane < we) va = __ldcg(v + pa.perm);
     __syncwarp();
     for (int base = wb; base < we; base += 32) {
         const int cnt = min(32, we - base);
@@ -468,7 +463,7 @@ spread3c_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pse
             *reinterpret_cast<int*>(st + kCode) = pa.code;
         }
         pa = pb;
-        if (base + 32 + lane < we) va = __ldg(v + pa.perm);
+        if (base + 32 + lane < we) va = __ldcg(v + pa.perm);
         if (base + 64 + lane < we) pb.load(ps, base + 64 + lane);
         __syncwarp();
         int p = 0;
@@ -543,14 +538,14 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     tile_coords(it.tile, D, wn.ntile, tc);
     __shared__ double sR[PE];
     if (threadIdx.x < PE) sR[threadIdx.x] = wn.R[threadIdx.x];
-    __syncthreads();
-    pdl_wait();
-    load_halo3_r<PE, TC>(halo, wn, tc, sR);
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
-    Pref<D> pa, pb;  // factors of the current and the next batch
+    Pref<D> pa, pb;  // factors of the current and the next batch (plan data: before the wait)
     if (wb + lane < we) pa.load(ps, wb + lane);
     if (wb + 32 + lane < we) pb.load(ps, wb + 32 + lane);
+    __syncthreads();
+    pdl_wait();
+    load_halo3_r<PE, TC>(halo, *launder(&wn), tc, sR);  // H: written by the grid kernels
     __syncthreads();
 
     // B fragments: hb[k] = H[(k/2, 4(k%2)+t), c = g] of the current cell
@@ -640,9 +635,13 @@ gather3c_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pse
     const int col = 4 * l0 + warp;
     const int wb = __ldg(colb + blockIdx.x * kColBounds + col);
     const int we = __ldg(colb + blockIdx.x * kColBounds + col + 1);
+    Pref<3> pa, pb;  // plan data: prefetched before the dependency wait
+    if (wb + lane < we) pa.load(ps, wb + lane);
+    if (wb + 32 + lane < we) pb.load(ps, wb + 32 + lane);
     __syncthreads();
     pdl_wait();
     if (threadIdx.x < PE * PE) {  // column (n1, n2) of the slab, walking n0 = l0 .. l0 + 7
+        const double* __restrict__ Hg = launder(wn.H);  // written by the grid kernels
         const int k = threadIdx.x, n1 = k / PE, n2 = k - n1 * PE;
         const int Lg = wn.Lg;
         const long long plane = static_cast<long long>(Lg) * Lg;
@@ -650,11 +649,11 @@ gather3c_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pse
         if (!wn.wrap) {
             const int i0 = tc[0] * TC + l0, i1 = tc[1] * TC + n1, i2 = tc[2] * TC + n2;
             const bool ok12 = i1 < Lg && i2 < Lg;
-            const double* src = wn.H + (static_cast<long long>(i0) * Lg + i1) * Lg + i2;
+            const double* src = Hg + (static_cast<long long>(i0) * Lg + i1) * Lg + i2;
 #pragma unroll
             for (int a = 0; a < S; ++a) {
                 const bool ok = ok12 && i0 + a < Lg;
-                halo[a * PE * PE + k] = ok ? __ldg(src + a * plane) * (r12 * sR[l0 + a]) : 0.0;
+                halo[a * PE * PE + k] = ok ? __ldcg(src + a * plane) * (r12 * sR[l0 + a]) : 0.0;
             }
         } else {
             const long long o12 = static_cast<long long>(pmod(wn.lo + tc[1] * TC + n1, wn.M)) * Lg +
@@ -662,14 +661,11 @@ gather3c_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pse
             int i0 = pmod(wn.lo + tc[0] * TC + l0, wn.M);
 #pragma unroll
             for (int a = 0; a < S; ++a) {
-                halo[a * PE * PE + k] = __ldg(wn.H + i0 * plane + o12) * (r12 * sR[l0 + a]);
+                halo[a * PE * PE + k] = __ldcg(Hg + i0 * plane + o12) * (r12 * sR[l0 + a]);
                 i0 = i0 + 1 == wn.M ? 0 : i0 + 1;
             }
         }
     }
-    Pref<3> pa, pb;
-    if (wb + lane < we) pa.load(ps, wb + lane);
-    if (wb + 32 + lane < we) pb.load(ps, wb + 32 + lane);
     __syncthreads();
     if (wb >= we) return;
 
@@ -751,7 +747,9 @@ spread2_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     for (int k = lane; k < PV; k += 32) wp[k] = 0.0;
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
-    pdl_wait();
+    Pref<D> pa, pb;  // plan data: prefetched before the dependency wait
+    if (wb + lane < we) pa.load(ps, wb + lane);
+    if (wb + 32 + lane < we) pb.load(ps, wb + 32 + lane);
     const int a = lane >> 2, b0 = (lane & 3) << 1;
     double acc0 = 0.0, acc1 = 0.0;
     int cur = -1;
@@ -762,22 +760,19 @@ spread2_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
         acc0 = acc1 = 0.0;
     };
     // software pipeline: per-point factors two batches ahead, v one batch ahead
-    Pref<D> pa, pb;
     double va = 0.0;
     {
-        const int i0 = wb + lane, i1 = wb + 32 + lane;
-        if (i0 < we) {
-            pa.load(ps, i0);
-            va = __ldg(v + pa.perm);
-        }
-        if (i1 < we) pb.load(ps, i1);
+        const int i0 = wb + lane;
+        pdl_wait();  // v may come from the previous kernel (plan factors above did not)
+        v = launder(v);
+        if (i0 < we) va = __ldcg(v + pa.perm);
     }
     __syncwarp();
     for (int base = wb; base < we; base += 32) {
         const int cnt = min(32, we - base);
         if (lane < cnt) stage_row<D, S>(stage + lane * RL, R, pa.P * va, pa.Q, pa.code);
         pa = pb;
-        if (base + 32 + lane < we) va = __ldg(v + pa.perm);
+        if (base + 32 + lane < we) va = __ldcg(v + pa.perm);
         if (base + 64 + lane < we) pb.load(ps, base + 64 + lane);
         __syncwarp();
         for (int p = 0; p < cnt; ++p) {
@@ -823,13 +818,13 @@ gather2_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     for (int o = 0; o < S; ++o) R[o] = wn.R[o];
     int tc[3];
     tile_coords(it.tile, D, wn.ntile, tc);
-    pdl_wait();
-    load_halo<D, PE, TC>(halo, wn, tc, TC, PE, PV);
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
-    Pref<D> pa, pb;
+    Pref<D> pa, pb;  // plan data: prefetched before the dependency wait
     if (wb + lane < we) pa.load(ps, wb + lane);
     if (wb + 32 + lane < we) pb.load(ps, wb + 32 + lane);
+    pdl_wait();
+    load_halo<D, PE, TC>(halo, *launder(&wn), tc, TC, PE, PV);
     int permc = 0;
     __syncthreads();
     const int a = lane >> 2, b0 = (lane & 3) << 1;
@@ -892,10 +887,11 @@ spread1_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
     pdl_wait();
+    v = launder(v);
     for (int i = wb + lane; i < we; i += 32) {
         const double2 f = __ldg(reinterpret_cast<const double2*>(ps.F + i));
         const int2 cp = __ldg(ps.CP + i);
-        double q = f.x * __ldg(v + cp.y);
+        double q = f.x * __ldcg(v + cp.y);
         const double Q = f.y;
         double* col = lp + cp.x * 32 + lane;
 #pragma unroll
@@ -931,7 +927,7 @@ gather1_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     int tc[3];
     tile_coords(it.tile, D, wn.ntile, tc);
     pdl_wait();
-    load_halo<D, PE, TC>(smem, wn, tc, TC, PE, PE);
+    load_halo<D, PE, TC>(smem, *launder(&wn), tc, TC, PE, PE);
     __syncthreads();
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
@@ -991,7 +987,7 @@ __global__ void spread_generic_kernel(const Item* __restrict__ items,
             const double4 f = ps.F[i];
             const double Qs[3] = {f.y, f.z, f.w};
             for (int t = 0; t < D; ++t) {
-                double q = t == 0 ? f.x * v[ps.CP[i].y] : 1.0;
+                double q = t == 0 ? f.x * __ldcg(v + ps.CP[i].y) : 1.0;
                 const double Q = Qs[t];
                 for (int o = 0; o < S; ++o) {
                     st[t * kMaxSpan + o] = q * wn.R[o];
@@ -1056,7 +1052,7 @@ __global__ void gather_generic_kernel(const Item* __restrict__ items,
     int tc[3] = {0, 0, 0};
     tile_coords(it.tile, D, wn.ntile, tc);
     pdl_wait();
-    load_halo<D>(halo, wn, tc, TC, PE, PV);
+    load_halo<D>(halo, *launder(&wn), tc, TC, PE, PV);
     __syncthreads();
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
@@ -1126,15 +1122,16 @@ __global__ void tile_reduce_kernel(const DWin* __restrict__ wins, const int2* __
     double* base = patches + wn.patch_base + static_cast<long long>(k0 - wn.item_base) * PV;
     const int nk = k1 - k0;
     pdl_wait();
+    base = launder(base);  // patches: written by the spread kernels
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < PV; e += gridDim.x * blockDim.x) {
         // eight interleaved partial sums (8 loads in flight), combined in a fixed order
         double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         int k = 0;
         for (; k + 8 <= nk; k += 8) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) s[j] += base[static_cast<long long>(k + j) * PV + e];
+            for (int j = 0; j < 8; ++j) s[j] += __ldcg(base + static_cast<long long>(k + j) * PV + e);
         }
-        for (int j = 0; k + j < nk; ++j) s[j] += base[static_cast<long long>(k + j) * PV + e];
+        for (int j = 0; k + j < nk; ++j) s[j] += __ldcg(base + static_cast<long long>(k + j) * PV + e);
         base[e] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
     }
 }
@@ -1149,6 +1146,7 @@ __global__ void reduce_patches_kernel(const DWin* __restrict__ wins, const int* 
     pdl_trigger();
     const DWin& wn = wins[slots[blockIdx.y]];
     pdl_wait();
+    patches = launder(patches);
     if (wn.d != D || !wn.wrap) return;  // non-wrapping grids use reduce_owner_kernel
     const int Lg = wn.Lg, TC = wn.TC, PE = wn.PE, nt = wn.ntile;
     int nodes = 1;
@@ -1178,7 +1176,7 @@ __global__ void reduce_patches_kernel(const DWin* __restrict__ wins, const int* 
             if (T0 < 0 || o0 >= PE) continue;
             if constexpr (D == 1) {
                 const long long off = tp[T0];
-                if (off >= 0) sum += patches[off + o0];
+                if (off >= 0) sum += __ldcg(patches + off + o0);
             } else {
 #pragma unroll
                 for (int a1 = 0; a1 < NC; ++a1) {
@@ -1186,14 +1184,14 @@ __global__ void reduce_patches_kernel(const DWin* __restrict__ wins, const int* 
                     if (T1 < 0 || o1 >= PE) continue;
                     if constexpr (D == 2) {
                         const long long off = tp[T0 * nt + T1];
-                        if (off >= 0) sum += patches[off + o0 * PE + o1];
+                        if (off >= 0) sum += __ldcg(patches + off + o0 * PE + o1);
                     } else {
 #pragma unroll
                         for (int a2 = 0; a2 < NC; ++a2) {
                             const int T2 = thi[2] - a2, o2 = lg[2] - T2 * TC;
                             if (T2 < 0 || o2 >= PE) continue;
                             const long long off = tp[(T0 * nt + T1) * nt + T2];
-                            if (off >= 0) sum += patches[off + (o0 * PE + o1) * PE + o2];
+                            if (off >= 0) sum += __ldcg(patches + off + (o0 * PE + o1) * PE + o2);
                         }
                     }
                 }
@@ -1212,19 +1210,19 @@ __global__ void reduce_patches_kernel(const DWin* __restrict__ wins, const int* 
                 const int o0 = e0 - T0 * TC;
                 if constexpr (D == 1) {
                     const long long off = tp[T0];
-                    if (off >= 0) sum += patches[off + o0];
+                    if (off >= 0) sum += __ldcg(patches + off + o0);
                 } else {
                     for (int e1 = e0s[1]; e1 < Eext; e1 += wn.M)
                         for (int T1 = KSVM_TLO(e1); T1 <= KSVM_THI(e1); ++T1) {
                             const int o1 = o0 * PE + e1 - T1 * TC;
                             if constexpr (D == 2) {
                                 const long long off = tp[T0 * nt + T1];
-                                if (off >= 0) sum += patches[off + o1];
+                                if (off >= 0) sum += __ldcg(patches + off + o1);
                             } else {
                                 for (int e2 = e0s[2]; e2 < Eext; e2 += wn.M)
                                     for (int T2 = KSVM_TLO(e2); T2 <= KSVM_THI(e2); ++T2) {
                                         const long long off = tp[(T0 * nt + T1) * nt + T2];
-                                        if (off >= 0) sum += patches[off + o1 * PE + e2 - T2 * TC];
+                                        if (off >= 0) sum += __ldcg(patches + off + o1 * PE + e2 - T2 * TC);
                                     }
                             }
                         }
@@ -1305,6 +1303,7 @@ __device__ void reduce_owner_unit(const DWin& wn, int tileT, const double* __res
     }
     const bool have = *any != 0;
     pdl_wait();  // patches come from the spread / tile_reduce kernels
+    patches = launder(patches);
     for (int k = threadIdx.x; k < nodes; k += blockDim.x) {
         int r = k, e[3] = {0, 0, 0};
 #pragma unroll
@@ -1341,7 +1340,7 @@ __device__ void reduce_owner_unit(const DWin& wn, int tileT, const double* __res
                     o = o * PE + od[t][a[t]];
                 }
                 const long long off = soff[q];
-                if (ok && off >= 0) sum += patches[off + o];
+                if (ok && off >= 0) sum += __ldcg(patches + off + o);
             }
         }
         long long gi = 0;
@@ -1379,14 +1378,16 @@ __device__ void conv_tile_unit(const DWin& wn, int stage, int tile) {
     const double* __restrict__ tS = wn.tabS;
     const int KS = (Lg + 3) >> 2;
     pdl_wait();  // G / T come from the reduce / previous stage
+    in0 = launder(in0);
+    if (in1) in1 = launder(in1);
     double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
     double e00 = 0.0, e01 = 0.0, e10 = 0.0, e11 = 0.0;
 #pragma unroll 4
     for (int ks = 0; ks < KS; ++ks) {
         const int j = 4 * ks + t;
         const bool jok = j < Lg && fok;
-        const double bx = jok ? in0[bb + j * jstride] : 0.0;
-        const double by = (jok && two_in) ? in1[bb + j * jstride] : 0.0;
+        const double bx = jok ? __ldcg(in0 + bb + j * jstride) : 0.0;
+        const double by = (jok && two_in) ? __ldcg(in1 + bb + j * jstride) : 0.0;
         const int r = i0 + g - j;
         const bool rok = r > -Lg && r < Lg;
         const double a = rok ? __ldg(tA + r + Lg - 1) : 0.0;
@@ -1506,7 +1507,7 @@ __global__ void combine_kernel(double* __restrict__ y, const double* const* __re
          j += static_cast<long long>(gridDim.x) * blockDim.x) {
         double acc = 0.0;
         if (!any_map) {
-            for (int l = 0; l < P; ++l) acc += s_eta[l] * __ldg(s_src[l] + j);
+            for (int l = 0; l < P; ++l) acc += s_eta[l] * __ldcg(s_src[l] + j);
         } else {
             for (int l = 0; l < P; ++l) {
                 // exact-duplicate window: the value of the point's distinct point
@@ -1515,7 +1516,7 @@ __global__ void combine_kernel(double* __restrict__ y, const double* const* __re
                 const uint8_t* i8 = sm ? s_inv8[l] : inv8[l];
                 const long long k =
                     i8 ? static_cast<long long>(__ldg(i8 + j)) : (iv ? static_cast<long long>(__ldg(iv + j)) : j);
-                acc += (sm ? s_eta[l] : eta[l]) * (sm ? s_src[l] : src[l])[k];
+                acc += (sm ? s_eta[l] : eta[l]) * __ldcg((sm ? s_src[l] : src[l]) + k);
             }
         }
         y[j] = acc;
@@ -1534,7 +1535,7 @@ __global__ void seg_partial_kernel(const double* __restrict__ v, const int* __re
     if (c >= C) return;
     const int2 ch = chunks[c];
     double s = 0.0;
-    for (int i = ch.x + lane; i < ch.y; i += 32) s += __ldg(v + __ldg(members + i));
+    for (int i = ch.x + lane; i < ch.y; i += 32) s += __ldcg(v + __ldg(members + i));
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) partial[c] = s;
@@ -1561,7 +1562,8 @@ bins_partial_kernel(const double* __restrict__ v, const uint8_t* const* __restri
 #pragma unroll
     for (int u = 0; u < NB; ++u) bins[warp][u][lane] = 0.0;
     pdl_wait();
-    for (long long i = b0 + threadIdx.x; i < b1; i += blockDim.x) bins[warp][__ldg(cq + i)][lane] += __ldg(v + i);
+    v = launder(v);
+    for (long long i = b0 + threadIdx.x; i < b1; i += blockDim.x) bins[warp][__ldg(cq + i)][lane] += __ldcg(v + i);
     __syncwarp();
     if (lane < NB) {
         double s = 0.0;
@@ -1586,7 +1588,7 @@ __global__ void bins_sum_kernel(const double* __restrict__ partial, int nblk, in
     const int q = blockIdx.x, u = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (q >= nwl || u >= nu[q]) return;
     double acc = 0.0;
-    for (int b = lane; b < nblk; b += 32) acc += partial[(static_cast<long long>(b) * nwl + q) * NB + u];
+    for (int b = lane; b < nblk; b += 32) acc += __ldcg(partial + (static_cast<long long>(b) * nwl + q) * NB + u);
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) vs[vs_off[q] + u] = acc;
@@ -1604,7 +1606,7 @@ __global__ void seg_sum_kernel(const double* __restrict__ partial, const int* __
     const int c0 = seg_cb[u], c1 = seg_cb[u + 1];
     if (c0 == c1) return;  // entry of a register-bin window (bins_sum_kernel)
     double acc = 0.0;
-    for (int c = c0 + lane; c < c1; c += 32) acc += partial[c];
+    for (int c = c0 + lane; c < c1; c += 32) acc += __ldcg(partial + c);
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0) vs[u] = acc;

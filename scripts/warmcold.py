@@ -1,5 +1,7 @@
 """Diagnostic: apply time with and without the 256 MiB L2 flush (config 2)."""
+import os
 import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2312_00538_b200 import AnovaKernelSpec, Dataset, FeatureWindowing, anova_fast_operator, workloads
 

@@ -15,7 +15,7 @@ from paper_2312_00538_b200 import (AnovaKernelSpec, Dataset, DomainError, Fastsu
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-10
-GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "ref_*.npz")))
 
 
 def rel(a, b):
