@@ -359,14 +359,23 @@ void build_pointset(PointSet& ps, const std::vector<double>& scaled_cm, int64_t 
 
 // Points per spread item: ~24 items per SM over all windows of the operator
 // (load balance) but no more, since each item writes one (TC+2m-1)^d patch
-// that must be reduced. Gather items carry no patch, so they are finer.
+// that must be reduced; d = 3 items hold >= 1024 points (measured: 2048
+// left config 3's dense tiles too coarse, 512 cost more patch reduction).
+// Gather items carry no patch, so they are finer.
 int64_t item_chunk(int64_t total_points, int d) {
     // d = 3: large items (a 4^3-cell tile is rarely split, so no pre-reduce);
     // d <= 2 have few, large tiles and need splitting for parallelism
-    return std::max<int64_t>(d == 3 ? 2048 : 512, (total_points + 148 * 24 - 1) / (148 * 24));
+    int64_t floor_pts = d == 3 ? 1024 : 512;
+    if (const char* e = std::getenv(d == 3 ? "KSVM_NFFT_ITEM3" : "KSVM_NFFT_ITEM12")) floor_pts = std::max(32, std::atoi(e));
+    return std::max<int64_t>(floor_pts, (total_points + 148 * 24 - 1) / (148 * 24));
 }
-int64_t gather_chunk(int64_t total_points) {
-    return std::max<int64_t>(128, (total_points + 148 * 48 - 1) / (148 * 48));
+// d = 3 gather items load an 11^3 halo (10.6 KB) each: >= 512 points
+// amortise it (config 3: 0.1865 -> 0.1721 ms); d <= 2 halos are small, so
+// finer items balance better (config 2's d = 2 gather).
+int64_t gather_chunk(int64_t total_points, int d) {
+    int64_t floor_pts = d == 3 ? 512 : 128;
+    if (const char* e = std::getenv("KSVM_NFFT_GITEM")) floor_pts = std::max(32, std::atoi(e));
+    return std::max<int64_t>(floor_pts, (total_points + 148 * 48 - 1) / (148 * 48));
 }
 
 // Affine map of P:src/fastsum.cpp:126-140 on a column-major n x d block.
@@ -610,11 +619,11 @@ struct Engine {
                 w.inv.upload(inv.data(), inv.size(), stream);
             }
             build_pointset(w.src, su, nu, d, g, item_chunk(n * n_owned_windows, d),
-                           gather_chunk(n * n_owned_windows), stream);
+                           gather_chunk(n * n_owned_windows, d), stream);
         } else {
             w.nu = 0;
             build_pointset(w.src, sc, n, d, g, item_chunk(n * n_owned_windows, d),
-                           gather_chunk(n * n_owned_windows), stream);
+                           gather_chunk(n * n_owned_windows, d), stream);
         }
 
         DWin& dw = w.dw;
@@ -1658,7 +1667,7 @@ int ksvm_nfft_plan_apply_cross(const ksvm_nfft_plan* plan, const double* targets
         std::lock_guard<std::mutex> lk(E.mu);
         const Geometry g = w.geom;
         PointSet tp;
-        build_pointset(tp, sc, t, w.d, g, item_chunk(t, w.d), gather_chunk(t), E.stream);
+        build_pointset(tp, sc, t, w.d, g, item_chunk(t, w.d), gather_chunk(t, w.d), E.stream);
         DevBuf<double> tout;
         tout.alloc(t);
         DPSet dp{};
