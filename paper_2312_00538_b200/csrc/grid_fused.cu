@@ -375,6 +375,10 @@ static size_t tables_doubles(int Lg) { return static_cast<size_t>(((2 * Lg + 6) 
 
 // Planes per CTA for d = 3 (C = ceil(Lg / np) CTAs per cluster, C <= 16).
 int fused3_planes(int Lg) { return (Lg + kFusedMaxCluster - 1) / kFusedMaxCluster; }
+int fused3_cluster_size(int Lg) {
+    const int np = fused3_planes(Lg);
+    return (Lg + np - 1) / np;
+}
 
 // Tile grid bound: ntile = ceil(ncell / TC) <= ceil(Lg / TC), TC = 4 / 8 / 32 for d = 3 / 2 / 1.
 static long long tiles_bound(int D, int Lg) {

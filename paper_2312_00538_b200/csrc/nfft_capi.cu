@@ -46,11 +46,12 @@ int conv_max_lg();
 cudaError_t init_fused_attributes();
 size_t fused_smem_bytes(int D, int Lg);
 bool fused3_supported(int Lg, int NC);
+int fused3_cluster_size(int Lg);
 void launch_grid_fused(const DWin* wins, const int* slots, int nslots, int D, int NC, int Lg_max,
                        const double* patches, cudaStream_t st, bool conv_only);
 
 void launch_combine(double* y, const double* const* src, const int* const* inv, const uint8_t* const* inv8,
-                    const double* eta, int P, long long n, cudaStream_t st);
+                    const int* nu8, const double* eta, int P, long long n, cudaStream_t st);
 void launch_bin_sums(const double* v, const uint8_t* const* codes, int nwl, long long n, double* partial,
                      int nblk, const long long* vs_off, const int* nu, double* vs, cudaStream_t st);
 void launch_seg_sums(const double* v, const int* members, const int2* chunks, double* partial, int C,
@@ -471,6 +472,7 @@ struct Engine {
     DevBuf<const double*> d_src;
     DevBuf<const int*> d_inv;
     DevBuf<const uint8_t*> d_inv8, d_codes;  // combine maps; codes of the register-bin windows
+    DevBuf<int> d_nu8;                       // distinct points of each register-bin window (0: other)
     DevBuf<long long> d_small_off;
     DevBuf<int> d_small_nu;
     DevBuf<double> bin_partial;
@@ -769,6 +771,9 @@ struct Engine {
                 if (ok && fused_smem_bytes(D, lg) > 227 * 1024) ok = false;
                 if (ok && D == 3 && !fused3_supported(lg, ncT)) ok = false;
                 if (ok && conv3 && ncT != 3) ok = false;
+                // one cluster per window: past one wave of SMs (config 4's 18
+                // windows x 14 CTAs) the staged convolutions use the GPU better
+                if (ok && D == 3 && static_cast<long long>(nslots_cls[D]) * fused3_cluster_size(lg) > 148) ok = false;
                 grid_fused[D] = ok;
                 grid_conv_only[D] = ok && conv3;
                 grid_nc[D] = ncT;
@@ -789,6 +794,7 @@ struct Engine {
         std::vector<const double*> srcs(static_cast<size_t>(P));
         std::vector<const int*> invs(static_cast<size_t>(P), nullptr);
         std::vector<const uint8_t*> inv8s(static_cast<size_t>(P), nullptr), codes;
+        std::vector<int> nu8s(static_cast<size_t>(std::max(P, 1)), 0);
         std::vector<long long> small_off;
         std::vector<int> small_nu;
         long long uoff = 0;
@@ -809,6 +815,7 @@ struct Engine {
                 p.out = uout_all.p + uoff;
                 srcs[static_cast<size_t>(s)] = p.out;
                 inv8s[static_cast<size_t>(s)] = w.inv8.p;
+                nu8s[static_cast<size_t>(s)] = static_cast<int>(w.nu);
                 uoff += w.nu;
             } else if (w.nu > 0) {
                 // the CSR segments are numbered in vs_all order: pad the
@@ -845,6 +852,7 @@ struct Engine {
         d_src.upload(srcs.data(), srcs.size(), stream);
         d_inv.upload(invs.data(), invs.size(), stream);
         d_inv8.upload(inv8s.data(), inv8s.size(), stream);
+        d_nu8.upload(nu8s.data(), nu8s.size(), stream);
         n_small = static_cast<int>(codes.size());
         if (n_small > 0) {
             d_codes.upload(codes.data(), codes.size(), stream);
@@ -993,7 +1001,7 @@ struct Engine {
         nticks = 0;
         run_classes(v, true);
         tick("combine");
-        launch_combine(y, SRC(), d_inv.p, d_inv8.p, d_eta.p, P, n, S());
+        launch_combine(y, SRC(), d_inv.p, d_inv8.p, d_nu8.p, d_eta.p, P, n, S());
         ++launch_counter();
         CK(cudaGetLastError());
         tick("end");

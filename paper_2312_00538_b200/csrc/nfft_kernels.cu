@@ -1481,19 +1481,26 @@ conv_stage_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots, 
 
 // y[j] = sum over owned windows (ascending) of eta_l * out_l[j]
 // (P:src/fastsum.cpp:346-351: out = 0; out += eta_l * apply_l).
-__global__ void combine_kernel(double* __restrict__ y, const double* const* __restrict__ src,
-                               const int* const* __restrict__ inv, const uint8_t* const* __restrict__ inv8,
-                               const double* __restrict__ eta, int P, long long n) {
+// Duplicate-merged windows with <= kSmallBins distinct points read their
+// distinct-point outputs from an SMEM table (filled after the wait: the
+// gathers write them) through one-byte codes (plan data), so no value load
+// waits on a code load from memory.
+__global__ void __launch_bounds__(256)
+combine_kernel(double* __restrict__ y, const double* const* __restrict__ src,
+               const int* const* __restrict__ inv, const uint8_t* const* __restrict__ inv8,
+               const int* __restrict__ nu8, const double* __restrict__ eta, int P, long long n) {
     constexpr int kMaxP = 64;  // window table staged in SMEM (plan data, before the wait)
     __shared__ const double* s_src[kMaxP];
     __shared__ const int* s_inv[kMaxP];
     __shared__ const uint8_t* s_inv8[kMaxP];
     __shared__ double s_eta[kMaxP];
-    __shared__ int s_any;
+    __shared__ double s_tab[kMaxP][kSmallBins];
     pdl_trigger();
-    if (threadIdx.x == 0) s_any = 0;
+    __shared__ int s_any;
+    const int PS = min(P, kMaxP);
+    if (threadIdx.x == 0) s_any = P > kMaxP;
     __syncthreads();
-    for (int l = threadIdx.x; l < min(P, kMaxP); l += blockDim.x) {
+    for (int l = threadIdx.x; l < PS; l += blockDim.x) {
         s_src[l] = src[l];
         s_inv[l] = inv[l];
         s_inv8[l] = inv8[l];
@@ -1501,22 +1508,38 @@ __global__ void combine_kernel(double* __restrict__ y, const double* const* __re
         if (inv[l] || inv8[l]) s_any = 1;
     }
     __syncthreads();
-    const bool any_map = s_any != 0 || P > kMaxP;
+    const bool any_map = s_any != 0;
     pdl_wait();
+    if (!any_map) {  // no duplicate-merged window: straight window-order sum
+        for (long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
+             j += static_cast<long long>(gridDim.x) * blockDim.x) {
+            double acc = 0.0;
+            for (int l = 0; l < P; ++l) acc += s_eta[l] * __ldcg(s_src[l] + j);
+            y[j] = acc;
+        }
+        return;
+    }
+    for (int k = threadIdx.x; k < PS * kSmallBins; k += blockDim.x) {
+        const int l = k / kSmallBins, u = k - l * kSmallBins;
+        if (s_inv8[l] && u < nu8[l]) s_tab[l][u] = __ldcg(s_src[l] + u);  // outputs of this apply's gathers
+    }
+    __syncthreads();
     for (long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
          j += static_cast<long long>(gridDim.x) * blockDim.x) {
         double acc = 0.0;
-        if (!any_map) {
-            for (int l = 0; l < P; ++l) acc += s_eta[l] * __ldcg(s_src[l] + j);
-        } else {
-            for (int l = 0; l < P; ++l) {
-                // exact-duplicate window: the value of the point's distinct point
-                const bool sm = l < kMaxP;
-                const int* iv = sm ? s_inv[l] : inv[l];
-                const uint8_t* i8 = sm ? s_inv8[l] : inv8[l];
-                const long long k =
-                    i8 ? static_cast<long long>(__ldg(i8 + j)) : (iv ? static_cast<long long>(__ldg(iv + j)) : j);
-                acc += (sm ? s_eta[l] : eta[l]) * __ldcg((sm ? s_src[l] : src[l]) + k);
+#pragma unroll 4
+        for (int l = 0; l < P; ++l) {  // window order; the unrolled windows' loads are in flight together
+            double val;
+            if (l < kMaxP) {
+                const uint8_t* i8 = s_inv8[l];
+                const int* iv = s_inv[l];
+                if (i8) val = s_tab[l][__ldg(i8 + j)];
+                else val = __ldcg(s_src[l] + (iv ? static_cast<long long>(__ldg(iv + j)) : j));
+                acc += s_eta[l] * val;
+            } else {
+                const long long k = inv8[l] ? static_cast<long long>(__ldg(inv8[l] + j))
+                                            : (inv[l] ? static_cast<long long>(__ldg(inv[l] + j)) : j);
+                acc += eta[l] * __ldcg(src[l] + k);
             }
         }
         y[j] = acc;
@@ -1563,7 +1586,17 @@ bins_partial_kernel(const double* __restrict__ v, const uint8_t* const* __restri
     for (int u = 0; u < NB; ++u) bins[warp][u][lane] = 0.0;
     pdl_wait();
     v = launder(v);
-    for (long long i = b0 + threadIdx.x; i < b1; i += blockDim.x) bins[warp][__ldg(cq + i)][lane] += __ldcg(v + i);
+    long long i = b0 + threadIdx.x;
+    for (; i + 3 * blockDim.x < b1; i += 4 * blockDim.x) {  // four elements' loads in flight
+        const long long s1 = blockDim.x;
+        const uint8_t c0 = __ldg(cq + i), c1 = __ldg(cq + i + s1), c2 = __ldg(cq + i + 2 * s1), c3 = __ldg(cq + i + 3 * s1);
+        const double x0 = __ldcg(v + i), x1 = __ldcg(v + i + s1), x2 = __ldcg(v + i + 2 * s1), x3 = __ldcg(v + i + 3 * s1);
+        bins[warp][c0][lane] += x0;
+        bins[warp][c1][lane] += x1;
+        bins[warp][c2][lane] += x2;
+        bins[warp][c3][lane] += x3;
+    }
+    for (; i < b1; i += blockDim.x) bins[warp][__ldg(cq + i)][lane] += __ldcg(v + i);
     __syncwarp();
     if (lane < NB) {
         double s = 0.0;
@@ -1857,9 +1890,9 @@ void launch_conv(const DWin* wins, const int* slots, int nslots, int Lg_max, lon
 int conv_max_lg() { return kConvMaxL; }
 
 void launch_combine(double* y, const double* const* src, const int* const* inv, const uint8_t* const* inv8,
-                    const double* eta, int P, long long n, cudaStream_t st) {
+                    const int* nu8, const double* eta, int P, long long n, cudaStream_t st) {
     const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 16));
-    launch_k(combine_kernel, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, st, y, src, inv, inv8, eta, P, n);
+    launch_k(combine_kernel, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, st, y, src, inv, inv8, nu8, eta, P, n);
 }
 
 void launch_bin_sums(const double* v, const uint8_t* const* codes, int nwl, long long n, double* partial,
