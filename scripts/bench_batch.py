@@ -2,6 +2,9 @@
 columns through ksvm_nfft_op_apply_batch (device-resident), for 1, 2 and 4
 apply lanes, on a BASELINE config (default 2). One JSON line; the value is
 the 4-lane throughput."""
+import os
+import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import argparse
 import json
 import os

@@ -5,6 +5,9 @@ WindowOperator entries (P:src/pipeline.cpp:159-163). GPU: all windows, device
 time (CUDA events). CPU: the oracle restatement (1 thread) on a bounded
 sample (one window), scaled by the window count. One JSON line.
 """
+import os
+import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import argparse
 import json
 import time

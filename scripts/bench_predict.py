@@ -5,6 +5,9 @@ stood in by the workload's [-1/4, 1/4] scaling), coeff ~ N(0, 1) * 0.01.
 GPU: host wall clock of the synchronous call (plans + cross transforms +
 exact fallback). CPU: the oracle restatement on a bounded sample (one
 window's plan + cross transform), scaled by the window count. One JSON line."""
+import os
+import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import json
 import time
 

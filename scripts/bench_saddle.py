@@ -10,6 +10,9 @@ bounded sample (first 3 GMRES iterations), scaled to the GPU's iteration
 count. Prints one JSON line.
 """
 import argparse
+import os
+import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import json
 import time
 
@@ -26,9 +29,11 @@ ap.add_argument("--rank", type=int, default=50)
 ap.add_argument("--tol", type=float, default=1e-6)
 ap.add_argument("--max-iter", type=int, default=100)
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--n", type=int, default=None)
+ap.add_argument("--no-oracle", action="store_true")
 args = ap.parse_args()
 
-w = workloads.make(args.config)
+w = workloads.make(args.config, args.n)
 n = w.n
 rng = np.random.default_rng(7)
 spec = AnovaKernelSpec(FeatureWindowing.explicit(w.windows))
@@ -55,6 +60,23 @@ for _ in range(args.reps):
     times.append(s.elapsed_time(e))
 gpu_ms = sorted(times)[len(times) // 2]
 
+v1 = torch.from_numpy(w.v).cuda()
+y1 = torch.empty_like(v1)
+for _ in range(3):
+    K.apply_into(v1, y1)
+torch.cuda.synchronize()
+s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+s_.record()
+for _ in range(10):
+    K.apply_into(v1, y1)
+e_.record()
+torch.cuda.synchronize()
+matvec_ms = s_.elapsed_time(e_) / 10
+if args.no_oracle:
+    print(json.dumps({"config": args.config, "n": n, "rank": args.rank, "gmres_iterations": st.iterations,
+                      "solve_ms": gpu_ms, "ms_per_iteration": gpu_ms / max(st.iterations, 1),
+                      "matvec_ms_back_to_back": matvec_ms, "refresh_s": refresh_s}))
+    raise SystemExit(0)
 Ko = oracle.Lib("oracle").anova(w.points, w.windows, fit=1 / 1.2)
 t0 = time.perf_counter()
 _, so = oracle.gmres_solve(Ko, y, theta, Z, rhs, args.tol, 3)
