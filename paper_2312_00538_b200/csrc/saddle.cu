@@ -32,8 +32,27 @@
 namespace ksvm_nfft {
 namespace {
 
-constexpr int kRows = 8;   // basis rows per pass of the multi-dot kernel
+constexpr int kRows = 16;  // basis rows per pass of the multi-dot kernel
 constexpr int kMaxRank = 1024;
+
+// sum_a M[a][i] c[a] for a < rows with four independent accumulators
+// (a mod 4), so eight row loads are in flight per thread; fixed order.
+__device__ __forceinline__ double rows_dot(const double* __restrict__ M, long long ld, int rows, long long i,
+                                          const double* __restrict__ c) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int a = 0;
+#pragma unroll 2
+    for (; a + 4 <= rows; a += 4) {
+        const double m0 = M[static_cast<long long>(a) * ld + i], m1 = M[static_cast<long long>(a + 1) * ld + i];
+        const double m2 = M[static_cast<long long>(a + 2) * ld + i], m3 = M[static_cast<long long>(a + 3) * ld + i];
+        s0 += m0 * c[a];
+        s1 += m1 * c[a + 1];
+        s2 += m2 * c[a + 2];
+        s3 += m3 * c[a + 3];
+    }
+    for (; a < rows; ++a) s0 += M[static_cast<long long>(a) * ld + i] * c[a];
+    return (s0 + s1) + (s2 + s3);
+}
 
 __global__ void __launch_bounds__(kRT) k_mul(double* __restrict__ out, const double* __restrict__ a,
                                              const double* __restrict__ b, long long n,
@@ -150,8 +169,7 @@ __global__ void __launch_bounds__(kRT) k_smw_out(double* __restrict__ out, const
     __syncthreads();
     double acc = 0.0;
     KSVM_FOR_BLOCK_INDEX(j, n) {
-        double s = 0.0;
-        for (int a = 0; a < k; ++a) s += Z[static_cast<long long>(a) * n + j] * s_inner[a];
+        const double s = rows_dot(Z, n, k, j, s_inner);
         const double x1 = g[j] / theta[j] - y[j] * s / theta[j];
         out[j] = x1;
         acc += y[j] * x1;
@@ -185,8 +203,7 @@ __global__ void __launch_bounds__(kRT) k_combine_rows(double* __restrict__ w, co
     pdl_wait();
     if (stop && *stop) return;  // GMRES look-ahead past convergence
     KSVM_FOR_BLOCK_INDEX(i, L) {
-        double s = 0.0;
-        for (int a = 0; a < rows; ++a) s += V[static_cast<long long>(a) * ld + i] * c[a];
+        const double s = rows_dot(V, ld, rows, i, c);
         w[i] = mode == 0 ? w[i] - s : s;
     }
 }
@@ -301,8 +318,7 @@ __global__ void __launch_bounds__(kRT) gk_precond_out(double* __restrict__ z, do
     KSVM_FOR_BLOCK_INDEX(j, n) {
         double x1;
         if (mode == 0) {
-            double s = 0.0;
-            for (int a = 0; a < k; ++a) s += Z[static_cast<long long>(a) * n + j] * s_inner[a];
+            const double s = rows_dot(Z, n, k, j, s_inner);
             x1 = g[j] / theta[j] - y[j] * s / theta[j];
         } else if (mode == 1) {
             x1 = g[j] / theta[j];
@@ -405,9 +421,7 @@ __global__ void __launch_bounds__(kRT) gk_cgs_combine(const double* __restrict__
     if (stop && *stop) return;
     double sq = 0.0;
     KSVM_FOR_BLOCK_INDEX(i, n1) {
-        double s = 0.0;
-        for (int a = 0; a < rows; ++a) s += V[static_cast<long long>(a) * ld + i] * h[a];
-        const double wi = w[i] - s;
+        const double wi = w[i] - rows_dot(V, ld, rows, i, h);
         w[i] = wi;
         sq += wi * wi;
     }
