@@ -175,3 +175,22 @@ def test_pipeline_more_windows_match_oracle_fixtures(fixture):
     f = model.decision_values(w.points[g["te"]])
     assert rel(f, g["f"]) <= 1e-6
     assert (np.where(f >= 0, 1.0, -1.0) == np.where(g["f"] >= 0, 1.0, -1.0)).mean() >= 0.999
+
+
+def test_plain_c_training_example_runs(tmp_path):
+    """examples/c_train_example.c: the training entry points from plain C."""
+    import os
+    import subprocess
+    from paper_2312_00538_b200 import _lib
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "c_train_example"
+    r = subprocess.run(["gcc", "-std=c99", "-O2", "-I", os.path.join(root, "include"),
+                        os.path.join(root, "examples", "c_train_example.c"), "-L", os.path.dirname(_lib.LIB_PATH),
+                        "-lksvm_nfft", "-lm", "-o", str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    env = dict(os.environ, LD_LIBRARY_PATH=os.path.dirname(_lib.LIB_PATH), KSVM_NFFT_QUIET="1")
+    out = subprocess.run([str(exe)], capture_output=True, text=True, env=env, timeout=300)
+    assert out.returncode == 0, out.stderr
+    assert "status 0" in out.stdout and "training accuracy" in out.stdout
+    acc = float(out.stdout.rsplit(" ", 1)[1])
+    assert acc >= 0.9, out.stdout

@@ -143,11 +143,12 @@ def test_window_sharding_gloo_world2(tmp_path):
     assert np.linalg.norm(y - full) <= 1e-13 * np.linalg.norm(full)
 
 
-def test_c_example_compiles_and_links(tmp_path):
+@pytest.mark.parametrize("example", ["c_api_example", "c_train_example"])
+def test_c_example_compiles_and_links(tmp_path, example):
     import subprocess
-    exe = tmp_path / "c_api_example"
+    exe = tmp_path / example
     r = subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
-                        os.path.join(ROOT, "examples", "c_api_example.c"), "-L",
+                        os.path.join(ROOT, "examples", example + ".c"), "-L",
                         os.path.dirname(_lib.LIB_PATH), "-lksvm_nfft", "-lm", "-o", str(exe)],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
