@@ -119,3 +119,23 @@ def test_duplicate_merge_extremes():
         y, yo = g.apply(v), o.apply(v)
         assert np.linalg.norm(y - yo) <= 1e-10 * np.linalg.norm(yo)
         assert all(g.window_points(l) <= 2 for l in range(len(wins)))
+
+
+def test_pinned_host_apply_equals_pageable():
+    """Host applies from pinned buffers (the bench's e2e path) are
+    bit-identical to pageable-host and device applies, across repeated calls
+    and changing inputs."""
+    import torch
+    from paper_2312_00538_b200 import AnovaKernelSpec, Dataset, FeatureWindowing, anova_fast_operator, workloads
+    w = workloads.make(2, 5000)
+    op = anova_fast_operator(Dataset(w.points), AnovaKernelSpec(FeatureWindowing.explicit(w.windows)))
+    vh = torch.empty(w.n, dtype=torch.float64).pin_memory()
+    yh = torch.empty(w.n, dtype=torch.float64).pin_memory()
+    rng = np.random.default_rng(3)
+    for _ in range(3):
+        x = rng.standard_normal(w.n)
+        vh.numpy()[:] = x
+        op.apply(vh.numpy(), out=yh.numpy())
+        ref = op.apply(x.copy())
+        dev = op.apply(torch.from_numpy(x).cuda()).cpu().numpy()
+        assert np.array_equal(yh.numpy(), ref) and np.array_equal(ref, dev)
