@@ -17,6 +17,7 @@ random-pivot Cholesky and random Fourier features are outside this path
 from __future__ import annotations
 
 import ctypes as C
+import os
 import time
 from dataclasses import dataclass, field
 from typing import List, Optional
@@ -150,15 +151,35 @@ def build_precond_factor(op, train: Dataset, spec: AnovaKernelSpec, cfg: Pipelin
     ranks = window_ranks(cfg, P, train.n())
     t0 = time.perf_counter()
     factors = []
-    for l in range(P):
+    if cfg.precond == "nystrom-gaussian":
+        # The sketch draws (the reference's sequential libstdc++ normal stream,
+        # seed + l) dominate on the host; windows are independent, so their
+        # factors are built concurrently (ctypes releases the GIL; each window
+        # has its own operator and stream).
+        from concurrent.futures import ThreadPoolExecutor
+        fops = [fast_window_operator(train.points, w.windows[l], w.length_scales[l], cfg.fastsum, op.device)
+                for l in range(P)]
+        if on_device:
+            import torch
+            torch.cuda.current_stream(torch.device("cuda", op.device)).synchronize()
+
+        def one(l):
+            if on_device:
+                import torch
+                torch.cuda.set_device(op.device)
+            return nystrom(fops[l], ranks[l], "gaussian", int(cfg.seed) + l, on_device=on_device)
+
+        with ThreadPoolExecutor(max_workers=max(1, min(P, os.cpu_count() or 1))) as ex:
+            factors = list(ex.map(one, range(P)))
+        if on_device:
+            import torch
+            torch.cuda.synchronize(op.device)
+    for l in range(P if cfg.precond != "nystrom-gaussian" else 0):
         seed = int(cfg.seed) + l
         if cfg.precond == "cholesky-greedy":
             f = pivoted_cholesky_greedy(op, ranks[l], cfg.cholesky_err_tol, window=l, on_device=on_device)
-        elif cfg.precond == "nystrom-columns":
-            f = nystrom(op, ranks[l], "columns", seed, window=l, on_device=on_device)
         else:
-            fop = fast_window_operator(train.points, w.windows[l], w.length_scales[l], cfg.fastsum, op.device)
-            f = nystrom(fop, ranks[l], "gaussian", seed, on_device=on_device)
+            f = nystrom(op, ranks[l], "columns", seed, window=l, on_device=on_device)
         factors.append(f)
     if on_device:
         import torch
