@@ -12,8 +12,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <memory>
+#include <string>
+#include <thread>
 #include <vector>
 
 #include "capi_common.cuh"
@@ -103,43 +106,73 @@ extern "C" int ksvm_nfft_decision_values(const double* train, int64_t n, int d, 
         std::vector<double> f(static_cast<size_t>(t), 0.0);
         std::vector<char> offending(static_cast<size_t>(t), backend == KSVM_NFFT_PREDICT_EXACT ? 1 : 0);
         if (backend == KSVM_NFFT_PREDICT_FAST) {
-            for (int l = 0; l < P; ++l) {  // P:src/ipm.cpp:247-276
-                const int dl = window_sizes[l];
-                std::vector<double> src(static_cast<size_t>(n) * dl), tgt(static_cast<size_t>(t) * dl);
-                for (int q = 0; q < dl; ++q) {
-                    const int fq = window_features[woff[static_cast<size_t>(l)] + q];
-                    for (int64_t i = 0; i < n; ++i) src[static_cast<size_t>(q * n + i)] = at(train, i, fq, ld_train, layout);
-                    for (int64_t j = 0; j < t; ++j) tgt[static_cast<size_t>(q * t + j)] = at(test, j, fq, ld_test, layout);
-                }
-                ksvm_nfft_plan* plan = nullptr;
-                int rc = ksvm_nfft_plan_create(src.data(), n, dl, n, KSVM_NFFT_COL_MAJOR, length_scales[l], &c,
-                                               1.0 / 1.2, device, &plan);
-                if (rc != KSVM_NFFT_OK) throw std::runtime_error(ksvm_nfft_last_error());
-                std::unique_ptr<ksvm_nfft_plan, void (*)(ksvm_nfft_plan*)> guard(plan, ksvm_nfft_plan_free);
-                std::vector<double> scaled(static_cast<size_t>(t) * dl);
-                if (t > 0) {
-                    rc = ksvm_nfft_plan_scale_points(plan, tgt.data(), t, t, KSVM_NFFT_COL_MAJOR, scaled.data());
-                    if (rc != KSVM_NFFT_OK) throw std::runtime_error(ksvm_nfft_last_error());
-                }
+            // P:src/ipm.cpp:247-276. Windows are independent (own plan, own
+            // stream), so they run on concurrent host threads; their parts are
+            // added to f afterwards in window order (the reference's order).
+            struct WinOut {
                 std::vector<int64_t> ok;
-                for (int64_t j = 0; j < t; ++j) {
-                    double s2 = 0.0;
-                    for (int q = 0; q < dl; ++q) s2 += scaled[static_cast<size_t>(q * t + j)] * scaled[static_cast<size_t>(q * t + j)];
-                    if (std::sqrt(s2) <= c.torus_radius)
-                        ok.push_back(j);
-                    else
-                        offending[static_cast<size_t>(j)] = 1;
+                std::vector<double> part;
+                std::vector<char> off;
+                std::string err;
+            };
+            std::vector<WinOut> outs(static_cast<size_t>(P));
+            auto work = [&](int l) {
+                WinOut& o = outs[static_cast<size_t>(l)];
+                try {
+                    const int dl = window_sizes[l];
+                    std::vector<double> src(static_cast<size_t>(n) * dl), tgt(static_cast<size_t>(t) * dl);
+                    for (int q = 0; q < dl; ++q) {
+                        const int fq = window_features[woff[static_cast<size_t>(l)] + q];
+                        for (int64_t i = 0; i < n; ++i) src[static_cast<size_t>(q * n + i)] = at(train, i, fq, ld_train, layout);
+                        for (int64_t j = 0; j < t; ++j) tgt[static_cast<size_t>(q * t + j)] = at(test, j, fq, ld_test, layout);
+                    }
+                    ksvm_nfft_plan* plan = nullptr;
+                    int rc = ksvm_nfft_plan_create(src.data(), n, dl, n, KSVM_NFFT_COL_MAJOR, length_scales[l], &c,
+                                                   1.0 / 1.2, device, &plan);
+                    if (rc != KSVM_NFFT_OK) throw std::runtime_error(ksvm_nfft_last_error());
+                    std::unique_ptr<ksvm_nfft_plan, void (*)(ksvm_nfft_plan*)> guard(plan, ksvm_nfft_plan_free);
+                    std::vector<double> scaled(static_cast<size_t>(t) * dl);
+                    if (t > 0) {
+                        rc = ksvm_nfft_plan_scale_points(plan, tgt.data(), t, t, KSVM_NFFT_COL_MAJOR, scaled.data());
+                        if (rc != KSVM_NFFT_OK) throw std::runtime_error(ksvm_nfft_last_error());
+                    }
+                    o.off.assign(static_cast<size_t>(t), 0);
+                    for (int64_t j = 0; j < t; ++j) {
+                        double s2 = 0.0;
+                        for (int q = 0; q < dl; ++q) s2 += scaled[static_cast<size_t>(q * t + j)] * scaled[static_cast<size_t>(q * t + j)];
+                        if (std::sqrt(s2) <= c.torus_radius)
+                            o.ok.push_back(j);
+                        else
+                            o.off[static_cast<size_t>(j)] = 1;
+                    }
+                    if (o.ok.empty()) return;
+                    const int64_t m = static_cast<int64_t>(o.ok.size());
+                    std::vector<double> tok(static_cast<size_t>(m) * dl);
+                    o.part.resize(static_cast<size_t>(m));
+                    for (int q = 0; q < dl; ++q)
+                        for (int64_t r = 0; r < m; ++r)
+                            tok[static_cast<size_t>(q * m + r)] = tgt[static_cast<size_t>(q * t + o.ok[static_cast<size_t>(r)])];
+                    rc = ksvm_nfft_plan_apply_cross(plan, tok.data(), m, m, KSVM_NFFT_COL_MAJOR, coeff, o.part.data(),
+                                                    KSVM_NFFT_HOST, nullptr);
+                    if (rc != KSVM_NFFT_OK) throw std::runtime_error(ksvm_nfft_last_error());
+                } catch (const std::exception& e) {
+                    o.err = e.what();
                 }
-                if (ok.empty()) continue;
-                const int64_t m = static_cast<int64_t>(ok.size());
-                std::vector<double> tok(static_cast<size_t>(m) * dl), part(static_cast<size_t>(m));
-                for (int q = 0; q < dl; ++q)
-                    for (int64_t r = 0; r < m; ++r)
-                        tok[static_cast<size_t>(q * m + r)] = tgt[static_cast<size_t>(q * t + ok[static_cast<size_t>(r)])];
-                rc = ksvm_nfft_plan_apply_cross(plan, tok.data(), m, m, KSVM_NFFT_COL_MAJOR, coeff, part.data(),
-                                                KSVM_NFFT_HOST, nullptr);
-                if (rc != KSVM_NFFT_OK) throw std::runtime_error(ksvm_nfft_last_error());
-                for (int64_t r = 0; r < m; ++r) f[static_cast<size_t>(ok[static_cast<size_t>(r)])] += weights[l] * part[static_cast<size_t>(r)];
+            };
+            const int nthr = std::max(1, std::min<int>(P, static_cast<int>(std::thread::hardware_concurrency())));
+            std::atomic<int> next{0};
+            std::vector<std::thread> pool;
+            for (int k = 0; k < nthr; ++k)
+                pool.emplace_back([&] {
+                    for (int l = next++; l < P; l = next++) work(l);
+                });
+            for (auto& th : pool) th.join();
+            for (int l = 0; l < P; ++l) {
+                const WinOut& o = outs[static_cast<size_t>(l)];
+                if (!o.err.empty()) throw std::runtime_error(o.err);
+                for (int64_t j = 0; j < t; ++j)
+                    if (o.off[static_cast<size_t>(j)]) offending[static_cast<size_t>(j)] = 1;
+                for (size_t r = 0; r < o.ok.size(); ++r) f[static_cast<size_t>(o.ok[r])] += weights[l] * o.part[r];
             }
         }
         std::vector<long long> redo;
