@@ -28,8 +28,8 @@
  * ksvm_nfft_op_free                ~AnovaFastOperator
  * ksvm_nfft_saddle_create/         SaddleOperator           P:include/ksvm/saddle.hpp:14-31, P:src/saddle.cpp:7-33
  *   set_theta/apply/free
- * ksvm_nfft_precond_create/        SaddlePreconditioner     P:include/ksvm/saddle.hpp:33-58, P:src/saddle.cpp:35-90
- *   refresh/apply/identity/
+ * ksvm_nfft_precond_create(_ex)/   SaddlePreconditioner     P:include/ksvm/saddle.hpp:33-58, P:src/saddle.cpp:35-90
+ *   refresh/apply/identity/          (_ex: the stacked factor Z already in device memory)
  *   diagonal_fallback/free
  * ksvm_nfft_gmres_solve            gmres_solve              P:include/ksvm/saddle.hpp:60-77, P:src/saddle.cpp:92-178
  * ksvm_nfft_pivoted_cholesky       pivoted_cholesky_greedy  P:include/ksvm/low_rank.hpp, P:src/low_rank.cpp:25-92
