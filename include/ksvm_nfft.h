@@ -26,6 +26,8 @@
  *                                                           P:src/pipeline.cpp:103-105, P:src/low_rank.cpp:49-51
  * ksvm_nfft_kernel_diag            diagonal loop            P:src/low_rank.cpp:33-35
  * ksvm_nfft_op_free                ~AnovaFastOperator
+ * ksvm_nfft_op_create_sharded/     (multi-GPU point sharding: two-phase apply with a grid exchange;
+ *   apply_spread/grids/finish       SURVEY.md 8(e) hybrid, no reference counterpart)
  * ksvm_nfft_saddle_create/         SaddleOperator           P:include/ksvm/saddle.hpp:14-31, P:src/saddle.cpp:7-33
  *   set_theta/apply/free
  * ksvm_nfft_precond_create(_ex)/   SaddlePreconditioner     P:include/ksvm/saddle.hpp:33-58, P:src/saddle.cpp:35-90
@@ -165,6 +167,38 @@ int ksvm_nfft_op_set_stage_timing(ksvm_nfft_op* op, int on);
 int ksvm_nfft_op_last_stage_ms(const ksvm_nfft_op* op, float* ms, int cap);
 const char* ksvm_nfft_op_stage_name(const ksvm_nfft_op* op, int i);
 int ksvm_nfft_op_device(const ksvm_nfft_op* op);
+
+/* ---- point-sharded operator (hybrid sharding) -------------
+ * Multi-GPU decomposition by points instead of windows: every rank creates
+ * the operator from ALL n points (so the affine maps and grids are
+ * identical on every rank) plus the ascending indices of the points it owns.
+ * One matvec is then
+ *   ksvm_nfft_op_apply_spread(op, v)     spread of the owned points' v into
+ *                                        each window's grid G (v: length n;
+ *                                        entries of other ranks' points ignored)
+ *   sum the G buffers over the ranks     (ksvm_nfft_op_grids: device pointers
+ *                                        and lengths, in window order; e.g. one
+ *                                        NCCL all-reduce per window, in place)
+ *   ksvm_nfft_op_apply_finish(op, y)     convolution, gather at the owned
+ *                                        points, window sum; y (length n) holds
+ *                                        the owned points' entries and 0 elsewhere
+ * and a sum (all-reduce) of y over the ranks gives the full product. Spreading
+ * is linear in the points, so the summed grids equal the unsharded operator's
+ * and the result equals it to rounding. Exact duplicate merging is off for
+ * sharded operators; a plain ksvm_nfft_op_apply on one returns the
+ * owned-points block product. ksvm_nfft_op_grids returns the number of grids
+ * (filling at most max_grids entries), or minus the status on error.
+ * Replaces nothing in the reference (its apply is single-process); the
+ * window-sharded alternative is window_mask in ksvm_nfft_op_create. */
+int ksvm_nfft_op_create_sharded(const double* points, int64_t n, int64_t d, int64_t ld, int layout,
+                                const int* window_features, const int* window_sizes, int num_windows,
+                                const double* weights, const double* length_scales,
+                                const ksvm_nfft_config* cfg, double fit_fraction,
+                                const int64_t* own_points, int64_t n_own, int device, int precision,
+                                ksvm_nfft_op** out);
+int ksvm_nfft_op_apply_spread(ksvm_nfft_op* op, const double* v, int ptr_kind, void* stream);
+int ksvm_nfft_op_grids(const ksvm_nfft_op* op, double** grids, int64_t* lengths, int max_grids);
+int ksvm_nfft_op_apply_finish(ksvm_nfft_op* op, double* y, int ptr_kind, void* stream);
 
 /* ---- Newton saddle system, GPU resident ----------------
  * The IPM's inner solve, A [v; w] = [Y K Y v + Theta v - w y; -y^T v] with K

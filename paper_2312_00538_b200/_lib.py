@@ -84,6 +84,12 @@ _SIGS = {
     "ksvm_nfft_op_last_stage_ms": (C.c_int, [_vp, C.POINTER(C.c_float), C.c_int]),
     "ksvm_nfft_op_stage_name": (C.c_char_p, [_vp, C.c_int]),
     "ksvm_nfft_op_free": (None, [_vp]),
+    "ksvm_nfft_op_create_sharded": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int64, C.c_int, _ip, _ip, C.c_int, _dp,
+                                              _dp, C.POINTER(Config), C.c_double, _vp, C.c_int64, C.c_int, C.c_int,
+                                              C.POINTER(_vp)]),
+    "ksvm_nfft_op_apply_spread": (C.c_int, [_vp, _vp, C.c_int, _vp]),
+    "ksvm_nfft_op_grids": (C.c_int, [_vp, _vp, _vp, C.c_int]),
+    "ksvm_nfft_op_apply_finish": (C.c_int, [_vp, _vp, C.c_int, _vp]),
     "ksvm_nfft_op_device": (C.c_int, [_vp]),
     # Newton saddle system
     "ksvm_nfft_saddle_create": (C.c_int, [_vp, _vp, _vp, C.POINTER(_vp)]),

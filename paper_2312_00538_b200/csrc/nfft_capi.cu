@@ -516,6 +516,12 @@ struct Engine {
     int P_owned() const { return static_cast<int>(owned.size()); }
     int64_t n_owned_windows = 1;  // set before planning (item sizing)
     bool data_range = false;      // grid range from the data (self-apply only operators)
+    // Point sharding (SURVEY.md 8(e) hybrid): this operator spreads / gathers
+    // only the points own_idx (ascending global indices) while its grids are
+    // planned from all n points, so every rank's grid is the same and the
+    // partial grids add up (ksvm_nfft_op_apply_spread / _grids / _finish).
+    std::vector<int64_t> own_idx;
+    bool sharded() const { return !own_idx.empty(); }
     bool has_wrap[4] = {false, false, false, false}, has_nowrap[4] = {false, false, false, false};
     int max_tiles[4] = {0, 0, 0, 0};
 
@@ -591,7 +597,23 @@ struct Engine {
         for (int k = 0; k < (d == 1 ? 0 : (d == 2 ? 2 : 4)); ++k) w.T[k].alloc(nodes);
         std::vector<int> inv;
         int64_t nu = 0;
-        if (data_range && dedup_enabled() && find_duplicates(sc, n, d, inv, nu)) {
+        if (sharded()) {
+            w.nu = 0;
+            const int64_t no = static_cast<int64_t>(own_idx.size());
+            std::vector<double> so(static_cast<size_t>(no) * d);
+            for (int t = 0; t < d; ++t)
+                for (int64_t r = 0; r < no; ++r)
+                    so[static_cast<size_t>(t * no + r)] = sc[static_cast<size_t>(t * n + own_idx[static_cast<size_t>(r)])];
+            build_pointset(w.src, so, no, d, g, item_chunk(no * n_owned_windows, d),
+                           gather_chunk(no * n_owned_windows, d), stream);
+            // point-set indices are local to the owned rows: map them to global ones
+            std::vector<int2> cp(static_cast<size_t>(no));
+            CK(cudaMemcpyAsync(cp.data(), w.src.CP.p, sizeof(int2) * cp.size(), cudaMemcpyDeviceToHost, stream));
+            CK(cudaStreamSynchronize(stream));
+            for (auto& e : cp) e.y = static_cast<int>(own_idx[static_cast<size_t>(e.y)]);
+            CK(cudaMemcpyAsync(w.src.CP.p, cp.data(), sizeof(int2) * cp.size(), cudaMemcpyHostToDevice, stream));
+            CK(cudaStreamSynchronize(stream));
+        } else if (data_range && dedup_enabled() && find_duplicates(sc, n, d, inv, nu)) {
             // distinct points (first occurrence order) and the CSR member lists
             std::vector<double> su(static_cast<size_t>(nu) * d);
             std::vector<int> first(static_cast<size_t>(nu), -1);
@@ -754,7 +776,8 @@ struct Engine {
             const std::string gm = ge ? ge : "conv3";
             for (int D = 1; D <= 3; ++D) {
                 const bool conv3 = gm == "conv3" && D == 3;
-                const bool allow = gm == "fused" || ((gm == "fused12" || gm == "conv3") && D < 3) || conv3;
+                bool allow = gm == "fused" || ((gm == "fused12" || gm == "conv3") && D < 3) || conv3;
+                if (sharded()) allow = conv3;  // the node reduction must stay a separate phase
                 bool ok = allow && nslots_cls[D] > 0;
                 int lg = 0, nc = 0;
                 for (int s = 0; s < P && ok; ++s) {
@@ -781,6 +804,8 @@ struct Engine {
             }
         }
         parts.alloc(static_cast<size_t>(std::max(P, 1)) * n);
+        if (sharded())  // gathers write the owned points only; the rest stays 0 for the combine
+            CK(cudaMemsetAsync(parts.p, 0, sizeof(double) * parts.n, stream));
         // exact-duplicate windows: member chunks of <= kSegChunk within one
         // distinct point, global distinct-point numbering in slot order
         std::vector<int> segm, segcb(1, 0);
@@ -891,12 +916,19 @@ struct Engine {
     // One dimension class (all owned windows with d_l = D): spread -> patch
     // reduce -> separable convolution -> (gather). Classes are independent
     // until `combine`, so they run on separate streams (graph branches).
+    // Phases of one class: spread (spread, tile pre-reduction, node reduction
+    // unless fused into the grid kernel), grid (convolution stages), gather.
+    enum : int { kPhSpread = 1, kPhGrid = 2, kPhGather = 4, kPhAll = 7 };
     void run_class(int D, const double* v, cudaStream_t st, bool gather) {
+        run_class_phases(D, v, st, kPhSpread | kPhGrid | (gather ? kPhGather : 0));
+    }
+    void run_class_phases(int D, const double* v, cudaStream_t st, int ph) {
         static const char* kSpread[4] = {"", "spread_d1", "spread_d2", "spread_d3"};
         static const char* kGather[4] = {"", "gather_d1", "gather_d2", "gather_d3"};
         static const char* kConv[3] = {"conv_0", "conv_1", "conv_2"};
         const int cnt = class_end[D] - class_begin[D];
         if (cnt == 0) return;
+        if (ph & kPhSpread) {
         tick(kSpread[D]);
         launch_spread(D, 2 * cfg.window_cutoff, class_PE[D], d_items.p + class_begin[D], cnt, PS(),
                       WINS(), v, PATCHES(),
@@ -912,17 +944,8 @@ struct Engine {
             tick("reduce");
             launch_reduce(WINS(), d_slots.p + slot_begin[D], nslots_cls[D], max_nodes, D, 2 * cfg.window_cutoff,
                           PATCHES(), false, max_tiles[D], st);
-            tick("conv_d3");
-            launch_grid_fused(WINS(), d_slots.p + slot_begin[D], nslots_cls[D], D, grid_nc[D], grid_lg[D],
-                              PATCHES(), st, true);
-            launch_counter() += 2;
-        } else if (grid_fused[D]) {
-            static const char* kGrid[4] = {"", "grid_d1", "grid_d2", "grid_d3"};
-            tick(kGrid[D]);
-            launch_grid_fused(WINS(), d_slots.p + slot_begin[D], nslots_cls[D], D, grid_nc[D], grid_lg[D],
-                              PATCHES(), st, false);
             ++launch_counter();
-        } else {
+        } else if (!grid_fused[D]) {
             tick("reduce");
             for (int wrap = 0; wrap < 2; ++wrap) {
                 if (!(wrap ? has_wrap : has_nowrap)[D]) continue;
@@ -930,13 +953,29 @@ struct Engine {
                               2 * cfg.window_cutoff, PATCHES(), wrap != 0, max_tiles[D], st);
                 ++launch_counter();
             }
+        }
+        }  // spread phase
+        if (ph & kPhGrid) {
+        if (grid_conv_only[D]) {
+            tick("conv_d3");
+            launch_grid_fused(WINS(), d_slots.p + slot_begin[D], nslots_cls[D], D, grid_nc[D], grid_lg[D],
+                              PATCHES(), st, true);
+            ++launch_counter();
+        } else if (grid_fused[D]) {
+            static const char* kGrid[4] = {"", "grid_d1", "grid_d2", "grid_d3"};
+            tick(kGrid[D]);
+            launch_grid_fused(WINS(), d_slots.p + slot_begin[D], nslots_cls[D], D, grid_nc[D], grid_lg[D],
+                              PATCHES(), st, false);
+            ++launch_counter();
+        } else {
             for (int stg = 0; stg < D; ++stg) {
                 tick(kConv[stg]);
                 launch_conv(WINS(), d_slots.p + slot_begin[D], nslots_cls[D], max_lg, max_fibres, stg, st);
                 ++launch_counter();
             }
         }
-        if (gather) {
+        }  // grid phase
+        if (ph & kPhGather) {
             const int gcnt = gclass_end[D] - gclass_begin[D];
             tick(kGather[D]);
             if (gather_columns[D]) {
@@ -990,6 +1029,21 @@ struct Engine {
 
     // grid stage only (cross applies gather over their own targets afterwards)
     void run_grid(const double* v) { run_classes(v, false); }
+
+    // Point-sharded two-phase apply (no duplicate merge on sharded operators):
+    // spread + node reduction into the windows' grids G, then -- after the
+    // caller has summed G over the ranks -- convolution, gather and combine.
+    void run_spread_phase(const double* v) {
+        nticks = 0;
+        for (int D = 3; D >= 1; --D) run_class_phases(D, v, S(), kPhSpread);
+        CK(cudaGetLastError());
+    }
+    void run_finish_phase(double* y) {
+        for (int D = 3; D >= 1; --D) run_class_phases(D, nullptr, S(), kPhGrid | kPhGather);
+        launch_combine(y, SRC(), d_inv.p, d_inv8.p, d_nu8.p, d_eta.p, P_owned(), n, S());
+        ++launch_counter();
+        CK(cudaGetLastError());
+    }
 
     void run_apply(const double* v, double* y) {
         const int P = P_owned();
@@ -1121,6 +1175,7 @@ struct Engine {
         }
         L->patches.alloc(patches.n);
         L->parts.alloc(parts.n);
+        if (sharded()) CK(cudaMemsetAsync(L->parts.p, 0, sizeof(double) * parts.n, stream));
         L->vbuf.alloc(vbuf.n);
         L->ybuf.alloc(ybuf.n);
         if (vs_all.p) L->vs_all.alloc(vs_all.n);
@@ -1244,7 +1299,8 @@ namespace {
 void build_engine(Engine& E, const double* points, int64_t n, int64_t d, int64_t ld, int layout,
                   const int* feats, const int* sizes, int P, const double* weights,
                   const double* ells, const ksvm_nfft_config* cfg, double fit, const int* mask,
-                  int device, int precision, bool data_range) {
+                  int device, int precision, bool data_range, const int64_t* own = nullptr,
+                  int64_t n_own = 0) {
     if (!points || !feats || !sizes || !weights || !ells || !cfg)
         throw std::invalid_argument("null argument");
     validate_cfg(*cfg);
@@ -1280,6 +1336,13 @@ void build_engine(Engine& E, const double* points, int64_t n, int64_t d, int64_t
     E.fit = fit;
     E.data_range = data_range;
     E.n = n;
+    if (own) {  // point shard: owned rows, strictly ascending, in [0, n)
+        if (n_own < 1) throw std::invalid_argument("a point shard needs at least one point");
+        E.own_idx.assign(own, own + n_own);
+        for (int64_t r = 0; r < n_own; ++r)
+            if (own[r] < 0 || own[r] >= n || (r > 0 && own[r] <= own[r - 1]))
+                throw std::invalid_argument("own_points must be strictly ascending indices in [0, n)");
+    }
     E.dfull = d;
     off = 0;
     for (int l = 0; l < P; ++l) {
@@ -1387,6 +1450,58 @@ int ksvm_nfft_op_apply(const ksvm_nfft_op* op, const double* v, double* y, int p
         if (!op || !v || !y) throw std::invalid_argument("null argument");
         Engine& E = const_cast<Engine&>(op->e);
         E.with_io(v, y, ptr_kind, stream, E.n, E.n, [&](const double* dv, double* dy) { E.apply(dv, dy); });
+    });
+}
+
+int ksvm_nfft_op_create_sharded(const double* points, int64_t n, int64_t d, int64_t ld, int layout,
+                                const int* window_features, const int* window_sizes, int num_windows,
+                                const double* weights, const double* length_scales, const ksvm_nfft_config* cfg,
+                                double fit_fraction, const int64_t* own_points, int64_t n_own, int device,
+                                int precision, ksvm_nfft_op** out) {
+    return guarded([&] {
+        if (!out || !own_points) throw std::invalid_argument("null argument");
+        auto op = std::make_unique<ksvm_nfft_op>();
+        build_engine(op->e, points, n, d, ld, layout, window_features, window_sizes, num_windows, weights,
+                     length_scales, cfg, fit_fraction, nullptr, device, precision, true, own_points, n_own);
+        *out = op.release();
+    });
+}
+
+int ksvm_nfft_op_apply_spread(ksvm_nfft_op* op, const double* v, int ptr_kind, void* stream) {
+    return guarded([&] {
+        if (!op || !v) throw std::invalid_argument("null argument");
+        Engine& E = op->e;
+        if (!E.sharded()) throw std::invalid_argument("apply_spread needs a point-sharded operator");
+        E.with_io(v, nullptr, ptr_kind, stream, E.n, 0, [&](const double* dv, double*) { E.run_spread_phase(dv); });
+    });
+}
+
+int ksvm_nfft_op_grids(const ksvm_nfft_op* op, double** grids, int64_t* lengths, int max_grids) {
+    int count = 0;
+    const int rc = guarded([&] {
+        if (!op) throw std::invalid_argument("null argument");
+        const Engine& E = op->e;
+        if (!E.sharded()) throw std::invalid_argument("grids are exposed by point-sharded operators only");
+        for (const auto& w : E.wins) {
+            if (!w->owned) continue;
+            if (count < max_grids && grids && lengths) {
+                long long nodes = 1;
+                for (int t = 0; t < w->d; ++t) nodes *= w->dw.Lg;
+                grids[count] = w->G.p;
+                lengths[count] = nodes;
+            }
+            ++count;
+        }
+    });
+    return rc == KSVM_NFFT_OK ? count : -rc;
+}
+
+int ksvm_nfft_op_apply_finish(ksvm_nfft_op* op, double* y, int ptr_kind, void* stream) {
+    return guarded([&] {
+        if (!op || !y) throw std::invalid_argument("null argument");
+        Engine& E = op->e;
+        if (!E.sharded()) throw std::invalid_argument("apply_finish needs a point-sharded operator");
+        E.with_io(nullptr, y, ptr_kind, stream, 0, E.n, [&](const double*, double* dy) { E.run_finish_phase(dy); });
     });
 }
 

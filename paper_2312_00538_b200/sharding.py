@@ -90,3 +90,118 @@ def numpy_allreduce_via_torch(a: np.ndarray) -> None:
     import torch.distributed as dist
     t = torch.from_numpy(a)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
+
+
+# ---- point sharding (SURVEY.md 8(e) hybrid: balance independent of P) -------
+
+def point_shard(n: int, world: int, rank: int) -> np.ndarray:
+    """Owned rows of `rank`: a contiguous block of the n points (sizes differ
+    by at most one)."""
+    lo = n * rank // world
+    hi = n * (rank + 1) // world
+    return np.arange(lo, hi, dtype=np.int64)
+
+
+class _DevView:
+    """__cuda_array_interface__ view of library-owned device memory (zero copy)."""
+
+    def __init__(self, ptr: int, length: int):
+        self.__cuda_array_interface__ = {"shape": (int(length),), "typestr": "<f8", "data": (int(ptr), False),
+                                          "version": 3}
+
+
+class PointShardedOperator:
+    """One rank's share of a point-sharded ANOVA operator
+    (ksvm_nfft_op_create_sharded): planned from all n points, spreading and
+    gathering only `own_points`. A matvec is
+
+        op.apply_spread(v)                 # owned points -> per-window grids
+        for g in op.grids(): allreduce(g)  # sum the partial grids over ranks
+        op.apply_finish(y)                 # owned rows of y, zeros elsewhere
+        allreduce(y)                       # full y on every rank
+
+    (``matvec(v, y, allreduce)`` does exactly that). v and y are CUDA tensors
+    on the operator's device (torch's current stream) or numpy arrays."""
+
+    def __init__(self, data, spec, own_points, cfg=None, fit_fraction: float = 1.0, device: int = 0):
+        import ctypes as C
+        from . import _lib
+        from .fastsum import FastsumConfig, _host_matrix, _raise
+        cfg = cfg or FastsumConfig()
+        a = _host_matrix(data.points if hasattr(data, "points") else data)
+        n, d = a.shape
+        w = spec.windowing
+        P = w.num_windows()
+        feats = (C.c_int * max(1, sum(len(x) for x in w.windows)))(*[int(f) for x in w.windows for f in x])
+        sizes = (C.c_int * max(1, P))(*[len(x) for x in w.windows])
+        eta = (C.c_double * max(1, P))(*[float(x) for x in w.weights])
+        ell = (C.c_double * max(1, P))(*[float(x) for x in w.length_scales])
+        own = np.ascontiguousarray(np.asarray(own_points, dtype=np.int64))
+        c = cfg._c()
+        h = C.c_void_p()
+        _raise(_lib.load().ksvm_nfft_op_create_sharded(C.c_void_p(a.ctypes.data), n, d, d, _lib.ROW_MAJOR, feats, sizes,
+                                                       P, eta, ell, C.byref(c), float(fit_fraction),
+                                                       C.c_void_p(own.ctypes.data), own.shape[0], int(device),
+                                                       _lib.FP64, C.byref(h)))
+        self._h, self._n, self.device, self.own = h, n, int(device), own
+        self._free = _lib.load().ksvm_nfft_op_free
+
+    def __del__(self):
+        h, free = getattr(self, "_h", None), getattr(self, "_free", None)
+        if h and free is not None:
+            free(h)
+            self._h = None
+
+    def size(self) -> int:
+        return self._n
+
+    def _io(self, x, n):
+        import ctypes as C
+        from . import _lib
+        try:
+            import torch
+            if isinstance(x, torch.Tensor) and x.is_cuda:
+                if x.dtype != torch.float64 or not x.is_contiguous() or x.numel() != n:
+                    raise ValueError("expected a contiguous float64 CUDA tensor of length n")
+                return C.c_void_p(x.data_ptr()), _lib.DEVICE, C.c_void_p(torch.cuda.current_stream(x.device).cuda_stream)
+        except ImportError:
+            pass
+        if not (isinstance(x, np.ndarray) and x.dtype == np.float64 and x.flags.c_contiguous and x.size == n):
+            raise ValueError("expected a contiguous float64 array of length n")
+        return C.c_void_p(x.ctypes.data), _lib.HOST, C.c_void_p(0)
+
+    def apply_spread(self, v) -> None:
+        from . import _lib
+        from .fastsum import _raise
+        p, kind, st = self._io(v, self._n)
+        _raise(_lib.load().ksvm_nfft_op_apply_spread(self._h, p, kind, st))
+
+    def grids(self):
+        """The per-window grids G (CUDA tensor views, window order)."""
+        import ctypes as C
+        import torch
+        from . import _lib
+        cnt = _lib.load().ksvm_nfft_op_grids(self._h, None, None, 0)
+        if cnt < 0:
+            from .fastsum import _raise
+            _raise(-cnt)
+        ptrs = (C.c_void_p * max(cnt, 1))()
+        lens = (C.c_int64 * max(cnt, 1))()
+        _lib.load().ksvm_nfft_op_grids(self._h, ptrs, lens, cnt)
+        dev = torch.device("cuda", self.device)
+        return [torch.as_tensor(_DevView(ptrs[k], lens[k]), device=dev) for k in range(cnt)]
+
+    def apply_finish(self, y) -> None:
+        from . import _lib
+        from .fastsum import _raise
+        p, kind, st = self._io(y, self._n)
+        _raise(_lib.load().ksvm_nfft_op_apply_finish(self._h, p, kind, st))
+
+    def matvec(self, v, y, allreduce: Callable = None) -> None:
+        self.apply_spread(v)
+        if allreduce is not None:
+            for g in self.grids():
+                allreduce(g)
+        self.apply_finish(y)
+        if allreduce is not None:
+            allreduce(y)

@@ -164,3 +164,12 @@ def test_window_costs_count_distinct_points():
     owner = sharding.lpt_assign(costs, 4)
     assert sorted(owner[:4]) == [0, 1, 2, 3]  # one heavy window per rank
     assert sharding.window_costs(w.windows) == [1024] * 18
+
+
+def test_point_shard_partition():
+    for n, world in ((10, 3), (60000, 8), (5, 5), (7, 1)):
+        parts = [sharding.point_shard(n, world, r) for r in range(world)]
+        cat = np.concatenate(parts)
+        assert np.array_equal(cat, np.arange(n))
+        sizes = [len(p) for p in parts]
+        assert max(sizes) - min(sizes) <= 1
