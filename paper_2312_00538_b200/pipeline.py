@@ -157,17 +157,16 @@ def build_precond_factor(op, train: Dataset, spec: AnovaKernelSpec, cfg: Pipelin
         # factors are built concurrently (ctypes releases the GIL; each window
         # has its own operator and stream).
         from concurrent.futures import ThreadPoolExecutor
-        fops = [fast_window_operator(train.points, w.windows[l], w.length_scales[l], cfg.fastsum, op.device)
-                for l in range(P)]
         if on_device:
             import torch
             torch.cuda.current_stream(torch.device("cuda", op.device)).synchronize()
 
-        def one(l):
+        def one(l):  # the window's FastWindowOperator (its own plan) and its sketch
             if on_device:
                 import torch
                 torch.cuda.set_device(op.device)
-            return nystrom(fops[l], ranks[l], "gaussian", int(cfg.seed) + l, on_device=on_device)
+            fop = fast_window_operator(train.points, w.windows[l], w.length_scales[l], cfg.fastsum, op.device)
+            return nystrom(fop, ranks[l], "gaussian", int(cfg.seed) + l, on_device=on_device)
 
         with ThreadPoolExecutor(max_workers=max(1, min(P, os.cpu_count() or 1))) as ex:
             factors = list(ex.map(one, range(P)))
