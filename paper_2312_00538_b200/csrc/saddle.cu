@@ -269,6 +269,133 @@ __global__ void k_cap_finish(const double* __restrict__ partial, int nchunks, in
     C[idx] = (a == b ? 1.0 : 0.0) + s;
 }
 
+// Capacitance inverse on the device (one CTA, deterministic): Gauss-Jordan
+// with partial pivoting (pivot = first row of largest |a|, as getrf / Eigen's
+// PartialPivLU choose it) on [C | I] (k x 2k, row-major, in global memory /
+// L2), plus the reference's guards (P:src/saddle.cpp:55-60): a non-finite
+// capacitance, a zero pivot or rcond = 1 / (|C|_1 |C^-1|_1) < 1e-15 set
+// *flag (the diagonal fallback); otherwise Cinv receives C^-1.
+__device__ __forceinline__ double block_max_1024(double v, double* sh) {
+    for (int o = 16; o >= 1; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double m = sh[0];
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) m = fmax(m, sh[w]);
+    __syncthreads();
+    return m;
+}
+
+__global__ void __launch_bounds__(1024) k_cap_invert(double* __restrict__ A, const double* __restrict__ C, int k,
+                                                      double* __restrict__ Cinv, int* __restrict__ flag) {
+    extern __shared__ double s_f[];  // k multipliers of the current column
+    __shared__ double sh[32];
+    __shared__ int s_piv;
+    __shared__ double s_pval;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int w2 = 2 * k;
+    int bad = 0;
+    for (int e = tid; e < k * w2; e += nt) {
+        const int r = e / w2, j = e - r * w2;
+        const double v = j < k ? C[r * k + j] : (j - k == r ? 1.0 : 0.0);
+        if (!isfinite(v)) bad = 1;
+        A[e] = v;
+    }
+    double cs = 0.0;  // |C|_1: column abs sums
+    for (int j = tid; j < k; j += nt) {
+        double s = 0.0;
+        for (int r = 0; r < k; ++r) s += fabs(C[r * k + j]);
+        cs = fmax(cs, s);
+    }
+    bad = __syncthreads_or(bad);
+    if (bad) {
+        if (tid == 0) *flag = 1;
+        return;
+    }
+    const double anorm = block_max_1024(cs, sh);
+    for (int c = 0; c < k; ++c) {
+        // pivot: first row r >= c with the largest |A[r][c]|
+        double best = -1.0;
+        int bi = k;
+#pragma unroll 4
+        for (int r = c + tid; r < k; r += nt) {
+            const double a = fabs(A[r * w2 + c]);
+            if (a > best) {
+                best = a;
+                bi = r;
+            }
+        }
+        for (int o = 16; o >= 1; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ob > best || (ob == best && oi < bi)) {
+                best = ob;
+                bi = oi;
+            }
+        }
+        if ((tid & 31) == 0) {
+            sh[tid >> 5] = best;
+            reinterpret_cast<int*>(s_f)[tid >> 5] = bi;  // scratch before s_f is used this step
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double b = sh[0];
+            int p = reinterpret_cast<int*>(s_f)[0];
+            for (int w = 1; w < nt / 32; ++w) {
+                const double ob = sh[w];
+                const int oi = reinterpret_cast<int*>(s_f)[w];
+                if (ob > b || (ob == b && oi < p)) {
+                    b = ob;
+                    p = oi;
+                }
+            }
+            s_piv = p;
+            s_pval = p < k ? A[p * w2 + c] : 0.0;
+        }
+        __syncthreads();
+        const int p = s_piv;
+        const double pv = s_pval;
+        if (pv == 0.0) {  // singular (P:src/saddle.cpp:59-60 via rcond)
+            if (tid == 0) *flag = 1;
+            return;
+        }
+        if (p != c)
+            for (int j = tid; j < w2; j += nt) {
+                const double t = A[c * w2 + j];
+                A[c * w2 + j] = A[p * w2 + j];
+                A[p * w2 + j] = t;
+            }
+        __syncthreads();
+        for (int j = tid; j < w2; j += nt) A[c * w2 + j] /= pv;
+        for (int r = tid; r < k; r += nt) s_f[r] = r == c ? 0.0 : A[r * w2 + c];
+        __syncthreads();
+        // row c of the right block and of columns >= c are reread by every row:
+        // stage them in registers per thread column j (fixed j per thread when
+        // nt is a multiple of w2 is not guaranteed, so read through L1)
+#pragma unroll 8
+        for (int e = tid; e < k * w2; e += nt) {
+            const int r = e / w2, j = e - r * w2;
+            if (r != c && j >= c) A[e] -= s_f[r] * __ldcg(A + c * w2 + j);
+        }
+        __syncthreads();
+    }
+    double is = 0.0;  // |C^-1|_1
+    for (int j = tid; j < k; j += nt) {
+        double s = 0.0;
+        for (int r = 0; r < k; ++r) s += fabs(A[r * w2 + k + j]);
+        is = fmax(is, s);
+    }
+    const double inorm = block_max_1024(is, sh);
+    const double rcond = 1.0 / (anorm * inorm);
+    if (!isfinite(rcond) || rcond < 1e-15) {
+        if (tid == 0) *flag = 1;
+        return;
+    }
+    for (int e = tid; e < k * k; e += nt) {
+        const int r = e / k, j = e - r * k;
+        Cinv[e] = A[r * w2 + k + j];
+    }
+}
+
 // ---- fused GMRES-iteration kernels ----------------------------------------
 // The iteration's vector work, fused where the pieces share a block's index
 // set (no grid-wide dependency between them): the preconditioner output also
@@ -658,67 +785,20 @@ void precond_refresh(ksvm_nfft_precond& P, const double* theta_in, bool device, 
     launch_k(k_cap_finish, dim3((k * k + 255) / 256), dim3(256), 0, st, part.p, nchunks, nt, k, C.p);
     launch_counter() += 2;
     CK(cudaGetLastError());
-    std::vector<double> cap(static_cast<size_t>(k) * k);
-    CK(cudaMemcpyAsync(cap.data(), C.p, sizeof(double) * cap.size(), cudaMemcpyDeviceToHost, st));
+    // inverse on the device: Gauss-Jordan with the reference's pivot rule and guards
+    DevBuf<double> aug;
+    DevBuf<int> flag;
+    aug.alloc(static_cast<size_t>(k) * 2 * k);
+    flag.alloc(1);
+    if (P.Cinv.n < static_cast<size_t>(k) * k) P.Cinv.alloc(static_cast<size_t>(k) * k);
+    CK(cudaMemsetAsync(flag.p, 0, sizeof(int), st));
+    k_cap_invert<<<1, 1024, sizeof(double) * std::max(k, 32), st>>>(aug.p, C.p, k, P.Cinv.p, flag.p);
+    ++launch_counter();
+    CK(cudaGetLastError());
+    int hflag = 0;
+    CK(cudaMemcpyAsync(&hflag, flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    for (double c : cap)
-        if (!std::isfinite(c)) {  // P:src/saddle.cpp:55-58
-            P.fallback = true;
-            return;
-        }
-    double anorm = 0.0;
-    for (int b = 0; b < k; ++b) {
-        double s = 0.0;
-        for (int a = 0; a < k; ++a) s += std::fabs(cap[static_cast<size_t>(a) * k + b]);
-        anorm = std::max(anorm, s);
-    }
-    std::vector<double> lu = cap;
-    std::vector<int> piv(static_cast<size_t>(k));
-    for (int c = 0; c < k; ++c) {
-        int p = c;
-        for (int r = c + 1; r < k; ++r)
-            if (std::fabs(lu[static_cast<size_t>(r) * k + c]) > std::fabs(lu[static_cast<size_t>(p) * k + c])) p = r;
-        piv[static_cast<size_t>(c)] = p;
-        if (p != c)
-            for (int q = 0; q < k; ++q) std::swap(lu[static_cast<size_t>(c) * k + q], lu[static_cast<size_t>(p) * k + q]);
-        const double d = lu[static_cast<size_t>(c) * k + c];
-        if (d == 0.0) {
-            P.fallback = true;
-            return;
-        }
-        for (int r = c + 1; r < k; ++r) {
-            const double f = lu[static_cast<size_t>(r) * k + c] / d;
-            lu[static_cast<size_t>(r) * k + c] = f;
-            for (int q = c + 1; q < k; ++q) lu[static_cast<size_t>(r) * k + q] -= f * lu[static_cast<size_t>(c) * k + q];
-        }
-    }
-    std::vector<double> inv(static_cast<size_t>(k) * k);
-    double inorm = 0.0;
-    std::vector<double> e(static_cast<size_t>(k));
-    for (int b = 0; b < k; ++b) {  // column b of the inverse
-        std::fill(e.begin(), e.end(), 0.0);
-        e[static_cast<size_t>(b)] = 1.0;
-        for (int c = 0; c < k; ++c) std::swap(e[static_cast<size_t>(c)], e[static_cast<size_t>(piv[static_cast<size_t>(c)])]);
-        for (int r = 0; r < k; ++r)
-            for (int c = 0; c < r; ++c) e[static_cast<size_t>(r)] -= lu[static_cast<size_t>(r) * k + c] * e[static_cast<size_t>(c)];
-        for (int r = k - 1; r >= 0; --r) {
-            for (int c = r + 1; c < k; ++c) e[static_cast<size_t>(r)] -= lu[static_cast<size_t>(r) * k + c] * e[static_cast<size_t>(c)];
-            e[static_cast<size_t>(r)] /= lu[static_cast<size_t>(r) * k + r];
-        }
-        double s = 0.0;
-        for (int a = 0; a < k; ++a) {
-            inv[static_cast<size_t>(a) * k + b] = e[static_cast<size_t>(a)];
-            s += std::fabs(e[static_cast<size_t>(a)]);
-        }
-        inorm = std::max(inorm, s);
-    }
-    const double rcond = 1.0 / (anorm * inorm);
-    if (!std::isfinite(rcond) || rcond < 1e-15) {  // P:src/saddle.cpp:59-60
-        P.fallback = true;
-        return;
-    }
-    P.Cinv.upload(inv.data(), inv.size(), st);
-    CK(cudaStreamSynchronize(st));
+    if (hflag) P.fallback = true;  // P:src/saddle.cpp:55-60
 }
 
 cudaStream_t pick_stream(int ptr_kind, void* stream, cudaStream_t own) {
