@@ -13,9 +13,10 @@
 //    with one re-orthogonalisation pass; H(:,k) = h1 + h2 in both, and the
 //    Arnoldi relation is the same;
 //  * the capacitance I + Z Theta^{-1} Z^T is formed on the FP64 tensor cores
-//    and inverted explicitly after a partial-pivot LU on the host (the
-//    reference keeps the LU, P:src/saddle.cpp:57); the rcond < 1e-15
-//    fallback (:59-60) uses the exact 1-norm condition number.
+//    and inverted explicitly on the device by Gauss-Jordan with the same
+//    partial-pivoting rule (the reference keeps the LU, P:src/saddle.cpp:57);
+//    the rcond < 1e-15 fallback (:59-60) uses the exact 1-norm condition
+//    number.
 #include <cuda_runtime.h>
 
 #include <algorithm>
