@@ -173,3 +173,40 @@ def test_point_shard_partition():
         assert np.array_equal(cat, np.arange(n))
         sizes = [len(p) for p in parts]
         assert max(sizes) - min(sizes) <= 1
+
+
+def test_pdl_prewait_loads_read_plan_data_only(tmp_path):
+    """Every read-only (ld.global.nc) load ptxas schedules before a kernel's
+    griddepcontrol.wait must read plan data (items, point-set and window
+    tables, point factors); data written earlier in the stream is read with
+    coherent loads after the wait (PDL and read-only loads)."""
+    import shutil
+    import subprocess
+    import sys
+    if not (shutil.which("cuobjdump") and shutil.which("nvdisasm")):
+        pytest.skip("CUDA binary tools absent")
+    sys.path.insert(0, os.path.join(ROOT, "scripts"))
+    from sass_pdl_lines import prewait_loads, src_line
+    allowed = ("items[", "psets[", "wins[", "wn.", "colb", "multi[", "= src[l]", "= inv[l]",
+               "= inv8[l]", "= eta[l]", "codes[q]", "tile_coords", "nown", "conv_tiles", "nfib")
+    # inlined __ldg calls are attributed to the intrinsics header, so the
+    # source must also never read predecessor data through __ldg
+    src = open(os.path.join(ROOT, "paper_2312_00538_b200", "csrc", "nfft_kernels.cu")).read()
+    for bad in ("__ldg(v +", "__ldg(wn.H", "__ldg(Hg", "__ldg(src +", "__ldg(s_src", "__ldg(patches",
+                "__ldg(partial", "__ldg(base"):
+        assert bad not in src, bad
+    objdir = os.path.join(ROOT, "paper_2312_00538_b200", "csrc", "build")
+    checked = 0
+    for obj in ("nfft_kernels.o", "grid_fused.o", "saddle.o", "ipm.o", "lowrank.o"):
+        path = os.path.join(objdir, obj)
+        if not os.path.exists(path):
+            pytest.skip("objects not built")
+        subprocess.run(["cuobjdump", "-xelf", "all", path], cwd=tmp_path, capture_output=True, check=True)
+        for cubin in tmp_path.glob(obj.replace(".o", "") + "*.cubin"):
+            for kernel, pre in prewait_loads(str(cubin)).items():
+                for (f, ln) in pre:
+                    text = src_line(f, ln)
+                    assert f.endswith("sm_32_intrinsics.hpp") or any(a in text for a in allowed), \
+                        f"{kernel}: pre-wait read-only load at {f}:{ln}: {text}"
+                    checked += 1
+    assert checked > 0
