@@ -17,6 +17,10 @@ on the launching stream, with a 256 MiB L2 flush (untimed) before every step
 because config 2's inputs fit in the 126 MB L2; barrier + synchronize on both
 sides; max over ranks. nvidia-smi samples clocks during the timed region.
 
+On one GPU the line also carries "training": north_star's end-to-end IPM
+training on BASELINE config 1 through train_pipeline (wall clock and the
+Newton/GMRES trajectory; informational, not the metric).
+
 --impl reference times the reference's own CPU fastsum (oracle/_ref, the
 reference's fastsum.cpp compiled unmodified by path; the oracle restatement
 if that library is absent) with every host thread on the same workload.
@@ -261,6 +265,26 @@ def fp64_peak_tflops(dev):
     return 2 * 8192 ** 3 / (best * 1e-3) / 1e12
 
 
+def training_line():
+    """north_star's end-to-end IPM training on BASELINE config 1 (split,
+    z-score, rank-50 greedy Cholesky, IPM with C = 1, bias) through
+    train_pipeline, wall clock, plus the trajectory the GPU tests compare with
+    the oracle's (tests/test_gpu_ipm.py). Informational: not the metric."""
+    try:
+        from paper_2312_00538_b200 import Dataset, IpmConfig, PipelineConfig, train_pipeline, workloads
+        w1 = workloads.config1()
+        pc = PipelineConfig(explicit_windows=w1.windows, rank=50, ipm=IpmConfig(C=1.0))
+        train_pipeline(Dataset(w1.points[:400], w1.labels[:400]), pc)  # warm-up
+        t0 = time.perf_counter()
+        model, test, rep, res = train_pipeline(Dataset(w1.points, w1.labels), pc)
+        secs = time.perf_counter() - t0
+        return {"workload": "cfg1 n=2000 d=6 windows(3,3) IPM C=1, greedy Cholesky rank 50", "seconds": secs,
+                "status": rep.status.name, "newton_steps": rep.ipm_iters,
+                "gmres_per_step": [i.gmres.iterations for i in res.iterations], "n_train": rep.n_train}
+    except Exception as e:  # never let the informational leg break the bench line
+        return {"error": str(e)[:200]}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -402,6 +426,8 @@ def run_ours(args):
                         "d2h_bytes_per_step": 8 * w.n}}
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(w, args.cpu_budget_s)
+        if world == 1:
+            line["training"] = training_line()
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
