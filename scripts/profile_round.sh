@@ -22,3 +22,11 @@ python scripts/ncu_summary.py gpurun_out/prof_cfg2.ncu-rep > gpurun_out/ncu_cfg2
 python scripts/ncu_summary.py gpurun_out/prof_cfg4.ncu-rep > gpurun_out/ncu_cfg4_full.txt
 python scripts/launch_table.py gpurun_out/launches_cfg2.csv > gpurun_out/launches_cfg2.txt
 tail -1 gpurun_out/ncu_full2.log gpurun_out/ncu_full4.log
+# end-to-end training and the callers of the matvec
+python scripts/bench_ipm.py --config 1 --oracle > gpurun_out/ipm1.json 2>/dev/null
+python scripts/bench_ipm.py --config 3 > gpurun_out/ipm3.json 2>/dev/null
+python scripts/bench_ipm.py --config 5 > gpurun_out/ipm5.json 2>/dev/null
+python scripts/bench_saddle.py > gpurun_out/saddle2.json 2>/dev/null
+python scripts/bench_lowrank.py > gpurun_out/lowrank3.json 2>/dev/null
+python scripts/bench_predict.py > gpurun_out/predict3.json 2>/dev/null
+python scripts/bench_batch.py > gpurun_out/batch2.json 2>/dev/null
