@@ -20,13 +20,13 @@ import ctypes as C
 import os
 import time
 from dataclasses import dataclass, field
-from typing import List, Optional
+from typing import List
 
 import numpy as np
 
 from . import _lib
 from .fastsum import (AnovaKernelSpec, Dataset, FastsumConfig, FeatureWindowing, _raise, anova_fast_operator)
-from .ipm import FeatureStats, IpmConfig, IpmResult, IpmStatus, TrainedModel, ipm_train, make_model
+from .ipm import FeatureStats, IpmConfig, IpmStatus, ipm_train, make_model
 from .lowrank import fast_window_operator, nystrom, pivoted_cholesky_greedy, stack_anova_factors
 
 PRECOND_METHODS = ("none", "cholesky-greedy", "nystrom-columns", "nystrom-gaussian")  # P:src/pipeline.cpp:8-18

@@ -4,7 +4,6 @@ import os
 import sys
 import time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np  # noqa: E402
 from paper_2312_00538_b200 import (Dataset, balance_and_split, fast_window_operator, nystrom, workloads,  # noqa: E402
                                    zscore_fit_transform)
 
