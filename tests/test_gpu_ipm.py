@@ -40,16 +40,16 @@ def dual(alpha, y, Ko):
     return alpha.sum() - 0.5 * ya @ Ko.apply(ya)
 
 
-def check_same_run(res, alpha_o, r_o, log_o, y, Ko, alpha_tol=1e-6):
+def check_same_run(res, alpha_o, r_o, log_o, y, Ko, alpha_tol=1e-6, lam_tol=1e-6, dual_tol=1e-9):
     assert res.status.name.lower() == r_o["status"]
     assert len(res.iterations) == r_o["iterations"]
     assert [it.gmres.iterations for it in res.iterations] == [int(x) for x in log_o[:, 4]]
     assert np.allclose([it.mu for it in res.iterations], log_o[:, 0], rtol=1e-14)
     assert rel(res.alpha, alpha_o) <= alpha_tol
-    assert abs(res.lambda_ - r_o["lambda"]) <= 1e-6 * max(1.0, abs(r_o["lambda"]))
+    assert abs(res.lambda_ - r_o["lambda"]) <= lam_tol * max(1.0, abs(r_o["lambda"]))
     assert abs(res.xi_lambda_rel - r_o["xi_lambda_rel"]) <= 1e-5 * max(r_o["xi_lambda_rel"], 1e-3)
     d_gpu, d_o = dual(res.alpha, y, Ko), dual(alpha_o, y, Ko)
-    assert abs(d_gpu - d_o) <= 1e-9 * abs(d_o)
+    assert abs(d_gpu - d_o) <= dual_tol * abs(d_o)
 
 
 @pytest.mark.parametrize("n,seed", [(200, 11), (600, 23)])
@@ -194,3 +194,34 @@ def test_plain_c_training_example_runs(tmp_path):
     assert "status 0" in out.stdout and "training accuracy" in out.stdout
     acc = float(out.stdout.rsplit(" ", 1)[1])
     assert acc >= 0.9, out.stdout
+
+
+@pytest.mark.parametrize("C_,n,seed", [(0.05, 150, 41), (10.0, 150, 43), (1.0, 4, 47)])
+def test_ipm_edge_cases_match_oracle(C_, n, seed):
+    """Tight / loose box constraints and a 4-point problem (P:tests/test_ipm.cpp
+    exercises C and tiny n through the same loop)."""
+    pts, y = oracle.blobs(n, 2, 2.0, seed)
+    K, Ko = ops(pts, [[0, 1]])
+    res = ipm_train(K, y, None, IpmConfig(C=C_))
+    alpha_o, r_o, log_o = oracle.ipm_train(Ko, y, C=C_)
+    # with C = 10 the unpreconditioned GMRES hits its 100-iteration cap
+    # (residual 2e-3) at the last Newton steps: the truncated iterate carries
+    # rounding-level differences amplified by the ill-conditioning (alpha and
+    # lambda 1e-5, dual objective 1e-7)
+    check_same_run(res, alpha_o, r_o, log_o, y, Ko, alpha_tol=1e-5, lam_tol=1e-5, dual_tol=1e-7)
+    assert res.alpha.min() > 0.0 and res.alpha.max() < C_
+
+
+def test_ipm_device_factor_equals_host_factor():
+    """The stacked factor passed as a CUDA tensor (kept in HBM) gives the same
+    run as the host array."""
+    pts, y = oracle.blobs(500, 3, 2.0, 53)
+    windows = [[0, 1], [2]]
+    K, _ = ops(pts, windows)
+    from paper_2312_00538_b200 import pivoted_cholesky_greedy
+    fs = [pivoted_cholesky_greedy(K, 15, 1e-5, window=l) for l in range(2)]
+    Z = np.vstack([np.sqrt(0.5) * f.Z for f in fs])
+    a = ipm_train(K, y, Z, IpmConfig(C=1.0))
+    import torch
+    b = ipm_train(K, y, torch.from_numpy(Z).cuda(), IpmConfig(C=1.0))
+    assert np.array_equal(a.alpha, b.alpha) and a.lambda_ == b.lambda_
