@@ -17,10 +17,12 @@
 //    partial-pivoting rule (the reference keeps the LU, P:src/saddle.cpp:57);
 //    the rcond < 1e-15 fallback (:59-60) uses the exact 1-norm condition
 //    number.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -231,6 +233,117 @@ __global__ void __launch_bounds__(kRT) k_sq_diff(const double* __restrict__ a, c
     block_partial(acc, partial);
 }
 
+// Capacitance partials, SMEM-staged (k <= kGramMaxK): CTA x owns a fixed
+// column range and stages 32-column slices of Z (all k rows, one HBM read of
+// Z per refresh) in shared memory; each warp owns a contiguous run of the
+// upper-triangle 8x8 tiles (ta <= tb; C is symmetric) and accumulates them in
+// registers with DMMA.8x8x4 over the whole range. Slices arrive by cp.async
+// into two SMEM buffers (the next one in flight during the current MMAs). partial[x][tile][64], tile
+// in row-major upper-triangle order; k_cap_finish_sym sums x in order.
+constexpr int kGramWarps = 16, kGramTiles = 24, kGramCols = 32, kGramLd = 36;
+constexpr int kGramMaxK = 256;
+constexpr int kGramCTAs = 148;                                     // one per B200 SM
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool valid) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 8 : 0) : "memory");
+}
+
+__global__ void __launch_bounds__(kGramWarps * 32, 1)
+    k_cap_gram(const double* __restrict__ Z, const double* __restrict__ theta, int k, long long n, int nt, int T,
+               long long cols, double* __restrict__ partial) {
+    extern __shared__ double s_z[];  // 2 buffers: nt*8 rows x kGramLd, then kGramCols theta values
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+    const int rows = nt * 8, nthr = kGramWarps * 32, bufsz = rows * kGramLd + kGramCols;
+    const long long jb = blockIdx.x * cols, je = min(n, jb + cols);
+    // this warp's tiles [L0, L1) of the T upper-triangle tiles
+    const int L0 = warp * T / kGramWarps, L1 = (warp + 1) * T / kGramWarps, cnt = L1 - L0;
+    int ta0 = 0, rs = 0;
+    while (ta0 < nt && rs + (nt - ta0) <= L0) {
+        rs += nt - ta0;
+        ++ta0;
+    }
+    const int tb0 = ta0 + (L0 - rs);
+    double acc[kGramTiles][2];
+#pragma unroll
+    for (int i = 0; i < kGramTiles; ++i) acc[i][0] = acc[i][1] = 0.0;
+    auto issue = [&](long long j0, double* buf) {  // slice [j0, j0 + 32) -> buf (zero-filled outside)
+        for (int e = tid; e < rows * kGramCols; e += nthr) {
+            const int r = e >> 5, c = e & 31;
+            const long long j = j0 + c;
+            const bool ok = r < k && j < je;
+            cp_async8(buf + r * kGramLd + c, ok ? Z + static_cast<long long>(r) * n + j : Z, ok);
+        }
+        if (tid < kGramCols) {
+            const bool ok = j0 + tid < je;
+            cp_async8(buf + rows * kGramLd + tid, ok ? theta + j0 + tid : theta, ok);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    if (jb < je) issue(jb, s_z);
+    int it = 0;
+    for (long long j0 = jb; j0 < je; j0 += kGramCols, ++it) {
+        const double* cur = s_z + (it & 1) * bufsz;
+        if (j0 + kGramCols < je)
+            issue(j0 + kGramCols, s_z + ((it + 1) & 1) * bufsz);  // in flight during the MMAs
+        else
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        __syncthreads();  // slice `it` landed for every thread
+        if (cnt > 0) {
+#pragma unroll 2
+            for (int kk = 0; kk < kGramCols / 4; ++kk) {
+                const int col = kk * 4 + t;
+                const double th = cur[rows * kGramLd + col];
+                const double sc = th != 0.0 ? 1.0 / th : 0.0;  // zero-filled columns past the range
+                int ta = ta0, tb = tb0;
+                double a = cur[(ta * 8 + g) * kGramLd + col] * sc;
+#pragma unroll
+                for (int i = 0; i < kGramTiles; ++i)
+                    if (i < cnt) {
+                        const double b = cur[(tb * 8 + g) * kGramLd + col];
+                        asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                            : "+d"(acc[i][0]), "+d"(acc[i][1])
+                            : "d"(a), "d"(b));
+                        if (++tb == nt) {
+                            ++ta;
+                            tb = ta;
+                            if (ta < nt) a = cur[(ta * 8 + g) * kGramLd + col] * sc;
+                        }
+                    }
+            }
+        }
+        __syncthreads();  // slice consumed before its buffer is refilled
+    }
+    double* out = partial + static_cast<long long>(blockIdx.x) * T * 64;
+#pragma unroll
+    for (int i = 0; i < kGramTiles; ++i)
+        if (i < cnt) {
+            out[static_cast<long long>(L0 + i) * 64 + g * 8 + 2 * t] = acc[i][0];
+            out[static_cast<long long>(L0 + i) * 64 + g * 8 + 2 * t + 1] = acc[i][1];
+        }
+}
+
+// C[a][b] = (a == b) + sum over column ranges (in order) of the symmetric tile
+__global__ void k_cap_finish_sym(const double* __restrict__ partial, int nparts, int nt, int T, int k,
+                                 double* __restrict__ C) {
+    pdl_trigger();
+    pdl_wait();
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= k * k) return;
+    int a = idx / k, b = idx % k;
+    if ((a >> 3) > (b >> 3)) {
+        const int s = a;
+        a = b;
+        b = s;
+    }
+    const int ta = a >> 3, tb = b >> 3;
+    const int tile = ta * nt - ta * (ta - 1) / 2 + (tb - ta), e = (a & 7) * 8 + (b & 7);
+    double s = 0.0;
+    for (int c = 0; c < nparts; ++c) s += partial[(static_cast<long long>(c) * T + tile) * 64 + e];
+    C[idx] = (idx / k == idx % k ? 1.0 : 0.0) + s;
+}
+
 // Capacitance partials on the FP64 tensor cores: warp (ta, tb, chunk) forms
 // the 8x8 tile sum_{j in chunk} (Z[a][j] / theta_j) Z[b][j] with DMMA.8x8x4
 // (P:src/saddle.cpp:52-54 computes Z * Theta^{-1} * Z^T).
@@ -395,6 +508,193 @@ __global__ void __launch_bounds__(1024) k_cap_invert(double* __restrict__ A, con
         const int r = e / k, j = e - r * k;
         Cinv[e] = A[r * w2 + k + j];
     }
+}
+
+// The same inverse with [C | I] resident in the shared memory of a cluster of
+// kCapCTAs CTAs (CTA q holds rows [q R, q R + R), R = ceil(k / kCapCTAs)):
+// Gauss-Jordan with implicit partial pivoting (no row swaps: the pivot of
+// column c is the unused row of largest |a|, lowest row on ties, found from
+// one candidate per CTA over DSMEM; every CTA reads the pivot row from its
+// owner and eliminates its own rows in SMEM). Row p_c ends as [e_c | row c of
+// C^-1]. Two cluster barriers per column instead of the one-CTA kernel's
+// passes over an L2-resident k x 2k matrix. All CTAs take the same decisions
+// from the same data, so the guards (non-finite C, zero pivot, rcond) exit
+// uniformly through the final barrier.
+constexpr int kCapCTAs = 8, kCapThreads = 512;
+
+__device__ __forceinline__ void cap_cluster_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+size_t cap_cluster_smem(int k) {
+    const size_t R = (k + kCapCTAs - 1) / kCapCTAs, W = 2 * static_cast<size_t>(k);
+    return sizeof(double) * (R * W + W + k + R + 8) + sizeof(int) * (2 * R + 8);
+}
+
+__global__ void __launch_bounds__(kCapThreads) k_cap_invert_cluster(const double* __restrict__ C, int k,
+                                                                      double* __restrict__ Cinv,
+                                                                      int* __restrict__ flag) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    extern __shared__ double s_cap[];
+    const int R = (k + kCapCTAs - 1) / kCapCTAs, W = 2 * k;
+    const int q = static_cast<int>(cl.block_rank());
+    const int r0 = q * R, nr = max(0, min(k, r0 + R) - r0);
+    double* A = s_cap;              // nr x W
+    double* prow = A + R * W;       // W
+    double* s_col = prow + W;       // k column |.| sums of this CTA's rows
+    double* s_f = s_col + k;        // R factors of the current column
+    double* s_cand = s_f + R;       // [0] |a|, [1] signed a, [2] pivot value, [3] bad flag, [4] norm
+    int* s_used = reinterpret_cast<int*>(s_cand + 8);  // R: step at which the row was the pivot, -1
+    int* s_ci = s_used + R;         // [0] candidate row, [1] pivot row, [2] status
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kCapThreads / 32;
+    int bad = 0;
+    for (int e = tid; e < nr * W; e += kCapThreads) {
+        const int r = e / W, j = e - r * W;
+        const double v = j < k ? C[static_cast<long long>(r0 + r) * k + j] : (j - k == r0 + r ? 1.0 : 0.0);
+        if (!isfinite(v)) bad = 1;
+        A[e] = v;
+    }
+    for (int r = tid; r < R; r += kCapThreads) s_used[r] = -1;
+    bad = __syncthreads_or(bad);
+    for (int j = tid; j < k; j += kCapThreads) {
+        double s = 0.0;
+        for (int r = 0; r < nr; ++r) s += fabs(A[r * W + j]);
+        s_col[j] = s;
+    }
+    if (tid == 0) s_cand[3] = bad ? 1.0 : 0.0;
+    cap_cluster_barrier();
+    // identical in every CTA: any non-finite entry, |C|_1
+    double anorm = 0.0;
+    bool fail = false;
+    if (warp == 0) {
+        double m = 0.0;
+        for (int j = lane; j < k; j += 32) {
+            double s = 0.0;
+            for (int o = 0; o < kCapCTAs; ++o) s += cl.map_shared_rank(s_col, o)[j];
+            m = fmax(m, s);
+        }
+        for (int o = 16; o >= 1; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        int b = lane < kCapCTAs ? cl.map_shared_rank(s_cand, lane)[3] != 0.0 : 0;
+        b = __any_sync(0xffffffffu, b);
+        if (lane == 0) {
+            s_cand[4] = m;
+            s_ci[2] = b;
+        }
+    }
+    __syncthreads();
+    anorm = s_cand[4];
+    fail = s_ci[2] != 0;
+    for (int c = 0; c < k && !fail; ++c) {
+        // this CTA's candidate and the factors of column c
+        if (warp == 0) {
+            double best = -1.0, sv = 0.0;
+            int bi = k;
+            for (int r = lane; r < nr; r += 32) {
+                const double a = A[r * W + c];
+                s_f[r] = a;
+                if (s_used[r] < 0 && fabs(a) > best) {
+                    best = fabs(a);
+                    sv = a;
+                    bi = r0 + r;
+                }
+            }
+            for (int o = 16; o >= 1; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, best, o), os = __shfl_xor_sync(0xffffffffu, sv, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ob > best || (ob == best && oi < bi)) {
+                    best = ob;
+                    sv = os;
+                    bi = oi;
+                }
+            }
+            if (lane == 0) {
+                s_cand[0] = best;
+                s_cand[1] = sv;
+                s_ci[0] = bi;
+            }
+        }
+        cap_cluster_barrier();  // #1: candidates and factors complete
+        if (warp == 0) {
+            double best = -1.0, sv = 0.0;
+            int bi = k;
+            if (lane < kCapCTAs) {
+                const double* rc = cl.map_shared_rank(s_cand, lane);
+                best = rc[0];
+                sv = rc[1];
+                bi = cl.map_shared_rank(s_ci, lane)[0];
+            }
+            for (int o = 16; o >= 1; o >>= 1) {
+                const double ob = __shfl_xor_sync(0xffffffffu, best, o), os = __shfl_xor_sync(0xffffffffu, sv, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ob > best || (ob == best && oi < bi)) {
+                    best = ob;
+                    sv = os;
+                    bi = oi;
+                }
+            }
+            if (lane == 0) {
+                s_ci[1] = bi;
+                s_cand[2] = bi < k ? sv : 0.0;
+            }
+        }
+        __syncthreads();
+        const int p = s_ci[1];
+        const double pv = s_cand[2];
+        if (pv == 0.0) {  // singular (P:src/saddle.cpp:59-60 via rcond); same in every CTA
+            fail = true;
+            break;
+        }
+        {
+            const int po = p / R, pr = p - po * R;
+            const double* src = cl.map_shared_rank(A, po) + static_cast<long long>(pr) * W;
+            for (int j = c + tid; j < W; j += kCapThreads) prow[j] = src[j] / pv;
+        }
+        cap_cluster_barrier();  // #2: every CTA holds the pivot row; the owner may overwrite it
+        const int pl = p - r0;  // local index of the pivot row (if this CTA owns it)
+        for (int r = warp; r < nr; r += nw) {
+            double* row = A + r * W;
+            if (r == pl) {
+                for (int j = c + lane; j < W; j += 32) row[j] = prow[j];
+                if (lane == 0) s_used[r] = c;
+            } else {
+                const double f = s_f[r];
+                if (f != 0.0)
+                    for (int j = c + lane; j < W; j += 32) row[j] -= f * prow[j];
+            }
+        }
+        __syncthreads();
+    }
+    if (!fail) {
+        // |C^-1|_1: right halves over all rows (a row permutation of C^-1)
+        for (int j = tid; j < k; j += kCapThreads) {
+            double s = 0.0;
+            for (int r = 0; r < nr; ++r) s += fabs(A[r * W + k + j]);
+            s_col[j] = s;
+        }
+        cap_cluster_barrier();
+        if (warp == 0) {
+            double m = 0.0;
+            for (int j = lane; j < k; j += 32) {
+                double s = 0.0;
+                for (int o = 0; o < kCapCTAs; ++o) s += cl.map_shared_rank(s_col, o)[j];
+                m = fmax(m, s);
+            }
+            for (int o = 16; o >= 1; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (lane == 0) s_cand[4] = m;
+        }
+        __syncthreads();
+        const double rcond = 1.0 / (anorm * s_cand[4]);
+        fail = !isfinite(rcond) || rcond < 1e-15;
+        if (!fail)
+            for (int e = tid; e < nr * k; e += kCapThreads) {
+                const int r = e / k, j = e - r * k;
+                Cinv[static_cast<long long>(s_used[r]) * k + j] = A[r * W + k + j];
+            }
+    }
+    if (fail && q == 0 && tid == 0) *flag = 1;
+    cap_cluster_barrier();  // no CTA leaves while another may read its shared memory
 }
 
 // ---- fused GMRES-iteration kernels ----------------------------------------
@@ -756,6 +1056,35 @@ void precond_apply_dev(const ksvm_nfft_precond& P, const double* g, double* out,
     CK(cudaGetLastError());
 }
 
+// The cluster inverse when [C | I] fits the cluster's shared memory
+// (k <= ~330); false: use the one-CTA kernel. KSVM_NFFT_CAP=single forces it.
+bool launch_cap_cluster(const double* C, int k, double* Cinv, int* flag, cudaStream_t st) {
+    static const bool disabled = [] {
+        const char* e = std::getenv("KSVM_NFFT_CAP");
+        return e && std::strcmp(e, "single") == 0;
+    }();
+    const size_t smem = cap_cluster_smem(k);
+    if (disabled || smem > 227 * 1024) return false;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        CK(cudaFuncSetAttribute(k_cap_invert_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    });
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kCapCTAs, 1, 1);
+    cfg.blockDim = dim3(kCapThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kCapCTAs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k_cap_invert_cluster, C, k, Cinv, flag));
+    return true;
+}
+
 // Capacitance I + Z Theta^{-1} Z^T, partial-pivot LU, rcond, inverse.
 // Theta on the host (device == false, P's own stream) or on the device
 // (ordered on the caller's stream st).
@@ -780,20 +1109,37 @@ void precond_refresh(ksvm_nfft_precond& P, const double* theta_in, bool device, 
     const int nchunks = static_cast<int>(std::min<long long>(64, std::max<long long>(1, n / 1024)));
     const long long chunk = ((n + nchunks - 1) / nchunks + 3) / 4 * 4;
     DevBuf<double> part, C;
-    part.alloc(static_cast<size_t>(nchunks) * nt * nt * 64);
     C.alloc(static_cast<size_t>(k) * k);
-    launch_k(k_cap_partial, dim3(dim3(nt * nt, nchunks)), dim3(32), 0, st, P.Z.p, P.theta.p, k, n, chunk, nt, part.p);
-    launch_k(k_cap_finish, dim3((k * k + 255) / 256), dim3(256), 0, st, part.p, nchunks, nt, k, C.p);
+    const int T = nt * (nt + 1) / 2;
+    if (k <= kGramMaxK && T <= kGramWarps * kGramTiles) {
+        static std::once_flag once;
+        std::call_once(once, [] {
+            CK(cudaFuncSetAttribute(k_cap_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        });
+        const long long slices = (n + kGramCols - 1) / kGramCols;
+        const long long per = (slices + kGramCTAs - 1) / kGramCTAs;  // slices per CTA
+        const int nparts = static_cast<int>((slices + per - 1) / per);
+        part.alloc(static_cast<size_t>(nparts) * T * 64);
+        const size_t smem = 2 * sizeof(double) * (static_cast<size_t>(nt) * 8 * kGramLd + kGramCols);
+        k_cap_gram<<<nparts, kGramWarps * 32, smem, st>>>(P.Z.p, P.theta.p, k, n, nt, T, per * kGramCols, part.p);
+        launch_k(k_cap_finish_sym, dim3((k * k + 255) / 256), dim3(256), 0, st, part.p, nparts, nt, T, k, C.p);
+    } else {
+        part.alloc(static_cast<size_t>(nchunks) * nt * nt * 64);
+        launch_k(k_cap_partial, dim3(dim3(nt * nt, nchunks)), dim3(32), 0, st, P.Z.p, P.theta.p, k, n, chunk, nt, part.p);
+        launch_k(k_cap_finish, dim3((k * k + 255) / 256), dim3(256), 0, st, part.p, nchunks, nt, k, C.p);
+    }
     launch_counter() += 2;
     CK(cudaGetLastError());
     // inverse on the device: Gauss-Jordan with the reference's pivot rule and guards
     DevBuf<double> aug;
     DevBuf<int> flag;
-    aug.alloc(static_cast<size_t>(k) * 2 * k);
     flag.alloc(1);
     if (P.Cinv.n < static_cast<size_t>(k) * k) P.Cinv.alloc(static_cast<size_t>(k) * k);
     CK(cudaMemsetAsync(flag.p, 0, sizeof(int), st));
-    k_cap_invert<<<1, 1024, sizeof(double) * std::max(k, 32), st>>>(aug.p, C.p, k, P.Cinv.p, flag.p);
+    if (!launch_cap_cluster(C.p, k, P.Cinv.p, flag.p, st)) {
+        aug.alloc(static_cast<size_t>(k) * 2 * k);
+        k_cap_invert<<<1, 1024, sizeof(double) * std::max(k, 32), st>>>(aug.p, C.p, k, P.Cinv.p, flag.p);
+    }
     ++launch_counter();
     CK(cudaGetLastError());
     int hflag = 0;

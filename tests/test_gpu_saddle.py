@@ -47,7 +47,9 @@ def test_saddle_apply_matches_oracle(n):
     assert A.size() == n + 1
 
 
-@pytest.mark.parametrize("rank", [0, 1, 5, 40])
+# 200: SMEM-staged Gram + cluster inverse; 230: per-tile Gram + cluster
+# inverse; 340: per-tile Gram + one-CTA inverse (saddle.cu)
+@pytest.mark.parametrize("rank", [0, 1, 5, 40, 200, 230, 340])
 def test_preconditioner_matches_oracle(rank):
     n = 2000
     inst = Inst(n, 31)
