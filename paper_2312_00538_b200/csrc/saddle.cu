@@ -977,6 +977,8 @@ struct ksvm_nfft_precond {
     int k = 0, device = 0;
     bool identity = false, fallback = false, fresh = false;
     DevBuf<double> Z, y, theta, Cinv, partial, s, inner;
+    DevBuf<double> cap_part, cap_C, cap_aug;  // refresh workspace, kept across refreshes
+    DevBuf<int> cap_flag;
     cudaStream_t stream = nullptr;
     mutable std::mutex mu;
     ~ksvm_nfft_precond() {
@@ -1108,8 +1110,12 @@ void precond_refresh(ksvm_nfft_precond& P, const double* theta_in, bool device, 
     const int k = P.k, nt = (k + 7) / 8;
     const int nchunks = static_cast<int>(std::min<long long>(64, std::max<long long>(1, n / 1024)));
     const long long chunk = ((n + nchunks - 1) / nchunks + 3) / 4 * 4;
-    DevBuf<double> part, C;
-    C.alloc(static_cast<size_t>(k) * k);
+    auto grow = [](auto& b, size_t count) {
+        if (b.n < count) b.alloc(count);
+    };
+    DevBuf<double>& part = P.cap_part;
+    DevBuf<double>& C = P.cap_C;
+    grow(C, static_cast<size_t>(k) * k);
     const int T = nt * (nt + 1) / 2;
     if (k <= kGramMaxK && T <= kGramWarps * kGramTiles) {
         static std::once_flag once;
@@ -1119,25 +1125,25 @@ void precond_refresh(ksvm_nfft_precond& P, const double* theta_in, bool device, 
         const long long slices = (n + kGramCols - 1) / kGramCols;
         const long long per = (slices + kGramCTAs - 1) / kGramCTAs;  // slices per CTA
         const int nparts = static_cast<int>((slices + per - 1) / per);
-        part.alloc(static_cast<size_t>(nparts) * T * 64);
+        grow(part, static_cast<size_t>(nparts) * T * 64);
         const size_t smem = 2 * sizeof(double) * (static_cast<size_t>(nt) * 8 * kGramLd + kGramCols);
         k_cap_gram<<<nparts, kGramWarps * 32, smem, st>>>(P.Z.p, P.theta.p, k, n, nt, T, per * kGramCols, part.p);
         launch_k(k_cap_finish_sym, dim3((k * k + 255) / 256), dim3(256), 0, st, part.p, nparts, nt, T, k, C.p);
     } else {
-        part.alloc(static_cast<size_t>(nchunks) * nt * nt * 64);
+        grow(part, static_cast<size_t>(nchunks) * nt * nt * 64);
         launch_k(k_cap_partial, dim3(dim3(nt * nt, nchunks)), dim3(32), 0, st, P.Z.p, P.theta.p, k, n, chunk, nt, part.p);
         launch_k(k_cap_finish, dim3((k * k + 255) / 256), dim3(256), 0, st, part.p, nchunks, nt, k, C.p);
     }
     launch_counter() += 2;
     CK(cudaGetLastError());
     // inverse on the device: Gauss-Jordan with the reference's pivot rule and guards
-    DevBuf<double> aug;
-    DevBuf<int> flag;
-    flag.alloc(1);
+    DevBuf<double>& aug = P.cap_aug;
+    DevBuf<int>& flag = P.cap_flag;
+    grow(flag, 1);
     if (P.Cinv.n < static_cast<size_t>(k) * k) P.Cinv.alloc(static_cast<size_t>(k) * k);
     CK(cudaMemsetAsync(flag.p, 0, sizeof(int), st));
     if (!launch_cap_cluster(C.p, k, P.Cinv.p, flag.p, st)) {
-        aug.alloc(static_cast<size_t>(k) * 2 * k);
+        grow(aug, static_cast<size_t>(k) * 2 * k);
         k_cap_invert<<<1, 1024, sizeof(double) * std::max(k, 32), st>>>(aug.p, C.p, k, P.Cinv.p, flag.p);
     }
     ++launch_counter();

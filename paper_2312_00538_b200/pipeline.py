@@ -23,6 +23,7 @@ from dataclasses import dataclass, field
 from typing import List
 
 import numpy as np
+import torch
 
 from . import _lib
 from .fastsum import (AnovaKernelSpec, Dataset, FastsumConfig, FeatureWindowing, _raise, anova_fast_operator)
@@ -102,8 +103,9 @@ def balance_and_split(data: Dataset, train_fraction: float = 0.5, seed: int = 0)
                                                    C.c_void_p(tr.ctypes.data), C.byref(ntr),
                                                    C.c_void_p(te.ctypes.data), C.byref(nte)))
     tr, te = tr[: ntr.value], te[: nte.value]
-    pts = np.asarray(data.points, dtype=np.float64)
-    return Dataset(pts[tr].copy(), lab[tr].copy()), Dataset(pts[te].copy(), lab[te].copy())
+    pts = torch.from_numpy(np.ascontiguousarray(data.points, dtype=np.float64))
+    rows = lambda idx: torch.index_select(pts, 0, torch.from_numpy(idx)).numpy()  # threaded exact row copy
+    return Dataset(rows(tr), lab[tr]), Dataset(rows(te), lab[te])
 
 
 def zscore_fit_transform(train: Dataset, test: Dataset):
@@ -112,14 +114,21 @@ def zscore_fit_transform(train: Dataset, test: Dataset):
     applied to both parts. Returns the FeatureStats list."""
     if train.n() == 0:
         raise ValueError("empty training split")
-    X = np.asarray(train.points, dtype=np.float64)
+    # sums in numpy (fixed order), elementwise passes on torch's CPU threads
+    # (exact: the same IEEE operations per element)
+    Xt = torch.from_numpy(np.ascontiguousarray(train.points, dtype=np.float64)).clone()
+    X = Xt.numpy()
     n = X.shape[0]
     mean = X.sum(axis=0) / n
-    sd = np.sqrt(((X - mean) ** 2).sum(axis=0) / n)
+    Xt.sub_(torch.from_numpy(mean))
+    sd = np.sqrt(torch.mul(Xt, Xt).numpy().sum(axis=0) / n)  # = ((X - mean) ** 2).sum(0) / n
     sd[sd < 1e-300] = 1.0  # constant column maps to zeros
-    train.points = (X - mean) / sd
+    Xt.div_(torch.from_numpy(sd))
+    train.points = X
     if test is not None and test.n() > 0:
-        test.points = (np.asarray(test.points, dtype=np.float64) - mean) / sd
+        Tt = torch.from_numpy(np.ascontiguousarray(test.points, dtype=np.float64)).clone()
+        Tt.sub_(torch.from_numpy(mean)).div_(torch.from_numpy(sd))
+        test.points = Tt.numpy()
     return [FeatureStats(float(a), float(b)) for a, b in zip(mean, sd)]
 
 
