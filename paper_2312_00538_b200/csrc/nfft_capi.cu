@@ -18,6 +18,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -380,7 +381,7 @@ int64_t gather_chunk(int64_t total_points, int d) {
 }
 
 // Affine map of P:src/fastsum.cpp:126-140 on a column-major n x d block.
-void affine_map(Window& w, const std::vector<double>& cm, int64_t n, double fit, double rT) {
+void affine_map(Window& w, const double* cm, int64_t n, double fit, double rT) {
     const int d = w.d;
     for (int t = 0; t < d; ++t) {
         double hi = cm[static_cast<size_t>(t) * n], lo = hi;
@@ -542,21 +543,34 @@ struct Engine {
     }
 
     // plan_fastsum for one window (P:src/fastsum.cpp:103-209) on the device.
-    void plan_window(Window& w, const std::vector<double>& cm) {
+    // Host half of plan_fastsum for one window: affine map, scaled
+    // coordinates, data range. Touches only w and `out` (windows run on
+    // concurrent host threads).
+    struct WinPrep {
+        std::vector<double> sc;
+        double range[2] = {0.0, 0.0};
+    };
+    void prep_window(Window& w, const double* cm, WinPrep& out) const {
         const int d = w.d;
         affine_map(w, cm, n, fit, cfg.torus_radius);
-        std::vector<double> sc(static_cast<size_t>(n) * d);
+        std::vector<double>& sc = out.sc;
+        sc.resize(static_cast<size_t>(n) * d);
         for (int t = 0; t < d; ++t)
             for (int64_t i = 0; i < n; ++i)
                 sc[static_cast<size_t>(t * n + i)] = (cm[static_cast<size_t>(t * n + i)] - w.center[t]) * w.scale;
-        double range[2] = {0.0, 0.0};
         if (data_range) {
-            range[0] = range[1] = sc[0];
+            out.range[0] = out.range[1] = sc[0];
             for (double x : sc) {
-                range[0] = std::min(range[0], x);
-                range[1] = std::max(range[1], x);
+                out.range[0] = std::min(out.range[0], x);
+                out.range[1] = std::max(out.range[1], x);
             }
         }
+    }
+
+    void plan_window(Window& w, WinPrep& prep) {
+        const int d = w.d;
+        std::vector<double>& sc = prep.sc;
+        const double* range = prep.range;
         const Geometry g = geometry(cfg, d, data_range ? range : nullptr);
         w.geom = g;
         const double bwin = g.bwin;
@@ -1378,18 +1392,35 @@ void build_engine(Engine& E, const double* points, int64_t n, int64_t d, int64_t
     E.n_owned_windows = 0;
     for (auto& w : E.wins) E.n_owned_windows += w->owned ? 1 : 0;
     E.n_owned_windows = std::max<int64_t>(1, E.n_owned_windows);
-    int col0 = 0;
+    // host halves of the owned windows' plans on concurrent threads (a
+    // window's feature columns are contiguous in soa), device halves in
+    // window order
+    std::vector<Engine::WinPrep> prep(static_cast<size_t>(P));
+    {
+        std::vector<int> col0(static_cast<size_t>(P), 0);
+        for (int l = 1; l < P; ++l) col0[static_cast<size_t>(l)] = col0[static_cast<size_t>(l - 1)] + E.wins[static_cast<size_t>(l - 1)]->d;
+        std::atomic<int> next{0};
+        auto work = [&] {
+            for (int l; (l = next.fetch_add(1)) < P;) {
+                Window& w = *E.wins[static_cast<size_t>(l)];
+                if (w.owned)
+                    E.prep_window(w, soa.data() + static_cast<size_t>(col0[static_cast<size_t>(l)]) * n,
+                                  prep[static_cast<size_t>(l)]);
+            }
+        };
+        const int nthr = std::max(1, std::min<int>(P, static_cast<int>(std::thread::hardware_concurrency())));
+        std::vector<std::thread> pool;
+        for (int t = 1; t < nthr; ++t) pool.emplace_back(work);
+        work();
+        for (auto& th : pool) th.join();
+    }
     for (int l = 0; l < P; ++l) {
         Window& w = *E.wins[static_cast<size_t>(l)];
         if (w.owned) {
-            std::vector<double> cm(static_cast<size_t>(n) * w.d);
-            for (int t = 0; t < w.d; ++t)
-                std::memcpy(cm.data() + static_cast<size_t>(t) * n, soa.data() + static_cast<size_t>(col0 + t) * n,
-                            sizeof(double) * n);
-            E.plan_window(w, cm);
+            E.plan_window(w, prep[static_cast<size_t>(l)]);
+            std::vector<double>().swap(prep[static_cast<size_t>(l)].sc);
             E.owned.push_back(l);
         }
-        col0 += w.d;
     }
     E.finalize();
 }
