@@ -35,7 +35,7 @@
 namespace ksvm_nfft {
 namespace {
 
-constexpr int kRows = 16;  // basis rows per pass of the multi-dot kernel
+constexpr int kRows = 32;  // basis rows per pass of the multi-dot kernels
 constexpr int kMaxRank = 1024;
 
 // sum_a M[a][i] c[a] for a < rows with four independent accumulators
