@@ -5,17 +5,27 @@
 
 One step = one ANOVA matvec y = sum_l eta_l K~_l v over the whole workload
 (plan construction excluded, as P:tests/acceptance.cpp:232-244 does). The
-default workload is BASELINE.json configs[1] (config 2: n=60000, d=8,
-windows {0,1,2},{3,4,5},{6,7}); --config selects another (1..5).
+default workload is BASELINE.json configs[4] (config 5: n = 10^7, d = 28,
+9 three-feature windows + 1 singleton), the largest configuration that fits
+one GPU; BASELINE's metric names no config, and its 1/2/4/8-GPU axis belongs
+to configs 4 and 5. --config selects another (1..5; config 2 is the small,
+latency-bound matvec).
 
 N > 1 (torchrun, one process per GPU): windows are sharded over ranks (LPT)
 and one NCCL all-reduce per step sums the length-n partial outputs, so each
 step is still ONE matvec of the fixed workload ("scaling": "strong").
 
 Timing: W untimed warm-up steps; K timed steps, each bracketed by CUDA events
-on the launching stream, with a 256 MiB L2 flush (untimed) before every step
-because config 2's inputs fit in the 126 MB L2; barrier + synchronize on both
-sides; max over ranks. nvidia-smi samples clocks during the timed region.
+on the launching stream, with a 256 MiB L2 flush (untimed) before every step;
+barrier + synchronize on both sides; max over ranks. nvidia-smi samples
+clocks during the timed region.
+
+Roofline: the path is FP64-bound (1024 FMA per point per 3-D
+window against 56 B), so "roofline" is the dominant kernel's FP64 rate
+against cuBLAS DGEMM measured in the same run ("bound": "fp64"; the 3-D
+spread/gather run on the FP64 tensor cores, DMMA, which share the FP64
+datapath with DFMA); its HBM rate against MEASURED_PEAKS.json sits beside it
+("hbm"), as does the matvec-level HBM fraction the BASELINE metric names.
 
 On one GPU the line also carries "training": north_star's end-to-end IPM
 training on BASELINE config 1 through train_pipeline (wall clock and the
@@ -44,9 +54,9 @@ import numpy as np  # noqa: E402
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--n", type=int, default=None, help="override n (debug only)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -128,6 +138,13 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def config_dict(w, cfg: int) -> dict:
+    """The workload description both arms print (identical keys and values)."""
+    return {"workload": w.name, "n": w.n, "d": w.d, "windows": w.windows,
+            "fit_fraction": w.fit_fraction, "N": 32, "m": 4, "sigma": 2, "seed": 1000 + cfg,
+            "l2": "GPU arm: 256 MiB L2 flush before every timed step"}
+
+
 # ------------------------------------------------------------ CPU legs -----
 def cpu_lib():
     import oracle
@@ -178,10 +195,12 @@ def cpu_baseline(w, budget_s: float):
 
 def run_reference(args):
     """The reference's CPU fastsum with every host thread: each step runs one
-    full matvec per thread concurrently on the same (immutable, thread-safe,
+    matvec per thread concurrently on the same (immutable, thread-safe,
     P:include/ksvm/kernel.hpp:28-31) operator. For n > 100000 a step is a
-    bounded sample: matvecs on the first 100000 points, reported scaled to
-    the full n by the single-thread two-size extrapolation of cpu_baseline."""
+    bounded sample: the matvecs run on the first 50000 points and the rate is
+    scaled to the full n by the single-thread ratio t(50000) / t(n), t(n) from
+    cpu_baseline's two-size extrapolation (the CPU path is O(n) plus a fixed
+    grid cost per window)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
@@ -189,7 +208,7 @@ def run_reference(args):
     w = workloads.make(args.config, args.n)
     lib, kind = cpu_lib()
     T = max(1, os.cpu_count() or 1)
-    ns = min(w.n, 100000)
+    ns = w.n if w.n <= 100000 else 50000
     op = lib.anova(w.points[:ns], w.windows, fit=w.fit_fraction)
     vs = w.v[:ns]
 
@@ -207,19 +226,24 @@ def run_reference(args):
         step()
     el = time.perf_counter() - t0
     value = T * args.steps / el
-    sample = f"each step = {T} concurrent full matvecs (one per host thread)"
+    sample = f"each step = {T} concurrent matvecs (one per host thread)"
     if ns < w.n:
         base = cpu_baseline(w, 10.0)
-        t_small = _cpu_time_one(lib, w, ns)
+        t_small = min(_cpu_time_one(lib, w, ns) for _ in range(2))
         value *= (t_small * base["value"])  # throughput at ns scaled by t(ns)/t(n)
-        sample += f" on the first {ns} points, scaled to n={w.n} by the 1-thread t(ns)/t(n) ratio"
+        sample += (f" on the first {ns} of the {w.n} points, scaled to n={w.n} by the 1-thread ratio "
+                   f"t({ns})/t({w.n}) = {t_small:.3f} s / {base['s_per_matvec']:.2f} s ({base['sample']})")
+    else:
+        sample += f" of the full workload"
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": w.name, "n": w.n, "d": w.d, "windows": w.windows,
-                       "fit_fraction": w.fit_fraction, "N": 32, "m": 4, "sigma": 2},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": T, "kind": kind, "sample": sample},
+            "config": config_dict(w, args.config),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": T, "kind": kind, "sample": sample,
+                             "fft": "the reference's FFTW calls run on oracle/shim/fftw3.h (exact radix-2 "
+                                    "complex FFT; ~5x slower than FFTW per 64^3 transform, so this arm "
+                                    "is somewhat slower than the reference built with FFTW)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -400,25 +424,28 @@ def run_ours(args):
             except Exception:
                 pass
             fpk = fp64_peak_tflops(dev)
-            fma_rate = kernel_fmas(w, dom, pts) / (ms * 1e-3)
-            roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
-                    "frac": ach / hbm_peak, "peak_source": peak_kind, "traffic": traffic,
-                    "kernel_ms": ms,
-                    "fp64": {"achieved_tflops": 2 * fma_rate / 1e12, "peak_tflops": fpk,
-                             "peak_source": "measured cuBLAS DGEMM 8192^3 (torch.matmul f64)",
-                             "frac": 2 * fma_rate / 1e12 / fpk}}
+            tflops = 2 * kernel_fmas(w, dom, pts) / (ms * 1e-3) / 1e12
+            roof = {"bound": "fp64", "kernel": dom, "achieved": tflops, "peak": fpk, "unit": "TFLOP/s",
+                    "frac": tflops / fpk,
+                    "peak_source": "cuBLAS DGEMM 8192^3 (torch.matmul f64) measured in this run",
+                    "per_launch": {"fma": kernel_fmas(w, dom, pts), "algorithmic_bytes": kernel_bytes(w, dom, pts),
+                                   "ms": ms},
+                    "traffic": traffic,
+                    "hbm": {"achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+                            "peak_source": peak_kind},
+                    "timing": "per-launch CUDA events on the operator's stream in a separate pass of K "
+                              "matvecs with the same L2 flush (stage timing serialises the dimension "
+                              "classes, so the per-launch sum exceeds the graph-timed step slightly)"}
         step_ms = total_ms / K
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
                 "warmup": max(3, args.warmup), "ms_per_step": step_ms, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": w.name, "n": w.n, "d": w.d, "windows": w.windows,
-                           "fit_fraction": w.fit_fraction, "N": 32, "m": 4, "sigma": 2,
-                           "l2": "256 MiB flush before every timed step",
-                           "parallelism": f"window-sharded x{world} + NCCL allreduce" if world > 1 else "1 GPU",
-                           "seed": 1000 + args.config,
-                           "dedup": {str(l): p for l, p in enumerate(pts) if 0 < p < w.n}},
+                "config": config_dict(w, args.config),
+                "parallelism": f"window-sharded x{world} + NCCL allreduce" if world > 1 else "1 GPU",
+                "dedup": {str(l): p for l, p in enumerate(pts) if 0 < p < w.n},
                 "hbm_fraction_matvec": (w.hbm_bytes() / (step_ms * 1e-3) / 1e9) / peaks()[0],
                 "per_launch_ms": per_launch,
+                "per_launch_sum_ms": sum(per_launch.values()),
                 "roofline": roof,
                 "clocks": clk.summary(),
                 "gpu_launches": launches,

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <exception>
 #include <atomic>
 #include <cmath>
 #include <cstdio>
@@ -1399,20 +1400,33 @@ void build_engine(Engine& E, const double* points, int64_t n, int64_t d, int64_t
     {
         std::vector<int> col0(static_cast<size_t>(P), 0);
         for (int l = 1; l < P; ++l) col0[static_cast<size_t>(l)] = col0[static_cast<size_t>(l - 1)] + E.wins[static_cast<size_t>(l - 1)]->d;
+        // A worker's exception (bad_alloc in the scaled copy, ...) is caught
+        // into its window's slot and rethrown here after every started
+        // thread joined: nothing may escape a std::thread (std::terminate).
         std::atomic<int> next{0};
+        std::vector<std::exception_ptr> err(static_cast<size_t>(P));
         auto work = [&] {
             for (int l; (l = next.fetch_add(1)) < P;) {
                 Window& w = *E.wins[static_cast<size_t>(l)];
-                if (w.owned)
+                if (!w.owned) continue;
+                try {
                     E.prep_window(w, soa.data() + static_cast<size_t>(col0[static_cast<size_t>(l)]) * n,
                                   prep[static_cast<size_t>(l)]);
+                } catch (...) {
+                    err[static_cast<size_t>(l)] = std::current_exception();
+                }
             }
         };
         const int nthr = std::max(1, std::min<int>(P, static_cast<int>(std::thread::hardware_concurrency())));
         std::vector<std::thread> pool;
-        for (int t = 1; t < nthr; ++t) pool.emplace_back(work);
+        try {
+            for (int t = 1; t < nthr; ++t) pool.emplace_back(work);
+        } catch (...) {  // could not start a thread: the ones started (and this one) finish the work
+        }
         work();
         for (auto& th : pool) th.join();
+        for (auto& e : err)
+            if (e) std::rethrow_exception(e);
     }
     for (int l = 0; l < P; ++l) {
         Window& w = *E.wins[static_cast<size_t>(l)];

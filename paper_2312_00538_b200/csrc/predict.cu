@@ -24,14 +24,10 @@
 namespace ksvm_nfft {
 namespace {
 
-constexpr int kMaxFeat = 1024;
-
-__constant__ int c_feat[kMaxFeat];
-
 // out[r] = sum_i coeff_i sum_l w_l exp(-||x_i^l - t_r^l||^2 / ell_l^2)
 // train: n x d column-major (ld n); targets: m x d column-major (ld m)
 __global__ void __launch_bounds__(256) k_exact_anova(const double* __restrict__ train, long long n,
-                                                     const int* __restrict__ woff, int P,
+                                                     const int* __restrict__ woff, const int* __restrict__ feat, int P,
                                                      const double* __restrict__ w, const double* __restrict__ ell2,
                                                      const double* __restrict__ coeff, const double* __restrict__ tgt,
                                                      long long m, const long long* __restrict__ rows,
@@ -44,7 +40,7 @@ __global__ void __launch_bounds__(256) k_exact_anova(const double* __restrict__ 
         for (int l = 0; l < P; ++l) {
             double d2 = 0.0;
             for (int q = woff[l]; q < woff[l + 1]; ++q) {
-                const int f = c_feat[q];
+                const int f = feat[q];
                 const double diff = train[static_cast<long long>(f) * n + i] - tgt[static_cast<long long>(f) * m + tr];
                 d2 += diff * diff;
             }
@@ -99,7 +95,6 @@ extern "C" int ksvm_nfft_decision_values(const double* train, int64_t n, int d, 
             if (window_sizes[l] < 1) throw std::invalid_argument("decision_values: empty window");
             woff[static_cast<size_t>(l) + 1] = woff[static_cast<size_t>(l)] + window_sizes[l];
         }
-        if (woff[static_cast<size_t>(P)] > kMaxFeat) throw std::invalid_argument("decision_values: too many features");
         for (int q = 0; q < woff[static_cast<size_t>(P)]; ++q)
             if (window_features[q] < 0 || window_features[q] >= d)
                 throw std::invalid_argument("decision_values: feature index out of range");
@@ -190,7 +185,7 @@ extern "C" int ksvm_nfft_decision_values(const double* train, int64_t n, int d, 
             }
             for (int l = 0; l < P; ++l) ell2[static_cast<size_t>(l)] = length_scales[l] * length_scales[l];
             DevBuf<double> dtr, dte, dw, de, dc, dout;
-            DevBuf<int> doff;
+            DevBuf<int> doff, dfeat;  // per-call buffers: concurrent calls share nothing
             DevBuf<long long> drows;
             dtr.upload(tr_cm.data(), tr_cm.size(), st);
             dte.upload(te_cm.data(), te_cm.size(), st);
@@ -200,10 +195,9 @@ extern "C" int ksvm_nfft_decision_values(const double* train, int64_t n, int d, 
             doff.upload(woff.data(), woff.size(), st);
             drows.upload(redo.data(), redo.size(), st);
             dout.alloc(redo.size());
-            CK(cudaMemcpyToSymbolAsync(c_feat, window_features, sizeof(int) * woff[static_cast<size_t>(P)], 0,
-                                       cudaMemcpyHostToDevice, st));
-            k_exact_anova<<<static_cast<unsigned>(redo.size()), 256, 0, st>>>(dtr.p, n, doff.p, P, dw.p, de.p, dc.p,
-                                                                               dte.p, t, drows.p, dout.p);
+            dfeat.upload(window_features, static_cast<size_t>(woff[static_cast<size_t>(P)]), st);
+            k_exact_anova<<<static_cast<unsigned>(redo.size()), 256, 0, st>>>(dtr.p, n, doff.p, dfeat.p, P, dw.p, de.p,
+                                                                               dc.p, dte.p, t, drows.p, dout.p);
             ++launch_counter();
             CK(cudaGetLastError());
             std::vector<double> vals(redo.size());

@@ -26,6 +26,7 @@
 #include <cstring>
 #include <memory>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "capi_common.cuh"
@@ -947,6 +948,23 @@ __global__ void gk_norm_givens(const double* __restrict__ npartial, int nb, doub
 
 int blocks_for(long long L) { return reduce_blocks(L); }
 
+constexpr size_t kGivensMaxSmem = 227 * 1024;
+
+// gk_norm_givens past 48 KB of dynamic shared memory (max_iter > 2047):
+// per-device opt-in, set the first time each device needs it.
+void ensure_givens_attributes() {
+    static std::mutex mu;
+    static std::vector<bool> done(256, false);
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev >= 0 && dev < 256 && !done[static_cast<size_t>(dev)]) {
+        CK(cudaFuncSetAttribute(gk_norm_givens, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kGivensMaxSmem)));
+        done[static_cast<size_t>(dev)] = true;
+    }
+}
+
 }  // namespace
 }  // namespace ksvm_nfft
 
@@ -1058,6 +1076,22 @@ void precond_apply_dev(const ksvm_nfft_precond& P, const double* g, double* out,
     CK(cudaGetLastError());
 }
 
+// The capacitance kernels' shared-memory opt-in is a per-device function
+// attribute: set it the first time each device is seen (like
+// ensure_attributes in nfft_capi.cu), on the current device.
+void ensure_cap_attributes() {
+    static std::mutex mu;
+    static std::vector<bool> done(256, false);
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev >= 0 && dev < 256 && !done[static_cast<size_t>(dev)]) {
+        CK(cudaFuncSetAttribute(k_cap_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        CK(cudaFuncSetAttribute(k_cap_invert_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        done[static_cast<size_t>(dev)] = true;
+    }
+}
+
 // The cluster inverse when [C | I] fits the cluster's shared memory
 // (k <= ~330); false: use the one-CTA kernel. KSVM_NFFT_CAP=single forces it.
 bool launch_cap_cluster(const double* C, int k, double* Cinv, int* flag, cudaStream_t st) {
@@ -1067,10 +1101,7 @@ bool launch_cap_cluster(const double* C, int k, double* Cinv, int* flag, cudaStr
     }();
     const size_t smem = cap_cluster_smem(k);
     if (disabled || smem > 227 * 1024) return false;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        CK(cudaFuncSetAttribute(k_cap_invert_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    });
+    ensure_cap_attributes();
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(kCapCTAs, 1, 1);
     cfg.blockDim = dim3(kCapThreads, 1, 1);
@@ -1101,10 +1132,14 @@ void precond_refresh(ksvm_nfft_precond& P, const double* theta_in, bool device, 
         st = P.stream;
         P.theta.upload(theta_in, static_cast<size_t>(n), st);
     }
-    P.fallback = false;
-    P.fresh = true;
+    // Not fresh until every step below succeeded: a throw part-way (launch
+    // failure, out of memory) must not leave the new Theta paired with the
+    // previous refresh's inverse.
+    P.fresh = false;
     if (P.identity || P.k == 0) {
         CK(cudaStreamSynchronize(st));
+        P.fallback = false;
+        P.fresh = true;
         return;
     }
     const int k = P.k, nt = (k + 7) / 8;
@@ -1118,10 +1153,7 @@ void precond_refresh(ksvm_nfft_precond& P, const double* theta_in, bool device, 
     grow(C, static_cast<size_t>(k) * k);
     const int T = nt * (nt + 1) / 2;
     if (k <= kGramMaxK && T <= kGramWarps * kGramTiles) {
-        static std::once_flag once;
-        std::call_once(once, [] {
-            CK(cudaFuncSetAttribute(k_cap_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        });
+        ensure_cap_attributes();
         const long long slices = (n + kGramCols - 1) / kGramCols;
         const long long per = (slices + kGramCTAs - 1) / kGramCTAs;  // slices per CTA
         const int nparts = static_cast<int>((slices + per - 1) / per);
@@ -1151,7 +1183,8 @@ void precond_refresh(ksvm_nfft_precond& P, const double* theta_in, bool device, 
     int hflag = 0;
     CK(cudaMemcpyAsync(&hflag, flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (hflag) P.fallback = true;  // P:src/saddle.cpp:55-60
+    P.fallback = hflag != 0;  // P:src/saddle.cpp:55-60
+    P.fresh = true;
 }
 
 cudaStream_t pick_stream(int ptr_kind, void* stream, cudaStream_t own) {
@@ -1326,6 +1359,11 @@ int ksvm_nfft_gmres_solve(const ksvm_nfft_saddle* s, const ksvm_nfft_precond* p,
         if (!s || !p || !rhs || !x || !stats) throw std::invalid_argument("gmres: null argument");
         if (!(tol > 0.0)) throw std::invalid_argument("gmres tol must be positive");
         if (max_iter < 0) throw std::invalid_argument("gmres max_iter must be >= 0");
+        // gk_norm_givens stages the new Hessenberg column and the stored
+        // rotations, 3 max_iter + 3 doubles, in shared memory
+        if (static_cast<size_t>(3) * max_iter + 3 > kGivensMaxSmem / sizeof(double))
+            throw std::invalid_argument("gmres max_iter must be <= " +
+                                        std::to_string((kGivensMaxSmem / sizeof(double) - 3) / 3));
         if (p->n != s->n) throw std::invalid_argument("gmres: preconditioner size mismatch");
         if (p->device != s->device) throw std::invalid_argument("gmres: operator and preconditioner on different GPUs");
         std::lock_guard<std::mutex> lk(s->mu);
@@ -1334,6 +1372,7 @@ int ksvm_nfft_gmres_solve(const ksvm_nfft_saddle* s, const ksvm_nfft_precond* p,
         const ksvm_nfft_precond& P = *p;
         if (!P.identity && !P.fresh) throw std::logic_error("SaddlePreconditioner: refresh() before apply()");
         DeviceGuard dg(S.device);
+        if ((static_cast<size_t>(3) * max_iter + 3) * sizeof(double) > 48 * 1024) ensure_givens_attributes();
         cudaStream_t st = pick_stream(ptr_kind, stream, S.stream);
         const long long n1 = S.n + 1;
         const int MI = max_iter, MIc = std::max(MI, 1);
@@ -1464,12 +1503,14 @@ int ksvm_nfft_gmres_solve(const ksvm_nfft_saddle* s, const ksvm_nfft_precond* p,
                      static_cast<const double*>(S.w.p), n1, static_cast<const double*>(S.scal.p + 1), stop);
             launch_counter() += 9;
             if ((k + 1) % kLookAhead == 0 && k + 1 < MI) {
+                CK(cudaGetLastError());  // a failed launch must not read as "not converged"
                 CK(cudaMemcpyAsync(hstat, S.gstat.p, sizeof(int) * 8, cudaMemcpyDeviceToHost, st));
                 CK(cudaStreamSynchronize(st));
                 if (hstat[0]) break;
             }
         }
         // final state: H, beta, history, counters
+        CK(cudaGetLastError());
         CK(cudaMemcpyAsync(hstat, S.gstat.p, sizeof(int) * 8, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(hp, S.gH.p, sizeof(double) * static_cast<size_t>(MI + 1) * MIc, cudaMemcpyDeviceToHost, st));
         double* hbeta = hp + static_cast<size_t>(MI + 1) * MIc;

@@ -1,0 +1,121 @@
+"""GPU vs the reference's own fastsum at the FULL BASELINE sizes (configs 3, 4, 5).
+
+The checker is the reference's ``src/fastsum.cpp`` compiled unmodified by path
+(``oracle/_ref/libref.so``; the bit-identical restatement ``liboracle.so`` when
+that file is absent). ``AnovaFastOperator::apply`` (P:src/fastsum.cpp:345-352)
+is ``out = 0; for l: out += eta_l * apply_fastsum(plan_l, v)``: the windows are
+independent single-window transforms, so here each window's
+``plan_fastsum`` + ``apply_fastsum`` (P:src/fastsum.cpp:103-209, 300-305) runs on
+its own host thread (ctypes releases the GIL) and the results are summed in
+window order exactly as the loop does. One matvec costs the single-threaded
+reference about 3 s (config 3), 31 s (config 4) and 300 s (config 5,
+profiles/r1_bench_cfg*.json); with the windows concurrent the wall time is
+that of the slowest window (~35 s for config 5 on the GPU box's 16 threads).
+
+Config 4 runs twice: with the exact duplicate merge of its 14 all-binary
+windows (KSVM_NFFT_DEDUP=1, the default: 8 distinct points per window, one
+cell holding ~364k points) and without it (=0: heavy-cell item splitting at
+full n). Bar: relative l2 <= 1e-10 (BASELINE north_star).
+"""
+import os
+import threading
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2312_00538_b200 import AnovaKernelSpec, Dataset, FeatureWindowing, anova_fast_operator, workloads
+
+pytestmark = pytest.mark.gpu
+
+_CACHE = {}
+
+
+def workload(cfg):
+    if cfg not in _CACHE:
+        _CACHE.clear()  # config 5 is 2.2 GB of points: keep one workload alive
+        _CACHE[cfg] = workloads.make(cfg)
+    return _CACHE[cfg]
+
+
+def reference_lib():
+    if oracle.available("ref"):
+        return oracle.Lib("ref")
+    if not oracle.available("oracle"):
+        oracle.build()
+    return oracle.Lib("oracle")
+
+
+def reference_matvec(w, v):
+    """P:src/fastsum.cpp:345-352 with each window's transform on its own thread."""
+    lib = reference_lib()
+    P = len(w.windows)
+    parts = [None] * P
+    errs = []
+
+    def one(l):
+        try:
+            cols = np.ascontiguousarray(w.points[:, w.windows[l]])
+            plan = lib.plan(cols, ell=1.0, fit=w.fit_fraction)
+            parts[l] = plan.apply(v)
+            del plan
+        except Exception as e:  # surfaced on the main thread
+            errs.append(e)
+
+    threads = [threading.Thread(target=one, args=(l,)) for l in range(P)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    if errs:
+        raise errs[0]
+    out = np.zeros(w.n)
+    for l in range(P):  # window order, eta_l = 1/P (P:src/pipeline.cpp:241)
+        out += (1.0 / P) * parts[l]
+    return out
+
+
+def gpu_matvec(w, v):
+    op = anova_fast_operator(Dataset(w.points), AnovaKernelSpec(FeatureWindowing.explicit(w.windows)),
+                             fit_fraction=w.fit_fraction)
+    y = op.apply(v)
+    pts = [op.window_points(l) for l in range(len(w.windows))]
+    del op
+    return y, pts
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def test_config3_full_size_vs_reference():
+    w = workload(3)
+    assert w.n == 100_000
+    y, _ = gpu_matvec(w, w.v)
+    assert rel(y, reference_matvec(w, w.v)) <= 1e-10
+
+
+@pytest.mark.parametrize("dedup", ["1", "0"])
+def test_config4_full_size_vs_reference(dedup, monkeypatch):
+    monkeypatch.setenv("KSVM_NFFT_DEDUP", dedup)
+    w = workload(4)
+    assert w.n == 500_000
+    y, pts = gpu_matvec(w, w.v)
+    merged = sum(1 for p in pts if p < w.n)
+    if dedup == "1":
+        assert merged >= 14  # the all-binary windows run on their distinct points
+    else:
+        assert merged == 0
+    assert rel(y, reference_matvec(w, w.v)) <= 1e-10
+
+
+def test_config5_full_size_vs_reference():
+    w = workload(5)
+    assert w.n == 10_000_000
+    y, _ = gpu_matvec(w, w.v)
+    ref = reference_matvec(w, w.v)
+    assert np.all(np.isfinite(y))
+    assert rel(y, ref) <= 1e-10
+    # and entrywise on a deterministic sample (no cancellation hides a bad block)
+    idx = np.random.default_rng(5).choice(w.n, 20000, replace=False)
+    assert np.max(np.abs(y[idx] - ref[idx])) <= 1e-9 * np.max(np.abs(ref))

@@ -1,5 +1,7 @@
 """GPU: BASELINE configs at full size, checked through size-independent
-properties (the oracle is too slow at these n) plus a dense spot check.
+properties plus a dense spot check. (Full-size 1e-10 parity against the
+reference's own fastsum for configs 3, 4 and 5 is in
+tests/test_gpu_fullsize_parity.py; these properties complement it.)
 
 * bit-identical re-application (P:tests/test_fastsum.cpp:208-215),
 * linearity and the symmetry of the bilinear form (:177-189),
