@@ -569,3 +569,95 @@ def nystrom_window(pts, feats, ell, rank, mode, seed, ldl_threshold=1e-8, N=32, 
     if code != 0:
         raise OracleError(code, L.oracle_nystrom_last_error().decode())
     return Z.reshape(-1, n)[: int(rank)]
+
+
+# --- the reference's own host driver (oracle/driver, oracle/_ref/libdriver_*.so) ---
+class Driver:
+    """The reference's train_pipeline / gmres_solve compiled unmodified by path
+    (P:src/{dataset,windowing,kernel,low_rank,saddle,ipm,pipeline}.cpp)
+    against oracle/shim2, with either the reference's own fastsum.cpp
+    (kind "cpu") or the drop-in paper_2312_00538_b200/cpp/ksvm_fastsum_gpu.cpp
+    on libksvm_nfft.so (kind "gpu")."""
+
+    PRECOND = {"none": 0, "cholesky-greedy": 1, "nystrom-gaussian": 4}
+
+    def __init__(self, kind: str = "cpu"):
+        path = os.path.join(HERE, "_ref", f"libdriver_{kind}.so")
+        if not os.path.exists(path):
+            raise FileNotFoundError(path + " (built by `make -C oracle` where /root/reference exists)")
+        self.L = C.CDLL(path)
+        self.L.drv_last_error.restype = C.c_char_p
+        self.L.drv_train_pipeline.restype = C.c_int
+        self.L.drv_train_pipeline.argtypes = [_dp, _dp, C.c_int64, C.c_int, C.c_char_p, C.c_int, C.c_int,
+                                              C.c_double, C.c_uint64, C.c_int, _dp, _dp, _dp, _dp]
+        self.L.drv_train_steps.restype = C.c_int
+        self.L.drv_train_steps.argtypes = [_dp, _dp, C.c_int64, C.c_int, C.c_char_p, C.c_int, C.c_int, C.c_double,
+                                           C.c_uint64, _dp, _dp, _dp, _dp, C.c_int]
+        self.L.drv_gmres.restype = C.c_int
+        self.L.drv_gmres.argtypes = [_dp, C.c_int64, C.c_int, C.c_char_p, _dp, _dp, _dp, C.c_int, _dp,
+                                     C.c_double, C.c_int, _dp, _dp]
+
+    @staticmethod
+    def available(kind: str) -> bool:
+        return os.path.exists(os.path.join(HERE, "_ref", f"libdriver_{kind}.so"))
+
+    def _check(self, code):
+        if code != 0:
+            raise OracleError(code, self.L.drv_last_error().decode())
+
+    def train_pipeline(self, points, labels, windows, precond="cholesky-greedy", rank=200, C_=1.0, seed=0,
+                       fast=True):
+        """ksvm::train_pipeline; returns a dict with the TrainReport fields, the
+        dual objective, alpha, bias and the held-out split's decision values
+        and labels."""
+        X = _f64(points)
+        n, d = X.shape
+        lab = _f64(labels)
+        spec = windows if isinstance(windows, str) else ";".join(",".join(str(f) for f in w) for w in windows)
+        scal = np.zeros(12)
+        alpha = np.zeros(n)
+        dec = np.zeros(n)
+        tl = np.zeros(n)
+        self._check(self.L.drv_train_pipeline(_ptr(X), _ptr(lab), n, d, spec.encode(), self.PRECOND[precond],
+                                              int(rank), float(C_), int(seed), 1 if fast else 0, _ptr(scal),
+                                              _ptr(alpha), _ptr(dec), _ptr(tl)))
+        ntr, nte = int(scal[0]), int(scal[1])
+        return {"n_train": ntr, "n_test": nte, "ipm_iters": int(scal[2]), "mean_gmres": scal[3],
+                "status": int(scal[4]), "rank": int(scal[5]), "xi_alpha": scal[6], "xi_lambda": scal[7],
+                "mu_final": scal[8], "dual_objective": scal[9], "bias": scal[10], "dual_feasibility": scal[11],
+                "alpha": alpha[:ntr].copy(), "test_decision": dec[:nte].copy(), "test_labels": tl[:nte].copy()}
+
+    def train_steps(self, points, labels, windows, precond="cholesky-greedy", rank=200, C_=1.0, seed=0):
+        """train_on_prepared's steps on the reference's functions (fast
+        backend), with the per-Newton-step log: rows (mu, xi_alpha_rel,
+        xi_lambda_rel, step_alpha, gmres_iterations, gmres_converged)."""
+        X = _f64(points)
+        n, d = X.shape
+        spec = windows if isinstance(windows, str) else ";".join(",".join(str(f) for f in w) for w in windows)
+        scal = np.zeros(12)
+        alpha = np.zeros(n)
+        dec = np.zeros(n)
+        log = np.zeros(6 * 64)
+        self._check(self.L.drv_train_steps(_ptr(X), _ptr(_f64(labels)), n, d, spec.encode(), self.PRECOND[precond],
+                                           int(rank), float(C_), int(seed), _ptr(scal), _ptr(alpha), _ptr(dec),
+                                           _ptr(log), 64))
+        ntr, nte, its = int(scal[0]), int(scal[1]), int(scal[2])
+        return {"n_train": ntr, "n_test": nte, "ipm_iters": its, "mean_gmres": scal[3], "status": int(scal[4]),
+                "rank": int(scal[5]), "xi_alpha": scal[6], "xi_lambda": scal[7], "mu_final": scal[8],
+                "dual_objective": scal[9], "bias": scal[10], "lambda": scal[11], "alpha": alpha[:ntr].copy(),
+                "test_decision": dec[:nte].copy(), "log": log[:6 * its].reshape(its, 6).copy()}
+
+    def gmres(self, points, windows, y, theta, Z, rhs, tol=1e-3, max_iter=100):
+        """ksvm::gmres_solve on the fast operator (fit 1/1.2) with the
+        reference's SaddlePreconditioner of the stacked factor Z (k x n)."""
+        X = _f64(points)
+        n, d = X.shape
+        spec = windows if isinstance(windows, str) else ";".join(",".join(str(f) for f in w) for w in windows)
+        k = 0 if Z is None else int(np.asarray(Z).shape[0])
+        Zc = _f64(Z) if k else np.zeros(1)
+        x = np.zeros(n + 1)
+        scal = np.zeros(4)
+        self._check(self.L.drv_gmres(_ptr(X), n, d, spec.encode(), _ptr(_f64(y)), _ptr(_f64(theta)), _ptr(Zc), k,
+                                     _ptr(_f64(rhs)), float(tol), int(max_iter), _ptr(x), _ptr(scal)))
+        return x, {"iterations": int(scal[0]), "relative_residual": scal[1], "converged": bool(scal[2]),
+                   "diagonal_fallback": bool(scal[3])}

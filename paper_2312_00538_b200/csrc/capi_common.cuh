@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <atomic>
 #include <cstdint>
@@ -84,6 +85,19 @@ struct DevBuf {
         alloc(count);
         CK(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, st));
     }
+};
+
+// NVTX range (header-only NVTX3; a no-op unless a profiler such as Nsight
+// Systems is attached). The apply path brackets each stage - spread_dK
+// (spread, tile pre-reduction, node reduction), grid_dK (the convolution
+// stages), gather_dK, combine - and the host-pointer copies (h2d / d2h), so a
+// timeline shows the per-stage host enqueue and, under graph replay, the
+// apply as one range. Stage GPU times: ksvm_nfft_op_set_stage_timing.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 struct DeviceGuard {

@@ -944,6 +944,7 @@ struct Engine {
         const int cnt = class_end[D] - class_begin[D];
         if (cnt == 0) return;
         if (ph & kPhSpread) {
+        NvtxRange nr(kSpread[D]);
         tick(kSpread[D]);
         launch_spread(D, 2 * cfg.window_cutoff, class_PE[D], d_items.p + class_begin[D], cnt, PS(),
                       WINS(), v, PATCHES(),
@@ -971,6 +972,8 @@ struct Engine {
         }
         }  // spread phase
         if (ph & kPhGrid) {
+        static const char* kGridR[4] = {"", "grid_d1", "grid_d2", "grid_d3"};
+        NvtxRange nr(kGridR[D]);
         if (grid_conv_only[D]) {
             tick("conv_d3");
             launch_grid_fused(WINS(), d_slots.p + slot_begin[D], nslots_cls[D], D, grid_nc[D], grid_lg[D],
@@ -991,6 +994,7 @@ struct Engine {
         }
         }  // grid phase
         if (ph & kPhGather) {
+            NvtxRange nr(kGather[D]);
             const int gcnt = gclass_end[D] - gclass_begin[D];
             tick(kGather[D]);
             if (gather_columns[D]) {
@@ -1069,6 +1073,7 @@ struct Engine {
         }
         nticks = 0;
         run_classes(v, true);
+        NvtxRange nr("combine");
         tick("combine");
         launch_combine(y, SRC(), d_inv.p, d_inv8.p, d_nu8.p, d_eta.p, P, n, S());
         ++launch_counter();
@@ -1223,6 +1228,7 @@ struct Engine {
 
     // One apply: replays a captured graph (one launch) or captures it first.
     void apply(const double* v, double* y) {
+        NvtxRange nr("ksvm_nfft_apply");
         (void)cudaGetLastError();  // a stale error must not be blamed on this apply
         if (!use_graphs || P_owned() == 0) {
             run_apply(v, y);
@@ -1280,8 +1286,12 @@ struct Engine {
         DeviceGuard dg(device);
         std::lock_guard<std::mutex> lk(mu);
         if (ptr_kind == KSVM_NFFT_HOST) {
-            if (vin > 0) CK(cudaMemcpyAsync(vbuf.p, v, sizeof(double) * vin, cudaMemcpyHostToDevice, stream));
+            {
+                NvtxRange nr("h2d");
+                if (vin > 0) CK(cudaMemcpyAsync(vbuf.p, v, sizeof(double) * vin, cudaMemcpyHostToDevice, stream));
+            }
             body(vbuf.p, ybuf.p);
+            NvtxRange nr("d2h");
             if (yout > 0) CK(cudaMemcpyAsync(y, ybuf.p, sizeof(double) * yout, cudaMemcpyDeviceToHost, stream));
             CK(cudaStreamSynchronize(stream));
         } else if (ptr_kind == KSVM_NFFT_DEVICE) {

@@ -253,18 +253,57 @@ __device__ __forceinline__ void spread3_epilogue(const double* smem, const DWin&
 // rest of the group is masked to zero and handled next round).
 // Lane l = 4g + t: A[g][t] = U[(r, g), point t], B[t][g] = W2[point t][g],
 // accumulator tile r holds G[(r, g), 2t..2t+1].
+//
+// Staging rows are kRow3 = 26 doubles (13 16-byte chunks; 13 is odd, so the
+// 8 rows a quarter warp stores land in 8 different chunk slots mod 8 and the
+// 128-bit staging stores are bank-conflict free; the 4 rows a group reads
+// are distinct chunk slots too). The run structure of a 32-point batch
+// (which points continue the cell of their predecessor) is one ballot, so
+// the DMMA loop carries no shared-memory loads of cell codes; a batch that
+// lies entirely in the current cell (the common case for dense data) runs
+// eight unmasked groups with no control flow.
 // ===========================================================================
-template <int W>
+constexpr int kRow3 = 26;  // w0[8] | w1[8] | w2[8] | {code, perm}
+
+// Power rows of one point, written as 128-bit pairs: w0[o] = P Q0^o,
+// w1[o] = Q1^o, w2[o] = Q2^o (the per-node factor R[o] is applied at flush /
+// halo load), then {code, perm}. Same product sequence as stage_pow.
+__device__ __forceinline__ void stage_pow3(double* st, double P, const double* Q, int code, int perm) {
+    double2* s2 = reinterpret_cast<double2*>(st);
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+        double q0 = t == 0 ? P : 1.0;
+#pragma unroll
+        for (int o = 0; o < 8; o += 2) {
+            const double q1 = q0 * Q[t];
+            s2[(t * 8 + o) >> 1] = make_double2(q0, q1);
+            if (o + 2 < 8) q0 = q1 * Q[t];
+        }
+    }
+    *reinterpret_cast<int2*>(st + 24) = make_int2(code, perm);
+}
+
+// Length of the run of same-cell points starting at p: bit q of `same` says
+// point q continues the cell of point q - 1.
+__device__ __forceinline__ int run_len(unsigned same, int p) {
+    const unsigned s = p + 1 < 32 ? (same >> (p + 1)) : 0u;
+    return __ffs(~s);  // 1 + number of consecutive set bits above p
+}
+
+template <int W, int B>
 __global__ void __launch_bounds__(W * 32)
 spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
                   const DWin* __restrict__ wins, const double* __restrict__ v,
                   double* __restrict__ patches) {
-    constexpr int D = 3, S = 8, PE = 11, PV = PE * PE * PE, RL = Row<D, S>::kLen;
+    constexpr int S = 8, PE = 11, PV = PE * PE * PE, RL = kRow3;
+    constexpr unsigned kFull = 0xffffffffu;
     extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
     double* wp = smem + warp * PV;
-    double* stage = smem + ((W * PV + 1) & ~1) + warp * 32 * RL;
+    static_assert(B == 16 || B == 32, "points per staging batch");
+    constexpr unsigned kBatch = B == 32 ? kFull : (1u << B) - 1u;
+    double* stage = smem + ((W * PV + 1) & ~1) + warp * B * RL;
 
     pdl_trigger();
     const Item it = items[blockIdx.x];
@@ -274,9 +313,9 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     for (int k = lane; k < PV; k += 32) wp[k] = 0.0;
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
-    Pref<D> pa, pb;  // plan data: prefetched before the dependency wait
-    if (wb + lane < we) pa.load(ps, wb + lane);
-    if (wb + 32 + lane < we) pb.load(ps, wb + 32 + lane);
+    Pref<3> pa, pb;  // plan data: prefetched before the dependency wait
+    if (lane < B && wb + lane < we) pa.load(ps, wb + lane);
+    if (lane < B && wb + B + lane < we) pb.load(ps, wb + B + lane);
 
     double acc[8][2];
 #pragma unroll
@@ -292,8 +331,22 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
             acc[r][0] = acc[r][1] = 0.0;
         }
     };
-    // 4 points of the current cell (lane t carries point p0 + t), no masking
-    auto group4 = [&](int p0) {
+    // 4 points p0..p0+3 of the current cell; lanes t >= nv contribute zero
+    auto group4 = [&](int p0, int nv) {
+        const bool valid = t < nv;
+        const double* st = stage + (p0 + (valid ? t : 0)) * RL;
+        const double2 w01 = ld2(st), w23 = ld2(st + 2), w45 = ld2(st + 4), w67 = ld2(st + 6);
+        const double w1g = valid ? st[S + g] : 0.0, bq = valid ? st[2 * S + g] : 0.0;
+        dmma(acc[0][0], acc[0][1], w01.x * w1g, bq);
+        dmma(acc[1][0], acc[1][1], w01.y * w1g, bq);
+        dmma(acc[2][0], acc[2][1], w23.x * w1g, bq);
+        dmma(acc[3][0], acc[3][1], w23.y * w1g, bq);
+        dmma(acc[4][0], acc[4][1], w45.x * w1g, bq);
+        dmma(acc[5][0], acc[5][1], w45.y * w1g, bq);
+        dmma(acc[6][0], acc[6][1], w67.x * w1g, bq);
+        dmma(acc[7][0], acc[7][1], w67.y * w1g, bq);
+    };
+    auto group4f = [&](int p0) {  // unmasked
         const double* st = stage + (p0 + t) * RL;
         const double2 w01 = ld2(st), w23 = ld2(st + 2), w45 = ld2(st + 4), w67 = ld2(st + 6);
         const double w1g = st[S + g], bq = st[2 * S + g];
@@ -313,45 +366,44 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
         const int i0 = wb + lane;
         pdl_wait();  // v may come from the previous kernel (plan factors above did not)
         v = launder(v);
-        if (i0 < we) va = __ldcg(v + pa.perm);
+        if (lane < B && i0 < we) va = __ldcg(v + pa.perm);
     }
     __syncwarp();
-    for (int base = wb; base < we; base += 32) {
-        const int cnt = min(32, we - base);
-        if (lane < cnt) stage_pow<D, S>(stage + lane * RL, pa.P * va, pa.Q, pa.code);
+    for (int base = wb; base < we; base += B) {
+        const int cnt = min(B, we - base);
+        const int code = pa.code;
+        if (lane < cnt) stage_pow3(stage + lane * RL, pa.P * va, pa.Q, code, 0);
+        const int prev = __shfl_up_sync(kFull, code, 1);
+        const unsigned same = __ballot_sync(kFull, lane < cnt && code == (lane == 0 ? cur : prev));
         pa = pb;
-        if (base + 32 + lane < we) va = __ldcg(v + pa.perm);
-        if (base + 64 + lane < we) pb.load(ps, base + 64 + lane);
+        if (lane < B && base + B + lane < we) va = __ldcg(v + pa.perm);
+        if (lane < B && base + 2 * B + lane < we) pb.load(ps, base + 2 * B + lane);
         __syncwarp();
-        int p = 0;
-        while (p < cnt) {
-            const int cp = row_code(stage + p * RL, D, S);
-            if (cp != cur) {
-                if (cur >= 0) flush(cur);
-                cur = cp;
+        if (same == kBatch) {  // the whole batch continues the current cell
+#pragma unroll
+            for (int q = 0; q < B / 4; ++q) group4f(4 * q);
+        } else {
+            int p = 0;
+            while (p < cnt) {
+                if (!((same >> p) & 1u)) {  // a new cell starts at p
+                    if (cur >= 0) flush(cur);
+                    cur = __shfl_sync(kFull, code, p);
+                }
+                int L = run_len(same, p);
+                for (; L >= 8; L -= 8, p += 8) {
+                    group4f(p);
+                    group4f(p + 4);
+                }
+                if (L >= 4) {
+                    group4f(p);
+                    p += 4;
+                    L -= 4;
+                }
+                if (L > 0) {
+                    group4(p, L);
+                    p += L;
+                }
             }
-            if (p + 7 < cnt && row_code(stage + (p + 7) * RL, D, S) == cur) {
-                group4(p);  // 8 points of one cell (sorted): two unmasked rounds
-                group4(p + 4);
-                p += 8;
-                continue;
-            }
-            const int q = p + t;
-            const bool valid = q < cnt && row_code(stage + q * RL, D, S) == cur;
-            const int nvalid = __popc(__ballot_sync(0xffffffffu, valid) & 0xFu);
-            const double* st = stage + (valid ? q : p) * RL;
-            const double w1g = valid ? st[S + g] : 0.0;
-            const double b = valid ? st[2 * S + g] : 0.0;
-            const double2 w01 = ld2(st), w23 = ld2(st + 2), w45 = ld2(st + 4), w67 = ld2(st + 6);
-            dmma(acc[0][0], acc[0][1], w01.x * w1g, b);
-            dmma(acc[1][0], acc[1][1], w01.y * w1g, b);
-            dmma(acc[2][0], acc[2][1], w23.x * w1g, b);
-            dmma(acc[3][0], acc[3][1], w23.y * w1g, b);
-            dmma(acc[4][0], acc[4][1], w45.x * w1g, b);
-            dmma(acc[5][0], acc[5][1], w45.y * w1g, b);
-            dmma(acc[6][0], acc[6][1], w67.x * w1g, b);
-            dmma(acc[7][0], acc[7][1], w67.y * w1g, b);
-            p += nvalid;
         }
         __syncwarp();
     }
@@ -513,17 +565,26 @@ spread3c_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pse
 // Gather, d = 3, m = 4, on the FP64 tensor cores, 8 same-cell points per round:
 //   Z[p, c] = sum_{(a,b)} U[p, (a,b)] H[(a,b), c],  U[p, (a,b)] = P_p w0_p[a] w1_p[b]
 //   y_p     = sum_c Z[p, c] w2_p[c]
-// M = 8 points, N = c, K = 64 (a,b) pairs in 16 k-steps of 4, split over four
-// accumulators (fixed combine order). Lane l = 4g + t: A[g][t] = U[point g,
-// (k/2, 4(k%2)+t)] (one DMUL each), B[t][g] = H[(k/2, 4(k%2)+t), c=g] (16
-// values, reloaded per cell), D holds Z[point g][2t..2t+1]; the c-sum is a
-// 2-step xor over t.
+// M = 8 points, N = c, K = 64 (a,b) pairs in 16 k-steps of 4, split over two
+// accumulators (dependent DMMAs two issues apart, past the DMMA latency;
+// fixed combine order). Lane l = 4g + t: A[g][t] = U[point g, (k/2,
+// 4(k%2)+t)] (one DMUL each), B[t][g] = H[(k/2, 4(k%2)+t), c=g] (16 values,
+// reloaded per cell), D holds Z[point g][2t..2t+1]; the c-sum is a 2-step
+// xor over t. (Contracting dimension 0 on the tensor cores with A = P w0
+// directly and dimensions 1, 2 per point needs fewer FP64 instructions, 20
+// vs 22 per 16 DMMA, but measured 5 % slower: 3.95 vs 3.75 ms at config 5.)
+//
+// Staging as in spread3_s8 (kRow3 rows, conflict-free 128-bit stores), row =
+// P w0[0..7] | (w1[t], w1[t+4]) pairs | w2[0..7] | {code, perm}; runs of
+// same-cell points come from one ballot per batch and a batch entirely in
+// the current cell runs four unmasked 8-point rounds.
 // ===========================================================================
 template <int W>
 __global__ void __launch_bounds__(W * 32, 4)
 gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
-                  const DWin* __restrict__ wins) {
-    constexpr int D = 3, S = 8, TC = 4, PE = TC + S - 1, PV = PE * PE * PE, RL = Row<D, S>::kLen;
+                   const DWin* __restrict__ wins) {
+    constexpr int S = 8, TC = 4, PE = TC + S - 1, PV = PE * PE * PE, RL = kRow3;
+    constexpr unsigned kFull = 0xffffffffu;
     extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane >> 2, t = lane & 3;
@@ -535,20 +596,19 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     const DPSet ps = psets[it.ps];
     const DWin& wn = wins[ps.win];
     int tc[3];
-    tile_coords(it.tile, D, wn.ntile, tc);
+    tile_coords(it.tile, 3, wn.ntile, tc);
     __shared__ double sR[PE];
     if (threadIdx.x < PE) sR[threadIdx.x] = wn.R[threadIdx.x];
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
-    Pref<D> pa, pb;  // factors of the current and the next batch (plan data: before the wait)
+    Pref<3> pa, pb;
     if (wb + lane < we) pa.load(ps, wb + lane);
     if (wb + 32 + lane < we) pb.load(ps, wb + 32 + lane);
     __syncthreads();
     pdl_wait();
-    load_halo3_r<PE, TC>(halo, *launder(&wn), tc, sR);  // H: written by the grid kernels
+    load_halo3_r<PE, TC>(halo, *launder(&wn), tc, sR);
     __syncthreads();
 
-    // B fragments: hb[k] = H[(k/2, 4(k%2)+t), c = g] of the current cell
     double hb[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) hb[k] = 0.0;
@@ -559,42 +619,73 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
 #pragma unroll
         for (int k = 0; k < 16; ++k) hb[k] = src[(k >> 1) * PE * PE + 4 * (k & 1) * PE];
     };
+    auto group8 = [&](int p0, int nv) {
+        const bool vg = g < nv;
+        const double* sg = stage + (p0 + (vg ? g : 0)) * RL;
+        const double2 w01 = ld2(sg), w23 = ld2(sg + 2), w45 = ld2(sg + 4), w67 = ld2(sg + 6);
+        const double w0[8] = {w01.x, w01.y, w23.x, w23.y, w45.x, w45.y, w67.x, w67.y};
+        const double2 uu = ld2(sg + S + 2 * t);
+        const double u0 = vg ? uu.x : 0.0, u1 = vg ? uu.y : 0.0;
+        const double2 w2 = ld2(sg + 2 * S + 2 * t);
+        double z[2][2] = {{0, 0}, {0, 0}};
+#pragma unroll
+        for (int k = 0; k < 16; ++k) dmma(z[k & 1][0], z[k & 1][1], w0[k >> 1] * ((k & 1) ? u1 : u0), hb[k]);
+        const double z0 = z[0][0] + z[1][0], z1 = z[0][1] + z[1][1];
+        double part = fma(z0, w2.x, z1 * w2.y);
+        part += __shfl_xor_sync(kFull, part, 1);
+        part += __shfl_xor_sync(kFull, part, 2);
+        if (t == 0 && vg) ps.out[reinterpret_cast<const int*>(sg + 24)[1]] = part;
+    };
 
     for (int base = wb; base < we; base += 32) {
         const int cnt = min(32, we - base);
+        const int code = pa.code;
         if (lane < cnt) {
-            double* st = stage + lane * RL;
-            stage_pow<D, S>(st, pa.P, pa.Q, pa.code);
-            reinterpret_cast<int*>(st + D * S)[1] = pa.perm;
+            double2* s2 = reinterpret_cast<double2*>(stage + lane * RL);
+            double q = pa.P;
+#pragma unroll
+            for (int o = 0; o < 8; o += 2) {
+                const double q1 = q * pa.Q[0];
+                s2[o >> 1] = make_double2(q, q1);
+                if (o + 2 < 8) q = q1 * pa.Q[0];
+            }
+            double w1[8];
+            w1[0] = 1.0;
+#pragma unroll
+            for (int o = 1; o < 8; ++o) w1[o] = w1[o - 1] * pa.Q[1];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) s2[4 + j] = make_double2(w1[j], w1[j + 4]);
+            q = 1.0;
+#pragma unroll
+            for (int o = 0; o < 8; o += 2) {
+                const double q1 = q * pa.Q[2];
+                s2[8 + (o >> 1)] = make_double2(q, q1);
+                if (o + 2 < 8) q = q1 * pa.Q[2];
+            }
+            *reinterpret_cast<int2*>(stage + lane * RL + 24) = make_int2(code, pa.perm);
         }
+        const int prev = __shfl_up_sync(kFull, code, 1);
+        const unsigned same = __ballot_sync(kFull, lane < cnt && code == (lane == 0 ? cur : prev));
         pa = pb;
         if (base + 64 + lane < we) pb.load(ps, base + 64 + lane);
         __syncwarp();
-        int p = 0;
-        while (p < cnt) {
-            const int cp = row_code(stage + p * RL, D, S);
-            if (cp != cur) {
-                cur = cp;
-                reload(cp);
-            }
-            const int qg = p + g;
-            const bool vg = qg < cnt && row_code(stage + qg * RL, D, S) == cur;
-            const int nvalid = __popc(__ballot_sync(0xffffffffu, vg) & 0x11111111u);
-            const double* sg = stage + (vg ? qg : p) * RL;
-            const double2 w01 = ld2(sg), w23 = ld2(sg + 2), w45 = ld2(sg + 4), w67 = ld2(sg + 6);
-            const double w0[8] = {w01.x, w01.y, w23.x, w23.y, w45.x, w45.y, w67.x, w67.y};
-            const double u0 = vg ? sg[S + t] : 0.0, u1 = vg ? sg[S + 4 + t] : 0.0;
-            const double2 w2 = ld2(sg + 2 * S + 2 * t);
-            double z[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+        if (same == kFull) {
 #pragma unroll
-            for (int k = 0; k < 16; ++k) dmma(z[k & 3][0], z[k & 3][1], w0[k >> 1] * ((k & 1) ? u1 : u0), hb[k]);
-            const double z0 = (z[0][0] + z[1][0]) + (z[2][0] + z[3][0]);
-            const double z1 = (z[0][1] + z[1][1]) + (z[2][1] + z[3][1]);
-            double part = fma(z0, w2.x, z1 * w2.y);
-            part += __shfl_xor_sync(0xffffffffu, part, 1);
-            part += __shfl_xor_sync(0xffffffffu, part, 2);
-            if (t == 0 && vg) ps.out[reinterpret_cast<const int*>(sg + D * S)[1]] = part;
-            p += nvalid;
+            for (int q = 0; q < 4; ++q) group8(8 * q, 8);
+        } else {
+            int p = 0;
+            while (p < cnt) {
+                if (!((same >> p) & 1u)) {
+                    cur = __shfl_sync(kFull, code, p);
+                    reload(cur);
+                }
+                for (int L = run_len(same, p); L > 0;) {
+                    const int nv = min(L, 8);
+                    group8(p, nv);
+                    p += nv;
+                    L -= nv;
+                }
+            }
         }
         __syncwarp();
     }
@@ -1750,8 +1841,8 @@ constexpr int kW1 = 8;
 
 size_t gather3c_smem() { return sizeof(double) * (8 * 121 + 4 * 32 * kCol3Row); }
 size_t spread3c_smem() { return sizeof(double) * (kColWarps * (kCol3Sub + 32 * kCol3Row)); }
-size_t spread3_smem() { return sizeof(double) * (((kW3 * 1331 + 1) & ~1) + kW3 * 32 * Row<3, 8>::kLen); }
-size_t gather3_smem() { return sizeof(double) * (1332 + kW3 * 32 * Row<3, 8>::kLen); }
+size_t spread3_smem(int B) { return sizeof(double) * (((kW3 * 1331 + 1) & ~1) + kW3 * B * kRow3); }
+size_t gather3_smem() { return sizeof(double) * (1332 + kW3 * 32 * kRow3); }
 size_t spread2_smem() { return sizeof(double) * (((kW2 * 225 + 1) & ~1) + kW2 * 32 * Row<2, 8>::kLen); }
 size_t gather2_smem() { return sizeof(double) * (226 + kW2 * 32 * Row<2, 8>::kLen); }
 size_t spread1_smem() { return sizeof(double) * (kW1 * 39 * 32); }
@@ -1782,7 +1873,8 @@ cudaError_t init_kernel_attributes() {
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
     };
-    set(reinterpret_cast<const void*>(spread3_s8_kernel<kW3>), spread3_smem());
+    set(reinterpret_cast<const void*>(spread3_s8_kernel<kW3, 32>), spread3_smem(32));
+    set(reinterpret_cast<const void*>(spread3_s8_kernel<kW3, 16>), spread3_smem(16));
     set(reinterpret_cast<const void*>(spread3c_s8_kernel), spread3c_smem());
     set(reinterpret_cast<const void*>(gather3c_s8_kernel), gather3c_smem());
     set(reinterpret_cast<const void*>(gather3_s8_kernel<kW3>), gather3_smem());
@@ -1808,8 +1900,18 @@ void launch_spread(int D, int S, int PE, const Item* items, int nitems, const DP
         if (D == 3 && colb)
             launch_k(spread3c_s8_kernel, dim3(nitems), dim3(kColWarps * 32), spread3c_smem(), st, items, ps, wins, v,
                      patches, colb);
-        else if (D == 3)
-            launch_k(spread3_s8_kernel<kW3>, dim3(nitems), dim3(kW3 * 32), spread3_smem(), st, items, ps, wins, v, patches);
+        else if (D == 3) {
+            static const int B = [] {  // points per staging batch (A/B knob, default 32)
+                const char* e = std::getenv("KSVM_NFFT_S3B");
+                return e && std::atoi(e) == 16 ? 16 : 32;
+            }();
+            if (B == 16)
+                launch_k(spread3_s8_kernel<kW3, 16>, dim3(nitems), dim3(kW3 * 32), spread3_smem(16), st, items, ps,
+                         wins, v, patches);
+            else
+                launch_k(spread3_s8_kernel<kW3, 32>, dim3(nitems), dim3(kW3 * 32), spread3_smem(32), st, items, ps,
+                         wins, v, patches);
+        }
         else if (D == 2)
             launch_k(spread2_s8_kernel<kW2>, dim3(nitems), dim3(kW2 * 32), spread2_smem(), st, items, ps, wins, v, patches);
         else

@@ -15,6 +15,7 @@ import numpy as np
 import pytest
 
 import oracle
+from pipeline_oracle import oracle_pipeline
 from paper_2312_00538_b200 import (AnovaKernelSpec, Dataset, FeatureWindowing, IpmConfig, IpmStatus,
                                    PipelineConfig, anova_fast_operator, compute_bias, dual_objective, ipm_train,
                                    train_pipeline, workloads)
@@ -108,26 +109,6 @@ def test_compute_bias_rules_match_oracle():
     rng = np.random.default_rng(0)
     for alpha in (rng.uniform(0, 1, 120), np.where(rng.random(120) < 0.5, 1.0, 0.0), np.zeros(120)):
         assert abs(compute_bias(alpha, y, K, 1.0, 1e-4) - oracle.compute_bias(Ko, alpha, y, 1.0, 1e-4)) <= 1e-10
-
-
-def oracle_pipeline(w, windows, rank, C, seed=0, precond="cholesky-greedy"):
-    """train_pipeline restated on the oracle pieces (P:src/pipeline.cpp:229-265)."""
-    tr, te = oracle.balance_and_split(w.labels, 0.5, seed)
-    Xtr, Xte, mu, sd = oracle.zscore(w.points[tr], w.points[te])
-    ytr = w.labels[tr]
-    P = len(windows)
-    if precond == "cholesky-greedy":
-        Zs = [oracle.pivoted_cholesky(Xtr, windows, window=l, rank=max(1, rank // P), err_tol=1e-5)[0]
-              for l in range(P)]
-    else:
-        mode = oracle.NYSTROM_GAUSSIAN if precond == "nystrom-gaussian" else oracle.NYSTROM_COLUMNS
-        Zs = [oracle.nystrom_window(Xtr, windows[l], 1.0, max(1, rank // P), mode, seed + l) for l in range(P)]
-    Z = np.vstack([np.sqrt(1.0 / P) * z for z in Zs])
-    Ko = oracle.Lib("oracle").anova(Xtr, windows, fit=FIT)
-    alpha, res, log = oracle.ipm_train(Ko, ytr, Z, C=C)
-    b = oracle.compute_bias(Ko, alpha, ytr, C, 1e-4 * C)
-    f, _ = oracle.decision_values(Xtr, windows, [1.0 / P] * P, [1.0] * P, alpha * ytr, b, Xte, fast=True)
-    return dict(tr=tr, te=te, alpha=alpha, res=res, log=log, bias=b, f=f, Ko=Ko, ytr=ytr, Z=Z)
 
 
 @pytest.mark.parametrize("precond", ["cholesky-greedy", "nystrom-gaussian", "nystrom-columns"])
