@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--n", type=int, default=None, help="override n (debug only)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--precision", choices=["fp64", "fp32"], default="fp64",
+                    help="fp32: north_star's optional fp32 mode (d = 3 windows in fp32, <= 1e-5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
     return ap.parse_args()
@@ -250,16 +252,17 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------ GPU arm ------
-def kernel_bytes(w, name, pts):
+def kernel_bytes(w, name, pts, word=8):
     """Algorithmic HBM bytes of one launch (SURVEY.md 8(d) split per kernel):
     spread_dK reads the coordinates of its windows + v once; gather_dK reads
     the coordinates + writes y once. pts[l] = points window l is evaluated
-    on (n, or its distinct points after the exact duplicate merge)."""
+    on (n, or its distinct points after the exact duplicate merge). word = 4
+    for the fp32 mode's d = 3 kernels (B32 = 4 n (2D + 2))."""
     if not (name.startswith("spread_d") or name.startswith("gather_d")):
         return 0
     k = int(name[-1])
     sel = [(len(x), p) for x, p in zip(w.windows, pts) if len(x) == k and p > 0]
-    return 8 * (sum(d * p for d, p in sel) + max((p for _, p in sel), default=0))
+    return word * (sum(d * p for d, p in sel) + max((p for _, p in sel), default=0))
 
 
 def kernel_fmas(w, name, pts, m=4):
@@ -270,10 +273,14 @@ def kernel_fmas(w, name, pts, m=4):
     return sum(p * (2 * m) ** len(x) for x, p in zip(w.windows, pts) if len(x) == k)
 
 
-def fp64_peak_tflops(dev):
+def fp64_peak_tflops(dev, dtype=None):
+    """cuBLAS GEMM 8192^3 measured in this run: DGEMM (FP64 tensor cores), or
+    with dtype=float32 SGEMM with TF32 disabled (the FFMA datapath)."""
     import torch
-    a = torch.randn(8192, 8192, dtype=torch.float64, device=dev)
-    b = torch.randn(8192, 8192, dtype=torch.float64, device=dev)
+    dtype = dtype or torch.float64
+    torch.backends.cuda.matmul.allow_tf32 = False
+    a = torch.randn(8192, 8192, dtype=dtype, device=dev)
+    b = torch.randn(8192, 8192, dtype=dtype, device=dev)
     for _ in range(2):
         torch.matmul(a, b)
     torch.cuda.synchronize(dev)
@@ -330,7 +337,8 @@ def run_ours(args):
     mask = sharding.window_mask(owner, rank) if world > 1 else None
     os.environ.setdefault("KSVM_NFFT_QUIET", "1")
     op = anova_fast_operator(Dataset(w.points), spec, fit_fraction=w.fit_fraction, device=local,
-                             window_mask=mask)
+                             window_mask=mask, precision=args.precision)
+    f32 = args.precision == "fp32"
     v = torch.from_numpy(w.v).to(dev)
     y = torch.empty_like(v)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
@@ -416,20 +424,23 @@ def run_ours(args):
         roof = None
         if dom is not None:
             ms = per_launch[dom]
-            ach = kernel_bytes(w, dom, pts) / (ms * 1e-3) / 1e9
+            word = 4 if (f32 and dom.endswith("3")) else 8
+            ach = kernel_bytes(w, dom, pts, word) / (ms * 1e-3) / 1e9
             traffic = None
             try:
                 with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-                    traffic = json.load(f).get(f"cfg{args.config}", {}).get(dom)
+                    key = f"cfg{args.config}" + ("_fp32" if f32 else "")
+                    traffic = json.load(f).get(key, {}).get(dom)
             except Exception:
                 pass
-            fpk = fp64_peak_tflops(dev)
+            fpk = fp64_peak_tflops(dev, torch.float32 if word == 4 else torch.float64)
             tflops = 2 * kernel_fmas(w, dom, pts) / (ms * 1e-3) / 1e12
-            roof = {"bound": "fp64", "kernel": dom, "achieved": tflops, "peak": fpk, "unit": "TFLOP/s",
-                    "frac": tflops / fpk,
-                    "peak_source": "cuBLAS DGEMM 8192^3 (torch.matmul f64) measured in this run",
-                    "per_launch": {"fma": kernel_fmas(w, dom, pts), "algorithmic_bytes": kernel_bytes(w, dom, pts),
-                                   "ms": ms},
+            roof = {"bound": "fp32" if word == 4 else "fp64", "kernel": dom, "achieved": tflops, "peak": fpk,
+                    "unit": "TFLOP/s", "frac": tflops / fpk,
+                    "peak_source": ("cuBLAS SGEMM 8192^3 (torch.matmul f32, TF32 off) measured in this run"
+                                    if word == 4 else "cuBLAS DGEMM 8192^3 (torch.matmul f64) measured in this run"),
+                    "per_launch": {"fma": kernel_fmas(w, dom, pts),
+                                   "algorithmic_bytes": kernel_bytes(w, dom, pts, word), "ms": ms},
                     "traffic": traffic,
                     "hbm": {"achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
                             "peak_source": peak_kind},
@@ -439,11 +450,12 @@ def run_ours(args):
         step_ms = total_ms / K
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
                 "warmup": max(3, args.warmup), "ms_per_step": step_ms, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32" if f32 else "f64", "data": "synthetic",
                 "config": config_dict(w, args.config),
+                "precision": args.precision,
                 "parallelism": f"window-sharded x{world} + NCCL allreduce" if world > 1 else "1 GPU",
                 "dedup": {str(l): p for l, p in enumerate(pts) if 0 < p < w.n},
-                "hbm_fraction_matvec": (w.hbm_bytes() / (step_ms * 1e-3) / 1e9) / peaks()[0],
+                "hbm_fraction_matvec": (w.hbm_bytes(4 if f32 else 8) / (step_ms * 1e-3) / 1e9) / peaks()[0],
                 "per_launch_ms": per_launch,
                 "per_launch_sum_ms": sum(per_launch.values()),
                 "roofline": roof,
@@ -451,6 +463,8 @@ def run_ours(args):
                 "gpu_launches": launches,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * w.n,
                         "d2h_bytes_per_step": 8 * w.n}}
+        if f32:
+            line["metric"] = METRIC.replace("(fp64)", "(fp32 mode)")
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(w, args.cpu_budget_s)
         if world == 1:

@@ -80,7 +80,12 @@ enum {
 
 enum { KSVM_NFFT_ROW_MAJOR = 0, KSVM_NFFT_COL_MAJOR = 1 };
 enum { KSVM_NFFT_HOST = 0, KSVM_NFFT_DEVICE = 1 };
-enum { KSVM_NFFT_FP64 = 0 };
+/* precision of ksvm_nfft_op_create / _create_sharded. FP32 (north_star's
+ * optional fp32 mode, <= 1e-5 relative l2 against the fp64 reference): the
+ * d = 3, m = 4 windows spread and gather with fp32 window weights and fp32
+ * FFMA accumulation (cell-relative factors, 16 B per point); d <= 2 windows,
+ * the grid stage and the window sum stay fp64; v and y are fp64 either way. */
+enum { KSVM_NFFT_FP64 = 0, KSVM_NFFT_FP32 = 1 };
 
 /* FastsumConfig (P:include/ksvm/fastsum.hpp:13-20). */
 typedef struct {

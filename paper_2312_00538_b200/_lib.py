@@ -16,6 +16,7 @@ OK, ERR_DATA, ERR_CONFIG, ERR_INTERNAL = 0, 2, 4, 5
 ROW_MAJOR, COL_MAJOR = 0, 1
 HOST, DEVICE = 0, 1
 FP64 = 0
+FP32 = 1  # optional fp32 mode (include/ksvm_nfft.h)
 PREDICT_EXACT, PREDICT_FAST = 0, 1
 
 

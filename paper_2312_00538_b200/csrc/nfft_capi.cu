@@ -68,6 +68,14 @@ void launch_cell_keys(const double* x0, const double* x1, const double* x2, int 
 void launch_factors(const double* x0, const double* x1, const double* x2, const int* perm, int d,
                     long long n, double Mf, int m, double invb, double Cw, int cmin, int TC,
                     int tile_rel, double4* F, int2* CP, cudaStream_t st);
+// fp32 mode of the d = 3, m = 4 spread / gather (nfft_f32.cu)
+cudaError_t init_f32_attributes();
+void launch_spread3_f32(const Item* items, int nitems, const DPSet* ps, const DWin* wins, const double* v,
+                        double* patches, cudaStream_t st);
+void launch_gather3_f32(const Item* items, int nitems, const DPSet* ps, const DWin* wins, cudaStream_t st);
+void launch_factors32(const double* x0, const double* x1, const double* x2, const int* perm, long long n,
+                      double Mf, int m, double invb, double Cw, int cmin, int TC, float4* F, int2* CP,
+                      cudaStream_t st);
 
 namespace {
 
@@ -78,6 +86,7 @@ void ensure_attributes(int dev) {
     if (dev >= 0 && dev < 256 && !done[static_cast<size_t>(dev)]) {
         CK(init_kernel_attributes());
         CK(init_fused_attributes());
+        CK(init_f32_attributes());
         done[static_cast<size_t>(dev)] = true;
     }
 }
@@ -147,6 +156,7 @@ struct PointSet {
     int64_t n = 0;
     int d = 0;
     DevBuf<double4> F;  // window factors {P, Q0, Q1, Q2}, sorted order (nfft_engine.cuh)
+    DevBuf<float4> F32; // fp32 mode (d = 3, m = 4): cell-relative factors instead of F (nfft_f32.cu)
     DevBuf<int2> CP;    // {tile-local cell code, original index}
     DevBuf<int> perm;
     std::vector<Item> items;      // spread items (one patch each; global numbering later)
@@ -270,7 +280,8 @@ Geometry geometry(const ksvm_nfft_config& c, int d, const double* range = nullpt
 
 // Sort a point set by (tile, cell) on the device and split tiles into items.
 void build_pointset(PointSet& ps, const std::vector<double>& scaled_cm, int64_t n, int d,
-                    const Geometry& g, int64_t chunk_points, int64_t gather_chunk, cudaStream_t st) {
+                    const Geometry& g, int64_t chunk_points, int64_t gather_chunk, cudaStream_t st,
+                    bool f32 = false) {
     ps.n = n;
     ps.d = d;
     DevBuf<double> raw[3];
@@ -298,11 +309,17 @@ void build_pointset(PointSet& ps, const std::vector<double>& scaled_cm, int64_t 
     tmp.alloc(tmp_bytes);
     CK(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, keys_in.p, keys_out.p, idx_in.p,
                                        ps.perm.p, static_cast<int>(n), 0, bits, st));
-    ps.F.alloc(n);
     ps.CP.alloc(n);
+    ps.F.alloc(n);
     launch_factors(raw[0].p, d > 1 ? raw[1].p : nullptr, d > 2 ? raw[2].p : nullptr, ps.perm.p, d, n,
                    static_cast<double>(g.M), g.m, g.invb, g.Cw, g.cmin, g.TC,
                    /*tile_rel=*/(d == 3 && g.S == 8) ? 1 : 0, ps.F.p, ps.CP.p, st);
+    if (f32) {  // fp32 mode (d = 3, m = 4): cell-relative float factors too; the
+                // engine keeps one of F / F32 once it knows the class density
+        ps.F32.alloc(n);
+        launch_factors32(raw[0].p, raw[1].p, raw[2].p, ps.perm.p, n, static_cast<double>(g.M), g.m, g.invb,
+                         g.Cw, g.cmin, g.TC, ps.F32.p, ps.CP.p, st);
+    }
     CK(cudaGetLastError());
     std::vector<unsigned> hk(static_cast<size_t>(n));
     int hbad = 0;
@@ -442,6 +459,15 @@ struct Engine {
     bool stage_timing = false;
     ksvm_nfft_config cfg{};
     double fit = 1.0;
+    int precision = KSVM_NFFT_FP64;
+    // fp32 mode covers the d = 3, m = 4 windows with dense cells (the
+    // FP64-bound part). Sparse-cell classes are latency-bound and keep the
+    // fp64 column kernels (faster there; exact, so within the 1e-5 contract);
+    // KSVM_NFFT_F32=all forces the fp32 kernels on them too. d <= 2 windows,
+    // the grid side and the window sum stay fp64.
+    bool f32_want(int D) const { return precision == KSVM_NFFT_FP32 && D == 3 && cfg.window_cutoff == 4; }
+    bool f32_dense[4] = {false, false, false, false};  // decided in finalize()
+    bool f32_class(int D) const { return f32_dense[D]; }
     int64_t n = 0;
     int64_t dfull = 0;
     std::vector<std::unique_ptr<Window>> wins;  // all windows, window order
@@ -620,7 +646,7 @@ struct Engine {
                 for (int64_t r = 0; r < no; ++r)
                     so[static_cast<size_t>(t * no + r)] = sc[static_cast<size_t>(t * n + own_idx[static_cast<size_t>(r)])];
             build_pointset(w.src, so, no, d, g, item_chunk(no * n_owned_windows, d),
-                           gather_chunk(no * n_owned_windows, d), stream);
+                           gather_chunk(no * n_owned_windows, d), stream, f32_want(d));
             // point-set indices are local to the owned rows: map them to global ones
             std::vector<int2> cp(static_cast<size_t>(no));
             CK(cudaMemcpyAsync(cp.data(), w.src.CP.p, sizeof(int2) * cp.size(), cudaMemcpyDeviceToHost, stream));
@@ -658,11 +684,11 @@ struct Engine {
                 w.inv.upload(inv.data(), inv.size(), stream);
             }
             build_pointset(w.src, su, nu, d, g, item_chunk(n * n_owned_windows, d),
-                           gather_chunk(n * n_owned_windows, d), stream);
+                           gather_chunk(n * n_owned_windows, d), stream, f32_want(d));
         } else {
             w.nu = 0;
             build_pointset(w.src, sc, n, d, g, item_chunk(n * n_owned_windows, d),
-                           gather_chunk(n * n_owned_windows, d), stream);
+                           gather_chunk(n * n_owned_windows, d), stream, f32_want(d));
         }
 
         DWin& dw = w.dw;
@@ -755,8 +781,18 @@ struct Engine {
                 }
             }
             class_end[D] = static_cast<int>(all.size());
-            spread_columns[D] = D == 3 && use_columns(D, "KSVM_NFFT_SPREAD3");
-            gather_columns[D] = D == 3 && use_columns(D, "KSVM_NFFT_GATHER3");
+            if (f32_want(D)) {
+                const char* fe = std::getenv("KSVM_NFFT_F32");
+                f32_dense[D] = (fe && std::strcmp(fe, "all") == 0) || !use_columns(D, "KSVM_NFFT_F32_DENSITY");
+                for (int s = 0; s < P; ++s) {  // keep the factors the chosen kernels read
+                    Window& w = *wins[static_cast<size_t>(owned[static_cast<size_t>(s)])];
+                    if (w.d != D) continue;
+                    if (f32_dense[D]) w.src.F.reset();
+                    else w.src.F32.reset();
+                }
+            }
+            spread_columns[D] = D == 3 && !f32_class(D) && use_columns(D, "KSVM_NFFT_SPREAD3");
+            gather_columns[D] = D == 3 && !f32_class(D) && use_columns(D, "KSVM_NFFT_GATHER3");
             gclass_begin[D] = static_cast<int>(gall.size());
             for (int s = 0; s < P; ++s) {
                 Window& w = *wins[static_cast<size_t>(owned[static_cast<size_t>(s)])];
@@ -844,6 +880,7 @@ struct Engine {
             eta[static_cast<size_t>(s)] = w.eta;
             DPSet& p = ps[static_cast<size_t>(s)];
             p.F = w.src.F.p;
+            p.F32 = w.src.F32.p;
             p.CP = w.src.CP.p;
             p.win = s;
             if (w.nu > 0 && w.nu <= kSmallBins) {
@@ -946,10 +983,13 @@ struct Engine {
         if (ph & kPhSpread) {
         NvtxRange nr(kSpread[D]);
         tick(kSpread[D]);
-        launch_spread(D, 2 * cfg.window_cutoff, class_PE[D], d_items.p + class_begin[D], cnt, PS(),
-                      WINS(), v, PATCHES(),
-                      spread_columns[D] ? d_colb.p + static_cast<size_t>(class_begin[D]) * kColBounds : nullptr,
-                      st);
+        if (f32_class(D))
+            launch_spread3_f32(d_items.p + class_begin[D], cnt, PS(), WINS(), v, PATCHES(), st);
+        else
+            launch_spread(D, 2 * cfg.window_cutoff, class_PE[D], d_items.p + class_begin[D], cnt, PS(),
+                          WINS(), v, PATCHES(),
+                          spread_columns[D] ? d_colb.p + static_cast<size_t>(class_begin[D]) * kColBounds : nullptr,
+                          st);
         ++launch_counter();
         if (n_multi_cls[D]) {
             tick("tile_reduce");
@@ -997,7 +1037,9 @@ struct Engine {
             NvtxRange nr(kGather[D]);
             const int gcnt = gclass_end[D] - gclass_begin[D];
             tick(kGather[D]);
-            if (gather_columns[D]) {
+            if (f32_class(D)) {
+                launch_gather3_f32(d_gitems.p + gclass_begin[D], gcnt, PS(), WINS(), st);
+            } else if (gather_columns[D]) {
                 launch_gather3c(d_items.p + class_begin[D], cnt, PS(), WINS(),
                                 d_colb.p + static_cast<size_t>(class_begin[D]) * kColBounds, st);
             } else {
@@ -1329,7 +1371,8 @@ void build_engine(Engine& E, const double* points, int64_t n, int64_t d, int64_t
     if (!points || !feats || !sizes || !weights || !ells || !cfg)
         throw std::invalid_argument("null argument");
     validate_cfg(*cfg);
-    if (precision != KSVM_NFFT_FP64) throw std::invalid_argument("only KSVM_NFFT_FP64 is supported");
+    if (precision != KSVM_NFFT_FP64 && precision != KSVM_NFFT_FP32)
+        throw std::invalid_argument("precision must be KSVM_NFFT_FP64 or KSVM_NFFT_FP32");
     if (n < 1) throw std::invalid_argument("empty node set");
     if (n > 2147483647LL) throw std::invalid_argument("n must be < 2^31");
     if (!(fit > 0.0 && fit <= 1.0)) throw std::invalid_argument("fit_fraction must lie in (0, 1]");
@@ -1359,6 +1402,7 @@ void build_engine(Engine& E, const double* points, int64_t n, int64_t d, int64_t
     E.init(device);
     E.cfg = *cfg;
     E.fit = fit;
+    E.precision = precision;
     E.data_range = data_range;
     E.n = n;
     if (own) {  // point shard: owned rows, strictly ascending, in [0, n)

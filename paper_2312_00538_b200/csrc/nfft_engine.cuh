@@ -74,6 +74,7 @@ struct DWin {
 // A sorted point set (a window's sources, or cross-apply targets).
 struct DPSet {
     const double4* F;    // {P, Q0, Q1, Q2}: P = (pi b)^{-d/2} exp(-sum u^2/b), Q_t = exp(2 u_t/b)
+    const float4* F32;   // fp32 mode, d = 3, m = 4: cell-relative {P, Q0, Q1, Q2} (nfft_f32.cu); else null
     const int2* CP;      // {tile-local cell code sum_t (c_t mod TC) TC^{d-1-t}, original index}
     long long n;
     int win;             // owning window slot

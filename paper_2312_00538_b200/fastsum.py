@@ -267,11 +267,13 @@ class AnovaFastOperator(KernelOperator):
     ``window_mask`` (list of bools, one per window) restricts the windows
     whose fast applies run here (multi-GPU window sharding, see
     :mod:`paper_2312_00538_b200.sharding`); ``apply`` then returns the partial
-    sum over the owned windows.
+    sum over the owned windows. ``precision`` is "fp64" (default) or "fp32"
+    (north_star's optional fp32 mode: the d = 3 windows spread and gather in
+    fp32, <= 1e-5 relative l2 against the fp64 reference).
     """
 
     def __init__(self, data, spec: AnovaKernelSpec, cfg: Optional[FastsumConfig] = None,
-                 fit_fraction: float = 1.0, device: int = 0, window_mask=None):
+                 fit_fraction: float = 1.0, device: int = 0, window_mask=None, precision: str = "fp64"):
         cfg = cfg or FastsumConfig()
         pts = data.points if hasattr(data, "points") else data
         a = _host_matrix(pts)
@@ -293,8 +295,9 @@ class AnovaFastOperator(KernelOperator):
         h = C.c_void_p()
         _raise(_lib.load().ksvm_nfft_op_create(C.c_void_p(a.ctypes.data), n, d, d, _lib.ROW_MAJOR, feats,
                                                sizes, P, eta, ell, C.byref(c), float(fit_fraction), mask,
-                                               int(device), _lib.FP64, C.byref(h)))
+                                               int(device), _precision(precision), C.byref(h)))
         self._h = h
+        self.precision = precision
         self._free = _lib.load().ksvm_nfft_op_free  # kept: module globals may be gone in __del__
         self._apply_fn = _lib.load().ksvm_nfft_op_apply
         self._n = n
@@ -401,10 +404,18 @@ class AnovaFastOperator(KernelOperator):
         return out
 
 
+def _precision(p: str) -> int:
+    table = {"fp64": _lib.FP64, "fp32": _lib.FP32}
+    if p not in table:
+        raise ValueError("precision must be 'fp64' or 'fp32'")
+    return table[p]
+
+
 def anova_fast_operator(data, spec: AnovaKernelSpec, cfg: Optional[FastsumConfig] = None,
-                        fit_fraction: float = 1.0, device: int = 0, window_mask=None) -> AnovaFastOperator:
+                        fit_fraction: float = 1.0, device: int = 0, window_mask=None,
+                        precision: str = "fp64") -> AnovaFastOperator:
     """anova_fast_operator (P:src/fastsum.cpp:366-371) on cuda:`device`."""
-    return AnovaFastOperator(data, spec, cfg, fit_fraction, device, window_mask)
+    return AnovaFastOperator(data, spec, cfg, fit_fraction, device, window_mask, precision)
 
 
 # ---- prediction (SURVEY.md 8(f)4) -------------------------------------------

@@ -123,10 +123,11 @@ class PointShardedOperator:
     (``matvec(v, y, allreduce)`` does exactly that). v and y are CUDA tensors
     on the operator's device (torch's current stream) or numpy arrays."""
 
-    def __init__(self, data, spec, own_points, cfg=None, fit_fraction: float = 1.0, device: int = 0):
+    def __init__(self, data, spec, own_points, cfg=None, fit_fraction: float = 1.0, device: int = 0,
+                 precision: str = "fp64"):
         import ctypes as C
         from . import _lib
-        from .fastsum import FastsumConfig, _host_matrix, _raise
+        from .fastsum import FastsumConfig, _host_matrix, _precision, _raise
         cfg = cfg or FastsumConfig()
         a = _host_matrix(data.points if hasattr(data, "points") else data)
         n, d = a.shape
@@ -142,7 +143,7 @@ class PointShardedOperator:
         _raise(_lib.load().ksvm_nfft_op_create_sharded(C.c_void_p(a.ctypes.data), n, d, d, _lib.ROW_MAJOR, feats, sizes,
                                                        P, eta, ell, C.byref(c), float(fit_fraction),
                                                        C.c_void_p(own.ctypes.data), own.shape[0], int(device),
-                                                       _lib.FP64, C.byref(h)))
+                                                       _precision(precision), C.byref(h)))
         self._h, self._n, self.device, self.own = h, n, int(device), own
         self._free = _lib.load().ksvm_nfft_op_free
 
