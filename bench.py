@@ -61,6 +61,14 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--precision", choices=["fp64", "fp32"], default="fp64",
                     help="fp32: north_star's optional fp32 mode (d = 3 windows in fp32, <= 1e-5)")
+    ap.add_argument("--shard", choices=["windows", "points"], default="windows",
+                    help="N > 1: windows (north_star: LPT window sharding, one chunked all-reduce of y, "
+                         "overlapped with the window sum) or points (SURVEY 8(e) hybrid: one all-reduce of "
+                         "the grid pool, one all-gather of y)")
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl")
+    ap.add_argument("--same-device", action="store_true",
+                    help="every rank on cuda:0 (exercises the N > 1 path on a 1-GPU lease; use --backend gloo)")
+    ap.add_argument("--chunks", type=int, default=4, help="row chunks of the pipelined y all-reduce")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
     return ap.parse_args()
@@ -325,28 +333,45 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if args.same_device else int(os.environ.get("LOCAL_RANK", "0"))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+    allreduce, allreduce_async, allgather = sharding.make_collectives(args.backend)
 
     w = workloads.make(args.config, args.n)
     spec = AnovaKernelSpec(FeatureWindowing.explicit(w.windows))
-    owner = sharding.lpt_assign(sharding.window_costs(w.windows, points=w.points), world)
-    mask = sharding.window_mask(owner, rank) if world > 1 else None
     os.environ.setdefault("KSVM_NFFT_QUIET", "1")
-    op = anova_fast_operator(Dataset(w.points), spec, fit_fraction=w.fit_fraction, device=local,
-                             window_mask=mask, precision=args.precision)
     f32 = args.precision == "fp32"
     v = torch.from_numpy(w.v).to(dev)
-    y = torch.empty_like(v)
+    points_mode = world > 1 and args.shard == "points"
+    if points_mode:
+        # SURVEY.md 8(e) hybrid: every rank plans all windows from all points
+        # and spreads / gathers its block of rows
+        op = sharding.PointShardedOperator(Dataset(w.points), spec, sharding.point_block(w.n, world, rank),
+                                           fit_fraction=w.fit_fraction, device=local, precision=args.precision)
+        blk = -(-w.n // world)
+        y_pad = torch.zeros(world * blk, dtype=torch.float64, device=dev)
+        y = y_pad[:w.n]
+    else:
+        owner = sharding.lpt_assign(sharding.window_costs(w.windows, points=w.points), world)
+        mask = sharding.window_mask(owner, rank) if world > 1 else None
+        op = anova_fast_operator(Dataset(w.points), spec, fit_fraction=w.fit_fraction, device=local,
+                                 window_mask=mask, precision=args.precision)
+        y = torch.empty_like(v)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def step():
-        op.apply_into(v, y)
-        if world > 1:
-            dist.all_reduce(y)
+        if points_mode:
+            op.matvec_blocks(v, y_pad, rank, world, allreduce, allgather)
+        elif world > 1:
+            sharding.pipelined_matvec(op, v, y, args.chunks, allreduce_async)
+        else:
+            op.apply_into(v, y)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -376,15 +401,19 @@ def run_ours(args):
     value = K / (total_ms * 1e-3)
 
     # --- per-launch timing pass (same flush discipline) for the roofline ----
-    op.set_stage_timing(True)
-    acc = {}
-    for k in range(K):
-        flush.zero_()
-        step()
-        for name, ms in op.last_stage_ms().items():
-            acc[name] = acc.get(name, 0.0) + ms
-    op.set_stage_timing(False)
-    per_launch = {k2: v2 / K for k2, v2 in acc.items()}
+    # (one rank's own windows; point-sharded ranks run two phases with a
+    # collective between them, so they report no per-launch split)
+    per_launch = {}
+    if not points_mode:
+        op.set_stage_timing(True)
+        acc = {}
+        for k in range(K):
+            flush.zero_()
+            op.apply_into(v, y)
+            for name, ms in op.last_stage_ms().items():
+                acc[name] = acc.get(name, 0.0) + ms
+        op.set_stage_timing(False)
+        per_launch = {k2: v2 / K for k2, v2 in acc.items()}
 
     # --- end-to-end through the public API with host buffers ---------------
     vh = torch.from_numpy(w.v).pin_memory()
@@ -418,7 +447,8 @@ def run_ours(args):
 
     if rank == 0:
         hbm_peak, peak_kind = peaks()
-        pts = [op.window_points(l) for l in range(len(w.windows))]
+        pts = ([w.n] * len(w.windows) if points_mode else
+               [op.window_points(l) for l in range(len(w.windows))])
         dom = max((k2 for k2 in per_launch if kernel_bytes(w, k2, pts) > 0), key=lambda k2: per_launch[k2],
                   default=None)
         roof = None
@@ -453,7 +483,11 @@ def run_ours(args):
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32" if f32 else "f64", "data": "synthetic",
                 "config": config_dict(w, args.config),
                 "precision": args.precision,
-                "parallelism": f"window-sharded x{world} + NCCL allreduce" if world > 1 else "1 GPU",
+                "parallelism": ("1 GPU" if world == 1 else
+                                (f"point-sharded x{world}: grid-pool all-reduce + y all-gather ({args.backend})"
+                                 if points_mode else
+                                 f"window-sharded x{world} (LPT) + {args.chunks}-chunk pipelined y all-reduce "
+                                 f"({args.backend})")) + (", ranks share cuda:0" if args.same_device else ""),
                 "dedup": {str(l): p for l, p in enumerate(pts) if 0 < p < w.n},
                 "hbm_fraction_matvec": (w.hbm_bytes(4 if f32 else 8) / (step_ms * 1e-3) / 1e9) / peaks()[0],
                 "per_launch_ms": per_launch,

@@ -204,6 +204,26 @@ int ksvm_nfft_op_create_sharded(const double* points, int64_t n, int64_t d, int6
 int ksvm_nfft_op_apply_spread(ksvm_nfft_op* op, const double* v, int ptr_kind, void* stream);
 int ksvm_nfft_op_grids(const ksvm_nfft_op* op, double** grids, int64_t* lengths, int max_grids);
 int ksvm_nfft_op_apply_finish(ksvm_nfft_op* op, double* y, int ptr_kind, void* stream);
+/* The owned windows' grids G of a point-sharded operator as ONE contiguous
+ * device buffer (the concatenation ksvm_nfft_op_grids lists, window order):
+ * the ranks sum it with a single all-reduce per matvec. */
+int ksvm_nfft_op_grid_pool(const ksvm_nfft_op* op, double** pool, int64_t* length);
+
+/* ---- window-sharded matvec, pipelined with the cross-rank sum -------------
+ * with windows sharded over GPUs (window_mask), the length-n
+ * partial sums are all-reduced once per matvec. Splitting the apply lets the
+ * caller overlap that all-reduce with the window sum:
+ *   ksvm_nfft_op_apply_windows(op, v)          spread / grid / gather of every
+ *                                              owned window (per-window outputs)
+ *   for each row range [lo, hi):
+ *     ksvm_nfft_op_combine_range(op, y, lo, hi)  y[lo:hi) = sum_l eta_l out_l
+ *     all-reduce y[lo:hi) (async, e.g. NCCL)   overlaps the next range's sum
+ * Both take device pointers (ptr_kind KSVM_NFFT_DEVICE) and are ordered on
+ * `stream` like ksvm_nfft_op_apply; y[lo:hi) equals ksvm_nfft_op_apply's rows
+ * bit for bit. Replaces nothing in the reference (single process). */
+int ksvm_nfft_op_apply_windows(ksvm_nfft_op* op, const double* v, int ptr_kind, void* stream);
+int ksvm_nfft_op_combine_range(ksvm_nfft_op* op, double* y, int64_t lo, int64_t hi, int ptr_kind,
+                               void* stream);
 
 /* ---- Newton saddle system, GPU resident ----------------
  * The IPM's inner solve, A [v; w] = [Y K Y v + Theta v - w y; -y^T v] with K

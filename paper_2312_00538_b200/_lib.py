@@ -91,6 +91,9 @@ _SIGS = {
     "ksvm_nfft_op_apply_spread": (C.c_int, [_vp, _vp, C.c_int, _vp]),
     "ksvm_nfft_op_grids": (C.c_int, [_vp, _vp, _vp, C.c_int]),
     "ksvm_nfft_op_apply_finish": (C.c_int, [_vp, _vp, C.c_int, _vp]),
+    "ksvm_nfft_op_grid_pool": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(C.c_int64)]),
+    "ksvm_nfft_op_apply_windows": (C.c_int, [_vp, _vp, C.c_int, _vp]),
+    "ksvm_nfft_op_combine_range": (C.c_int, [_vp, _vp, C.c_int64, C.c_int64, C.c_int, _vp]),
     "ksvm_nfft_op_device": (C.c_int, [_vp]),
     # Newton saddle system
     "ksvm_nfft_saddle_create": (C.c_int, [_vp, _vp, _vp, C.POINTER(_vp)]),

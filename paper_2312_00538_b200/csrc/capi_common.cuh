@@ -69,6 +69,16 @@ struct DevBuf {
         o.p = nullptr;
         o.n = 0;
     }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            reset();
+            p = o.p;
+            n = o.n;
+            o.p = nullptr;
+            o.n = 0;
+        }
+        return *this;
+    }
     ~DevBuf() { reset(); }
     void reset() {
         if (p) cudaFree(p);

@@ -53,7 +53,7 @@ void launch_grid_fused(const DWin* wins, const int* slots, int nslots, int D, in
                        const double* patches, cudaStream_t st, bool conv_only);
 
 void launch_combine(double* y, const double* const* src, const int* const* inv, const uint8_t* const* inv8,
-                    const int* nu8, const double* eta, int P, long long n, cudaStream_t st);
+                    const int* nu8, const double* eta, int P, long long lo, long long hi, cudaStream_t st);
 void launch_bin_sums(const double* v, const uint8_t* const* codes, int nwl, long long n, double* partial,
                      int nblk, const long long* vs_off, const int* nu, double* vs, cudaStream_t st);
 void launch_seg_sums(const double* v, const int* members, const int2* chunks, double* partial, int C,
@@ -492,6 +492,8 @@ struct Engine {
     int grid_nc[4] = {0, 0, 0, 0}, grid_lg[4] = {0, 0, 0, 0};
     DevBuf<double> d_eta;
     DevBuf<double> patches, parts, vbuf, ybuf;
+    DevBuf<double> gpool;  // point-sharded operators: the owned windows' grids G, contiguous
+    int64_t gpool_len = 0;
     // exact-duplicate windows (Window::nu): segmented sums of v and output maps
     DevBuf<int> seg_members, seg_cb;
     DevBuf<int2> seg_chunks;
@@ -542,6 +544,25 @@ struct Engine {
     }
 
     int P_owned() const { return static_cast<int>(owned.size()); }
+
+    // Device SoA copy of the raw window features (entries), built on first use.
+    std::mutex raw_mu;
+    void ensure_raw_device() {
+        std::lock_guard<std::mutex> lk(raw_mu);
+        if (d_raw.p) return;
+        DeviceGuard dg(device);
+        const size_t nc = raw_cols.size();
+        std::vector<double> soa(static_cast<size_t>(n) * nc);
+        for (int64_t i = 0; i < n; ++i)
+            for (size_t c = 0; c < nc; ++c) soa[c * static_cast<size_t>(n) + static_cast<size_t>(i)] = raw_rm[static_cast<size_t>(i) * nc + c];
+        DevBuf<double> buf;
+        buf.upload(soa.data(), soa.size(), stream);
+        std::vector<const double*> cols(nc);
+        for (size_t c = 0; c < nc; ++c) cols[c] = buf.p + c * static_cast<size_t>(n);
+        d_rawcols.upload(cols.data(), cols.size(), stream);
+        CK(cudaStreamSynchronize(stream));
+        d_raw = std::move(buf);
+    }
     int64_t n_owned_windows = 1;  // set before planning (item sizing)
     bool data_range = false;      // grid range from the data (self-apply only operators)
     // Point sharding (SURVEY.md 8(e) hybrid): this operator spreads / gathers
@@ -854,6 +875,28 @@ struct Engine {
                 grid_lg[D] = lg;
             }
         }
+        if (sharded()) {
+            // the owned windows' spread grids G in one contiguous pool, so the
+            // ranks sum them with ONE all-reduce (ksvm_nfft_op_grid_pool)
+            size_t total = 0;
+            for (int s = 0; s < P; ++s) {
+                const Window& w = *wins[static_cast<size_t>(owned[static_cast<size_t>(s)])];
+                long long nodes = 1;
+                for (int t = 0; t < w.d; ++t) nodes *= w.dw.Lg;
+                total += static_cast<size_t>(nodes);
+            }
+            gpool.alloc(std::max<size_t>(total, 1));
+            size_t off = 0;
+            for (int s = 0; s < P; ++s) {
+                Window& w = *wins[static_cast<size_t>(owned[static_cast<size_t>(s)])];
+                long long nodes = 1;
+                for (int t = 0; t < w.d; ++t) nodes *= w.dw.Lg;
+                w.G.reset();
+                w.dw.G = gpool.p + off;
+                off += static_cast<size_t>(nodes);
+            }
+            gpool_len = static_cast<int64_t>(total);
+        }
         parts.alloc(static_cast<size_t>(std::max(P, 1)) * n);
         if (sharded())  // gathers write the owned points only; the rest stays 0 for the combine
             CK(cudaMemsetAsync(parts.p, 0, sizeof(double) * parts.n, stream));
@@ -1101,7 +1144,27 @@ struct Engine {
     }
     void run_finish_phase(double* y) {
         for (int D = 3; D >= 1; --D) run_class_phases(D, nullptr, S(), kPhGrid | kPhGather);
-        launch_combine(y, SRC(), d_inv.p, d_inv8.p, d_nu8.p, d_eta.p, P_owned(), n, S());
+        launch_combine(y, SRC(), d_inv.p, d_inv8.p, d_nu8.p, d_eta.p, P_owned(), 0, n, S());
+        ++launch_counter();
+        CK(cudaGetLastError());
+    }
+
+    // Window-sharded multi-GPU pipeline (ksvm_nfft_op_apply_windows /
+    // _combine_range): every owned window's transform into its per-window
+    // output, then the window-order sum over row ranges, so the caller can
+    // all-reduce range k while range k+1 is being summed.
+    void run_windows(const double* v) {
+        nticks = 0;
+        if (P_owned() > 0) run_classes(v, true);
+        CK(cudaGetLastError());
+    }
+    void run_combine(double* y, int64_t lo, int64_t hi) {
+        if (P_owned() == 0) {
+            launch_fill(y + lo, 0.0, hi - lo, S());
+        } else {
+            NvtxRange nr("combine");
+            launch_combine(y, SRC(), d_inv.p, d_inv8.p, d_nu8.p, d_eta.p, P_owned(), lo, hi, S());
+        }
         ++launch_counter();
         CK(cudaGetLastError());
     }
@@ -1117,7 +1180,7 @@ struct Engine {
         run_classes(v, true);
         NvtxRange nr("combine");
         tick("combine");
-        launch_combine(y, SRC(), d_inv.p, d_inv8.p, d_nu8.p, d_eta.p, P, n, S());
+        launch_combine(y, SRC(), d_inv.p, d_inv8.p, d_nu8.p, d_eta.p, P, 0, n, S());
         ++launch_counter();
         CK(cudaGetLastError());
         tick("end");
@@ -1436,10 +1499,9 @@ void build_engine(Engine& E, const double* points, int64_t n, int64_t d, int64_t
             E.raw_rm[static_cast<size_t>(i * nc + c)] = x;
             soa[static_cast<size_t>(c) * n + i] = x;
         }
-    E.d_raw.upload(soa.data(), soa.size(), E.stream);
-    std::vector<const double*> cols(static_cast<size_t>(nc));
-    for (int c = 0; c < nc; ++c) cols[static_cast<size_t>(c)] = E.d_raw.p + static_cast<size_t>(c) * n;
-    E.d_rawcols.upload(cols.data(), cols.size(), E.stream);
+    // the device SoA copy is uploaded from raw_rm on first use (kernel rows /
+    // diagonal / preconditioner entries), so a matvec-only operator -- every
+    // rank of a sharded matvec -- holds no device copy of the raw features
     std::vector<int> wdim;
     for (auto& w : E.wins) wdim.push_back(w->d);
     E.d_wdim.upload(wdim.data(), wdim.size(), E.stream);
@@ -1586,7 +1648,7 @@ int ksvm_nfft_op_grids(const ksvm_nfft_op* op, double** grids, int64_t* lengths,
             if (count < max_grids && grids && lengths) {
                 long long nodes = 1;
                 for (int t = 0; t < w->d; ++t) nodes *= w->dw.Lg;
-                grids[count] = w->G.p;
+                grids[count] = w->dw.G;
                 lengths[count] = nodes;
             }
             ++count;
@@ -1601,6 +1663,38 @@ int ksvm_nfft_op_apply_finish(ksvm_nfft_op* op, double* y, int ptr_kind, void* s
         Engine& E = op->e;
         if (!E.sharded()) throw std::invalid_argument("apply_finish needs a point-sharded operator");
         E.with_io(nullptr, y, ptr_kind, stream, 0, E.n, [&](const double*, double* dy) { E.run_finish_phase(dy); });
+    });
+}
+
+int ksvm_nfft_op_grid_pool(const ksvm_nfft_op* op, double** pool, int64_t* length) {
+    return guarded([&] {
+        if (!op || !pool || !length) throw std::invalid_argument("null argument");
+        const Engine& E = op->e;
+        if (!E.sharded()) throw std::invalid_argument("the grid pool belongs to point-sharded operators");
+        *pool = E.gpool.p;
+        *length = E.gpool_len;
+    });
+}
+
+int ksvm_nfft_op_apply_windows(ksvm_nfft_op* op, const double* v, int ptr_kind, void* stream) {
+    return guarded([&] {
+        if (!op || !v) throw std::invalid_argument("null argument");
+        if (ptr_kind != KSVM_NFFT_DEVICE) throw std::invalid_argument("apply_windows takes device pointers");
+        Engine& E = op->e;
+        if (E.sharded()) throw std::invalid_argument("apply_windows is for window-sharded operators");
+        E.with_io(v, nullptr, ptr_kind, stream, E.n, 0, [&](const double* dv, double*) { E.run_windows(dv); });
+    });
+}
+
+int ksvm_nfft_op_combine_range(ksvm_nfft_op* op, double* y, int64_t lo, int64_t hi, int ptr_kind, void* stream) {
+    return guarded([&] {
+        if (!op || !y) throw std::invalid_argument("null argument");
+        if (ptr_kind != KSVM_NFFT_DEVICE) throw std::invalid_argument("combine_range takes device pointers");
+        Engine& E = op->e;
+        if (E.sharded()) throw std::invalid_argument("combine_range is for window-sharded operators");
+        if (lo < 0 || hi > E.n || lo > hi) throw std::invalid_argument("row range out of bounds");
+        if (lo == hi) return;
+        E.with_io(nullptr, y, ptr_kind, stream, 0, 0, [&](const double*, double* dy) { E.run_combine(dy, lo, hi); });
     });
 }
 
@@ -1705,6 +1799,7 @@ void op_entry_view(const ksvm_nfft_op* op, int window, EntryView& v) {
     v.mu = &E.mu;
     v.n = E.n;
     v.nw = window < 0 ? P : 1;
+    E.ensure_raw_device();
     v.cols = E.d_rawcols.p + c0;
     v.wdim = E.d_wdim.p + (window < 0 ? 0 : window);
     v.wgt.clear();
@@ -1740,6 +1835,7 @@ int ksvm_nfft_kernel_rows(const ksvm_nfft_op* op, int window, const int64_t* row
             wgt.push_back(window < 0 ? w.eta : -1.0);  // -1: plain exp (WindowOperator)
             ell2.push_back(w.ell * w.ell);
         }
+        E.ensure_raw_device();
         DeviceGuard dg(E.device);
         std::lock_guard<std::mutex> lk(E.mu);
         DevBuf<long long> drows;

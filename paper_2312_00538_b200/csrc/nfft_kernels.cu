@@ -1579,7 +1579,7 @@ conv_stage_kernel(const DWin* __restrict__ wins, const int* __restrict__ slots, 
 __global__ void __launch_bounds__(256)
 combine_kernel(double* __restrict__ y, const double* const* __restrict__ src,
                const int* const* __restrict__ inv, const uint8_t* const* __restrict__ inv8,
-               const int* __restrict__ nu8, const double* __restrict__ eta, int P, long long n) {
+               const int* __restrict__ nu8, const double* __restrict__ eta, int P, long long lo, long long n) {
     constexpr int kMaxP = 64;  // window table staged in SMEM (plan data, before the wait)
     __shared__ const double* s_src[kMaxP];
     __shared__ const int* s_inv[kMaxP];
@@ -1602,7 +1602,7 @@ combine_kernel(double* __restrict__ y, const double* const* __restrict__ src,
     const bool any_map = s_any != 0;
     pdl_wait();
     if (!any_map) {  // no duplicate-merged window: straight window-order sum
-        for (long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
+        for (long long j = lo + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
              j += static_cast<long long>(gridDim.x) * blockDim.x) {
             double acc = 0.0;
             for (int l = 0; l < P; ++l) acc += s_eta[l] * __ldcg(s_src[l] + j);
@@ -1615,7 +1615,7 @@ combine_kernel(double* __restrict__ y, const double* const* __restrict__ src,
         if (s_inv8[l] && u < nu8[l]) s_tab[l][u] = __ldcg(s_src[l] + u);  // outputs of this apply's gathers
     }
     __syncthreads();
-    for (long long j = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
+    for (long long j = lo + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; j < n;
          j += static_cast<long long>(gridDim.x) * blockDim.x) {
         double acc = 0.0;
 #pragma unroll 4
@@ -1991,10 +1991,13 @@ void launch_conv(const DWin* wins, const int* slots, int nslots, int Lg_max, lon
 
 int conv_max_lg() { return kConvMaxL; }
 
+// y[j] = sum_l eta_l out_l[j] for j in [lo, hi) (the whole vector: lo = 0, hi = n)
 void launch_combine(double* y, const double* const* src, const int* const* inv, const uint8_t* const* inv8,
-                    const int* nu8, const double* eta, int P, long long n, cudaStream_t st) {
-    const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 16));
-    launch_k(combine_kernel, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, st, y, src, inv, inv8, nu8, eta, P, n);
+                    const int* nu8, const double* eta, int P, long long lo, long long hi, cudaStream_t st) {
+    const long long len = hi - lo;
+    const int blocks = static_cast<int>(std::min<long long>((len + 255) / 256, 148LL * 16));
+    launch_k(combine_kernel, dim3(blocks > 0 ? blocks : 1), dim3(256), 0, st, y, src, inv, inv8, nu8, eta, P, lo,
+             hi);
 }
 
 void launch_bin_sums(const double* v, const uint8_t* const* codes, int nwl, long long n, double* partial,

@@ -344,6 +344,23 @@ class AnovaFastOperator(KernelOperator):
         _raise(_lib.load().ksvm_nfft_op_apply(self._h, C.c_void_p(v.data_ptr()), C.c_void_p(out.data_ptr()),
                                               _lib.DEVICE, st))
 
+    def apply_windows(self, v) -> None:
+        """First half of the pipelined window-sharded matvec: every owned
+        window's transform into its per-window output (CUDA tensor v)."""
+        if not _is_cuda_tensor(v):
+            raise ValueError("apply_windows takes a CUDA tensor")
+        st = C.c_void_p(torch.cuda.current_stream(v.device).cuda_stream)
+        _raise(_lib.load().ksvm_nfft_op_apply_windows(self._h, C.c_void_p(v.data_ptr()), _lib.DEVICE, st))
+
+    def combine_range(self, y, lo: int, hi: int) -> None:
+        """y[lo:hi] = sum_l eta_l out_l[lo:hi] over the owned windows (after
+        apply_windows); equal to apply's rows bit for bit."""
+        if not _is_cuda_tensor(y):
+            raise ValueError("combine_range takes a CUDA tensor")
+        st = C.c_void_p(torch.cuda.current_stream(y.device).cuda_stream)
+        _raise(_lib.load().ksvm_nfft_op_combine_range(self._h, C.c_void_p(y.data_ptr()), int(lo), int(hi),
+                                                      _lib.DEVICE, st))
+
     def apply_batch(self, V):
         """Y = K V for an n x k block (Nystrom sketch, P:src/low_rank.cpp:139-150)."""
         if _is_cuda_tensor(V):

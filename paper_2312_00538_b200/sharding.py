@@ -79,6 +79,68 @@ class ShardedAnovaOperator:
         return [l for l, o in enumerate(self.owner) if o == self.rank]
 
 
+def pipelined_matvec(op, v, y, chunks: int, allreduce_async: Callable) -> None:
+    """Window-sharded matvec with the cross-rank sum chunked and overlapped
+    (SURVEY.md 8(e) "chunk it and overlap"): the rank's windows run first
+    (``op.apply_windows``), then for each of `chunks` row ranges the window
+    sum of that range is launched and its all-reduce issued asynchronously,
+    so range k is on the wire while range k+1 is being summed. `op` is a
+    window-masked AnovaFastOperator, v / y CUDA tensors of length n;
+    ``allreduce_async(t)`` returns a handle with ``wait()`` (torch.distributed
+    ``all_reduce(..., async_op=True)``). Returns after every handle is waited."""
+    n = y.numel()
+    op.apply_windows(v)
+    handles = []
+    for k in range(chunks):
+        lo, hi = n * k // chunks, n * (k + 1) // chunks
+        if hi > lo:
+            op.combine_range(y, lo, hi)
+            handles.append(allreduce_async(y[lo:hi]))
+    for h in handles:
+        h.wait()
+
+
+class _Done:
+    def wait(self):
+        return None
+
+
+def make_collectives(backend: str):
+    """(allreduce, allreduce_async, allgather) on the default process group
+    for CUDA tensors. "nccl": the NCCL collectives in place on the device
+    (NVLink / NVSwitch); "gloo": staged through host memory -- used to run the
+    multi-rank path on a single GPU (ranks sharing one device) and in tests;
+    its "async" all-reduce completes before returning."""
+    import torch
+    import torch.distributed as dist
+    if backend == "nccl":
+        def allreduce(t):
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+
+        def allreduce_async(t):
+            return dist.all_reduce(t, op=dist.ReduceOp.SUM, async_op=True)
+
+        def allgather(out, inp):
+            dist.all_gather_into_tensor(out, inp)
+        return allreduce, allreduce_async, allgather
+
+    def allreduce(t):
+        c = t.cpu()
+        dist.all_reduce(c, op=dist.ReduceOp.SUM)
+        t.copy_(c)
+
+    def allreduce_async(t):
+        allreduce(t)
+        return _Done()
+
+    def allgather(out, inp):
+        c = inp.cpu()
+        parts = [torch.empty_like(c) for _ in range(dist.get_world_size())]
+        dist.all_gather(parts, c)
+        out.copy_(torch.cat(parts))
+    return allreduce, allreduce_async, allgather
+
+
 def torch_allreduce(t) -> None:
     import torch.distributed as dist
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
@@ -100,6 +162,14 @@ def point_shard(n: int, world: int, rank: int) -> np.ndarray:
     lo = n * rank // world
     hi = n * (rank + 1) // world
     return np.arange(lo, hi, dtype=np.int64)
+
+
+def point_block(n: int, world: int, rank: int) -> np.ndarray:
+    """Owned rows of `rank` in blocks of ceil(n / world) rows (the last one
+    shorter), so the output can be assembled with one all-gather of equal
+    blocks: rank r's rows are [r b, min(n, (r + 1) b)), b = ceil(n / world)."""
+    b = -(-n // world)
+    return np.arange(min(n, rank * b), min(n, (rank + 1) * b), dtype=np.int64)
 
 
 class _DevView:
@@ -192,6 +262,17 @@ class PointShardedOperator:
         dev = torch.device("cuda", self.device)
         return [torch.as_tensor(_DevView(ptrs[k], lens[k]), device=dev) for k in range(cnt)]
 
+    def grid_pool(self):
+        """The owned windows' grids G as ONE contiguous CUDA tensor view
+        (ksvm_nfft_op_grid_pool): one all-reduce per matvec sums them."""
+        import ctypes as C
+        import torch
+        from . import _lib
+        from .fastsum import _raise
+        p, ln = C.c_void_p(), C.c_int64()
+        _raise(_lib.load().ksvm_nfft_op_grid_pool(self._h, C.byref(p), C.byref(ln)))
+        return torch.as_tensor(_DevView(p.value, ln.value), device=torch.device("cuda", self.device))
+
     def apply_finish(self, y) -> None:
         from . import _lib
         from .fastsum import _raise
@@ -201,8 +282,22 @@ class PointShardedOperator:
     def matvec(self, v, y, allreduce: Callable = None) -> None:
         self.apply_spread(v)
         if allreduce is not None:
-            for g in self.grids():
-                allreduce(g)
+            allreduce(self.grid_pool())
         self.apply_finish(y)
         if allreduce is not None:
             allreduce(y)
+
+    def matvec_blocks(self, v, y_pad, rank: int, world: int, allreduce: Callable, allgather: Callable) -> None:
+        """Matvec for point_block shards: grids summed with one all-reduce,
+        y assembled with one all-gather of the equal row blocks (half the
+        bytes of an all-reduce of y). y_pad: CUDA tensor of world * ceil(n /
+        world) entries; y_pad[:n] is the product afterwards.
+        ``allgather(out, inp)`` gathers equal blocks into out."""
+        n = self._n
+        b = -(-n // world)
+        self.apply_spread(v)
+        allreduce(self.grid_pool())
+        y = y_pad[:n]
+        self.apply_finish(y)
+        blk = y_pad[rank * b:(rank + 1) * b].clone()
+        allgather(y_pad, blk)
