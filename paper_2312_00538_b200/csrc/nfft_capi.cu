@@ -387,7 +387,11 @@ int64_t item_chunk(int64_t total_points, int d) {
     // d <= 2 have few, large tiles and need splitting for parallelism
     int64_t floor_pts = d == 3 ? 1024 : 512;
     if (const char* e = std::getenv(d == 3 ? "KSVM_NFFT_ITEM3" : "KSVM_NFFT_ITEM12")) floor_pts = std::max(32, std::atoi(e));
-    return std::max<int64_t>(floor_pts, (total_points + 148 * 24 - 1) / (148 * 24));
+    static const int64_t div = [] {  // items per SM target (A/B knob)
+        const char* e = std::getenv("KSVM_NFFT_ITEMS_PER_SM");
+        return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t{24};
+    }();
+    return std::max<int64_t>(floor_pts, (total_points + 148 * div - 1) / (148 * div));
 }
 // d = 3 gather items load an 11^3 halo (10.6 KB) each: >= 512 points
 // amortise it (config 3: 0.1865 -> 0.1721 ms); d <= 2 halos are small, so
@@ -395,7 +399,11 @@ int64_t item_chunk(int64_t total_points, int d) {
 int64_t gather_chunk(int64_t total_points, int d) {
     int64_t floor_pts = d == 3 ? 512 : 128;
     if (const char* e = std::getenv("KSVM_NFFT_GITEM")) floor_pts = std::max(32, std::atoi(e));
-    return std::max<int64_t>(floor_pts, (total_points + 148 * 48 - 1) / (148 * 48));
+    static const int64_t div = [] {
+        const char* e = std::getenv("KSVM_NFFT_GITEMS_PER_SM");
+        return e ? std::max<int64_t>(1, std::atoll(e)) : int64_t{48};
+    }();
+    return std::max<int64_t>(floor_pts, (total_points + 148 * div - 1) / (148 * div));
 }
 
 // Affine map of P:src/fastsum.cpp:126-140 on a column-major n x d block.

@@ -977,18 +977,35 @@ spread1_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     __syncwarp();
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
+    // four points per lane in flight: plan loads first, then the dependent
+    // v[perm] loads, then the SMEM updates in point order (a lane's points
+    // may share a column)
+    constexpr int U = 4;
     pdl_wait();
     v = launder(v);
-    for (int i = wb + lane; i < we; i += 32) {
-        const double2 f = __ldg(reinterpret_cast<const double2*>(ps.F + i));
-        const int2 cp = __ldg(ps.CP + i);
-        double q = f.x * __ldcg(v + cp.y);
-        const double Q = f.y;
-        double* col = lp + cp.x * 32 + lane;
+    for (int base = wb + lane; base < we; base += 32 * U) {
+        double2 f[U];
+        int2 cp[U];
+        double vv[U];
 #pragma unroll
-        for (int o = 0; o < S; ++o) {
-            col[o * 32] = fma(q, R[o], col[o * 32]);
-            q *= Q;
+        for (int u = 0; u < U; ++u) {
+            const int i = base + 32 * u;
+            f[u] = i < we ? __ldg(reinterpret_cast<const double2*>(ps.F + i)) : make_double2(0.0, 0.0);
+            cp[u] = i < we ? __ldg(ps.CP + i) : make_int2(0, -1);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) vv[u] = cp[u].y >= 0 ? __ldcg(v + cp[u].y) : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (cp[u].y < 0) break;
+            double q = f[u].x * vv[u];
+            const double Q = f[u].y;
+            double* col = lp + cp[u].x * 32 + lane;
+#pragma unroll
+            for (int o = 0; o < S; ++o) {
+                col[o * 32] = fma(q, R[o], col[o * 32]);
+                q *= Q;
+            }
         }
     }
     __syncthreads();
@@ -1022,19 +1039,29 @@ gather1_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     __syncthreads();
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
-    for (int i = wb + lane; i < we; i += 32) {
-        const double2 f = __ldg(reinterpret_cast<const double2*>(ps.F + i));
-        const int2 cp = __ldg(ps.CP + i);
-        double q = f.x;
-        const double Q = f.y;
-        const double* h = smem + cp.x;
-        double y = 0.0;
+    constexpr int U = 4;  // four points per lane in flight
+    for (int base = wb + lane; base < we; base += 32 * U) {
+        double2 f[U];
+        int2 cp[U];
 #pragma unroll
-        for (int o = 0; o < S; ++o) {
-            y = fma(h[o], q * R[o], y);
-            q *= Q;
+        for (int u = 0; u < U; ++u) {
+            const int i = base + 32 * u;
+            f[u] = i < we ? __ldg(reinterpret_cast<const double2*>(ps.F + i)) : make_double2(0.0, 0.0);
+            cp[u] = i < we ? __ldg(ps.CP + i) : make_int2(0, -1);
         }
-        ps.out[cp.y] = y;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            double q = f[u].x;
+            const double Q = f[u].y;
+            const double* h = smem + cp[u].x;
+            double y = 0.0;
+#pragma unroll
+            for (int o = 0; o < S; ++o) {
+                y = fma(h[o], q * R[o], y);
+                q *= Q;
+            }
+            if (cp[u].y >= 0) ps.out[cp[u].y] = y;
+        }
     }
 }
 
