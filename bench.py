@@ -403,17 +403,24 @@ def run_ours(args):
     # --- per-launch timing pass (same flush discipline) for the roofline ----
     # (one rank's own windows; point-sharded ranks run two phases with a
     # collective between them, so they report no per-launch split)
-    per_launch = {}
+    # Mode 2 keeps the untimed graph's topology (dimension classes concurrent)
+    # and adds event nodes on the main branch only (the d = 3 class and the
+    # window sum), so its step time matches the timed loop's.
+    per_launch, timing_step_ms = {}, None
     if not points_mode:
-        op.set_stage_timing(True)
+        op.set_stage_timing(2)
         acc = {}
+        ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
         for k in range(K):
             flush.zero_()
+            ev2[k][0].record()
             op.apply_into(v, y)
+            ev2[k][1].record()
             for name, ms in op.last_stage_ms().items():
                 acc[name] = acc.get(name, 0.0) + ms
         op.set_stage_timing(False)
         per_launch = {k2: v2 / K for k2, v2 in acc.items()}
+        timing_step_ms = sum(a.elapsed_time(b) for a, b in ev2) / K
 
     # --- end-to-end through the public API with host buffers ---------------
     vh = torch.from_numpy(w.v).pin_memory()
@@ -474,9 +481,11 @@ def run_ours(args):
                     "traffic": traffic,
                     "hbm": {"achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
                             "peak_source": peak_kind},
-                    "timing": "per-launch CUDA events on the operator's stream in a separate pass of K "
-                              "matvecs with the same L2 flush (stage timing serialises the dimension "
-                              "classes, so the per-launch sum exceeds the graph-timed step slightly)"}
+                    "timing": ("per-launch CUDA events recorded as event nodes of the same cached apply graph "
+                               "(main branch: the d = 3 class and the window sum; the other classes stay "
+                               "concurrent) in a second pass of K matvecs with the same L2 flush; that pass "
+                               f"ran at {timing_step_ms:.4f} ms/step vs {total_ms / K:.4f} in the timed loop"
+                               if timing_step_ms else "n/a")}
         step_ms = total_ms / K
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
                 "warmup": max(3, args.warmup), "ms_per_step": step_ms, "higher_is_better": True,
@@ -492,6 +501,7 @@ def run_ours(args):
                 "hbm_fraction_matvec": (w.hbm_bytes(4 if f32 else 8) / (step_ms * 1e-3) / 1e9) / peaks()[0],
                 "per_launch_ms": per_launch,
                 "per_launch_sum_ms": sum(per_launch.values()),
+                "per_launch_pass_step_ms": timing_step_ms,
                 "roofline": roof,
                 "clocks": clk.summary(),
                 "gpu_launches": launches,

@@ -167,7 +167,10 @@ int ksvm_nfft_kernel_diag(const ksvm_nfft_op* op, int window, double* out, int p
  * env KSVM_NFFT_STAGE_TIMING=1 also enables it). last_stage_ms fills the
  * device ms of each kernel launch of the last apply (synchronising on it)
  * and returns how many; stage_name(i) names launch i ("spread_d3",
- * "reduce", "conv_0", "gather_d3", "combine", ...). */
+ * "reduce", "conv_0", "gather_d3", "combine", ...). on = 1 times every
+ * launch and runs the dimension classes one after another; on = 2 times the
+ * main branch (the first class, d = 3 when present, and the window sum) and
+ * keeps the other classes concurrent as in an untimed apply. */
 int ksvm_nfft_op_set_stage_timing(ksvm_nfft_op* op, int on);
 int ksvm_nfft_op_last_stage_ms(const ksvm_nfft_op* op, float* ms, int cap);
 const char* ksvm_nfft_op_stage_name(const ksvm_nfft_op* op, int i);

@@ -464,7 +464,8 @@ struct Engine {
     cudaEvent_t ev_stage[kMaxTicks] = {};
     const char* tick_name[kMaxTicks] = {};
     int nticks = 0, last_nticks = 0;
-    bool stage_timing = false;
+    int stage_timing = 0;  // 0 off; 1 every launch, classes serialised; 2 main branch only, branches kept
+    cudaStream_t tick_stream = nullptr;  // stream of the class being enqueued (mode 2 ticks only there)
     ksvm_nfft_config cfg{};
     double fit = 1.0;
     int precision = KSVM_NFFT_FP64;
@@ -594,7 +595,7 @@ struct Engine {
         CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
-        stage_timing = std::getenv("KSVM_NFFT_STAGE_TIMING") != nullptr;
+        stage_timing = std::getenv("KSVM_NFFT_STAGE_TIMING") != nullptr ? 1 : 0;
         for (auto& e : ev_stage) CK(cudaEventCreate(&e));
     }
 
@@ -1010,6 +1011,7 @@ struct Engine {
     // Per-launch device timing: an event before each launch and one at the end.
     void tick(const char* name) {
         if (!stage_timing || nticks >= kMaxTicks) return;
+        if (stage_timing == 2 && tick_stream != S()) return;  // side branches run untimed
         tick_name[nticks] = name;
         // external event node when captured into a graph, so the event stays timeable
         CK(cudaEventRecordWithFlags(ev_stage[nticks], stream, capturing ? cudaEventRecordExternal : 0));
@@ -1031,6 +1033,7 @@ struct Engine {
         static const char* kConv[3] = {"conv_0", "conv_1", "conv_2"};
         const int cnt = class_end[D] - class_begin[D];
         if (cnt == 0) return;
+        tick_stream = st;
         if (ph & kPhSpread) {
         NvtxRange nr(kSpread[D]);
         tick(kSpread[D]);
@@ -1117,7 +1120,7 @@ struct Engine {
         }
         int ncls = 0;
         for (int D = 1; D <= 3; ++D) ncls += class_end[D] > class_begin[D] ? 1 : 0;
-        if (stage_timing || ncls < 2) {
+        if (stage_timing == 1 || ncls < 2) {
             for (int D = 3; D >= 1; --D) run_class(D, v, S(), gather);
             return;
         }
@@ -1186,6 +1189,7 @@ struct Engine {
         }
         nticks = 0;
         run_classes(v, true);
+        tick_stream = S();
         NvtxRange nr("combine");
         tick("combine");
         launch_combine(y, SRC(), d_inv.p, d_inv8.p, d_nu8.p, d_eta.p, P, 0, n, S());
@@ -1209,7 +1213,7 @@ struct Engine {
     struct GraphEntry {
         const double* v;
         double* y;
-        bool timed;
+        int timed;
         cudaGraphExec_t exec;
         int nticks;
         int64_t launches;
@@ -1909,7 +1913,7 @@ int ksvm_nfft_op_device(const ksvm_nfft_op* op) { return op ? op->e.device : -1;
 int ksvm_nfft_op_set_stage_timing(ksvm_nfft_op* op, int on) {
     if (!op) return KSVM_NFFT_ERR_CONFIG;
     std::lock_guard<std::mutex> lk(op->e.mu);
-    op->e.stage_timing = on != 0;
+    op->e.stage_timing = on == 2 ? 2 : (on != 0 ? 1 : 0);
     return KSVM_NFFT_OK;
 }
 

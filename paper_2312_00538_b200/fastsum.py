@@ -405,9 +405,12 @@ class AnovaFastOperator(KernelOperator):
         duplicate merge; 0 outside window_mask)."""
         return int(_lib.load().ksvm_nfft_op_window_points(self._h, int(window)))
 
-    def set_stage_timing(self, on: bool = True) -> None:
-        """Record CUDA events between the five stages of every apply."""
-        _raise(_lib.load().ksvm_nfft_op_set_stage_timing(self._h, 1 if on else 0))
+    def set_stage_timing(self, on=True) -> None:
+        """Record CUDA events between the launches of every apply: True / 1
+        times every launch (dimension classes serialised), 2 times the main
+        branch only (classes stay concurrent, as in an untimed apply)."""
+        mode = 2 if on == 2 else (1 if on else 0)
+        _raise(_lib.load().ksvm_nfft_op_set_stage_timing(self._h, mode))
 
     def last_stage_ms(self) -> dict:
         """{launch name: device ms} for each kernel launch of the last apply."""
