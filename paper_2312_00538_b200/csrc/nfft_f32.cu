@@ -87,7 +87,7 @@ __device__ __forceinline__ void weights_f32(float (&w)[3][8], float s, const flo
 // a function of the plan alone.
 // ---------------------------------------------------------------------------
 template <int W>
-__global__ void __launch_bounds__(W * 32, 4)
+__global__ void __launch_bounds__(W * 32, 5)
 spread3_f32_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
                    const DWin* __restrict__ wins, const double* __restrict__ v,
                    double* __restrict__ patches) {
