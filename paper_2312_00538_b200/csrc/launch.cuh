@@ -32,6 +32,52 @@ __device__ __forceinline__ T* launder(T* p) {
     return p;
 }
 
+// L2 eviction-priority hints. Per apply the plan streams (window factors,
+// cell codes: 40 B per point per window) are read once, while v (spread:
+// gathered through each window's sort permutation) and the per-window
+// outputs (gather: scattered through it) are touched in 8-byte pieces of
+// 32-byte sectors by every window: streaming the plan data evict-first and
+// keeping v / the outputs evict-last lets them stay in the 126 MB L2 instead
+// of being re-fetched (or read-for-ownership) sector by sector.
+__device__ __forceinline__ unsigned long long l2_evict_first() {
+    unsigned long long p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ unsigned long long l2_evict_last() {
+    unsigned long long p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// read-only plan data (may be issued before griddepcontrol.wait)
+__device__ __forceinline__ double2 ld_plan(const double2* p, unsigned long long pol) {
+    double2 r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+        : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ int2 ld_plan(const int2* p, unsigned long long pol) {
+    int2 r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;"
+        : "=r"(r.x), "=r"(r.y) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ float4 ld_plan(const float4* p, unsigned long long pol) {
+    float4 r;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+        : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p), "l"(pol));
+    return r;
+}
+// coherent L2 load of data a predecessor kernel may have written (after pdl_wait)
+__device__ __forceinline__ double ld_keep(const double* p, unsigned long long pol) {
+    double r;
+    asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(r) : "l"(p), "l"(pol) : "memory");
+    return r;
+}
+__device__ __forceinline__ void st_keep(double* p, double v, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
 inline bool pdl_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("KSVM_NFFT_PDL");

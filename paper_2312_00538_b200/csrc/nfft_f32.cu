@@ -54,9 +54,9 @@ __device__ __forceinline__ int half_stage(int row_len) { return kHalfRows * row_
 struct PrefF {
     float4 F = make_float4(0.f, 0.f, 0.f, 0.f);
     int code = 0, perm = 0;
-    __device__ __forceinline__ void load(const DPSet& ps, int i) {
-        F = __ldg(ps.F32 + i);
-        const int2 c = __ldg(ps.CP + i);
+    __device__ __forceinline__ void load(const DPSet& ps, int i, unsigned long long pol) {
+        F = ld_plan(ps.F32 + i, pol);  // streamed evict-first (launch.cuh)
+        const int2 c = ld_plan(ps.CP + i, pol);
         code = c.x;
         perm = c.y;
     }
@@ -115,13 +115,14 @@ spread3_f32_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pse
         we = min(wb + per, it.end);
     }
     PrefF pa, pb;
-    if (wb + lane < we) pa.load(ps, wb + lane);
-    if (wb + 32 + lane < we) pb.load(ps, wb + 32 + lane);
+    const unsigned long long pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
+    if (wb + lane < we) pa.load(ps, wb + lane, pol_stream);
+    if (wb + 32 + lane < we) pb.load(ps, wb + 32 + lane, pol_stream);
     __syncthreads();
     double va = 0.0;
     pdl_wait();  // v may be produced by the previous kernel (duplicate-merge sums)
     v = launder(v);
-    if (wb + lane < we) va = __ldcg(v + pa.perm);
+    if (wb + lane < we) va = ld_keep(v + pa.perm, pol_keep);
 
     float acc[4][8];
 #pragma unroll
@@ -180,8 +181,8 @@ spread3_f32_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pse
         // bit q: point q of the batch (half q >> 4, step q & 15) continues its half's cell
         const unsigned same = __ballot_sync(kFull, !valid || code == (hl == 0 ? cur : prev));
         pa = pb;
-        if (base + 32 + lane < we) va = __ldcg(v + pa.perm);
-        if (base + 64 + lane < we) pb.load(ps, base + 64 + lane);
+        if (base + 32 + lane < we) va = ld_keep(v + pa.perm, pol_keep);
+        if (base + 64 + lane < we) pb.load(ps, base + 64 + lane, pol_stream);
         __syncwarp();
         if (same == kFull) {
 #pragma unroll
@@ -256,8 +257,9 @@ gather3_f32_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pse
         we = min(wb + per, it.end);
     }
     PrefF pa, pb;
-    if (wb + lane < we) pa.load(ps, wb + lane);
-    if (wb + 32 + lane < we) pb.load(ps, wb + 32 + lane);
+    const unsigned long long pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
+    if (wb + lane < we) pa.load(ps, wb + lane, pol_stream);
+    if (wb + 32 + lane < we) pb.load(ps, wb + 32 + lane, pol_stream);
     pdl_wait();  // H is written by the grid stage
     {
         const DWin& w = *launder(&wn);
@@ -338,7 +340,7 @@ gather3_f32_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pse
         const int prev = __shfl_up_sync(kFull, code, 1);
         const unsigned same = __ballot_sync(kFull, !valid || code == (hl == 0 ? cur : prev));
         pa = pb;
-        if (base + 64 + lane < we) pb.load(ps, base + 64 + lane);
+        if (base + 64 + lane < we) pb.load(ps, base + 64 + lane, pol_stream);
         __syncwarp();
         if (same == kFull) {
 #pragma unroll
@@ -368,7 +370,7 @@ gather3_f32_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pse
                 part[k] = keep + __shfl_xor_sync(kFull, send, s);
             }
         }
-        if (valid) ps.out[perm] = static_cast<double>(part[0]);
+        if (valid) st_keep(ps.out + perm, static_cast<double>(part[0]), pol_keep);
         __syncwarp();
     }
 }

@@ -118,6 +118,21 @@ struct Pref {
         code = c.x;
         perm = c.y;
     }
+    // same, streamed through L2 evict-first (launch.cuh)
+    __device__ __forceinline__ void load(const DPSet& ps, int i, unsigned long long pol) {
+        const double2* f = reinterpret_cast<const double2*>(ps.F + i);
+        const double2 a = ld_plan(f, pol);
+        P = a.x;
+        Q[0] = a.y;
+        if (D > 1) {
+            const double2 b = ld_plan(f + 1, pol);
+            Q[1] = b.x;
+            Q[2] = b.y;
+        }
+        const int2 c = ld_plan(ps.CP + i, pol);
+        code = c.x;
+        perm = c.y;
+    }
 };
 
 }  // namespace
@@ -314,8 +329,9 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
     Pref<3> pa, pb;  // plan data: prefetched before the dependency wait
-    if (lane < B && wb + lane < we) pa.load(ps, wb + lane);
-    if (lane < B && wb + B + lane < we) pb.load(ps, wb + B + lane);
+    const unsigned long long pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
+    if (lane < B && wb + lane < we) pa.load(ps, wb + lane, pol_stream);
+    if (lane < B && wb + B + lane < we) pb.load(ps, wb + B + lane, pol_stream);
 
     double acc[8][2];
 #pragma unroll
@@ -366,7 +382,7 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
         const int i0 = wb + lane;
         pdl_wait();  // v may come from the previous kernel (plan factors above did not)
         v = launder(v);
-        if (lane < B && i0 < we) va = __ldcg(v + pa.perm);
+        if (lane < B && i0 < we) va = ld_keep(v + pa.perm, pol_keep);
     }
     __syncwarp();
     for (int base = wb; base < we; base += B) {
@@ -376,8 +392,8 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
         const int prev = __shfl_up_sync(kFull, code, 1);
         const unsigned same = __ballot_sync(kFull, lane < cnt && code == (lane == 0 ? cur : prev));
         pa = pb;
-        if (lane < B && base + B + lane < we) va = __ldcg(v + pa.perm);
-        if (lane < B && base + 2 * B + lane < we) pb.load(ps, base + 2 * B + lane);
+        if (lane < B && base + B + lane < we) va = ld_keep(v + pa.perm, pol_keep);
+        if (lane < B && base + 2 * B + lane < we) pb.load(ps, base + 2 * B + lane, pol_stream);
         __syncwarp();
         if (same == kBatch) {  // the whole batch continues the current cell
 #pragma unroll
@@ -602,8 +618,9 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
     Pref<3> pa, pb;
-    if (wb + lane < we) pa.load(ps, wb + lane);
-    if (wb + 32 + lane < we) pb.load(ps, wb + 32 + lane);
+    const unsigned long long pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
+    if (wb + lane < we) pa.load(ps, wb + lane, pol_stream);
+    if (wb + 32 + lane < we) pb.load(ps, wb + 32 + lane, pol_stream);
     __syncthreads();
     pdl_wait();
     load_halo3_r<PE, TC>(halo, *launder(&wn), tc, sR);
@@ -634,7 +651,7 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
         double part = fma(z0, w2.x, z1 * w2.y);
         part += __shfl_xor_sync(kFull, part, 1);
         part += __shfl_xor_sync(kFull, part, 2);
-        if (t == 0 && vg) ps.out[reinterpret_cast<const int*>(sg + 24)[1]] = part;
+        if (t == 0 && vg) st_keep(ps.out + reinterpret_cast<const int*>(sg + 24)[1], part, pol_keep);
     };
 
     for (int base = wb; base < we; base += 32) {
@@ -667,7 +684,7 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
         const int prev = __shfl_up_sync(kFull, code, 1);
         const unsigned same = __ballot_sync(kFull, lane < cnt && code == (lane == 0 ? cur : prev));
         pa = pb;
-        if (base + 64 + lane < we) pb.load(ps, base + 64 + lane);
+        if (base + 64 + lane < we) pb.load(ps, base + 64 + lane, pol_stream);
         __syncwarp();
         if (same == kFull) {
 #pragma unroll
@@ -981,6 +998,7 @@ spread1_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     // v[perm] loads, then the SMEM updates in point order (a lane's points
     // may share a column)
     constexpr int U = 4;
+    const unsigned long long pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
     pdl_wait();
     v = launder(v);
     for (int base = wb + lane; base < we; base += 32 * U) {
@@ -990,11 +1008,11 @@ spread1_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int i = base + 32 * u;
-            f[u] = i < we ? __ldg(reinterpret_cast<const double2*>(ps.F + i)) : make_double2(0.0, 0.0);
-            cp[u] = i < we ? __ldg(ps.CP + i) : make_int2(0, -1);
+            f[u] = i < we ? ld_plan(reinterpret_cast<const double2*>(ps.F + i), pol_stream) : make_double2(0.0, 0.0);
+            cp[u] = i < we ? ld_plan(ps.CP + i, pol_stream) : make_int2(0, -1);
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) vv[u] = cp[u].y >= 0 ? __ldcg(v + cp[u].y) : 0.0;
+        for (int u = 0; u < U; ++u) vv[u] = cp[u].y >= 0 ? ld_keep(v + cp[u].y, pol_keep) : 0.0;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (cp[u].y < 0) break;
@@ -1040,14 +1058,15 @@ gather1_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
     int wb, we;
     warp_range(it, warp, W, &wb, &we);
     constexpr int U = 4;  // four points per lane in flight
+    const unsigned long long pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
     for (int base = wb + lane; base < we; base += 32 * U) {
         double2 f[U];
         int2 cp[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int i = base + 32 * u;
-            f[u] = i < we ? __ldg(reinterpret_cast<const double2*>(ps.F + i)) : make_double2(0.0, 0.0);
-            cp[u] = i < we ? __ldg(ps.CP + i) : make_int2(0, -1);
+            f[u] = i < we ? ld_plan(reinterpret_cast<const double2*>(ps.F + i), pol_stream) : make_double2(0.0, 0.0);
+            cp[u] = i < we ? ld_plan(ps.CP + i, pol_stream) : make_int2(0, -1);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -1060,7 +1079,7 @@ gather1_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
                 y = fma(h[o], q * R[o], y);
                 q *= Q;
             }
-            if (cp[u].y >= 0) ps.out[cp[u].y] = y;
+            if (cp[u].y >= 0) st_keep(ps.out + cp[u].y, y, pol_keep);
         }
     }
 }

@@ -110,3 +110,21 @@ def test_config3_full_size_matches_reference_driver_fixture():
            "status": int(g["status"]), "ipm_iters": int(g["ipm_iters"]), "log": g["log"], "alpha": g["alpha"],
            "bias": float(g["bias"]), "dual_objective": float(g["dual"]), "test_decision": g["f"]}
     same_run(ours(w, "nystrom-gaussian", 200), ref)
+
+
+def test_config5_shape_n176k_matches_reference_driver_fixture():
+    """BASELINE config 5's shape (10 windows: 9 x 3 + 1, tanh-teacher labels)
+    at n = 176000 (n_train = 64238 after the balanced split), greedy Cholesky
+    rank 200, C = 1: this repo's GPU pipeline against the reference's own
+    driver + CPU fastsum (22 min on one host thread, run once in the build
+    container by tests/golden/make_ref_driver_golden.py). The reference
+    converges here in 7 Newton steps (38 .. 64 GMRES iterations per step)."""
+    path = os.path.join(GOLDEN, "drv_cfg5_n176k.npz")
+    if not os.path.exists(path):
+        pytest.skip("fixture not generated")
+    g = np.load(path)
+    w = workloads.make(5, int(g["n"]))
+    ref = {"n_train": int(g["n_train"]), "n_test": int(g["n_test"]), "rank": int(g["rank"]),
+           "status": int(g["status"]), "ipm_iters": int(g["ipm_iters"]), "log": g["log"], "alpha": g["alpha"],
+           "bias": float(g["bias"]), "dual_objective": float(g["dual"]), "test_decision": g["f"]}
+    same_run(ours(w, "cholesky-greedy", 200), ref)
