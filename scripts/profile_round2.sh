@@ -18,8 +18,10 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --cache-co
 timeout 900 ncu --set full --clock-control none --cache-control all --import-source on -k regex:"spread3|gather3" -c 2 -f -o $O/full_cfg5 python bench.py $A5 > $O/ncu_f5.log 2>&1
 timeout 900 ncu --set full --clock-control none --cache-control all --import-source on -k regex:"f32_kernel" -c 2 -f -o $O/full_cfg5_fp32 python bench.py --precision fp32 $A5 > $O/ncu_f5b.log 2>&1
 timeout 600 ncu --set full --clock-control none --cache-control all --import-source on -k regex:"spread3|gather3" -s 4 -c 2 -f -o $O/full_cfg2 python bench.py $A2 > $O/ncu_f2.log 2>&1
+timeout 600 ncu --set full --clock-control none --cache-control all --import-source on -k regex:"spread3|gather3" -s 4 -c 2 -f -o $O/full_cfg3 python bench.py --config 3 --steps 2 --warmup 3 --no-cpu-baseline > $O/ncu_f3.log 2>&1
 timeout 600 ncu --set full --clock-control none --cache-control all --import-source on -k regex:"spread3|gather3" -s 4 -c 2 -f -o $O/full_cfg4 python bench.py --config 4 --steps 2 --warmup 3 --no-cpu-baseline > $O/ncu_f4.log 2>&1
 timeout 600 python scripts/bench_ipm.py --config 1 --oracle > $O/ipm1.json 2> $O/ipm1.err
 timeout 600 python scripts/bench_ipm.py --config 3 > $O/ipm3.json 2> $O/ipm3.err
 timeout 900 python scripts/bench_ipm.py --config 5 > $O/ipm5.json 2> $O/ipm5.err
+timeout 1500 python scripts/ipm_scaling.py > $O/ipm_scaling.jsonl 2> $O/ipm_scaling.err
 echo done
