@@ -754,6 +754,9 @@ struct Engine {
     // Threshold: mean points per cell of the occupied tiles.
     bool use_columns(int D, const char* env) const {
         if (const char* e = std::getenv(env)) return std::strcmp(e, "column") == 0;
+        return sparse_cells(D);
+    }
+    bool sparse_cells(int D) const {
         long long pts = 0, cells = 0;
         for (size_t s = 0; s < owned.size(); ++s) {
             const Window& w = *wins[static_cast<size_t>(owned[s])];
@@ -813,7 +816,7 @@ struct Engine {
             class_end[D] = static_cast<int>(all.size());
             if (f32_want(D)) {
                 const char* fe = std::getenv("KSVM_NFFT_F32");
-                f32_dense[D] = (fe && std::strcmp(fe, "all") == 0) || !use_columns(D, "KSVM_NFFT_F32_DENSITY");
+                f32_dense[D] = (fe && std::strcmp(fe, "all") == 0) || !sparse_cells(D);
                 for (int s = 0; s < P; ++s) {  // keep the factors the chosen kernels read
                     Window& w = *wins[static_cast<size_t>(owned[static_cast<size_t>(s)])];
                     if (w.d != D) continue;

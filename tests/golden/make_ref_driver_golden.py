@@ -5,9 +5,11 @@ compiled unmodified by path), run once on the CPU of the build container:
   drv_cfg3_full.npz   BASELINE config 3 at full size (n = 100000,
                              n_train ~ 5e4), Nystrom-Gaussian rank 200, C = 1
   drv_cfg5_n176k.npz  BASELINE config 5's shape at n = 176000
-                             (n_train ~ 8.8e4), greedy Cholesky rank 200, C = 1
+                             (n_train = 64238), greedy Cholesky rank 200, C = 1
+  drv_cfg5_n500k.npz  the same at n = 500000 (n_train = 229246), where the
+                             GPU pipeline hits the reference's stall rule
 
-  python tests/golden/make_ref_driver_golden.py cfg3|cfg5
+  python tests/golden/make_ref_driver_golden.py cfg3|cfg5|cfg5_500k
 
 Each stores the split sizes, the per-Newton-step log (mu, xi_alpha_rel,
 xi_lambda_rel, step_alpha, GMRES iterations, GMRES converged), status, rank,
@@ -26,7 +28,8 @@ import oracle  # noqa: E402
 from paper_2312_00538_b200 import workloads  # noqa: E402
 
 CASES = {"cfg3": (3, None, "nystrom-gaussian", "drv_cfg3_full.npz"),
-         "cfg5": (5, 176000, "cholesky-greedy", "drv_cfg5_n176k.npz")}
+         "cfg5": (5, 176000, "cholesky-greedy", "drv_cfg5_n176k.npz"),
+         "cfg5_500k": (5, 500000, "cholesky-greedy", "drv_cfg5_n500k.npz")}
 
 
 def main(which):

@@ -115,3 +115,51 @@ def test_point_sharded_two_ranks(tmp_path, oracle_lib, case):
             assert rel(r[key], single) <= 1e-12, key
             assert rel(r[key], ref) <= 1e-10, key
         assert np.array_equal(r["blocks"], r["allreduce"])  # y rows come from one owner either way
+
+
+def test_pipelined_entry_points_check_their_arguments():
+    """ksvm_nfft_op_apply_windows / _combine_range take device pointers and a
+    window-sharded (not point-sharded) operator; the grid pool belongs to
+    point-sharded operators; errors map to status 4 (std::invalid_argument)."""
+    import torch
+    from paper_2312_00538_b200 import AnovaKernelSpec, Dataset, FeatureWindowing, anova_fast_operator, sharding
+    w = workloads.make(2, 4000)
+    spec = AnovaKernelSpec(FeatureWindowing.explicit(w.windows))
+    op = anova_fast_operator(Dataset(w.points), spec)
+    v = torch.from_numpy(w.v).cuda()
+    y = torch.zeros_like(v)
+    with pytest.raises(ValueError):
+        op.apply_windows(w.v)  # host array
+    op.apply_windows(v)
+    for lo, hi in ((-1, 10), (0, w.n + 1), (20, 10)):
+        with pytest.raises(ValueError):
+            op.combine_range(y, lo, hi)
+    op.combine_range(y, 0, 0)  # empty range: no-op
+    assert float(y.abs().sum()) == 0.0
+    pts = sharding.PointShardedOperator(Dataset(w.points), spec, sharding.point_block(w.n, 2, 0))
+    assert pts.grid_pool().numel() == sum(g.numel() for g in pts.grids())
+
+
+def test_point_shards_in_fp32_mode(oracle_lib):
+    """fp32 mode on point-sharded operators: the shards' partial grids add up
+    to the full product within the fp32 contract (1e-5)."""
+    import torch
+    from paper_2312_00538_b200 import AnovaKernelSpec, Dataset, FeatureWindowing, sharding
+    w = workloads.make(5, 200000)
+    spec = AnovaKernelSpec(FeatureWindowing.explicit(w.windows))
+    shards = [sharding.PointShardedOperator(Dataset(w.points), spec, sharding.point_block(w.n, 2, r),
+                                            fit_fraction=w.fit_fraction, precision="fp32") for r in range(2)]
+    v = torch.from_numpy(w.v).cuda()
+    for op in shards:
+        op.apply_spread(v)
+    pools = [op.grid_pool() for op in shards]
+    total = pools[0] + pools[1]
+    for p in pools:
+        p.copy_(total)
+    y = torch.zeros_like(v)
+    for op in shards:
+        part = torch.empty_like(v)
+        op.apply_finish(part)
+        y += part
+    ref = oracle_lib.anova(w.points, w.windows, fit=w.fit_fraction).apply(w.v)
+    assert rel(y.cpu().numpy(), ref) <= 1e-5
