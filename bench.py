@@ -61,10 +61,11 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--precision", choices=["fp64", "fp32"], default="fp64",
                     help="fp32: north_star's optional fp32 mode (d = 3 windows in fp32, <= 1e-5)")
-    ap.add_argument("--shard", choices=["windows", "points"], default="windows",
+    ap.add_argument("--shard", choices=["auto", "windows", "points"], default="auto",
                     help="N > 1: windows (north_star: LPT window sharding, one chunked all-reduce of y, "
-                         "overlapped with the window sum) or points (SURVEY 8(e) hybrid: one all-reduce of "
-                         "the grid pool, one all-gather of y)")
+                         "overlapped with the window sum), points (SURVEY 8(e) hybrid: one all-reduce of "
+                         "the grid pool, one all-gather of y), or auto: windows unless LPT leaves the "
+                         "busiest rank more than 20 %% above the mean load (the SURVEY 8(e) fix for imbalance)")
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl")
     ap.add_argument("--same-device", action="store_true",
                     help="every rank on cuda:0 (exercises the N > 1 path on a 1-GPU lease; use --backend gloo)")
@@ -348,7 +349,13 @@ def run_ours(args):
     os.environ.setdefault("KSVM_NFFT_QUIET", "1")
     f32 = args.precision == "fp32"
     v = torch.from_numpy(w.v).to(dev)
-    points_mode = world > 1 and args.shard == "points"
+    costs = sharding.window_costs(w.windows, points=w.points)
+    owner = sharding.lpt_assign(costs, world)
+    shard = args.shard
+    if shard == "auto":
+        loads = [sum(c for c, o in zip(costs, owner) if o == r) for r in range(world)]
+        shard = "points" if world > 1 and max(loads) > 1.2 * (sum(loads) / world) else "windows"
+    points_mode = world > 1 and shard == "points"
     if points_mode:
         # SURVEY.md 8(e) hybrid: every rank plans all windows from all points
         # and spreads / gathers its block of rows
@@ -358,7 +365,6 @@ def run_ours(args):
         y_pad = torch.zeros(world * blk, dtype=torch.float64, device=dev)
         y = y_pad[:w.n]
     else:
-        owner = sharding.lpt_assign(sharding.window_costs(w.windows, points=w.points), world)
         mask = sharding.window_mask(owner, rank) if world > 1 else None
         op = anova_fast_operator(Dataset(w.points), spec, fit_fraction=w.fit_fraction, device=local,
                                  window_mask=mask, precision=args.precision)
