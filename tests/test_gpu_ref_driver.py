@@ -128,3 +128,25 @@ def test_config5_shape_n176k_matches_reference_driver_fixture():
            "status": int(g["status"]), "ipm_iters": int(g["ipm_iters"]), "log": g["log"], "alpha": g["alpha"],
            "bias": float(g["bias"]), "dual_objective": float(g["dual"]), "test_decision": g["f"]}
     same_run(ours(w, "cholesky-greedy", 200), ref)
+
+
+def test_config5_shape_n500k_stall_matches_reference_driver_fixture():
+    """BASELINE config 5's shape at n = 500000 (n_train = 229246), greedy
+    Cholesky rank 200, C = 1 -- the smallest size of the sweep
+    (scripts/ipm_scaling.py) at which the IPM hits the reference's stall rule
+    (P:src/ipm.cpp:145-149) on the GPU. The reference's own driver + CPU
+    fastsum, run once in the build container, must take the same Newton steps
+    with the same GMRES counts and stop with the same status. The GMRES
+    solves that hit the 100-iteration cap are unconverged, so only the
+    trajectory (and the status) is compared here, not alpha to 1e-6."""
+    path = os.path.join(GOLDEN, "drv_cfg5_n500k.npz")
+    if not os.path.exists(path):
+        pytest.skip("fixture not generated")
+    g = np.load(path)
+    w = workloads.make(5, int(g["n"]))
+    a = ours(w, "cholesky-greedy", 200)
+    assert (a["n_train"], a["n_test"], a["rank"]) == (int(g["n_train"]), int(g["n_test"]), int(g["rank"]))
+    assert a["status"] == int(g["status"])
+    assert a["ipm_iters"] == int(g["ipm_iters"])
+    assert [int(x) for x in a["log"][:, 4]] == [int(x) for x in g["log"][:, 4]]
+    assert np.allclose(a["log"][:, 0], g["log"][:, 0], rtol=1e-14)  # mu trajectory
