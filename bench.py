@@ -334,6 +334,8 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if args.same_device and world > 1 and args.backend == "nccl":
+        raise SystemExit("--same-device needs --backend gloo (NCCL rejects two ranks on one GPU)")
     local = 0 if args.same_device else int(os.environ.get("LOCAL_RANK", "0"))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)

@@ -223,7 +223,10 @@ int ksvm_nfft_op_grid_pool(const ksvm_nfft_op* op, double** pool, int64_t* lengt
  *     all-reduce y[lo:hi) (async, e.g. NCCL)   overlaps the next range's sum
  * Both take device pointers (ptr_kind KSVM_NFFT_DEVICE) and are ordered on
  * `stream` like ksvm_nfft_op_apply; y[lo:hi) equals ksvm_nfft_op_apply's rows
- * bit for bit. Replaces nothing in the reference (single process). */
+ * bit for bit. combine_range reads the per-window outputs of the operator's
+ * most recent apply_windows (or apply): a caller that shares the operator
+ * between threads must not interleave other applies with one pipelined
+ * matvec. Replaces nothing in the reference (single process). */
 int ksvm_nfft_op_apply_windows(ksvm_nfft_op* op, const double* v, int ptr_kind, void* stream);
 int ksvm_nfft_op_combine_range(ksvm_nfft_op* op, double* y, int64_t lo, int64_t hi, int ptr_kind,
                                void* stream);
