@@ -12,6 +12,7 @@ reference about 3 s (config 3), 31 s (config 4) and 300 s (config 5,
 profiles/r1_bench_cfg*.json); with the windows concurrent the wall time is
 that of the slowest window (~35 s for config 5 on the GPU box's 16 threads).
 
+Config 5 also checks the optional fp32 mode at full size (bar 1e-5).
 Config 4 runs twice: with the exact duplicate merge of its 14 all-binary
 windows (KSVM_NFFT_DEDUP=1, the default: 8 distinct points per window, one
 cell holding ~364k points) and without it (=0: heavy-cell item splitting at
@@ -75,9 +76,9 @@ def reference_matvec(w, v):
     return out
 
 
-def gpu_matvec(w, v):
+def gpu_matvec(w, v, precision="fp64"):
     op = anova_fast_operator(Dataset(w.points), AnovaKernelSpec(FeatureWindowing.explicit(w.windows)),
-                             fit_fraction=w.fit_fraction)
+                             fit_fraction=w.fit_fraction, precision=precision)
     y = op.apply(v)
     pts = [op.window_points(l) for l in range(len(w.windows))]
     del op
@@ -119,3 +120,6 @@ def test_config5_full_size_vs_reference():
     # and entrywise on a deterministic sample (no cancellation hides a bad block)
     idx = np.random.default_rng(5).choice(w.n, 20000, replace=False)
     assert np.max(np.abs(y[idx] - ref[idx])) <= 1e-9 * np.max(np.abs(ref))
+    # the optional fp32 mode at full size: <= 1e-5 (BASELINE north_star)
+    y32, _ = gpu_matvec(w, w.v, "fp32")
+    assert rel(y32, ref) <= 1e-5
