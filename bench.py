@@ -269,7 +269,7 @@ def kernel_bytes(w, name, pts, word=8):
     for the fp32 mode's d = 3 kernels (B32 = 4 n (2D + 2))."""
     if not (name.startswith("spread_d") or name.startswith("gather_d")):
         return 0
-    k = int(name[-1])
+    k = int(name[len("spread_d")])  # spread_dK[_f32] / gather_dK[_f32]
     sel = [(len(x), p) for x, p in zip(w.windows, pts) if len(x) == k and p > 0]
     return word * (sum(d * p for d, p in sel) + max((p for _, p in sel), default=0))
 
@@ -278,7 +278,7 @@ def kernel_fmas(w, name, pts, m=4):
     """FP64 FMAs one launch executes: (2m)^d per evaluated point and window."""
     if not (name.startswith("spread_d") or name.startswith("gather_d")):
         return 0
-    k = int(name[-1])
+    k = int(name[len("spread_d")])
     return sum(p * (2 * m) ** len(x) for x, p in zip(w.windows, pts) if len(x) == k)
 
 
@@ -469,13 +469,13 @@ def run_ours(args):
         roof = None
         if dom is not None:
             ms = per_launch[dom]
-            word = 4 if (f32 and dom.endswith("3")) else 8
+            word = 4 if dom.endswith("_f32") else 8  # the class ran the fp32 kernels
             ach = kernel_bytes(w, dom, pts, word) / (ms * 1e-3) / 1e9
             traffic = None
             try:
                 with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-                    key = f"cfg{args.config}" + ("_fp32" if f32 else "")
-                    traffic = json.load(f).get(key, {}).get(dom)
+                    key = f"cfg{args.config}" + ("_fp32" if dom.endswith("_f32") else "")
+                    traffic = json.load(f).get(key, {}).get(dom.replace("_f32", ""))
             except Exception:
                 pass
             fpk = fp64_peak_tflops(dev, torch.float32 if word == 4 else torch.float64)

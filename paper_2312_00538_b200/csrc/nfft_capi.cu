@@ -1031,15 +1031,18 @@ struct Engine {
         run_class_phases(D, v, st, kPhSpread | kPhGrid | (gather ? kPhGather : 0));
     }
     void run_class_phases(int D, const double* v, cudaStream_t st, int ph) {
+        // the fp32-mode kernels carry a "_f32" suffix (bench.py reads it)
         static const char* kSpread[4] = {"", "spread_d1", "spread_d2", "spread_d3"};
         static const char* kGather[4] = {"", "gather_d1", "gather_d2", "gather_d3"};
+        static const char* kSpread32 = "spread_d3_f32";
+        static const char* kGather32 = "gather_d3_f32";
         static const char* kConv[3] = {"conv_0", "conv_1", "conv_2"};
         const int cnt = class_end[D] - class_begin[D];
         if (cnt == 0) return;
         tick_stream = st;
         if (ph & kPhSpread) {
-        NvtxRange nr(kSpread[D]);
-        tick(kSpread[D]);
+        NvtxRange nr(f32_class(D) ? kSpread32 : kSpread[D]);
+        tick(f32_class(D) ? kSpread32 : kSpread[D]);
         if (f32_class(D))
             launch_spread3_f32(d_items.p + class_begin[D], cnt, PS(), WINS(), v, PATCHES(), st);
         else
@@ -1091,9 +1094,9 @@ struct Engine {
         }
         }  // grid phase
         if (ph & kPhGather) {
-            NvtxRange nr(kGather[D]);
+            NvtxRange nr(f32_class(D) ? kGather32 : kGather[D]);
             const int gcnt = gclass_end[D] - gclass_begin[D];
-            tick(kGather[D]);
+            tick(f32_class(D) ? kGather32 : kGather[D]);
             if (f32_class(D)) {
                 launch_gather3_f32(d_gitems.p + gclass_begin[D], gcnt, PS(), WINS(), st);
             } else if (gather_columns[D]) {
