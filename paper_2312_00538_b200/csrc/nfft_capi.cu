@@ -770,6 +770,15 @@ struct Engine {
         return cells > 0 && pts < kColumnDensity * cells;
     }
 
+    // KSVM_NFFT_LPT=0 keeps the items in (window, tile) order (A/B knob).
+    static bool lpt_items() {
+        static const bool on = [] {
+            const char* e = std::getenv("KSVM_NFFT_LPT");
+            return !(e && e[0] == '0');
+        }();
+        return on;
+    }
+
     // Assign global item numbers / patch offsets and upload device tables.
     void finalize() {
         const int P = P_owned();
@@ -814,6 +823,27 @@ struct Engine {
                 }
             }
             class_end[D] = static_cast<int>(all.size());
+            // Largest items first: CTAs are dispatched in item order, so the
+            // last wave of a launch holds the smallest items (edge tiles)
+            // instead of whatever the tile order ends with. Patch offsets
+            // travel with the items; the column bounds are permuted alike.
+            if (lpt_items()) {
+                const size_t b = static_cast<size_t>(class_begin[D]), e = all.size();
+                std::vector<size_t> ord(e - b);
+                for (size_t q = 0; q < ord.size(); ++q) ord[q] = b + q;
+                std::stable_sort(ord.begin(), ord.end(), [&](size_t x, size_t y) {
+                    return all[x].end - all[x].begin > all[y].end - all[y].begin;
+                });
+                std::vector<Item> sorted_items(ord.size());
+                std::vector<int> sorted_colb(ord.size() * kColBounds);
+                for (size_t q = 0; q < ord.size(); ++q) {
+                    sorted_items[q] = all[ord[q]];
+                    std::copy_n(colb.begin() + static_cast<long long>(ord[q]) * kColBounds, kColBounds,
+                                sorted_colb.begin() + static_cast<long long>(q) * kColBounds);
+                }
+                std::copy(sorted_items.begin(), sorted_items.end(), all.begin() + static_cast<long long>(b));
+                std::copy(sorted_colb.begin(), sorted_colb.end(), colb.begin() + static_cast<long long>(b) * kColBounds);
+            }
             if (f32_want(D)) {
                 const char* fe = std::getenv("KSVM_NFFT_F32");
                 f32_dense[D] = (fe && std::strcmp(fe, "all") == 0) || !sparse_cells(D);
@@ -837,6 +867,10 @@ struct Engine {
                 }
             }
             gclass_end[D] = static_cast<int>(gall.size());
+            if (lpt_items())
+                std::stable_sort(gall.begin() + gclass_begin[D], gall.end(), [](const Item& x, const Item& y) {
+                    return x.end - x.begin > y.end - y.begin;
+                });
             n_multi_cls[D] = static_cast<int>(multi.size()) - multi_begin[D];
         }
         std::vector<DWin> dws(static_cast<size_t>(P));

@@ -429,6 +429,154 @@ spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
 }
 
 // ===========================================================================
+// d = 3, m = 4 dense-cell spread, split-power form (the default). The tap
+// weights are powers, w1[b] = Q1^b, so with b = 4 b1 + b0 the 8^3 cell block
+// is G[(a, b1), (b0, c)] = sum_p (x_p[a] Y4_p^b1) (Q1_p^b0 z_p[c]),
+// x = P v Q0^a, z = Q2^c, Y4 = Q1^4: a 16 x 32 tile whose operands hold
+// 16 + 32 entries per point, 32 of them products, instead of the 64 + 8
+// (64 products) of G[(a,b), c] above. Per 4 same-cell points: A tiles
+// x, x Y4 (1 DMUL), B tiles z, z Q1, z Q1^2, z Q1^3 (3 DMUL), 2 x 4 = 8 DMMA.
+// Lane l = 4g + t: A[g][t] = A-tile entry (a = g, point t), B[t][g] = B-tile
+// entry (point t, c = g); accumulator (b1, b0) holds G[a = g][b = 4 b1 + b0]
+// [c = 2t..2t+1]. Staging rows are kRow3s = 22 doubles (11 16-byte chunks, odd:
+// conflict-free 128-bit stores): x[8] | z[8] | Q1, Q1^2, Q1^3, Q1^4 | {code, perm}.
+// ===========================================================================
+constexpr int kRow3s = 22;
+
+__device__ __forceinline__ void stage_split3(double* st, double P, const double* Q, int code, int perm) {
+    double2* s2 = reinterpret_cast<double2*>(st);
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {  // x = P Q0^a, z = Q2^c
+        const double q = Q[t == 0 ? 0 : 2];
+        double q0 = t == 0 ? P : 1.0;
+#pragma unroll
+        for (int o = 0; o < 8; o += 2) {
+            const double q1 = q0 * q;
+            s2[(t * 8 + o) >> 1] = make_double2(q0, q1);
+            if (o + 2 < 8) q0 = q1 * q;
+        }
+    }
+    const double y2 = Q[1] * Q[1];
+    s2[8] = make_double2(Q[1], y2);
+    s2[9] = make_double2(y2 * Q[1], y2 * y2);
+    *reinterpret_cast<int2*>(st + 20) = make_int2(code, perm);
+}
+
+template <int W>
+__global__ void __launch_bounds__(W * 32)
+spread3_s8p_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
+                   const DWin* __restrict__ wins, const double* __restrict__ v,
+                   double* __restrict__ patches) {
+    constexpr int PE = 11, PV = PE * PE * PE, RL = kRow3s, B = 32;
+    constexpr unsigned kFull = 0xffffffffu;
+    extern __shared__ __align__(16) double smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    double* wp = smem + warp * PV;
+    double* stage = smem + ((W * PV + 1) & ~1) + warp * B * RL;
+
+    pdl_trigger();
+    const Item it = items[blockIdx.x];
+    const DPSet ps = psets[it.ps];
+    if (ps.vsrc) v = ps.vsrc;  // exact-duplicate window: per-distinct-point sums of v
+    const DWin& wn = wins[ps.win];
+    for (int k = lane; k < PV; k += 32) wp[k] = 0.0;
+    int wb, we;
+    warp_range(it, warp, W, &wb, &we);
+    Pref<3> pa, pb;  // plan data: prefetched before the dependency wait
+    const unsigned long long pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
+    if (wb + lane < we) pa.load(ps, wb + lane, pol_stream);
+    if (wb + B + lane < we) pb.load(ps, wb + B + lane, pol_stream);
+
+    double acc[8][2];  // [4 b1 + b0]
+#pragma unroll
+    for (int r = 0; r < 8; ++r) acc[r][0] = acc[r][1] = 0.0;
+    int cur = -1;
+    auto flush = [&](int cell) {
+        const int l0 = cell >> 4, l1 = (cell >> 2) & 3, l2 = cell & 3;
+        double* dst = wp + ((l0 + g) * PE + l1) * PE + l2 + 2 * t;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {  // b = r
+            dst[r * PE] += acc[r][0];
+            dst[r * PE + 1] += acc[r][1];
+            acc[r][0] = acc[r][1] = 0.0;
+        }
+    };
+    auto mma8 = [&](double xg, double zg, double2 y12, double2 y34) {
+        const double a1 = xg * y34.y, b1 = zg * y12.x, b2 = zg * y12.y, b3 = zg * y34.x;
+        dmma(acc[0][0], acc[0][1], xg, zg);
+        dmma(acc[1][0], acc[1][1], xg, b1);
+        dmma(acc[2][0], acc[2][1], xg, b2);
+        dmma(acc[3][0], acc[3][1], xg, b3);
+        dmma(acc[4][0], acc[4][1], a1, zg);
+        dmma(acc[5][0], acc[5][1], a1, b1);
+        dmma(acc[6][0], acc[6][1], a1, b2);
+        dmma(acc[7][0], acc[7][1], a1, b3);
+    };
+    // 4 points p0..p0+3 of the current cell; lanes t >= nv contribute zero
+    auto group4 = [&](int p0, int nv) {
+        const bool valid = t < nv;
+        const double* st = stage + (p0 + (valid ? t : 0)) * RL;
+        mma8(valid ? st[g] : 0.0, st[8 + g], ld2(st + 16), ld2(st + 18));
+    };
+    auto group4f = [&](int p0) {  // unmasked
+        const double* st = stage + (p0 + t) * RL;
+        mma8(st[g], st[8 + g], ld2(st + 16), ld2(st + 18));
+    };
+
+    // software pipeline: per-point factors two batches ahead, v one batch ahead
+    double va = 0.0;
+    {
+        const int i0 = wb + lane;
+        pdl_wait();  // v may come from the previous kernel (plan factors above did not)
+        v = launder(v);
+        if (i0 < we) va = ld_keep(v + pa.perm, pol_keep);
+    }
+    __syncwarp();
+    for (int base = wb; base < we; base += B) {
+        const int cnt = min(B, we - base);
+        const int code = pa.code;
+        if (lane < cnt) stage_split3(stage + lane * RL, pa.P * va, pa.Q, code, 0);
+        const int prev = __shfl_up_sync(kFull, code, 1);
+        const unsigned same = __ballot_sync(kFull, lane < cnt && code == (lane == 0 ? cur : prev));
+        pa = pb;
+        if (base + B + lane < we) va = ld_keep(v + pa.perm, pol_keep);
+        if (base + 2 * B + lane < we) pb.load(ps, base + 2 * B + lane, pol_stream);
+        __syncwarp();
+        if (same == kFull) {  // the whole batch continues the current cell
+#pragma unroll
+            for (int q = 0; q < B / 4; ++q) group4f(4 * q);
+        } else {
+            int p = 0;
+            while (p < cnt) {
+                if (!((same >> p) & 1u)) {  // a new cell starts at p
+                    if (cur >= 0) flush(cur);
+                    cur = __shfl_sync(kFull, code, p);
+                }
+                int L = run_len(same, p);
+                for (; L >= 8; L -= 8, p += 8) {
+                    group4f(p);
+                    group4f(p + 4);
+                }
+                if (L >= 4) {
+                    group4f(p);
+                    p += 4;
+                    L -= 4;
+                }
+                if (L > 0) {
+                    group4(p, L);
+                    p += L;
+                }
+            }
+        }
+        __syncwarp();
+    }
+    if (cur >= 0) flush(cur);
+    __syncthreads();
+    spread3_epilogue<W, PE>(smem, wn, patches + it.patch);
+}
+
+// ===========================================================================
 // d = 3, m = 4 spread for sparse cells (few points per cell): one accumulator
 // block per cell COLUMN (l0, l1 fixed, l2 = 0..3; consecutive in the sorted
 // order), so the SMEM flush happens once per column instead of once per cell
@@ -680,6 +828,128 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
                 if (o + 2 < 8) q = q1 * pa.Q[2];
             }
             *reinterpret_cast<int2*>(stage + lane * RL + 24) = make_int2(code, pa.perm);
+        }
+        const int prev = __shfl_up_sync(kFull, code, 1);
+        const unsigned same = __ballot_sync(kFull, lane < cnt && code == (lane == 0 ? cur : prev));
+        pa = pb;
+        if (base + 64 + lane < we) pb.load(ps, base + 64 + lane, pol_stream);
+        __syncwarp();
+        if (same == kFull) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) group8(8 * q, 8);
+        } else {
+            int p = 0;
+            while (p < cnt) {
+                if (!((same >> p) & 1u)) {
+                    cur = __shfl_sync(kFull, code, p);
+                    reload(cur);
+                }
+                for (int L = run_len(same, p); L > 0;) {
+                    const int nv = min(L, 8);
+                    group8(p, nv);
+                    p += nv;
+                    L -= nv;
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// ===========================================================================
+// Dense-cell gather, d = 3, m = 4, split-power form (the default). With
+// b = 2 b1 + b0 and Y = Q1:
+//   Z[p, (b0, c)] = sum_{(a, b1)} (x_p[a] Y_p^{2 b1}) H[a, 2 b1 + b0, c]
+//   y_p           = sum_c z_p[c] (Z[p, (0, c)] + Y_p Z[p, (1, c)])
+// M = 8 points, K = 32 (a, b1) in 8 k-steps of 4, N = 16 (b0, c) in two
+// tiles = 16 DMMA per 8 points as above, but the A operand has 32 entries
+// per point (24 products, 6 DMUL per lane) instead of 64, and the epilogue is
+// 5 FP64 instructions per lane. Lane l = 4g + t, k-step s: A[g][t] = x_g[4(s%2) + t]
+// Y_g^{2(s/2)}, B[t][g] = H[4(s%2) + t, 2(s/2) + b0, c = g] (16 values per
+// lane, reloaded per cell), D(b0) holds Z[point g][(b0, 2t..2t+1)].
+// Row: x[8] (P folded) | z[8] | Y^2, Y^4, Y^6, Y | {code, perm}.
+// ===========================================================================
+template <int W, int MINB>
+__global__ void __launch_bounds__(W * 32, MINB)
+gather3_s8p_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
+                    const DWin* __restrict__ wins) {
+    constexpr int S = 8, TC = 4, PE = TC + S - 1, PV = PE * PE * PE, RL = kRow3s;
+    constexpr unsigned kFull = 0xffffffffu;
+    extern __shared__ __align__(16) double smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    double* halo = smem;
+    double* stage = smem + ((PV + 1) & ~1) + warp * 32 * RL;
+
+    pdl_trigger();
+    const Item it = items[blockIdx.x];
+    const DPSet ps = psets[it.ps];
+    const DWin& wn = wins[ps.win];
+    int tc[3];
+    tile_coords(it.tile, 3, wn.ntile, tc);
+    __shared__ double sR[PE];
+    if (threadIdx.x < PE) sR[threadIdx.x] = wn.R[threadIdx.x];
+    int wb, we;
+    warp_range(it, warp, W, &wb, &we);
+    Pref<3> pa, pb;
+    const unsigned long long pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
+    if (wb + lane < we) pa.load(ps, wb + lane, pol_stream);
+    if (wb + 32 + lane < we) pb.load(ps, wb + 32 + lane, pol_stream);
+    __syncthreads();
+    pdl_wait();
+    load_halo3_r<PE, TC>(halo, *launder(&wn), tc, sR);
+    __syncthreads();
+
+    double hb[16];  // [2 s + b0]
+#pragma unroll
+    for (int k = 0; k < 16; ++k) hb[k] = 0.0;
+    int cur = -1;
+    auto reload = [&](int cell) {
+        const int l0 = cell >> 4, l1 = (cell >> 2) & 3, l2 = cell & 3;
+        const double* src = halo + ((l0 + t) * PE + l1) * PE + l2 + g;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) hb[k] = src[4 * ((k >> 1) & 1) * PE * PE + (2 * (k >> 2) + (k & 1)) * PE];
+    };
+    auto group8 = [&](int p0, int nv) {
+        const bool vg = g < nv;
+        const double* sg = stage + (p0 + (vg ? g : 0)) * RL;
+        const double xa = vg ? sg[t] : 0.0, xb = vg ? sg[4 + t] : 0.0;
+        const double2 y24 = ld2(sg + 16), y6y = ld2(sg + 18);
+        const double A[8] = {xa, xb, xa * y24.x, xb * y24.x, xa * y24.y, xb * y24.y, xa * y6y.x, xb * y6y.x};
+        double z[2][2] = {{0, 0}, {0, 0}};
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+            dmma(z[0][0], z[0][1], A[s], hb[2 * s]);
+            dmma(z[1][0], z[1][1], A[s], hb[2 * s + 1]);
+        }
+        const double2 w2 = ld2(sg + 8 + 2 * t);
+        const double e0 = fma(z[0][0], w2.x, z[0][1] * w2.y), e1 = fma(z[1][0], w2.x, z[1][1] * w2.y);
+        double part = fma(y6y.y, e1, e0);
+        part += __shfl_xor_sync(kFull, part, 1);
+        part += __shfl_xor_sync(kFull, part, 2);
+        if (t == 0 && vg) st_keep(ps.out + reinterpret_cast<const int*>(sg + 20)[1], part, pol_keep);
+    };
+
+    for (int base = wb; base < we; base += 32) {
+        const int cnt = min(32, we - base);
+        const int code = pa.code;
+        if (lane < cnt) {
+            double2* s2 = reinterpret_cast<double2*>(stage + lane * RL);
+#pragma unroll
+            for (int d = 0; d < 2; ++d) {
+                const double qd = pa.Q[d == 0 ? 0 : 2];
+                double q = d == 0 ? pa.P : 1.0;
+#pragma unroll
+                for (int o = 0; o < 8; o += 2) {
+                    const double q1 = q * qd;
+                    s2[(d * 8 + o) >> 1] = make_double2(q, q1);
+                    if (o + 2 < 8) q = q1 * qd;
+                }
+            }
+            const double y2 = pa.Q[1] * pa.Q[1], y4 = y2 * y2;
+            s2[8] = make_double2(y2, y4);
+            s2[9] = make_double2(y4 * y2, pa.Q[1]);
+            *reinterpret_cast<int2*>(stage + lane * RL + 20) = make_int2(code, pa.perm);
         }
         const int prev = __shfl_up_sync(kFull, code, 1);
         const unsigned same = __ballot_sync(kFull, lane < cnt && code == (lane == 0 ? cur : prev));
@@ -1889,6 +2159,16 @@ size_t gather3c_smem() { return sizeof(double) * (8 * 121 + 4 * 32 * kCol3Row); 
 size_t spread3c_smem() { return sizeof(double) * (kColWarps * (kCol3Sub + 32 * kCol3Row)); }
 size_t spread3_smem(int B) { return sizeof(double) * (((kW3 * 1331 + 1) & ~1) + kW3 * B * kRow3); }
 size_t gather3_smem() { return sizeof(double) * (1332 + kW3 * 32 * kRow3); }
+size_t spread3p_smem() { return sizeof(double) * (((kW3 * 1331 + 1) & ~1) + kW3 * 32 * kRow3s); }
+size_t gather3p_smem() { return sizeof(double) * (1332 + kW3 * 32 * kRow3s); }
+// dense d = 3 kernels: split-power form unless KSVM_NFFT_D3=pair (A/B knob)
+bool d3_split() {
+    static const bool on = [] {
+        const char* e = std::getenv("KSVM_NFFT_D3");
+        return !(e && e[0] == 'p');
+    }();
+    return on;
+}
 size_t spread2_smem() { return sizeof(double) * (((kW2 * 225 + 1) & ~1) + kW2 * 32 * Row<2, 8>::kLen); }
 size_t gather2_smem() { return sizeof(double) * (226 + kW2 * 32 * Row<2, 8>::kLen); }
 size_t spread1_smem() { return sizeof(double) * (kW1 * 39 * 32); }
@@ -1924,6 +2204,9 @@ cudaError_t init_kernel_attributes() {
     set(reinterpret_cast<const void*>(spread3c_s8_kernel), spread3c_smem());
     set(reinterpret_cast<const void*>(gather3c_s8_kernel), gather3c_smem());
     set(reinterpret_cast<const void*>(gather3_s8_kernel<kW3>), gather3_smem());
+    set(reinterpret_cast<const void*>(spread3_s8p_kernel<kW3>), spread3p_smem());
+    set(reinterpret_cast<const void*>(gather3_s8p_kernel<kW3, 4>), gather3p_smem());
+    set(reinterpret_cast<const void*>(gather3_s8p_kernel<kW3, 5>), gather3p_smem());
     set(reinterpret_cast<const void*>(spread2_s8_kernel<kW2>), spread2_smem());
     set(reinterpret_cast<const void*>(gather2_s8_kernel<kW2>), gather2_smem());
     set(reinterpret_cast<const void*>(spread1_s8_kernel<kW1>), spread1_smem());
@@ -1951,7 +2234,10 @@ void launch_spread(int D, int S, int PE, const Item* items, int nitems, const DP
                 const char* e = std::getenv("KSVM_NFFT_S3B");
                 return e && std::atoi(e) == 16 ? 16 : 32;
             }();
-            if (B == 16)
+            if (d3_split())
+                launch_k(spread3_s8p_kernel<kW3>, dim3(nitems), dim3(kW3 * 32), spread3p_smem(), st, items, ps, wins, v,
+                         patches);
+            else if (B == 16)
                 launch_k(spread3_s8_kernel<kW3, 16>, dim3(nitems), dim3(kW3 * 32), spread3_smem(16), st, items, ps,
                          wins, v, patches);
             else
@@ -1983,7 +2269,17 @@ void launch_gather(int D, int S, int PE, const Item* items, int nitems, const DP
                    const DWin* wins, cudaStream_t st) {
     if (nitems == 0) return;
     if (S == 8) {
-        if (D == 3) launch_k(gather3_s8_kernel<kW3>, dim3(nitems), dim3(kW3 * 32), gather3_smem(), st, items, ps, wins);
+        if (D == 3 && d3_split()) {
+            static const bool occ5 = [] {  // CTAs per SM the register allocation targets (A/B knob)
+                const char* e = std::getenv("KSVM_NFFT_G3OCC");
+                return e && std::atoi(e) == 5;
+            }();
+            if (occ5)
+                launch_k(gather3_s8p_kernel<kW3, 5>, dim3(nitems), dim3(kW3 * 32), gather3p_smem(), st, items, ps, wins);
+            else
+                launch_k(gather3_s8p_kernel<kW3, 4>, dim3(nitems), dim3(kW3 * 32), gather3p_smem(), st, items, ps, wins);
+        }
+        else if (D == 3) launch_k(gather3_s8_kernel<kW3>, dim3(nitems), dim3(kW3 * 32), gather3_smem(), st, items, ps, wins);
         else if (D == 2) launch_k(gather2_s8_kernel<kW2>, dim3(nitems), dim3(kW2 * 32), gather2_smem(), st, items, ps, wins);
         else launch_k(gather1_s8_kernel<kW1>, dim3(nitems), dim3(kW1 * 32), gather1_smem(), st, items, ps, wins);
         return;
