@@ -260,43 +260,35 @@ __device__ __forceinline__ void spread3_epilogue(const double* smem, const DWin&
 }
 
 // ===========================================================================
-// d = 3, m = 4 (S = 8) on the FP64 tensor cores.
-// The 8^3 block of one cell is G[(a,b), c] with a, b, c in 0..7. Spread adds
-// sum_p U[(a,b), p] W2[p, c] with U = (v P w0[a]) w1[b]: eight 8x8 tiles
-// (one per a), K = 4 points of the cell per DMMA. Points are sorted by cell;
-// a group is the run of <= 4 consecutive points in the current cell (the
-// rest of the group is masked to zero and handled next round).
-// Lane l = 4g + t: A[g][t] = U[(r, g), point t], B[t][g] = W2[point t][g],
-// accumulator tile r holds G[(r, g), 2t..2t+1].
+// d = 3, m = 4 (S = 8), dense cells, on the FP64 tensor cores (DMMA.8x8x4).
+// The tap weights are powers, w_t[o] = Q_t^o (the per-node factor R[o] is
+// applied at flush / halo load), so with b = 4 b1 + b0 the 8^3 block of one
+// cell is
+//   G[(a, b1), (b0, c)] = sum_p (x_p[a] Y4_p^b1) (Q1_p^b0 z_p[c]),
+//   x = P v Q0^a, z = Q2^c, Y4 = Q1^4:
+// a 16 x 32 tile whose operands hold 16 + 32 entries per point, 32 of them
+// products. (The plain form G[(a,b), c] = sum_p (x[a] w1[b]) z[c] needs 64
+// products per point; each DMUL costs 4-6 cycles of the FP64 datapath it
+// shares with DMMA, scripts/micro/dmma_interleave.cu, and the split form took
+// config 5's spread from 3.77 to 3.26 ms.) Per 4 same-cell points: A tiles
+// x, x Y4 (1 DMUL), B tiles z, z Q1, z Q1^2, z Q1^3 (3 DMUL), 2 x 4 = 8 DMMA,
+// K = the 4 points. Points are sorted by cell; a group is the run of <= 4
+// consecutive points in the current cell (the rest of the group is masked to
+// zero and handled next round).
+// Lane l = 4g + t: A[g][t] = A-tile entry (a = g, point t), B[t][g] = B-tile
+// entry (point t, c = g); accumulator (b1, b0) holds G[a = g][b = 4 b1 + b0]
+// [c = 2t..2t+1].
 //
-// Staging rows are kRow3 = 26 doubles (13 16-byte chunks; 13 is odd, so the
+// Staging rows are kRow3s = 22 doubles (11 16-byte chunks; 11 is odd, so the
 // 8 rows a quarter warp stores land in 8 different chunk slots mod 8 and the
-// 128-bit staging stores are bank-conflict free; the 4 rows a group reads
-// are distinct chunk slots too). The run structure of a 32-point batch
-// (which points continue the cell of their predecessor) is one ballot, so
-// the DMMA loop carries no shared-memory loads of cell codes; a batch that
-// lies entirely in the current cell (the common case for dense data) runs
-// eight unmasked groups with no control flow.
+// 128-bit staging stores are bank-conflict free):
+// x[8] | z[8] | Q1, Q1^2, Q1^3, Q1^4 | {code, perm}. The run structure of a
+// 32-point batch (which points continue the cell of their predecessor) is one
+// ballot, so the DMMA loop carries no shared-memory loads of cell codes; a
+// batch that lies entirely in the current cell (the common case for dense
+// data) runs eight unmasked groups with no control flow.
 // ===========================================================================
-constexpr int kRow3 = 26;  // w0[8] | w1[8] | w2[8] | {code, perm}
-
-// Power rows of one point, written as 128-bit pairs: w0[o] = P Q0^o,
-// w1[o] = Q1^o, w2[o] = Q2^o (the per-node factor R[o] is applied at flush /
-// halo load), then {code, perm}. Same product sequence as stage_pow.
-__device__ __forceinline__ void stage_pow3(double* st, double P, const double* Q, int code, int perm) {
-    double2* s2 = reinterpret_cast<double2*>(st);
-#pragma unroll
-    for (int t = 0; t < 3; ++t) {
-        double q0 = t == 0 ? P : 1.0;
-#pragma unroll
-        for (int o = 0; o < 8; o += 2) {
-            const double q1 = q0 * Q[t];
-            s2[(t * 8 + o) >> 1] = make_double2(q0, q1);
-            if (o + 2 < 8) q0 = q1 * Q[t];
-        }
-    }
-    *reinterpret_cast<int2*>(st + 24) = make_int2(code, perm);
-}
+constexpr int kRow3s = 22;
 
 // Length of the run of same-cell points starting at p: bit q of `same` says
 // point q continues the cell of point q - 1.
@@ -304,144 +296,6 @@ __device__ __forceinline__ int run_len(unsigned same, int p) {
     const unsigned s = p + 1 < 32 ? (same >> (p + 1)) : 0u;
     return __ffs(~s);  // 1 + number of consecutive set bits above p
 }
-
-template <int W, int B>
-__global__ void __launch_bounds__(W * 32)
-spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
-                  const DWin* __restrict__ wins, const double* __restrict__ v,
-                  double* __restrict__ patches) {
-    constexpr int S = 8, PE = 11, PV = PE * PE * PE, RL = kRow3;
-    constexpr unsigned kFull = 0xffffffffu;
-    extern __shared__ __align__(16) double smem[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int g = lane >> 2, t = lane & 3;
-    double* wp = smem + warp * PV;
-    static_assert(B == 16 || B == 32, "points per staging batch");
-    constexpr unsigned kBatch = B == 32 ? kFull : (1u << B) - 1u;
-    double* stage = smem + ((W * PV + 1) & ~1) + warp * B * RL;
-
-    pdl_trigger();
-    const Item it = items[blockIdx.x];
-    const DPSet ps = psets[it.ps];
-    if (ps.vsrc) v = ps.vsrc;  // exact-duplicate window: per-distinct-point sums of v
-    const DWin& wn = wins[ps.win];
-    for (int k = lane; k < PV; k += 32) wp[k] = 0.0;
-    int wb, we;
-    warp_range(it, warp, W, &wb, &we);
-    Pref<3> pa, pb;  // plan data: prefetched before the dependency wait
-    const unsigned long long pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
-    if (lane < B && wb + lane < we) pa.load(ps, wb + lane, pol_stream);
-    if (lane < B && wb + B + lane < we) pb.load(ps, wb + B + lane, pol_stream);
-
-    double acc[8][2];
-#pragma unroll
-    for (int r = 0; r < 8; ++r) acc[r][0] = acc[r][1] = 0.0;
-    int cur = -1;
-    auto flush = [&](int cell) {
-        const int l0 = cell >> 4, l1 = (cell >> 2) & 3, l2 = cell & 3;
-        double* dst = wp + (l0 * PE + l1 + g) * PE + l2 + 2 * t;
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            dst[r * PE * PE] += acc[r][0];
-            dst[r * PE * PE + 1] += acc[r][1];
-            acc[r][0] = acc[r][1] = 0.0;
-        }
-    };
-    // 4 points p0..p0+3 of the current cell; lanes t >= nv contribute zero
-    auto group4 = [&](int p0, int nv) {
-        const bool valid = t < nv;
-        const double* st = stage + (p0 + (valid ? t : 0)) * RL;
-        const double2 w01 = ld2(st), w23 = ld2(st + 2), w45 = ld2(st + 4), w67 = ld2(st + 6);
-        const double w1g = valid ? st[S + g] : 0.0, bq = valid ? st[2 * S + g] : 0.0;
-        dmma(acc[0][0], acc[0][1], w01.x * w1g, bq);
-        dmma(acc[1][0], acc[1][1], w01.y * w1g, bq);
-        dmma(acc[2][0], acc[2][1], w23.x * w1g, bq);
-        dmma(acc[3][0], acc[3][1], w23.y * w1g, bq);
-        dmma(acc[4][0], acc[4][1], w45.x * w1g, bq);
-        dmma(acc[5][0], acc[5][1], w45.y * w1g, bq);
-        dmma(acc[6][0], acc[6][1], w67.x * w1g, bq);
-        dmma(acc[7][0], acc[7][1], w67.y * w1g, bq);
-    };
-    auto group4f = [&](int p0) {  // unmasked
-        const double* st = stage + (p0 + t) * RL;
-        const double2 w01 = ld2(st), w23 = ld2(st + 2), w45 = ld2(st + 4), w67 = ld2(st + 6);
-        const double w1g = st[S + g], bq = st[2 * S + g];
-        dmma(acc[0][0], acc[0][1], w01.x * w1g, bq);
-        dmma(acc[1][0], acc[1][1], w01.y * w1g, bq);
-        dmma(acc[2][0], acc[2][1], w23.x * w1g, bq);
-        dmma(acc[3][0], acc[3][1], w23.y * w1g, bq);
-        dmma(acc[4][0], acc[4][1], w45.x * w1g, bq);
-        dmma(acc[5][0], acc[5][1], w45.y * w1g, bq);
-        dmma(acc[6][0], acc[6][1], w67.x * w1g, bq);
-        dmma(acc[7][0], acc[7][1], w67.y * w1g, bq);
-    };
-
-    // software pipeline: per-point factors two batches ahead, v one batch ahead
-    double va = 0.0;
-    {
-        const int i0 = wb + lane;
-        pdl_wait();  // v may come from the previous kernel (plan factors above did not)
-        v = launder(v);
-        if (lane < B && i0 < we) va = ld_keep(v + pa.perm, pol_keep);
-    }
-    __syncwarp();
-    for (int base = wb; base < we; base += B) {
-        const int cnt = min(B, we - base);
-        const int code = pa.code;
-        if (lane < cnt) stage_pow3(stage + lane * RL, pa.P * va, pa.Q, code, 0);
-        const int prev = __shfl_up_sync(kFull, code, 1);
-        const unsigned same = __ballot_sync(kFull, lane < cnt && code == (lane == 0 ? cur : prev));
-        pa = pb;
-        if (lane < B && base + B + lane < we) va = ld_keep(v + pa.perm, pol_keep);
-        if (lane < B && base + 2 * B + lane < we) pb.load(ps, base + 2 * B + lane, pol_stream);
-        __syncwarp();
-        if (same == kBatch) {  // the whole batch continues the current cell
-#pragma unroll
-            for (int q = 0; q < B / 4; ++q) group4f(4 * q);
-        } else {
-            int p = 0;
-            while (p < cnt) {
-                if (!((same >> p) & 1u)) {  // a new cell starts at p
-                    if (cur >= 0) flush(cur);
-                    cur = __shfl_sync(kFull, code, p);
-                }
-                int L = run_len(same, p);
-                for (; L >= 8; L -= 8, p += 8) {
-                    group4f(p);
-                    group4f(p + 4);
-                }
-                if (L >= 4) {
-                    group4f(p);
-                    p += 4;
-                    L -= 4;
-                }
-                if (L > 0) {
-                    group4(p, L);
-                    p += L;
-                }
-            }
-        }
-        __syncwarp();
-    }
-    if (cur >= 0) flush(cur);
-    __syncthreads();
-    spread3_epilogue<W, PE>(smem, wn, patches + it.patch);
-}
-
-// ===========================================================================
-// d = 3, m = 4 dense-cell spread, split-power form (the default). The tap
-// weights are powers, w1[b] = Q1^b, so with b = 4 b1 + b0 the 8^3 cell block
-// is G[(a, b1), (b0, c)] = sum_p (x_p[a] Y4_p^b1) (Q1_p^b0 z_p[c]),
-// x = P v Q0^a, z = Q2^c, Y4 = Q1^4: a 16 x 32 tile whose operands hold
-// 16 + 32 entries per point, 32 of them products, instead of the 64 + 8
-// (64 products) of G[(a,b), c] above. Per 4 same-cell points: A tiles
-// x, x Y4 (1 DMUL), B tiles z, z Q1, z Q1^2, z Q1^3 (3 DMUL), 2 x 4 = 8 DMMA.
-// Lane l = 4g + t: A[g][t] = A-tile entry (a = g, point t), B[t][g] = B-tile
-// entry (point t, c = g); accumulator (b1, b0) holds G[a = g][b = 4 b1 + b0]
-// [c = 2t..2t+1]. Staging rows are kRow3s = 22 doubles (11 16-byte chunks, odd:
-// conflict-free 128-bit stores): x[8] | z[8] | Q1, Q1^2, Q1^3, Q1^4 | {code, perm}.
-// ===========================================================================
-constexpr int kRow3s = 22;
 
 __device__ __forceinline__ void stage_split3(double* st, double P, const double* Q, int code, int perm) {
     double2* s2 = reinterpret_cast<double2*>(st);
@@ -464,10 +318,10 @@ __device__ __forceinline__ void stage_split3(double* st, double P, const double*
 
 template <int W>
 __global__ void __launch_bounds__(W * 32)
-spread3_s8p_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
+spread3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
                    const DWin* __restrict__ wins, const double* __restrict__ v,
                    double* __restrict__ patches) {
-    constexpr int PE = 11, PV = PE * PE * PE, RL = kRow3s, B = 32;
+    constexpr int PE = 11, PV = PE * PE * PE, RL = kRow3s, B = 32;  // B: points per staging batch
     constexpr unsigned kFull = 0xffffffffu;
     extern __shared__ __align__(16) double smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -726,137 +580,6 @@ spread3c_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pse
 }
 
 // ===========================================================================
-// Gather, d = 3, m = 4, on the FP64 tensor cores, 8 same-cell points per round:
-//   Z[p, c] = sum_{(a,b)} U[p, (a,b)] H[(a,b), c],  U[p, (a,b)] = P_p w0_p[a] w1_p[b]
-//   y_p     = sum_c Z[p, c] w2_p[c]
-// M = 8 points, N = c, K = 64 (a,b) pairs in 16 k-steps of 4, split over two
-// accumulators (dependent DMMAs two issues apart, past the DMMA latency;
-// fixed combine order). Lane l = 4g + t: A[g][t] = U[point g, (k/2,
-// 4(k%2)+t)] (one DMUL each), B[t][g] = H[(k/2, 4(k%2)+t), c=g] (16 values,
-// reloaded per cell), D holds Z[point g][2t..2t+1]; the c-sum is a 2-step
-// xor over t. (Contracting dimension 0 on the tensor cores with A = P w0
-// directly and dimensions 1, 2 per point needs fewer FP64 instructions, 20
-// vs 22 per 16 DMMA, but measured 5 % slower: 3.95 vs 3.75 ms at config 5.)
-//
-// Staging as in spread3_s8 (kRow3 rows, conflict-free 128-bit stores), row =
-// P w0[0..7] | (w1[t], w1[t+4]) pairs | w2[0..7] | {code, perm}; runs of
-// same-cell points come from one ballot per batch and a batch entirely in
-// the current cell runs four unmasked 8-point rounds.
-// ===========================================================================
-template <int W>
-__global__ void __launch_bounds__(W * 32, 4)
-gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
-                   const DWin* __restrict__ wins) {
-    constexpr int S = 8, TC = 4, PE = TC + S - 1, PV = PE * PE * PE, RL = kRow3;
-    constexpr unsigned kFull = 0xffffffffu;
-    extern __shared__ __align__(16) double smem[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int g = lane >> 2, t = lane & 3;
-    double* halo = smem;
-    double* stage = smem + ((PV + 1) & ~1) + warp * 32 * RL;
-
-    pdl_trigger();
-    const Item it = items[blockIdx.x];
-    const DPSet ps = psets[it.ps];
-    const DWin& wn = wins[ps.win];
-    int tc[3];
-    tile_coords(it.tile, 3, wn.ntile, tc);
-    __shared__ double sR[PE];
-    if (threadIdx.x < PE) sR[threadIdx.x] = wn.R[threadIdx.x];
-    int wb, we;
-    warp_range(it, warp, W, &wb, &we);
-    Pref<3> pa, pb;
-    const unsigned long long pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
-    if (wb + lane < we) pa.load(ps, wb + lane, pol_stream);
-    if (wb + 32 + lane < we) pb.load(ps, wb + 32 + lane, pol_stream);
-    __syncthreads();
-    pdl_wait();
-    load_halo3_r<PE, TC>(halo, *launder(&wn), tc, sR);
-    __syncthreads();
-
-    double hb[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) hb[k] = 0.0;
-    int cur = -1;
-    auto reload = [&](int cell) {
-        const int l0 = cell >> 4, l1 = (cell >> 2) & 3, l2 = cell & 3;
-        const double* src = halo + (l0 * PE + l1 + t) * PE + l2 + g;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) hb[k] = src[(k >> 1) * PE * PE + 4 * (k & 1) * PE];
-    };
-    auto group8 = [&](int p0, int nv) {
-        const bool vg = g < nv;
-        const double* sg = stage + (p0 + (vg ? g : 0)) * RL;
-        const double2 w01 = ld2(sg), w23 = ld2(sg + 2), w45 = ld2(sg + 4), w67 = ld2(sg + 6);
-        const double w0[8] = {w01.x, w01.y, w23.x, w23.y, w45.x, w45.y, w67.x, w67.y};
-        const double2 uu = ld2(sg + S + 2 * t);
-        const double u0 = vg ? uu.x : 0.0, u1 = vg ? uu.y : 0.0;
-        const double2 w2 = ld2(sg + 2 * S + 2 * t);
-        double z[2][2] = {{0, 0}, {0, 0}};
-#pragma unroll
-        for (int k = 0; k < 16; ++k) dmma(z[k & 1][0], z[k & 1][1], w0[k >> 1] * ((k & 1) ? u1 : u0), hb[k]);
-        const double z0 = z[0][0] + z[1][0], z1 = z[0][1] + z[1][1];
-        double part = fma(z0, w2.x, z1 * w2.y);
-        part += __shfl_xor_sync(kFull, part, 1);
-        part += __shfl_xor_sync(kFull, part, 2);
-        if (t == 0 && vg) st_keep(ps.out + reinterpret_cast<const int*>(sg + 24)[1], part, pol_keep);
-    };
-
-    for (int base = wb; base < we; base += 32) {
-        const int cnt = min(32, we - base);
-        const int code = pa.code;
-        if (lane < cnt) {
-            double2* s2 = reinterpret_cast<double2*>(stage + lane * RL);
-            double q = pa.P;
-#pragma unroll
-            for (int o = 0; o < 8; o += 2) {
-                const double q1 = q * pa.Q[0];
-                s2[o >> 1] = make_double2(q, q1);
-                if (o + 2 < 8) q = q1 * pa.Q[0];
-            }
-            double w1[8];
-            w1[0] = 1.0;
-#pragma unroll
-            for (int o = 1; o < 8; ++o) w1[o] = w1[o - 1] * pa.Q[1];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) s2[4 + j] = make_double2(w1[j], w1[j + 4]);
-            q = 1.0;
-#pragma unroll
-            for (int o = 0; o < 8; o += 2) {
-                const double q1 = q * pa.Q[2];
-                s2[8 + (o >> 1)] = make_double2(q, q1);
-                if (o + 2 < 8) q = q1 * pa.Q[2];
-            }
-            *reinterpret_cast<int2*>(stage + lane * RL + 24) = make_int2(code, pa.perm);
-        }
-        const int prev = __shfl_up_sync(kFull, code, 1);
-        const unsigned same = __ballot_sync(kFull, lane < cnt && code == (lane == 0 ? cur : prev));
-        pa = pb;
-        if (base + 64 + lane < we) pb.load(ps, base + 64 + lane, pol_stream);
-        __syncwarp();
-        if (same == kFull) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) group8(8 * q, 8);
-        } else {
-            int p = 0;
-            while (p < cnt) {
-                if (!((same >> p) & 1u)) {
-                    cur = __shfl_sync(kFull, code, p);
-                    reload(cur);
-                }
-                for (int L = run_len(same, p); L > 0;) {
-                    const int nv = min(L, 8);
-                    group8(p, nv);
-                    p += nv;
-                    L -= nv;
-                }
-            }
-        }
-        __syncwarp();
-    }
-}
-
-// ===========================================================================
 // Dense-cell gather, d = 3, m = 4, split-power form (the default). With
 // b = 2 b1 + b0 and Y = Q1:
 //   Z[p, (b0, c)] = sum_{(a, b1)} (x_p[a] Y_p^{2 b1}) H[a, 2 b1 + b0, c]
@@ -869,9 +592,9 @@ gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pset
 // lane, reloaded per cell), D(b0) holds Z[point g][(b0, 2t..2t+1)].
 // Row: x[8] (P folded) | z[8] | Y^2, Y^4, Y^6, Y | {code, perm}.
 // ===========================================================================
-template <int W, int MINB>
-__global__ void __launch_bounds__(W * 32, MINB)
-gather3_s8p_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
+template <int W>
+__global__ void __launch_bounds__(W * 32, 4)
+gather3_s8_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
                     const DWin* __restrict__ wins) {
     constexpr int S = 8, TC = 4, PE = TC + S - 1, PV = PE * PE * PE, RL = kRow3s;
     constexpr unsigned kFull = 0xffffffffu;
@@ -910,9 +633,8 @@ gather3_s8p_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pse
 #pragma unroll
         for (int k = 0; k < 16; ++k) hb[k] = src[4 * ((k >> 1) & 1) * PE * PE + (2 * (k >> 2) + (k & 1)) * PE];
     };
-    auto group8 = [&](int p0, int nv) {
-        const bool vg = g < nv;
-        const double* sg = stage + (p0 + (vg ? g : 0)) * RL;
+    // one 8-point round; returns lane (g, t)'s share of point g's sum (c = 2t, 2t+1)
+    auto round8 = [&](const double* sg, bool vg) {
         const double xa = vg ? sg[t] : 0.0, xb = vg ? sg[4 + t] : 0.0;
         const double2 y24 = ld2(sg + 16), y6y = ld2(sg + 18);
         const double A[8] = {xa, xb, xa * y24.x, xb * y24.x, xa * y24.y, xb * y24.y, xa * y6y.x, xb * y6y.x};
@@ -924,10 +646,29 @@ gather3_s8p_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pse
         }
         const double2 w2 = ld2(sg + 8 + 2 * t);
         const double e0 = fma(z[0][0], w2.x, z[0][1] * w2.y), e1 = fma(z[1][0], w2.x, z[1][1] * w2.y);
-        double part = fma(y6y.y, e1, e0);
+        return fma(y6y.y, e1, e0);
+    };
+    auto group8 = [&](int p0, int nv) {
+        const bool vg = g < nv;
+        const double* sg = stage + (p0 + (vg ? g : 0)) * RL;
+        double part = round8(sg, vg);
         part += __shfl_xor_sync(kFull, part, 1);
         part += __shfl_xor_sync(kFull, part, 2);
         if (t == 0 && vg) st_keep(ps.out + reinterpret_cast<const int*>(sg + 20)[1], part, pol_keep);
+    };
+    // a full batch in one cell: four rounds, then one transposed butterfly
+    // over t (3 adds instead of 8); lane (g, t) ends with the sum of point
+    // 8 j + g, j = 2 (t & 1) + (t >> 1), and all 32 lanes store.
+    auto batch32 = [&]() {
+        double q[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) q[j] = round8(stage + (8 * j + g) * RL, true);
+        const bool odd = (t & 1) != 0, hi = (t & 2) != 0;
+        const double k0 = (odd ? q[2] : q[0]) + __shfl_xor_sync(kFull, odd ? q[0] : q[2], 1);
+        const double k1 = (odd ? q[3] : q[1]) + __shfl_xor_sync(kFull, odd ? q[1] : q[3], 1);
+        const double sum = (hi ? k1 : k0) + __shfl_xor_sync(kFull, hi ? k0 : k1, 2);
+        const int j = 2 * (t & 1) + (t >> 1);
+        st_keep(ps.out + reinterpret_cast<const int*>(stage + (8 * j + g) * RL + 20)[1], sum, pol_keep);
     };
 
     for (int base = wb; base < we; base += 32) {
@@ -957,8 +698,7 @@ gather3_s8p_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pse
         if (base + 64 + lane < we) pb.load(ps, base + 64 + lane, pol_stream);
         __syncwarp();
         if (same == kFull) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) group8(8 * q, 8);
+            batch32();
         } else {
             int p = 0;
             while (p < cnt) {
@@ -2157,18 +1897,8 @@ constexpr int kW1 = 8;
 
 size_t gather3c_smem() { return sizeof(double) * (8 * 121 + 4 * 32 * kCol3Row); }
 size_t spread3c_smem() { return sizeof(double) * (kColWarps * (kCol3Sub + 32 * kCol3Row)); }
-size_t spread3_smem(int B) { return sizeof(double) * (((kW3 * 1331 + 1) & ~1) + kW3 * B * kRow3); }
-size_t gather3_smem() { return sizeof(double) * (1332 + kW3 * 32 * kRow3); }
-size_t spread3p_smem() { return sizeof(double) * (((kW3 * 1331 + 1) & ~1) + kW3 * 32 * kRow3s); }
-size_t gather3p_smem() { return sizeof(double) * (1332 + kW3 * 32 * kRow3s); }
-// dense d = 3 kernels: split-power form unless KSVM_NFFT_D3=pair (A/B knob)
-bool d3_split() {
-    static const bool on = [] {
-        const char* e = std::getenv("KSVM_NFFT_D3");
-        return !(e && e[0] == 'p');
-    }();
-    return on;
-}
+size_t spread3_smem() { return sizeof(double) * (((kW3 * 1331 + 1) & ~1) + kW3 * 32 * kRow3s); }
+size_t gather3_smem() { return sizeof(double) * (1332 + kW3 * 32 * kRow3s); }
 size_t spread2_smem() { return sizeof(double) * (((kW2 * 225 + 1) & ~1) + kW2 * 32 * Row<2, 8>::kLen); }
 size_t gather2_smem() { return sizeof(double) * (226 + kW2 * 32 * Row<2, 8>::kLen); }
 size_t spread1_smem() { return sizeof(double) * (kW1 * 39 * 32); }
@@ -2199,14 +1929,10 @@ cudaError_t init_kernel_attributes() {
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
     };
-    set(reinterpret_cast<const void*>(spread3_s8_kernel<kW3, 32>), spread3_smem(32));
-    set(reinterpret_cast<const void*>(spread3_s8_kernel<kW3, 16>), spread3_smem(16));
+    set(reinterpret_cast<const void*>(spread3_s8_kernel<kW3>), spread3_smem());
     set(reinterpret_cast<const void*>(spread3c_s8_kernel), spread3c_smem());
     set(reinterpret_cast<const void*>(gather3c_s8_kernel), gather3c_smem());
     set(reinterpret_cast<const void*>(gather3_s8_kernel<kW3>), gather3_smem());
-    set(reinterpret_cast<const void*>(spread3_s8p_kernel<kW3>), spread3p_smem());
-    set(reinterpret_cast<const void*>(gather3_s8p_kernel<kW3, 4>), gather3p_smem());
-    set(reinterpret_cast<const void*>(gather3_s8p_kernel<kW3, 5>), gather3p_smem());
     set(reinterpret_cast<const void*>(spread2_s8_kernel<kW2>), spread2_smem());
     set(reinterpret_cast<const void*>(gather2_s8_kernel<kW2>), gather2_smem());
     set(reinterpret_cast<const void*>(spread1_s8_kernel<kW1>), spread1_smem());
@@ -2229,21 +1955,9 @@ void launch_spread(int D, int S, int PE, const Item* items, int nitems, const DP
         if (D == 3 && colb)
             launch_k(spread3c_s8_kernel, dim3(nitems), dim3(kColWarps * 32), spread3c_smem(), st, items, ps, wins, v,
                      patches, colb);
-        else if (D == 3) {
-            static const int B = [] {  // points per staging batch (A/B knob, default 32)
-                const char* e = std::getenv("KSVM_NFFT_S3B");
-                return e && std::atoi(e) == 16 ? 16 : 32;
-            }();
-            if (d3_split())
-                launch_k(spread3_s8p_kernel<kW3>, dim3(nitems), dim3(kW3 * 32), spread3p_smem(), st, items, ps, wins, v,
-                         patches);
-            else if (B == 16)
-                launch_k(spread3_s8_kernel<kW3, 16>, dim3(nitems), dim3(kW3 * 32), spread3_smem(16), st, items, ps,
-                         wins, v, patches);
-            else
-                launch_k(spread3_s8_kernel<kW3, 32>, dim3(nitems), dim3(kW3 * 32), spread3_smem(32), st, items, ps,
-                         wins, v, patches);
-        }
+        else if (D == 3)
+            launch_k(spread3_s8_kernel<kW3>, dim3(nitems), dim3(kW3 * 32), spread3_smem(), st, items, ps, wins, v,
+                     patches);
         else if (D == 2)
             launch_k(spread2_s8_kernel<kW2>, dim3(nitems), dim3(kW2 * 32), spread2_smem(), st, items, ps, wins, v, patches);
         else
@@ -2269,17 +1983,7 @@ void launch_gather(int D, int S, int PE, const Item* items, int nitems, const DP
                    const DWin* wins, cudaStream_t st) {
     if (nitems == 0) return;
     if (S == 8) {
-        if (D == 3 && d3_split()) {
-            static const bool occ5 = [] {  // CTAs per SM the register allocation targets (A/B knob)
-                const char* e = std::getenv("KSVM_NFFT_G3OCC");
-                return e && std::atoi(e) == 5;
-            }();
-            if (occ5)
-                launch_k(gather3_s8p_kernel<kW3, 5>, dim3(nitems), dim3(kW3 * 32), gather3p_smem(), st, items, ps, wins);
-            else
-                launch_k(gather3_s8p_kernel<kW3, 4>, dim3(nitems), dim3(kW3 * 32), gather3p_smem(), st, items, ps, wins);
-        }
-        else if (D == 3) launch_k(gather3_s8_kernel<kW3>, dim3(nitems), dim3(kW3 * 32), gather3_smem(), st, items, ps, wins);
+        if (D == 3) launch_k(gather3_s8_kernel<kW3>, dim3(nitems), dim3(kW3 * 32), gather3_smem(), st, items, ps, wins);
         else if (D == 2) launch_k(gather2_s8_kernel<kW2>, dim3(nitems), dim3(kW2 * 32), gather2_smem(), st, items, ps, wins);
         else launch_k(gather1_s8_kernel<kW1>, dim3(nitems), dim3(kW1 * 32), gather1_smem(), st, items, ps, wins);
         return;
