@@ -771,12 +771,9 @@ struct Engine {
     }
 
     // KSVM_NFFT_LPT=0 keeps the items in (window, tile) order (A/B knob).
-    static int lpt_items() {
-        static const int on = [] {
-            const char* e = std::getenv("KSVM_NFFT_LPT");
-            return e ? std::atoi(e) : 1;
-        }();
-        return on;
+    static int lpt_items() {  // read per plan (tests compare both orders in one process)
+        const char* e = std::getenv("KSVM_NFFT_LPT");
+        return e ? std::atoi(e) : 1;
     }
 
     // Assign global item numbers / patch offsets and upload device tables.

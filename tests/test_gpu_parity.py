@@ -135,6 +135,24 @@ def test_d3_kernel_variants_match_oracle(oracle_lib, monkeypatch, spread, gather
     assert rel(apply_fastsum_cross(p, tg, v), q.apply_cross(tg, v)) <= TOL
 
 
+def test_item_order_does_not_change_a_bit(monkeypatch):
+    # items are dispatched largest first (KSVM_NFFT_LPT, default 1); patch
+    # offsets travel with the items and every reduction keeps its plan order,
+    # so the result is bit-identical to the (window, tile) order -- dense and
+    # sparse d = 3 classes (cell / column kernels, column bounds permuted
+    # with the items), d = 2 and d = 1 windows, heavy tiles split into items
+    rng = np.random.default_rng(97)
+    n = 120000
+    x = np.concatenate([rng.normal(size=(n, 4)) * 0.3, rng.uniform(-1, 1, size=(n, 5))], axis=1)
+    v = rng.normal(size=n)
+    wins = [[0, 1, 2], [4, 5, 6], [3, 7], [8]]
+    out = {}
+    for order in ("0", "1", "2"):
+        monkeypatch.setenv("KSVM_NFFT_LPT", order)
+        out[order] = anova_fast_operator(Dataset(x), spec_of(wins)).apply(v)
+    assert np.array_equal(out["0"], out["1"]) and np.array_equal(out["0"], out["2"])
+
+
 @pytest.mark.parametrize("dedup", ["1", "0"])
 def test_duplicate_points_match_oracle(oracle_lib, monkeypatch, dedup):
     # config-4-like windows: all-binary features (8 distinct points: the
