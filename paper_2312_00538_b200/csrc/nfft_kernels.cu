@@ -1258,8 +1258,11 @@ __global__ void gather_generic_kernel(const Item* __restrict__ items,
 // node reduction below reads one patch per covering tile. Work list:
 // (window slot, tile) pairs of multi-item tiles; blockIdx.y = pair.
 // ===========================================================================
-__global__ void tile_reduce_kernel(const DWin* __restrict__ wins, const int2* __restrict__ multi,
-                                   double* __restrict__ patches) {
+constexpr int kTrSlices = 4;  // tile_reduce: threads per element (patches k = slice, slice + 4, ...)
+
+__global__ void __launch_bounds__(64 * kTrSlices)
+tile_reduce_kernel(const DWin* __restrict__ wins, const int2* __restrict__ multi, double* __restrict__ patches) {
+    __shared__ double part[kTrSlices][64];
     pdl_trigger();
     const int2 wt = multi[blockIdx.y];
     const DWin& wn = wins[wt.x];
@@ -1267,19 +1270,28 @@ __global__ void tile_reduce_kernel(const DWin* __restrict__ wins, const int2* __
     for (int t = 0; t < wn.d; ++t) PV *= wn.PE;
     const int k0 = wn.tile_first[wt.y], k1 = wn.tile_first[wt.y + 1];
     double* base = patches + wn.patch_base + static_cast<long long>(k0 - wn.item_base) * PV;
-    const int nk = k1 - k0;
+    const int nk = k1 - k0, sl = threadIdx.y;
     pdl_wait();
     base = launder(base);  // patches: written by the spread kernels
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < PV; e += gridDim.x * blockDim.x) {
-        // eight interleaved partial sums (8 loads in flight), combined in a fixed order
-        double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        int k = 0;
-        for (; k + 8 <= nk; k += 8) {
+    for (int e0 = blockIdx.x * 64; e0 < PV; e0 += gridDim.x * 64) {
+        const int e = e0 + threadIdx.x;
+        // slice sl sums patches sl, sl + 4, ... in four interleaved partial
+        // sums (16 loads in flight per element); slices and partials are
+        // combined in a fixed order
+        double s[4] = {0, 0, 0, 0};
+        if (e < PV) {
+            int k = sl;
+            for (; k + 3 * kTrSlices < nk; k += 4 * kTrSlices) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) s[j] += __ldcg(base + static_cast<long long>(k + j) * PV + e);
+                for (int j = 0; j < 4; ++j) s[j] += __ldcg(base + static_cast<long long>(k + j * kTrSlices) * PV + e);
+            }
+            for (int j = 0; k < nk; k += kTrSlices, ++j) s[j] += __ldcg(base + static_cast<long long>(k) * PV + e);
         }
-        for (int j = 0; k + j < nk; ++j) s[j] += __ldcg(base + static_cast<long long>(k + j) * PV + e);
-        base[e] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+        part[sl][threadIdx.x] = (s[0] + s[1]) + (s[2] + s[3]);
+        __syncthreads();
+        if (sl == 0 && e < PV)
+            base[e] = (part[0][threadIdx.x] + part[1][threadIdx.x]) + (part[2][threadIdx.x] + part[3][threadIdx.x]);
+        __syncthreads();
     }
 }
 
@@ -1998,9 +2010,9 @@ void launch_gather(int D, int S, int PE, const Item* items, int nitems, const DP
 void launch_tile_reduce(const DWin* wins, const int2* multi, int nmulti, int max_pv, double* patches,
                         cudaStream_t st) {
     if (nmulti == 0) return;
-    // narrow blocks: one heavy tile's patches are read by ~max_pv/64 SMs
+    // narrow blocks (64 elements x 4 patch slices): one heavy tile's patches are read by ~max_pv/64 SMs
     dim3 grid(static_cast<unsigned>((max_pv + 63) / 64), static_cast<unsigned>(nmulti));
-    launch_k(tile_reduce_kernel, dim3(grid), dim3(64), 0, st, wins, multi, patches);
+    launch_k(tile_reduce_kernel, dim3(grid), dim3(64, kTrSlices), 0, st, wins, multi, patches);
 }
 
 void launch_reduce(const DWin* wins, const int* slots, int nslots, long long max_nodes, int D, int S,
