@@ -3,21 +3,31 @@
 // P:src/fastsum.cpp:257-296, computed with fp32 window weights and fp32
 // FFMA accumulation on the CUDA cores).
 //
-// Why CUDA cores: B200 has no fp32 tensor-core kind that is accurate to
-// 1e-5 without splitting (tf32 keeps 10 mantissa bits), and FFMA runs at
-// 128 FMA/clk/SM, twice the FP64 datapath the fp64 kernels (DMMA) share.
+// Two kernel pairs. The default runs on the warp-level tensor path with
+// 3xTF32 splitting (spread3_t32 / gather3_t32 below): tf32 keeps 11
+// significant bits, so every operand is split x = hi + lo (hi = x with the
+// low 13 mantissa bits cleared, lo = x - hi, exact) and a product is
+// lo*hi + hi*lo + hi*hi on HMMA.1688.F32.TF32 with fp32 accumulation
+// (mma.sync: 8.6 cycles per m16n8k8 per SM sub-partition on B200, 277
+// TFLOP/s, scripts/micro/mma_legacy_rates.cu; there is no tcgen05 route for
+// an M = 16, N = 8 tile that changes operands every 8 points). The operands
+// use the split-power form of the fp64 kernels (nfft_kernels.cu): 32 operand
+// products per point. KSVM_NFFT_F32K=ffma selects the CUDA-core pair
+// (spread3_f32 / gather3_f32: fp32 weights, scalar FFMA at 128 FMA/clk/SM).
 // The grid side (node reduction, separable convolution) and the window sum
 // stay fp64: they are a few percent of the work. Inputs (v) and outputs
 // (per-window results, y) stay fp64, so the C ABI does not change.
 //
-// Window factors (factors32_kernel) are CELL-relative (u_t in [m-1, m)):
+// Window factors (factors32_kernel) are relative to the CELL CENTRE
+// (u' = x M - floor(x M) - 1/2 in [-1/2, 1/2), u = u' + m - 1/2):
 //   w_t[o] = C e^{-(u_t - o)^2/b} = P_t Q_t^o R[o],
-//   P = C^3 e^{-sum_t u_t^2/b},  Q_t = e^{2 u_t/b},  R[o] = e^{-o^2/b},
-// all comfortably inside the fp32 range (the fp64 kernels' tile-relative
-// factors would not be). A plan stores {P, Q0, Q1, Q2} as float4 (16 B per
-// point instead of 32 B).
+//   P = C^3 e^{-sum_t (u'_t^2 + (2m-1) u'_t)/b},  Q_t = e^{2 u'_t/b},  R[o] = e^{-(o - m + 1/2)^2/b},
+// so Q is in [0.55, 1.8] and every power and operand product stays within a
+// few decades of 1 (the fp64 kernels' tile-relative factors would leave the
+// fp32 range). A plan stores {P, Q0, Q1, Q2} as float4 (16 B per point
+// instead of 32 B).
 //
-// Decomposition (both kernels): a CTA is one item (a 4^3-cell tile's point
+// Decomposition (FFMA pair): a CTA is one item (a 4^3-cell tile's point
 // range), W warps, and every warp runs two independent half-warp streams in
 // lockstep. A half-warp processes one point per step; its lane (a, bq)
 // (a = 0..7, bq = 0 or 4) owns the 32 taps (a, bq..bq+3, 0..7) of the
@@ -30,6 +40,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "launch.cuh"
 #include "nfft_engine.cuh"
@@ -61,6 +72,12 @@ struct PrefF {
         perm = c.y;
     }
 };
+
+// R[o] = e^{-(o - m + 1/2)^2/b} of the centred factors (m = 4).
+__device__ __forceinline__ float centred_R(const DWin& wn, int o) {
+    const double c = static_cast<double>(o) - (static_cast<double>(wn.m) - 0.5);
+    return static_cast<float>(exp(-c * c * wn.invb));
+}
 
 // Window weights of one point: w[t][o] = (s P for t = 0) Q_t^o R[o].
 __device__ __forceinline__ void weights_f32(float (&w)[3][8], float s, const float4& F, const float* sR) {
@@ -106,7 +123,7 @@ spread3_f32_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pse
     const DPSet ps = psets[it.ps];
     if (ps.vsrc) v = ps.vsrc;
     const DWin& wn = wins[ps.win];
-    if (threadIdx.x < 8) sR[threadIdx.x] = static_cast<float>(wn.R[threadIdx.x]);
+    if (threadIdx.x < 8) sR[threadIdx.x] = centred_R(wn, threadIdx.x);
     for (int k = lane; k < kHP; k += 32) wp[k] = 0.f;
     int wb, we;
     {
@@ -249,7 +266,7 @@ gather3_f32_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pse
             tile /= wn.ntile;
         }
     }
-    if (threadIdx.x < 8) sR[threadIdx.x] = static_cast<float>(wn.R[threadIdx.x]);
+    if (threadIdx.x < 8) sR[threadIdx.x] = centred_R(wn, threadIdx.x);
     int wb, we;
     {
         const int len = it.end - it.begin, per = (len + W - 1) / W;
@@ -375,7 +392,397 @@ gather3_f32_kernel(const Item* __restrict__ items, const DPSet* __restrict__ pse
     }
 }
 
-// Cell-relative fp32 window factors of each sorted point, plus {code, perm}
+// ===========================================================================
+// 3xTF32 tensor-core pair (the default fp32 kernels).
+// One warp-level HMMA.1688.F32.TF32 is D(16x8) += A(16x8) B(8x8); lane
+// l = 4g + t holds A[g][t], A[g+8][t], A[g][t+4], A[g+8][t+4], B[t][g],
+// B[t+4][g] and D[g][2t..2t+1], D[g+8][2t..2t+1].
+// Staging rows are kRowT = 24 floats: 24 t mod 32 = 0, 24, 16, 8 for the four
+// rows a load touches, so 8-word segments of 4 consecutive rows hit disjoint
+// banks. Row: x[8] | z[8] | four powers of Q1 | {code, perm}.
+// ===========================================================================
+constexpr int kRowT = 24;
+
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const unsigned (&a)[4], const unsigned (&b)[2]) {
+    asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+// x = hi + lo exactly; hi has the 11 significant bits tf32 keeps
+__device__ __forceinline__ void split_tf32(float x, unsigned& hi, unsigned& lo) {
+    hi = __float_as_uint(x) & 0xffffe000u;
+    lo = __float_as_uint(x - __uint_as_float(hi));
+}
+
+// Power rows of one point: x[o] = p Q0^o, z[o] = Q2^o, then four powers of Q1.
+__device__ __forceinline__ void stage_t32(float* row, float p, const float4& F, float y0, float y1, float y2,
+                                          float y3, int code, int perm) {
+    float4* r4 = reinterpret_cast<float4*>(row);
+    float q[8];
+    q[0] = p;
+#pragma unroll
+    for (int o = 1; o < 8; ++o) q[o] = q[o - 1] * F.y;
+    r4[0] = make_float4(q[0], q[1], q[2], q[3]);
+    r4[1] = make_float4(q[4], q[5], q[6], q[7]);
+    q[0] = 1.0f;
+#pragma unroll
+    for (int o = 1; o < 8; ++o) q[o] = q[o - 1] * F.w;
+    r4[2] = make_float4(q[0], q[1], q[2], q[3]);
+    r4[3] = make_float4(q[4], q[5], q[6], q[7]);
+    r4[4] = make_float4(y0, y1, y2, y3);
+    *reinterpret_cast<int2*>(row + 20) = make_int2(code, perm);
+}
+
+__device__ __forceinline__ int run_len32(unsigned same, int p) {
+    const unsigned s = p + 1 < 32 ? (same >> (p + 1)) : 0u;
+    return __ffs(~s);  // 1 + number of consecutive set bits above p
+}
+
+// ---------------------------------------------------------------------------
+// Spread, 3xTF32. Per cell the 8^3 block is G[(a, b1), (b0, c)], b = 4 b1 + b0
+// (split-power form): A[(a, b1)][p] = x_p[a] (Q1_p^4)^b1, B[p][(b0, c)] =
+// Q1_p^b0 z_p[c], K = 8 same-cell points per MMA, four N tiles (b0) -> 12 HMMA
+// per 8 points. Accumulator tile b0 holds G[a = g][b = b0 | 4 + b0][c = 2t..2t+1].
+// R[a] R[b] R[c] is applied when a cell's block is added into the warp's SMEM
+// patch (fp32); the epilogue adds the W patches in fp64 in a fixed order.
+// ---------------------------------------------------------------------------
+template <int W>
+__global__ void __launch_bounds__(W * 32, 4)
+spread3_t32_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
+                   const DWin* __restrict__ wins, const double* __restrict__ v,
+                   double* __restrict__ patches) {
+    constexpr unsigned kFull = 0xffffffffu;
+    constexpr int PE = kPEf;
+    extern __shared__ __align__(16) float smf[];
+    __shared__ float sR[8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    float* wp = smf + warp * kHP;
+    float* stage = smf + W * kHP + warp * 32 * kRowT;
+
+    pdl_trigger();
+    const Item it = items[blockIdx.x];
+    const DPSet ps = psets[it.ps];
+    if (ps.vsrc) v = ps.vsrc;
+    const DWin& wn = wins[ps.win];
+    if (threadIdx.x < 8) sR[threadIdx.x] = centred_R(wn, threadIdx.x);
+    for (int k = lane; k < kHP; k += 32) wp[k] = 0.f;
+    int wb, we;
+    {
+        const int len = it.end - it.begin, per = (len + W - 1) / W;
+        wb = min(it.begin + warp * per, it.end);
+        we = min(wb + per, it.end);
+    }
+    // Two point buffers in rotation (the loop is unrolled by two batches, so no
+    // buffer is ever copied): a batch's plan data is requested two batches
+    // ahead, right after the buffer has been staged, and its v one batch
+    // ahead. With a copy `pa = pb` the warp waits for the newest load every
+    // iteration, and these kernels consume a batch faster than DRAM answers.
+    PrefF p0, p1;
+    double v0 = 0.0, v1 = 0.0;
+    const unsigned long long pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
+    // Loads are unconditional with the index clamped into the item (lanes past
+    // the range read a valid point they never use): a predicated load lands in
+    // a temporary and its predicated copy waits for the data at once.
+    const int last = it.end - 1;
+    p0.load(ps, min(wb + lane, last), pol_stream);
+    p1.load(ps, min(wb + 32 + lane, last), pol_stream);
+    __syncthreads();
+    pdl_wait();  // v may be produced by the previous kernel (duplicate-merge sums)
+    v = launder(v);
+    v0 = ld_keep(v + p0.perm, pol_keep);
+
+    // The tensor cores add into an fp32 accumulator with truncation, a bias
+    // that grows with the length of the chain (measured 3e-6 relative at 58
+    // points per cell), so a chain is at most one 32-point batch plus a
+    // partial one: `acc` is drained into `sum` (round-to-nearest adds) after
+    // every full batch.
+    float acc[4][4], sum[4][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[j][c] = sum[j][c] = 0.f;
+    int cur = -1;
+    auto drain = [&]() {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                sum[j][c] += acc[j][c];
+                acc[j][c] = 0.f;
+            }
+    };
+    auto flush = [&](int cell) {
+        const int l0 = cell >> 4, l1 = (cell >> 2) & 3, l2 = cell & 3;
+        float* dst = wp + ((l0 + g) * PE + l1) * PE + l2 + 2 * t;
+        const float rg = sR[g], rc0 = sR[2 * t], rc1 = sR[2 * t + 1];
+        drain();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float r0 = rg * sR[j], r1 = rg * sR[4 + j];
+            dst[j * PE] += (sum[j][0] * r0) * rc0;
+            dst[j * PE + 1] += (sum[j][1] * r0) * rc1;
+            dst[(4 + j) * PE] += (sum[j][2] * r1) * rc0;
+            dst[(4 + j) * PE + 1] += (sum[j][3] * r1) * rc1;
+            sum[j][0] = sum[j][1] = sum[j][2] = sum[j][3] = 0.f;
+        }
+    };
+    // 8 points p0..p0+7 of the current cell (K index t -> p0 + t, t + 4 -> p0 + t + 4);
+    // points >= nv contribute zero
+    auto group8 = [&](int p0, int nv) {
+        const bool v0 = t < nv, v1 = t + 4 < nv;
+        const float* r0 = stage + (p0 + (v0 ? t : 0)) * kRowT;
+        const float* r1 = stage + (p0 + (v1 ? t + 4 : 0)) * kRowT;
+        const float x0 = v0 ? r0[g] : 0.f, x1 = v1 ? r1[g] : 0.f;
+        const float z0 = r0[8 + g], z1 = r1[8 + g];
+        const float4 y0 = *reinterpret_cast<const float4*>(r0 + 16);  // Q1, Q1^2, Q1^3, Q1^4
+        const float4 y1 = *reinterpret_cast<const float4*>(r1 + 16);
+        unsigned ah[4], al[4];
+        split_tf32(x0, ah[0], al[0]);
+        split_tf32(x0 * y0.w, ah[1], al[1]);
+        split_tf32(x1, ah[2], al[2]);
+        split_tf32(x1 * y1.w, ah[3], al[3]);
+        const float f0[4] = {1.0f, y0.x, y0.y, y0.z}, f1[4] = {1.0f, y1.x, y1.y, y1.z};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {  // small terms first
+            unsigned bh[2], bl[2];
+            split_tf32(j == 0 ? z0 : z0 * f0[j], bh[0], bl[0]);
+            split_tf32(j == 0 ? z1 : z1 * f1[j], bh[1], bl[1]);
+            mma_tf32(acc[j], al, bh);
+            mma_tf32(acc[j], ah, bl);
+            mma_tf32(acc[j], ah, bh);
+        }
+    };
+
+    // one 32-point batch from buffer (pc, vc); pn / vn is the next batch's buffer
+    auto batch = [&](int base, PrefF& pc, double vc, const PrefF& pn, double& vn) {
+        const int cnt = min(32, we - base);
+        const int code = pc.code;
+        if (lane < cnt) {
+            const float y1 = pc.F.z, y2 = y1 * y1;
+            stage_t32(stage + lane * kRowT, static_cast<float>(vc) * pc.F.x, pc.F, y1, y2, y2 * y1, y2 * y2, code, 0);
+        }
+        const int prev = __shfl_up_sync(kFull, code, 1);
+        const unsigned same = __ballot_sync(kFull, lane < cnt && code == (lane == 0 ? cur : prev));
+        vn = ld_keep(v + pn.perm, pol_keep);
+        pc.load(ps, min(base + 64 + lane, last), pol_stream);
+        __syncwarp();
+        if (same == kFull) {  // the whole batch continues the current cell
+#pragma unroll
+            for (int q = 0; q < 4; ++q) group8(8 * q, 8);
+            drain();
+        } else {
+            int p = 0;
+            while (p < cnt) {
+                if (!((same >> p) & 1u)) {  // a new cell starts at p
+                    if (cur >= 0) flush(cur);
+                    cur = __shfl_sync(kFull, code, p);
+                }
+                for (int L = run_len32(same, p); L > 0;) {
+                    const int nv = min(L, 8);
+                    group8(p, nv);
+                    p += nv;
+                    L -= nv;
+                }
+            }
+        }
+        __syncwarp();
+    };
+    for (int base = wb; base < we; base += 64) {
+        batch(base, p0, v0, p1, v1);
+        if (base + 32 < we) batch(base + 32, p1, v1, p0, v0);
+    }
+    if (cur >= 0) flush(cur);
+    __syncthreads();
+    // epilogue: the W warp patches in fixed order, in fp64
+    if (threadIdx.x < PE * PE) {
+        double* out = patches + it.patch;
+        for (int n0 = 0; n0 < PE; ++n0) {
+            const int e = n0 * PE * PE + threadIdx.x;
+            double s = 0.0;
+#pragma unroll
+            for (int q = 0; q < W; ++q) s += static_cast<double>(smf[q * kHP + e]);
+            out[e] = s;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Gather, 3xTF32. With b = 2 b1 + b0, Y = Q1:
+//   Z[p, (b0, c)] = sum_{(a, b1)} (x_p[a] Y_p^{2 b1}) H[a, 2 b1 + b0, c]
+//   y_p           = sum_c z_p[c] (Z[p, (0, c)] + Y_p Z[p, (1, c)])
+// M = 16 same-cell points per MMA, K = 32 in four k-steps (k-step s: b1 = s,
+// column a), N = 16 in two tiles (b0) -> 24 HMMA per 16 points. The cell's
+// halo values (times R[a] R[b] R[c]) are kept split in registers and reloaded
+// when the cell changes. Row: x[8] (P folded) | z[8] | Y^2, Y^4, Y^6, Y | {code, perm}.
+// ---------------------------------------------------------------------------
+template <int W>
+__global__ void __launch_bounds__(W * 32, 4)
+gather3_t32_kernel(const Item* __restrict__ items, const DPSet* __restrict__ psets,
+                   const DWin* __restrict__ wins) {
+    constexpr unsigned kFull = 0xffffffffu;
+    constexpr int TC = 4, PE = kPEf;
+    extern __shared__ __align__(16) float smf[];
+    __shared__ float sR[8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    float* halo = smf;
+    float* stage = smf + kHP + warp * 32 * kRowT;
+
+    pdl_trigger();
+    const Item it = items[blockIdx.x];
+    const DPSet ps = psets[it.ps];
+    const DWin& wn = wins[ps.win];
+    int tc[3];
+    {
+        int tile = it.tile;
+        for (int k = 2; k >= 0; --k) {
+            tc[k] = tile % wn.ntile;
+            tile /= wn.ntile;
+        }
+    }
+    if (threadIdx.x < 8) sR[threadIdx.x] = centred_R(wn, threadIdx.x);
+    int wb, we;
+    {
+        const int len = it.end - it.begin, per = (len + W - 1) / W;
+        wb = min(it.begin + warp * per, it.end);
+        we = min(wb + per, it.end);
+    }
+    PrefF p0, p1;  // two buffers in rotation, see spread3_t32_kernel
+    const unsigned long long pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
+    const int last = it.end - 1;  // unconditional, clamped loads: see spread3_t32_kernel
+    p0.load(ps, min(wb + lane, last), pol_stream);
+    p1.load(ps, min(wb + 32 + lane, last), pol_stream);
+    pdl_wait();  // H is written by the grid stage
+    {
+        const DWin& w = *launder(&wn);
+        const int Lg = w.Lg, M = w.M;
+        const bool wrap = w.wrap != 0;
+        const double* H = w.H;
+        for (int k = threadIdx.x; k < PE * PE; k += blockDim.x) {
+            const int n1 = k / PE, n2 = k - n1 * PE;
+            const int i1 = tc[1] * TC + n1, i2 = tc[2] * TC + n2;
+            for (int n0 = 0; n0 < PE; ++n0) {
+                const int i0 = tc[0] * TC + n0;
+                double hv;
+                if (!wrap) {
+                    hv = (i0 < Lg && i1 < Lg && i2 < Lg)
+                             ? __ldcg(H + (static_cast<long long>(i0) * Lg + i1) * Lg + i2)
+                             : 0.0;
+                } else {
+                    auto pm = [M](int x) { int r = x % M; return r < 0 ? r + M : r; };
+                    hv = __ldcg(H + (static_cast<long long>(pm(w.lo + i0)) * Lg + pm(w.lo + i1)) * Lg +
+                                pm(w.lo + i2));
+                }
+                halo[n0 * PE * PE + k] = static_cast<float>(hv);
+            }
+        }
+    }
+    __syncthreads();
+
+    unsigned bh[4][2][2], bl[4][2][2];  // [k-step s][tile b0][a = t | t + 4]
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) bh[s][nt][0] = bh[s][nt][1] = bl[s][nt][0] = bl[s][nt][1] = 0u;
+    int cur = -1;
+    auto reload = [&](int cell) {
+        const int l0 = cell >> 4, l1 = (cell >> 2) & 3, l2 = cell & 3;
+        const float* src = halo + ((l0 + t) * PE + l1) * PE + l2 + g;
+        const float rc = sR[g], ra0 = sR[t] * rc, ra1 = sR[t + 4] * rc;
+#pragma unroll
+        for (int s = 0; s < 4; ++s)
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+                const int b = 2 * s + nt;
+                split_tf32(src[b * PE] * (ra0 * sR[b]), bh[s][nt][0], bl[s][nt][0]);
+                split_tf32(src[4 * PE * PE + b * PE] * (ra1 * sR[b]), bh[s][nt][1], bl[s][nt][1]);
+            }
+    };
+    // 16 points p0..p0+15 of the current cell (row g -> p0 + g, row g + 8 -> p0 + g + 8)
+    auto group16 = [&](int p0, int nv) {
+        const bool v0 = g < nv, v1 = g + 8 < nv;
+        const float* r0 = stage + (p0 + (v0 ? g : 0)) * kRowT;
+        const float* r1 = stage + (p0 + (v1 ? g + 8 : 0)) * kRowT;
+        const float xa0 = v0 ? r0[t] : 0.f, xb0 = v0 ? r0[t + 4] : 0.f;
+        const float xa1 = v1 ? r1[t] : 0.f, xb1 = v1 ? r1[t + 4] : 0.f;
+        const float4 Y0 = *reinterpret_cast<const float4*>(r0 + 16);  // Y^2, Y^4, Y^6, Y
+        const float4 Y1 = *reinterpret_cast<const float4*>(r1 + 16);
+        const float f0[4] = {1.0f, Y0.x, Y0.y, Y0.z}, f1[4] = {1.0f, Y1.x, Y1.y, Y1.z};
+        float d[2][2][4];  // [tile b0][k-step parity][fragment]
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) d[nt][q][0] = d[nt][q][1] = d[nt][q][2] = d[nt][q][3] = 0.f;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            unsigned ah[4], al[4];
+            split_tf32(s == 0 ? xa0 : xa0 * f0[s], ah[0], al[0]);
+            split_tf32(s == 0 ? xa1 : xa1 * f1[s], ah[1], al[1]);
+            split_tf32(s == 0 ? xb0 : xb0 * f0[s], ah[2], al[2]);
+            split_tf32(s == 0 ? xb1 : xb1 * f1[s], ah[3], al[3]);
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) mma_tf32(d[nt][s & 1], al, bh[s][nt]);
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) mma_tf32(d[nt][s & 1], ah, bl[s][nt]);
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) mma_tf32(d[nt][s & 1], ah, bh[s][nt]);
+        }
+        const float2 z0 = *reinterpret_cast<const float2*>(r0 + 8 + 2 * t);
+        const float2 z1 = *reinterpret_cast<const float2*>(r1 + 8 + 2 * t);
+        float e[2][4];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) e[nt][c] = d[nt][0][c] + d[nt][1][c];
+        float part0 = fmaf(z0.x, fmaf(Y0.w, e[1][0], e[0][0]), z0.y * fmaf(Y0.w, e[1][1], e[0][1]));
+        float part1 = fmaf(z1.x, fmaf(Y1.w, e[1][2], e[0][2]), z1.y * fmaf(Y1.w, e[1][3], e[0][3]));
+        part0 += __shfl_xor_sync(kFull, part0, 1);
+        part1 += __shfl_xor_sync(kFull, part1, 1);
+        part0 += __shfl_xor_sync(kFull, part0, 2);
+        part1 += __shfl_xor_sync(kFull, part1, 2);
+        if (t == 0 && v0) st_keep(ps.out + reinterpret_cast<const int*>(r0 + 20)[1], static_cast<double>(part0), pol_keep);
+        if (t == 1 && v1) st_keep(ps.out + reinterpret_cast<const int*>(r1 + 20)[1], static_cast<double>(part1), pol_keep);
+    };
+
+    auto batch = [&](int base, PrefF& pc) {
+        const int cnt = min(32, we - base);
+        const int code = pc.code;
+        if (lane < cnt) {
+            const float y1 = pc.F.z, y2 = y1 * y1, y4 = y2 * y2;
+            stage_t32(stage + lane * kRowT, pc.F.x, pc.F, y2, y4, y4 * y2, y1, code, pc.perm);
+        }
+        const int prev = __shfl_up_sync(kFull, code, 1);
+        const unsigned same = __ballot_sync(kFull, lane < cnt && code == (lane == 0 ? cur : prev));
+        pc.load(ps, min(base + 64 + lane, last), pol_stream);
+        __syncwarp();
+        if (same == kFull) {
+            group16(0, 16);
+            group16(16, 16);
+        } else {
+            int p = 0;
+            while (p < cnt) {
+                if (!((same >> p) & 1u)) {
+                    cur = __shfl_sync(kFull, code, p);
+                    reload(cur);
+                }
+                for (int L = run_len32(same, p); L > 0;) {
+                    const int nv = min(L, 16);
+                    group16(p, nv);
+                    p += nv;
+                    L -= nv;
+                }
+            }
+        }
+        __syncwarp();
+    };
+    for (int base = wb; base < we; base += 64) {
+        batch(base, p0);
+        if (base + 32 < we) batch(base + 32, p1);
+    }
+}
+
+// Centre-relative fp32 window factors of each sorted point, plus {code, perm}
 // (the same tile-local cell code as factors_kernel).
 __global__ void factors32_kernel(const double* __restrict__ x0, const double* __restrict__ x1,
                                  const double* __restrict__ x2, const int* __restrict__ perm,
@@ -392,8 +799,8 @@ __global__ void factors32_kernel(const double* __restrict__ x0, const double* __
         for (int t = 0; t < 3; ++t) {
             const double xm = xs[t][src] * Mf;
             const double fl = floor(xm);
-            const double u = (xm - fl) + static_cast<double>(m - 1);
-            ex += u * u;
+            const double u = (xm - fl) - 0.5;  // relative to the cell centre
+            ex += u * u + static_cast<double>(2 * m - 1) * u;
             Q[t] = exp((2.0 * u) * invb);
             cd = cd * TC + (static_cast<int>(fl) - cmin) % TC;
         }
@@ -405,26 +812,48 @@ __global__ void factors32_kernel(const double* __restrict__ x0, const double* __
 
 size_t spread3_f32_smem() { return sizeof(float) * (kW3f * kHP + kW3f * 2 * (kHalfRows * kRowS + 8)); }
 size_t gather3_f32_smem() { return sizeof(float) * (kHP + kW3f * 2 * (kHalfRows * kRowG + 8)); }
+size_t spread3_t32_smem() { return sizeof(float) * (kW3f * kHP + kW3f * 32 * kRowT); }
+size_t gather3_t32_smem() { return sizeof(float) * (kHP + kW3f * 32 * kRowT); }
+
+// KSVM_NFFT_F32K=ffma: the CUDA-core kernels instead of the 3xTF32 pair
+static bool f32_ffma() {
+    static const bool on = [] {
+        const char* e = std::getenv("KSVM_NFFT_F32K");
+        return e && e[0] == 'f';
+    }();
+    return on;
+}
 
 cudaError_t init_f32_attributes() {
-    cudaError_t e = cudaFuncSetAttribute(spread3_f32_kernel<kW3f>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(spread3_f32_smem()));
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(gather3_f32_kernel<kW3f>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(gather3_f32_smem()));
+    cudaError_t e = cudaSuccess;
+    auto set = [&](const void* f, size_t bytes) {
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+    };
+    set(reinterpret_cast<const void*>(spread3_f32_kernel<kW3f>), spread3_f32_smem());
+    set(reinterpret_cast<const void*>(gather3_f32_kernel<kW3f>), gather3_f32_smem());
+    set(reinterpret_cast<const void*>(spread3_t32_kernel<kW3f>), spread3_t32_smem());
+    set(reinterpret_cast<const void*>(gather3_t32_kernel<kW3f>), gather3_t32_smem());
     return e;
 }
 
 void launch_spread3_f32(const Item* items, int nitems, const DPSet* ps, const DWin* wins, const double* v,
                         double* patches, cudaStream_t st) {
     if (nitems == 0) return;
-    launch_k(spread3_f32_kernel<kW3f>, dim3(nitems), dim3(kW3f * 32), spread3_f32_smem(), st, items, ps, wins, v,
-             patches);
+    if (f32_ffma())
+        launch_k(spread3_f32_kernel<kW3f>, dim3(nitems), dim3(kW3f * 32), spread3_f32_smem(), st, items, ps, wins, v,
+                 patches);
+    else
+        launch_k(spread3_t32_kernel<kW3f>, dim3(nitems), dim3(kW3f * 32), spread3_t32_smem(), st, items, ps, wins, v,
+                 patches);
 }
 
 void launch_gather3_f32(const Item* items, int nitems, const DPSet* ps, const DWin* wins, cudaStream_t st) {
     if (nitems == 0) return;
-    launch_k(gather3_f32_kernel<kW3f>, dim3(nitems), dim3(kW3f * 32), gather3_f32_smem(), st, items, ps, wins);
+    if (f32_ffma())
+        launch_k(gather3_f32_kernel<kW3f>, dim3(nitems), dim3(kW3f * 32), gather3_f32_smem(), st, items, ps, wins);
+    else
+        launch_k(gather3_t32_kernel<kW3f>, dim3(nitems), dim3(kW3f * 32), gather3_t32_smem(), st, items, ps, wins);
 }
 
 void launch_factors32(const double* x0, const double* x1, const double* x2, const int* perm, long long n,
