@@ -816,12 +816,9 @@ size_t spread3_t32_smem() { return sizeof(float) * (kW3f * kHP + kW3f * 32 * kRo
 size_t gather3_t32_smem() { return sizeof(float) * (kHP + kW3f * 32 * kRowT); }
 
 // KSVM_NFFT_F32K=ffma: the CUDA-core kernels instead of the 3xTF32 pair
-static bool f32_ffma() {
-    static const bool on = [] {
-        const char* e = std::getenv("KSVM_NFFT_F32K");
-        return e && e[0] == 'f';
-    }();
-    return on;
+static bool f32_ffma() {  // read per launch (a graph capture fixes it for the operator)
+    const char* e = std::getenv("KSVM_NFFT_F32K");
+    return e && e[0] == 'f';
 }
 
 cudaError_t init_f32_attributes() {

@@ -10,7 +10,8 @@ import sys
 
 STAGE = {"spread3c_s8": "spread_d3", "spread3_s8": "spread_d3", "gather3c_s8": "gather_d3",
          "gather3_s8": "gather_d3", "spread2_s8": "spread_d2", "gather2_s8": "gather_d2",
-         "spread3_f32": "spread_d3", "gather3_f32": "gather_d3"}
+         "spread3_f32": "spread_d3", "gather3_f32": "gather_d3",
+         "spread3_t32": "spread_d3", "gather3_t32": "gather_d3"}
 
 
 def unit_bytes(val, unit):

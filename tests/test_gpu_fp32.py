@@ -2,7 +2,8 @@
 optional fp32 mode") against the fp64 reference fastsum.
 
 The d = 3, m = 4 windows with dense cells spread and gather in fp32
-(csrc/nfft_f32.cu); sparse-cell classes (configs 1, 2), the grid stage, the
+(csrc/nfft_f32.cu: the 3xTF32 tensor-core kernels by default, the FFMA kernels
+with KSVM_NFFT_F32K=ffma; both are tested); sparse-cell classes (configs 1, 2), the grid stage, the
 d <= 2 windows and the window sum stay fp64. KSVM_NFFT_F32=all forces the
 fp32 kernels on sparse cells too, so they are tested there as well. The checker is
 the oracle restatement (bit-identical to the reference's own
@@ -38,9 +39,11 @@ def fp32_op(w, **kw):
                                precision="fp32", **kw)
 
 
+@pytest.mark.parametrize("kernels", ["tf32", "ffma"])
 @pytest.mark.parametrize("cfg,n", [(1, None), (2, None), (3, None), (4, 50000), (5, 200000)])
-def test_fp32_matches_fp64_oracle(oracle_lib, monkeypatch, cfg, n):
+def test_fp32_matches_fp64_oracle(oracle_lib, monkeypatch, cfg, n, kernels):
     monkeypatch.setenv("KSVM_NFFT_F32", "all")  # fp32 kernels even on sparse cells
+    monkeypatch.setenv("KSVM_NFFT_F32K", kernels)
     w = workloads.make(cfg, n)
     ref = oracle_lib.anova(w.points, w.windows, fit=w.fit_fraction).apply(w.v)
     before = _lib.launch_count()
@@ -63,8 +66,10 @@ def test_fp32_default_density_rule(oracle_lib, cfg, n):
     assert (e <= 1e-10) == (cfg == 2), e
 
 
-def test_fp32_without_duplicate_merge(oracle_lib, monkeypatch):
+@pytest.mark.parametrize("kernels", ["tf32", "ffma"])
+def test_fp32_without_duplicate_merge(oracle_lib, monkeypatch, kernels):
     monkeypatch.setenv("KSVM_NFFT_F32", "all")
+    monkeypatch.setenv("KSVM_NFFT_F32K", kernels)
     # config 4's binary windows at full cell density (one cell holds ~7 % of
     # the points): heavy-cell item splitting and long same-cell runs
     monkeypatch.setenv("KSVM_NFFT_DEDUP", "0")
