@@ -82,9 +82,11 @@ enum { KSVM_NFFT_ROW_MAJOR = 0, KSVM_NFFT_COL_MAJOR = 1 };
 enum { KSVM_NFFT_HOST = 0, KSVM_NFFT_DEVICE = 1 };
 /* precision of ksvm_nfft_op_create / _create_sharded. FP32 (north_star's
  * optional fp32 mode, <= 1e-5 relative l2 against the fp64 reference): the
- * d = 3, m = 4 windows spread and gather with fp32 window weights and fp32
- * FFMA accumulation (cell-relative factors, 16 B per point); d <= 2 windows,
- * the grid stage and the window sum stay fp64; v and y are fp64 either way. */
+ * dense d = 3, m = 4 windows spread and gather with fp32 window weights on the
+ * tensor cores (3xTF32 split products, fp32 accumulation; 16 B of factors per
+ * point; KSVM_NFFT_F32K=ffma in the environment selects the CUDA-core
+ * kernels); d <= 2 windows, sparse d = 3 classes, the grid stage and the
+ * window sum stay fp64; v and y are fp64 either way. */
 enum { KSVM_NFFT_FP64 = 0, KSVM_NFFT_FP32 = 1 };
 
 /* FastsumConfig (P:include/ksvm/fastsum.hpp:13-20). */
