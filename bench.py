@@ -482,7 +482,8 @@ def run_ours(args):
             tflops = 2 * kernel_fmas(w, dom, pts) / (ms * 1e-3) / 1e12
             roof = {"bound": "fp32" if word == 4 else "fp64", "kernel": dom, "achieved": tflops, "peak": fpk,
                     "unit": "TFLOP/s", "frac": tflops / fpk,
-                    "peak_source": ("cuBLAS SGEMM 8192^3 (torch.matmul f32, TF32 off) measured in this run"
+                    "peak_source": ("cuBLAS SGEMM 8192^3 (torch.matmul f32, TF32 off: the fp32-accurate library "
+                                    "GEMM) measured in this run; the kernel itself runs 3xTF32 on the tensor cores"
                                     if word == 4 else "cuBLAS DGEMM 8192^3 (torch.matmul f64) measured in this run"),
                     "per_launch": {"fma": kernel_fmas(w, dom, pts),
                                    "algorithmic_bytes": kernel_bytes(w, dom, pts, word), "ms": ms},
